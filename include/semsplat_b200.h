@@ -1,0 +1,200 @@
+/* semsplat_b200.h -- C ABI of libsemsplat_b200.so, the B200-native
+ * implementation of SLAG's per-Gaussian language-embedding pass and cosine
+ * top-k query (reference: /root/reference/proj/include/semsplat/, a
+ * header-only C++20 CPU library with no C ABI of its own).
+ *
+ * Every entry point below replaces the reference function cited beside it;
+ * the C++ drop-in layer (include/semsplat_b200/semsplat_b200.hpp) and the
+ * Python host mirror (paper_2505_08124_b200/semsplat.py) bind these symbols
+ * and re-raise the reference's exception classes from ss_last_error_kind().
+ *
+ * Conventions: plain C types; int return = ss_status (0 = ok); per-thread
+ * ss_last_error() text; one ss_ctx per device, used from one host thread at a
+ * time; host pointers unless a parameter is named d_* (device pointer).
+ * All kernels are sm_100a; there is no CPU fallback -- ss_create() fails with
+ * SS_ERR_CUDA when no sm_100 device is present.
+ */
+#ifndef SEMSPLAT_B200_H
+#define SEMSPLAT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Error kinds, mapped onto the reference's exception taxonomy
+ * (core.hpp:14-57). */
+enum ss_status {
+    SS_OK = 0,
+    SS_ERR_CONTRACT = 1, /* ContractError  (core.hpp:27) */
+    SS_ERR_DATA = 2,     /* DataError      (core.hpp:21) */
+    SS_ERR_NUMERIC = 3,  /* NumericError   (core.hpp:33) */
+    SS_ERR_FORMAT = 4,   /* FormatError    (core.hpp:15) */
+    SS_ERR_IO = 5,       /* IoError        (core.hpp:39) */
+    SS_ERR_PIPELINE = 6, /* PipelineError  (core.hpp:51) */
+    SS_ERR_CUDA = 7      /* device / driver failure (no reference analogue) */
+};
+
+/* WeightMode (rasterizer.hpp:33-36) */
+enum ss_weight_mode { SS_ALPHA_COMPOSITED = 0, SS_FALLOFF_ONLY = 1 };
+
+/* CameraPose (scene.hpp:79-85) at raster resolution, i.e. after
+ * camera_scaled_to (pipeline.hpp:196-207).  R is row-major world-to-camera. */
+typedef struct ss_camera {
+    double fx, fy, cx, cy;
+    double R[9];
+    double t[3];
+    uint32_t width, height, image_id, pad;
+} ss_camera;
+
+/* Projected2D (projection.hpp:24-31) */
+typedef struct ss_projected {
+    uint32_t gaussian_id;
+    uint32_t visible;
+    double mu_x, mu_y, cov_xx, cov_xy, cov_yy, depth;
+} ss_projected;
+
+/* WeightEntry (rasterizer.hpp:38-43) */
+typedef struct ss_weight_entry {
+    uint32_t gaussian_id;
+    uint32_t pixel;
+    float weight;
+} ss_weight_entry;
+
+/* One view's SAM masks in their on-disk encoding (providers.hpp:77-127:
+ * alternating run lengths over row-major bits, zeros first) plus the mask
+ * CLIP vectors (providers.hpp:156-204).  Masks are resampled to the raster
+ * resolution on the device (providers.hpp:359-373). */
+typedef struct ss_view_masks {
+    uint32_t n_masks;
+    uint32_t mask_width, mask_height;
+    uint32_t pad;
+    const uint32_t* runs;        /* all masks' runs, concatenated */
+    const uint64_t* run_offsets; /* n_masks + 1 prefix offsets into runs */
+    const float* clip;           /* n_masks x dim, row-major */
+} ss_view_masks;
+
+typedef struct ss_ctx ss_ctx;
+
+/* ---- context ---------------------------------------------------------- */
+int ss_create(int device, ss_ctx** out);
+void ss_destroy(ss_ctx* ctx);
+const char* ss_last_error(void);
+int ss_last_error_kind(void);
+/* Run subsequent work on this CUDA stream (cudaStream_t as uintptr; 0 = the
+ * context's own stream).  Lets a host framework order our kernels with its
+ * own collectives. */
+int ss_set_stream(ss_ctx* ctx, uintptr_t stream);
+int ss_synchronize(ss_ctx* ctx);
+
+/* ---- scene (GaussianScene, scene.hpp:54-76) --------------------------- */
+/* mean/scale: n x 3; quat_xyzw: n x 4 in Eigen coeffs() order; opacity: n.
+ * Stored on the device as three float4 SoA streams. */
+int ss_scene_set(ss_ctx* ctx, const float* mean, const float* scale, const float* quat_xyzw, const float* opacity,
+                 uint64_t n);
+
+/* ---- projection / rasterizer (parity entry points) -------------------- */
+/* project_gaussian (projection.hpp:33-55) for every Gaussian. */
+int ss_project(ss_ctx* ctx, const ss_camera* cam, ss_projected* out);
+/* rasterize_weights_only (rasterizer.hpp:268-271): runs projection, depth
+ * sort, tile binning and the capture-mode compositor; results stay on the
+ * device until ss_raster_fetch. */
+int ss_raster_capture(ss_ctx* ctx, const ss_camera* cam, int mode, uint64_t* n_entries, uint64_t* n_splats,
+                      uint64_t* n_tile_instances);
+/* Copies the last capture to host.  Any pointer may be NULL.
+ * entries: n_entries, (pixel, front-to-back rank) order (rasterizer.hpp:250)
+ * per_pixel_total / alpha: width*height (rasterizer.hpp:48-53, :231-232)
+ * splat_gid: n_splats, the depth-sorted, box-culled splat list
+ * tile_offsets: tiles+1; tile_splats: n_tile_instances splat indices
+ * (rasterizer.hpp:183-194 tile_bins, flattened). */
+int ss_raster_fetch(ss_ctx* ctx, ss_weight_entry* entries, float* per_pixel_total, float* alpha,
+                    uint32_t* splat_gid, uint32_t* tile_offsets, uint32_t* tile_splats);
+
+/* ---- embedding pass (encode_scene, pipeline.hpp:280-470) -------------- */
+/* Zeroes the per-Gaussian accumulators (N x dim fp32 sums + N fp32 totals).
+ * d_sums / d_totals may be caller-owned device buffers (e.g. torch tensors
+ * that a collective will reduce-scatter) or NULL for context-owned ones. */
+int ss_encode_begin(ss_ctx* ctx, uint32_t dim, float* d_sums, float* d_totals);
+/* One view: device RLE decode + resample to a per-pixel mask bitset, project,
+ * depth sort, tile binning, fused mask-gated compositing into per-(Gaussian,
+ * mask) scalars, then the sparse 512-d contraction into the sums.  Replaces
+ * worker_body's per-image loop (pipeline.hpp:306-356) plus accumulate
+ * (pipeline.hpp:70-86). */
+int ss_encode_view(ss_ctx* ctx, const ss_camera* raster_cam, const ss_view_masks* masks, int mode);
+/* Batch form: nviews cameras and mask sets, processed in order. */
+int ss_encode_views(ss_ctx* ctx, uint32_t nviews, const ss_camera* raster_cams, const ss_view_masks* masks,
+                    int mode);
+/* finalize_into (pipeline.hpp:120-135) for rows [row_lo, row_hi) of the
+ * context's accumulators: rows_out (row_hi-row_lo) x dim and coverage_out
+ * (row_hi-row_lo).  out_on_device != 0: the outputs are device pointers. */
+int ss_encode_finalize(ss_ctx* ctx, uint64_t row_lo, uint64_t row_hi, float* rows_out, float* coverage_out,
+                       int out_on_device);
+/* finalize over caller-provided device buffers (a reduce-scattered shard):
+ * rows d_sums[n x dim] / d_totals[n] -> d_rows_out, d_coverage_out. */
+int ss_normalize_device(ss_ctx* ctx, const float* d_sums, const float* d_totals, uint64_t n, uint32_t dim,
+                        float* d_rows_out, float* d_coverage_out);
+
+/* ---- vector store + query (vecstore.hpp:21-146) ----------------------- */
+/* build_store (vecstore.hpp:88-103): covered rows of a table -> unit rows
+ * (normalized_copy, vecstore.hpp:34-42, f64 norm).  Keeps the store on the
+ * device; returns the number of covered rows. */
+int ss_store_build(ss_ctx* ctx, const float* rows, const float* coverage, uint64_t n, uint32_t dim,
+                   uint64_t* count_out);
+/* Upload an already-normalized store (ids + unit rows). */
+int ss_store_set(ss_ctx* ctx, const uint32_t* ids, const float* unit_rows, uint64_t count, uint32_t dim);
+/* Fetch the device store (ids: count; unit_rows: count x dim). */
+int ss_store_fetch(ss_ctx* ctx, uint32_t* ids, float* unit_rows);
+/* query_topk (vecstore.hpp:121-132) for nq queries (raw, un-normalized):
+ * out_ids/out_sims nq x k; out_counts[q] = min(k, count). */
+int ss_query_topk(ss_ctx* ctx, const float* queries, uint32_t nq, uint32_t k, uint32_t* out_ids, float* out_sims,
+                  uint64_t* out_counts);
+/* query_threshold (vecstore.hpp:135-146) for one query: all sims >= tau,
+ * (sim desc, id asc).  capacity = size of out arrays. */
+int ss_query_threshold(ss_ctx* ctx, const float* query, float tau, uint32_t* out_ids, float* out_sims,
+                       uint64_t capacity, uint64_t* out_count);
+
+/* ---- instrumentation --------------------------------------------------- */
+/* Per-kernel-class device time (CUDA events on the launching stream) and
+ * algorithmic byte/flop counts, accumulated while enabled. */
+enum ss_kernel_class {
+    SS_K_MASKS = 0,    /* RLE decode + resample into per-pixel bitsets */
+    SS_K_PROJECT = 1,  /* project (+ ordered compaction) */
+    SS_K_SORT = 2,     /* depth sort + tile-key sort */
+    SS_K_BIN = 3,      /* record gather, tile counts, key emission, ranges */
+    SS_K_RASTER = 4,   /* fused mask-gated compositor */
+    SS_K_CONTRACT = 5, /* sparse 512-d contraction */
+    SS_K_NORMALIZE = 6,
+    SS_K_QUERY = 7,
+    SS_K_H2D = 8,
+    SS_K_COUNT = 9
+};
+int ss_profile_enable(ss_ctx* ctx, int on);
+int ss_profile_reset(ss_ctx* ctx);
+/* ms[SS_K_COUNT], launches[SS_K_COUNT], bytes[SS_K_COUNT] (algorithmic). */
+int ss_profile_read(ss_ctx* ctx, double* ms, uint64_t* launches, double* bytes);
+/* Running totals of the geometry counters (SURVEY.md 8 notation), summed over
+ * views since ss_profile_reset: [0]=N_vis [1]=I_v [2]=G_v [3]=K_v [4]=views. */
+int ss_counters_read(ss_ctx* ctx, uint64_t* out5);
+/* Number of kernels this library launched (own + CUB) since reset. */
+int ss_launch_count(ss_ctx* ctx, uint64_t* own, uint64_t* cub);
+
+/* ---- synthetic workload (main.cpp:334-410 write_bench_dataset) --------- */
+/* Bench-style uniform scene (main.cpp:340-352) from std::mt19937_64(seed). */
+int ss_synth_scene(uint64_t seed, uint64_t n, double xy_extent, double z_extent, float* mean, float* scale,
+                   float* quat_xyzw, float* opacity, float* color);
+/* fixture.hpp:65-84 look_at */
+int ss_synth_look_at(const double* eye, const double* target, uint32_t width, uint32_t height, double focal,
+                     ss_camera* out);
+/* providers.hpp:381-400 synth_embedding */
+int ss_synth_embedding(const char* label, uint32_t dim, float* out);
+/* Random-rectangle masks for one view (main.cpp:386-396) from the rng state
+ * seeded by seed; writes RLE runs (capacity >= n_masks*(2*height+2)) and
+ * run_offsets (n_masks+1). */
+int ss_synth_rect_masks(uint64_t seed, uint32_t width, uint32_t height, uint32_t n_masks, uint32_t* runs,
+                        uint64_t* run_offsets);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SEMSPLAT_B200_H */

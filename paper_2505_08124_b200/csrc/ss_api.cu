@@ -1,0 +1,1023 @@
+// libsemsplat_b200 host runtime: the C ABI of include/semsplat_b200.h.
+//
+// One ss_ctx per device.  It owns the resident scene (float4 SoA), the
+// capacity-managed per-view scratch, the per-(rank, mask) scalar buffer and
+// the N x D fp32 accumulators, and drives the per-view pipeline
+//   RLE -> bitset -> project -> ordered compaction -> depth radix sort ->
+//   record gather + tile counts -> scan -> key emission -> tile radix sort ->
+//   tile ranges -> fused compositor -> sparse contraction
+// on one CUDA stream.  Replaces encode_scene's phase 1/phase 2 loops
+// (pipeline.hpp:280-470) for the views handed to it.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
+
+#include "ss_kernels.cuh"
+
+namespace ss {
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_kind = 0;
+
+struct Error : std::runtime_error {
+    int kind;
+    Error(int k, const std::string& m) : std::runtime_error(m), kind(k) {}
+};
+
+#define SS_CUDA(expr)                                                                                       \
+    do {                                                                                                    \
+        cudaError_t _e = (expr);                                                                            \
+        if (_e != cudaSuccess)                                                                              \
+            throw Error(SS_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e) + " (" __FILE__ ":" + \
+                                         std::to_string(__LINE__) + ")");                                   \
+    } while (0)
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        g_err.clear();
+        g_kind = 0;
+        return 0;
+    } catch (const Error& e) {
+        g_err = e.what();
+        g_kind = e.kind;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        g_kind = SS_ERR_CUDA;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        g_kind = SS_ERR_CUDA;
+    }
+    return g_kind;
+}
+
+// Grow-only device buffer.
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void* ensure(size_t want) {
+        if (want <= bytes && p) return p;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        size_t cap = std::max<size_t>(want, 256);
+        cap = cap + cap / 8; // slack so slowly growing sizes do not thrash
+        SS_CUDA(cudaMalloc(&p, cap));
+        bytes = cap;
+        return p;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+struct ProfState {
+    bool on = false;
+    std::vector<cudaEvent_t> pool;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+    double ms[SS_K_COUNT] = {};
+    uint64_t launches[SS_K_COUNT] = {};
+    double bytes[SS_K_COUNT] = {};
+    cudaEvent_t get() {
+        if (pool.empty()) {
+            cudaEvent_t e;
+            SS_CUDA(cudaEventCreate(&e));
+            return e;
+        }
+        cudaEvent_t e = pool.back();
+        pool.pop_back();
+        return e;
+    }
+};
+
+} // namespace
+} // namespace ss
+
+struct ss_ctx {
+    int device = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+
+    // scene
+    uint64_t n = 0;
+    ss::DevBuf mean_op, scale, quat;
+
+    // per-view geometry scratch
+    ss::DevBuf rec, keys, flags, keys_sel, ids_sel, keys_sorted, order, rec_sorted, ntiles, offsets;
+    ss::DevBuf tile_keys, tile_vals, tile_keys_sorted, tile_ranks, tile_start, tile_end;
+    ss::DevBuf cub_tmp, num_sel;
+    ss::DevBuf info;
+    ss::ViewInfo* h_info = nullptr; // pinned
+    ss::ViewInfo* h_init = nullptr; // pinned
+    uint32_t* h_u32 = nullptr;      // pinned scratch
+
+    // masks
+    ss::DevBuf pix_bits, mask_bits, runs, run_offsets, clip;
+    // capture
+    ss::DevBuf pix_count, pix_offset, entries, per_pixel_total, alpha;
+    uint64_t cap_entries = 0, cap_splats = 0, cap_instances = 0;
+    uint32_t cap_width = 0, cap_height = 0, cap_tiles = 0;
+    // fused path
+    ss::DevBuf acc, touched, touched_list;
+    uint64_t acc_elems = 0; // zero-initialised elements of acc
+    ss::DevBuf counters;    // [0] G_v sum, [1] K_v sum
+    // accumulators
+    uint32_t dim = 0;
+    float* sums = nullptr;
+    float* totals = nullptr;
+    bool own_acc = false;
+    ss::DevBuf sums_buf, totals_buf;
+    // store + query
+    ss::DevBuf store_rows, store_ids, qbuf, qnorm, scores, topk_ids, topk_sims, sel_flags, thr_keys, thr_keys_sorted,
+        thr_ids, thr_ids_sorted, zero_flag;
+    uint64_t store_count = 0;
+    uint32_t store_dim = 0;
+
+    // instrumentation
+    ss::ProfState prof;
+    uint64_t launches_own = 0, launches_cub = 0;
+    uint64_t cnt_vis = 0, cnt_inst = 0, cnt_views = 0;
+};
+
+namespace ss {
+namespace {
+
+struct Scope {
+    ss_ctx* c;
+    int cls;
+    cudaEvent_t a = nullptr, b = nullptr;
+    Scope(ss_ctx* ctx, int k) : c(ctx), cls(k) {
+        if (c->prof.on) {
+            a = c->prof.get();
+            b = c->prof.get();
+            SS_CUDA(cudaEventRecord(a, c->stream));
+        }
+    }
+    ~Scope() {
+        if (c->prof.on && a) {
+            cudaEventRecord(b, c->stream);
+            c->prof.pending.push_back({cls, {a, b}});
+        }
+    }
+};
+
+inline void own_launch(ss_ctx* c, cudaError_t e, int cls, uint64_t count = 1) {
+    if (e != cudaSuccess) throw Error(SS_ERR_CUDA, std::string("kernel launch failed: ") + cudaGetErrorString(e));
+    c->launches_own += count;
+    c->prof.launches[cls] += count;
+}
+
+void set_device(ss_ctx* c) { SS_CUDA(cudaSetDevice(c->device)); }
+
+void reset_info(ss_ctx* c) {
+    SS_CUDA(cudaMemcpyAsync(c->info.p, c->h_init, sizeof(ViewInfo), cudaMemcpyHostToDevice, c->stream));
+}
+
+void sync_info(ss_ctx* c) {
+    SS_CUDA(cudaMemcpyAsync(c->h_info, c->info.p, sizeof(ViewInfo), cudaMemcpyDeviceToHost, c->stream));
+    SS_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+uint32_t bits_for(uint64_t v) { // number of bits to represent v (v >= 1 -> >= 1)
+    uint32_t b = 0;
+    while (b < 64 && (v >> b) != 0) ++b;
+    return b ? b : 1;
+}
+
+void check_camera(const ss_camera* cam) {
+    if (!cam) throw Error(SS_ERR_CONTRACT, "camera is null");
+    if (cam->width == 0 || cam->height == 0) throw Error(SS_ERR_DATA, "camera has zero raster resolution");
+    if (cam->width > 65535 || cam->height > 65535)
+        throw Error(SS_ERR_CONTRACT, "raster resolution above 65535 is not supported");
+}
+
+struct Geometry {
+    uint64_t n_surv = 0;
+    uint64_t n_inst = 0;
+    uint32_t tiles_x = 0, tiles_y = 0, tiles = 0;
+};
+
+// project -> ordered compaction -> depth sort -> gather -> tile keys -> tile sort -> ranges
+Geometry run_geometry(ss_ctx* c, const ss_camera& cam, int err_kind, const char* err_prefix) {
+    Geometry g;
+    const uint64_t N = c->n;
+    g.tiles_x = (cam.width + kTile - 1) / kTile;
+    g.tiles_y = (cam.height + kTile - 1) / kTile;
+    g.tiles = g.tiles_x * g.tiles_y;
+    cudaStream_t s = c->stream;
+
+    auto* rec = static_cast<SplatRec*>(c->rec.ensure(std::max<uint64_t>(N, 1) * sizeof(SplatRec)));
+    auto* keys = static_cast<unsigned long long*>(c->keys.ensure(std::max<uint64_t>(N, 1) * 8));
+    auto* flags = static_cast<uint8_t*>(c->flags.ensure(std::max<uint64_t>(N, 1)));
+    auto* keys_sel = static_cast<unsigned long long*>(c->keys_sel.ensure(std::max<uint64_t>(N, 1) * 8));
+    auto* ids_sel = static_cast<uint32_t*>(c->ids_sel.ensure(std::max<uint64_t>(N, 1) * 4));
+    auto* keys_sorted = static_cast<unsigned long long*>(c->keys_sorted.ensure(std::max<uint64_t>(N, 1) * 8));
+    auto* order = static_cast<uint32_t*>(c->order.ensure(std::max<uint64_t>(N, 1) * 4));
+    auto* rec_sorted = static_cast<SplatRec*>(c->rec_sorted.ensure(std::max<uint64_t>(N, 1) * sizeof(SplatRec)));
+    auto* ntiles = static_cast<uint32_t*>(c->ntiles.ensure((N + 1) * 4));
+    auto* offsets = static_cast<uint32_t*>(c->offsets.ensure((N + 1) * 4));
+    auto* num_sel = static_cast<int*>(c->num_sel.ensure(16));
+    auto* tstart = static_cast<uint32_t*>(c->tile_start.ensure((size_t)g.tiles * 4));
+    auto* tend = static_cast<uint32_t*>(c->tile_end.ensure((size_t)g.tiles * 4));
+    ViewInfo* info = c->info.as<ViewInfo>();
+
+    reset_info(c);
+    {
+        Scope sc(c, SS_K_PROJECT);
+        ProjectParams p;
+        p.mean_op = c->mean_op.as<float4>();
+        p.scale = c->scale.as<float4>();
+        p.quat = c->quat.as<float4>();
+        p.n = N;
+        p.cam = cam;
+        p.rec = rec;
+        p.keys = keys;
+        p.flags = flags;
+        p.info = info;
+        p.dbg = nullptr;
+        own_launch(c, launch_project(p, s), SS_K_PROJECT);
+        // ordered compaction of (depth key, id) for the survivors
+        size_t tb = 0, tb2 = 0;
+        cub::CountingInputIterator<uint32_t> ids(0);
+        SS_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, keys, flags, keys_sel, num_sel, (int)N, s));
+        SS_CUDA(cub::DeviceSelect::Flagged(nullptr, tb2, ids, flags, ids_sel, num_sel + 1, (int)N, s));
+        void* tmp = c->cub_tmp.ensure(std::max(tb, tb2));
+        tb = c->cub_tmp.bytes;
+        SS_CUDA(cub::DeviceSelect::Flagged(tmp, tb, keys, flags, keys_sel, num_sel, (int)N, s));
+        SS_CUDA(cub::DeviceSelect::Flagged(tmp, tb, ids, flags, ids_sel, num_sel + 1, (int)N, s));
+        c->launches_cub += 4;
+        c->prof.launches[SS_K_PROJECT] += 4;
+        c->prof.bytes[SS_K_PROJECT] += 44.0 * (double)N;
+    }
+    sync_info(c);
+    if (c->h_info->err_count)
+        throw Error(err_kind, std::string(err_prefix) + "singular screen covariance for gaussian " +
+                                  std::to_string(c->h_info->err_gid));
+    g.n_surv = c->h_info->n_surv;
+    const uint64_t n = g.n_surv;
+    c->prof.bytes[SS_K_PROJECT] += 76.0 * (double)n;
+
+    SS_CUDA(cudaMemsetAsync(tstart, 0, (size_t)g.tiles * 4, s));
+    SS_CUDA(cudaMemsetAsync(tend, 0, (size_t)g.tiles * 4, s));
+    if (n == 0) return g;
+
+    {
+        Scope sc(c, SS_K_SORT);
+        // depth sort on the varying bit range; stable => ties keep id order
+        const uint32_t hb = bits_for(c->h_info->min_key ^ c->h_info->max_key);
+        const uint32_t end_bit = (c->h_info->min_key == c->h_info->max_key) ? 1 : hb;
+        size_t tb = 0;
+        SS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys_sel, keys_sorted, ids_sel, order, (int)n, 0,
+                                                (int)end_bit, s));
+        void* tmp = c->cub_tmp.ensure(tb);
+        tb = c->cub_tmp.bytes;
+        SS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys_sel, keys_sorted, ids_sel, order, (int)n, 0,
+                                                (int)end_bit, s));
+        c->launches_cub += 1;
+        c->prof.launches[SS_K_SORT] += 1;
+        c->prof.bytes[SS_K_SORT] += 24.0 * (double)n;
+    }
+    {
+        Scope sc(c, SS_K_BIN);
+        own_launch(c, launch_gather(order, n, rec, rec_sorted, ntiles, s), SS_K_BIN);
+        SS_CUDA(cudaMemsetAsync(ntiles + n, 0, 4, s));
+        size_t tb = 0;
+        SS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, ntiles, offsets, (int)(n + 1), s));
+        void* tmp = c->cub_tmp.ensure(tb);
+        tb = c->cub_tmp.bytes;
+        SS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, ntiles, offsets, (int)(n + 1), s));
+        c->launches_cub += 1;
+        c->prof.launches[SS_K_BIN] += 1;
+        SS_CUDA(cudaMemcpyAsync(c->h_u32, offsets + n, 4, cudaMemcpyDeviceToHost, s));
+        SS_CUDA(cudaStreamSynchronize(s));
+    }
+    g.n_inst = c->h_u32[0];
+    const uint64_t I = g.n_inst;
+    auto* tkeys = static_cast<uint32_t*>(c->tile_keys.ensure(std::max<uint64_t>(I, 1) * 4));
+    auto* tvals = static_cast<uint32_t*>(c->tile_vals.ensure(std::max<uint64_t>(I, 1) * 4));
+    auto* tkeys_sorted = static_cast<uint32_t*>(c->tile_keys_sorted.ensure(std::max<uint64_t>(I, 1) * 4));
+    auto* tranks = static_cast<uint32_t*>(c->tile_ranks.ensure(std::max<uint64_t>(I, 1) * 4));
+    {
+        Scope sc(c, SS_K_BIN);
+        own_launch(c, launch_emit_keys(rec_sorted, offsets, n, g.tiles_x, tkeys, tvals, s), SS_K_BIN);
+        c->prof.bytes[SS_K_BIN] += 128.0 * (double)n + 8.0 * (double)I;
+    }
+    {
+        Scope sc(c, SS_K_SORT);
+        const uint32_t tbits = bits_for(g.tiles - 1);
+        size_t tb = 0;
+        SS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, tkeys, tkeys_sorted, tvals, tranks, (int)I, 0,
+                                                (int)tbits, s));
+        void* tmp = c->cub_tmp.ensure(tb);
+        tb = c->cub_tmp.bytes;
+        SS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, tkeys, tkeys_sorted, tvals, tranks, (int)I, 0, (int)tbits,
+                                                s));
+        c->launches_cub += 1;
+        c->prof.launches[SS_K_SORT] += 1;
+        c->prof.bytes[SS_K_SORT] += 16.0 * (double)I;
+    }
+    {
+        Scope sc(c, SS_K_BIN);
+        own_launch(c, launch_tile_ranges(tkeys_sorted, I, tstart, tend, s), SS_K_BIN);
+        c->prof.bytes[SS_K_BIN] += 4.0 * (double)I + 8.0 * g.tiles;
+    }
+    c->cnt_vis += n;
+    c->cnt_inst += I;
+    return g;
+}
+
+RasterParams raster_params(ss_ctx* c, const ss_camera& cam, const Geometry& g) {
+    RasterParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.rec_sorted = c->rec_sorted.as<SplatRec>();
+    p.tile_ranks = c->tile_ranks.as<uint32_t>();
+    p.tile_start = c->tile_start.as<uint32_t>();
+    p.tile_end = c->tile_end.as<uint32_t>();
+    p.width = cam.width;
+    p.height = cam.height;
+    p.tiles_x = g.tiles_x;
+    p.info = c->info.as<ViewInfo>();
+    return p;
+}
+
+uint32_t mask_words_for(uint32_t m) { return m <= 32 ? 1 : (m <= 64 ? 2 : 4); }
+
+// Upload one view's RLE masks + CLIP and build the raster-resolution bitsets.
+void build_mask_bits(ss_ctx* c, const ss_camera& cam, const ss_view_masks* vm, uint32_t words, uint32_t image_id) {
+    cudaStream_t s = c->stream;
+    const uint32_t M = vm->n_masks;
+    const uint64_t P = (uint64_t)cam.width * cam.height;
+    auto* pb = static_cast<uint32_t*>(c->pix_bits.ensure(P * words * 4));
+    Scope sc(c, SS_K_MASKS);
+    SS_CUDA(cudaMemsetAsync(pb, 0, P * words * 4, s));
+    if (M == 0) return;
+    const uint64_t mw = vm->mask_width, mh = vm->mask_height;
+    if (mw == 0 || mh == 0) throw Error(SS_ERR_CONTRACT, "resample_mask: zero mask resolution");
+    // validate run streams against the mask area (providers.hpp:97-107)
+    const uint64_t nr = vm->run_offsets[M] - vm->run_offsets[0];
+    for (uint32_t m = 0; m < M; ++m) {
+        uint64_t tot = 0;
+        for (uint64_t r = vm->run_offsets[m]; r < vm->run_offsets[m + 1]; ++r) tot += vm->runs[r];
+        if (tot != mw * mh)
+            throw Error(SS_ERR_FORMAT, "image " + std::to_string(image_id) + ": mask RLE length mismatch: runs cover " +
+                                           std::to_string(tot) + " of " + std::to_string(mw * mh) + " pixels");
+    }
+    auto* d_runs = static_cast<uint32_t*>(c->runs.ensure(std::max<uint64_t>(nr, 1) * 4));
+    auto* d_off = static_cast<uint64_t*>(c->run_offsets.ensure((M + 1) * 8ull));
+    std::vector<uint64_t> rel(M + 1);
+    for (uint32_t m = 0; m <= M; ++m) rel[m] = vm->run_offsets[m] - vm->run_offsets[0];
+    {
+        Scope h(c, SS_K_H2D);
+        SS_CUDA(cudaMemcpyAsync(d_runs, vm->runs + vm->run_offsets[0], nr * 4, cudaMemcpyHostToDevice, s));
+        SS_CUDA(cudaMemcpyAsync(d_off, rel.data(), (M + 1) * 8ull, cudaMemcpyHostToDevice, s));
+        c->prof.bytes[SS_K_H2D] += nr * 4.0 + (M + 1) * 8.0;
+    }
+    const bool same = mw == cam.width && mh == cam.height;
+    uint32_t* target = pb;
+    if (!same) {
+        target = static_cast<uint32_t*>(c->mask_bits.ensure(mw * mh * words * 4));
+        SS_CUDA(cudaMemsetAsync(target, 0, mw * mh * words * 4, s));
+    }
+    own_launch(c, launch_rle_to_bits(d_runs, d_off, M, words, target, s), SS_K_MASKS);
+    if (!same)
+        own_launch(c, launch_resample_bits(target, (uint32_t)mw, (uint32_t)mh, pb, cam.width, cam.height, words, s),
+                   SS_K_MASKS);
+    c->prof.bytes[SS_K_MASKS] += nr * 4.0 + (double)P * ((M + 7) / 8);
+    // std::vector rel must outlive the async copy from pageable memory: cudaMemcpyAsync
+    // from pageable memory is staged synchronously, so returning is safe.
+}
+
+void encode_one(ss_ctx* c, const ss_camera& cam, const ss_view_masks* vm, int mode) {
+    check_camera(&cam);
+    if (!c->sums) throw Error(SS_ERR_CONTRACT, "ss_encode_view before ss_encode_begin");
+    if (c->n == 0) return;
+    const uint32_t M = vm ? vm->n_masks : 0;
+    if (M > 128) throw Error(SS_ERR_CONTRACT, "at most 128 masks per view are supported");
+    const uint32_t words = mask_words_for(M);
+    const std::string prefix = "image " + std::to_string(cam.image_id) + ": ";
+    cudaStream_t s = c->stream;
+    if (M) build_mask_bits(c, cam, vm, words, cam.image_id);
+    auto* d_clip = static_cast<float*>(c->clip.ensure(std::max<uint64_t>((uint64_t)M * c->dim, 1) * 4));
+    if (M) {
+        Scope h(c, SS_K_H2D);
+        SS_CUDA(cudaMemcpyAsync(d_clip, vm->clip, (size_t)M * c->dim * 4, cudaMemcpyHostToDevice, s));
+        c->prof.bytes[SS_K_H2D] += (double)M * c->dim * 4;
+    }
+    const Geometry g = run_geometry(c, cam, SS_ERR_DATA, prefix.c_str());
+    c->cnt_views += 1;
+    if (g.n_surv == 0 || M == 0) return;
+
+    // per-(rank, mask) scalars: grow-only and kept zero by consume-and-clear
+    const uint64_t need = g.n_surv * (uint64_t)M;
+    if (need > c->acc_elems) {
+        const uint64_t cap = std::max<uint64_t>(need, c->n * (uint64_t)std::min<uint32_t>(std::max(M, 16u), 128u));
+        c->acc.release();
+        c->acc.ensure(cap * 4);
+        SS_CUDA(cudaMemsetAsync(c->acc.p, 0, c->acc.bytes, s));
+        c->acc_elems = c->acc.bytes / 4;
+    }
+    auto* touched = static_cast<uint32_t*>(c->touched.p);
+    if (c->touched.bytes < c->n * 4) {
+        c->touched.release();
+        touched = static_cast<uint32_t*>(c->touched.ensure(c->n * 4));
+        SS_CUDA(cudaMemsetAsync(touched, 0, c->touched.bytes, s));
+    }
+    auto* tlist = static_cast<uint32_t*>(c->touched_list.ensure(c->n * 4));
+
+    {
+        Scope sc(c, SS_K_RASTER);
+        RasterParams p = raster_params(c, cam, g);
+        p.pix_bits = c->pix_bits.as<uint32_t>();
+        p.mask_words = words;
+        p.n_masks = M;
+        p.acc = c->acc.as<float>();
+        p.touched = touched;
+        p.touched_list = tlist;
+        own_launch(c, launch_raster_fused(p, mode, g.tiles, s), SS_K_RASTER);
+        const uint64_t P = (uint64_t)cam.width * cam.height;
+        c->prof.bytes[SS_K_RASTER] += 64.0 * (double)g.n_inst + (double)P * ((M + 7) / 8);
+    }
+    {
+        Scope sc(c, SS_K_CONTRACT);
+        ContractParams q;
+        q.touched_list = tlist;
+        q.touched = touched;
+        q.order = c->order.as<uint32_t>();
+        q.acc = c->acc.as<float>();
+        q.n_masks = M;
+        q.clip = d_clip;
+        q.dim = c->dim;
+        q.sums = c->sums;
+        q.totals = c->totals;
+        q.info = c->info.as<ViewInfo>();
+        q.count_pairs = 1;
+        q.cum = c->counters.as<unsigned long long>();
+        own_launch(c, launch_contract(q, g.n_surv, s), SS_K_CONTRACT);
+        c->prof.bytes[SS_K_CONTRACT] += (double)M * c->dim * 4;
+    }
+}
+
+void profile_drain(ss_ctx* c) {
+    if (c->prof.pending.empty()) return;
+    SS_CUDA(cudaStreamSynchronize(c->stream));
+    for (auto& pe : c->prof.pending) {
+        float ms = 0;
+        SS_CUDA(cudaEventElapsedTime(&ms, pe.second.first, pe.second.second));
+        c->prof.ms[pe.first] += ms;
+        c->prof.pool.push_back(pe.second.first);
+        c->prof.pool.push_back(pe.second.second);
+    }
+    c->prof.pending.clear();
+}
+
+} // namespace
+} // namespace ss
+
+using namespace ss;
+
+extern "C" {
+
+const char* ss_last_error(void) { return ss::g_err.c_str(); }
+int ss_last_error_kind(void) { return ss::g_kind; }
+
+int ss_create(int device, ss_ctx** out) {
+    return guarded([&] {
+        if (!out) throw Error(SS_ERR_CONTRACT, "out is null");
+        int ndev = 0;
+        cudaError_t e = cudaGetDeviceCount(&ndev);
+        if (e != cudaSuccess || ndev == 0)
+            throw Error(SS_ERR_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+        if (device < 0 || device >= ndev) throw Error(SS_ERR_CONTRACT, "device index out of range");
+        cudaDeviceProp prop;
+        SS_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10)
+            throw Error(SS_ERR_CUDA, std::string("libsemsplat_b200 is built for sm_100a; device is ") + prop.name);
+        auto* c = new ss_ctx();
+        c->device = device;
+        SS_CUDA(cudaSetDevice(device));
+        SS_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+        c->stream = c->own_stream;
+        SS_CUDA(cudaMallocHost(&c->h_info, sizeof(ViewInfo)));
+        SS_CUDA(cudaMallocHost(&c->h_init, sizeof(ViewInfo)));
+        SS_CUDA(cudaMallocHost(&c->h_u32, 64));
+        std::memset(c->h_init, 0, sizeof(ViewInfo));
+        c->h_init->min_key = ~0ull;
+        c->h_init->err_gid = ~0u;
+        c->info.ensure(sizeof(ViewInfo));
+        c->counters.ensure(16);
+        SS_CUDA(cudaMemset(c->counters.p, 0, c->counters.bytes));
+        *out = c;
+    });
+}
+
+void ss_destroy(ss_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    ss::DevBuf* bufs[] = {&c->mean_op, &c->scale, &c->quat, &c->rec, &c->keys, &c->flags, &c->keys_sel, &c->ids_sel,
+                          &c->keys_sorted, &c->order, &c->rec_sorted, &c->ntiles, &c->offsets, &c->tile_keys,
+                          &c->tile_vals, &c->tile_keys_sorted, &c->tile_ranks, &c->tile_start, &c->tile_end,
+                          &c->cub_tmp, &c->num_sel, &c->info, &c->pix_bits, &c->mask_bits, &c->runs,
+                          &c->run_offsets, &c->clip, &c->pix_count, &c->pix_offset, &c->entries,
+                          &c->per_pixel_total, &c->alpha, &c->acc, &c->touched, &c->touched_list, &c->counters,
+                          &c->sums_buf, &c->totals_buf, &c->store_rows, &c->store_ids, &c->qbuf, &c->qnorm,
+                          &c->scores, &c->topk_ids, &c->topk_sims, &c->sel_flags, &c->thr_keys, &c->thr_keys_sorted,
+                          &c->thr_ids, &c->thr_ids_sorted, &c->zero_flag};
+    for (auto* b : bufs) b->release();
+    for (auto e : c->prof.pool) cudaEventDestroy(e);
+    for (auto& pe : c->prof.pending) {
+        cudaEventDestroy(pe.second.first);
+        cudaEventDestroy(pe.second.second);
+    }
+    if (c->h_info) cudaFreeHost(c->h_info);
+    if (c->h_init) cudaFreeHost(c->h_init);
+    if (c->h_u32) cudaFreeHost(c->h_u32);
+    if (c->own_stream) cudaStreamDestroy(c->own_stream);
+    delete c;
+}
+
+int ss_set_stream(ss_ctx* c, uintptr_t stream) {
+    return guarded([&] {
+        if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
+        c->stream = stream ? reinterpret_cast<cudaStream_t>(stream) : c->own_stream;
+    });
+}
+
+int ss_synchronize(ss_ctx* c) {
+    return guarded([&] {
+        set_device(c);
+        SS_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int ss_scene_set(ss_ctx* c, const float* mean, const float* scale, const float* quat_xyzw, const float* opacity,
+                 uint64_t n) {
+    return guarded([&] {
+        if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
+        if (n >= (1ull << 32)) throw Error(SS_ERR_CONTRACT, "gaussian ids are u32 (scene.hpp:23)");
+        set_device(c);
+        std::vector<float> a(std::max<uint64_t>(n, 1) * 4), b(std::max<uint64_t>(n, 1) * 4),
+            q(std::max<uint64_t>(n, 1) * 4);
+        for (uint64_t k = 0; k < n; ++k) {
+            a[4 * k] = mean[3 * k];
+            a[4 * k + 1] = mean[3 * k + 1];
+            a[4 * k + 2] = mean[3 * k + 2];
+            a[4 * k + 3] = opacity[k];
+            b[4 * k] = scale[3 * k];
+            b[4 * k + 1] = scale[3 * k + 1];
+            b[4 * k + 2] = scale[3 * k + 2];
+            b[4 * k + 3] = 0.0f;
+            for (int i = 0; i < 4; ++i) q[4 * k + i] = quat_xyzw[4 * k + i];
+        }
+        c->n = n;
+        const size_t bytes = std::max<uint64_t>(n, 1) * 16;
+        SS_CUDA(cudaMemcpyAsync(c->mean_op.ensure(bytes), a.data(), n * 16, cudaMemcpyHostToDevice, c->stream));
+        SS_CUDA(cudaMemcpyAsync(c->scale.ensure(bytes), b.data(), n * 16, cudaMemcpyHostToDevice, c->stream));
+        SS_CUDA(cudaMemcpyAsync(c->quat.ensure(bytes), q.data(), n * 16, cudaMemcpyHostToDevice, c->stream));
+        SS_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int ss_project(ss_ctx* c, const ss_camera* cam, ss_projected* out) {
+    return guarded([&] {
+        if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
+        check_camera(cam);
+        set_device(c);
+        const uint64_t N = c->n;
+        if (N == 0) return;
+        cudaStream_t s = c->stream;
+        auto* dbg = static_cast<ss_projected*>(c->scores.ensure(N * sizeof(ss_projected)));
+        reset_info(c);
+        ProjectParams p;
+        p.mean_op = c->mean_op.as<float4>();
+        p.scale = c->scale.as<float4>();
+        p.quat = c->quat.as<float4>();
+        p.n = N;
+        p.cam = *cam;
+        p.rec = static_cast<SplatRec*>(c->rec.ensure(N * sizeof(SplatRec)));
+        p.keys = static_cast<unsigned long long*>(c->keys.ensure(N * 8));
+        p.flags = static_cast<uint8_t*>(c->flags.ensure(N));
+        p.info = c->info.as<ViewInfo>();
+        p.dbg = dbg;
+        own_launch(c, launch_project(p, s), SS_K_PROJECT);
+        SS_CUDA(cudaMemcpyAsync(out, dbg, N * sizeof(ss_projected), cudaMemcpyDeviceToHost, s));
+        SS_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int ss_raster_capture(ss_ctx* c, const ss_camera* cam, int mode, uint64_t* n_entries, uint64_t* n_splats,
+                      uint64_t* n_tile_instances) {
+    return guarded([&] {
+        if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
+        check_camera(cam);
+        set_device(c);
+        cudaStream_t s = c->stream;
+        const uint64_t P = (uint64_t)cam->width * cam->height;
+        const Geometry g = run_geometry(c, *cam, SS_ERR_NUMERIC, "");
+        auto* cnt = static_cast<uint32_t*>(c->pix_count.ensure((P + 1) * 4));
+        auto* off = static_cast<uint32_t*>(c->pix_offset.ensure((P + 1) * 4));
+        auto* ppt = static_cast<float*>(c->per_pixel_total.ensure(P * 4));
+        auto* alp = static_cast<float*>(c->alpha.ensure(P * 4));
+        SS_CUDA(cudaMemsetAsync(cnt, 0, (P + 1) * 4, s));
+        SS_CUDA(cudaMemsetAsync(ppt, 0, P * 4, s));
+        SS_CUDA(cudaMemsetAsync(alp, 0, P * 4, s));
+        RasterParams p = raster_params(c, *cam, g);
+        if (g.n_surv) {
+            p.pix_count = cnt;
+            own_launch(c, launch_raster_count(p, mode, g.tiles, s), SS_K_RASTER);
+        }
+        size_t tb = 0;
+        SS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, (int)(P + 1), s));
+        void* tmp = c->cub_tmp.ensure(tb);
+        tb = c->cub_tmp.bytes;
+        SS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, off, (int)(P + 1), s));
+        c->launches_cub += 1;
+        SS_CUDA(cudaMemcpyAsync(c->h_u32, off + P, 4, cudaMemcpyDeviceToHost, s));
+        SS_CUDA(cudaStreamSynchronize(s));
+        const uint64_t E = c->h_u32[0];
+        auto* ent = static_cast<ss_weight_entry*>(c->entries.ensure(std::max<uint64_t>(E, 1) * sizeof(ss_weight_entry)));
+        if (g.n_surv) {
+            p.pix_offset = off;
+            p.entries = ent;
+            p.per_pixel_total = ppt;
+            p.alpha = alp;
+            own_launch(c, launch_raster_capture(p, mode, g.tiles, s), SS_K_RASTER);
+        }
+        SS_CUDA(cudaStreamSynchronize(s));
+        c->cap_entries = E;
+        c->cap_splats = g.n_surv;
+        c->cap_instances = g.n_inst;
+        c->cap_width = cam->width;
+        c->cap_height = cam->height;
+        c->cap_tiles = g.tiles;
+        if (n_entries) *n_entries = E;
+        if (n_splats) *n_splats = g.n_surv;
+        if (n_tile_instances) *n_tile_instances = g.n_inst;
+    });
+}
+
+int ss_raster_fetch(ss_ctx* c, ss_weight_entry* entries, float* per_pixel_total, float* alpha, uint32_t* splat_gid,
+                    uint32_t* tile_offsets, uint32_t* tile_splats) {
+    return guarded([&] {
+        if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
+        set_device(c);
+        const uint64_t P = (uint64_t)c->cap_width * c->cap_height;
+        if (entries && c->cap_entries)
+            SS_CUDA(cudaMemcpy(entries, c->entries.p, c->cap_entries * sizeof(ss_weight_entry), cudaMemcpyDeviceToHost));
+        if (per_pixel_total && P) SS_CUDA(cudaMemcpy(per_pixel_total, c->per_pixel_total.p, P * 4, cudaMemcpyDeviceToHost));
+        if (alpha && P) SS_CUDA(cudaMemcpy(alpha, c->alpha.p, P * 4, cudaMemcpyDeviceToHost));
+        if (splat_gid && c->cap_splats)
+            SS_CUDA(cudaMemcpy(splat_gid, c->order.p, c->cap_splats * 4, cudaMemcpyDeviceToHost));
+        if (tile_offsets || tile_splats) {
+            std::vector<uint32_t> st(c->cap_tiles), en(c->cap_tiles);
+            if (c->cap_tiles) {
+                SS_CUDA(cudaMemcpy(st.data(), c->tile_start.p, c->cap_tiles * 4, cudaMemcpyDeviceToHost));
+                SS_CUDA(cudaMemcpy(en.data(), c->tile_end.p, c->cap_tiles * 4, cudaMemcpyDeviceToHost));
+            }
+            if (tile_offsets) {
+                // tiles are contiguous in key order, so start of tile t is the
+                // running count of instances in tiles < t
+                uint32_t run = 0;
+                for (uint32_t t = 0; t < c->cap_tiles; ++t) {
+                    tile_offsets[t] = run;
+                    run += en[t] - st[t];
+                }
+                tile_offsets[c->cap_tiles] = run;
+            }
+            if (tile_splats && c->cap_instances)
+                SS_CUDA(cudaMemcpy(tile_splats, c->tile_ranks.p, c->cap_instances * 4, cudaMemcpyDeviceToHost));
+        }
+    });
+}
+
+int ss_encode_begin(ss_ctx* c, uint32_t dim, float* d_sums, float* d_totals) {
+    return guarded([&] {
+        if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
+        if (dim == 0) throw Error(SS_ERR_CONTRACT, "embedding dimension must be positive");
+        if ((d_sums == nullptr) != (d_totals == nullptr))
+            throw Error(SS_ERR_CONTRACT, "pass both external accumulators or neither");
+        set_device(c);
+        c->dim = dim;
+        const uint64_t N = std::max<uint64_t>(c->n, 1);
+        if (d_sums) {
+            c->sums = d_sums;
+            c->totals = d_totals;
+            c->own_acc = false;
+        } else {
+            c->sums = static_cast<float*>(c->sums_buf.ensure(N * dim * 4));
+            c->totals = static_cast<float*>(c->totals_buf.ensure(N * 4));
+            c->own_acc = true;
+        }
+        SS_CUDA(cudaMemsetAsync(c->sums, 0, N * dim * 4, c->stream));
+        SS_CUDA(cudaMemsetAsync(c->totals, 0, N * 4, c->stream));
+    });
+}
+
+int ss_encode_view(ss_ctx* c, const ss_camera* cam, const ss_view_masks* masks, int mode) {
+    return guarded([&] {
+        if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
+        set_device(c);
+        encode_one(c, *cam, masks, mode);
+    });
+}
+
+int ss_encode_views(ss_ctx* c, uint32_t nviews, const ss_camera* cams, const ss_view_masks* masks, int mode) {
+    return guarded([&] {
+        if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
+        set_device(c);
+        for (uint32_t v = 0; v < nviews; ++v) encode_one(c, cams[v], masks ? &masks[v] : nullptr, mode);
+    });
+}
+
+int ss_encode_finalize(ss_ctx* c, uint64_t row_lo, uint64_t row_hi, float* rows_out, float* coverage_out,
+                       int out_on_device) {
+    return guarded([&] {
+        if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
+        if (!c->sums) throw Error(SS_ERR_CONTRACT, "finalize before ss_encode_begin");
+        if (row_lo > row_hi || row_hi > c->n) throw Error(SS_ERR_CONTRACT, "finalize_into: rows do not fit the table");
+        set_device(c);
+        const uint64_t n = row_hi - row_lo;
+        if (n == 0) return;
+        cudaStream_t s = c->stream;
+        float* d_rows = rows_out;
+        float* d_cov = coverage_out;
+        if (!out_on_device) {
+            d_rows = static_cast<float*>(c->scores.ensure(n * c->dim * 4 + n * 4));
+            d_cov = d_rows + n * c->dim;
+        }
+        {
+            Scope sc(c, SS_K_NORMALIZE);
+            own_launch(c, launch_normalize(c->sums + row_lo * c->dim, c->totals + row_lo, n, c->dim, d_rows, d_cov, s),
+                       SS_K_NORMALIZE);
+            c->prof.bytes[SS_K_NORMALIZE] += (double)n * (8.0 * c->dim + 8.0);
+        }
+        if (!out_on_device) {
+            SS_CUDA(cudaMemcpyAsync(rows_out, d_rows, n * c->dim * 4, cudaMemcpyDeviceToHost, s));
+            SS_CUDA(cudaMemcpyAsync(coverage_out, d_cov, n * 4, cudaMemcpyDeviceToHost, s));
+            SS_CUDA(cudaStreamSynchronize(s));
+        }
+    });
+}
+
+int ss_normalize_device(ss_ctx* c, const float* d_sums, const float* d_totals, uint64_t n, uint32_t dim,
+                        float* d_rows_out, float* d_coverage_out) {
+    return guarded([&] {
+        if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
+        set_device(c);
+        Scope sc(c, SS_K_NORMALIZE);
+        own_launch(c, launch_normalize(d_sums, d_totals, n, dim, d_rows_out, d_coverage_out, c->stream),
+                   SS_K_NORMALIZE);
+        c->prof.bytes[SS_K_NORMALIZE] += (double)n * (8.0 * dim + 8.0);
+    });
+}
+
+// ------------------------------------------------------------------ store
+int ss_store_set(ss_ctx* c, const uint32_t* ids, const float* unit_rows, uint64_t count, uint32_t dim) {
+    return guarded([&] {
+        if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
+        set_device(c);
+        c->store_count = count;
+        c->store_dim = dim;
+        SS_CUDA(cudaMemcpy(c->store_ids.ensure(std::max<uint64_t>(count, 1) * 4), ids, count * 4,
+                           cudaMemcpyHostToDevice));
+        SS_CUDA(cudaMemcpy(c->store_rows.ensure(std::max<uint64_t>(count, 1) * dim * 4), unit_rows,
+                           count * dim * 4, cudaMemcpyHostToDevice));
+    });
+}
+
+int ss_store_build(ss_ctx* c, const float* rows, const float* coverage, uint64_t n, uint32_t dim,
+                   uint64_t* count_out) {
+    return guarded([&] {
+        if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
+        set_device(c);
+        cudaStream_t s = c->stream;
+        auto* d_in = static_cast<float*>(c->scores.ensure(std::max<uint64_t>(n, 1) * (dim + 1) * 4));
+        float* d_cov = d_in + n * dim;
+        SS_CUDA(cudaMemcpyAsync(d_in, rows, n * dim * 4, cudaMemcpyHostToDevice, s));
+        SS_CUDA(cudaMemcpyAsync(d_cov, coverage, n * 4, cudaMemcpyHostToDevice, s));
+        auto* flags = static_cast<uint8_t*>(c->sel_flags.ensure(std::max<uint64_t>(n, 1)));
+        auto* ids = static_cast<uint32_t*>(c->store_ids.ensure(std::max<uint64_t>(n, 1) * 4));
+        auto* num = static_cast<int*>(c->num_sel.ensure(16));
+        own_launch(c, launch_flag_covered(d_cov, n, flags, s), SS_K_QUERY);
+        size_t tb = 0;
+        cub::CountingInputIterator<uint32_t> it(0);
+        SS_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, it, flags, ids, num, (int)n, s));
+        void* tmp = c->cub_tmp.ensure(tb);
+        tb = c->cub_tmp.bytes;
+        SS_CUDA(cub::DeviceSelect::Flagged(tmp, tb, it, flags, ids, num, (int)n, s));
+        c->launches_cub += 1;
+        SS_CUDA(cudaMemcpyAsync(c->h_u32, num, 4, cudaMemcpyDeviceToHost, s));
+        SS_CUDA(cudaStreamSynchronize(s));
+        const uint64_t count = c->h_u32[0];
+        auto* out = static_cast<float*>(c->store_rows.ensure(std::max<uint64_t>(count, 1) * dim * 4));
+        auto* zf = static_cast<int*>(c->zero_flag.ensure(16));
+        SS_CUDA(cudaMemsetAsync(zf, 0, 4, s));
+        own_launch(c, launch_normalize_rows(d_in, ids, count, dim, out, zf, s), SS_K_QUERY);
+        SS_CUDA(cudaMemcpyAsync(c->h_u32, zf, 4, cudaMemcpyDeviceToHost, s));
+        SS_CUDA(cudaStreamSynchronize(s));
+        if (c->h_u32[0]) throw Error(SS_ERR_DATA, "build_store: a covered gaussian has a zero embedding row");
+        c->store_count = count;
+        c->store_dim = dim;
+        if (count_out) *count_out = count;
+    });
+}
+
+int ss_store_fetch(ss_ctx* c, uint32_t* ids, float* unit_rows) {
+    return guarded([&] {
+        set_device(c);
+        if (ids && c->store_count)
+            SS_CUDA(cudaMemcpy(ids, c->store_ids.p, c->store_count * 4, cudaMemcpyDeviceToHost));
+        if (unit_rows && c->store_count)
+            SS_CUDA(cudaMemcpy(unit_rows, c->store_rows.p, c->store_count * c->store_dim * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
+namespace {
+// vecstore.hpp:112-115 prepare_query for nq raw queries -> device unit queries
+float* prepare_queries(ss_ctx* c, const float* queries, uint32_t nq) {
+    cudaStream_t s = c->stream;
+    const uint32_t dim = c->store_dim;
+    auto* d_q = static_cast<float*>(c->qbuf.ensure(std::max<uint64_t>(nq, 1) * dim * 4));
+    auto* d_qn = static_cast<float*>(c->qnorm.ensure(std::max<uint64_t>(nq, 1) * dim * 4));
+    SS_CUDA(cudaMemcpyAsync(d_q, queries, (size_t)nq * dim * 4, cudaMemcpyHostToDevice, s));
+    auto* zf = static_cast<int*>(c->zero_flag.ensure(16));
+    SS_CUDA(cudaMemsetAsync(zf, 0, 4, s));
+    own_launch(c, launch_normalize_rows(d_q, nullptr, nq, dim, d_qn, zf, s), SS_K_QUERY);
+    SS_CUDA(cudaMemcpyAsync(c->h_u32, zf, 4, cudaMemcpyDeviceToHost, s));
+    SS_CUDA(cudaStreamSynchronize(s));
+    if (c->h_u32[0]) throw Error(SS_ERR_NUMERIC, "cannot normalize a zero vector");
+    return d_qn;
+}
+} // namespace
+
+int ss_query_topk(ss_ctx* c, const float* queries, uint32_t nq, uint32_t k, uint32_t* out_ids, float* out_sims,
+                  uint64_t* out_counts) {
+    return guarded([&] {
+        if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
+        set_device(c);
+        const uint64_t count = c->store_count;
+        const uint64_t take = std::min<uint64_t>(k, count);
+        for (uint32_t q = 0; q < nq; ++q) out_counts[q] = (k == 0 || count == 0) ? 0 : take;
+        if (k == 0 || count == 0 || nq == 0) return; // vecstore.hpp:122
+        if (k > 64) throw Error(SS_ERR_CONTRACT, "query_topk: k above 64 is not supported on the device path");
+        cudaStream_t s = c->stream;
+        Scope sc(c, SS_K_QUERY);
+        const float* d_qn = prepare_queries(c, queries, nq);
+        const uint32_t qt = (uint32_t)score_query_tile();
+        const uint32_t tile = std::max<uint32_t>(qt, 64);
+        auto* sc_buf = static_cast<float*>(c->scores.ensure((size_t)tile * count * 4));
+        auto* oid = static_cast<uint32_t*>(c->topk_ids.ensure((size_t)nq * k * 4));
+        auto* osim = static_cast<float*>(c->topk_sims.ensure((size_t)nq * k * 4));
+        for (uint32_t q0 = 0; q0 < nq; q0 += tile) {
+            const uint32_t nt = std::min(tile, nq - q0);
+            for (uint32_t t = 0; t < nt; t += qt)
+                own_launch(c, launch_score(c->store_rows.as<float>(), count, c->store_dim, d_qn, q0 + std::min(nt, t + qt),
+                                           q0 + t, sc_buf + (size_t)t * count, s),
+                           SS_K_QUERY);
+            own_launch(c, launch_topk(sc_buf, c->store_ids.as<uint32_t>(), count, k, nt, q0, oid, osim, s), SS_K_QUERY);
+        }
+        // rows written by topk are [q][k] with k stride; take <= k
+        std::vector<uint32_t> hid((size_t)nq * k);
+        std::vector<float> hsim((size_t)nq * k);
+        SS_CUDA(cudaMemcpyAsync(hid.data(), oid, hid.size() * 4, cudaMemcpyDeviceToHost, s));
+        SS_CUDA(cudaMemcpyAsync(hsim.data(), osim, hsim.size() * 4, cudaMemcpyDeviceToHost, s));
+        SS_CUDA(cudaStreamSynchronize(s));
+        std::memcpy(out_ids, hid.data(), hid.size() * 4);
+        std::memcpy(out_sims, hsim.data(), hsim.size() * 4);
+        c->prof.bytes[SS_K_QUERY] += 2.0 * nq * (double)count * c->store_dim; // flops
+    });
+}
+
+int ss_query_threshold(ss_ctx* c, const float* query, float tau, uint32_t* out_ids, float* out_sims,
+                       uint64_t capacity, uint64_t* out_count) {
+    return guarded([&] {
+        if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
+        if (!(tau >= -1.0f && tau <= 1.0f)) throw Error(SS_ERR_CONTRACT, "cosine threshold must lie in [-1, 1]");
+        set_device(c);
+        *out_count = 0;
+        const uint64_t count = c->store_count;
+        if (count == 0) return;
+        cudaStream_t s = c->stream;
+        const float* d_qn = prepare_queries(c, query, 1);
+        auto* sc_buf = static_cast<float*>(c->scores.ensure(count * 4));
+        own_launch(c, launch_score(c->store_rows.as<float>(), count, c->store_dim, d_qn, 1, 0, sc_buf, s), SS_K_QUERY);
+        auto* keys = static_cast<unsigned long long*>(c->thr_keys.ensure(count * 8));
+        auto* flags = static_cast<uint8_t*>(c->sel_flags.ensure(count));
+        own_launch(c, launch_threshold_keys(sc_buf, c->store_ids.as<uint32_t>(), count, tau, keys, flags, s), SS_K_QUERY);
+        auto* ksel = static_cast<unsigned long long*>(c->thr_ids.ensure(count * 8));
+        auto* ksorted = static_cast<unsigned long long*>(c->thr_keys_sorted.ensure(count * 8));
+        auto* num = static_cast<int*>(c->num_sel.ensure(16));
+        size_t tb = 0;
+        SS_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, keys, flags, ksel, num, (int)count, s));
+        size_t tb2 = 0;
+        SS_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb2, ksel, ksorted, (int)count, 0, 64, s));
+        void* tmp = c->cub_tmp.ensure(std::max(tb, tb2));
+        tb = c->cub_tmp.bytes;
+        SS_CUDA(cub::DeviceSelect::Flagged(tmp, tb, keys, flags, ksel, num, (int)count, s));
+        SS_CUDA(cudaMemcpyAsync(c->h_u32, num, 4, cudaMemcpyDeviceToHost, s));
+        SS_CUDA(cudaStreamSynchronize(s));
+        const uint64_t m = c->h_u32[0];
+        tb = c->cub_tmp.bytes;
+        SS_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, ksel, ksorted, (int)m, 0, 64, s));
+        c->launches_cub += 2;
+        std::vector<unsigned long long> hk(m);
+        SS_CUDA(cudaMemcpyAsync(hk.data(), ksorted, m * 8, cudaMemcpyDeviceToHost, s));
+        SS_CUDA(cudaStreamSynchronize(s));
+        const uint64_t out = std::min<uint64_t>(m, capacity);
+        for (uint64_t i = 0; i < out; ++i) {
+            out_ids[i] = (uint32_t)(hk[i] & 0xffffffffu);
+            uint32_t b = ~(uint32_t)(hk[i] >> 32);
+            b = (b & 0x80000000u) ? (b & 0x7fffffffu) : ~b;
+            float f;
+            std::memcpy(&f, &b, 4);
+            out_sims[i] = f;
+        }
+        *out_count = m;
+    });
+}
+
+// ---------------------------------------------------------- instrumentation
+int ss_profile_enable(ss_ctx* c, int on) {
+    return guarded([&] {
+        set_device(c);
+        if (!on) profile_drain(c);
+        c->prof.on = on != 0;
+    });
+}
+
+int ss_profile_reset(ss_ctx* c) {
+    return guarded([&] {
+        set_device(c);
+        profile_drain(c);
+        for (int i = 0; i < SS_K_COUNT; ++i) {
+            c->prof.ms[i] = 0;
+            c->prof.launches[i] = 0;
+            c->prof.bytes[i] = 0;
+        }
+        c->launches_own = c->launches_cub = 0;
+        c->cnt_vis = c->cnt_inst = c->cnt_views = 0;
+        SS_CUDA(cudaMemsetAsync(c->counters.p, 0, c->counters.bytes, c->stream));
+    });
+}
+
+int ss_profile_read(ss_ctx* c, double* ms, uint64_t* launches, double* bytes) {
+    return guarded([&] {
+        set_device(c);
+        profile_drain(c);
+        // fold the device-side G_v / K_v counters into raster + contract bytes
+        unsigned long long h[2];
+        SS_CUDA(cudaMemcpy(h, c->counters.p, 16, cudaMemcpyDeviceToHost));
+        const double gv = (double)h[0], kv = (double)h[1];
+        for (int i = 0; i < SS_K_COUNT; ++i) {
+            if (ms) ms[i] = c->prof.ms[i];
+            if (launches) launches[i] = c->prof.launches[i];
+            if (bytes) bytes[i] = c->prof.bytes[i];
+        }
+        if (bytes) {
+            const double D = c->dim ? c->dim : 512;
+            bytes[SS_K_RASTER] += 8.0 * kv;
+            bytes[SS_K_CONTRACT] += 8.0 * kv + gv * (8.0 * D + 8.0);
+        }
+    });
+}
+
+int ss_counters_read(ss_ctx* c, uint64_t* out5) {
+    return guarded([&] {
+        set_device(c);
+        SS_CUDA(cudaStreamSynchronize(c->stream));
+        unsigned long long h[2];
+        SS_CUDA(cudaMemcpy(h, c->counters.p, 16, cudaMemcpyDeviceToHost));
+        const uint64_t gv = h[0], kv = h[1];
+        out5[0] = c->cnt_vis;
+        out5[1] = c->cnt_inst;
+        out5[2] = gv;
+        out5[3] = kv;
+        out5[4] = c->cnt_views;
+    });
+}
+
+int ss_launch_count(ss_ctx* c, uint64_t* own, uint64_t* cub) {
+    if (own) *own = c->launches_own;
+    if (cub) *cub = c->launches_cub;
+    return 0;
+}
+
+} // extern "C"

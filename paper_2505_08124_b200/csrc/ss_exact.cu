@@ -1,0 +1,407 @@
+// Bit-exact fp64 kernels: projection and the tile compositor.
+//
+// Compiled with -fmad=false AND written with explicit __dmul_rn/__dadd_rn/
+// __ddiv_rn/__dsqrt_rn so no FMA contraction can creep in: the reference is
+// built for baseline x86-64 (no FMA, proj/CMakeLists.txt:11), and its bits
+// -- depth order, per-tile lists, per-pixel contributor lists and f32
+// weights -- must be reproduced exactly (BASELINE.json north_star).
+// Evaluation order: SURVEY.md Appendix A.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "glibc_exp.cuh"
+#include "ss_internal.cuh"
+
+namespace ss {
+namespace {
+
+__device__ __forceinline__ double dm(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double da(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double ds(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dd(double a, double b) { return __ddiv_rn(a, b); }
+
+// x86 cvttsd2si semantics (rasterizer.hpp:173-176): NaN / out of range -> INT_MIN
+__device__ __forceinline__ int32_t cvt_i32_x86(double v) {
+    if (!(v >= -2147483648.0 && v < 2147483648.0)) return INT32_MIN;
+    return (int32_t)v;
+}
+
+constexpr double kNearPlane = 0.01;        // projection.hpp:15
+constexpr double kCovDilation = 0.3;       // projection.hpp:17
+constexpr double kWeightCutoff = 1.0 / 255.0; // rasterizer.hpp:17
+constexpr double kAlphaMax = 0.99;         // rasterizer.hpp:19
+constexpr double kAlphaSkip = 1.0 / 255.0; // rasterizer.hpp:21
+constexpr double kTransmittanceFloor = 1e-4; // rasterizer.hpp:23
+constexpr double kMahalanobisSqCutoff = 9.0; // rasterizer.hpp:26
+
+// ---------------------------------------------------------------- project
+// One thread per Gaussian (id order).  scene.hpp:33-37 covariance3d +
+// projection.hpp:33-55 project_gaussian + rasterizer.hpp:66-71 conic_of +
+// the padded 3-sigma box and cull (rasterizer.hpp:160-179).  Survivors get
+// their depth bit pattern as sort key (positive f64 => monotone as u64).
+__global__ void __launch_bounds__(256) project_kernel(ProjectParams p) {
+    const uint64_t id = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool survive = false;
+    unsigned long long key = ~0ull;
+    if (id < p.n) {
+        const float4 mo = p.mean_op[id];
+        const ss_camera& cam = p.cam;
+        const double m0 = mo.x, m1 = mo.y, m2 = mo.z;
+        const double* Rc = cam.R;
+        double xc[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+            xc[i] = da(da(dm(Rc[3 * i], m0), da(dm(Rc[3 * i + 1], m1), dm(Rc[3 * i + 2], m2))), cam.t[i]);
+        if (p.dbg) p.dbg[id] = ss_projected{(uint32_t)id, 0u, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        if (xc[2] > kNearPlane) {
+            const double z = xc[2];
+            const double mu_x = da(dd(dm(cam.fx, xc[0]), z), cam.cx);
+            const double mu_y = da(dd(dm(cam.fy, xc[1]), z), cam.cy);
+
+            // quaternion normalize (Eigen 2-wide redux) + toRotationMatrix
+            const float4 q = p.quat[id];
+            double qx = q.x, qy = q.y, qz = q.z, qw = q.w;
+            const double n2 = da(da(dm(qx, qx), dm(qz, qz)), da(dm(qy, qy), dm(qw, qw)));
+            if (n2 > 0.0) {
+                const double nn = __dsqrt_rn(n2);
+                qx = dd(qx, nn);
+                qy = dd(qy, nn);
+                qz = dd(qz, nn);
+                qw = dd(qw, nn);
+            }
+            const double tx = dm(2.0, qx), ty = dm(2.0, qy), tz = dm(2.0, qz);
+            const double twx = dm(tx, qw), twy = dm(ty, qw), twz = dm(tz, qw);
+            const double txx = dm(tx, qx), txy = dm(ty, qx), txz = dm(tz, qx);
+            const double tyy = dm(ty, qy), tyz = dm(tz, qy), tzz = dm(tz, qz);
+            double R[9];
+            R[0] = ds(1.0, da(tyy, tzz));
+            R[1] = ds(txy, twz);
+            R[2] = da(txz, twy);
+            R[3] = da(txy, twz);
+            R[4] = ds(1.0, da(txx, tzz));
+            R[5] = ds(tyz, twx);
+            R[6] = ds(txz, twy);
+            R[7] = da(tyz, twx);
+            R[8] = ds(1.0, da(txx, tyy));
+            const float4 sc = p.scale[id];
+            const double s0 = sc.x, s1 = sc.y, s2c = sc.z;
+            const double s2[3] = {dm(s0, s0), dm(s1, s1), dm(s2c, s2c)};
+            double S[9];
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+#pragma unroll
+                for (int j = 0; j < 3; ++j)
+                    S[3 * i + j] = da(dm(dm(R[3 * i], s2[0]), R[3 * j]),
+                                      da(dm(dm(R[3 * i + 1], s2[1]), R[3 * j + 1]),
+                                         dm(dm(R[3 * i + 2], s2[2]), R[3 * j + 2])));
+            const double zz = dm(z, z);
+            const double J00 = dd(cam.fx, z), J02 = dd(dm(-cam.fx, xc[0]), zz);
+            const double J11 = dd(cam.fy, z), J12 = dd(dm(-cam.fy, xc[1]), zz);
+            double M[6];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                M[j] = da(da(dm(J00, Rc[j]), dm(0.0, Rc[3 + j])), dm(J02, Rc[6 + j]));
+                M[3 + j] = da(da(dm(0.0, Rc[j]), dm(J11, Rc[3 + j])), dm(J12, Rc[6 + j]));
+            }
+            double T[6];
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < 3; ++j)
+                    T[3 * i + j] = da(da(dm(M[3 * i], S[j]), dm(M[3 * i + 1], S[3 + j])), dm(M[3 * i + 2], S[6 + j]));
+            double C[4];
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < 2; ++j)
+                    C[2 * i + j] =
+                        da(da(dm(T[3 * i], M[3 * j]), dm(T[3 * i + 1], M[3 * j + 1])), dm(T[3 * i + 2], M[3 * j + 2]));
+            const double cxx = da(C[0], kCovDilation);
+            const double cxy = dm(0.5, da(C[1], C[2]));
+            const double cyy = da(C[3], kCovDilation);
+            if (p.dbg) p.dbg[id] = ss_projected{(uint32_t)id, 1u, mu_x, mu_y, cxx, cxy, cyy, z};
+
+            // conic_of
+            const double det = ds(dm(cxx, cyy), dm(cxy, cxy));
+            if (det < 1e-12) {
+                atomicAdd(&p.info->err_count, 1u);
+                atomicMin(&p.info->err_gid, (unsigned int)id);
+            } else {
+                SplatRec r;
+                r.mu_x = mu_x;
+                r.mu_y = mu_y;
+                r.a = dd(cyy, det);
+                r.b2 = dm(2.0, dd(-cxy, det));
+                r.c = dd(cxx, det);
+                r.opacity = mo.w;
+                r.gid = (uint32_t)id;
+                const double rx = da(dm(3.0, __dsqrt_rn(cxx)), 1.0);
+                const double ry = da(dm(3.0, __dsqrt_rn(cyy)), 1.0);
+                const int32_t W = (int32_t)cam.width, H = (int32_t)cam.height;
+                int32_t v;
+                v = cvt_i32_x86(ceil(ds(mu_x, rx)));
+                const int32_t x0 = v > 0 ? v : 0;
+                v = cvt_i32_x86(floor(da(mu_x, rx)));
+                const int32_t x1 = v < W - 1 ? v : W - 1;
+                v = cvt_i32_x86(ceil(ds(mu_y, ry)));
+                const int32_t y0 = v > 0 ? v : 0;
+                v = cvt_i32_x86(floor(da(mu_y, ry)));
+                const int32_t y1 = v < H - 1 ? v : H - 1;
+                if (!(x0 > x1 || y0 > y1)) {
+                    r.x0 = (uint16_t)x0;
+                    r.x1 = (uint16_t)x1;
+                    r.y0 = (uint16_t)y0;
+                    r.y1 = (uint16_t)y1;
+                    r.pad0 = r.pad1 = 0;
+                    p.rec[id] = r;
+                    survive = true;
+                    key = (unsigned long long)__double_as_longlong(z);
+                }
+            }
+        }
+        p.keys[id] = key;
+        p.flags[id] = survive ? 1 : 0;
+    }
+    // block-reduce survivors' count and key range, one atomic per block
+    const unsigned long long kmin = survive ? key : ~0ull;
+    const unsigned long long kmax = survive ? key : 0ull;
+    __shared__ unsigned long long s_min[8], s_max[8];
+    __shared__ unsigned int s_cnt[8];
+    unsigned long long wmin = kmin, wmax = kmax;
+    unsigned int wcnt = __popc(__ballot_sync(0xffffffffu, survive));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long a = __shfl_xor_sync(0xffffffffu, wmin, o);
+        const unsigned long long b = __shfl_xor_sync(0xffffffffu, wmax, o);
+        wmin = a < wmin ? a : wmin;
+        wmax = b > wmax ? b : wmax;
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        s_min[warp] = wmin;
+        s_max[warp] = wmax;
+        s_cnt[warp] = wcnt;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long bmin = ~0ull, bmax = 0;
+        unsigned int bcnt = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            bmin = s_min[w] < bmin ? s_min[w] : bmin;
+            bmax = s_max[w] > bmax ? s_max[w] : bmax;
+            bcnt += s_cnt[w];
+        }
+        if (bcnt) {
+            atomicAdd(&p.info->n_surv, (unsigned long long)bcnt);
+            atomicMin(&p.info->min_key, bmin);
+            atomicMax(&p.info->max_key, bmax);
+        }
+    }
+}
+
+// ------------------------------------------------------------- compositor
+// One CTA per 16x16 tile, one thread per pixel; the tile's depth-ordered
+// splat list is staged through shared memory 256 records at a time and every
+// thread composites its own pixel front to back (rasterizer.hpp:112-133,
+// 213-247), with the reference's box test first, Mahalanobis cutoff, alpha
+// clamp, skip rule, weight cutoff and transmittance floor.
+//
+// KIND 0: count contributions per pixel (sizes the capture).
+// KIND 1: capture -- write WeightEntry records at per-pixel offsets, in rank
+//         order (= the reference's stable_sort by pixel), per_pixel_total and
+//         alpha = 1 - T_final.
+// KIND 2: fused -- gate each contribution by the pixel's mask bitset and add
+//         w into per-(rank, mask) fp32 scalars; lanes with identical bitsets
+//         are summed with a fixed-order butterfly first, so each (splat,
+//         warp, bitset group) costs one atomic per mask, never a 512-d scatter.
+template <int KIND, bool FALLOFF, int MW>
+__global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) {
+    __shared__ SplatRec srec[kRasterThreads];
+    __shared__ unsigned long long stab[256];
+    stab[threadIdx.x] = kExpTab[threadIdx.x];
+
+    const uint32_t tile = blockIdx.x;
+    const uint32_t tx = tile % p.tiles_x, ty = tile / p.tiles_x;
+    const uint32_t px = tx * kTile + (threadIdx.x & 15u);
+    const uint32_t py = ty * kTile + (threadIdx.x >> 4);
+    const bool inside = px < p.width && py < p.height;
+    const uint32_t pixel = py * p.width + px;
+    const uint32_t start = p.tile_start[tile], end = p.tile_end[tile];
+    const double dpx = (double)(int32_t)px, dpy = (double)(int32_t)py;
+
+    double T = 1.0;
+    double total = 0.0;
+    uint32_t count = 0;
+    uint32_t out = 0;
+    bool done = !inside;
+    if constexpr (KIND == 1) {
+        if (inside) out = p.pix_offset[pixel];
+    }
+    // fused-mode per-pixel mask bitset and lane grouping by identical bitset
+    uint32_t bits[MW > 0 ? MW : 1];
+    uint32_t grp = 0;
+    bool any_bits = false;
+    const int lane = threadIdx.x & 31;
+    if constexpr (KIND == 2) {
+#pragma unroll
+        for (int w = 0; w < MW; ++w) {
+            bits[w] = inside ? p.pix_bits[(size_t)pixel * MW + w] : 0u;
+            any_bits |= bits[w] != 0;
+        }
+        if constexpr (MW == 1) {
+            grp = __match_any_sync(0xffffffffu, bits[0]);
+        } else if constexpr (MW == 2) {
+            grp = __match_any_sync(0xffffffffu, ((unsigned long long)bits[1] << 32) | bits[0]);
+        } else {
+            grp = __match_any_sync(0xffffffffu, ((unsigned long long)bits[1] << 32) | bits[0]) &
+                  __match_any_sync(0xffffffffu, ((unsigned long long)bits[3] << 32) | bits[2]);
+        }
+        done = done || !any_bits; // unmasked pixels contribute nothing
+    }
+    __syncthreads();
+
+    for (uint32_t base = start; base < end; base += kRasterThreads) {
+        if (__syncthreads_and(done)) break;
+        const uint32_t i = base + threadIdx.x;
+        if (i < end) {
+            const uint4* src = reinterpret_cast<const uint4*>(p.rec_sorted + p.tile_ranks[i]);
+            uint4* dst = reinterpret_cast<uint4*>(srec + threadIdx.x);
+            dst[0] = __ldg(src);
+            dst[1] = __ldg(src + 1);
+            dst[2] = __ldg(src + 2);
+            dst[3] = __ldg(src + 3);
+        }
+        __syncthreads();
+        const uint32_t nb = min((uint32_t)kRasterThreads, end - base);
+        for (uint32_t j = 0; j < nb; ++j) {
+            bool contrib = false;
+            float wf = 0.0f;
+            if (!done) {
+                const SplatRec& s = srec[j];
+                if (px >= s.x0 && px <= s.x1 && py >= s.y0 && py <= s.y1) {
+                    const double dx = ds(dpx, s.mu_x), dy = ds(dpy, s.mu_y);
+                    const double d2 = da(da(dm(dm(s.a, dx), dx), dm(dm(s.b2, dx), dy)), dm(dm(s.c, dy), dy));
+                    if (!(d2 > kMahalanobisSqCutoff)) {
+                        const double g = glibc_exp(dm(-0.5, d2), stab);
+                        if constexpr (FALLOFF) {
+                            if (g >= kWeightCutoff) {
+                                contrib = true;
+                                wf = __double2float_rn(g);
+                            }
+                        } else {
+                            const double og = dm((double)s.opacity, g);
+                            const double alpha = og < kAlphaMax ? og : kAlphaMax;
+                            if (!(alpha < kAlphaSkip)) {
+                                const double w = dm(alpha, T);
+                                if (w >= kWeightCutoff) {
+                                    contrib = true;
+                                    wf = __double2float_rn(w);
+                                }
+                                T = dm(T, ds(1.0, alpha));
+                                if (T < kTransmittanceFloor) done = true;
+                            }
+                        }
+                    }
+                }
+            }
+            if constexpr (KIND == 0) {
+                count += contrib ? 1u : 0u;
+            } else if constexpr (KIND == 1) {
+                if (contrib) {
+                    p.entries[out++] = ss_weight_entry{srec[j].gid, pixel, wf};
+                    total = da(total, (double)wf);
+                }
+            } else {
+                const uint32_t em = __ballot_sync(0xffffffffu, contrib);
+                if (em) {
+                    const uint32_t rank = p.tile_ranks[base + j];
+                    uint32_t rem = em;
+                    while (rem) {
+                        const int leader = __ffs(rem) - 1;
+                        const uint32_t gm = __shfl_sync(0xffffffffu, grp, leader);
+                        float v = (contrib && ((gm >> lane) & 1u)) ? wf : 0.0f;
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                        if (lane == leader) {
+                            float* row = p.acc + (size_t)rank * p.n_masks;
+#pragma unroll
+                            for (int w = 0; w < MW; ++w) {
+                                uint32_t b = bits[w];
+                                while (b) {
+                                    const int m = __ffs(b) - 1;
+                                    b &= b - 1;
+                                    atomicAdd(row + w * 32 + m, v);
+                                }
+                            }
+                        }
+                        rem &= ~gm;
+                    }
+                    if (lane == __ffs(em) - 1) {
+                        // first toucher of this rank appends it to the contraction list
+                        if (*reinterpret_cast<volatile uint32_t*>(p.touched + rank) == 0u &&
+                            atomicExch(p.touched + rank, 1u) == 0u) {
+                            const unsigned long long slot = atomicAdd(&p.info->n_touched, 1ull);
+                            p.touched_list[slot] = rank;
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if constexpr (KIND == 0) {
+        if (inside) p.pix_count[pixel] = count;
+    } else if constexpr (KIND == 1) {
+        if (inside) {
+            p.per_pixel_total[pixel] = __double2float_rn(total);
+            p.alpha[pixel] = __double2float_rn(ds(1.0, T));
+        }
+    }
+}
+
+template <int KIND>
+cudaError_t launch_raster(const RasterParams& p, int mode, uint32_t tiles, cudaStream_t s) {
+    if (tiles == 0) return cudaSuccess;
+    if (mode == SS_FALLOFF_ONLY)
+        raster_kernel<KIND, true, 1><<<tiles, kRasterThreads, 0, s>>>(p);
+    else
+        raster_kernel<KIND, false, 1><<<tiles, kRasterThreads, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+} // namespace
+
+cudaError_t launch_project(const ProjectParams& p, cudaStream_t s) {
+    if (p.n == 0) return cudaSuccess;
+    const unsigned blocks = (unsigned)((p.n + 255) / 256);
+    project_kernel<<<blocks, 256, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_raster_count(const RasterParams& p, int mode, uint32_t tiles, cudaStream_t s) {
+    return launch_raster<0>(p, mode, tiles, s);
+}
+cudaError_t launch_raster_capture(const RasterParams& p, int mode, uint32_t tiles, cudaStream_t s) {
+    return launch_raster<1>(p, mode, tiles, s);
+}
+
+cudaError_t launch_raster_fused(const RasterParams& p, int mode, uint32_t tiles, cudaStream_t s) {
+    if (tiles == 0) return cudaSuccess;
+    const bool fo = mode == SS_FALLOFF_ONLY;
+#define SS_FUSED(MWV)                                                                       \
+    do {                                                                                    \
+        if (fo) raster_kernel<2, true, MWV><<<tiles, kRasterThreads, 0, s>>>(p);           \
+        else raster_kernel<2, false, MWV><<<tiles, kRasterThreads, 0, s>>>(p);             \
+    } while (0)
+    switch (p.mask_words) {
+    case 1: SS_FUSED(1); break;
+    case 2: SS_FUSED(2); break;
+    case 3:
+    case 4: SS_FUSED(4); break;
+    default: return cudaErrorInvalidValue;
+    }
+#undef SS_FUSED
+    return cudaGetLastError();
+}
+
+} // namespace ss

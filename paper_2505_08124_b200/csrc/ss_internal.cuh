@@ -1,0 +1,80 @@
+// Internal declarations shared by the libsemsplat_b200 translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/semsplat_b200.h"
+
+namespace ss {
+
+constexpr uint32_t kTile = 16;          // rasterizer.hpp:30 kTileSize
+constexpr int kRasterThreads = 256;     // one thread per pixel of a 16x16 tile
+constexpr int kMaxMaskWords = 4;        // up to 128 masks per view
+
+// Per-splat record staged through shared memory by the compositor.  64 B so a
+// batch of 256 is 16 KB and every record is one aligned 64 B segment.
+// Fields are the reference's SplatRecord (rasterizer.hpp:99-106) minus color.
+struct __align__(16) SplatRec {
+    double mu_x, mu_y; // rasterizer.hpp:101
+    double a, b2, c;   // conic (rasterizer.hpp:66-71); b2 = 2*b (exact)
+    float opacity;     // widened to f64 at use, as SplatRecord::opacity
+    uint32_t gid;
+    uint16_t x0, x1, y0, y1; // inclusive padded 3-sigma box (rasterizer.hpp:171-176)
+    uint32_t pad0, pad1;
+};
+static_assert(sizeof(SplatRec) == 64, "SplatRec must stay 64 B");
+
+// Per-view scalar results the host reads back (one small D2H per view).
+struct ViewInfo {
+    unsigned long long n_surv;       // visible, box-non-empty splats
+    unsigned long long min_key;      // min / max depth bit patterns over them
+    unsigned long long max_key;
+    unsigned long long n_instances;  // tile instances I_v
+    unsigned int err_count;          // singular screen covariances
+    unsigned int err_gid;            // smallest gid with one
+    unsigned long long n_touched;    // G_v (ranks with any masked weight)
+    unsigned long long n_pairs;      // K_v (nonzero (rank, mask) scalars)
+};
+
+struct ProjectParams {
+    const float4* mean_op; // x, y, z, opacity
+    const float4* scale;   // sx, sy, sz, -
+    const float4* quat;    // x, y, z, w (Eigen coeffs order)
+    uint64_t n;
+    ss_camera cam;
+    SplatRec* rec;        // [n] by gid
+    unsigned long long* keys; // [n] depth bits
+    uint8_t* flags;       // [n] survive
+    ViewInfo* info;
+    ss_projected* dbg;    // optional Projected2D dump (parity entry point)
+};
+
+struct RasterParams {
+    const SplatRec* rec_sorted; // by rank
+    const uint32_t* tile_ranks; // per tile instance, rank
+    const uint32_t* tile_start;
+    const uint32_t* tile_end;
+    uint32_t width, height, tiles_x;
+    // capture mode
+    uint32_t* pix_count;           // pass 0 output [P]
+    const uint32_t* pix_offset;    // pass 1 input  [P]
+    ss_weight_entry* entries;      // pass 1 output
+    float* per_pixel_total;        // pass 1 output [P]
+    float* alpha;                  // pass 1 output [P]
+    // fused mode
+    const uint32_t* pix_bits;      // [P * mask_words]
+    uint32_t mask_words, n_masks;
+    float* acc;                    // [n_surv * n_masks] per-(rank, mask) scalars
+    uint32_t* touched;             // [n_surv] 0/1
+    uint32_t* touched_list;        // [n_surv]
+    ViewInfo* info;
+};
+
+// Kernel launchers (return cudaError_t of the launch).
+cudaError_t launch_project(const ProjectParams& p, cudaStream_t s);
+cudaError_t launch_raster_count(const RasterParams& p, int mode, uint32_t tiles, cudaStream_t s);
+cudaError_t launch_raster_capture(const RasterParams& p, int mode, uint32_t tiles, cudaStream_t s);
+cudaError_t launch_raster_fused(const RasterParams& p, int mode, uint32_t tiles, cudaStream_t s);
+
+} // namespace ss

@@ -1,0 +1,455 @@
+// Integer / fp32 kernels of the embedding pass and the vector query:
+// mask decode, tile binning helpers, the sparse 512-d contraction,
+// normalisation, store build and exact cosine scoring / top-k.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cub/block/block_scan.cuh>
+
+#include "ss_kernels.cuh"
+
+namespace ss {
+namespace {
+
+// ------------------------------------------------------------ mask decode
+// providers.hpp:95-109 rle_decode (alternating runs, zeros first) straight
+// into a per-pixel mask bitset: one CTA per mask, a block scan turns run
+// lengths into start positions 256 runs at a time, each "ones" run sets bit m
+// of its pixels' bitset words.
+__global__ void __launch_bounds__(256) rle_to_bits_kernel(const uint32_t* runs, const uint64_t* run_offsets,
+                                                          uint32_t words, uint32_t* bits) {
+    using Scan = cub::BlockScan<unsigned long long, 256>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ unsigned long long carry;
+    const uint32_t m = blockIdx.x;
+    const uint64_t r0 = run_offsets[m], r1 = run_offsets[m + 1];
+    const uint32_t word = m >> 5, bit = 1u << (m & 31u);
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (uint64_t base = r0; base < r1; base += 256) {
+        const uint64_t k = base + threadIdx.x;
+        const unsigned long long len = k < r1 ? runs[k] : 0ull;
+        unsigned long long pos, agg;
+        Scan(tmp).ExclusiveSum(len, pos, agg);
+        pos += carry;
+        if (k < r1 && ((k - r0) & 1ull)) {
+            for (unsigned long long p = pos; p < pos + len; ++p) atomicOr(bits + p * words + word, bit);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) carry += agg;
+        __syncthreads();
+    }
+}
+
+// providers.hpp:359-373 resample_mask (nearest neighbour, u64 index math)
+__global__ void resample_bits_kernel(const uint32_t* src, uint32_t sw, uint32_t sh, uint32_t* dst, uint32_t tw,
+                                     uint32_t th, uint32_t words) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (uint64_t)tw * th) return;
+    const uint32_t x = (uint32_t)(i % tw), y = (uint32_t)(i / tw);
+    uint32_t sy = (uint32_t)((2ull * y + 1) * sh / (2ull * th));
+    uint32_t sx = (uint32_t)((2ull * x + 1) * sw / (2ull * tw));
+    sy = sy < sh - 1 ? sy : sh - 1;
+    sx = sx < sw - 1 ? sx : sw - 1;
+    const uint32_t* s = src + ((uint64_t)sy * sw + sx) * words;
+    for (uint32_t w = 0; w < words; ++w) dst[i * words + w] = s[w];
+}
+
+// ------------------------------------------------------------- binning
+// rank-order gather of splat records + tiles covered per splat
+// (rasterizer.hpp:185-194 walks the same boxes)
+__global__ void gather_kernel(const uint32_t* order, uint64_t n, const SplatRec* rec, SplatRec* rec_sorted,
+                              uint32_t* ntiles) {
+    const uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const uint4* src = reinterpret_cast<const uint4*>(rec + order[r]);
+    uint4* dst = reinterpret_cast<uint4*>(rec_sorted + r);
+    const uint4 a = src[0], b = src[1], c = src[2], d = src[3];
+    dst[0] = a;
+    dst[1] = b;
+    dst[2] = c;
+    dst[3] = d;
+    // box fields share the 4th 16-byte word: .x = x0 | x1 << 16, .y = y0 | y1 << 16
+    const uint32_t x0 = d.x & 0xffffu, x1 = d.x >> 16, y0 = d.y & 0xffffu, y1 = d.y >> 16;
+    ntiles[r] = (x1 / kTile - x0 / kTile + 1) * (y1 / kTile - y0 / kTile + 1);
+}
+
+__global__ void emit_keys_kernel(const SplatRec* rec_sorted, const uint32_t* offsets, uint64_t n, uint32_t tiles_x,
+                                 uint32_t* keys, uint32_t* vals) {
+    const uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const SplatRec& s = rec_sorted[r];
+    uint32_t o = offsets[r];
+    for (uint32_t ty = s.y0 / kTile; ty <= (uint32_t)s.y1 / kTile; ++ty)
+        for (uint32_t tx = s.x0 / kTile; tx <= (uint32_t)s.x1 / kTile; ++tx) {
+            keys[o] = ty * tiles_x + tx;
+            vals[o] = (uint32_t)r;
+            ++o;
+        }
+}
+
+__global__ void tile_ranges_kernel(const uint32_t* keys, uint64_t n, uint32_t* start, uint32_t* end) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t k = keys[i];
+    if (i == 0 || keys[i - 1] != k) start[k] = (uint32_t)i;
+    if (i == n - 1 || keys[i + 1] != k) end[k] = (uint32_t)(i + 1);
+}
+
+// --------------------------------------------------------- contraction
+// pipeline.hpp:70-80 accumulate, per view: for every rank the compositor
+// touched, row[gid] += sum_m acc[rank, m] * CLIP_m and total[gid] +=
+// sum_m acc[rank, m]; then the scalars are cleared for the next view.  One
+// warp per touched Gaussian; the 2 KB fp32 row moves as four coalesced
+// float4 sweeps; CLIP rows stay L1/L2-resident (M x 2 KB per view).
+template <bool DIM512>
+__global__ void __launch_bounds__(256) contract_kernel(ContractParams p) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const unsigned long long n_touched = p.info->n_touched;
+    unsigned long long pairs = 0;
+    for (uint64_t t = warp0; t < n_touched; t += nwarps) {
+        const uint32_t r = p.touched_list[t];
+        const uint32_t gid = p.order[r];
+        float* accrow = p.acc + (size_t)r * p.n_masks;
+        float* row = p.sums + (size_t)gid * p.dim;
+        float4 racc[4];
+        if constexpr (DIM512) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) racc[q] = reinterpret_cast<const float4*>(row)[lane + 32 * q];
+        }
+        float wsum = 0.0f;
+        for (uint32_t c = 0; c < p.n_masks; c += 32) {
+            const uint32_t mi = c + lane;
+            float v = 0.0f;
+            if (mi < p.n_masks) {
+                v = accrow[mi];
+                if (v != 0.0f) accrow[mi] = 0.0f;
+            }
+            wsum += v;
+            uint32_t bal = __ballot_sync(0xffffffffu, v != 0.0f);
+            pairs += __popc(bal);
+            while (bal) {
+                const int src = __ffs(bal) - 1;
+                bal &= bal - 1;
+                const float w = __shfl_sync(0xffffffffu, v, src);
+                const float* e = p.clip + (size_t)(c + src) * p.dim;
+                if constexpr (DIM512) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const float4 ev = __ldg(reinterpret_cast<const float4*>(e) + lane + 32 * q);
+                        racc[q].x += w * ev.x;
+                        racc[q].y += w * ev.y;
+                        racc[q].z += w * ev.z;
+                        racc[q].w += w * ev.w;
+                    }
+                } else {
+                    for (uint32_t d = lane; d < p.dim; d += 32) row[d] += w * __ldg(e + d);
+                }
+            }
+        }
+        if constexpr (DIM512) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) reinterpret_cast<float4*>(row)[lane + 32 * q] = racc[q];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+        if (lane == 0) {
+            p.totals[gid] += wsum;
+            p.touched[r] = 0u;
+        }
+    }
+    if (p.count_pairs) {
+        // pairs is warp-uniform (ballot popcounts); count once per warp
+        if (lane == 0 && pairs) atomicAdd(p.cum + 1, pairs);
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(p.cum, n_touched);
+    }
+}
+
+// pipeline.hpp:120-135 finalize_into: covered rows (total > 1e-8) become
+// sum/total, coverage = total; uncovered rows are exactly zero.
+__global__ void __launch_bounds__(256) normalize_kernel(const float* sums, const float* totals, uint64_t n,
+                                                        uint32_t dim, float* rows, float* coverage) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const bool vec = (dim & 3u) == 0;
+    for (uint64_t k = warp0; k < n; k += nwarps) {
+        const float t = totals[k];
+        const bool cov = (double)t > 1e-8;
+        const double inv = cov ? 1.0 / (double)t : 0.0;
+        const float* s = sums + k * dim;
+        float* o = rows + k * dim;
+        if (vec) {
+            for (uint32_t d = lane * 4; d < dim; d += 128) {
+                float4 v = *reinterpret_cast<const float4*>(s + d);
+                if (cov) {
+                    v.x = __double2float_rn((double)v.x * inv);
+                    v.y = __double2float_rn((double)v.y * inv);
+                    v.z = __double2float_rn((double)v.z * inv);
+                    v.w = __double2float_rn((double)v.w * inv);
+                } else {
+                    v = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+                *reinterpret_cast<float4*>(o + d) = v;
+            }
+        } else {
+            for (uint32_t d = lane; d < dim; d += 32) o[d] = cov ? __double2float_rn((double)s[d] * inv) : 0.0f;
+        }
+        if (lane == 0) coverage[k] = cov ? t : 0.0f;
+    }
+}
+
+// ---------------------------------------------------------------- query
+// vecstore.hpp:34-42 normalized_copy, one warp per row: the f64 square sum is
+// accumulated strictly sequentially (lane 0 walks the row staged in
+// registers via shuffles) so the unit rows are bit-identical.
+__global__ void __launch_bounds__(256) normalize_rows_kernel(const float* in, const uint32_t* select, uint64_t n,
+                                                             uint32_t dim, float* out, int* zero_flag) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t k = warp0; k < n; k += nwarps) {
+        const uint64_t src = select ? select[k] : k;
+        const float* v = in + src * dim;
+        double ns = 0.0;
+        for (uint32_t c = 0; c < dim; c += 32) {
+            const float x = (c + lane < dim) ? v[c + lane] : 0.0f;
+            const double sq = (double)x * (double)x; // exact
+            const uint32_t cnt = min(32u, dim - c);
+            for (uint32_t j = 0; j < cnt; ++j) ns = __dadd_rn(ns, __shfl_sync(0xffffffffu, sq, j));
+        }
+        if (!(ns > 0.0)) {
+            if (lane == 0) atomicExch(zero_flag, 1);
+            continue;
+        }
+        const double inv = __ddiv_rn(1.0, __dsqrt_rn(ns));
+        for (uint32_t d = lane; d < dim; d += 32) out[k * dim + d] = __double2float_rn(__dmul_rn((double)v[d], inv));
+    }
+}
+
+// vecstore.hpp:21-31 dot_lanes, exactly: eight fp32 lanes accumulated in
+// index order with separate rounded multiply and add (no FMA), pairwise
+// combine, then the tail.  One thread per store row, QT queries per block
+// held in shared memory, so each row is read once per query tile.
+template <int QT>
+__global__ void __launch_bounds__(256) score_kernel(const float* rows, uint64_t count, uint32_t dim,
+                                                    const float* queries, uint32_t nq, uint32_t q0, float* scores) {
+    extern __shared__ float sq[]; // QT x dim
+    const uint32_t qn = min((uint32_t)QT, nq - q0);
+    for (uint32_t i = threadIdx.x; i < QT * dim; i += blockDim.x) {
+        const uint32_t qi = i / dim;
+        sq[i] = qi < qn ? queries[(size_t)(q0 + qi) * dim + (i % dim)] : 0.0f;
+    }
+    __syncthreads();
+    const uint32_t d8 = dim & ~7u;
+    for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < count; r += (uint64_t)gridDim.x * blockDim.x) {
+        const float* a = rows + r * dim;
+        float lanes[QT][8];
+#pragma unroll
+        for (int q = 0; q < QT; ++q)
+#pragma unroll
+            for (int l = 0; l < 8; ++l) lanes[q][l] = 0.0f;
+        for (uint32_t i = 0; i < d8; i += 8) {
+            float av[8];
+            if ((dim & 3u) == 0) {
+                const float4 x = __ldg(reinterpret_cast<const float4*>(a + i));
+                const float4 y = __ldg(reinterpret_cast<const float4*>(a + i + 4));
+                av[0] = x.x; av[1] = x.y; av[2] = x.z; av[3] = x.w;
+                av[4] = y.x; av[5] = y.y; av[6] = y.z; av[7] = y.w;
+            } else {
+#pragma unroll
+                for (int l = 0; l < 8; ++l) av[l] = __ldg(a + i + l);
+            }
+#pragma unroll
+            for (int q = 0; q < QT; ++q)
+#pragma unroll
+                for (int l = 0; l < 8; ++l) lanes[q][l] = __fadd_rn(lanes[q][l], __fmul_rn(av[l], sq[q * dim + i + l]));
+        }
+#pragma unroll
+        for (int q = 0; q < QT; ++q) {
+            if ((uint32_t)q >= qn) break;
+            float tail = 0.0f;
+            for (uint32_t i = d8; i < dim; ++i) tail = __fadd_rn(tail, __fmul_rn(__ldg(a + i), sq[q * dim + i]));
+            const float s01 = __fadd_rn(lanes[q][0], lanes[q][1]), s23 = __fadd_rn(lanes[q][2], lanes[q][3]);
+            const float s45 = __fadd_rn(lanes[q][4], lanes[q][5]), s67 = __fadd_rn(lanes[q][6], lanes[q][7]);
+            scores[(size_t)q * count + r] = __fadd_rn(__fadd_rn(__fadd_rn(s01, s23), __fadd_rn(s45, s67)), tail);
+        }
+    }
+}
+
+__device__ __forceinline__ bool scored_before(float sa, uint32_t ia, float sb, uint32_t ib) {
+    // vecstore.hpp:107-110
+    if (sa != sb) return sa > sb;
+    return ia < ib;
+}
+
+// Per-query exact top-k over a score row: each thread keeps a sorted local
+// list of the best k it has seen, then the block merges the 256 lists in
+// shared memory.  k <= kMaxK.
+constexpr int kMaxK = 64;
+__global__ void __launch_bounds__(256) topk_kernel(const float* scores, const uint32_t* ids, uint64_t count,
+                                                   uint32_t k, uint32_t q0, uint32_t* out_ids, float* out_sims) {
+    const uint32_t qi = blockIdx.x;
+    const float* s = scores + (size_t)qi * count;
+    float bs[kMaxK];
+    uint32_t bi[kMaxK];
+    uint32_t have = 0;
+    const uint32_t take = (uint32_t)min((uint64_t)k, count);
+    for (uint64_t r = threadIdx.x; r < count; r += blockDim.x) {
+        const float v = s[r];
+        const uint32_t id = ids[r];
+        if (have == take && !scored_before(v, id, bs[take - 1], bi[take - 1])) continue;
+        uint32_t pos = have < take ? have : take - 1;
+        while (pos > 0 && scored_before(v, id, bs[pos - 1], bi[pos - 1])) {
+            bs[pos] = bs[pos - 1];
+            bi[pos] = bi[pos - 1];
+            --pos;
+        }
+        bs[pos] = v;
+        bi[pos] = id;
+        if (have < take) ++have;
+    }
+    // block merge: repeatedly extract the best head among the threads
+    __shared__ float hs[256];
+    __shared__ uint32_t hi[256];
+    __shared__ int hwin;
+    uint32_t head = 0;
+    for (uint32_t outk = 0; outk < take; ++outk) {
+        hs[threadIdx.x] = head < have ? bs[head] : -INFINITY;
+        hi[threadIdx.x] = head < have ? bi[head] : 0xffffffffu;
+        const bool valid = head < have;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int best = -1;
+            for (int t = 0; t < (int)blockDim.x; ++t) {
+                const bool tv = hi[t] != 0xffffffffu || hs[t] != -INFINITY;
+                if (!tv) continue;
+                if (best < 0 || scored_before(hs[t], hi[t], hs[best], hi[best])) best = t;
+            }
+            hwin = best;
+            if (best >= 0) {
+                out_ids[(size_t)(q0 + qi) * k + outk] = hi[best];
+                out_sims[(size_t)(q0 + qi) * k + outk] = hs[best];
+            }
+        }
+        __syncthreads();
+        if ((int)threadIdx.x == hwin && valid) ++head;
+        __syncthreads();
+    }
+}
+
+__global__ void flag_covered_kernel(const float* coverage, uint64_t n, uint8_t* flags) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) flags[i] = coverage[i] > 1e-8f ? 1 : 0; // EmbeddingTable::covered, pipeline.hpp:115
+}
+
+// (sim desc, id asc) as one ascending u64 radix key
+__global__ void threshold_keys_kernel(const float* scores, const uint32_t* ids, uint64_t count, float tau,
+                                      unsigned long long* keys, uint8_t* flags) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const float v = scores[i];
+    flags[i] = v >= tau ? 1 : 0;
+    uint32_t b = __float_as_uint(v);
+    b = (b & 0x80000000u) ? ~b : (b | 0x80000000u); // ascending-orderable
+    b = ~b;                                          // descending
+    keys[i] = ((unsigned long long)b << 32) | ids[i];
+}
+
+} // namespace
+
+// ---------------------------------------------------------------- launchers
+static inline unsigned blocks_for(uint64_t n, unsigned t) { return (unsigned)((n + t - 1) / t); }
+static inline unsigned warp_grid(uint64_t n) {
+    const uint64_t b = (n + 7) / 8; // 8 warps per 256-thread block
+    return (unsigned)(b < 148ull * 16 ? (b ? b : 1) : 148ull * 16);
+}
+
+cudaError_t launch_rle_to_bits(const uint32_t* runs, const uint64_t* run_offsets, uint32_t n_masks, uint32_t words,
+                               uint32_t* bits, cudaStream_t s) {
+    if (n_masks == 0) return cudaSuccess;
+    rle_to_bits_kernel<<<n_masks, 256, 0, s>>>(runs, run_offsets, words, bits);
+    return cudaGetLastError();
+}
+cudaError_t launch_resample_bits(const uint32_t* src, uint32_t sw, uint32_t sh, uint32_t* dst, uint32_t tw,
+                                 uint32_t th, uint32_t words, cudaStream_t s) {
+    const uint64_t n = (uint64_t)tw * th;
+    if (!n) return cudaSuccess;
+    resample_bits_kernel<<<blocks_for(n, 256), 256, 0, s>>>(src, sw, sh, dst, tw, th, words);
+    return cudaGetLastError();
+}
+cudaError_t launch_gather(const uint32_t* order, uint64_t n, const SplatRec* rec, SplatRec* rec_sorted,
+                          uint32_t* ntiles, cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    gather_kernel<<<blocks_for(n, 256), 256, 0, s>>>(order, n, rec, rec_sorted, ntiles);
+    return cudaGetLastError();
+}
+cudaError_t launch_emit_keys(const SplatRec* rec_sorted, const uint32_t* offsets, uint64_t n, uint32_t tiles_x,
+                             uint32_t* keys, uint32_t* vals, cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    emit_keys_kernel<<<blocks_for(n, 256), 256, 0, s>>>(rec_sorted, offsets, n, tiles_x, keys, vals);
+    return cudaGetLastError();
+}
+cudaError_t launch_tile_ranges(const uint32_t* keys, uint64_t n, uint32_t* start, uint32_t* end, cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    tile_ranges_kernel<<<blocks_for(n, 256), 256, 0, s>>>(keys, n, start, end);
+    return cudaGetLastError();
+}
+cudaError_t launch_contract(const ContractParams& p, uint64_t max_touched, cudaStream_t s) {
+    if (!max_touched) return cudaSuccess;
+    if (p.dim == 512)
+        contract_kernel<true><<<warp_grid(max_touched), 256, 0, s>>>(p);
+    else
+        contract_kernel<false><<<warp_grid(max_touched), 256, 0, s>>>(p);
+    return cudaGetLastError();
+}
+cudaError_t launch_normalize(const float* sums, const float* totals, uint64_t n, uint32_t dim, float* rows,
+                             float* coverage, cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    normalize_kernel<<<warp_grid(n), 256, 0, s>>>(sums, totals, n, dim, rows, coverage);
+    return cudaGetLastError();
+}
+cudaError_t launch_normalize_rows(const float* in, const uint32_t* select, uint64_t n, uint32_t dim, float* out,
+                                  int* zero_flag, cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    normalize_rows_kernel<<<warp_grid(n), 256, 0, s>>>(in, select, n, dim, out, zero_flag);
+    return cudaGetLastError();
+}
+cudaError_t launch_flag_covered(const float* coverage, uint64_t n, uint8_t* flags, cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    flag_covered_kernel<<<blocks_for(n, 256), 256, 0, s>>>(coverage, n, flags);
+    return cudaGetLastError();
+}
+constexpr int kScoreQT = 8;
+int score_query_tile() { return kScoreQT; }
+cudaError_t launch_score(const float* rows, uint64_t count, uint32_t dim, const float* queries, uint32_t nq, uint32_t q0,
+                         float* scores, cudaStream_t s) {
+    if (!count) return cudaSuccess;
+    const size_t smem = (size_t)kScoreQT * dim * sizeof(float);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(score_kernel<kScoreQT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    unsigned g = blocks_for(count, 256);
+    if (g > 148u * 8) g = 148u * 8;
+    score_kernel<kScoreQT><<<g, 256, smem, s>>>(rows, count, dim, queries, nq, q0, scores);
+    return cudaGetLastError();
+}
+cudaError_t launch_topk(const float* scores, const uint32_t* ids, uint64_t count, uint32_t k, uint32_t nq_tile,
+                        uint32_t q0, uint32_t* out_ids, float* out_sims, cudaStream_t s) {
+    if (!nq_tile || !count || !k) return cudaSuccess;
+    if (k > (uint32_t)kMaxK) return cudaErrorInvalidValue;
+    topk_kernel<<<nq_tile, 256, 0, s>>>(scores, ids, count, k, q0, out_ids, out_sims);
+    return cudaGetLastError();
+}
+cudaError_t launch_threshold_keys(const float* scores, const uint32_t* ids, uint64_t count, float tau,
+                                  unsigned long long* keys, uint8_t* flags, cudaStream_t s) {
+    if (!count) return cudaSuccess;
+    threshold_keys_kernel<<<blocks_for(count, 256), 256, 0, s>>>(scores, ids, count, tau, keys, flags);
+    return cudaGetLastError();
+}
+
+} // namespace ss

@@ -1,0 +1,45 @@
+// Launchers of the non-exact kernels (ss_kernels.cu).
+#pragma once
+#include "ss_internal.cuh"
+
+namespace ss {
+
+struct ContractParams {
+    const uint32_t* touched_list;
+    uint32_t* touched;
+    const uint32_t* order; // rank -> gid
+    float* acc;            // [n_surv x n_masks]
+    uint32_t n_masks;
+    const float* clip;     // [n_masks x dim]
+    uint32_t dim;
+    float* sums;           // [N x dim]
+    float* totals;         // [N]
+    ViewInfo* info;
+    int count_pairs;
+    unsigned long long* cum; // running [G_v, K_v] totals
+};
+
+cudaError_t launch_rle_to_bits(const uint32_t* runs, const uint64_t* run_offsets, uint32_t n_masks, uint32_t words,
+                               uint32_t* bits, cudaStream_t s);
+cudaError_t launch_resample_bits(const uint32_t* src, uint32_t sw, uint32_t sh, uint32_t* dst, uint32_t tw,
+                                 uint32_t th, uint32_t words, cudaStream_t s);
+cudaError_t launch_gather(const uint32_t* order, uint64_t n, const SplatRec* rec, SplatRec* rec_sorted,
+                          uint32_t* ntiles, cudaStream_t s);
+cudaError_t launch_emit_keys(const SplatRec* rec_sorted, const uint32_t* offsets, uint64_t n, uint32_t tiles_x,
+                             uint32_t* keys, uint32_t* vals, cudaStream_t s);
+cudaError_t launch_tile_ranges(const uint32_t* keys, uint64_t n, uint32_t* start, uint32_t* end, cudaStream_t s);
+cudaError_t launch_contract(const ContractParams& p, uint64_t max_touched, cudaStream_t s);
+cudaError_t launch_normalize(const float* sums, const float* totals, uint64_t n, uint32_t dim, float* rows,
+                             float* coverage, cudaStream_t s);
+cudaError_t launch_normalize_rows(const float* in, const uint32_t* select, uint64_t n, uint32_t dim, float* out,
+                                  int* zero_flag, cudaStream_t s);
+cudaError_t launch_flag_covered(const float* coverage, uint64_t n, uint8_t* flags, cudaStream_t s);
+int score_query_tile();
+cudaError_t launch_score(const float* rows, uint64_t count, uint32_t dim, const float* queries, uint32_t nq,
+                         uint32_t q0, float* scores, cudaStream_t s);
+cudaError_t launch_topk(const float* scores, const uint32_t* ids, uint64_t count, uint32_t k, uint32_t nq_tile,
+                        uint32_t q0, uint32_t* out_ids, float* out_sims, cudaStream_t s);
+cudaError_t launch_threshold_keys(const float* scores, const uint32_t* ids, uint64_t count, float tau,
+                                  unsigned long long* keys, uint8_t* flags, cudaStream_t s);
+
+} // namespace ss
