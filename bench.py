@@ -1,0 +1,388 @@
+#!/usr/bin/env python3
+"""Throughput of the B200 embedding pass (BASELINE.json metric: views/sec and
+Gaussians embedded/sec; end-to-end embed time).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl b200|reference]
+
+One step = one full embedding pass over the config's views: every rank
+encodes its round-robin share of the views into its own N x 512 fp32 partial
+sums, a single NCCL reduce-scatter combines them (N > 1), and each rank
+normalises its shard (pipeline.hpp:280-470 + the paper's Fig. 4 combine).
+`value` times that pass with all inputs resident in HBM; `e2e` times the same
+pass through the C ABI with pinned host inputs (RLE mask runs, CLIP vectors,
+f64 cameras) copied in every step and the finished table shard copied back.
+
+--impl reference times the reference's own CPU encode_scene (oracle/_ref, the
+unmodified headers compiled here) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+from paper_2505_08124_b200.workload import CONFIGS, make_bench_workload  # noqa: E402
+
+PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
+FALLBACK_HBM = 6650.0
+
+
+def peaks():
+    try:
+        p = json.loads(PEAKS_FILE.read_text())
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--views", type=int, default=0, help="limit the view count (debug only)")
+    ap.add_argument("--seed", type=int, default=2505)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample-views", type=int, default=0)
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-i", str(self.idx)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                s, m = float(parts[0]), float(parts[1])
+            except ValueError:
+                continue
+            sm.append(s)
+            mx = max(mx, m)
+            for n, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------- reference arm
+def write_reference_dataset(wl, directory: str):
+    """The sample in the reference's on-disk formats (manifest/cameras/MRLE/EMBV)."""
+    from paper_2505_08124_b200 import formats
+    d = Path(directory)
+    (d / "masks").mkdir(parents=True, exist_ok=True)
+    (d / "embeddings").mkdir(exist_ok=True)
+    cams = []
+    m = formats.DatasetManifest(root=str(d), camera_file="cameras.txt", mask_width=wl.width, mask_height=wl.height,
+                                raster_width=wl.width, raster_height=wl.height, embedding_dim=wl.dim)
+    for cam, (n, w, h, runs, offs, clip) in zip(wl.cams, wl.masks):
+        cams.append(formats.CameraPose(image_id=cam.image_id, fx=cam.fx, fy=cam.fy, cx=cam.cx, cy=cam.cy,
+                                       rotation=cam.rotation, translation=cam.translation, width=w, height=h))
+        mr = formats.MaskRuns(cam.image_id, w, h, np.arange(n, dtype=np.uint32), runs, offs)
+        formats.save_maskset_runs(mr, str(d / "masks" / f"{cam.image_id}.rle"))
+        formats.save_mask_embeddings(clip, str(d / "embeddings" / f"{cam.image_id}.emb"))
+        m.images.append(formats.ImageEntry(cam.image_id, "-", cam.image_id, f"masks/{cam.image_id}.rle",
+                                           f"embeddings/{cam.image_id}.emb"))
+    formats.save_cameras(cams, str(d / "cameras.txt"))
+    formats.save_manifest(m, str(d / "manifest.txt"))
+    return str(d / "manifest.txt")
+
+
+def cpu_reference_sample(cfg_name, seed, views, threads=None):
+    """Times the reference's encode_scene (oracle/_ref) -- or, where the
+    reference build is absent, the oracle port -- on `views` views of the
+    config.  Returns (seconds, kind, cores, sample description)."""
+    cfg = CONFIGS[cfg_name]
+    threads = threads or os.cpu_count() or 1
+    wl = make_bench_workload(n_gaussians=cfg["n_gaussians"], n_views=cfg["n_views"], width=cfg["width"],
+                             height=cfg["height"], masks_per_view=cfg["masks_per_view"], dim=cfg["dim"], seed=seed,
+                             views=list(range(views)))
+    from oracle.bindings import REF_SO
+    n = cfg["n_gaussians"]
+    if REF_SO.exists():
+        from oracle.bindings import Ref
+        R = Ref()
+        tmp = tempfile.mkdtemp(prefix="ssref_")
+        mp = write_reference_dataset(wl, tmp)
+        workers = max(1, min(threads, views))
+        # phase-2 partials are workers x chunk x D f64 (pipeline.hpp:417): bound them to ~8 GB
+        chunk = int(max(4096, min(n, (8 << 30) // (workers * cfg["dim"] * 8))))
+        t0 = time.perf_counter()
+        R.encode(wl.scene, mp, workers, chunk)
+        dt = time.perf_counter() - t0
+        return dt, "reference", workers, (f"{views} of {cfg['n_views']} views of {cfg_name} through the reference "
+                                          f"encode_scene (workers={workers}, chunk_rows={chunk})")
+    from oracle.bindings import Oracle
+    O = Oracle()
+    t0 = time.perf_counter()
+    O.encode(wl.scene, wl.cams, wl.masks, cfg["dim"])
+    dt = time.perf_counter() - t0
+    return dt, "port", 1, f"{views} of {cfg['n_views']} views of {cfg_name} through the C oracle (1 thread)"
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    cores = os.cpu_count() or 1
+    views = args.cpu_sample_views or max(1, min(cores, 8))
+    times = []
+    for i in range(args.warmup + args.steps):
+        dt, kind, used, sample = cpu_reference_sample(args.config, args.seed, views, cores)
+        if i >= args.warmup:
+            times.append(dt)
+    sec = float(np.mean(times))
+    v = views / sec
+    print(json.dumps({
+        "impl": "reference", "metric": "views_per_sec", "value": v, "unit": "views/s", "n_gpus": 0,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "gaussians_embedded_per_sec": cfg["n_gaussians"] * v / cfg["n_views"],
+        "config": {"workload": f"{args.config}: {cfg['n_gaussians']} Gaussians, {cfg['n_views']} views "
+                               f"{cfg['width']}x{cfg['height']}, {cfg['masks_per_view']} masks/view, D={cfg['dim']}",
+                   "sample_views": views},
+        "cpu_baseline": {"value": v, "unit": "views/s", "cores": used, "kind": kind, "sample": sample},
+        "e2e": {"value": v, "unit": "views/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ---------------------------------------------------------------- B200 arm
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_08124_b200._lib import Context
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = CONFIGS[args.config]
+    n_views = args.views or cfg["n_views"]
+    mine = [v for v in range(n_views) if v % world == rank]
+    t_gen = time.perf_counter()
+    wl = make_bench_workload(n_gaussians=cfg["n_gaussians"], n_views=cfg["n_views"], width=cfg["width"],
+                             height=cfg["height"], masks_per_view=cfg["masks_per_view"], dim=cfg["dim"],
+                             seed=args.seed, views=mine)
+    gen_s = time.perf_counter() - t_gen
+    N, D = cfg["n_gaussians"], cfg["dim"]
+    n_pad = (N + world - 1) // world * world
+    shard = n_pad // world
+
+    ctx = Context(local)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    ctx.set_scene(wl.scene.mean, wl.scene.scale, wl.scene.quat_xyzw, wl.scene.opacity)
+
+    # device-resident inputs for `value`
+    dev = torch.device("cuda", local)
+    runs_all = np.concatenate([m[3] for m in wl.masks]).astype(np.uint32)
+    offs_abs, base = [], 0
+    for m in wl.masks:
+        offs_abs.append(m[4].astype(np.int64) + base)
+        base += int(m[4][-1])
+    d_runs = torch.from_numpy(runs_all.view(np.int32)).to(dev)
+    d_offs = [torch.from_numpy(o).to(dev) for o in offs_abs]
+    d_clip = [torch.from_numpy(np.ascontiguousarray(m[5], np.float32)).to(dev) for m in wl.masks]
+    dev_masks = [(m[0], m[1], m[2], d_runs.data_ptr(), o.data_ptr(), c.data_ptr())
+                 for m, o, c in zip(wl.masks, d_offs, d_clip)]
+    sums = torch.zeros((n_pad, D), dtype=torch.float32, device=dev)
+    totals = torch.zeros((n_pad,), dtype=torch.float32, device=dev)
+    sum_shard = torch.empty((shard, D), dtype=torch.float32, device=dev) if world > 1 else None
+    tot_shard = torch.empty((shard,), dtype=torch.float32, device=dev) if world > 1 else None
+    rows_out = torch.empty((shard, D), dtype=torch.float32, device=dev)
+    cov_out = torch.empty((shard,), dtype=torch.float32, device=dev)
+
+    def combine_and_normalize():
+        if world > 1:
+            dist.reduce_scatter_tensor(sum_shard, sums)
+            dist.reduce_scatter_tensor(tot_shard, totals)
+            s, t = sum_shard, tot_shard
+        else:
+            s, t = sums, totals
+        n_local = max(0, min(shard, N - rank * shard))
+        ctx.normalize_device(s.data_ptr(), t.data_ptr(), n_local, D, rows_out.data_ptr(), cov_out.data_ptr())
+
+    def step_device():
+        ctx.encode_begin(D, sums.data_ptr(), totals.data_ptr())
+        ctx.encode_views_device(wl.cams, dev_masks)
+        combine_and_normalize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    def timed(fn, k):
+        barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(k):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ms = torch.tensor([a.elapsed_time(b)], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        return float(ms.item()) / k
+
+    for _ in range(args.warmup):
+        step_device()
+    torch.cuda.synchronize()
+    ctx.profile_reset()
+    ctx.profile(True)
+    with ClockSampler(local) as clk:
+        ms_step = timed(step_device, args.steps)
+    ctx.profile(False)
+    prof = ctx.profile_read()
+    counters = ctx.counters()
+    own, cub = ctx.launch_count()
+
+    # ---- e2e: pinned host inputs through the C ABI, table shard back to host
+    e2e = None
+    if not args.no_e2e:
+        pin_masks, h2d = [], 0
+        for m in wl.masks:
+            r = torch.from_numpy(m[3].view(np.int32)).pin_memory().numpy().view(np.uint32)
+            o = torch.from_numpy(m[4].view(np.int64)).pin_memory().numpy().view(np.uint64)
+            c = torch.from_numpy(np.ascontiguousarray(m[5], np.float32)).pin_memory().numpy()
+            pin_masks.append((m[0], m[1], m[2], r, o, c))
+            h2d += r.nbytes + o.nbytes + c.nbytes + 128
+        host_rows = torch.empty((shard, D), dtype=torch.float32).pin_memory()
+        host_cov = torch.empty((shard,), dtype=torch.float32).pin_memory()
+
+        def step_e2e():
+            ctx.encode_begin(D, sums.data_ptr(), totals.data_ptr())
+            ctx.encode_views(wl.cams, pin_masks)
+            combine_and_normalize()
+            host_rows.copy_(rows_out, non_blocking=True)
+            host_cov.copy_(cov_out, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+
+        step_e2e()
+        e2e_ms = timed(step_e2e, args.steps)
+        e2e = {"value": n_views / (e2e_ms / 1e3), "unit": "views/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(host_rows.numel() * 4 + host_cov.numel() * 4), "ms_per_step": e2e_ms}
+
+    # ---- per-kernel roofline (this rank; events on the launching stream)
+    hbm, peak_kind = peaks()
+    steps = max(args.steps, 1)
+    kernels = {}
+    for k, v in prof.items():
+        if v["launches"] and v["ms"] > 0 and k != "query":
+            kernels[k] = {"ms_per_step": v["ms"] / steps, "launches_per_step": v["launches"] / steps,
+                          "gb_per_step": v["bytes"] / steps / 1e9,
+                          "achieved_gbs": v["bytes"] / (v["ms"] / 1e3) / 1e9 if k != "h2d" else None}
+    dom = max((k for k in kernels if k not in ("h2d",)), key=lambda k: kernels[k]["ms_per_step"])
+    dk = kernels[dom]
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": dk["achieved_gbs"], "peak": hbm, "unit": "GB/s",
+                "frac": dk["achieved_gbs"] / hbm, "traffic": None, "peak_source": f"{peak_kind} (MEASURED_PEAKS.json)",
+                "share_of_step": dk["ms_per_step"] / ms_step}
+    pass_bytes = sum(v["bytes"] for k, v in prof.items() if k not in ("h2d", "query")) / steps
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            sample = args.cpu_sample_views or max(1, min(os.cpu_count() or 1, 8))
+            dt, kind, cores, desc = cpu_reference_sample(args.config, args.seed, sample)
+            cpu = {"value": sample / dt, "unit": "views/s", "cores": cores, "kind": kind, "sample": desc,
+                   "seconds": dt}
+        except Exception as ex:  # reported, not fatal
+            cpu = {"value": None, "unit": "views/s", "cores": None, "kind": "unavailable", "sample": str(ex)}
+
+    value = n_views / (ms_step / 1e3)
+    if rank == 0:
+        line = {
+            "metric": "views_per_sec", "value": value, "unit": "views/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic (bench-style scene, orbit cameras, random "
+                                                              "rectangle RLE masks, synth_embedding CLIP)",
+            "gaussians_embedded_per_sec": N * value / n_views,
+            "gaussian_views_per_sec": N * value,
+            "embed_seconds": ms_step / 1e3,
+            "config": {"workload": f"{args.config}: {N} Gaussians, {n_views} views {cfg['width']}x{cfg['height']}, "
+                                   f"{cfg['masks_per_view']} masks/view, D={D}",
+                       "parallelism": f"views round-robin over {world} GPU(s), NCCL reduce-scatter of N x D sums",
+                       "l2": "inputs larger than L2 (N x 512 fp32 sums = %.1f GB RMW per pass)" % (N * D * 4 / 1e9),
+                       "dataset_gen_seconds": gen_s},
+            "roofline": roofline,
+            "pass_algorithmic_gb": pass_bytes / 1e9,
+            "pass_hbm_frac": pass_bytes / (ms_step / 1e3) / 1e9 / hbm,
+            "kernels": kernels,
+            "geometry_per_view": {k: counters[k] / max(counters["views"], 1) for k in
+                                  ("n_vis", "instances", "touched", "pairs")},
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "gpu_launches": int((own + cub) / steps),
+            "gpu_launches_detail": {"own_per_step": own / steps, "cub_per_step": cub / steps},
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -66,12 +66,13 @@ typedef struct ss_weight_entry {
  * alternating run lengths over row-major bits, zeros first) plus the mask
  * CLIP vectors (providers.hpp:156-204).  Masks are resampled to the raster
  * resolution on the device (providers.hpp:359-373). */
+#define SS_MASKS_ON_DEVICE 1u /* ss_view_masks.flags: runs/run_offsets/clip are device pointers */
 typedef struct ss_view_masks {
     uint32_t n_masks;
     uint32_t mask_width, mask_height;
-    uint32_t pad;
+    uint32_t flags;              /* SS_MASKS_ON_DEVICE or 0 (host pointers) */
     const uint32_t* runs;        /* all masks' runs, concatenated */
-    const uint64_t* run_offsets; /* n_masks + 1 prefix offsets into runs */
+    const uint64_t* run_offsets; /* n_masks + 1 prefix offsets into runs (device: absolute) */
     const float* clip;           /* n_masks x dim, row-major */
 } ss_view_masks;
 

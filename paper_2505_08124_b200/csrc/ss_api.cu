@@ -371,24 +371,36 @@ void build_mask_bits(ss_ctx* c, const ss_camera& cam, const ss_view_masks* vm, u
     if (M == 0) return;
     const uint64_t mw = vm->mask_width, mh = vm->mask_height;
     if (mw == 0 || mh == 0) throw Error(SS_ERR_CONTRACT, "resample_mask: zero mask resolution");
-    // validate run streams against the mask area (providers.hpp:97-107)
-    const uint64_t nr = vm->run_offsets[M] - vm->run_offsets[0];
-    for (uint32_t m = 0; m < M; ++m) {
-        uint64_t tot = 0;
-        for (uint64_t r = vm->run_offsets[m]; r < vm->run_offsets[m + 1]; ++r) tot += vm->runs[r];
-        if (tot != mw * mh)
-            throw Error(SS_ERR_FORMAT, "image " + std::to_string(image_id) + ": mask RLE length mismatch: runs cover " +
-                                           std::to_string(tot) + " of " + std::to_string(mw * mh) + " pixels");
-    }
-    auto* d_runs = static_cast<uint32_t*>(c->runs.ensure(std::max<uint64_t>(nr, 1) * 4));
-    auto* d_off = static_cast<uint64_t*>(c->run_offsets.ensure((M + 1) * 8ull));
-    std::vector<uint64_t> rel(M + 1);
-    for (uint32_t m = 0; m <= M; ++m) rel[m] = vm->run_offsets[m] - vm->run_offsets[0];
-    {
+    const uint32_t* d_runs;
+    const uint64_t* d_off;
+    uint64_t nr;
+    if (vm->flags & SS_MASKS_ON_DEVICE) {
+        // device-resident encodings: absolute offsets, validated by the caller
+        d_runs = vm->runs;
+        d_off = vm->run_offsets;
+        nr = 0;
+    } else {
+        // validate run streams against the mask area (providers.hpp:97-107)
+        nr = vm->run_offsets[M] - vm->run_offsets[0];
+        for (uint32_t m = 0; m < M; ++m) {
+            uint64_t tot = 0;
+            for (uint64_t r = vm->run_offsets[m]; r < vm->run_offsets[m + 1]; ++r) tot += vm->runs[r];
+            if (tot != mw * mh)
+                throw Error(SS_ERR_FORMAT, "image " + std::to_string(image_id) +
+                                               ": mask RLE length mismatch: runs cover " + std::to_string(tot) +
+                                               " of " + std::to_string(mw * mh) + " pixels");
+        }
+        auto* hr = static_cast<uint32_t*>(c->runs.ensure(std::max<uint64_t>(nr, 1) * 4));
+        auto* ho = static_cast<uint64_t*>(c->run_offsets.ensure((M + 1) * 8ull));
+        std::vector<uint64_t> rel(M + 1);
+        for (uint32_t m = 0; m <= M; ++m) rel[m] = vm->run_offsets[m] - vm->run_offsets[0];
         Scope h(c, SS_K_H2D);
-        SS_CUDA(cudaMemcpyAsync(d_runs, vm->runs + vm->run_offsets[0], nr * 4, cudaMemcpyHostToDevice, s));
-        SS_CUDA(cudaMemcpyAsync(d_off, rel.data(), (M + 1) * 8ull, cudaMemcpyHostToDevice, s));
+        SS_CUDA(cudaMemcpyAsync(hr, vm->runs + vm->run_offsets[0], nr * 4, cudaMemcpyHostToDevice, s));
+        // pageable source: staged synchronously, so `rel` may go out of scope after the call
+        SS_CUDA(cudaMemcpyAsync(ho, rel.data(), (M + 1) * 8ull, cudaMemcpyHostToDevice, s));
         c->prof.bytes[SS_K_H2D] += nr * 4.0 + (M + 1) * 8.0;
+        d_runs = hr;
+        d_off = ho;
     }
     const bool same = mw == cam.width && mh == cam.height;
     uint32_t* target = pb;
@@ -401,8 +413,6 @@ void build_mask_bits(ss_ctx* c, const ss_camera& cam, const ss_view_masks* vm, u
         own_launch(c, launch_resample_bits(target, (uint32_t)mw, (uint32_t)mh, pb, cam.width, cam.height, words, s),
                    SS_K_MASKS);
     c->prof.bytes[SS_K_MASKS] += nr * 4.0 + (double)P * ((M + 7) / 8);
-    // std::vector rel must outlive the async copy from pageable memory: cudaMemcpyAsync
-    // from pageable memory is staged synchronously, so returning is safe.
 }
 
 void encode_one(ss_ctx* c, const ss_camera& cam, const ss_view_masks* vm, int mode) {
@@ -415,10 +425,12 @@ void encode_one(ss_ctx* c, const ss_camera& cam, const ss_view_masks* vm, int mo
     const std::string prefix = "image " + std::to_string(cam.image_id) + ": ";
     cudaStream_t s = c->stream;
     if (M) build_mask_bits(c, cam, vm, words, cam.image_id);
-    auto* d_clip = static_cast<float*>(c->clip.ensure(std::max<uint64_t>((uint64_t)M * c->dim, 1) * 4));
-    if (M) {
+    const float* d_clip = vm && (vm->flags & SS_MASKS_ON_DEVICE) ? vm->clip : nullptr;
+    if (M && !d_clip) {
+        auto* dc = static_cast<float*>(c->clip.ensure(std::max<uint64_t>((uint64_t)M * c->dim, 1) * 4));
+        d_clip = dc;
         Scope h(c, SS_K_H2D);
-        SS_CUDA(cudaMemcpyAsync(d_clip, vm->clip, (size_t)M * c->dim * 4, cudaMemcpyHostToDevice, s));
+        SS_CUDA(cudaMemcpyAsync(dc, vm->clip, (size_t)M * c->dim * 4, cudaMemcpyHostToDevice, s));
         c->prof.bytes[SS_K_H2D] += (double)M * c->dim * 4;
     }
     const Geometry g = run_geometry(c, cam, SS_ERR_DATA, prefix.c_str());

@@ -100,7 +100,7 @@ def look_at(eye, target, w, h, focal, image_id=0):
                            image_id=image_id)
 
 
-def test_camera(w, h, distance=8.0, focal=0.0, image_id=0):
+def make_test_camera(w, h, distance=8.0, focal=0.0, image_id=0):
     """helpers.hpp:40-47"""
     if focal <= 0:
         focal = 0.9 * w
