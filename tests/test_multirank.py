@@ -1,0 +1,89 @@
+"""CPU, world_size 2 over gloo: the multi-GPU host logic of bench.py / the
+paper's Fig. 4 combine -- views sharded round-robin, per-rank partial sums, one
+reduce-scatter of the N x D sums + N totals, per-shard finalize -- reproduces
+the single-worker encode (the reference's worker-count invariance,
+test_pipeline.cpp:312-317, 1e-5 relative).  Each rank's partial sums come from
+the oracle (the device kernels run only on the GPU box)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import torch
+    import torch.distributed as dist
+
+    from oracle.bindings import Oracle
+    from paper_2505_08124_b200.multigpu import padded_rows, reduce_scatter_rows, shard_rows, shard_views
+    from paper_2505_08124_b200.workload import make_bench_workload
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    wl = make_bench_workload(n_gaussians=1501, n_views=5, width=64, height=48, masks_per_view=12, dim=32, seed=3)
+    O = Oracle()
+    mine = shard_views(5, world, rank)
+    cams = [wl.cams[v] for v in mine]
+    masks = [wl.masks[v] for v in mine]
+    s, t = O.encode_partial(wl.scene, cams, masks, 32, 0, len(mine))
+    n = 1501
+    npad = padded_rows(n, world)
+    full_s = torch.zeros((npad, 32), dtype=torch.float64)
+    full_t = torch.zeros((npad,), dtype=torch.float64)
+    full_s[:n] = torch.from_numpy(s)
+    full_t[:n] = torch.from_numpy(t)
+    per = npad // world
+    sh_s = torch.empty((per, 32), dtype=torch.float64)
+    sh_t = torch.empty((per,), dtype=torch.float64)
+    reduce_scatter_rows(sh_s, full_s)
+    reduce_scatter_rows(sh_t, full_t)
+    lo, hi = shard_rows(n, world, rank)
+    rows = np.zeros((hi - lo, 32), np.float32)
+    cov = np.zeros(hi - lo, np.float32)
+    O.L.sso_finalize(sh_s.numpy().ctypes.data, sh_t.numpy().ctypes.data, hi - lo, 32, rows.ctypes.data,
+                     cov.ctypes.data)
+    q.put((rank, lo, hi, rows, cov))
+    dist.destroy_process_group()
+
+
+def test_two_rank_combine_matches_single_worker():
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    parts = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    parts.sort()
+    rows = np.concatenate([p[3] for p in parts])
+    cov = np.concatenate([p[4] for p in parts])
+
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    from oracle.bindings import Oracle
+    from paper_2505_08124_b200.workload import make_bench_workload
+    wl = make_bench_workload(n_gaussians=1501, n_views=5, width=64, height=48, masks_per_view=12, dim=32, seed=3)
+    er, ec = Oracle().encode(wl.scene, wl.cams, wl.masks, 32)
+    assert np.array_equal(cov > 0, ec > 0)
+    e, g = er.astype(np.float64), rows.astype(np.float64)
+    den = np.sqrt((e ** 2).sum(1))
+    rel = np.sqrt(((e - g) ** 2).sum(1)) / np.where(den > 0, den, 1)
+    assert rel.max() <= 1e-5
+    np.testing.assert_allclose(cov, ec, rtol=1e-6)
