@@ -244,7 +244,7 @@ def main():
     d_runs = torch.from_numpy(runs_all.view(np.int32)).to(dev)
     d_offs = [torch.from_numpy(o).to(dev) for o in offs_abs]
     d_clip = [torch.from_numpy(np.ascontiguousarray(m[5], np.float32)).to(dev) for m in wl.masks]
-    dev_masks = [(m[0], m[1], m[2], d_runs.data_ptr(), o.data_ptr(), c.data_ptr())
+    dev_masks = [(m[0], m[1], m[2], d_runs.data_ptr(), o.data_ptr(), c.data_ptr(), int(m[4][-1] - m[4][0]))
                  for m, o, c in zip(wl.masks, d_offs, d_clip)]
     sums = torch.zeros((n_pad, D), dtype=torch.float32, device=dev)
     totals = torch.zeros((n_pad,), dtype=torch.float32, device=dev)

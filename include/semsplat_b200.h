@@ -74,6 +74,7 @@ typedef struct ss_view_masks {
     const uint32_t* runs;        /* all masks' runs, concatenated */
     const uint64_t* run_offsets; /* n_masks + 1 prefix offsets into runs (device: absolute) */
     const float* clip;           /* n_masks x dim, row-major */
+    uint64_t n_runs;             /* total runs of the view (required with SS_MASKS_ON_DEVICE) */
 } ss_view_masks;
 
 typedef struct ss_ctx ss_ctx;

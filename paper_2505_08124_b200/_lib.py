@@ -31,6 +31,7 @@ class ViewMasks(C.Structure):
     _fields_ = [
         ("n_masks", C.c_uint32), ("mask_width", C.c_uint32), ("mask_height", C.c_uint32), ("flags", C.c_uint32),
         ("runs", C.POINTER(C.c_uint32)), ("run_offsets", C.POINTER(C.c_uint64)), ("clip", C.POINTER(C.c_float)),
+        ("n_runs", C.c_uint64),
     ]
 
 
@@ -203,20 +204,21 @@ class Context:
             clip = np.ascontiguousarray(clip, np.float32)
             keep += [runs, offs, clip]
             marr[i] = ViewMasks(int(n_masks), int(mw), int(mh), 0, _ptr(runs, C.c_uint32), _ptr(offs, C.c_uint64),
-                                _ptr(clip, C.c_float))
+                                _ptr(clip, C.c_float), int(offs[-1] - offs[0]) if offs.size else 0)
         check(self._L.ss_encode_views(self.h, nv, carr, marr, int(mode)))
 
     def encode_views_device(self, cams, dev_masks, mode: int = 0):
-        """dev_masks: per view (n_masks, mask_w, mask_h, runs_ptr, offsets_ptr, clip_ptr) with device
-        pointers (absolute run offsets)."""
+        """dev_masks: per view (n_masks, mask_w, mask_h, runs_ptr, offsets_ptr, clip_ptr, n_runs) with
+        device pointers (absolute run offsets)."""
         nv = len(cams)
         carr = (Camera * max(nv, 1))()
         marr = (ViewMasks * max(nv, 1))()
         for i, (cam, m) in enumerate(zip(cams, dev_masks)):
             carr[i] = camera_struct(cam)
-            n_masks, mw, mh, rp, op, cp = m
+            n_masks, mw, mh, rp, op, cp, nr = m
             marr[i] = ViewMasks(int(n_masks), int(mw), int(mh), 1, C.cast(C.c_void_p(rp), C.POINTER(C.c_uint32)),
-                                C.cast(C.c_void_p(op), C.POINTER(C.c_uint64)), C.cast(C.c_void_p(cp), C.POINTER(C.c_float)))
+                                C.cast(C.c_void_p(op), C.POINTER(C.c_uint64)), C.cast(C.c_void_p(cp), C.POINTER(C.c_float)),
+                                int(nr))
         check(self._L.ss_encode_views(self.h, nv, carr, marr, int(mode)))
 
     def encode_finalize(self, row_lo: int = 0, row_hi: int | None = None):

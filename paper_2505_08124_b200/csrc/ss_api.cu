@@ -73,7 +73,7 @@ struct DevBuf {
         p = nullptr;
         bytes = 0;
         size_t cap = std::max<size_t>(want, 256);
-        cap = cap + cap / 8; // slack so slowly growing sizes do not thrash
+        cap = (cap + cap / 8 + 255) & ~(size_t)255; // slack so slowly growing sizes do not thrash; 256-B granules
         SS_CUDA(cudaMalloc(&p, cap));
         bytes = cap;
         return p;
@@ -130,7 +130,7 @@ struct ss_ctx {
     uint32_t* h_u32 = nullptr;      // pinned scratch
 
     // masks
-    ss::DevBuf pix_bits, mask_bits, runs, run_offsets, clip;
+    ss::DevBuf pix_bits, mask_bits, runs, run_offsets, clip, spans;
     // capture
     ss::DevBuf pix_count, pix_offset, entries, per_pixel_total, alpha;
     uint64_t cap_entries = 0, cap_splats = 0, cap_instances = 0;
@@ -408,7 +408,11 @@ void build_mask_bits(ss_ctx* c, const ss_camera& cam, const ss_view_masks* vm, u
         target = static_cast<uint32_t*>(c->mask_bits.ensure(mw * mh * words * 4));
         SS_CUDA(cudaMemsetAsync(target, 0, mw * mh * words * 4, s));
     }
-    own_launch(c, launch_rle_to_bits(d_runs, d_off, M, words, target, s), SS_K_MASKS);
+    // spans: at most one per run; the run count is bounded by the RLE stream length
+    const uint64_t max_spans = ((vm->flags & SS_MASKS_ON_DEVICE) ? vm->n_runs : nr) / 2 + M;
+    auto* spans = static_cast<uint4*>(c->spans.ensure(std::max<uint64_t>(max_spans, 1) * 16 + 16));
+    auto* n_spans = reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(c->spans.p) + c->spans.bytes - 16);
+    own_launch(c, launch_rle_to_bits(d_runs, d_off, M, words, target, spans, n_spans, s), SS_K_MASKS, 2);
     if (!same)
         own_launch(c, launch_resample_bits(target, (uint32_t)mw, (uint32_t)mh, pb, cam.width, cam.height, words, s),
                    SS_K_MASKS);
@@ -548,7 +552,7 @@ void ss_destroy(ss_ctx* c) {
                           &c->keys_sorted, &c->order, &c->rec_sorted, &c->ntiles, &c->offsets, &c->tile_keys,
                           &c->tile_vals, &c->tile_keys_sorted, &c->tile_ranks, &c->tile_start, &c->tile_end,
                           &c->cub_tmp, &c->num_sel, &c->info, &c->pix_bits, &c->mask_bits, &c->runs,
-                          &c->run_offsets, &c->clip, &c->pix_count, &c->pix_offset, &c->entries,
+                          &c->run_offsets, &c->clip, &c->spans, &c->pix_count, &c->pix_offset, &c->entries,
                           &c->per_pixel_total, &c->alpha, &c->acc, &c->touched, &c->touched_list, &c->counters,
                           &c->sums_buf, &c->totals_buf, &c->store_rows, &c->store_ids, &c->qbuf, &c->qnorm,
                           &c->scores, &c->topk_ids, &c->topk_sims, &c->sel_flags, &c->thr_keys, &c->thr_keys_sorted,

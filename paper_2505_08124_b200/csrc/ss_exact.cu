@@ -206,6 +206,11 @@ __global__ void __launch_bounds__(256) project_kernel(ProjectParams p) {
 // 213-247), with the reference's box test first, Mahalanobis cutoff, alpha
 // clamp, skip rule, weight cutoff and transmittance floor.
 //
+// Work shaping (no effect on the arithmetic): each warp owns an 8x4 pixel
+// block of the tile, so a warp-uniform test of the splat's box against the
+// block skips splats that cannot touch any of its pixels, and a warp whose 32
+// pixels have all terminated stops walking the batch.
+//
 // KIND 0: count contributions per pixel (sizes the capture).
 // KIND 1: capture -- write WeightEntry records at per-pixel offsets, in rank
 //         order (= the reference's stable_sort by pixel), per_pixel_total and
@@ -217,13 +222,19 @@ __global__ void __launch_bounds__(256) project_kernel(ProjectParams p) {
 template <int KIND, bool FALLOFF, int MW>
 __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) {
     __shared__ SplatRec srec[kRasterThreads];
+    __shared__ uint32_t srank[kRasterThreads];
+    __shared__ uint2 sbox[kRasterThreads]; // x0|x1<<16, y0|y1<<16 (conflict-free ballot reads)
     __shared__ unsigned long long stab[256];
     stab[threadIdx.x] = kExpTab[threadIdx.x];
 
     const uint32_t tile = blockIdx.x;
     const uint32_t tx = tile % p.tiles_x, ty = tile / p.tiles_x;
-    const uint32_t px = tx * kTile + (threadIdx.x & 15u);
-    const uint32_t py = ty * kTile + (threadIdx.x >> 4);
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    // warp w covers columns 8*(w&1) .. +7, rows 4*(w>>1) .. +3 of the tile
+    const uint32_t bx0 = tx * kTile + 8u * (warp & 1u), by0 = ty * kTile + 4u * (warp >> 1);
+    const uint32_t px = bx0 + (lane & 7u);
+    const uint32_t py = by0 + (lane >> 3);
+    const uint32_t bx1 = bx0 + 7u, by1 = by0 + 3u;
     const bool inside = px < p.width && py < p.height;
     const uint32_t pixel = py * p.width + px;
     const uint32_t start = p.tile_start[tile], end = p.tile_end[tile];
@@ -240,9 +251,8 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
     // fused-mode per-pixel mask bitset and lane grouping by identical bitset
     uint32_t bits[MW > 0 ? MW : 1];
     uint32_t grp = 0;
-    bool any_bits = false;
-    const int lane = threadIdx.x & 31;
     if constexpr (KIND == 2) {
+        bool any_bits = false;
 #pragma unroll
         for (int w = 0; w < MW; ++w) {
             bits[w] = inside ? p.pix_bits[(size_t)pixel * MW + w] : 0u;
@@ -264,42 +274,67 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
         if (__syncthreads_and(done)) break;
         const uint32_t i = base + threadIdx.x;
         if (i < end) {
-            const uint4* src = reinterpret_cast<const uint4*>(p.rec_sorted + p.tile_ranks[i]);
+            const uint32_t r = p.tile_ranks[i];
+            srank[threadIdx.x] = r;
+            const uint4* src = reinterpret_cast<const uint4*>(p.rec_sorted + r);
             uint4* dst = reinterpret_cast<uint4*>(srec + threadIdx.x);
             dst[0] = __ldg(src);
             dst[1] = __ldg(src + 1);
             dst[2] = __ldg(src + 2);
-            dst[3] = __ldg(src + 3);
+            const uint4 w3 = __ldg(src + 3);
+            dst[3] = w3;
+            sbox[threadIdx.x] = make_uint2(w3.x, w3.y);
         }
         __syncthreads();
         const uint32_t nb = min((uint32_t)kRasterThreads, end - base);
-        for (uint32_t j = 0; j < nb; ++j) {
+        // per-warp candidate set: splats of the batch whose box meets this warp's 8x4 block
+        uint32_t cand[kRasterThreads / 32];
+#pragma unroll
+        for (int q = 0; q < kRasterThreads / 32; ++q) {
+            const uint32_t k = (uint32_t)q * 32u + lane;
+            bool hit = false;
+            if (k < nb) {
+                const uint2 box = sbox[k];
+                hit = !((box.x >> 16) < bx0 || (box.x & 0xffffu) > bx1 || (box.y >> 16) < by0 ||
+                        (box.y & 0xffffu) > by1);
+            }
+            cand[q] = __ballot_sync(0xffffffffu, hit);
+        }
+        if (__all_sync(0xffffffffu, done)) {
+#pragma unroll
+            for (int q = 0; q < kRasterThreads / 32; ++q) cand[q] = 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < kRasterThreads / 32; ++q)
+        while (cand[q]) {
+            const uint32_t j = (uint32_t)q * 32u + (uint32_t)(__ffs(cand[q]) - 1);
+            cand[q] &= cand[q] - 1u;
+            const SplatRec& s = srec[j];
+            const uint2 box = sbox[j];
+            const uint32_t sx0 = box.x & 0xffffu, sx1 = box.x >> 16, sy0 = box.y & 0xffffu, sy1 = box.y >> 16;
             bool contrib = false;
             float wf = 0.0f;
-            if (!done) {
-                const SplatRec& s = srec[j];
-                if (px >= s.x0 && px <= s.x1 && py >= s.y0 && py <= s.y1) {
-                    const double dx = ds(dpx, s.mu_x), dy = ds(dpy, s.mu_y);
-                    const double d2 = da(da(dm(dm(s.a, dx), dx), dm(dm(s.b2, dx), dy)), dm(dm(s.c, dy), dy));
-                    if (!(d2 > kMahalanobisSqCutoff)) {
-                        const double g = glibc_exp(dm(-0.5, d2), stab);
-                        if constexpr (FALLOFF) {
-                            if (g >= kWeightCutoff) {
+            if (!done && px >= sx0 && px <= sx1 && py >= sy0 && py <= sy1) {
+                const double dx = ds(dpx, s.mu_x), dy = ds(dpy, s.mu_y);
+                const double d2 = da(da(dm(dm(s.a, dx), dx), dm(dm(s.b2, dx), dy)), dm(dm(s.c, dy), dy));
+                if (!(d2 > kMahalanobisSqCutoff)) {
+                    const double g = glibc_exp(dm(-0.5, d2), stab);
+                    if constexpr (FALLOFF) {
+                        if (g >= kWeightCutoff) {
+                            contrib = true;
+                            wf = __double2float_rn(g);
+                        }
+                    } else {
+                        const double og = dm((double)s.opacity, g);
+                        const double alpha = og < kAlphaMax ? og : kAlphaMax;
+                        if (!(alpha < kAlphaSkip)) {
+                            const double w = dm(alpha, T);
+                            if (w >= kWeightCutoff) {
                                 contrib = true;
-                                wf = __double2float_rn(g);
+                                wf = __double2float_rn(w);
                             }
-                        } else {
-                            const double og = dm((double)s.opacity, g);
-                            const double alpha = og < kAlphaMax ? og : kAlphaMax;
-                            if (!(alpha < kAlphaSkip)) {
-                                const double w = dm(alpha, T);
-                                if (w >= kWeightCutoff) {
-                                    contrib = true;
-                                    wf = __double2float_rn(w);
-                                }
-                                T = dm(T, ds(1.0, alpha));
-                                if (T < kTransmittanceFloor) done = true;
-                            }
+                            T = dm(T, ds(1.0, alpha));
+                            if (T < kTransmittanceFloor) done = true;
                         }
                     }
                 }
@@ -308,13 +343,13 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
                 count += contrib ? 1u : 0u;
             } else if constexpr (KIND == 1) {
                 if (contrib) {
-                    p.entries[out++] = ss_weight_entry{srec[j].gid, pixel, wf};
+                    p.entries[out++] = ss_weight_entry{s.gid, pixel, wf};
                     total = da(total, (double)wf);
                 }
             } else {
                 const uint32_t em = __ballot_sync(0xffffffffu, contrib);
                 if (em) {
-                    const uint32_t rank = p.tile_ranks[base + j];
+                    const uint32_t rank = srank[j];
                     uint32_t rem = em;
                     while (rem) {
                         const int leader = __ffs(rem) - 1;
@@ -322,7 +357,7 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
                         float v = (contrib && ((gm >> lane) & 1u)) ? wf : 0.0f;
 #pragma unroll
                         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                        if (lane == leader) {
+                        if ((int)lane == leader) {
                             float* row = p.acc + (size_t)rank * p.n_masks;
 #pragma unroll
                             for (int w = 0; w < MW; ++w) {
@@ -336,7 +371,7 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
                         }
                         rem &= ~gm;
                     }
-                    if (lane == __ffs(em) - 1) {
+                    if ((int)lane == __ffs(em) - 1) {
                         // first toucher of this rank appends it to the contraction list
                         if (*reinterpret_cast<volatile uint32_t*>(p.touched + rank) == 0u &&
                             atomicExch(p.touched + rank, 1u) == 0u) {
@@ -345,6 +380,10 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
                         }
                     }
                 }
+            }
+            if (__all_sync(0xffffffffu, done)) {
+#pragma unroll
+                for (int r2 = 0; r2 < kRasterThreads / 32; ++r2) cand[r2] = 0u;
             }
         }
         __syncthreads();

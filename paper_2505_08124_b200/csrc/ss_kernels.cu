@@ -13,17 +13,17 @@ namespace {
 
 // ------------------------------------------------------------ mask decode
 // providers.hpp:95-109 rle_decode (alternating runs, zeros first) straight
-// into a per-pixel mask bitset: one CTA per mask, a block scan turns run
-// lengths into start positions 256 runs at a time, each "ones" run sets bit m
-// of its pixels' bitset words.
-__global__ void __launch_bounds__(256) rle_to_bits_kernel(const uint32_t* runs, const uint64_t* run_offsets,
-                                                          uint32_t words, uint32_t* bits) {
+// into a per-pixel mask bitset.  Pass 1 (one CTA per mask): a block scan turns
+// run lengths into start positions and emits every "ones" run as a (start,
+// len, mask) span.  Pass 2: one warp per span, lanes stride its pixels and
+// OR bit m into the pixel's bitset word (spans of different masks share words).
+__global__ void __launch_bounds__(256) rle_spans_kernel(const uint32_t* runs, const uint64_t* run_offsets,
+                                                        uint4* spans, unsigned int* n_spans) {
     using Scan = cub::BlockScan<unsigned long long, 256>;
     __shared__ typename Scan::TempStorage tmp;
     __shared__ unsigned long long carry;
     const uint32_t m = blockIdx.x;
     const uint64_t r0 = run_offsets[m], r1 = run_offsets[m + 1];
-    const uint32_t word = m >> 5, bit = 1u << (m & 31u);
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
     for (uint64_t base = r0; base < r1; base += 256) {
@@ -32,12 +32,31 @@ __global__ void __launch_bounds__(256) rle_to_bits_kernel(const uint32_t* runs, 
         unsigned long long pos, agg;
         Scan(tmp).ExclusiveSum(len, pos, agg);
         pos += carry;
-        if (k < r1 && ((k - r0) & 1ull)) {
-            for (unsigned long long p = pos; p < pos + len; ++p) atomicOr(bits + p * words + word, bit);
+        const bool ones = k < r1 && ((k - r0) & 1ull) && len > 0;
+        const unsigned int bal = __ballot_sync(0xffffffffu, ones);
+        unsigned int slot0 = 0;
+        if ((threadIdx.x & 31) == 0 && bal) slot0 = atomicAdd(n_spans, (unsigned int)__popc(bal));
+        slot0 = __shfl_sync(0xffffffffu, slot0, 0);
+        if (ones) {
+            const unsigned int slot = slot0 + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u));
+            spans[slot] = make_uint4((uint32_t)pos, (uint32_t)(pos >> 32), (uint32_t)len, m);
         }
         __syncthreads();
         if (threadIdx.x == 0) carry += agg;
         __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(256) spans_to_bits_kernel(const uint4* spans, const unsigned int* n_spans,
+                                                            uint32_t words, uint32_t* bits) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const unsigned int n = *n_spans;
+    for (uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n;
+         w += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint4 sp = spans[w];
+        const unsigned long long pos = ((unsigned long long)sp.y << 32) | sp.x;
+        const uint32_t word = sp.w >> 5, bit = 1u << (sp.w & 31u);
+        for (uint32_t i = lane; i < sp.z; i += 32) atomicOr(bits + (pos + i) * words + word, bit);
     }
 }
 
@@ -368,9 +387,12 @@ static inline unsigned warp_grid(uint64_t n) {
 }
 
 cudaError_t launch_rle_to_bits(const uint32_t* runs, const uint64_t* run_offsets, uint32_t n_masks, uint32_t words,
-                               uint32_t* bits, cudaStream_t s) {
+                               uint32_t* bits, uint4* spans, unsigned int* n_spans, cudaStream_t s) {
     if (n_masks == 0) return cudaSuccess;
-    rle_to_bits_kernel<<<n_masks, 256, 0, s>>>(runs, run_offsets, words, bits);
+    cudaError_t e = cudaMemsetAsync(n_spans, 0, sizeof(unsigned int), s);
+    if (e != cudaSuccess) return e;
+    rle_spans_kernel<<<n_masks, 256, 0, s>>>(runs, run_offsets, spans, n_spans);
+    spans_to_bits_kernel<<<148 * 8, 256, 0, s>>>(spans, n_spans, words, bits);
     return cudaGetLastError();
 }
 cudaError_t launch_resample_bits(const uint32_t* src, uint32_t sw, uint32_t sh, uint32_t* dst, uint32_t tw,

@@ -20,7 +20,7 @@ struct ContractParams {
 };
 
 cudaError_t launch_rle_to_bits(const uint32_t* runs, const uint64_t* run_offsets, uint32_t n_masks, uint32_t words,
-                               uint32_t* bits, cudaStream_t s);
+                               uint32_t* bits, uint4* spans, unsigned int* n_spans, cudaStream_t s);
 cudaError_t launch_resample_bits(const uint32_t* src, uint32_t sw, uint32_t sh, uint32_t* dst, uint32_t tw,
                                  uint32_t th, uint32_t words, cudaStream_t s);
 cudaError_t launch_gather(const uint32_t* order, uint64_t n, const SplatRec* rec, SplatRec* rec_sorted,
