@@ -123,7 +123,7 @@ struct ss_ctx {
     // per-view geometry scratch
     ss::DevBuf rec, keys, flags, keys_sel, ids_sel, keys_sorted, order, rec_sorted, ntiles, offsets;
     ss::DevBuf tile_keys, tile_vals, tile_keys_sorted, tile_ranks, tile_start, tile_end;
-    ss::DevBuf cub_tmp, num_sel;
+    ss::DevBuf cub_tmp, num_sel, k32, k32_sorted;
     ss::DevBuf info;
     ss::ViewInfo* h_info = nullptr; // pinned
     ss::ViewInfo* h_init = nullptr; // pinned
@@ -281,16 +281,21 @@ Geometry run_geometry(ss_ctx* c, const ss_camera& cam, int err_kind, const char*
 
     {
         Scope sc(c, SS_K_SORT);
-        // depth sort on the varying bit range; stable => ties keep id order
+        // depth sort on 32-bit narrowed keys (stable => ties keep id order), then
+        // an exact fixup of the rare runs that share a narrowed key
         const uint32_t hb = bits_for(c->h_info->min_key ^ c->h_info->max_key);
-        const uint32_t end_bit = (c->h_info->min_key == c->h_info->max_key) ? 1 : hb;
+        const uint32_t shift = hb > 32 ? hb - 32 : 0;
+        const uint32_t end_bit = std::max<uint32_t>(1, std::min<uint32_t>(hb, 32));
+        auto* k32 = static_cast<uint32_t*>(c->k32.ensure(std::max<uint64_t>(n, 1) * 4));
+        auto* k32s = static_cast<uint32_t*>(c->k32_sorted.ensure(std::max<uint64_t>(n, 1) * 4));
+        own_launch(c, launch_narrow_keys(keys_sel, n, c->h_info->min_key, shift, k32, s), SS_K_SORT);
         size_t tb = 0;
-        SS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys_sel, keys_sorted, ids_sel, order, (int)n, 0,
-                                                (int)end_bit, s));
+        SS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k32, k32s, ids_sel, order, (int)n, 0, (int)end_bit, s));
         void* tmp = c->cub_tmp.ensure(tb);
         tb = c->cub_tmp.bytes;
-        SS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys_sel, keys_sorted, ids_sel, order, (int)n, 0,
-                                                (int)end_bit, s));
+        SS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k32, k32s, ids_sel, order, (int)n, 0, (int)end_bit, s));
+        if (shift > 0) own_launch(c, launch_tie_fixup(k32s, n, keys, order, s), SS_K_SORT);
+        (void)keys_sorted;
         c->launches_cub += 1;
         c->prof.launches[SS_K_SORT] += 1;
         c->prof.bytes[SS_K_SORT] += 24.0 * (double)n;
@@ -311,32 +316,42 @@ Geometry run_geometry(ss_ctx* c, const ss_camera& cam, int err_kind, const char*
     }
     g.n_inst = c->h_u32[0];
     const uint64_t I = g.n_inst;
-    auto* tkeys = static_cast<uint32_t*>(c->tile_keys.ensure(std::max<uint64_t>(I, 1) * 4));
+    const bool k16 = g.tiles <= 65536u;
+    void* tkeys = c->tile_keys.ensure(std::max<uint64_t>(I, 1) * 4);
     auto* tvals = static_cast<uint32_t*>(c->tile_vals.ensure(std::max<uint64_t>(I, 1) * 4));
-    auto* tkeys_sorted = static_cast<uint32_t*>(c->tile_keys_sorted.ensure(std::max<uint64_t>(I, 1) * 4));
+    void* tkeys_sorted = c->tile_keys_sorted.ensure(std::max<uint64_t>(I, 1) * 4);
     auto* tranks = static_cast<uint32_t*>(c->tile_ranks.ensure(std::max<uint64_t>(I, 1) * 4));
     {
         Scope sc(c, SS_K_BIN);
-        own_launch(c, launch_emit_keys(rec_sorted, offsets, n, g.tiles_x, tkeys, tvals, s), SS_K_BIN);
+        own_launch(c, launch_emit_keys(rec_sorted, offsets, n, g.tiles_x, tkeys, k16, tvals, s), SS_K_BIN);
         c->prof.bytes[SS_K_BIN] += 128.0 * (double)n + 8.0 * (double)I;
     }
     {
         Scope sc(c, SS_K_SORT);
         const uint32_t tbits = bits_for(g.tiles - 1);
         size_t tb = 0;
-        SS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, tkeys, tkeys_sorted, tvals, tranks, (int)I, 0,
-                                                (int)tbits, s));
-        void* tmp = c->cub_tmp.ensure(tb);
-        tb = c->cub_tmp.bytes;
-        SS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, tkeys, tkeys_sorted, tvals, tranks, (int)I, 0, (int)tbits,
-                                                s));
+        if (k16) {
+            auto* kin = static_cast<uint16_t*>(tkeys);
+            auto* kout = static_cast<uint16_t*>(tkeys_sorted);
+            SS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, tvals, tranks, (int)I, 0, (int)tbits, s));
+            void* tmp = c->cub_tmp.ensure(tb);
+            tb = c->cub_tmp.bytes;
+            SS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, kin, kout, tvals, tranks, (int)I, 0, (int)tbits, s));
+        } else {
+            auto* kin = static_cast<uint32_t*>(tkeys);
+            auto* kout = static_cast<uint32_t*>(tkeys_sorted);
+            SS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, tvals, tranks, (int)I, 0, (int)tbits, s));
+            void* tmp = c->cub_tmp.ensure(tb);
+            tb = c->cub_tmp.bytes;
+            SS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, kin, kout, tvals, tranks, (int)I, 0, (int)tbits, s));
+        }
         c->launches_cub += 1;
         c->prof.launches[SS_K_SORT] += 1;
         c->prof.bytes[SS_K_SORT] += 16.0 * (double)I;
     }
     {
         Scope sc(c, SS_K_BIN);
-        own_launch(c, launch_tile_ranges(tkeys_sorted, I, tstart, tend, s), SS_K_BIN);
+        own_launch(c, launch_tile_ranges(tkeys_sorted, k16, I, tstart, tend, s), SS_K_BIN);
         c->prof.bytes[SS_K_BIN] += 4.0 * (double)I + 8.0 * g.tiles;
     }
     c->cnt_vis += n;
@@ -551,7 +566,7 @@ void ss_destroy(ss_ctx* c) {
     ss::DevBuf* bufs[] = {&c->mean_op, &c->scale, &c->quat, &c->rec, &c->keys, &c->flags, &c->keys_sel, &c->ids_sel,
                           &c->keys_sorted, &c->order, &c->rec_sorted, &c->ntiles, &c->offsets, &c->tile_keys,
                           &c->tile_vals, &c->tile_keys_sorted, &c->tile_ranks, &c->tile_start, &c->tile_end,
-                          &c->cub_tmp, &c->num_sel, &c->info, &c->pix_bits, &c->mask_bits, &c->runs,
+                          &c->cub_tmp, &c->num_sel, &c->k32, &c->k32_sorted, &c->info, &c->pix_bits, &c->mask_bits, &c->runs,
                           &c->run_offsets, &c->clip, &c->spans, &c->pix_count, &c->pix_offset, &c->entries,
                           &c->per_pixel_total, &c->alpha, &c->acc, &c->touched, &c->touched_list, &c->counters,
                           &c->sums_buf, &c->totals_buf, &c->store_rows, &c->store_ids, &c->qbuf, &c->qnorm,

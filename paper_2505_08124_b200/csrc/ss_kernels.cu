@@ -93,26 +93,63 @@ __global__ void gather_kernel(const uint32_t* order, uint64_t n, const SplatRec*
     ntiles[r] = (x1 / kTile - x0 / kTile + 1) * (y1 / kTile - y0 / kTile + 1);
 }
 
+template <typename K>
 __global__ void emit_keys_kernel(const SplatRec* rec_sorted, const uint32_t* offsets, uint64_t n, uint32_t tiles_x,
-                                 uint32_t* keys, uint32_t* vals) {
+                                 K* keys, uint32_t* vals) {
     const uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
-    const SplatRec& s = rec_sorted[r];
+    const uint4 w3 = reinterpret_cast<const uint4*>(rec_sorted + r)[3];
+    const uint32_t x0 = w3.x & 0xffffu, x1 = w3.x >> 16, y0 = w3.y & 0xffffu, y1 = w3.y >> 16;
     uint32_t o = offsets[r];
-    for (uint32_t ty = s.y0 / kTile; ty <= (uint32_t)s.y1 / kTile; ++ty)
-        for (uint32_t tx = s.x0 / kTile; tx <= (uint32_t)s.x1 / kTile; ++tx) {
-            keys[o] = ty * tiles_x + tx;
+    for (uint32_t ty = y0 / kTile; ty <= y1 / kTile; ++ty)
+        for (uint32_t tx = x0 / kTile; tx <= x1 / kTile; ++tx) {
+            keys[o] = (K)(ty * tiles_x + tx);
             vals[o] = (uint32_t)r;
             ++o;
         }
 }
 
-__global__ void tile_ranges_kernel(const uint32_t* keys, uint64_t n, uint32_t* start, uint32_t* end) {
+template <typename K>
+__global__ void tile_ranges_kernel(const K* keys, uint64_t n, uint32_t* start, uint32_t* end) {
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t k = keys[i];
     if (i == 0 || keys[i - 1] != k) start[k] = (uint32_t)i;
     if (i == n - 1 || keys[i + 1] != k) end[k] = (uint32_t)(i + 1);
+}
+
+// Depth keys narrowed to 32 bits: (bits - min) >> shift is monotone in the
+// f64 depth, so a stable sort on it orders by (key32, id); the fixup below
+// restores the exact (depth, id) order inside runs of equal key32
+// (projection.hpp:59-64).
+__global__ void narrow_keys_kernel(const unsigned long long* keys, uint64_t n, unsigned long long kmin,
+                                   uint32_t shift, uint32_t* k32) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) k32[i] = (uint32_t)((keys[i] - kmin) >> shift);
+}
+
+__global__ void tie_fixup_kernel(const uint32_t* k32, uint64_t n, const unsigned long long* full_by_id,
+                                 uint32_t* order) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i + 1 >= n) return;
+    if (i > 0 && k32[i - 1] == k32[i]) return; // not a run start
+    if (k32[i + 1] != k32[i]) return;          // singleton
+    uint64_t e = i + 2;
+    while (e < n && k32[e] == k32[i]) ++e;
+    // insertion sort of order[i, e) by (full depth bits, id); runs are short
+    for (uint64_t a = i + 1; a < e; ++a) {
+        const uint32_t id = order[a];
+        const unsigned long long key = full_by_id[id];
+        uint64_t b = a;
+        while (b > i) {
+            const uint32_t pid = order[b - 1];
+            const unsigned long long pk = full_by_id[pid];
+            if (pk < key || (pk == key && pid < id)) break;
+            order[b] = pid;
+            --b;
+        }
+        order[b] = id;
+    }
 }
 
 // --------------------------------------------------------- contraction
@@ -409,14 +446,37 @@ cudaError_t launch_gather(const uint32_t* order, uint64_t n, const SplatRec* rec
     return cudaGetLastError();
 }
 cudaError_t launch_emit_keys(const SplatRec* rec_sorted, const uint32_t* offsets, uint64_t n, uint32_t tiles_x,
-                             uint32_t* keys, uint32_t* vals, cudaStream_t s) {
+                             void* keys, bool keys16, uint32_t* vals, cudaStream_t s) {
     if (!n) return cudaSuccess;
-    emit_keys_kernel<<<blocks_for(n, 256), 256, 0, s>>>(rec_sorted, offsets, n, tiles_x, keys, vals);
+    if (keys16)
+        emit_keys_kernel<uint16_t><<<blocks_for(n, 256), 256, 0, s>>>(rec_sorted, offsets, n, tiles_x,
+                                                                      static_cast<uint16_t*>(keys), vals);
+    else
+        emit_keys_kernel<uint32_t><<<blocks_for(n, 256), 256, 0, s>>>(rec_sorted, offsets, n, tiles_x,
+                                                                      static_cast<uint32_t*>(keys), vals);
     return cudaGetLastError();
 }
-cudaError_t launch_tile_ranges(const uint32_t* keys, uint64_t n, uint32_t* start, uint32_t* end, cudaStream_t s) {
+cudaError_t launch_tile_ranges(const void* keys, bool keys16, uint64_t n, uint32_t* start, uint32_t* end,
+                               cudaStream_t s) {
     if (!n) return cudaSuccess;
-    tile_ranges_kernel<<<blocks_for(n, 256), 256, 0, s>>>(keys, n, start, end);
+    if (keys16)
+        tile_ranges_kernel<uint16_t><<<blocks_for(n, 256), 256, 0, s>>>(static_cast<const uint16_t*>(keys), n, start,
+                                                                        end);
+    else
+        tile_ranges_kernel<uint32_t><<<blocks_for(n, 256), 256, 0, s>>>(static_cast<const uint32_t*>(keys), n, start,
+                                                                        end);
+    return cudaGetLastError();
+}
+cudaError_t launch_narrow_keys(const unsigned long long* keys, uint64_t n, unsigned long long kmin, uint32_t shift,
+                               uint32_t* k32, cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    narrow_keys_kernel<<<blocks_for(n, 256), 256, 0, s>>>(keys, n, kmin, shift, k32);
+    return cudaGetLastError();
+}
+cudaError_t launch_tie_fixup(const uint32_t* k32, uint64_t n, const unsigned long long* full_by_id, uint32_t* order,
+                             cudaStream_t s) {
+    if (n < 2) return cudaSuccess;
+    tie_fixup_kernel<<<blocks_for(n, 256), 256, 0, s>>>(k32, n, full_by_id, order);
     return cudaGetLastError();
 }
 cudaError_t launch_contract(const ContractParams& p, uint64_t max_touched, cudaStream_t s) {

@@ -26,8 +26,13 @@ cudaError_t launch_resample_bits(const uint32_t* src, uint32_t sw, uint32_t sh, 
 cudaError_t launch_gather(const uint32_t* order, uint64_t n, const SplatRec* rec, SplatRec* rec_sorted,
                           uint32_t* ntiles, cudaStream_t s);
 cudaError_t launch_emit_keys(const SplatRec* rec_sorted, const uint32_t* offsets, uint64_t n, uint32_t tiles_x,
-                             uint32_t* keys, uint32_t* vals, cudaStream_t s);
-cudaError_t launch_tile_ranges(const uint32_t* keys, uint64_t n, uint32_t* start, uint32_t* end, cudaStream_t s);
+                             void* keys, bool keys16, uint32_t* vals, cudaStream_t s);
+cudaError_t launch_tile_ranges(const void* keys, bool keys16, uint64_t n, uint32_t* start, uint32_t* end,
+                               cudaStream_t s);
+cudaError_t launch_narrow_keys(const unsigned long long* keys, uint64_t n, unsigned long long kmin, uint32_t shift,
+                               uint32_t* k32, cudaStream_t s);
+cudaError_t launch_tie_fixup(const uint32_t* k32, uint64_t n, const unsigned long long* full_by_id, uint32_t* order,
+                             cudaStream_t s);
 cudaError_t launch_contract(const ContractParams& p, uint64_t max_touched, cudaStream_t s);
 cudaError_t launch_normalize(const float* sums, const float* totals, uint64_t n, uint32_t dim, float* rows,
                              float* coverage, cudaStream_t s);

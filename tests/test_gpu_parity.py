@@ -103,6 +103,23 @@ def test_depth_ties_break_by_id(gpu_ctx, oracle):
     _assert_capture_equal(got, oracle.rasterize(s, cam))
 
 
+def test_depth_order_exact_with_coarse_narrowed_keys(gpu_ctx, oracle):
+    """A far outlier widens the depth range so the 32-bit narrowed sort keys
+    collide across thousands of near-equal depths: the tie fixup must restore
+    the exact (depth, id) order."""
+    rng = np.random.default_rng(4)
+    n = 3000
+    mean = np.zeros((n, 3), np.float32)
+    mean[:, 0] = rng.uniform(-1, 1, n)
+    mean[:, 1] = rng.uniform(-1, 1, n)
+    mean[:, 2] = (8.0 + rng.uniform(0, 1e-5, n)).astype(np.float32)
+    mean[0] = [0.0, 0.0, 1.0e5]
+    s = scene_ns(mean, np.full((n, 3), 0.05), np.tile([0, 0, 0, 1.0], (n, 1)), rng.uniform(0.1, 0.6, n))
+    cam = plain_camera(40.0, 40.0, 24.0, 24.0, 48, 48)
+    got = _capture(gpu_ctx, s, cam)
+    _assert_capture_equal(got, oracle.rasterize(s, cam))
+
+
 def test_empty_and_culled_scenes(gpu_ctx, oracle):
     cam = plain_camera(50, 50, 16, 16, 32, 32)
     behind = scene_ns([[0, 0, -1], [0, 0, 0.005]], [[0.1] * 3] * 2, [[0, 0, 0, 1]] * 2, [0.5, 0.5])
