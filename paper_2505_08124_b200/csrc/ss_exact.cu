@@ -221,9 +221,8 @@ __global__ void __launch_bounds__(256) project_kernel(ProjectParams p) {
 //         warp, bitset group) costs one atomic per mask, never a 512-d scatter.
 template <int KIND, bool FALLOFF, int MW>
 __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) {
-    __shared__ SplatRec srec[kRasterThreads];
+    __shared__ SplatRec srec[kRasterThreads]; // warp w stages its hits in srec[32w, 32w+32)
     __shared__ uint32_t srank[kRasterThreads];
-    __shared__ uint2 sbox[kRasterThreads]; // x0|x1<<16, y0|y1<<16 (conflict-free ballot reads)
     __shared__ unsigned long long stab[256];
     stab[threadIdx.x] = kExpTab[threadIdx.x];
 
@@ -239,6 +238,8 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
     const uint32_t pixel = py * p.width + px;
     const uint32_t start = p.tile_start[tile], end = p.tile_end[tile];
     const double dpx = (double)(int32_t)px, dpy = (double)(int32_t)py;
+    SplatRec* wrec = srec + 32u * warp;
+    uint32_t* wrank = srank + 32u * warp;
 
     double T = 1.0;
     double total = 0.0;
@@ -268,49 +269,38 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
         }
         done = done || !any_bits; // unmasked pixels contribute nothing
     }
-    __syncthreads();
+    __syncthreads(); // exp table staged
 
-    for (uint32_t base = start; base < end; base += kRasterThreads) {
-        if (__syncthreads_and(done)) break;
-        const uint32_t i = base + threadIdx.x;
+    // Each warp walks the tile's list independently, 32 splats at a time: one
+    // ballot culls the splats whose box misses the warp's 8x4 block, the hits
+    // are staged in the warp's smem slice, and the warp stops once all of its
+    // pixels have terminated.
+    for (uint32_t base = start; base < end; base += 32u) {
+        if (__all_sync(0xffffffffu, done)) break;
+        const uint32_t i = base + lane;
+        uint32_t r = 0;
+        bool hit = false;
         if (i < end) {
-            const uint32_t r = p.tile_ranks[i];
-            srank[threadIdx.x] = r;
+            r = __ldg(p.tile_ranks + i);
+            const uint2 box = __ldg(reinterpret_cast<const uint2*>(&p.rec_sorted[r].x0));
+            hit = !((box.x >> 16) < bx0 || (box.x & 0xffffu) > bx1 || (box.y >> 16) < by0 || (box.y & 0xffffu) > by1);
+        }
+        uint32_t cand = __ballot_sync(0xffffffffu, hit);
+        if (hit) {
+            const uint32_t slot = __popc(cand & ((1u << lane) - 1u));
             const uint4* src = reinterpret_cast<const uint4*>(p.rec_sorted + r);
-            uint4* dst = reinterpret_cast<uint4*>(srec + threadIdx.x);
+            uint4* dst = reinterpret_cast<uint4*>(wrec + slot);
             dst[0] = __ldg(src);
             dst[1] = __ldg(src + 1);
             dst[2] = __ldg(src + 2);
-            const uint4 w3 = __ldg(src + 3);
-            dst[3] = w3;
-            sbox[threadIdx.x] = make_uint2(w3.x, w3.y);
+            dst[3] = __ldg(src + 3);
+            wrank[slot] = r;
         }
-        __syncthreads();
-        const uint32_t nb = min((uint32_t)kRasterThreads, end - base);
-        // per-warp candidate set: splats of the batch whose box meets this warp's 8x4 block
-        uint32_t cand[kRasterThreads / 32];
-#pragma unroll
-        for (int q = 0; q < kRasterThreads / 32; ++q) {
-            const uint32_t k = (uint32_t)q * 32u + lane;
-            bool hit = false;
-            if (k < nb) {
-                const uint2 box = sbox[k];
-                hit = !((box.x >> 16) < bx0 || (box.x & 0xffffu) > bx1 || (box.y >> 16) < by0 ||
-                        (box.y & 0xffffu) > by1);
-            }
-            cand[q] = __ballot_sync(0xffffffffu, hit);
-        }
-        if (__all_sync(0xffffffffu, done)) {
-#pragma unroll
-            for (int q = 0; q < kRasterThreads / 32; ++q) cand[q] = 0u;
-        }
-#pragma unroll
-        for (int q = 0; q < kRasterThreads / 32; ++q)
-        while (cand[q]) {
-            const uint32_t j = (uint32_t)q * 32u + (uint32_t)(__ffs(cand[q]) - 1);
-            cand[q] &= cand[q] - 1u;
-            const SplatRec& s = srec[j];
-            const uint2 box = sbox[j];
+        __syncwarp();
+        const uint32_t nh = __popc(cand);
+        for (uint32_t j = 0; j < nh; ++j) {
+            const SplatRec& s = wrec[j];
+            const uint2 box = *reinterpret_cast<const uint2*>(&s.x0);
             const uint32_t sx0 = box.x & 0xffffu, sx1 = box.x >> 16, sy0 = box.y & 0xffffu, sy1 = box.y >> 16;
             bool contrib = false;
             float wf = 0.0f;
@@ -349,7 +339,7 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
             } else {
                 const uint32_t em = __ballot_sync(0xffffffffu, contrib);
                 if (em) {
-                    const uint32_t rank = srank[j];
+                    const uint32_t rank = wrank[j];
                     uint32_t rem = em;
                     while (rem) {
                         const int leader = __ffs(rem) - 1;
@@ -357,17 +347,13 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
                         float v = (contrib && ((gm >> lane) & 1u)) ? wf : 0.0f;
 #pragma unroll
                         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                        if ((int)lane == leader) {
-                            float* row = p.acc + (size_t)rank * p.n_masks;
+                        // every lane holds the (bit-identical) group sum after the xor
+                        // butterfly; lane m adds it to mask 32w+m when the group has that bit
+                        float* row = p.acc + (size_t)rank * p.n_masks + lane;
 #pragma unroll
-                            for (int w = 0; w < MW; ++w) {
-                                uint32_t b = bits[w];
-                                while (b) {
-                                    const int m = __ffs(b) - 1;
-                                    b &= b - 1;
-                                    atomicAdd(row + w * 32 + m, v);
-                                }
-                            }
+                        for (int w = 0; w < MW; ++w) {
+                            const uint32_t gb = __shfl_sync(0xffffffffu, bits[w], leader);
+                            if ((gb >> lane) & 1u) atomicAdd(row + w * 32, v);
                         }
                         rem &= ~gm;
                     }
@@ -380,13 +366,13 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
                         }
                     }
                 }
+                if (__all_sync(0xffffffffu, done)) break;
             }
-            if (__all_sync(0xffffffffu, done)) {
-#pragma unroll
-                for (int r2 = 0; r2 < kRasterThreads / 32; ++r2) cand[r2] = 0u;
+            if constexpr (KIND != 2) {
+                if (__all_sync(0xffffffffu, done)) break;
             }
         }
-        __syncthreads();
+        __syncwarp();
     }
     if constexpr (KIND == 0) {
         if (inside) p.pix_count[pixel] = count;
