@@ -108,6 +108,39 @@ struct ProfState {
     }
 };
 
+// Per-view scratch + stream of one pipeline lane.  Consecutive views
+// alternate between two lanes so one view's sorts and host handshakes overlap
+// the previous view's compositor; the contraction into the shared N x D sums
+// stays in view order through an event chain.
+struct Lane {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t contract_done = nullptr, done = nullptr;
+    DevBuf rec, keys, flags, keys_sel, ids_sel, keys_sorted, order, rec_sorted, ntiles, offsets;
+    DevBuf tile_keys, tile_vals, tile_keys_sorted, tile_ranks, tile_start, tile_end;
+    DevBuf cub_tmp, num_sel, k32, k32_sorted, info;
+    DevBuf pix_bits, mask_bits, runs, run_offsets, clip, spans;
+    DevBuf acc, touched, touched_list;
+    uint64_t acc_elems = 0;        // zero-initialised elements of acc
+    ViewInfo* h_info = nullptr;    // pinned
+    uint32_t* h_u32 = nullptr;     // pinned scratch
+    void release_all() {
+        DevBuf* b[] = {&rec, &keys, &flags, &keys_sel, &ids_sel, &keys_sorted, &order, &rec_sorted, &ntiles, &offsets,
+                       &tile_keys, &tile_vals, &tile_keys_sorted, &tile_ranks, &tile_start, &tile_end, &cub_tmp,
+                       &num_sel, &k32, &k32_sorted, &info, &pix_bits, &mask_bits, &runs, &run_offsets, &clip, &spans,
+                       &acc, &touched, &touched_list};
+        for (auto* x : b) x->release();
+        if (h_info) cudaFreeHost(h_info);
+        if (h_u32) cudaFreeHost(h_u32);
+        if (contract_done) cudaEventDestroy(contract_done);
+        if (done) cudaEventDestroy(done);
+        if (stream) cudaStreamDestroy(stream);
+        h_info = nullptr;
+        h_u32 = nullptr;
+        contract_done = done = nullptr;
+        stream = nullptr;
+    }
+};
+
 } // namespace
 } // namespace ss
 
@@ -120,25 +153,19 @@ struct ss_ctx {
     uint64_t n = 0;
     ss::DevBuf mean_op, scale, quat;
 
-    // per-view geometry scratch
-    ss::DevBuf rec, keys, flags, keys_sel, ids_sel, keys_sorted, order, rec_sorted, ntiles, offsets;
-    ss::DevBuf tile_keys, tile_vals, tile_keys_sorted, tile_ranks, tile_start, tile_end;
-    ss::DevBuf cub_tmp, num_sel, k32, k32_sorted;
-    ss::DevBuf info;
-    ss::ViewInfo* h_info = nullptr; // pinned
-    ss::ViewInfo* h_init = nullptr; // pinned
-    uint32_t* h_u32 = nullptr;      // pinned scratch
+    // per-view pipeline lanes (scratch + stream each)
+    ss::Lane lanes[2];
+    uint32_t next_lane = 0;
+    cudaEvent_t ev_user = nullptr;
+    ss::DevBuf cub_tmp, num_sel, info; // store / query scratch
+    ss::ViewInfo* h_init = nullptr;    // pinned
+    uint32_t* h_u32 = nullptr;         // pinned scratch
 
-    // masks
-    ss::DevBuf pix_bits, mask_bits, runs, run_offsets, clip, spans;
     // capture
     ss::DevBuf pix_count, pix_offset, entries, per_pixel_total, alpha;
     uint64_t cap_entries = 0, cap_splats = 0, cap_instances = 0;
     uint32_t cap_width = 0, cap_height = 0, cap_tiles = 0;
-    // fused path
-    ss::DevBuf acc, touched, touched_list;
-    uint64_t acc_elems = 0; // zero-initialised elements of acc
-    ss::DevBuf counters;    // [0] G_v sum, [1] K_v sum
+    ss::DevBuf counters; // [0] G_v sum, [1] K_v sum
     // accumulators
     uint32_t dim = 0;
     float* sums = nullptr;
@@ -162,18 +189,19 @@ namespace {
 
 struct Scope {
     ss_ctx* c;
+    cudaStream_t st;
     int cls;
     cudaEvent_t a = nullptr, b = nullptr;
-    Scope(ss_ctx* ctx, int k) : c(ctx), cls(k) {
+    Scope(ss_ctx* ctx, cudaStream_t stream, int k) : c(ctx), st(stream), cls(k) {
         if (c->prof.on) {
             a = c->prof.get();
             b = c->prof.get();
-            SS_CUDA(cudaEventRecord(a, c->stream));
+            SS_CUDA(cudaEventRecord(a, st));
         }
     }
     ~Scope() {
         if (c->prof.on && a) {
-            cudaEventRecord(b, c->stream);
+            cudaEventRecord(b, st);
             c->prof.pending.push_back({cls, {a, b}});
         }
     }
@@ -187,13 +215,13 @@ inline void own_launch(ss_ctx* c, cudaError_t e, int cls, uint64_t count = 1) {
 
 void set_device(ss_ctx* c) { SS_CUDA(cudaSetDevice(c->device)); }
 
-void reset_info(ss_ctx* c) {
-    SS_CUDA(cudaMemcpyAsync(c->info.p, c->h_init, sizeof(ViewInfo), cudaMemcpyHostToDevice, c->stream));
+void reset_info(ss_ctx* c, Lane& L, cudaStream_t s) {
+    SS_CUDA(cudaMemcpyAsync(L.info.p, c->h_init, sizeof(ViewInfo), cudaMemcpyHostToDevice, s));
 }
 
-void sync_info(ss_ctx* c) {
-    SS_CUDA(cudaMemcpyAsync(c->h_info, c->info.p, sizeof(ViewInfo), cudaMemcpyDeviceToHost, c->stream));
-    SS_CUDA(cudaStreamSynchronize(c->stream));
+void sync_info(Lane& L, cudaStream_t s) {
+    SS_CUDA(cudaMemcpyAsync(L.h_info, L.info.p, sizeof(ViewInfo), cudaMemcpyDeviceToHost, s));
+    SS_CUDA(cudaStreamSynchronize(s));
 }
 
 uint32_t bits_for(uint64_t v) { // number of bits to represent v (v >= 1 -> >= 1)
@@ -216,32 +244,32 @@ struct Geometry {
 };
 
 // project -> ordered compaction -> depth sort -> gather -> tile keys -> tile sort -> ranges
-Geometry run_geometry(ss_ctx* c, const ss_camera& cam, int err_kind, const char* err_prefix) {
+Geometry run_geometry(ss_ctx* c, Lane& L, cudaStream_t s, const ss_camera& cam, int err_kind,
+                      const char* err_prefix) {
     Geometry g;
     const uint64_t N = c->n;
     g.tiles_x = (cam.width + kTile - 1) / kTile;
     g.tiles_y = (cam.height + kTile - 1) / kTile;
     g.tiles = g.tiles_x * g.tiles_y;
-    cudaStream_t s = c->stream;
 
-    auto* rec = static_cast<SplatRec*>(c->rec.ensure(std::max<uint64_t>(N, 1) * sizeof(SplatRec)));
-    auto* keys = static_cast<unsigned long long*>(c->keys.ensure(std::max<uint64_t>(N, 1) * 8));
-    auto* flags = static_cast<uint8_t*>(c->flags.ensure(std::max<uint64_t>(N, 1)));
-    auto* keys_sel = static_cast<unsigned long long*>(c->keys_sel.ensure(std::max<uint64_t>(N, 1) * 8));
-    auto* ids_sel = static_cast<uint32_t*>(c->ids_sel.ensure(std::max<uint64_t>(N, 1) * 4));
-    auto* keys_sorted = static_cast<unsigned long long*>(c->keys_sorted.ensure(std::max<uint64_t>(N, 1) * 8));
-    auto* order = static_cast<uint32_t*>(c->order.ensure(std::max<uint64_t>(N, 1) * 4));
-    auto* rec_sorted = static_cast<SplatRec*>(c->rec_sorted.ensure(std::max<uint64_t>(N, 1) * sizeof(SplatRec)));
-    auto* ntiles = static_cast<uint32_t*>(c->ntiles.ensure((N + 1) * 4));
-    auto* offsets = static_cast<uint32_t*>(c->offsets.ensure((N + 1) * 4));
-    auto* num_sel = static_cast<int*>(c->num_sel.ensure(16));
-    auto* tstart = static_cast<uint32_t*>(c->tile_start.ensure((size_t)g.tiles * 4));
-    auto* tend = static_cast<uint32_t*>(c->tile_end.ensure((size_t)g.tiles * 4));
-    ViewInfo* info = c->info.as<ViewInfo>();
+    auto* rec = static_cast<SplatRec*>(L.rec.ensure(std::max<uint64_t>(N, 1) * sizeof(SplatRec)));
+    auto* keys = static_cast<unsigned long long*>(L.keys.ensure(std::max<uint64_t>(N, 1) * 8));
+    auto* flags = static_cast<uint8_t*>(L.flags.ensure(std::max<uint64_t>(N, 1)));
+    auto* keys_sel = static_cast<unsigned long long*>(L.keys_sel.ensure(std::max<uint64_t>(N, 1) * 8));
+    auto* ids_sel = static_cast<uint32_t*>(L.ids_sel.ensure(std::max<uint64_t>(N, 1) * 4));
+    auto* keys_sorted = static_cast<unsigned long long*>(L.keys_sorted.ensure(std::max<uint64_t>(N, 1) * 8));
+    auto* order = static_cast<uint32_t*>(L.order.ensure(std::max<uint64_t>(N, 1) * 4));
+    auto* rec_sorted = static_cast<SplatRec*>(L.rec_sorted.ensure(std::max<uint64_t>(N, 1) * sizeof(SplatRec)));
+    auto* ntiles = static_cast<uint32_t*>(L.ntiles.ensure((N + 1) * 4));
+    auto* offsets = static_cast<uint32_t*>(L.offsets.ensure((N + 1) * 4));
+    auto* num_sel = static_cast<int*>(L.num_sel.ensure(16));
+    auto* tstart = static_cast<uint32_t*>(L.tile_start.ensure((size_t)g.tiles * 4));
+    auto* tend = static_cast<uint32_t*>(L.tile_end.ensure((size_t)g.tiles * 4));
+    ViewInfo* info = L.info.as<ViewInfo>();
 
-    reset_info(c);
+    reset_info(c, L, s);
     {
-        Scope sc(c, SS_K_PROJECT);
+        Scope sc(c, s, SS_K_PROJECT);
         ProjectParams p;
         p.mean_op = c->mean_op.as<float4>();
         p.scale = c->scale.as<float4>();
@@ -259,19 +287,19 @@ Geometry run_geometry(ss_ctx* c, const ss_camera& cam, int err_kind, const char*
         cub::CountingInputIterator<uint32_t> ids(0);
         SS_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, keys, flags, keys_sel, num_sel, (int)N, s));
         SS_CUDA(cub::DeviceSelect::Flagged(nullptr, tb2, ids, flags, ids_sel, num_sel + 1, (int)N, s));
-        void* tmp = c->cub_tmp.ensure(std::max(tb, tb2));
-        tb = c->cub_tmp.bytes;
+        void* tmp = L.cub_tmp.ensure(std::max(tb, tb2));
+        tb = L.cub_tmp.bytes;
         SS_CUDA(cub::DeviceSelect::Flagged(tmp, tb, keys, flags, keys_sel, num_sel, (int)N, s));
         SS_CUDA(cub::DeviceSelect::Flagged(tmp, tb, ids, flags, ids_sel, num_sel + 1, (int)N, s));
         c->launches_cub += 4;
         c->prof.launches[SS_K_PROJECT] += 4;
         c->prof.bytes[SS_K_PROJECT] += 44.0 * (double)N;
     }
-    sync_info(c);
-    if (c->h_info->err_count)
+    sync_info(L, s);
+    if (L.h_info->err_count)
         throw Error(err_kind, std::string(err_prefix) + "singular screen covariance for gaussian " +
-                                  std::to_string(c->h_info->err_gid));
-    g.n_surv = c->h_info->n_surv;
+                                  std::to_string(L.h_info->err_gid));
+    g.n_surv = L.h_info->n_surv;
     const uint64_t n = g.n_surv;
     c->prof.bytes[SS_K_PROJECT] += 76.0 * (double)n;
 
@@ -280,19 +308,19 @@ Geometry run_geometry(ss_ctx* c, const ss_camera& cam, int err_kind, const char*
     if (n == 0) return g;
 
     {
-        Scope sc(c, SS_K_SORT);
+        Scope sc(c, s, SS_K_SORT);
         // depth sort on 32-bit narrowed keys (stable => ties keep id order), then
         // an exact fixup of the rare runs that share a narrowed key
-        const uint32_t hb = bits_for(c->h_info->min_key ^ c->h_info->max_key);
+        const uint32_t hb = bits_for(L.h_info->min_key ^ L.h_info->max_key);
         const uint32_t shift = hb > 32 ? hb - 32 : 0;
         const uint32_t end_bit = std::max<uint32_t>(1, std::min<uint32_t>(hb, 32));
-        auto* k32 = static_cast<uint32_t*>(c->k32.ensure(std::max<uint64_t>(n, 1) * 4));
-        auto* k32s = static_cast<uint32_t*>(c->k32_sorted.ensure(std::max<uint64_t>(n, 1) * 4));
-        own_launch(c, launch_narrow_keys(keys_sel, n, c->h_info->min_key, shift, k32, s), SS_K_SORT);
+        auto* k32 = static_cast<uint32_t*>(L.k32.ensure(std::max<uint64_t>(n, 1) * 4));
+        auto* k32s = static_cast<uint32_t*>(L.k32_sorted.ensure(std::max<uint64_t>(n, 1) * 4));
+        own_launch(c, launch_narrow_keys(keys_sel, n, L.h_info->min_key, shift, k32, s), SS_K_SORT);
         size_t tb = 0;
         SS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k32, k32s, ids_sel, order, (int)n, 0, (int)end_bit, s));
-        void* tmp = c->cub_tmp.ensure(tb);
-        tb = c->cub_tmp.bytes;
+        void* tmp = L.cub_tmp.ensure(tb);
+        tb = L.cub_tmp.bytes;
         SS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k32, k32s, ids_sel, order, (int)n, 0, (int)end_bit, s));
         if (shift > 0) own_launch(c, launch_tie_fixup(k32s, n, keys, order, s), SS_K_SORT);
         (void)keys_sorted;
@@ -301,48 +329,48 @@ Geometry run_geometry(ss_ctx* c, const ss_camera& cam, int err_kind, const char*
         c->prof.bytes[SS_K_SORT] += 24.0 * (double)n;
     }
     {
-        Scope sc(c, SS_K_BIN);
+        Scope sc(c, s, SS_K_BIN);
         own_launch(c, launch_gather(order, n, rec, rec_sorted, ntiles, s), SS_K_BIN);
         SS_CUDA(cudaMemsetAsync(ntiles + n, 0, 4, s));
         size_t tb = 0;
         SS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, ntiles, offsets, (int)(n + 1), s));
-        void* tmp = c->cub_tmp.ensure(tb);
-        tb = c->cub_tmp.bytes;
+        void* tmp = L.cub_tmp.ensure(tb);
+        tb = L.cub_tmp.bytes;
         SS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, ntiles, offsets, (int)(n + 1), s));
         c->launches_cub += 1;
         c->prof.launches[SS_K_BIN] += 1;
-        SS_CUDA(cudaMemcpyAsync(c->h_u32, offsets + n, 4, cudaMemcpyDeviceToHost, s));
+        SS_CUDA(cudaMemcpyAsync(L.h_u32, offsets + n, 4, cudaMemcpyDeviceToHost, s));
         SS_CUDA(cudaStreamSynchronize(s));
     }
-    g.n_inst = c->h_u32[0];
+    g.n_inst = L.h_u32[0];
     const uint64_t I = g.n_inst;
     const bool k16 = g.tiles <= 65536u;
-    void* tkeys = c->tile_keys.ensure(std::max<uint64_t>(I, 1) * 4);
-    auto* tvals = static_cast<uint32_t*>(c->tile_vals.ensure(std::max<uint64_t>(I, 1) * 4));
-    void* tkeys_sorted = c->tile_keys_sorted.ensure(std::max<uint64_t>(I, 1) * 4);
-    auto* tranks = static_cast<uint32_t*>(c->tile_ranks.ensure(std::max<uint64_t>(I, 1) * 4));
+    void* tkeys = L.tile_keys.ensure(std::max<uint64_t>(I, 1) * 4);
+    auto* tvals = static_cast<uint32_t*>(L.tile_vals.ensure(std::max<uint64_t>(I, 1) * 4));
+    void* tkeys_sorted = L.tile_keys_sorted.ensure(std::max<uint64_t>(I, 1) * 4);
+    auto* tranks = static_cast<uint32_t*>(L.tile_ranks.ensure(std::max<uint64_t>(I, 1) * 4));
     {
-        Scope sc(c, SS_K_BIN);
+        Scope sc(c, s, SS_K_BIN);
         own_launch(c, launch_emit_keys(rec_sorted, offsets, n, g.tiles_x, tkeys, k16, tvals, s), SS_K_BIN);
         c->prof.bytes[SS_K_BIN] += 128.0 * (double)n + 8.0 * (double)I;
     }
     {
-        Scope sc(c, SS_K_SORT);
+        Scope sc(c, s, SS_K_SORT);
         const uint32_t tbits = bits_for(g.tiles - 1);
         size_t tb = 0;
         if (k16) {
             auto* kin = static_cast<uint16_t*>(tkeys);
             auto* kout = static_cast<uint16_t*>(tkeys_sorted);
             SS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, tvals, tranks, (int)I, 0, (int)tbits, s));
-            void* tmp = c->cub_tmp.ensure(tb);
-            tb = c->cub_tmp.bytes;
+            void* tmp = L.cub_tmp.ensure(tb);
+            tb = L.cub_tmp.bytes;
             SS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, kin, kout, tvals, tranks, (int)I, 0, (int)tbits, s));
         } else {
             auto* kin = static_cast<uint32_t*>(tkeys);
             auto* kout = static_cast<uint32_t*>(tkeys_sorted);
             SS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, tvals, tranks, (int)I, 0, (int)tbits, s));
-            void* tmp = c->cub_tmp.ensure(tb);
-            tb = c->cub_tmp.bytes;
+            void* tmp = L.cub_tmp.ensure(tb);
+            tb = L.cub_tmp.bytes;
             SS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, kin, kout, tvals, tranks, (int)I, 0, (int)tbits, s));
         }
         c->launches_cub += 1;
@@ -350,7 +378,7 @@ Geometry run_geometry(ss_ctx* c, const ss_camera& cam, int err_kind, const char*
         c->prof.bytes[SS_K_SORT] += 16.0 * (double)I;
     }
     {
-        Scope sc(c, SS_K_BIN);
+        Scope sc(c, s, SS_K_BIN);
         own_launch(c, launch_tile_ranges(tkeys_sorted, k16, I, tstart, tend, s), SS_K_BIN);
         c->prof.bytes[SS_K_BIN] += 4.0 * (double)I + 8.0 * g.tiles;
     }
@@ -359,29 +387,29 @@ Geometry run_geometry(ss_ctx* c, const ss_camera& cam, int err_kind, const char*
     return g;
 }
 
-RasterParams raster_params(ss_ctx* c, const ss_camera& cam, const Geometry& g) {
+RasterParams raster_params(Lane& L, const ss_camera& cam, const Geometry& g) {
     RasterParams p;
     std::memset(&p, 0, sizeof(p));
-    p.rec_sorted = c->rec_sorted.as<SplatRec>();
-    p.tile_ranks = c->tile_ranks.as<uint32_t>();
-    p.tile_start = c->tile_start.as<uint32_t>();
-    p.tile_end = c->tile_end.as<uint32_t>();
+    p.rec_sorted = L.rec_sorted.as<SplatRec>();
+    p.tile_ranks = L.tile_ranks.as<uint32_t>();
+    p.tile_start = L.tile_start.as<uint32_t>();
+    p.tile_end = L.tile_end.as<uint32_t>();
     p.width = cam.width;
     p.height = cam.height;
     p.tiles_x = g.tiles_x;
-    p.info = c->info.as<ViewInfo>();
+    p.info = L.info.as<ViewInfo>();
     return p;
 }
 
 uint32_t mask_words_for(uint32_t m) { return m <= 32 ? 1 : (m <= 64 ? 2 : 4); }
 
 // Upload one view's RLE masks + CLIP and build the raster-resolution bitsets.
-void build_mask_bits(ss_ctx* c, const ss_camera& cam, const ss_view_masks* vm, uint32_t words, uint32_t image_id) {
-    cudaStream_t s = c->stream;
+void build_mask_bits(ss_ctx* c, Lane& L, cudaStream_t s, const ss_camera& cam, const ss_view_masks* vm,
+                     uint32_t words, uint32_t image_id) {
     const uint32_t M = vm->n_masks;
     const uint64_t P = (uint64_t)cam.width * cam.height;
-    auto* pb = static_cast<uint32_t*>(c->pix_bits.ensure(P * words * 4));
-    Scope sc(c, SS_K_MASKS);
+    auto* pb = static_cast<uint32_t*>(L.pix_bits.ensure(P * words * 4));
+    Scope sc(c, s, SS_K_MASKS);
     SS_CUDA(cudaMemsetAsync(pb, 0, P * words * 4, s));
     if (M == 0) return;
     const uint64_t mw = vm->mask_width, mh = vm->mask_height;
@@ -405,11 +433,11 @@ void build_mask_bits(ss_ctx* c, const ss_camera& cam, const ss_view_masks* vm, u
                                                ": mask RLE length mismatch: runs cover " + std::to_string(tot) +
                                                " of " + std::to_string(mw * mh) + " pixels");
         }
-        auto* hr = static_cast<uint32_t*>(c->runs.ensure(std::max<uint64_t>(nr, 1) * 4));
-        auto* ho = static_cast<uint64_t*>(c->run_offsets.ensure((M + 1) * 8ull));
+        auto* hr = static_cast<uint32_t*>(L.runs.ensure(std::max<uint64_t>(nr, 1) * 4));
+        auto* ho = static_cast<uint64_t*>(L.run_offsets.ensure((M + 1) * 8ull));
         std::vector<uint64_t> rel(M + 1);
         for (uint32_t m = 0; m <= M; ++m) rel[m] = vm->run_offsets[m] - vm->run_offsets[0];
-        Scope h(c, SS_K_H2D);
+        Scope h(c, s, SS_K_H2D);
         SS_CUDA(cudaMemcpyAsync(hr, vm->runs + vm->run_offsets[0], nr * 4, cudaMemcpyHostToDevice, s));
         // pageable source: staged synchronously, so `rel` may go out of scope after the call
         SS_CUDA(cudaMemcpyAsync(ho, rel.data(), (M + 1) * 8ull, cudaMemcpyHostToDevice, s));
@@ -420,13 +448,13 @@ void build_mask_bits(ss_ctx* c, const ss_camera& cam, const ss_view_masks* vm, u
     const bool same = mw == cam.width && mh == cam.height;
     uint32_t* target = pb;
     if (!same) {
-        target = static_cast<uint32_t*>(c->mask_bits.ensure(mw * mh * words * 4));
+        target = static_cast<uint32_t*>(L.mask_bits.ensure(mw * mh * words * 4));
         SS_CUDA(cudaMemsetAsync(target, 0, mw * mh * words * 4, s));
     }
     // spans: at most one per run; the run count is bounded by the RLE stream length
     const uint64_t max_spans = ((vm->flags & SS_MASKS_ON_DEVICE) ? vm->n_runs : nr) / 2 + M;
-    auto* spans = static_cast<uint4*>(c->spans.ensure(std::max<uint64_t>(max_spans, 1) * 16 + 16));
-    auto* n_spans = reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(c->spans.p) + c->spans.bytes - 16);
+    auto* spans = static_cast<uint4*>(L.spans.ensure(std::max<uint64_t>(max_spans, 1) * 16 + 16));
+    auto* n_spans = reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(L.spans.p) + L.spans.bytes - 16);
     own_launch(c, launch_rle_to_bits(d_runs, d_off, M, words, target, spans, n_spans, s), SS_K_MASKS, 2);
     if (!same)
         own_launch(c, launch_resample_bits(target, (uint32_t)mw, (uint32_t)mh, pb, cam.width, cam.height, words, s),
@@ -434,7 +462,7 @@ void build_mask_bits(ss_ctx* c, const ss_camera& cam, const ss_view_masks* vm, u
     c->prof.bytes[SS_K_MASKS] += nr * 4.0 + (double)P * ((M + 7) / 8);
 }
 
-void encode_one(ss_ctx* c, const ss_camera& cam, const ss_view_masks* vm, int mode) {
+void encode_one(ss_ctx* c, Lane& L, Lane& prev, const ss_camera& cam, const ss_view_masks* vm, int mode) {
     check_camera(&cam);
     if (!c->sums) throw Error(SS_ERR_CONTRACT, "ss_encode_view before ss_encode_begin");
     if (c->n == 0) return;
@@ -442,73 +470,99 @@ void encode_one(ss_ctx* c, const ss_camera& cam, const ss_view_masks* vm, int mo
     if (M > 128) throw Error(SS_ERR_CONTRACT, "at most 128 masks per view are supported");
     const uint32_t words = mask_words_for(M);
     const std::string prefix = "image " + std::to_string(cam.image_id) + ": ";
-    cudaStream_t s = c->stream;
-    if (M) build_mask_bits(c, cam, vm, words, cam.image_id);
+    cudaStream_t s = L.stream;
+    if (M) build_mask_bits(c, L, s, cam, vm, words, cam.image_id);
     const float* d_clip = vm && (vm->flags & SS_MASKS_ON_DEVICE) ? vm->clip : nullptr;
     if (M && !d_clip) {
-        auto* dc = static_cast<float*>(c->clip.ensure(std::max<uint64_t>((uint64_t)M * c->dim, 1) * 4));
+        auto* dc = static_cast<float*>(L.clip.ensure(std::max<uint64_t>((uint64_t)M * c->dim, 1) * 4));
         d_clip = dc;
-        Scope h(c, SS_K_H2D);
+        Scope h(c, s, SS_K_H2D);
         SS_CUDA(cudaMemcpyAsync(dc, vm->clip, (size_t)M * c->dim * 4, cudaMemcpyHostToDevice, s));
         c->prof.bytes[SS_K_H2D] += (double)M * c->dim * 4;
     }
-    const Geometry g = run_geometry(c, cam, SS_ERR_DATA, prefix.c_str());
+    const Geometry g = run_geometry(c, L, s, cam, SS_ERR_DATA, prefix.c_str());
     c->cnt_views += 1;
     if (g.n_surv == 0 || M == 0) return;
 
     // per-(rank, mask) scalars: grow-only and kept zero by consume-and-clear
     const uint64_t need = g.n_surv * (uint64_t)M;
-    if (need > c->acc_elems) {
+    if (need > L.acc_elems) {
         const uint64_t cap = std::max<uint64_t>(need, c->n * (uint64_t)std::min<uint32_t>(std::max(M, 16u), 128u));
-        c->acc.release();
-        c->acc.ensure(cap * 4);
-        SS_CUDA(cudaMemsetAsync(c->acc.p, 0, c->acc.bytes, s));
-        c->acc_elems = c->acc.bytes / 4;
+        L.acc.release();
+        L.acc.ensure(cap * 4);
+        SS_CUDA(cudaMemsetAsync(L.acc.p, 0, L.acc.bytes, s));
+        L.acc_elems = L.acc.bytes / 4;
     }
-    auto* touched = static_cast<uint32_t*>(c->touched.p);
-    if (c->touched.bytes < c->n * 4) {
-        c->touched.release();
-        touched = static_cast<uint32_t*>(c->touched.ensure(c->n * 4));
-        SS_CUDA(cudaMemsetAsync(touched, 0, c->touched.bytes, s));
+    auto* touched = static_cast<uint32_t*>(L.touched.p);
+    if (L.touched.bytes < c->n * 4) {
+        L.touched.release();
+        touched = static_cast<uint32_t*>(L.touched.ensure(c->n * 4));
+        SS_CUDA(cudaMemsetAsync(touched, 0, L.touched.bytes, s));
     }
-    auto* tlist = static_cast<uint32_t*>(c->touched_list.ensure(c->n * 4));
+    auto* tlist = static_cast<uint32_t*>(L.touched_list.ensure(c->n * 4));
 
     {
-        Scope sc(c, SS_K_RASTER);
-        RasterParams p = raster_params(c, cam, g);
-        p.pix_bits = c->pix_bits.as<uint32_t>();
+        Scope sc(c, s, SS_K_RASTER);
+        RasterParams p = raster_params(L, cam, g);
+        p.pix_bits = L.pix_bits.as<uint32_t>();
         p.mask_words = words;
         p.n_masks = M;
-        p.acc = c->acc.as<float>();
+        p.acc = L.acc.as<float>();
         p.touched = touched;
         p.touched_list = tlist;
         own_launch(c, launch_raster_fused(p, mode, g.tiles, s), SS_K_RASTER);
         const uint64_t P = (uint64_t)cam.width * cam.height;
         c->prof.bytes[SS_K_RASTER] += 64.0 * (double)g.n_inst + (double)P * ((M + 7) / 8);
     }
+    // contractions into the shared sums run in view order across the lanes
+    SS_CUDA(cudaStreamWaitEvent(s, prev.contract_done, 0));
     {
-        Scope sc(c, SS_K_CONTRACT);
+        Scope sc(c, s, SS_K_CONTRACT);
         ContractParams q;
         q.touched_list = tlist;
         q.touched = touched;
-        q.order = c->order.as<uint32_t>();
-        q.acc = c->acc.as<float>();
+        q.order = L.order.as<uint32_t>();
+        q.acc = L.acc.as<float>();
         q.n_masks = M;
         q.clip = d_clip;
         q.dim = c->dim;
         q.sums = c->sums;
         q.totals = c->totals;
-        q.info = c->info.as<ViewInfo>();
+        q.info = L.info.as<ViewInfo>();
         q.count_pairs = 1;
         q.cum = c->counters.as<unsigned long long>();
         own_launch(c, launch_contract(q, g.n_surv, s), SS_K_CONTRACT);
         c->prof.bytes[SS_K_CONTRACT] += (double)M * c->dim * 4;
+    }
+    SS_CUDA(cudaEventRecord(L.contract_done, s));
+}
+
+void encode_batch(ss_ctx* c, uint32_t nviews, const ss_camera* cams, const ss_view_masks* masks, int mode) {
+    // lanes start after everything already queued on the user stream
+    SS_CUDA(cudaEventRecord(c->ev_user, c->stream));
+    for (auto& L : c->lanes) SS_CUDA(cudaStreamWaitEvent(L.stream, c->ev_user, 0));
+    struct Join {
+        ss_ctx* c;
+        ~Join() {
+            // the user stream resumes after both lanes drain (also on errors)
+            for (auto& L : c->lanes) {
+                cudaEventRecord(L.done, L.stream);
+                cudaStreamWaitEvent(c->stream, L.done, 0);
+            }
+        }
+    } join{c};
+    for (uint32_t v = 0; v < nviews; ++v) {
+        Lane& L = c->lanes[c->next_lane];
+        Lane& prev = c->lanes[c->next_lane ^ 1u];
+        c->next_lane ^= 1u;
+        encode_one(c, L, prev, cams[v], masks ? &masks[v] : nullptr, mode);
     }
 }
 
 void profile_drain(ss_ctx* c) {
     if (c->prof.pending.empty()) return;
     SS_CUDA(cudaStreamSynchronize(c->stream));
+    for (auto& L : c->lanes) SS_CUDA(cudaStreamSynchronize(L.stream));
     for (auto& pe : c->prof.pending) {
         float ms = 0;
         SS_CUDA(cudaEventElapsedTime(&ms, pe.second.first, pe.second.second));
@@ -546,9 +600,17 @@ int ss_create(int device, ss_ctx** out) {
         SS_CUDA(cudaSetDevice(device));
         SS_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
         c->stream = c->own_stream;
-        SS_CUDA(cudaMallocHost(&c->h_info, sizeof(ViewInfo)));
         SS_CUDA(cudaMallocHost(&c->h_init, sizeof(ViewInfo)));
         SS_CUDA(cudaMallocHost(&c->h_u32, 64));
+        SS_CUDA(cudaEventCreateWithFlags(&c->ev_user, cudaEventDisableTiming));
+        for (auto& L : c->lanes) {
+            SS_CUDA(cudaStreamCreateWithFlags(&L.stream, cudaStreamNonBlocking));
+            SS_CUDA(cudaEventCreateWithFlags(&L.contract_done, cudaEventDisableTiming));
+            SS_CUDA(cudaEventCreateWithFlags(&L.done, cudaEventDisableTiming));
+            SS_CUDA(cudaMallocHost(&L.h_info, sizeof(ViewInfo)));
+            SS_CUDA(cudaMallocHost(&L.h_u32, 64));
+            L.info.ensure(sizeof(ViewInfo));
+        }
         std::memset(c->h_init, 0, sizeof(ViewInfo));
         c->h_init->min_key = ~0ull;
         c->h_init->err_gid = ~0u;
@@ -563,22 +625,20 @@ void ss_destroy(ss_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
-    ss::DevBuf* bufs[] = {&c->mean_op, &c->scale, &c->quat, &c->rec, &c->keys, &c->flags, &c->keys_sel, &c->ids_sel,
-                          &c->keys_sorted, &c->order, &c->rec_sorted, &c->ntiles, &c->offsets, &c->tile_keys,
-                          &c->tile_vals, &c->tile_keys_sorted, &c->tile_ranks, &c->tile_start, &c->tile_end,
-                          &c->cub_tmp, &c->num_sel, &c->k32, &c->k32_sorted, &c->info, &c->pix_bits, &c->mask_bits, &c->runs,
-                          &c->run_offsets, &c->clip, &c->spans, &c->pix_count, &c->pix_offset, &c->entries,
-                          &c->per_pixel_total, &c->alpha, &c->acc, &c->touched, &c->touched_list, &c->counters,
-                          &c->sums_buf, &c->totals_buf, &c->store_rows, &c->store_ids, &c->qbuf, &c->qnorm,
-                          &c->scores, &c->topk_ids, &c->topk_sims, &c->sel_flags, &c->thr_keys, &c->thr_keys_sorted,
-                          &c->thr_ids, &c->thr_ids_sorted, &c->zero_flag};
+    for (auto& L : c->lanes) cudaStreamSynchronize(L.stream);
+    ss::DevBuf* bufs[] = {&c->mean_op, &c->scale, &c->quat, &c->cub_tmp, &c->num_sel, &c->info, &c->pix_count,
+                          &c->pix_offset, &c->entries, &c->per_pixel_total, &c->alpha, &c->counters, &c->sums_buf,
+                          &c->totals_buf, &c->store_rows, &c->store_ids, &c->qbuf, &c->qnorm, &c->scores,
+                          &c->topk_ids, &c->topk_sims, &c->sel_flags, &c->thr_keys, &c->thr_keys_sorted, &c->thr_ids,
+                          &c->thr_ids_sorted, &c->zero_flag};
     for (auto* b : bufs) b->release();
     for (auto e : c->prof.pool) cudaEventDestroy(e);
     for (auto& pe : c->prof.pending) {
         cudaEventDestroy(pe.second.first);
         cudaEventDestroy(pe.second.second);
     }
-    if (c->h_info) cudaFreeHost(c->h_info);
+    for (auto& L : c->lanes) L.release_all();
+    if (c->ev_user) cudaEventDestroy(c->ev_user);
     if (c->h_init) cudaFreeHost(c->h_init);
     if (c->h_u32) cudaFreeHost(c->h_u32);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
@@ -636,17 +696,18 @@ int ss_project(ss_ctx* c, const ss_camera* cam, ss_projected* out) {
         if (N == 0) return;
         cudaStream_t s = c->stream;
         auto* dbg = static_cast<ss_projected*>(c->scores.ensure(N * sizeof(ss_projected)));
-        reset_info(c);
+        ss::Lane& L = c->lanes[0];
+        reset_info(c, L, s);
         ProjectParams p;
         p.mean_op = c->mean_op.as<float4>();
         p.scale = c->scale.as<float4>();
         p.quat = c->quat.as<float4>();
         p.n = N;
         p.cam = *cam;
-        p.rec = static_cast<SplatRec*>(c->rec.ensure(N * sizeof(SplatRec)));
-        p.keys = static_cast<unsigned long long*>(c->keys.ensure(N * 8));
-        p.flags = static_cast<uint8_t*>(c->flags.ensure(N));
-        p.info = c->info.as<ViewInfo>();
+        p.rec = static_cast<SplatRec*>(L.rec.ensure(N * sizeof(SplatRec)));
+        p.keys = static_cast<unsigned long long*>(L.keys.ensure(N * 8));
+        p.flags = static_cast<uint8_t*>(L.flags.ensure(N));
+        p.info = L.info.as<ViewInfo>();
         p.dbg = dbg;
         own_launch(c, launch_project(p, s), SS_K_PROJECT);
         SS_CUDA(cudaMemcpyAsync(out, dbg, N * sizeof(ss_projected), cudaMemcpyDeviceToHost, s));
@@ -662,7 +723,8 @@ int ss_raster_capture(ss_ctx* c, const ss_camera* cam, int mode, uint64_t* n_ent
         set_device(c);
         cudaStream_t s = c->stream;
         const uint64_t P = (uint64_t)cam->width * cam->height;
-        const Geometry g = run_geometry(c, *cam, SS_ERR_NUMERIC, "");
+        ss::Lane& L = c->lanes[0];
+        const Geometry g = run_geometry(c, L, s, *cam, SS_ERR_NUMERIC, "");
         auto* cnt = static_cast<uint32_t*>(c->pix_count.ensure((P + 1) * 4));
         auto* off = static_cast<uint32_t*>(c->pix_offset.ensure((P + 1) * 4));
         auto* ppt = static_cast<float*>(c->per_pixel_total.ensure(P * 4));
@@ -670,7 +732,7 @@ int ss_raster_capture(ss_ctx* c, const ss_camera* cam, int mode, uint64_t* n_ent
         SS_CUDA(cudaMemsetAsync(cnt, 0, (P + 1) * 4, s));
         SS_CUDA(cudaMemsetAsync(ppt, 0, P * 4, s));
         SS_CUDA(cudaMemsetAsync(alp, 0, P * 4, s));
-        RasterParams p = raster_params(c, *cam, g);
+        RasterParams p = raster_params(L, *cam, g);
         if (g.n_surv) {
             p.pix_count = cnt;
             own_launch(c, launch_raster_count(p, mode, g.tiles, s), SS_K_RASTER);
@@ -716,12 +778,12 @@ int ss_raster_fetch(ss_ctx* c, ss_weight_entry* entries, float* per_pixel_total,
         if (per_pixel_total && P) SS_CUDA(cudaMemcpy(per_pixel_total, c->per_pixel_total.p, P * 4, cudaMemcpyDeviceToHost));
         if (alpha && P) SS_CUDA(cudaMemcpy(alpha, c->alpha.p, P * 4, cudaMemcpyDeviceToHost));
         if (splat_gid && c->cap_splats)
-            SS_CUDA(cudaMemcpy(splat_gid, c->order.p, c->cap_splats * 4, cudaMemcpyDeviceToHost));
+            SS_CUDA(cudaMemcpy(splat_gid, c->lanes[0].order.p, c->cap_splats * 4, cudaMemcpyDeviceToHost));
         if (tile_offsets || tile_splats) {
             std::vector<uint32_t> st(c->cap_tiles), en(c->cap_tiles);
             if (c->cap_tiles) {
-                SS_CUDA(cudaMemcpy(st.data(), c->tile_start.p, c->cap_tiles * 4, cudaMemcpyDeviceToHost));
-                SS_CUDA(cudaMemcpy(en.data(), c->tile_end.p, c->cap_tiles * 4, cudaMemcpyDeviceToHost));
+                SS_CUDA(cudaMemcpy(st.data(), c->lanes[0].tile_start.p, c->cap_tiles * 4, cudaMemcpyDeviceToHost));
+                SS_CUDA(cudaMemcpy(en.data(), c->lanes[0].tile_end.p, c->cap_tiles * 4, cudaMemcpyDeviceToHost));
             }
             if (tile_offsets) {
                 // tiles are contiguous in key order, so start of tile t is the
@@ -734,7 +796,7 @@ int ss_raster_fetch(ss_ctx* c, ss_weight_entry* entries, float* per_pixel_total,
                 tile_offsets[c->cap_tiles] = run;
             }
             if (tile_splats && c->cap_instances)
-                SS_CUDA(cudaMemcpy(tile_splats, c->tile_ranks.p, c->cap_instances * 4, cudaMemcpyDeviceToHost));
+                SS_CUDA(cudaMemcpy(tile_splats, c->lanes[0].tile_ranks.p, c->cap_instances * 4, cudaMemcpyDeviceToHost));
         }
     });
 }
@@ -766,7 +828,7 @@ int ss_encode_view(ss_ctx* c, const ss_camera* cam, const ss_view_masks* masks, 
     return guarded([&] {
         if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
         set_device(c);
-        encode_one(c, *cam, masks, mode);
+        encode_batch(c, 1, cam, masks, mode);
     });
 }
 
@@ -774,7 +836,7 @@ int ss_encode_views(ss_ctx* c, uint32_t nviews, const ss_camera* cams, const ss_
     return guarded([&] {
         if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
         set_device(c);
-        for (uint32_t v = 0; v < nviews; ++v) encode_one(c, cams[v], masks ? &masks[v] : nullptr, mode);
+        encode_batch(c, nviews, cams, masks, mode);
     });
 }
 
@@ -795,7 +857,7 @@ int ss_encode_finalize(ss_ctx* c, uint64_t row_lo, uint64_t row_hi, float* rows_
             d_cov = d_rows + n * c->dim;
         }
         {
-            Scope sc(c, SS_K_NORMALIZE);
+            Scope sc(c, s, SS_K_NORMALIZE);
             own_launch(c, launch_normalize(c->sums + row_lo * c->dim, c->totals + row_lo, n, c->dim, d_rows, d_cov, s),
                        SS_K_NORMALIZE);
             c->prof.bytes[SS_K_NORMALIZE] += (double)n * (8.0 * c->dim + 8.0);
@@ -813,7 +875,7 @@ int ss_normalize_device(ss_ctx* c, const float* d_sums, const float* d_totals, u
     return guarded([&] {
         if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
         set_device(c);
-        Scope sc(c, SS_K_NORMALIZE);
+        Scope sc(c, c->stream, SS_K_NORMALIZE);
         own_launch(c, launch_normalize(d_sums, d_totals, n, dim, d_rows_out, d_coverage_out, c->stream),
                    SS_K_NORMALIZE);
         c->prof.bytes[SS_K_NORMALIZE] += (double)n * (8.0 * dim + 8.0);
@@ -910,7 +972,7 @@ int ss_query_topk(ss_ctx* c, const float* queries, uint32_t nq, uint32_t k, uint
         if (k == 0 || count == 0 || nq == 0) return; // vecstore.hpp:122
         if (k > 64) throw Error(SS_ERR_CONTRACT, "query_topk: k above 64 is not supported on the device path");
         cudaStream_t s = c->stream;
-        Scope sc(c, SS_K_QUERY);
+        Scope sc(c, s, SS_K_QUERY);
         const float* d_qn = prepare_queries(c, queries, nq);
         const uint32_t qt = (uint32_t)score_query_tile();
         const uint32_t tile = std::max<uint32_t>(qt, 64);
