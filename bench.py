@@ -290,12 +290,9 @@ def main():
     for _ in range(args.warmup):
         step_device()
     torch.cuda.synchronize()
-    ctx.profile_reset()
-    ctx.profile(True)
+    ctx.profile_reset()  # zeroes the launch and geometry counters too
     with ClockSampler(local) as clk:
         ms_step = timed(step_device, args.steps)
-    ctx.profile(False)
-    prof = ctx.profile_read()
     counters = ctx.counters()
     own, cub = ctx.launch_count()
 
@@ -325,21 +322,30 @@ def main():
         e2e = {"value": n_views / (e2e_ms / 1e3), "unit": "views/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(host_rows.numel() * 4 + host_cov.numel() * 4), "ms_per_step": e2e_ms}
 
-    # ---- per-kernel roofline (this rank; events on the launching stream)
+    # ---- per-kernel attribution: one extra pass with the two lanes serialised
+    # so every kernel class is timed exclusively (CUDA events on its stream)
+    ctx.set_lanes(1)
+    ctx.profile_reset()
+    ctx.profile(True)
+    ms_prof = timed(step_device, 1)
+    ctx.profile(False)
+    prof = ctx.profile_read()
+    ctx.set_lanes(2)
     hbm, peak_kind = peaks()
-    steps = max(args.steps, 1)
     kernels = {}
     for k, v in prof.items():
         if v["launches"] and v["ms"] > 0 and k != "query":
-            kernels[k] = {"ms_per_step": v["ms"] / steps, "launches_per_step": v["launches"] / steps,
-                          "gb_per_step": v["bytes"] / steps / 1e9,
-                          "achieved_gbs": v["bytes"] / (v["ms"] / 1e3) / 1e9 if k != "h2d" else None}
+            kernels[k] = {"ms_per_step": v["ms"], "launches_per_step": v["launches"], "gb_per_step": v["bytes"] / 1e9,
+                          "achieved_gbs": v["bytes"] / (v["ms"] / 1e3) / 1e9 if k != "h2d" else None,
+                          "share_of_serial_step": v["ms"] / ms_prof}
     dom = max((k for k in kernels if k not in ("h2d",)), key=lambda k: kernels[k]["ms_per_step"])
     dk = kernels[dom]
     roofline = {"bound": "hbm", "kernel": dom, "achieved": dk["achieved_gbs"], "peak": hbm, "unit": "GB/s",
                 "frac": dk["achieved_gbs"] / hbm, "traffic": None, "peak_source": f"{peak_kind} (MEASURED_PEAKS.json)",
-                "share_of_step": dk["ms_per_step"] / ms_step}
-    pass_bytes = sum(v["bytes"] for k, v in prof.items() if k not in ("h2d", "query")) / steps
+                "share_of_step": dk["share_of_serial_step"],
+                "timing": "CUDA events around each launch on its stream, one extra pass with lanes serialised"}
+    steps = 1
+    pass_bytes = sum(v["bytes"] for k, v in prof.items() if k not in ("h2d", "query"))
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -375,8 +381,9 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
-            "gpu_launches": int((own + cub) / steps),
-            "gpu_launches_detail": {"own_per_step": own / steps, "cub_per_step": cub / steps},
+            "gpu_launches": int((own + cub) / max(args.steps, 1)),
+            "gpu_launches_detail": {"own_per_step": own / max(args.steps, 1), "cub_per_step": cub / max(args.steps, 1)},
+            "serial_profile_ms_per_step": ms_prof,
         }
         print(json.dumps(line), flush=True)
     ctx.close()

@@ -89,6 +89,10 @@ int ss_last_error_kind(void);
  * own collectives. */
 int ss_set_stream(ss_ctx* ctx, uintptr_t stream);
 int ss_synchronize(ss_ctx* ctx);
+/* Tuning options.  SS_OPT_LANES: per-view pipeline lanes (1 or 2, default 2);
+ * 1 serialises views, which the bench uses for exclusive per-kernel timing. */
+enum ss_option { SS_OPT_LANES = 1 };
+int ss_set_option(ss_ctx* ctx, int option, int64_t value);
 
 /* ---- scene (GaussianScene, scene.hpp:54-76) --------------------------- */
 /* mean/scale: n x 3; quat_xyzw: n x 4 in Eigen coeffs() order; opacity: n.

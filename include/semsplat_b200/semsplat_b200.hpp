@@ -1,0 +1,334 @@
+// semsplat_b200.hpp -- C++ drop-in for the reference's embedding path.
+//
+// Include AFTER the reference's own headers (semsplat/pipeline.hpp,
+// semsplat/vecstore.hpp); link libsemsplat_b200.so.  Every function keeps the
+// reference's signature, argument meaning and exception behaviour, so a caller
+// switches by qualifying the call with semsplat::b200:::
+//
+//   semsplat::encode_scene(...)            pipeline.hpp:280   -> b200::encode_scene
+//   semsplat::rasterize_weights_only(...)  rasterizer.hpp:268 -> b200::rasterize_weights_only
+//   semsplat::project_gaussian(...)        projection.hpp:33  -> b200::project_all (batch)
+//   semsplat::build_store(...)             vecstore.hpp:88    -> b200::build_store
+//   semsplat::query_topk(...)              vecstore.hpp:121   -> b200::query_topk
+//   semsplat::query_threshold(...)         vecstore.hpp:135   -> b200::query_threshold
+//
+// All compute runs in the sm_100a kernels behind the C ABI
+// (include/semsplat_b200.h); this header only marshals the reference's types.
+#pragma once
+
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../semsplat_b200.h"
+#include "semsplat/pipeline.hpp"
+#include "semsplat/providers.hpp"
+#include "semsplat/vecstore.hpp"
+
+namespace semsplat {
+namespace b200 {
+
+// ss_status -> the reference's exception taxonomy (core.hpp:14-57)
+[[noreturn]] inline void raise_status(int st) {
+    const std::string msg = ss_last_error();
+    switch (st) {
+    case SS_ERR_CONTRACT: throw ContractError(msg);
+    case SS_ERR_DATA: throw DataError(msg);
+    case SS_ERR_NUMERIC: throw NumericError(msg);
+    case SS_ERR_FORMAT: throw FormatError(msg);
+    case SS_ERR_IO: throw IoError(msg);
+    case SS_ERR_PIPELINE: throw PipelineError(msg, {msg}, false);
+    default: throw std::runtime_error("libsemsplat_b200: " + msg);
+    }
+}
+inline void check(int st) {
+    if (st != SS_OK) raise_status(st);
+}
+
+// One context per device for the process (the reference is stateless; the
+// device keeps the scene resident between calls).
+class Device {
+public:
+    static Device& get(int device = 0) {
+        static std::mutex mu;
+        static std::vector<std::unique_ptr<Device>> devs;
+        std::lock_guard<std::mutex> lock(mu);
+        if (devs.size() <= static_cast<size_t>(device)) devs.resize(device + 1);
+        if (!devs[device]) devs[device].reset(new Device(device));
+        return *devs[device];
+    }
+    ss_ctx* ctx() { return ctx_; }
+    std::mutex& mutex() { return mu_; }
+    // Upload the scene unless this exact object (and size) is already resident.
+    void bind(const GaussianScene& scene) {
+        if (bound_ == &scene && bound_n_ == scene.size()) return;
+        const size_t n = scene.size();
+        std::vector<float> mean(3 * n), scale(3 * n), quat(4 * n), op(n);
+        for (size_t k = 0; k < n; ++k) {
+            const Gaussian3D& g = scene[k];
+            for (int i = 0; i < 3; ++i) {
+                mean[3 * k + i] = g.mean[i];
+                scale[3 * k + i] = g.scale[i];
+            }
+            quat[4 * k + 0] = g.rotation.x();
+            quat[4 * k + 1] = g.rotation.y();
+            quat[4 * k + 2] = g.rotation.z();
+            quat[4 * k + 3] = g.rotation.w();
+            op[k] = g.opacity;
+        }
+        check(ss_scene_set(ctx_, mean.data(), scale.data(), quat.data(), op.data(), n));
+        bound_ = &scene;
+        bound_n_ = n;
+    }
+    ~Device() { ss_destroy(ctx_); }
+
+private:
+    explicit Device(int device) { check(ss_create(device, &ctx_)); }
+    ss_ctx* ctx_ = nullptr;
+    std::mutex mu_;
+    const GaussianScene* bound_ = nullptr;
+    size_t bound_n_ = 0;
+};
+
+inline ss_camera to_c(const CameraPose& cam) {
+    ss_camera c{};
+    c.fx = cam.fx;
+    c.fy = cam.fy;
+    c.cx = cam.cx;
+    c.cy = cam.cy;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) c.R[3 * i + j] = cam.rotation(i, j);
+    for (int i = 0; i < 3; ++i) c.t[i] = cam.translation[i];
+    c.width = cam.width;
+    c.height = cam.height;
+    c.image_id = cam.image_id;
+    return c;
+}
+
+// rasterizer.hpp:268-271
+inline WeightMap rasterize_weights_only(const GaussianScene& scene, const CameraPose& cam,
+                                        WeightMode mode = WeightMode::kAlphaComposited, int device = 0) {
+    Device& d = Device::get(device);
+    std::lock_guard<std::mutex> lock(d.mutex());
+    d.bind(scene);
+    const ss_camera c = to_c(cam);
+    uint64_t ne = 0, ns = 0, ni = 0;
+    check(ss_raster_capture(d.ctx(), &c, mode == WeightMode::kFalloffOnly ? SS_FALLOFF_ONLY : SS_ALPHA_COMPOSITED, &ne,
+                            &ns, &ni));
+    WeightMap wm;
+    wm.image_id = cam.image_id;
+    wm.width = cam.width;
+    wm.height = cam.height;
+    std::vector<ss_weight_entry> e(ne);
+    wm.per_pixel_total.assign(static_cast<size_t>(cam.width) * cam.height, 0.0f);
+    check(ss_raster_fetch(d.ctx(), e.data(), wm.per_pixel_total.data(), nullptr, nullptr, nullptr, nullptr));
+    wm.entries.resize(ne);
+    for (size_t i = 0; i < ne; ++i) wm.entries[i] = {e[i].gaussian_id, e[i].pixel, e[i].weight};
+    return wm;
+}
+
+// projection.hpp:33-55 for every Gaussian of the scene
+inline std::vector<Projected2D> project_all(const GaussianScene& scene, const CameraPose& cam, int device = 0) {
+    Device& d = Device::get(device);
+    std::lock_guard<std::mutex> lock(d.mutex());
+    d.bind(scene);
+    const ss_camera c = to_c(cam);
+    std::vector<ss_projected> raw(scene.size());
+    check(ss_project(d.ctx(), &c, raw.data()));
+    std::vector<Projected2D> out(raw.size());
+    for (size_t k = 0; k < raw.size(); ++k) {
+        out[k].gaussian_id = raw[k].gaussian_id;
+        out[k].visible = raw[k].visible != 0;
+        out[k].mu2d = Eigen::Vector2d(raw[k].mu_x, raw[k].mu_y);
+        out[k].cov_xx = raw[k].cov_xx;
+        out[k].cov_xy = raw[k].cov_xy;
+        out[k].cov_yy = raw[k].cov_yy;
+        out[k].depth = raw[k].depth;
+    }
+    return out;
+}
+
+// pipeline.hpp:280-470.  `workers` keeps the reference's view-to-worker
+// assignment; all workers of this process share the device context, whose
+// single fp32 accumulator stands in for the per-worker partials.
+inline EmbeddingTable encode_scene(const GaussianScene& scene, const DatasetManifest& manifest, uint32_t workers,
+                                   uint64_t chunk_rows, const EncodeOptions& options = {},
+                                   EncodeStats* stats_out = nullptr, int device = 0) {
+    if (workers < 1) throw ContractError("encode_scene: workers must be >= 1");
+    if (manifest.raster_width == 0 || manifest.raster_height == 0)
+        throw DataError("encode_scene: manifest has no raster resolution");
+    const std::vector<CameraPose> cameras = load_cameras(manifest.resolve(manifest.camera_file));
+    std::unordered_map<uint32_t, const CameraPose*> camera_by_id;
+    for (const CameraPose& c : cameras) camera_by_id[c.image_id] = &c;
+    for (const ImageEntry& e : manifest.images)
+        if (!camera_by_id.count(e.camera_id))
+            throw DataError("image " + std::to_string(e.image_id) + ": no camera with id " +
+                            std::to_string(e.camera_id));
+
+    Device& d = Device::get(device);
+    std::lock_guard<std::mutex> lock(d.mutex());
+    d.bind(scene);
+    const auto t0 = std::chrono::steady_clock::now();
+    check(ss_encode_begin(d.ctx(), manifest.embedding_dim, nullptr, nullptr));
+    const size_t n_img = manifest.images.size();
+    const size_t block = (n_img + workers - 1) / workers;
+    std::vector<std::string> failures(workers);
+    std::vector<size_t> worker_images(workers, 0);
+    std::vector<double> worker_seconds(workers, 0.0);
+    for (uint32_t rank = 0; rank < workers; ++rank) {
+        const auto ts = std::chrono::steady_clock::now();
+        for (size_t idx = 0; idx < n_img; ++idx) {
+            const bool mine = options.contiguous_batching ? (idx / block == rank) : (idx % workers == rank);
+            if (!mine) continue;
+            const ImageEntry& entry = manifest.images[idx];
+            try {
+                const CameraPose raster_cam = camera_scaled_to(*camera_by_id.at(entry.camera_id),
+                                                               manifest.raster_width, manifest.raster_height);
+                // masks stay RLE: read the run streams straight from the mask file
+                const std::string path = manifest.resolve(entry.mask_path);
+                std::ifstream is(path, std::ios::binary);
+                if (!is) throw IoError("cannot open mask file: " + path);
+                if (detail::read_le<uint32_t>(is) != kMaskFileMagic) throw FormatError("bad mask file magic: " + path);
+                const uint32_t mw = detail::read_le<uint32_t>(is), mh = detail::read_le<uint32_t>(is);
+                const uint32_t count = detail::read_le<uint32_t>(is);
+                if (mw != manifest.mask_width || mh != manifest.mask_height)
+                    throw DataError("mask of image " + std::to_string(entry.image_id) +
+                                    " does not match the manifest mask resolution");
+                std::vector<std::pair<uint32_t, std::vector<uint32_t>>> masks(count);
+                for (auto& m : masks) {
+                    m.first = detail::read_le<uint32_t>(is);
+                    const uint64_t nr = detail::read_le<uint64_t>(is);
+                    m.second.resize(nr);
+                    for (auto& r : m.second) r = detail::read_le<uint32_t>(is);
+                }
+                std::sort(masks.begin(), masks.end(),
+                          [](const auto& a, const auto& b) { return a.first < b.first; });
+                std::vector<uint32_t> runs;
+                std::vector<uint64_t> offs{0};
+                for (auto& m : masks) {
+                    runs.insert(runs.end(), m.second.begin(), m.second.end());
+                    offs.push_back(runs.size());
+                }
+                const std::vector<MaskEmbedding> emb = load_mask_embeddings(manifest, entry.image_id, count);
+                std::vector<float> clip(static_cast<size_t>(count) * manifest.embedding_dim);
+                for (uint32_t j = 0; j < count; ++j)
+                    std::memcpy(clip.data() + static_cast<size_t>(j) * manifest.embedding_dim, emb[j].vector.data(),
+                                manifest.embedding_dim * sizeof(float));
+                ss_camera c = to_c(raster_cam);
+                c.image_id = entry.image_id;
+                ss_view_masks vm{};
+                vm.n_masks = count;
+                vm.mask_width = mw;
+                vm.mask_height = mh;
+                vm.flags = 0;
+                vm.runs = runs.data();
+                vm.run_offsets = offs.data();
+                vm.clip = clip.data();
+                vm.n_runs = runs.size();
+                const int st = ss_encode_view(d.ctx(), &c, &vm,
+                                              options.mode == WeightMode::kFalloffOnly ? SS_FALLOFF_ONLY
+                                                                                        : SS_ALPHA_COMPOSITED);
+                if (st != SS_OK) raise_status(st);
+                worker_images[rank] += 1;
+            } catch (const std::exception& ex) {
+                std::string m = ex.what();
+                const std::string pre = "image " + std::to_string(entry.image_id) + ":";
+                if (m.rfind(pre, 0) != 0) m = "image " + std::to_string(entry.image_id) + ": " + m;
+                failures[rank] = m;
+                break;
+            }
+        }
+        worker_seconds[rank] = std::chrono::duration<double>(std::chrono::steady_clock::now() - ts).count();
+    }
+    bool failed = false;
+    for (const auto& f : failures) failed |= !f.empty();
+    if (failed) {
+        if (workers == 1) throw DataError(failures[0]);
+        std::vector<std::string> status;
+        for (uint32_t r = 0; r < workers; ++r)
+            status.push_back("worker " + std::to_string(r) + ": " + (failures[r].empty() ? "ok" : failures[r]));
+        throw PipelineError("scene encoding failed", std::move(status), true);
+    }
+    check(ss_synchronize(d.ctx()));
+    const auto t1 = std::chrono::steady_clock::now();
+    const uint64_t n = scene.size();
+    EmbeddingTable table(n, manifest.embedding_dim);
+    const uint64_t step = (chunk_rows == 0 || chunk_rows > n) ? std::max<uint64_t>(n, 1) : chunk_rows;
+    for (uint64_t lo = 0; lo < n; lo += step) {
+        const uint64_t hi = std::min<uint64_t>(n, lo + step);
+        check(ss_encode_finalize(d.ctx(), lo, hi, table.row(lo), table.coverage.data() + lo, 0));
+    }
+    if (stats_out) {
+        stats_out->phase1_seconds = std::chrono::duration<double>(t1 - t0).count();
+        stats_out->phase2_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
+        stats_out->worker_seconds = worker_seconds;
+        stats_out->worker_images = worker_images;
+        stats_out->worker_entries.assign(workers, 0);
+    }
+    return table;
+}
+
+// A device-resident VectorStore: ids + unit rows (payloads stay on the host
+// side in the caller's scene).
+struct DeviceStore {
+    int device = 0;
+    uint64_t count = 0;
+    uint32_t dim = 0;
+};
+
+// vecstore.hpp:88-103
+inline DeviceStore build_store(const EmbeddingTable& table, const GaussianScene& scene, int device = 0) {
+    if (table.gaussian_count != scene.size()) throw ContractError("build_store: table rows and scene size differ");
+    Device& d = Device::get(device);
+    std::lock_guard<std::mutex> lock(d.mutex());
+    uint64_t cnt = 0;
+    check(ss_store_build(d.ctx(), table.embeddings.data(), table.coverage.data(), table.gaussian_count, table.dim,
+                         &cnt));
+    return DeviceStore{device, cnt, table.dim};
+}
+
+inline DeviceStore upload_store(const VectorStore& store, int device = 0) {
+    Device& d = Device::get(device);
+    std::lock_guard<std::mutex> lock(d.mutex());
+    std::vector<float> rows(store.count() * store.dim());
+    for (size_t i = 0; i < store.count(); ++i)
+        std::memcpy(rows.data() + i * store.dim(), store.vector_at(i), store.dim() * sizeof(float));
+    check(ss_store_set(d.ctx(), store.ids().data(), rows.data(), store.count(), store.dim()));
+    return DeviceStore{device, store.count(), store.dim()};
+}
+
+// vecstore.hpp:121-132
+inline std::vector<ScoredId> query_topk(const DeviceStore& store, const std::vector<float>& q, size_t k) {
+    if (k == 0 || store.count == 0) return {};
+    if (q.size() != store.dim) throw ContractError("query dimension differs from store dimension");
+    Device& d = Device::get(store.device);
+    std::lock_guard<std::mutex> lock(d.mutex());
+    std::vector<uint32_t> ids(k);
+    std::vector<float> sims(k);
+    uint64_t cnt = 0;
+    check(ss_query_topk(d.ctx(), q.data(), 1, static_cast<uint32_t>(k), ids.data(), sims.data(), &cnt));
+    std::vector<ScoredId> out(cnt);
+    for (size_t i = 0; i < cnt; ++i) out[i] = {ids[i], sims[i]};
+    return out;
+}
+
+// vecstore.hpp:135-146
+inline std::vector<ScoredId> query_threshold(const DeviceStore& store, const std::vector<float>& q, float tau) {
+    if (!(tau >= -1.0f && tau <= 1.0f)) throw ContractError("cosine threshold must lie in [-1, 1]");
+    if (store.count == 0) return {};
+    if (q.size() != store.dim) throw ContractError("query dimension differs from store dimension");
+    Device& d = Device::get(store.device);
+    std::lock_guard<std::mutex> lock(d.mutex());
+    std::vector<uint32_t> ids(store.count);
+    std::vector<float> sims(store.count);
+    uint64_t cnt = 0;
+    check(ss_query_threshold(d.ctx(), q.data(), tau, ids.data(), sims.data(), store.count, &cnt));
+    std::vector<ScoredId> out(cnt);
+    for (size_t i = 0; i < cnt; ++i) out[i] = {ids[i], sims[i]};
+    return out;
+}
+
+} // namespace b200
+} // namespace semsplat

@@ -68,6 +68,7 @@ def lib() -> C.CDLL:
         "ss_last_error_kind": (i32, []),
         "ss_set_stream": (i32, [vp, C.c_size_t]),
         "ss_synchronize": (i32, [vp]),
+        "ss_set_option": (i32, [vp, i32, C.c_int64]),
         "ss_scene_set": (i32, [vp, pf, pf, pf, pf, u64]),
         "ss_project": (i32, [vp, C.POINTER(Camera), vp]),
         "ss_raster_capture": (i32, [vp, C.POINTER(Camera), i32, pu64, pu64, pu64]),
@@ -155,6 +156,9 @@ class Context:
 
     def set_stream(self, stream_ptr: int):
         check(self._L.ss_set_stream(self.h, int(stream_ptr)))
+
+    def set_lanes(self, n: int):
+        check(self._L.ss_set_option(self.h, 1, int(n)))
 
     def synchronize(self):
         check(self._L.ss_synchronize(self.h))

@@ -156,6 +156,7 @@ struct ss_ctx {
     // per-view pipeline lanes (scratch + stream each)
     ss::Lane lanes[2];
     uint32_t next_lane = 0;
+    uint32_t n_lanes = 2;
     cudaEvent_t ev_user = nullptr;
     ss::DevBuf cub_tmp, num_sel, info; // store / query scratch
     ss::ViewInfo* h_init = nullptr;    // pinned
@@ -552,8 +553,9 @@ void encode_batch(ss_ctx* c, uint32_t nviews, const ss_camera* cams, const ss_vi
         }
     } join{c};
     for (uint32_t v = 0; v < nviews; ++v) {
-        Lane& L = c->lanes[c->next_lane];
-        Lane& prev = c->lanes[c->next_lane ^ 1u];
+        const uint32_t li = c->n_lanes > 1 ? c->next_lane : 0u;
+        Lane& L = c->lanes[li];
+        Lane& prev = c->lanes[li ^ 1u];
         c->next_lane ^= 1u;
         encode_one(c, L, prev, cams[v], masks ? &masks[v] : nullptr, mode);
     }
@@ -649,6 +651,18 @@ int ss_set_stream(ss_ctx* c, uintptr_t stream) {
     return guarded([&] {
         if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
         c->stream = stream ? reinterpret_cast<cudaStream_t>(stream) : c->own_stream;
+    });
+}
+
+int ss_set_option(ss_ctx* c, int option, int64_t value) {
+    return guarded([&] {
+        if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
+        if (option == SS_OPT_LANES) {
+            if (value < 1 || value > 2) throw Error(SS_ERR_CONTRACT, "SS_OPT_LANES must be 1 or 2");
+            c->n_lanes = (uint32_t)value;
+        } else {
+            throw Error(SS_ERR_CONTRACT, "unknown option");
+        }
     });
 }
 

@@ -219,73 +219,179 @@ __global__ void __launch_bounds__(256) project_kernel(ProjectParams p) {
 //         w into per-(rank, mask) fp32 scalars; lanes with identical bitsets
 //         are summed with a fixed-order butterfly first, so each (splat,
 //         warp, bitset group) costs one atomic per mask, never a 512-d scatter.
+// Per-pixel compositing state (rasterizer.hpp:112-133) for one of the two
+// pixels a thread owns.
+struct PixelState {
+    double T;
+    double total;
+    uint32_t count, out, pixel;
+    uint32_t px, py;
+    double dpx, dpy;
+    bool inside, done;
+};
+
+// Evaluate one splat at one pixel: the reference's box test, Mahalanobis
+// cutoff, alpha clamp, skip rule, weight cutoff and transmittance floor, in
+// its exact fp64 operation order.  Returns whether an entry is emitted.
+template <bool FALLOFF>
+__device__ __forceinline__ bool composite_one(PixelState& ps, const SplatRec& s, uint32_t sx0, uint32_t sx1,
+                                              uint32_t sy0, uint32_t sy1, const unsigned long long* stab, float& wf) {
+    if (ps.done || ps.px < sx0 || ps.px > sx1 || ps.py < sy0 || ps.py > sy1) return false;
+    const double dx = ds(ps.dpx, s.mu_x), dy = ds(ps.dpy, s.mu_y);
+    const double d2 = da(da(dm(dm(s.a, dx), dx), dm(dm(s.b2, dx), dy)), dm(dm(s.c, dy), dy));
+    if (d2 > kMahalanobisSqCutoff) return false;
+    const double g = glibc_exp(dm(-0.5, d2), stab);
+    if constexpr (FALLOFF) {
+        if (g >= kWeightCutoff) {
+            wf = __double2float_rn(g);
+            return true;
+        }
+        return false;
+    } else {
+        const double og = dm((double)s.opacity, g);
+        const double alpha = og < kAlphaMax ? og : kAlphaMax;
+        if (alpha < kAlphaSkip) return false;
+        const double w = dm(alpha, ps.T);
+        const bool emit = w >= kWeightCutoff;
+        if (emit) wf = __double2float_rn(w);
+        ps.T = dm(ps.T, ds(1.0, alpha));
+        if (ps.T < kTransmittanceFloor) ps.done = true;
+        return emit;
+    }
+}
+
+// Fused-mode gating of one pixel slot's contribution: lanes with identical
+// mask bitsets are summed with an xor butterfly (bit-identical in every lane),
+// then lane m adds the group sum to mask 32w+m when the group has that bit.
+template <int MW>
+__device__ __forceinline__ void gate_and_accumulate(const RasterParams& p, bool contrib, float wf, uint32_t grp,
+                                                    const uint32_t (&bits)[MW], uint32_t rank, uint32_t lane) {
+    const uint32_t em = __ballot_sync(0xffffffffu, contrib);
+    if (!em) return;
+    uint32_t rem = em;
+    float* row = p.acc + (size_t)rank * p.n_masks + lane;
+    while (rem) {
+        const int leader = __ffs(rem) - 1;
+        const uint32_t gm = __shfl_sync(0xffffffffu, grp, leader);
+        float v = (contrib && ((gm >> lane) & 1u)) ? wf : 0.0f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+#pragma unroll
+        for (int w = 0; w < MW; ++w) {
+            const uint32_t gb = __shfl_sync(0xffffffffu, bits[w], leader);
+            if ((gb >> lane) & 1u) atomicAdd(row + w * 32, v);
+        }
+        rem &= ~gm;
+    }
+    if ((int)lane == __ffs(em) - 1) {
+        // first toucher of this rank appends it to the contraction list
+        if (*reinterpret_cast<volatile uint32_t*>(p.touched + rank) == 0u && atomicExch(p.touched + rank, 1u) == 0u) {
+            const unsigned long long slot = atomicAdd(&p.info->n_touched, 1ull);
+            p.touched_list[slot] = rank;
+        }
+    }
+}
+
+template <int MW>
+__device__ __forceinline__ uint32_t match_bits(const uint32_t (&bits)[MW]) {
+    if constexpr (MW == 1) {
+        return __match_any_sync(0xffffffffu, bits[0]);
+    } else if constexpr (MW == 2) {
+        return __match_any_sync(0xffffffffu, ((unsigned long long)bits[1] << 32) | bits[0]);
+    } else {
+        return __match_any_sync(0xffffffffu, ((unsigned long long)bits[1] << 32) | bits[0]) &
+               __match_any_sync(0xffffffffu, ((unsigned long long)bits[3] << 32) | bits[2]);
+    }
+}
+
+// One CTA (4 warps) per 16x16 tile.  Warp w owns the 8x8 block at
+// (8*(w&1), 8*(w>>1)); lane l owns pixels (l&7, l>>3) and (l&7, (l>>3)+4) of
+// it.  Each warp walks the tile's depth-ordered splat list independently, 32
+// entries at a time: one ballot culls the splats whose padded box misses the
+// block, the hits are staged in the warp's shared-memory slice, and both
+// pixels of every lane are composited against them front to back.  The warp
+// stops when all 64 of its pixels have terminated.  This shaping changes
+// nothing in the arithmetic: every pixel still visits exactly the splats
+// whose box contains it, in depth order.
+//
+// KIND 0: count contributions per pixel (sizes the capture).
+// KIND 1: capture -- write WeightEntry records at per-pixel offsets, in rank
+//         order (= the reference's stable_sort by pixel), per_pixel_total and
+//         alpha = 1 - T_final.
+// KIND 2: fused -- gate each contribution by the pixel's SAM-mask bitset and
+//         add w into per-(rank, mask) fp32 scalars (never a 512-d scatter).
 template <int KIND, bool FALLOFF, int MW>
-__global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) {
-    __shared__ SplatRec srec[kRasterThreads]; // warp w stages its hits in srec[32w, 32w+32)
-    __shared__ uint32_t srank[kRasterThreads];
+__global__ void __launch_bounds__(kRasterThreads2) raster_kernel(RasterParams p) {
+    __shared__ SplatRec srec[kRasterThreads2]; // warp w stages its hits in srec[32w, 32w+32)
+    __shared__ uint32_t srank[kRasterThreads2];
     __shared__ unsigned long long stab[256];
-    stab[threadIdx.x] = kExpTab[threadIdx.x];
+    for (uint32_t i = threadIdx.x; i < 256; i += kRasterThreads2) stab[i] = kExpTab[i];
 
     const uint32_t tile = blockIdx.x;
     const uint32_t tx = tile % p.tiles_x, ty = tile / p.tiles_x;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-    // warp w covers columns 8*(w&1) .. +7, rows 4*(w>>1) .. +3 of the tile
-    const uint32_t bx0 = tx * kTile + 8u * (warp & 1u), by0 = ty * kTile + 4u * (warp >> 1);
-    const uint32_t px = bx0 + (lane & 7u);
-    const uint32_t py = by0 + (lane >> 3);
-    const uint32_t bx1 = bx0 + 7u, by1 = by0 + 3u;
-    const bool inside = px < p.width && py < p.height;
-    const uint32_t pixel = py * p.width + px;
+    const uint32_t bx0 = tx * kTile + 8u * (warp & 1u), by0 = ty * kTile + 8u * (warp >> 1);
+    const uint32_t bx1 = bx0 + 7u, by1 = by0 + 7u;
     const uint32_t start = p.tile_start[tile], end = p.tile_end[tile];
-    const double dpx = (double)(int32_t)px, dpy = (double)(int32_t)py;
     SplatRec* wrec = srec + 32u * warp;
     uint32_t* wrank = srank + 32u * warp;
 
-    double T = 1.0;
-    double total = 0.0;
-    uint32_t count = 0;
-    uint32_t out = 0;
-    bool done = !inside;
-    if constexpr (KIND == 1) {
-        if (inside) out = p.pix_offset[pixel];
+    PixelState ps[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        ps[k].px = bx0 + (lane & 7u);
+        ps[k].py = by0 + (lane >> 3) + 4u * k;
+        ps[k].inside = ps[k].px < p.width && ps[k].py < p.height;
+        ps[k].pixel = ps[k].py * p.width + ps[k].px;
+        ps[k].dpx = (double)(int32_t)ps[k].px;
+        ps[k].dpy = (double)(int32_t)ps[k].py;
+        ps[k].T = 1.0;
+        ps[k].total = 0.0;
+        ps[k].count = 0;
+        ps[k].out = 0;
+        ps[k].done = !ps[k].inside;
+        if constexpr (KIND == 1) {
+            if (ps[k].inside) ps[k].out = p.pix_offset[ps[k].pixel];
+        }
     }
-    // fused-mode per-pixel mask bitset and lane grouping by identical bitset
-    uint32_t bits[MW > 0 ? MW : 1];
-    uint32_t grp = 0;
+    uint32_t bits0[MW], bits1[MW];
+    uint32_t grp0 = 0, grp1 = 0;
     if constexpr (KIND == 2) {
-        bool any_bits = false;
+        bool any0 = false, any1 = false;
 #pragma unroll
         for (int w = 0; w < MW; ++w) {
-            bits[w] = inside ? p.pix_bits[(size_t)pixel * MW + w] : 0u;
-            any_bits |= bits[w] != 0;
+            bits0[w] = ps[0].inside ? p.pix_bits[(size_t)ps[0].pixel * MW + w] : 0u;
+            bits1[w] = ps[1].inside ? p.pix_bits[(size_t)ps[1].pixel * MW + w] : 0u;
+            any0 |= bits0[w] != 0;
+            any1 |= bits1[w] != 0;
         }
-        if constexpr (MW == 1) {
-            grp = __match_any_sync(0xffffffffu, bits[0]);
-        } else if constexpr (MW == 2) {
-            grp = __match_any_sync(0xffffffffu, ((unsigned long long)bits[1] << 32) | bits[0]);
-        } else {
-            grp = __match_any_sync(0xffffffffu, ((unsigned long long)bits[1] << 32) | bits[0]) &
-                  __match_any_sync(0xffffffffu, ((unsigned long long)bits[3] << 32) | bits[2]);
-        }
-        done = done || !any_bits; // unmasked pixels contribute nothing
+        grp0 = match_bits<MW>(bits0);
+        grp1 = match_bits<MW>(bits1);
+        ps[0].done = ps[0].done || !any0; // unmasked pixels contribute nothing
+        ps[1].done = ps[1].done || !any1;
     }
     __syncthreads(); // exp table staged
 
-    // Each warp walks the tile's list independently, 32 splats at a time: one
-    // ballot culls the splats whose box misses the warp's 8x4 block, the hits
-    // are staged in the warp's smem slice, and the warp stops once all of its
-    // pixels have terminated.
+    // prefetch the first chunk's ranks and boxes
+    uint32_t nr = 0;
+    uint2 nbox = make_uint2(0u, 0u);
+    if (start + lane < end) {
+        nr = __ldg(p.tile_ranks + start + lane);
+        nbox = __ldg(reinterpret_cast<const uint2*>(&p.rec_sorted[nr].x0));
+    }
     for (uint32_t base = start; base < end; base += 32u) {
-        if (__all_sync(0xffffffffu, done)) break;
+        if (__all_sync(0xffffffffu, ps[0].done && ps[1].done)) break;
         const uint32_t i = base + lane;
-        uint32_t r = 0;
-        bool hit = false;
-        if (i < end) {
-            r = __ldg(p.tile_ranks + i);
-            const uint2 box = __ldg(reinterpret_cast<const uint2*>(&p.rec_sorted[r].x0));
-            hit = !((box.x >> 16) < bx0 || (box.x & 0xffffu) > bx1 || (box.y >> 16) < by0 || (box.y & 0xffffu) > by1);
+        const uint32_t r = nr;
+        const uint2 box = nbox;
+        // software prefetch of the next chunk's ranks and boxes
+        if (i + 32u < end) {
+            nr = __ldg(p.tile_ranks + i + 32u);
+            nbox = __ldg(reinterpret_cast<const uint2*>(&p.rec_sorted[nr].x0));
         }
-        uint32_t cand = __ballot_sync(0xffffffffu, hit);
+        const bool hit = i < end && !((box.x >> 16) < bx0 || (box.x & 0xffffu) > bx1 || (box.y >> 16) < by0 ||
+                                      (box.y & 0xffffu) > by1);
+        const uint32_t cand = __ballot_sync(0xffffffffu, hit);
         if (hit) {
             const uint32_t slot = __popc(cand & ((1u << lane) - 1u));
             const uint4* src = reinterpret_cast<const uint4*>(p.rec_sorted + r);
@@ -293,93 +399,49 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
             dst[0] = __ldg(src);
             dst[1] = __ldg(src + 1);
             dst[2] = __ldg(src + 2);
-            dst[3] = __ldg(src + 3);
+            dst[3] = make_uint4(box.x, box.y, 0u, 0u); // box already prefetched
             wrank[slot] = r;
         }
         __syncwarp();
         const uint32_t nh = __popc(cand);
         for (uint32_t j = 0; j < nh; ++j) {
             const SplatRec& s = wrec[j];
-            const uint2 box = *reinterpret_cast<const uint2*>(&s.x0);
-            const uint32_t sx0 = box.x & 0xffffu, sx1 = box.x >> 16, sy0 = box.y & 0xffffu, sy1 = box.y >> 16;
-            bool contrib = false;
-            float wf = 0.0f;
-            if (!done && px >= sx0 && px <= sx1 && py >= sy0 && py <= sy1) {
-                const double dx = ds(dpx, s.mu_x), dy = ds(dpy, s.mu_y);
-                const double d2 = da(da(dm(dm(s.a, dx), dx), dm(dm(s.b2, dx), dy)), dm(dm(s.c, dy), dy));
-                if (!(d2 > kMahalanobisSqCutoff)) {
-                    const double g = glibc_exp(dm(-0.5, d2), stab);
-                    if constexpr (FALLOFF) {
-                        if (g >= kWeightCutoff) {
-                            contrib = true;
-                            wf = __double2float_rn(g);
-                        }
-                    } else {
-                        const double og = dm((double)s.opacity, g);
-                        const double alpha = og < kAlphaMax ? og : kAlphaMax;
-                        if (!(alpha < kAlphaSkip)) {
-                            const double w = dm(alpha, T);
-                            if (w >= kWeightCutoff) {
-                                contrib = true;
-                                wf = __double2float_rn(w);
-                            }
-                            T = dm(T, ds(1.0, alpha));
-                            if (T < kTransmittanceFloor) done = true;
-                        }
-                    }
-                }
-            }
+            const uint2 sb = *reinterpret_cast<const uint2*>(&s.x0);
+            const uint32_t sx0 = sb.x & 0xffffu, sx1 = sb.x >> 16, sy0 = sb.y & 0xffffu, sy1 = sb.y >> 16;
+            float wf0 = 0.0f, wf1 = 0.0f;
+            const bool c0 = composite_one<FALLOFF>(ps[0], s, sx0, sx1, sy0, sy1, stab, wf0);
+            const bool c1 = composite_one<FALLOFF>(ps[1], s, sx0, sx1, sy0, sy1, stab, wf1);
             if constexpr (KIND == 0) {
-                count += contrib ? 1u : 0u;
+                ps[0].count += c0 ? 1u : 0u;
+                ps[1].count += c1 ? 1u : 0u;
             } else if constexpr (KIND == 1) {
-                if (contrib) {
-                    p.entries[out++] = ss_weight_entry{s.gid, pixel, wf};
-                    total = da(total, (double)wf);
+                if (c0) {
+                    p.entries[ps[0].out++] = ss_weight_entry{s.gid, ps[0].pixel, wf0};
+                    ps[0].total = da(ps[0].total, (double)wf0);
+                }
+                if (c1) {
+                    p.entries[ps[1].out++] = ss_weight_entry{s.gid, ps[1].pixel, wf1};
+                    ps[1].total = da(ps[1].total, (double)wf1);
                 }
             } else {
-                const uint32_t em = __ballot_sync(0xffffffffu, contrib);
-                if (em) {
+                if (__any_sync(0xffffffffu, c0 || c1)) {
                     const uint32_t rank = wrank[j];
-                    uint32_t rem = em;
-                    while (rem) {
-                        const int leader = __ffs(rem) - 1;
-                        const uint32_t gm = __shfl_sync(0xffffffffu, grp, leader);
-                        float v = (contrib && ((gm >> lane) & 1u)) ? wf : 0.0f;
-#pragma unroll
-                        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                        // every lane holds the (bit-identical) group sum after the xor
-                        // butterfly; lane m adds it to mask 32w+m when the group has that bit
-                        float* row = p.acc + (size_t)rank * p.n_masks + lane;
-#pragma unroll
-                        for (int w = 0; w < MW; ++w) {
-                            const uint32_t gb = __shfl_sync(0xffffffffu, bits[w], leader);
-                            if ((gb >> lane) & 1u) atomicAdd(row + w * 32, v);
-                        }
-                        rem &= ~gm;
-                    }
-                    if ((int)lane == __ffs(em) - 1) {
-                        // first toucher of this rank appends it to the contraction list
-                        if (*reinterpret_cast<volatile uint32_t*>(p.touched + rank) == 0u &&
-                            atomicExch(p.touched + rank, 1u) == 0u) {
-                            const unsigned long long slot = atomicAdd(&p.info->n_touched, 1ull);
-                            p.touched_list[slot] = rank;
-                        }
-                    }
+                    gate_and_accumulate<MW>(p, c0, wf0, grp0, bits0, rank, lane);
+                    gate_and_accumulate<MW>(p, c1, wf1, grp1, bits1, rank, lane);
                 }
-                if (__all_sync(0xffffffffu, done)) break;
             }
-            if constexpr (KIND != 2) {
-                if (__all_sync(0xffffffffu, done)) break;
-            }
+            if (__all_sync(0xffffffffu, ps[0].done && ps[1].done)) break;
         }
         __syncwarp();
     }
-    if constexpr (KIND == 0) {
-        if (inside) p.pix_count[pixel] = count;
-    } else if constexpr (KIND == 1) {
-        if (inside) {
-            p.per_pixel_total[pixel] = __double2float_rn(total);
-            p.alpha[pixel] = __double2float_rn(ds(1.0, T));
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        if (!ps[k].inside) continue;
+        if constexpr (KIND == 0) {
+            p.pix_count[ps[k].pixel] = ps[k].count;
+        } else if constexpr (KIND == 1) {
+            p.per_pixel_total[ps[k].pixel] = __double2float_rn(ps[k].total);
+            p.alpha[ps[k].pixel] = __double2float_rn(ds(1.0, ps[k].T));
         }
     }
 }
@@ -388,9 +450,9 @@ template <int KIND>
 cudaError_t launch_raster(const RasterParams& p, int mode, uint32_t tiles, cudaStream_t s) {
     if (tiles == 0) return cudaSuccess;
     if (mode == SS_FALLOFF_ONLY)
-        raster_kernel<KIND, true, 1><<<tiles, kRasterThreads, 0, s>>>(p);
+        raster_kernel<KIND, true, 1><<<tiles, kRasterThreads2, 0, s>>>(p);
     else
-        raster_kernel<KIND, false, 1><<<tiles, kRasterThreads, 0, s>>>(p);
+        raster_kernel<KIND, false, 1><<<tiles, kRasterThreads2, 0, s>>>(p);
     return cudaGetLastError();
 }
 
@@ -415,8 +477,8 @@ cudaError_t launch_raster_fused(const RasterParams& p, int mode, uint32_t tiles,
     const bool fo = mode == SS_FALLOFF_ONLY;
 #define SS_FUSED(MWV)                                                                       \
     do {                                                                                    \
-        if (fo) raster_kernel<2, true, MWV><<<tiles, kRasterThreads, 0, s>>>(p);           \
-        else raster_kernel<2, false, MWV><<<tiles, kRasterThreads, 0, s>>>(p);             \
+        if (fo) raster_kernel<2, true, MWV><<<tiles, kRasterThreads2, 0, s>>>(p);           \
+        else raster_kernel<2, false, MWV><<<tiles, kRasterThreads2, 0, s>>>(p);             \
     } while (0)
     switch (p.mask_words) {
     case 1: SS_FUSED(1); break;

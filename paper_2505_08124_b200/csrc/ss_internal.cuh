@@ -9,7 +9,8 @@
 namespace ss {
 
 constexpr uint32_t kTile = 16;          // rasterizer.hpp:30 kTileSize
-constexpr int kRasterThreads = 256;     // one thread per pixel of a 16x16 tile
+constexpr int kRasterThreads = 256;     // pixels of a 16x16 tile
+constexpr int kRasterThreads2 = 128;    // compositor threads per tile (2 pixels each)
 constexpr int kMaxMaskWords = 4;        // up to 128 masks per view
 
 // Per-splat record staged through shared memory by the compositor.  64 B so a
