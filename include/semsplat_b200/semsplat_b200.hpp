@@ -61,9 +61,9 @@ public:
     }
     ss_ctx* ctx() { return ctx_; }
     std::mutex& mutex() { return mu_; }
-    // Upload the scene unless this exact object (and size) is already resident.
+    // Upload the scene (N x 48 B; cheap next to any call that uses it).  No
+    // caching by address: a caller may reuse the same object storage.
     void bind(const GaussianScene& scene) {
-        if (bound_ == &scene && bound_n_ == scene.size()) return;
         const size_t n = scene.size();
         std::vector<float> mean(3 * n), scale(3 * n), quat(4 * n), op(n);
         for (size_t k = 0; k < n; ++k) {
@@ -79,8 +79,6 @@ public:
             op[k] = g.opacity;
         }
         check(ss_scene_set(ctx_, mean.data(), scale.data(), quat.data(), op.data(), n));
-        bound_ = &scene;
-        bound_n_ = n;
     }
     ~Device() { ss_destroy(ctx_); }
 
@@ -88,8 +86,6 @@ private:
     explicit Device(int device) { check(ss_create(device, &ctx_)); }
     ss_ctx* ctx_ = nullptr;
     std::mutex mu_;
-    const GaussianScene* bound_ = nullptr;
-    size_t bound_n_ = 0;
 };
 
 inline ss_camera to_c(const CameraPose& cam) {

@@ -304,15 +304,14 @@ __device__ __forceinline__ uint32_t match_bits(const uint32_t (&bits)[MW]) {
     }
 }
 
-// One CTA (4 warps) per 16x16 tile.  Warp w owns the 8x8 block at
-// (8*(w&1), 8*(w>>1)); lane l owns pixels (l&7, l>>3) and (l&7, (l>>3)+4) of
-// it.  Each warp walks the tile's depth-ordered splat list independently, 32
-// entries at a time: one ballot culls the splats whose padded box misses the
-// block, the hits are staged in the warp's shared-memory slice, and both
-// pixels of every lane are composited against them front to back.  The warp
-// stops when all 64 of its pixels have terminated.  This shaping changes
-// nothing in the arithmetic: every pixel still visits exactly the splats
-// whose box contains it, in depth order.
+// One CTA (8 warps) per 16x16 tile, one thread per pixel.  Warp w owns the
+// 8x4 block at (8*(w&1), 4*(w>>1)).  Each warp walks the tile's depth-ordered
+// splat list independently, 32 entries at a time: one ballot culls the splats
+// whose padded box misses the block, the hits are staged in the warp's
+// shared-memory slice, and every lane composites its pixel against them front
+// to back; the warp stops when all 32 of its pixels have terminated.  This
+// shaping changes nothing in the arithmetic: every pixel still visits exactly
+// the splats whose box contains it, in depth order.
 //
 // KIND 0: count contributions per pixel (sizes the capture).
 // KIND 1: capture -- write WeightEntry records at per-pixel offsets, in rank
@@ -321,54 +320,47 @@ __device__ __forceinline__ uint32_t match_bits(const uint32_t (&bits)[MW]) {
 // KIND 2: fused -- gate each contribution by the pixel's SAM-mask bitset and
 //         add w into per-(rank, mask) fp32 scalars (never a 512-d scatter).
 template <int KIND, bool FALLOFF, int MW>
-__global__ void __launch_bounds__(kRasterThreads2) raster_kernel(RasterParams p) {
-    __shared__ SplatRec srec[kRasterThreads2]; // warp w stages its hits in srec[32w, 32w+32)
-    __shared__ uint32_t srank[kRasterThreads2];
+__global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) {
+    __shared__ SplatRec srec[kRasterThreads]; // warp w stages its hits in srec[32w, 32w+32)
+    __shared__ uint32_t srank[kRasterThreads];
     __shared__ unsigned long long stab[256];
-    for (uint32_t i = threadIdx.x; i < 256; i += kRasterThreads2) stab[i] = kExpTab[i];
+    stab[threadIdx.x] = kExpTab[threadIdx.x];
 
     const uint32_t tile = blockIdx.x;
     const uint32_t tx = tile % p.tiles_x, ty = tile / p.tiles_x;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-    const uint32_t bx0 = tx * kTile + 8u * (warp & 1u), by0 = ty * kTile + 8u * (warp >> 1);
-    const uint32_t bx1 = bx0 + 7u, by1 = by0 + 7u;
+    const uint32_t bx0 = tx * kTile + 8u * (warp & 1u), by0 = ty * kTile + 4u * (warp >> 1);
+    const uint32_t bx1 = bx0 + 7u, by1 = by0 + 3u;
     const uint32_t start = p.tile_start[tile], end = p.tile_end[tile];
     SplatRec* wrec = srec + 32u * warp;
     uint32_t* wrank = srank + 32u * warp;
 
-    PixelState ps[2];
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        ps[k].px = bx0 + (lane & 7u);
-        ps[k].py = by0 + (lane >> 3) + 4u * k;
-        ps[k].inside = ps[k].px < p.width && ps[k].py < p.height;
-        ps[k].pixel = ps[k].py * p.width + ps[k].px;
-        ps[k].dpx = (double)(int32_t)ps[k].px;
-        ps[k].dpy = (double)(int32_t)ps[k].py;
-        ps[k].T = 1.0;
-        ps[k].total = 0.0;
-        ps[k].count = 0;
-        ps[k].out = 0;
-        ps[k].done = !ps[k].inside;
-        if constexpr (KIND == 1) {
-            if (ps[k].inside) ps[k].out = p.pix_offset[ps[k].pixel];
-        }
+    PixelState ps;
+    ps.px = bx0 + (lane & 7u);
+    ps.py = by0 + (lane >> 3);
+    ps.inside = ps.px < p.width && ps.py < p.height;
+    ps.pixel = ps.py * p.width + ps.px;
+    ps.dpx = (double)(int32_t)ps.px;
+    ps.dpy = (double)(int32_t)ps.py;
+    ps.T = 1.0;
+    ps.total = 0.0;
+    ps.count = 0;
+    ps.out = 0;
+    ps.done = !ps.inside;
+    if constexpr (KIND == 1) {
+        if (ps.inside) ps.out = p.pix_offset[ps.pixel];
     }
-    uint32_t bits0[MW], bits1[MW];
-    uint32_t grp0 = 0, grp1 = 0;
+    uint32_t bits[MW];
+    uint32_t grp = 0;
     if constexpr (KIND == 2) {
-        bool any0 = false, any1 = false;
+        bool any = false;
 #pragma unroll
         for (int w = 0; w < MW; ++w) {
-            bits0[w] = ps[0].inside ? p.pix_bits[(size_t)ps[0].pixel * MW + w] : 0u;
-            bits1[w] = ps[1].inside ? p.pix_bits[(size_t)ps[1].pixel * MW + w] : 0u;
-            any0 |= bits0[w] != 0;
-            any1 |= bits1[w] != 0;
+            bits[w] = ps.inside ? p.pix_bits[(size_t)ps.pixel * MW + w] : 0u;
+            any |= bits[w] != 0;
         }
-        grp0 = match_bits<MW>(bits0);
-        grp1 = match_bits<MW>(bits1);
-        ps[0].done = ps[0].done || !any0; // unmasked pixels contribute nothing
-        ps[1].done = ps[1].done || !any1;
+        grp = match_bits<MW>(bits);
+        ps.done = ps.done || !any; // unmasked pixels contribute nothing
     }
     __syncthreads(); // exp table staged
 
@@ -380,12 +372,11 @@ __global__ void __launch_bounds__(kRasterThreads2) raster_kernel(RasterParams p)
         nbox = __ldg(reinterpret_cast<const uint2*>(&p.rec_sorted[nr].x0));
     }
     for (uint32_t base = start; base < end; base += 32u) {
-        if (__all_sync(0xffffffffu, ps[0].done && ps[1].done)) break;
+        if (__all_sync(0xffffffffu, ps.done)) break;
         const uint32_t i = base + lane;
         const uint32_t r = nr;
         const uint2 box = nbox;
-        // software prefetch of the next chunk's ranks and boxes
-        if (i + 32u < end) {
+        if (i + 32u < end) { // software prefetch of the next chunk
             nr = __ldg(p.tile_ranks + i + 32u);
             nbox = __ldg(reinterpret_cast<const uint2*>(&p.rec_sorted[nr].x0));
         }
@@ -407,41 +398,29 @@ __global__ void __launch_bounds__(kRasterThreads2) raster_kernel(RasterParams p)
         for (uint32_t j = 0; j < nh; ++j) {
             const SplatRec& s = wrec[j];
             const uint2 sb = *reinterpret_cast<const uint2*>(&s.x0);
-            const uint32_t sx0 = sb.x & 0xffffu, sx1 = sb.x >> 16, sy0 = sb.y & 0xffffu, sy1 = sb.y >> 16;
-            float wf0 = 0.0f, wf1 = 0.0f;
-            const bool c0 = composite_one<FALLOFF>(ps[0], s, sx0, sx1, sy0, sy1, stab, wf0);
-            const bool c1 = composite_one<FALLOFF>(ps[1], s, sx0, sx1, sy0, sy1, stab, wf1);
+            float wf = 0.0f;
+            const bool c = composite_one<FALLOFF>(ps, s, sb.x & 0xffffu, sb.x >> 16, sb.y & 0xffffu, sb.y >> 16, stab,
+                                                  wf);
             if constexpr (KIND == 0) {
-                ps[0].count += c0 ? 1u : 0u;
-                ps[1].count += c1 ? 1u : 0u;
+                ps.count += c ? 1u : 0u;
             } else if constexpr (KIND == 1) {
-                if (c0) {
-                    p.entries[ps[0].out++] = ss_weight_entry{s.gid, ps[0].pixel, wf0};
-                    ps[0].total = da(ps[0].total, (double)wf0);
-                }
-                if (c1) {
-                    p.entries[ps[1].out++] = ss_weight_entry{s.gid, ps[1].pixel, wf1};
-                    ps[1].total = da(ps[1].total, (double)wf1);
+                if (c) {
+                    p.entries[ps.out++] = ss_weight_entry{s.gid, ps.pixel, wf};
+                    ps.total = da(ps.total, (double)wf);
                 }
             } else {
-                if (__any_sync(0xffffffffu, c0 || c1)) {
-                    const uint32_t rank = wrank[j];
-                    gate_and_accumulate<MW>(p, c0, wf0, grp0, bits0, rank, lane);
-                    gate_and_accumulate<MW>(p, c1, wf1, grp1, bits1, rank, lane);
-                }
+                gate_and_accumulate<MW>(p, c, wf, grp, bits, wrank[j], lane);
             }
-            if (__all_sync(0xffffffffu, ps[0].done && ps[1].done)) break;
+            if (__all_sync(0xffffffffu, ps.done)) break;
         }
         __syncwarp();
     }
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        if (!ps[k].inside) continue;
+    if (ps.inside) {
         if constexpr (KIND == 0) {
-            p.pix_count[ps[k].pixel] = ps[k].count;
+            p.pix_count[ps.pixel] = ps.count;
         } else if constexpr (KIND == 1) {
-            p.per_pixel_total[ps[k].pixel] = __double2float_rn(ps[k].total);
-            p.alpha[ps[k].pixel] = __double2float_rn(ds(1.0, ps[k].T));
+            p.per_pixel_total[ps.pixel] = __double2float_rn(ps.total);
+            p.alpha[ps.pixel] = __double2float_rn(ds(1.0, ps.T));
         }
     }
 }
@@ -450,9 +429,9 @@ template <int KIND>
 cudaError_t launch_raster(const RasterParams& p, int mode, uint32_t tiles, cudaStream_t s) {
     if (tiles == 0) return cudaSuccess;
     if (mode == SS_FALLOFF_ONLY)
-        raster_kernel<KIND, true, 1><<<tiles, kRasterThreads2, 0, s>>>(p);
+        raster_kernel<KIND, true, 1><<<tiles, kRasterThreads, 0, s>>>(p);
     else
-        raster_kernel<KIND, false, 1><<<tiles, kRasterThreads2, 0, s>>>(p);
+        raster_kernel<KIND, false, 1><<<tiles, kRasterThreads, 0, s>>>(p);
     return cudaGetLastError();
 }
 
@@ -477,8 +456,8 @@ cudaError_t launch_raster_fused(const RasterParams& p, int mode, uint32_t tiles,
     const bool fo = mode == SS_FALLOFF_ONLY;
 #define SS_FUSED(MWV)                                                                       \
     do {                                                                                    \
-        if (fo) raster_kernel<2, true, MWV><<<tiles, kRasterThreads2, 0, s>>>(p);           \
-        else raster_kernel<2, false, MWV><<<tiles, kRasterThreads2, 0, s>>>(p);             \
+        if (fo) raster_kernel<2, true, MWV><<<tiles, kRasterThreads, 0, s>>>(p);           \
+        else raster_kernel<2, false, MWV><<<tiles, kRasterThreads, 0, s>>>(p);             \
     } while (0)
     switch (p.mask_words) {
     case 1: SS_FUSED(1); break;

@@ -113,11 +113,9 @@ def device_context(device: int = 0) -> Context:
 
 
 def _bind_scene(ctx: Context, scene: GaussianScene) -> None:
-    key = (id(scene), len(scene))
-    if getattr(ctx, "_scene_key", None) != key or getattr(ctx, "_scene_ref", None) is not scene:
-        ctx.set_scene(scene.mean, scene.scale, scene.quat_xyzw, scene.opacity)
-        ctx._scene_key = key
-        ctx._scene_ref = scene
+    """Upload the scene for this call (N x 48 B); no identity caching, since
+    arrays may be mutated in place between calls."""
+    ctx.set_scene(scene.mean, scene.scale, scene.quat_xyzw, scene.opacity)
 
 
 def camera_scaled_to(cam: CameraPose, width: int, height: int) -> CameraPose:
