@@ -115,19 +115,18 @@ struct ProfState {
 struct Lane {
     cudaStream_t stream = nullptr;
     cudaEvent_t contract_done = nullptr, done = nullptr;
-    DevBuf rec, keys, flags, keys_sel, ids_sel, keys_sorted, order, rec_sorted, ntiles, offsets;
-    DevBuf tile_keys, tile_vals, tile_keys_sorted, tile_ranks, tile_start, tile_end;
-    DevBuf cub_tmp, num_sel, k32, k32_sorted, info;
+    DevBuf rec, keys, k32, k32s, order, iota, tile_count, tile_start, fill, list;
+    uint64_t iota_n = 0;           // entries of the 0..n-1 sequence in `iota`
+    uint64_t list_cap = 0;         // entries of `list`
+    DevBuf cub_tmp, info;
     DevBuf pix_bits, mask_bits, runs, run_offsets, clip, spans;
     DevBuf acc, touched, touched_list;
     uint64_t acc_elems = 0;        // zero-initialised elements of acc
     ViewInfo* h_info = nullptr;    // pinned
     uint32_t* h_u32 = nullptr;     // pinned scratch
     void release_all() {
-        DevBuf* b[] = {&rec, &keys, &flags, &keys_sel, &ids_sel, &keys_sorted, &order, &rec_sorted, &ntiles, &offsets,
-                       &tile_keys, &tile_vals, &tile_keys_sorted, &tile_ranks, &tile_start, &tile_end, &cub_tmp,
-                       &num_sel, &k32, &k32_sorted, &info, &pix_bits, &mask_bits, &runs, &run_offsets, &clip, &spans,
-                       &acc, &touched, &touched_list};
+        DevBuf* b[] = {&rec, &keys, &k32, &k32s, &order, &iota, &tile_count, &tile_start, &fill, &list, &cub_tmp, &info, &pix_bits, &mask_bits,
+                       &runs, &run_offsets, &clip, &spans, &acc, &touched, &touched_list};
         for (auto* x : b) x->release();
         if (h_info) cudaFreeHost(h_info);
         if (h_u32) cudaFreeHost(h_u32);
@@ -159,6 +158,8 @@ struct ss_ctx {
     uint32_t n_lanes = 2;
     cudaEvent_t ev_user = nullptr;
     ss::DevBuf cub_tmp, num_sel, info; // store / query scratch
+    ss::DevBuf vstat; // per-view status of the last batch
+    uint64_t cap_n_surv = 0;
     ss::ViewInfo* h_init = nullptr;    // pinned
     uint32_t* h_u32 = nullptr;         // pinned scratch
 
@@ -239,14 +240,14 @@ void check_camera(const ss_camera* cam) {
 }
 
 struct Geometry {
-    uint64_t n_surv = 0;
-    uint64_t n_inst = 0;
     uint32_t tiles_x = 0, tiles_y = 0, tiles = 0;
 };
 
-// project -> ordered compaction -> depth sort -> gather -> tile keys -> tile sort -> ranges
-Geometry run_geometry(ss_ctx* c, Lane& L, cudaStream_t s, const ss_camera& cam, int err_kind,
-                      const char* err_prefix) {
+// project (+ per-tile instance counts) -> scan -> scatter ids into tile
+// slices -> per-tile (depth, id) sort.  No host synchronisation: sizes,
+// offsets and key ranges stay on the device; a view whose tile lists would
+// overflow the list buffer raises info->overflow and its compositor skips.
+Geometry run_geometry(ss_ctx* c, Lane& L, cudaStream_t s, const ss_camera& cam) {
     Geometry g;
     const uint64_t N = c->n;
     g.tiles_x = (cam.width + kTile - 1) / kTile;
@@ -255,17 +256,10 @@ Geometry run_geometry(ss_ctx* c, Lane& L, cudaStream_t s, const ss_camera& cam, 
 
     auto* rec = static_cast<SplatRec*>(L.rec.ensure(std::max<uint64_t>(N, 1) * sizeof(SplatRec)));
     auto* keys = static_cast<unsigned long long*>(L.keys.ensure(std::max<uint64_t>(N, 1) * 8));
-    auto* flags = static_cast<uint8_t*>(L.flags.ensure(std::max<uint64_t>(N, 1)));
-    auto* keys_sel = static_cast<unsigned long long*>(L.keys_sel.ensure(std::max<uint64_t>(N, 1) * 8));
-    auto* ids_sel = static_cast<uint32_t*>(L.ids_sel.ensure(std::max<uint64_t>(N, 1) * 4));
-    auto* keys_sorted = static_cast<unsigned long long*>(L.keys_sorted.ensure(std::max<uint64_t>(N, 1) * 8));
-    auto* order = static_cast<uint32_t*>(L.order.ensure(std::max<uint64_t>(N, 1) * 4));
-    auto* rec_sorted = static_cast<SplatRec*>(L.rec_sorted.ensure(std::max<uint64_t>(N, 1) * sizeof(SplatRec)));
-    auto* ntiles = static_cast<uint32_t*>(L.ntiles.ensure((N + 1) * 4));
-    auto* offsets = static_cast<uint32_t*>(L.offsets.ensure((N + 1) * 4));
-    auto* num_sel = static_cast<int*>(L.num_sel.ensure(16));
-    auto* tstart = static_cast<uint32_t*>(L.tile_start.ensure((size_t)g.tiles * 4));
-    auto* tend = static_cast<uint32_t*>(L.tile_end.ensure((size_t)g.tiles * 4));
+    if (g.tiles > 50000u) throw Error(SS_ERR_CONTRACT, "raster resolution too large (more than 50000 16x16 tiles)");
+    auto* tstart = static_cast<uint32_t*>(L.tile_start.ensure((g.tiles + 1ull) * 4));
+    if (L.list_cap == 0) L.list_cap = std::max<uint64_t>(16 * N, 1u << 20);
+    auto* list = static_cast<uint32_t*>(L.list.ensure(L.list_cap * 4));
     ViewInfo* info = L.info.as<ViewInfo>();
 
     reset_info(c, L, s);
@@ -279,126 +273,61 @@ Geometry run_geometry(ss_ctx* c, Lane& L, cudaStream_t s, const ss_camera& cam, 
         p.cam = cam;
         p.rec = rec;
         p.keys = keys;
-        p.flags = flags;
+        p.tile_count = nullptr;
+        p.tiles_x = g.tiles_x;
         p.info = info;
         p.dbg = nullptr;
         own_launch(c, launch_project(p, s), SS_K_PROJECT);
-        // ordered compaction of (depth key, id) for the survivors
-        size_t tb = 0, tb2 = 0;
-        cub::CountingInputIterator<uint32_t> ids(0);
-        SS_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, keys, flags, keys_sel, num_sel, (int)N, s));
-        SS_CUDA(cub::DeviceSelect::Flagged(nullptr, tb2, ids, flags, ids_sel, num_sel + 1, (int)N, s));
-        void* tmp = L.cub_tmp.ensure(std::max(tb, tb2));
-        tb = L.cub_tmp.bytes;
-        SS_CUDA(cub::DeviceSelect::Flagged(tmp, tb, keys, flags, keys_sel, num_sel, (int)N, s));
-        SS_CUDA(cub::DeviceSelect::Flagged(tmp, tb, ids, flags, ids_sel, num_sel + 1, (int)N, s));
-        c->launches_cub += 4;
-        c->prof.launches[SS_K_PROJECT] += 4;
         c->prof.bytes[SS_K_PROJECT] += 44.0 * (double)N;
     }
-    sync_info(L, s);
-    if (L.h_info->err_count)
-        throw Error(err_kind, std::string(err_prefix) + "singular screen covariance for gaussian " +
-                                  std::to_string(L.h_info->err_gid));
-    g.n_surv = L.h_info->n_surv;
-    const uint64_t n = g.n_surv;
-    c->prof.bytes[SS_K_PROJECT] += 76.0 * (double)n;
-
-    SS_CUDA(cudaMemsetAsync(tstart, 0, (size_t)g.tiles * 4, s));
-    SS_CUDA(cudaMemsetAsync(tend, 0, (size_t)g.tiles * 4, s));
-    if (n == 0) return g;
-
+    auto* k32 = static_cast<uint32_t*>(L.k32.ensure(std::max<uint64_t>(N, 1) * 4));
+    auto* k32s = static_cast<uint32_t*>(L.k32s.ensure(std::max<uint64_t>(N, 1) * 4));
+    auto* order = static_cast<uint32_t*>(L.order.ensure(std::max<uint64_t>(N, 1) * 4));
     {
+        // depth order of all Gaussians (culled ones last), no host round trip
         Scope sc(c, s, SS_K_SORT);
-        // depth sort on 32-bit narrowed keys (stable => ties keep id order), then
-        // an exact fixup of the rare runs that share a narrowed key
-        const uint32_t hb = bits_for(L.h_info->min_key ^ L.h_info->max_key);
-        const uint32_t shift = hb > 32 ? hb - 32 : 0;
-        const uint32_t end_bit = std::max<uint32_t>(1, std::min<uint32_t>(hb, 32));
-        auto* k32 = static_cast<uint32_t*>(L.k32.ensure(std::max<uint64_t>(n, 1) * 4));
-        auto* k32s = static_cast<uint32_t*>(L.k32_sorted.ensure(std::max<uint64_t>(n, 1) * 4));
-        own_launch(c, launch_narrow_keys(keys_sel, n, L.h_info->min_key, shift, k32, s), SS_K_SORT);
-        size_t tb = 0;
-        SS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k32, k32s, ids_sel, order, (int)n, 0, (int)end_bit, s));
-        void* tmp = L.cub_tmp.ensure(tb);
-        tb = L.cub_tmp.bytes;
-        SS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k32, k32s, ids_sel, order, (int)n, 0, (int)end_bit, s));
-        if (shift > 0) own_launch(c, launch_tie_fixup(k32s, n, keys, order, s), SS_K_SORT);
-        (void)keys_sorted;
-        c->launches_cub += 1;
-        c->prof.launches[SS_K_SORT] += 1;
-        c->prof.bytes[SS_K_SORT] += 24.0 * (double)n;
-    }
-    {
-        Scope sc(c, s, SS_K_BIN);
-        own_launch(c, launch_gather(order, n, rec, rec_sorted, ntiles, s), SS_K_BIN);
-        SS_CUDA(cudaMemsetAsync(ntiles + n, 0, 4, s));
-        size_t tb = 0;
-        SS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, ntiles, offsets, (int)(n + 1), s));
-        void* tmp = L.cub_tmp.ensure(tb);
-        tb = L.cub_tmp.bytes;
-        SS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, ntiles, offsets, (int)(n + 1), s));
-        c->launches_cub += 1;
-        c->prof.launches[SS_K_BIN] += 1;
-        SS_CUDA(cudaMemcpyAsync(L.h_u32, offsets + n, 4, cudaMemcpyDeviceToHost, s));
-        SS_CUDA(cudaStreamSynchronize(s));
-    }
-    g.n_inst = L.h_u32[0];
-    const uint64_t I = g.n_inst;
-    const bool k16 = g.tiles <= 65536u;
-    void* tkeys = L.tile_keys.ensure(std::max<uint64_t>(I, 1) * 4);
-    auto* tvals = static_cast<uint32_t*>(L.tile_vals.ensure(std::max<uint64_t>(I, 1) * 4));
-    void* tkeys_sorted = L.tile_keys_sorted.ensure(std::max<uint64_t>(I, 1) * 4);
-    auto* tranks = static_cast<uint32_t*>(L.tile_ranks.ensure(std::max<uint64_t>(I, 1) * 4));
-    {
-        Scope sc(c, s, SS_K_BIN);
-        own_launch(c, launch_emit_keys(rec_sorted, offsets, n, g.tiles_x, tkeys, k16, tvals, s), SS_K_BIN);
-        c->prof.bytes[SS_K_BIN] += 128.0 * (double)n + 8.0 * (double)I;
-    }
-    {
-        Scope sc(c, s, SS_K_SORT);
-        const uint32_t tbits = bits_for(g.tiles - 1);
-        size_t tb = 0;
-        if (k16) {
-            auto* kin = static_cast<uint16_t*>(tkeys);
-            auto* kout = static_cast<uint16_t*>(tkeys_sorted);
-            SS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, tvals, tranks, (int)I, 0, (int)tbits, s));
-            void* tmp = L.cub_tmp.ensure(tb);
-            tb = L.cub_tmp.bytes;
-            SS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, kin, kout, tvals, tranks, (int)I, 0, (int)tbits, s));
-        } else {
-            auto* kin = static_cast<uint32_t*>(tkeys);
-            auto* kout = static_cast<uint32_t*>(tkeys_sorted);
-            SS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, tvals, tranks, (int)I, 0, (int)tbits, s));
-            void* tmp = L.cub_tmp.ensure(tb);
-            tb = L.cub_tmp.bytes;
-            SS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, kin, kout, tvals, tranks, (int)I, 0, (int)tbits, s));
+        own_launch(c, launch_narrow_keys(keys, N, info, k32, s), SS_K_SORT);
+        if (L.iota_n < N) {
+            std::vector<uint32_t> h(N);
+            for (uint64_t i = 0; i < N; ++i) h[i] = (uint32_t)i;
+            SS_CUDA(cudaMemcpy(L.iota.ensure(N * 4), h.data(), N * 4, cudaMemcpyHostToDevice));
+            L.iota_n = N;
         }
+        const uint32_t* iota = L.iota.as<uint32_t>();
+        size_t tb = 0;
+        SS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k32, k32s, iota, order, (int)N, 0, 32, s));
+        void* tmp = L.cub_tmp.ensure(tb);
+        tb = L.cub_tmp.bytes;
+        SS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k32, k32s, iota, order, (int)N, 0, 32, s));
         c->launches_cub += 1;
         c->prof.launches[SS_K_SORT] += 1;
-        c->prof.bytes[SS_K_SORT] += 16.0 * (double)I;
+        own_launch(c, launch_tie_fixup(k32s, N, keys, order, s), SS_K_SORT);
     }
     {
         Scope sc(c, s, SS_K_BIN);
-        own_launch(c, launch_tile_ranges(tkeys_sorted, k16, I, tstart, tend, s), SS_K_BIN);
-        c->prof.bytes[SS_K_BIN] += 4.0 * (double)I + 8.0 * g.tiles;
+        uint64_t chunk = 0;
+        const uint32_t nch = tile_chunks(N, &chunk);
+        auto* ccounts = static_cast<uint32_t*>(L.tile_count.ensure((uint64_t)nch * g.tiles * 4 + 4));
+        auto* totals = static_cast<uint32_t*>(L.fill.ensure((uint64_t)g.tiles * 4 + 4));
+        own_launch(c,
+                   launch_tile_bins(rec, k32s, order, keys, N, g.tiles, g.tiles_x, ccounts, totals, tstart, list,
+                                    L.list_cap, info, s),
+                   SS_K_BIN, 5);
     }
-    c->cnt_vis += n;
-    c->cnt_inst += I;
     return g;
 }
 
-RasterParams raster_params(Lane& L, const ss_camera& cam, const Geometry& g) {
+RasterParams raster_params(ss_ctx* c, Lane& L, const ss_camera& cam, const Geometry& g) {
     RasterParams p;
     std::memset(&p, 0, sizeof(p));
-    p.rec_sorted = L.rec_sorted.as<SplatRec>();
-    p.tile_ranks = L.tile_ranks.as<uint32_t>();
+    p.rec = L.rec.as<SplatRec>();
+    p.tile_list = L.list.as<uint32_t>();
     p.tile_start = L.tile_start.as<uint32_t>();
-    p.tile_end = L.tile_end.as<uint32_t>();
     p.width = cam.width;
     p.height = cam.height;
     p.tiles_x = g.tiles_x;
     p.info = L.info.as<ViewInfo>();
+    (void)c;
     return p;
 }
 
@@ -463,14 +392,12 @@ void build_mask_bits(ss_ctx* c, Lane& L, cudaStream_t s, const ss_camera& cam, c
     c->prof.bytes[SS_K_MASKS] += nr * 4.0 + (double)P * ((M + 7) / 8);
 }
 
-void encode_one(ss_ctx* c, Lane& L, Lane& prev, const ss_camera& cam, const ss_view_masks* vm, int mode) {
+void encode_one(ss_ctx* c, Lane& L, Lane& prev, const ss_camera& cam, const ss_view_masks* vm, int mode,
+                ViewInfo* vstat_slot) {
     check_camera(&cam);
-    if (!c->sums) throw Error(SS_ERR_CONTRACT, "ss_encode_view before ss_encode_begin");
-    if (c->n == 0) return;
     const uint32_t M = vm ? vm->n_masks : 0;
     if (M > 128) throw Error(SS_ERR_CONTRACT, "at most 128 masks per view are supported");
     const uint32_t words = mask_words_for(M);
-    const std::string prefix = "image " + std::to_string(cam.image_id) + ": ";
     cudaStream_t s = L.stream;
     if (M) build_mask_bits(c, L, s, cam, vm, words, cam.image_id);
     const float* d_clip = vm && (vm->flags & SS_MASKS_ON_DEVICE) ? vm->clip : nullptr;
@@ -481,84 +408,125 @@ void encode_one(ss_ctx* c, Lane& L, Lane& prev, const ss_camera& cam, const ss_v
         SS_CUDA(cudaMemcpyAsync(dc, vm->clip, (size_t)M * c->dim * 4, cudaMemcpyHostToDevice, s));
         c->prof.bytes[SS_K_H2D] += (double)M * c->dim * 4;
     }
-    const Geometry g = run_geometry(c, L, s, cam, SS_ERR_DATA, prefix.c_str());
-    c->cnt_views += 1;
-    if (g.n_surv == 0 || M == 0) return;
-
-    // per-(rank, mask) scalars: grow-only and kept zero by consume-and-clear
-    const uint64_t need = g.n_surv * (uint64_t)M;
-    if (need > L.acc_elems) {
-        const uint64_t cap = std::max<uint64_t>(need, c->n * (uint64_t)std::min<uint32_t>(std::max(M, 16u), 128u));
-        L.acc.release();
-        L.acc.ensure(cap * 4);
-        SS_CUDA(cudaMemsetAsync(L.acc.p, 0, L.acc.bytes, s));
-        L.acc_elems = L.acc.bytes / 4;
+    const Geometry g = run_geometry(c, L, s, cam);
+    if (M) {
+        // per-(Gaussian, mask) scalars: grow-only and kept zero by consume-and-clear
+        const uint64_t need = c->n * (uint64_t)M;
+        if (need > L.acc_elems) {
+            L.acc.release();
+            L.acc.ensure(need * 4);
+            SS_CUDA(cudaMemsetAsync(L.acc.p, 0, L.acc.bytes, s));
+            L.acc_elems = L.acc.bytes / 4;
+        }
+        auto* touched = static_cast<uint32_t*>(L.touched.p);
+        if (L.touched.bytes < c->n * 4) {
+            L.touched.release();
+            touched = static_cast<uint32_t*>(L.touched.ensure(c->n * 4));
+            SS_CUDA(cudaMemsetAsync(touched, 0, L.touched.bytes, s));
+        }
+        auto* tlist = static_cast<uint32_t*>(L.touched_list.ensure(c->n * 4));
+        {
+            Scope sc(c, s, SS_K_RASTER);
+            RasterParams p = raster_params(c, L, cam, g);
+            p.pix_bits = L.pix_bits.as<uint32_t>();
+            p.mask_words = words;
+            p.n_masks = M;
+            p.acc = L.acc.as<float>();
+            p.touched = touched;
+            p.touched_list = tlist;
+            own_launch(c, launch_raster_fused(p, mode, g.tiles, s), SS_K_RASTER);
+        }
+        // contractions into the shared sums run in view order across the lanes
+        SS_CUDA(cudaStreamWaitEvent(s, prev.contract_done, 0));
+        {
+            Scope sc(c, s, SS_K_CONTRACT);
+            ContractParams q;
+            q.touched_list = tlist;
+            q.touched = touched;
+            q.acc = L.acc.as<float>();
+            q.n_masks = M;
+            q.clip = d_clip;
+            q.dim = c->dim;
+            q.sums = c->sums;
+            q.totals = c->totals;
+            q.info = L.info.as<ViewInfo>();
+            q.count_pairs = 1;
+            q.cum = c->counters.as<unsigned long long>();
+            own_launch(c, launch_contract(q, c->n, s), SS_K_CONTRACT);
+            c->prof.bytes[SS_K_CONTRACT] += (double)M * c->dim * 4;
+        }
+        SS_CUDA(cudaEventRecord(L.contract_done, s));
     }
-    auto* touched = static_cast<uint32_t*>(L.touched.p);
-    if (L.touched.bytes < c->n * 4) {
-        L.touched.release();
-        touched = static_cast<uint32_t*>(L.touched.ensure(c->n * 4));
-        SS_CUDA(cudaMemsetAsync(touched, 0, L.touched.bytes, s));
-    }
-    auto* tlist = static_cast<uint32_t*>(L.touched_list.ensure(c->n * 4));
-
-    {
-        Scope sc(c, s, SS_K_RASTER);
-        RasterParams p = raster_params(L, cam, g);
-        p.pix_bits = L.pix_bits.as<uint32_t>();
-        p.mask_words = words;
-        p.n_masks = M;
-        p.acc = L.acc.as<float>();
-        p.touched = touched;
-        p.touched_list = tlist;
-        own_launch(c, launch_raster_fused(p, mode, g.tiles, s), SS_K_RASTER);
-        const uint64_t P = (uint64_t)cam.width * cam.height;
-        c->prof.bytes[SS_K_RASTER] += 64.0 * (double)g.n_inst + (double)P * ((M + 7) / 8);
-    }
-    // contractions into the shared sums run in view order across the lanes
-    SS_CUDA(cudaStreamWaitEvent(s, prev.contract_done, 0));
-    {
-        Scope sc(c, s, SS_K_CONTRACT);
-        ContractParams q;
-        q.touched_list = tlist;
-        q.touched = touched;
-        q.order = L.order.as<uint32_t>();
-        q.acc = L.acc.as<float>();
-        q.n_masks = M;
-        q.clip = d_clip;
-        q.dim = c->dim;
-        q.sums = c->sums;
-        q.totals = c->totals;
-        q.info = L.info.as<ViewInfo>();
-        q.count_pairs = 1;
-        q.cum = c->counters.as<unsigned long long>();
-        own_launch(c, launch_contract(q, g.n_surv, s), SS_K_CONTRACT);
-        c->prof.bytes[SS_K_CONTRACT] += (double)M * c->dim * 4;
-    }
-    SS_CUDA(cudaEventRecord(L.contract_done, s));
+    SS_CUDA(cudaMemcpyAsync(vstat_slot, L.info.p, sizeof(ViewInfo), cudaMemcpyDeviceToDevice, s));
 }
 
+// Encodes a batch of views with no per-view host synchronisation; the host
+// looks at the per-view status once at the end: views whose tile lists
+// overflowed the list buffer contributed nothing and are re-run with a larger
+// buffer; singular covariances surface as the reference's per-image error.
 void encode_batch(ss_ctx* c, uint32_t nviews, const ss_camera* cams, const ss_view_masks* masks, int mode) {
-    // lanes start after everything already queued on the user stream
-    SS_CUDA(cudaEventRecord(c->ev_user, c->stream));
-    for (auto& L : c->lanes) SS_CUDA(cudaStreamWaitEvent(L.stream, c->ev_user, 0));
-    struct Join {
-        ss_ctx* c;
-        ~Join() {
-            // the user stream resumes after both lanes drain (also on errors)
-            for (auto& L : c->lanes) {
-                cudaEventRecord(L.done, L.stream);
-                cudaStreamWaitEvent(c->stream, L.done, 0);
+    if (!c->sums) throw Error(SS_ERR_CONTRACT, "ss_encode_view before ss_encode_begin");
+    if (nviews == 0 || c->n == 0) return;
+    auto* vstat = static_cast<ViewInfo*>(c->vstat.ensure((uint64_t)nviews * sizeof(ViewInfo)));
+    std::vector<ViewInfo> hstat(nviews);
+    std::vector<uint32_t> todo(nviews);
+    for (uint32_t v = 0; v < nviews; ++v) todo[v] = v;
+    for (int attempt = 0; attempt < 4 && !todo.empty(); ++attempt) {
+        // lanes start after everything already queued on the user stream
+        SS_CUDA(cudaEventRecord(c->ev_user, c->stream));
+        for (auto& L : c->lanes) SS_CUDA(cudaStreamWaitEvent(L.stream, c->ev_user, 0));
+        {
+            struct Join {
+                ss_ctx* c;
+                ~Join() {
+                    // the user stream resumes after both lanes drain (also on errors)
+                    for (auto& L : c->lanes) {
+                        cudaEventRecord(L.done, L.stream);
+                        cudaStreamWaitEvent(c->stream, L.done, 0);
+                    }
+                }
+            } join{c};
+            for (uint32_t v : todo) {
+                const uint32_t li = c->n_lanes > 1 ? c->next_lane : 0u;
+                Lane& L = c->lanes[li];
+                Lane& prev = c->lanes[li ^ 1u];
+                c->next_lane ^= 1u;
+                encode_one(c, L, prev, cams[v], masks ? &masks[v] : nullptr, mode, vstat + v);
             }
         }
-    } join{c};
-    for (uint32_t v = 0; v < nviews; ++v) {
-        const uint32_t li = c->n_lanes > 1 ? c->next_lane : 0u;
-        Lane& L = c->lanes[li];
-        Lane& prev = c->lanes[li ^ 1u];
-        c->next_lane ^= 1u;
-        encode_one(c, L, prev, cams[v], masks ? &masks[v] : nullptr, mode);
+        SS_CUDA(cudaMemcpyAsync(hstat.data(), vstat, (uint64_t)nviews * sizeof(ViewInfo), cudaMemcpyDeviceToHost,
+                                c->stream));
+        SS_CUDA(cudaStreamSynchronize(c->stream));
+        std::vector<uint32_t> again;
+        uint64_t need = 0;
+        for (uint32_t v : todo) {
+            const ViewInfo& st = hstat[v];
+            if (st.err_count)
+                throw Error(SS_ERR_DATA, "image " + std::to_string(cams[v].image_id) +
+                                             ": singular screen covariance for gaussian " + std::to_string(st.err_gid));
+            if (st.overflow) {
+                again.push_back(v);
+                need = std::max<uint64_t>(need, st.n_instances);
+                continue;
+            }
+            const double P = (double)cams[v].width * cams[v].height;
+            const uint32_t M = masks ? masks[v].n_masks : 0;
+            c->cnt_vis += st.n_surv;
+            c->cnt_inst += st.n_instances;
+            c->cnt_views += 1;
+            c->prof.bytes[SS_K_PROJECT] += 76.0 * (double)st.n_surv;
+            c->prof.bytes[SS_K_BIN] += 8.0 * (double)st.n_surv + 4.0 * (double)st.n_instances;
+            c->prof.bytes[SS_K_SORT] += 16.0 * (double)st.n_instances;
+            if (M) c->prof.bytes[SS_K_RASTER] += 64.0 * (double)st.n_instances + P * ((M + 7) / 8);
+        }
+        for (auto& L : c->lanes)
+            if (need > L.list_cap) {
+                L.list_cap = need + need / 4;
+                L.list.release();
+            }
+        todo.swap(again);
     }
+    if (!todo.empty()) throw Error(SS_ERR_CUDA, "tile-list buffer kept overflowing");
 }
 
 void profile_drain(ss_ctx* c) {
@@ -628,7 +596,7 @@ void ss_destroy(ss_ctx* c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     for (auto& L : c->lanes) cudaStreamSynchronize(L.stream);
-    ss::DevBuf* bufs[] = {&c->mean_op, &c->scale, &c->quat, &c->cub_tmp, &c->num_sel, &c->info, &c->pix_count,
+    ss::DevBuf* bufs[] = {&c->mean_op, &c->scale, &c->quat, &c->cub_tmp, &c->num_sel, &c->info, &c->vstat, &c->pix_count,
                           &c->pix_offset, &c->entries, &c->per_pixel_total, &c->alpha, &c->counters, &c->sums_buf,
                           &c->totals_buf, &c->store_rows, &c->store_ids, &c->qbuf, &c->qnorm, &c->scores,
                           &c->topk_ids, &c->topk_sims, &c->sel_flags, &c->thr_keys, &c->thr_keys_sorted, &c->thr_ids,
@@ -720,7 +688,8 @@ int ss_project(ss_ctx* c, const ss_camera* cam, ss_projected* out) {
         p.cam = *cam;
         p.rec = static_cast<SplatRec*>(L.rec.ensure(N * sizeof(SplatRec)));
         p.keys = static_cast<unsigned long long*>(L.keys.ensure(N * 8));
-        p.flags = static_cast<uint8_t*>(L.flags.ensure(N));
+        p.tile_count = nullptr;
+        p.tiles_x = 0;
         p.info = L.info.as<ViewInfo>();
         p.dbg = dbg;
         own_launch(c, launch_project(p, s), SS_K_PROJECT);
@@ -737,8 +706,23 @@ int ss_raster_capture(ss_ctx* c, const ss_camera* cam, int mode, uint64_t* n_ent
         set_device(c);
         cudaStream_t s = c->stream;
         const uint64_t P = (uint64_t)cam->width * cam->height;
+        const uint64_t N = c->n;
         ss::Lane& L = c->lanes[0];
-        const Geometry g = run_geometry(c, L, s, *cam, SS_ERR_NUMERIC, "");
+        // rasterize_weights_only (rasterizer.hpp:268-271): tile lists, then the
+        // counting and capture passes of the compositor
+        Geometry g;
+        for (int attempt = 0;; ++attempt) {
+            g = run_geometry(c, L, s, *cam);
+            SS_CUDA(cudaMemcpyAsync(L.h_info, L.info.p, sizeof(ViewInfo), cudaMemcpyDeviceToHost, s));
+            SS_CUDA(cudaStreamSynchronize(s));
+            if (!L.h_info->overflow) break;
+            if (attempt > 2) throw Error(SS_ERR_CUDA, "tile-list buffer kept overflowing");
+            L.list_cap = L.h_info->n_instances + L.h_info->n_instances / 4;
+            L.list.release();
+        }
+        if (L.h_info->err_count)
+            throw Error(SS_ERR_NUMERIC, "singular screen covariance for gaussian " + std::to_string(L.h_info->err_gid));
+        const uint64_t n_surv = L.h_info->n_surv, n_inst = L.h_info->n_instances;
         auto* cnt = static_cast<uint32_t*>(c->pix_count.ensure((P + 1) * 4));
         auto* off = static_cast<uint32_t*>(c->pix_offset.ensure((P + 1) * 4));
         auto* ppt = static_cast<float*>(c->per_pixel_total.ensure(P * 4));
@@ -746,8 +730,8 @@ int ss_raster_capture(ss_ctx* c, const ss_camera* cam, int mode, uint64_t* n_ent
         SS_CUDA(cudaMemsetAsync(cnt, 0, (P + 1) * 4, s));
         SS_CUDA(cudaMemsetAsync(ppt, 0, P * 4, s));
         SS_CUDA(cudaMemsetAsync(alp, 0, P * 4, s));
-        RasterParams p = raster_params(L, *cam, g);
-        if (g.n_surv) {
+        RasterParams p = raster_params(c, L, *cam, g);
+        if (n_surv) {
             p.pix_count = cnt;
             own_launch(c, launch_raster_count(p, mode, g.tiles, s), SS_K_RASTER);
         }
@@ -761,7 +745,7 @@ int ss_raster_capture(ss_ctx* c, const ss_camera* cam, int mode, uint64_t* n_ent
         SS_CUDA(cudaStreamSynchronize(s));
         const uint64_t E = c->h_u32[0];
         auto* ent = static_cast<ss_weight_entry*>(c->entries.ensure(std::max<uint64_t>(E, 1) * sizeof(ss_weight_entry)));
-        if (g.n_surv) {
+        if (n_surv) {
             p.pix_offset = off;
             p.entries = ent;
             p.per_pixel_total = ppt;
@@ -770,14 +754,14 @@ int ss_raster_capture(ss_ctx* c, const ss_camera* cam, int mode, uint64_t* n_ent
         }
         SS_CUDA(cudaStreamSynchronize(s));
         c->cap_entries = E;
-        c->cap_splats = g.n_surv;
-        c->cap_instances = g.n_inst;
+        c->cap_splats = n_surv;
+        c->cap_instances = n_inst;
         c->cap_width = cam->width;
         c->cap_height = cam->height;
         c->cap_tiles = g.tiles;
         if (n_entries) *n_entries = E;
-        if (n_splats) *n_splats = g.n_surv;
-        if (n_tile_instances) *n_tile_instances = g.n_inst;
+        if (n_splats) *n_splats = n_surv;
+        if (n_tile_instances) *n_tile_instances = n_inst;
     });
 }
 
@@ -791,26 +775,21 @@ int ss_raster_fetch(ss_ctx* c, ss_weight_entry* entries, float* per_pixel_total,
             SS_CUDA(cudaMemcpy(entries, c->entries.p, c->cap_entries * sizeof(ss_weight_entry), cudaMemcpyDeviceToHost));
         if (per_pixel_total && P) SS_CUDA(cudaMemcpy(per_pixel_total, c->per_pixel_total.p, P * 4, cudaMemcpyDeviceToHost));
         if (alpha && P) SS_CUDA(cudaMemcpy(alpha, c->alpha.p, P * 4, cudaMemcpyDeviceToHost));
-        if (splat_gid && c->cap_splats)
-            SS_CUDA(cudaMemcpy(splat_gid, c->lanes[0].order.p, c->cap_splats * 4, cudaMemcpyDeviceToHost));
-        if (tile_offsets || tile_splats) {
-            std::vector<uint32_t> st(c->cap_tiles), en(c->cap_tiles);
-            if (c->cap_tiles) {
-                SS_CUDA(cudaMemcpy(st.data(), c->lanes[0].tile_start.p, c->cap_tiles * 4, cudaMemcpyDeviceToHost));
-                SS_CUDA(cudaMemcpy(en.data(), c->lanes[0].tile_end.p, c->cap_tiles * 4, cudaMemcpyDeviceToHost));
-            }
-            if (tile_offsets) {
-                // tiles are contiguous in key order, so start of tile t is the
-                // running count of instances in tiles < t
-                uint32_t run = 0;
-                for (uint32_t t = 0; t < c->cap_tiles; ++t) {
-                    tile_offsets[t] = run;
-                    run += en[t] - st[t];
-                }
-                tile_offsets[c->cap_tiles] = run;
-            }
-            if (tile_splats && c->cap_instances)
-                SS_CUDA(cudaMemcpy(tile_splats, c->lanes[0].tile_ranks.p, c->cap_instances * 4, cudaMemcpyDeviceToHost));
+        std::vector<uint32_t> order(c->cap_splats);
+        if (c->cap_splats)
+            SS_CUDA(cudaMemcpy(order.data(), c->lanes[0].order.p, c->cap_splats * 4, cudaMemcpyDeviceToHost));
+        if (splat_gid) std::copy(order.begin(), order.end(), splat_gid);
+        if (tile_offsets && c->cap_tiles)
+            SS_CUDA(cudaMemcpy(tile_offsets, c->lanes[0].tile_start.p, (c->cap_tiles + 1ull) * 4,
+                               cudaMemcpyDeviceToHost));
+        if (tile_splats && c->cap_instances) {
+            // tile lists hold Gaussian ids; report them as indices into the
+            // depth-sorted splat list, as the reference's tile_bins do
+            std::vector<uint32_t> ids(c->cap_instances);
+            SS_CUDA(cudaMemcpy(ids.data(), c->lanes[0].list.p, c->cap_instances * 4, cudaMemcpyDeviceToHost));
+            std::vector<uint32_t> rank_of(c->n, 0xffffffffu);
+            for (uint64_t r = 0; r < order.size(); ++r) rank_of[order[r]] = (uint32_t)r;
+            for (uint64_t i = 0; i < ids.size(); ++i) tile_splats[i] = rank_of[ids[i]];
         }
     });
 }

@@ -148,6 +148,12 @@ __global__ void __launch_bounds__(256) project_kernel(ProjectParams p) {
                 v = cvt_i32_x86(floor(da(mu_y, ry)));
                 const int32_t y1 = v < H - 1 ? v : H - 1;
                 if (!(x0 > x1 || y0 > y1)) {
+                    if (p.tile_count) {
+                        // rasterizer.hpp:185-194: the splat joins every tile its box covers
+                        for (uint32_t ty = (uint32_t)y0 / kTile; ty <= (uint32_t)y1 / kTile; ++ty)
+                            for (uint32_t tx = (uint32_t)x0 / kTile; tx <= (uint32_t)x1 / kTile; ++tx)
+                                atomicAdd(p.tile_count + ty * p.tiles_x + tx, 1u);
+                    }
                     r.x0 = (uint16_t)x0;
                     r.x1 = (uint16_t)x1;
                     r.y0 = (uint16_t)y0;
@@ -160,7 +166,6 @@ __global__ void __launch_bounds__(256) project_kernel(ProjectParams p) {
             }
         }
         p.keys[id] = key;
-        p.flags[id] = survive ? 1 : 0;
     }
     // block-reduce survivors' count and key range, one atomic per block
     const unsigned long long kmin = survive ? key : ~0ull;
@@ -200,27 +205,7 @@ __global__ void __launch_bounds__(256) project_kernel(ProjectParams p) {
 }
 
 // ------------------------------------------------------------- compositor
-// One CTA per 16x16 tile, one thread per pixel; the tile's depth-ordered
-// splat list is staged through shared memory 256 records at a time and every
-// thread composites its own pixel front to back (rasterizer.hpp:112-133,
-// 213-247), with the reference's box test first, Mahalanobis cutoff, alpha
-// clamp, skip rule, weight cutoff and transmittance floor.
-//
-// Work shaping (no effect on the arithmetic): each warp owns an 8x4 pixel
-// block of the tile, so a warp-uniform test of the splat's box against the
-// block skips splats that cannot touch any of its pixels, and a warp whose 32
-// pixels have all terminated stops walking the batch.
-//
-// KIND 0: count contributions per pixel (sizes the capture).
-// KIND 1: capture -- write WeightEntry records at per-pixel offsets, in rank
-//         order (= the reference's stable_sort by pixel), per_pixel_total and
-//         alpha = 1 - T_final.
-// KIND 2: fused -- gate each contribution by the pixel's mask bitset and add
-//         w into per-(rank, mask) fp32 scalars; lanes with identical bitsets
-//         are summed with a fixed-order butterfly first, so each (splat,
-//         warp, bitset group) costs one atomic per mask, never a 512-d scatter.
-// Per-pixel compositing state (rasterizer.hpp:112-133) for one of the two
-// pixels a thread owns.
+// Per-pixel compositing state (rasterizer.hpp:112-133).
 struct PixelState {
     double T;
     double total;
@@ -265,11 +250,11 @@ __device__ __forceinline__ bool composite_one(PixelState& ps, const SplatRec& s,
 // then lane m adds the group sum to mask 32w+m when the group has that bit.
 template <int MW>
 __device__ __forceinline__ void gate_and_accumulate(const RasterParams& p, bool contrib, float wf, uint32_t grp,
-                                                    const uint32_t (&bits)[MW], uint32_t rank, uint32_t lane) {
+                                                    const uint32_t (&bits)[MW], uint32_t gid, uint32_t lane) {
     const uint32_t em = __ballot_sync(0xffffffffu, contrib);
     if (!em) return;
     uint32_t rem = em;
-    float* row = p.acc + (size_t)rank * p.n_masks + lane;
+    float* row = p.acc + (size_t)gid * p.n_masks + lane;
     while (rem) {
         const int leader = __ffs(rem) - 1;
         const uint32_t gm = __shfl_sync(0xffffffffu, grp, leader);
@@ -284,10 +269,10 @@ __device__ __forceinline__ void gate_and_accumulate(const RasterParams& p, bool 
         rem &= ~gm;
     }
     if ((int)lane == __ffs(em) - 1) {
-        // first toucher of this rank appends it to the contraction list
-        if (*reinterpret_cast<volatile uint32_t*>(p.touched + rank) == 0u && atomicExch(p.touched + rank, 1u) == 0u) {
+        // first toucher of this Gaussian appends it to the contraction list
+        if (*reinterpret_cast<volatile uint32_t*>(p.touched + gid) == 0u && atomicExch(p.touched + gid, 1u) == 0u) {
             const unsigned long long slot = atomicAdd(&p.info->n_touched, 1ull);
-            p.touched_list[slot] = rank;
+            p.touched_list[slot] = gid;
         }
     }
 }
@@ -314,15 +299,15 @@ __device__ __forceinline__ uint32_t match_bits(const uint32_t (&bits)[MW]) {
 // the splats whose box contains it, in depth order.
 //
 // KIND 0: count contributions per pixel (sizes the capture).
-// KIND 1: capture -- write WeightEntry records at per-pixel offsets, in rank
+// KIND 1: capture -- write WeightEntry records at per-pixel offsets, in depth
 //         order (= the reference's stable_sort by pixel), per_pixel_total and
 //         alpha = 1 - T_final.
 // KIND 2: fused -- gate each contribution by the pixel's SAM-mask bitset and
-//         add w into per-(rank, mask) fp32 scalars (never a 512-d scatter).
+//         add w into per-(Gaussian, mask) fp32 scalars (never a 512-d scatter).
 template <int KIND, bool FALLOFF, int MW>
 __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) {
     __shared__ SplatRec srec[kRasterThreads]; // warp w stages its hits in srec[32w, 32w+32)
-    __shared__ uint32_t srank[kRasterThreads];
+    __shared__ uint32_t sgid[kRasterThreads];
     __shared__ unsigned long long stab[256];
     stab[threadIdx.x] = kExpTab[threadIdx.x];
 
@@ -331,9 +316,10 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     const uint32_t bx0 = tx * kTile + 8u * (warp & 1u), by0 = ty * kTile + 4u * (warp >> 1);
     const uint32_t bx1 = bx0 + 7u, by1 = by0 + 3u;
-    const uint32_t start = p.tile_start[tile], end = p.tile_end[tile];
+    const uint32_t start = p.tile_start[tile], end = p.tile_start[tile + 1];
+    if (p.info->overflow) return; // tile lists incomplete: the view is re-run by the host
     SplatRec* wrec = srec + 32u * warp;
-    uint32_t* wrank = srank + 32u * warp;
+    uint32_t* wgid = sgid + 32u * warp;
 
     PixelState ps;
     ps.px = bx0 + (lane & 7u);
@@ -368,8 +354,8 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
     uint32_t nr = 0;
     uint2 nbox = make_uint2(0u, 0u);
     if (start + lane < end) {
-        nr = __ldg(p.tile_ranks + start + lane);
-        nbox = __ldg(reinterpret_cast<const uint2*>(&p.rec_sorted[nr].x0));
+        nr = __ldg(p.tile_list + start + lane);
+        nbox = __ldg(reinterpret_cast<const uint2*>(&p.rec[nr].x0));
     }
     for (uint32_t base = start; base < end; base += 32u) {
         if (__all_sync(0xffffffffu, ps.done)) break;
@@ -377,21 +363,21 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
         const uint32_t r = nr;
         const uint2 box = nbox;
         if (i + 32u < end) { // software prefetch of the next chunk
-            nr = __ldg(p.tile_ranks + i + 32u);
-            nbox = __ldg(reinterpret_cast<const uint2*>(&p.rec_sorted[nr].x0));
+            nr = __ldg(p.tile_list + i + 32u);
+            nbox = __ldg(reinterpret_cast<const uint2*>(&p.rec[nr].x0));
         }
         const bool hit = i < end && !((box.x >> 16) < bx0 || (box.x & 0xffffu) > bx1 || (box.y >> 16) < by0 ||
                                       (box.y & 0xffffu) > by1);
         const uint32_t cand = __ballot_sync(0xffffffffu, hit);
         if (hit) {
             const uint32_t slot = __popc(cand & ((1u << lane) - 1u));
-            const uint4* src = reinterpret_cast<const uint4*>(p.rec_sorted + r);
+            const uint4* src = reinterpret_cast<const uint4*>(p.rec + r);
             uint4* dst = reinterpret_cast<uint4*>(wrec + slot);
             dst[0] = __ldg(src);
             dst[1] = __ldg(src + 1);
             dst[2] = __ldg(src + 2);
             dst[3] = make_uint4(box.x, box.y, 0u, 0u); // box already prefetched
-            wrank[slot] = r;
+            wgid[slot] = r;
         }
         __syncwarp();
         const uint32_t nh = __popc(cand);
@@ -409,7 +395,7 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
                     ps.total = da(ps.total, (double)wf);
                 }
             } else {
-                gate_and_accumulate<MW>(p, c, wf, grp, bits, wrank[j], lane);
+                gate_and_accumulate<MW>(p, c, wf, grp, bits, wgid[j], lane);
             }
             if (__all_sync(0xffffffffu, ps.done)) break;
         }

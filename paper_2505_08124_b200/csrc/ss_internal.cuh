@@ -10,7 +10,6 @@ namespace ss {
 
 constexpr uint32_t kTile = 16;          // rasterizer.hpp:30 kTileSize
 constexpr int kRasterThreads = 256;     // pixels of a 16x16 tile
-constexpr int kRasterThreads2 = 128;    // compositor threads per tile (2 pixels each)
 constexpr int kMaxMaskWords = 4;        // up to 128 masks per view
 
 // Per-splat record staged through shared memory by the compositor.  64 B so a
@@ -26,16 +25,18 @@ struct __align__(16) SplatRec {
 };
 static_assert(sizeof(SplatRec) == 64, "SplatRec must stay 64 B");
 
-// Per-view scalar results the host reads back (one small D2H per view).
+// Per-view scalars kept on the device; the host reads them only at batch
+// boundaries (copied into a per-view status array), never per view.
 struct ViewInfo {
     unsigned long long n_surv;       // visible, box-non-empty splats
     unsigned long long min_key;      // min / max depth bit patterns over them
     unsigned long long max_key;
-    unsigned long long n_instances;  // tile instances I_v
+    unsigned long long n_instances;  // tile instances I_v (total of tile_count)
     unsigned int err_count;          // singular screen covariances
     unsigned int err_gid;            // smallest gid with one
-    unsigned long long n_touched;    // G_v (ranks with any masked weight)
-    unsigned long long n_pairs;      // K_v (nonzero (rank, mask) scalars)
+    unsigned long long n_touched;    // G_v (Gaussians with any masked weight)
+    unsigned int overflow;           // tile-list capacity exceeded: view skipped
+    unsigned int pad;
 };
 
 struct ProjectParams {
@@ -45,17 +46,17 @@ struct ProjectParams {
     uint64_t n;
     ss_camera cam;
     SplatRec* rec;        // [n] by gid
-    unsigned long long* keys; // [n] depth bits
-    uint8_t* flags;       // [n] survive
+    unsigned long long* keys; // [n] depth bits (~0 when culled)
+    uint32_t* tile_count; // [tiles] instances per tile (atomic), or null
+    uint32_t tiles_x;
     ViewInfo* info;
     ss_projected* dbg;    // optional Projected2D dump (parity entry point)
 };
 
 struct RasterParams {
-    const SplatRec* rec_sorted; // by rank
-    const uint32_t* tile_ranks; // per tile instance, rank
-    const uint32_t* tile_start;
-    const uint32_t* tile_end;
+    const SplatRec* rec;        // by Gaussian id
+    const uint32_t* tile_list;  // per tile: Gaussian ids in (depth, id) order
+    const uint32_t* tile_start; // [tiles + 1]; tile t is tile_list[start[t], start[t+1])
     uint32_t width, height, tiles_x;
     // capture mode
     uint32_t* pix_count;           // pass 0 output [P]
@@ -66,9 +67,9 @@ struct RasterParams {
     // fused mode
     const uint32_t* pix_bits;      // [P * mask_words]
     uint32_t mask_words, n_masks;
-    float* acc;                    // [n_surv * n_masks] per-(rank, mask) scalars
-    uint32_t* touched;             // [n_surv] 0/1
-    uint32_t* touched_list;        // [n_surv]
+    float* acc;                    // [N * n_masks] per-(Gaussian, mask) scalars
+    uint32_t* touched;             // [N] 0/1
+    uint32_t* touched_list;        // [N] Gaussian ids
     ViewInfo* info;
 };
 

@@ -7,8 +7,7 @@ namespace ss {
 struct ContractParams {
     const uint32_t* touched_list;
     uint32_t* touched;
-    const uint32_t* order; // rank -> gid
-    float* acc;            // [n_surv x n_masks]
+    float* acc;            // [N x n_masks]
     uint32_t n_masks;
     const float* clip;     // [n_masks x dim]
     uint32_t dim;
@@ -23,16 +22,15 @@ cudaError_t launch_rle_to_bits(const uint32_t* runs, const uint64_t* run_offsets
                                uint32_t* bits, uint4* spans, unsigned int* n_spans, cudaStream_t s);
 cudaError_t launch_resample_bits(const uint32_t* src, uint32_t sw, uint32_t sh, uint32_t* dst, uint32_t tw,
                                  uint32_t th, uint32_t words, cudaStream_t s);
-cudaError_t launch_gather(const uint32_t* order, uint64_t n, const SplatRec* rec, SplatRec* rec_sorted,
-                          uint32_t* ntiles, cudaStream_t s);
-cudaError_t launch_emit_keys(const SplatRec* rec_sorted, const uint32_t* offsets, uint64_t n, uint32_t tiles_x,
-                             void* keys, bool keys16, uint32_t* vals, cudaStream_t s);
-cudaError_t launch_tile_ranges(const void* keys, bool keys16, uint64_t n, uint32_t* start, uint32_t* end,
+uint32_t tile_chunks(uint64_t n, uint64_t* chunk);
+cudaError_t launch_narrow_keys(const unsigned long long* keys, uint64_t n, const ViewInfo* info, uint32_t* k32,
                                cudaStream_t s);
-cudaError_t launch_narrow_keys(const unsigned long long* keys, uint64_t n, unsigned long long kmin, uint32_t shift,
-                               uint32_t* k32, cudaStream_t s);
-cudaError_t launch_tie_fixup(const uint32_t* k32, uint64_t n, const unsigned long long* full_by_id, uint32_t* order,
+cudaError_t launch_tie_fixup(const uint32_t* k32s, uint64_t n, const unsigned long long* keys, uint32_t* order,
                              cudaStream_t s);
+cudaError_t launch_tile_bins(const SplatRec* rec, const uint32_t* k32s, const uint32_t* order,
+                             const unsigned long long* keys, uint64_t n, uint32_t tiles, uint32_t tiles_x,
+                             uint32_t* chunk_counts, uint32_t* totals, uint32_t* tile_start, uint32_t* list,
+                             uint64_t cap, ViewInfo* info, cudaStream_t s);
 cudaError_t launch_contract(const ContractParams& p, uint64_t max_touched, cudaStream_t s);
 cudaError_t launch_normalize(const float* sums, const float* totals, uint64_t n, uint32_t dim, float* rows,
                              float* coverage, cudaStream_t s);

@@ -120,6 +120,23 @@ def test_depth_order_exact_with_coarse_narrowed_keys(gpu_ctx, oracle):
     _assert_capture_equal(got, oracle.rasterize(s, cam))
 
 
+@pytest.mark.parametrize("n", [6000, 20000])
+def test_oversized_tiles_sort_exactly(gpu_ctx, oracle, n):
+    """Tiles whose lists exceed the shared-memory sort (4096 -> 512x32 class,
+    16384 -> in-place bitonic class) keep the exact (depth, id) order."""
+    rng = np.random.default_rng(n)
+    mean = np.zeros((n, 3), np.float32)
+    mean[:, 0] = rng.uniform(-0.2, 0.2, n)
+    mean[:, 1] = rng.uniform(-0.2, 0.2, n)
+    mean[:, 2] = rng.uniform(4.0, 6.0, n)
+    mean[: n // 4, 2] = mean[0, 2]  # a block of exact depth ties
+    s = scene_ns(mean, np.full((n, 3), 0.02), np.tile([0, 0, 0, 1.0], (n, 1)), rng.uniform(0.01, 0.05, n))
+    cam = plain_camera(30.0, 30.0, 8.0, 8.0, 16, 16)
+    got = _capture(gpu_ctx, s, cam)
+    assert got["tile_offsets"][-1] == n  # one tile holds every splat
+    _assert_capture_equal(got, oracle.rasterize(s, cam))
+
+
 def test_empty_and_culled_scenes(gpu_ctx, oracle):
     cam = plain_camera(50, 50, 16, 16, 32, 32)
     behind = scene_ns([[0, 0, -1], [0, 0, 0.005]], [[0.1] * 3] * 2, [[0, 0, 0, 1]] * 2, [0.5, 0.5])
