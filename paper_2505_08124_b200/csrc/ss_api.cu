@@ -115,7 +115,7 @@ struct ProfState {
 struct Lane {
     cudaStream_t stream = nullptr;
     cudaEvent_t contract_done = nullptr, done = nullptr;
-    DevBuf rec, keys, k32, k32s, order, iota, tile_count, tile_start, fill, list;
+    DevBuf rec, keys, k32, k32s, order, iota, offsets, tkeys, tkeys_sorted, tvals, tile_start, tile_end, list;
     uint64_t iota_n = 0;           // entries of the 0..n-1 sequence in `iota`
     uint64_t list_cap = 0;         // entries of `list`
     DevBuf cub_tmp, info;
@@ -125,7 +125,8 @@ struct Lane {
     ViewInfo* h_info = nullptr;    // pinned
     uint32_t* h_u32 = nullptr;     // pinned scratch
     void release_all() {
-        DevBuf* b[] = {&rec, &keys, &k32, &k32s, &order, &iota, &tile_count, &tile_start, &fill, &list, &cub_tmp, &info, &pix_bits, &mask_bits,
+        DevBuf* b[] = {&rec, &keys, &k32, &k32s, &order, &iota, &offsets, &tkeys, &tkeys_sorted, &tvals, &tile_start,
+                       &tile_end, &list, &cub_tmp, &info, &pix_bits, &mask_bits,
                        &runs, &run_offsets, &clip, &spans, &acc, &touched, &touched_list};
         for (auto* x : b) x->release();
         if (h_info) cudaFreeHost(h_info);
@@ -241,6 +242,7 @@ void check_camera(const ss_camera* cam) {
 
 struct Geometry {
     uint32_t tiles_x = 0, tiles_y = 0, tiles = 0;
+    bool k16 = true; // 16-bit tile keys
 };
 
 // project (+ per-tile instance counts) -> scan -> scatter ids into tile
@@ -258,8 +260,13 @@ Geometry run_geometry(ss_ctx* c, Lane& L, cudaStream_t s, const ss_camera& cam) 
     auto* keys = static_cast<unsigned long long*>(L.keys.ensure(std::max<uint64_t>(N, 1) * 8));
     if (g.tiles > 50000u) throw Error(SS_ERR_CONTRACT, "raster resolution too large (more than 50000 16x16 tiles)");
     auto* tstart = static_cast<uint32_t*>(L.tile_start.ensure((g.tiles + 1ull) * 4));
-    if (L.list_cap == 0) L.list_cap = std::max<uint64_t>(16 * N, 1u << 20);
+    auto* tend = static_cast<uint32_t*>(L.tile_end.ensure((g.tiles + 1ull) * 4));
+    g.k16 = g.tiles <= 65535u;
+    if (L.list_cap == 0) L.list_cap = std::max<uint64_t>(4 * N, 1u << 20);
     auto* list = static_cast<uint32_t*>(L.list.ensure(L.list_cap * 4));
+    L.tkeys.ensure(L.list_cap * (g.k16 ? 2 : 4));
+    L.tkeys_sorted.ensure(L.list_cap * (g.k16 ? 2 : 4));
+    L.tvals.ensure(L.list_cap * 4);
     ViewInfo* info = L.info.as<ViewInfo>();
 
     reset_info(c, L, s);
@@ -305,14 +312,52 @@ Geometry run_geometry(ss_ctx* c, Lane& L, cudaStream_t s, const ss_camera& cam) 
     }
     {
         Scope sc(c, s, SS_K_BIN);
-        uint64_t chunk = 0;
-        const uint32_t nch = tile_chunks(N, &chunk);
-        auto* ccounts = static_cast<uint32_t*>(L.tile_count.ensure((uint64_t)nch * g.tiles * 4 + 4));
-        auto* totals = static_cast<uint32_t*>(L.fill.ensure((uint64_t)g.tiles * 4 + 4));
+        auto* offsets = static_cast<uint32_t*>(L.offsets.ensure((N + 1) * 4));
+        size_t tb = 0;
+        SS_CUDA(launch_instance_offsets(rec, k32s, order, N, offsets, nullptr, &tb, s));
+        void* tmp = L.cub_tmp.ensure(tb);
+        tb = L.cub_tmp.bytes;
+        SS_CUDA(launch_instance_offsets(rec, k32s, order, N, offsets, tmp, &tb, s));
+        c->launches_cub += 1;
+        c->prof.launches[SS_K_BIN] += 1;
         own_launch(c,
-                   launch_tile_bins(rec, k32s, order, keys, N, g.tiles, g.tiles_x, ccounts, totals, tstart, list,
-                                    L.list_cap, info, s),
-                   SS_K_BIN, 5);
+                   launch_emit_instances(rec, k32s, order, N, offsets, g.tiles_x, L.list_cap, L.tkeys.p, g.k16,
+                                         L.tvals.as<uint32_t>(), info, s),
+                   SS_K_BIN, 2);
+    }
+    {
+        // stable sort by tile: slices come out in depth order
+        Scope sc(c, s, SS_K_SORT);
+        const uint32_t tbits = bits_for(g.tiles - 1);
+        size_t tb = 0;
+        const int cap = (int)L.list_cap;
+        auto* vin = L.tvals.as<uint32_t>();
+        if (g.k16) {
+            auto* kin = L.tkeys.as<uint16_t>();
+            auto* kout = L.tkeys_sorted.as<uint16_t>();
+            SS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, vin, list, cap, 0, (int)tbits, s));
+            void* tmp = L.cub_tmp.ensure(tb);
+            tb = L.cub_tmp.bytes;
+            SS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, kin, kout, vin, list, cap, 0, (int)tbits, s));
+        } else {
+            auto* kin = L.tkeys.as<uint32_t>();
+            auto* kout = L.tkeys_sorted.as<uint32_t>();
+            SS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, vin, list, cap, 0, (int)tbits, s));
+            void* tmp = L.cub_tmp.ensure(tb);
+            tb = L.cub_tmp.bytes;
+            SS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, kin, kout, vin, list, cap, 0, (int)tbits, s));
+        }
+        c->launches_cub += 1;
+        c->prof.launches[SS_K_SORT] += 1;
+    }
+    {
+        Scope sc(c, s, SS_K_BIN);
+        SS_CUDA(cudaMemsetAsync(tstart, 0, (g.tiles + 1ull) * 4, s));
+        SS_CUDA(cudaMemsetAsync(tend, 0, (g.tiles + 1ull) * 4, s));
+        own_launch(c,
+                   launch_tile_ranges(L.tkeys_sorted.p, g.k16, L.offsets.as<uint32_t>(), N, L.list_cap, tstart, tend,
+                                      info, s),
+                   SS_K_BIN);
     }
     return g;
 }
@@ -323,6 +368,7 @@ RasterParams raster_params(ss_ctx* c, Lane& L, const ss_camera& cam, const Geome
     p.rec = L.rec.as<SplatRec>();
     p.tile_list = L.list.as<uint32_t>();
     p.tile_start = L.tile_start.as<uint32_t>();
+    p.tile_end = L.tile_end.as<uint32_t>();
     p.width = cam.width;
     p.height = cam.height;
     p.tiles_x = g.tiles_x;
@@ -521,8 +567,7 @@ void encode_batch(ss_ctx* c, uint32_t nviews, const ss_camera* cams, const ss_vi
         }
         for (auto& L : c->lanes)
             if (need > L.list_cap) {
-                L.list_cap = need + need / 4;
-                L.list.release();
+                L.list_cap = need + need / 16;
             }
         todo.swap(again);
     }
@@ -717,8 +762,7 @@ int ss_raster_capture(ss_ctx* c, const ss_camera* cam, int mode, uint64_t* n_ent
             SS_CUDA(cudaStreamSynchronize(s));
             if (!L.h_info->overflow) break;
             if (attempt > 2) throw Error(SS_ERR_CUDA, "tile-list buffer kept overflowing");
-            L.list_cap = L.h_info->n_instances + L.h_info->n_instances / 4;
-            L.list.release();
+            L.list_cap = L.h_info->n_instances + L.h_info->n_instances / 16;
         }
         if (L.h_info->err_count)
             throw Error(SS_ERR_NUMERIC, "singular screen covariance for gaussian " + std::to_string(L.h_info->err_gid));
@@ -779,9 +823,18 @@ int ss_raster_fetch(ss_ctx* c, ss_weight_entry* entries, float* per_pixel_total,
         if (c->cap_splats)
             SS_CUDA(cudaMemcpy(order.data(), c->lanes[0].order.p, c->cap_splats * 4, cudaMemcpyDeviceToHost));
         if (splat_gid) std::copy(order.begin(), order.end(), splat_gid);
-        if (tile_offsets && c->cap_tiles)
-            SS_CUDA(cudaMemcpy(tile_offsets, c->lanes[0].tile_start.p, (c->cap_tiles + 1ull) * 4,
-                               cudaMemcpyDeviceToHost));
+        if (tile_offsets && c->cap_tiles) {
+            // tiles are contiguous in key order: tile t starts after all instances of tiles < t
+            std::vector<uint32_t> st(c->cap_tiles), en(c->cap_tiles);
+            SS_CUDA(cudaMemcpy(st.data(), c->lanes[0].tile_start.p, c->cap_tiles * 4, cudaMemcpyDeviceToHost));
+            SS_CUDA(cudaMemcpy(en.data(), c->lanes[0].tile_end.p, c->cap_tiles * 4, cudaMemcpyDeviceToHost));
+            uint32_t run = 0;
+            for (uint32_t t = 0; t < c->cap_tiles; ++t) {
+                tile_offsets[t] = run;
+                run += en[t] - st[t];
+            }
+            tile_offsets[c->cap_tiles] = run;
+        }
         if (tile_splats && c->cap_instances) {
             // tile lists hold Gaussian ids; report them as indices into the
             // depth-sorted splat list, as the reference's tile_bins do

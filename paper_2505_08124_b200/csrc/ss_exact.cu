@@ -219,9 +219,8 @@ struct PixelState {
 // cutoff, alpha clamp, skip rule, weight cutoff and transmittance floor, in
 // its exact fp64 operation order.  Returns whether an entry is emitted.
 template <bool FALLOFF>
-__device__ __forceinline__ bool composite_one(PixelState& ps, const SplatRec& s, uint32_t sx0, uint32_t sx1,
-                                              uint32_t sy0, uint32_t sy1, const unsigned long long* stab, float& wf) {
-    if (ps.done || ps.px < sx0 || ps.px > sx1 || ps.py < sy0 || ps.py > sy1) return false;
+__device__ __forceinline__ bool composite_one(PixelState& ps, const SplatRec& s, const unsigned long long* stab,
+                                              float& wf) {
     const double dx = ds(ps.dpx, s.mu_x), dy = ds(ps.dpy, s.mu_y);
     const double d2 = da(da(dm(dm(s.a, dx), dx), dm(dm(s.b2, dx), dy)), dm(dm(s.c, dy), dy));
     if (d2 > kMahalanobisSqCutoff) return false;
@@ -243,6 +242,22 @@ __device__ __forceinline__ bool composite_one(PixelState& ps, const SplatRec& s,
         if (ps.T < kTransmittanceFloor) ps.done = true;
         return emit;
     }
+}
+
+// Bits of a warp's 8x4 block (lane l = column l&7, row l>>3) inside the
+// splat's padded box: the reference's per-pixel box test (rasterizer.hpp:115)
+// evaluated once per (splat, block).
+__device__ __forceinline__ uint32_t block_box_mask(uint32_t sx0, uint32_t sx1, uint32_t sy0, uint32_t sy1, uint32_t bx0,
+                                                   uint32_t by0) {
+    const int c0 = max((int)sx0 - (int)bx0, 0), c1 = min((int)sx1 - (int)bx0, 7);
+    const int r0 = max((int)sy0 - (int)by0, 0), r1 = min((int)sy1 - (int)by0, 3);
+    if (c0 > c1 || r0 > r1) return 0u;
+    const uint32_t row = (0xffu >> (7 - c1)) & (0xffu << c0);
+    uint32_t m = 0u;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+        if (r >= r0 && r <= r1) m |= row << (8 * r);
+    return m;
 }
 
 // Fused-mode gating of one pixel slot's contribution: lanes with identical
@@ -308,6 +323,7 @@ template <int KIND, bool FALLOFF, int MW>
 __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) {
     __shared__ SplatRec srec[kRasterThreads]; // warp w stages its hits in srec[32w, 32w+32)
     __shared__ uint32_t sgid[kRasterThreads];
+    __shared__ uint32_t smask[kRasterThreads];
     __shared__ unsigned long long stab[256];
     stab[threadIdx.x] = kExpTab[threadIdx.x];
 
@@ -316,10 +332,11 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     const uint32_t bx0 = tx * kTile + 8u * (warp & 1u), by0 = ty * kTile + 4u * (warp >> 1);
     const uint32_t bx1 = bx0 + 7u, by1 = by0 + 3u;
-    const uint32_t start = p.tile_start[tile], end = p.tile_start[tile + 1];
+    const uint32_t start = p.tile_start[tile], end = p.tile_end[tile];
     if (p.info->overflow) return; // tile lists incomplete: the view is re-run by the host
     SplatRec* wrec = srec + 32u * warp;
     uint32_t* wgid = sgid + 32u * warp;
+    uint32_t* wmask = smask + 32u * warp;
 
     PixelState ps;
     ps.px = bx0 + (lane & 7u);
@@ -357,8 +374,10 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
         nr = __ldg(p.tile_list + start + lane);
         nbox = __ldg(reinterpret_cast<const uint2*>(&p.rec[nr].x0));
     }
+    const uint32_t lane_bit = 1u << lane;
     for (uint32_t base = start; base < end; base += 32u) {
-        if (__all_sync(0xffffffffu, ps.done)) break;
+        const uint32_t live = ~__ballot_sync(0xffffffffu, ps.done);
+        if (live == 0u) break;
         const uint32_t i = base + lane;
         const uint32_t r = nr;
         const uint2 box = nbox;
@@ -366,27 +385,29 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
             nr = __ldg(p.tile_list + i + 32u);
             nbox = __ldg(reinterpret_cast<const uint2*>(&p.rec[nr].x0));
         }
-        const bool hit = i < end && !((box.x >> 16) < bx0 || (box.x & 0xffffu) > bx1 || (box.y >> 16) < by0 ||
-                                      (box.y & 0xffffu) > by1);
-        const uint32_t cand = __ballot_sync(0xffffffffu, hit);
-        if (hit) {
-            const uint32_t slot = __popc(cand & ((1u << lane) - 1u));
+        const uint32_t sx0 = box.x & 0xffffu, sx1 = box.x >> 16, sy0 = box.y & 0xffffu, sy1 = box.y >> 16;
+        // pixels of the block inside the box that are still compositing
+        uint32_t m = 0u;
+        if (i < end && !(sx1 < bx0 || sx0 > bx1 || sy1 < by0 || sy0 > by1))
+            m = block_box_mask(sx0, sx1, sy0, sy1, bx0, by0) & live;
+        const uint32_t cand = __ballot_sync(0xffffffffu, m != 0u);
+        if (m) {
+            const uint32_t slot = __popc(cand & (lane_bit - 1u));
             const uint4* src = reinterpret_cast<const uint4*>(p.rec + r);
             uint4* dst = reinterpret_cast<uint4*>(wrec + slot);
             dst[0] = __ldg(src);
             dst[1] = __ldg(src + 1);
             dst[2] = __ldg(src + 2);
-            dst[3] = make_uint4(box.x, box.y, 0u, 0u); // box already prefetched
             wgid[slot] = r;
+            wmask[slot] = m;
         }
         __syncwarp();
         const uint32_t nh = __popc(cand);
         for (uint32_t j = 0; j < nh; ++j) {
             const SplatRec& s = wrec[j];
-            const uint2 sb = *reinterpret_cast<const uint2*>(&s.x0);
             float wf = 0.0f;
-            const bool c = composite_one<FALLOFF>(ps, s, sb.x & 0xffffu, sb.x >> 16, sb.y & 0xffffu, sb.y >> 16, stab,
-                                                  wf);
+            bool c = false;
+            if ((wmask[j] & lane_bit) && !ps.done) c = composite_one<FALLOFF>(ps, s, stab, wf);
             if constexpr (KIND == 0) {
                 ps.count += c ? 1u : 0u;
             } else if constexpr (KIND == 1) {
@@ -397,7 +418,7 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
             } else {
                 gate_and_accumulate<MW>(p, c, wf, grp, bits, wgid[j], lane);
             }
-            if (__all_sync(0xffffffffu, ps.done)) break;
+            if ((j & 7u) == 7u && __all_sync(0xffffffffu, ps.done)) break;
         }
         __syncwarp();
     }

@@ -56,7 +56,8 @@ struct ProjectParams {
 struct RasterParams {
     const SplatRec* rec;        // by Gaussian id
     const uint32_t* tile_list;  // per tile: Gaussian ids in (depth, id) order
-    const uint32_t* tile_start; // [tiles + 1]; tile t is tile_list[start[t], start[t+1])
+    const uint32_t* tile_start; // tile t is tile_list[start[t], end[t])
+    const uint32_t* tile_end;
     uint32_t width, height, tiles_x;
     // capture mode
     uint32_t* pix_count;           // pass 0 output [P]

@@ -7,6 +7,9 @@
 #include <algorithm>
 
 #include <cub/block/block_scan.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
+#include <cub/iterator/transform_input_iterator.cuh>
 
 #include "ss_kernels.cuh"
 
@@ -84,11 +87,10 @@ __global__ void resample_bits_kernel(const uint32_t* src, uint32_t sw, uint32_t 
 //  2. one stable radix sort of (key32, id) over all N Gaussians (CUB);
 //  3. tie_fixup: exact (depth bits, id) order inside runs of equal key32;
 //     => order[] is the reference's depth_sort order (projection.hpp:59-64);
-//  4. count / offsets / scatter over CHUNKS OF CONSECUTIVE RANKS, with the
-//     per-chunk tile histogram in shared memory: tile t's list is the
-//     concatenation, in chunk order, of one small segment per chunk;
-//  5. segment_sort: each (chunk, tile) segment (~8 entries) is put in depth
-//     order -- the whole tile list is then in global depth order.
+//  4. instances (tile, id) emitted in depth-rank order at scanned offsets;
+//  5. a stable radix sort by tile key (CUB) over a device-sized capacity
+//     (padding keys sort last) => every tile's slice is in depth order;
+//  6. tile_ranges: slice bounds by boundary detection.
 __device__ __forceinline__ uint32_t narrow_shift(const ViewInfo* info) {
     const unsigned long long span = info->min_key ^ info->max_key;
     const uint32_t hb = span ? 64u - (uint32_t)__clzll((long long)span) : 0u;
@@ -133,199 +135,68 @@ __global__ void tie_fixup_kernel(const uint32_t* k32, uint64_t n, const unsigned
     }
 }
 
-__device__ __forceinline__ bool rank_box(const SplatRec* rec, const uint32_t* k32s, const uint32_t* order, uint64_t r,
-                                         uint32_t& id, uint32_t& tx0, uint32_t& tx1, uint32_t& ty0, uint32_t& ty1) {
-    if (k32s[r] == 0xffffffffu) return false; // culled (projection.hpp:38 / rasterizer.hpp:177)
-    id = order[r];
-    const uint2 box = __ldg(reinterpret_cast<const uint2*>(&rec[id].x0));
-    tx0 = (box.x & 0xffffu) / kTile;
-    tx1 = (box.x >> 16) / kTile;
-    ty0 = (box.y & 0xffffu) / kTile;
-    ty1 = (box.y >> 16) / kTile;
-    return true;
-}
+// Tiles covered by the splat of depth rank r (0 for culled Gaussians).
+struct RankTiles {
+    const SplatRec* rec;
+    const uint32_t* k32s;
+    const uint32_t* order;
+    uint64_t n;
+    __host__ __device__ __forceinline__ uint32_t operator()(uint64_t r) const {
+#ifdef __CUDA_ARCH__
+        if (r >= n || k32s[r] == 0xffffffffu) return 0u;
+        const uint2 box = __ldg(reinterpret_cast<const uint2*>(&rec[order[r]].x0));
+        return ((box.x >> 16) / kTile - (box.x & 0xffffu) / kTile + 1u) *
+               ((box.y >> 16) / kTile - (box.y & 0xffffu) / kTile + 1u);
+#else
+        return 0u;
+#endif
+    }
+};
 
-__global__ void __launch_bounds__(1024) tile_count_kernel(const SplatRec* rec, const uint32_t* k32s,
-                                                         const uint32_t* order, uint64_t n, uint64_t chunk,
-                                                         uint32_t tiles, uint32_t tiles_x, uint32_t* chunk_counts) {
-    extern __shared__ uint32_t hist[];
-    for (uint32_t t = threadIdx.x; t < tiles; t += blockDim.x) hist[t] = 0;
-    __syncthreads();
-    const uint64_t lo = (uint64_t)blockIdx.x * chunk, hi = min(n, lo + chunk);
-    for (uint64_t r = lo + threadIdx.x; r < hi; r += blockDim.x) {
-        uint32_t id, tx0, tx1, ty0, ty1;
-        if (!rank_box(rec, k32s, order, r, id, tx0, tx1, ty0, ty1)) continue;
-        for (uint32_t ty = ty0; ty <= ty1; ++ty)
-            for (uint32_t tx = tx0; tx <= tx1; ++tx) atomicAdd(hist + ty * tiles_x + tx, 1u);
-    }
-    __syncthreads();
-    uint32_t* row = chunk_counts + (uint64_t)blockIdx.x * tiles;
-    for (uint32_t t = threadIdx.x; t < tiles; t += blockDim.x) row[t] = hist[t];
-}
-
-// Per tile (one thread each): exclusive prefix of the chunk counts down the
-// tile's column (in place, coalesced across threads) and the tile total.
-__global__ void __launch_bounds__(128) tile_column_prefix_kernel(uint32_t* chunk_counts, uint32_t n_chunks,
-                                                                 uint32_t tiles, uint32_t* totals) {
-    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= tiles) return;
-    uint32_t run = 0;
-    uint32_t c = 0;
-    for (; c + 8 <= n_chunks; c += 8) {
-        uint32_t v[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = chunk_counts[(uint64_t)(c + j) * tiles + t];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            chunk_counts[(uint64_t)(c + j) * tiles + t] = run;
-            run += v[j];
-        }
-    }
-    for (; c < n_chunks; ++c) {
-        const uint32_t v = chunk_counts[(uint64_t)c * tiles + t];
-        chunk_counts[(uint64_t)c * tiles + t] = run;
-        run += v;
-    }
-    totals[t] = run;
-}
-
-// One CTA: exclusive scan of the tile totals -> tile_start[0..tiles].
-__global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* totals, uint32_t tiles, uint32_t* tile_start,
-                                                        ViewInfo* info) {
-    using Scan = cub::BlockScan<uint32_t, 1024>;
-    __shared__ typename Scan::TempStorage tmp;
-    __shared__ uint32_t carry;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    for (uint32_t base = 0; base < tiles; base += 1024) {
-        const uint32_t t = base + threadIdx.x;
-        const uint32_t v = t < tiles ? totals[t] : 0u;
-        uint32_t ex, agg;
-        Scan(tmp).ExclusiveSum(v, ex, agg);
-        if (t < tiles) tile_start[t] = ex + carry;
-        __syncthreads();
-        if (threadIdx.x == 0) carry += agg;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        tile_start[tiles] = carry;
-        info->n_instances = carry;
-    }
-}
-
-__global__ void __launch_bounds__(1024) tile_scatter_kernel(const SplatRec* rec, const uint32_t* k32s,
-                                                           const uint32_t* order, uint64_t n, uint64_t chunk,
-                                                           uint32_t tiles, uint32_t tiles_x,
-                                                           const uint32_t* chunk_prefix, const uint32_t* tile_start,
-                                                           uint32_t* list, uint64_t cap, ViewInfo* info) {
-    extern __shared__ uint32_t cursor[];
-    if (info->n_instances > cap) { // the tile lists do not fit: the host re-runs the view
-        if (threadIdx.x == 0) info->overflow = 1u;
+// Instances in depth-rank order: splat of rank r writes (tile, id) for every
+// tile its box covers at offsets[r] (exclusive scan of RankTiles).  A stable
+// sort by tile then yields each tile's list in depth order.
+template <typename K>
+__global__ void emit_instances_kernel(const SplatRec* rec, const uint32_t* k32s, const uint32_t* order, uint64_t n,
+                                      const uint32_t* offsets, uint32_t tiles_x, uint64_t cap, K* keys, uint32_t* vals,
+                                      ViewInfo* info) {
+    const uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    if (offsets[n] > cap) { // lists do not fit: the host re-runs the view
+        if (r == 0) info->overflow = 1u;
         return;
     }
-    const uint32_t* pre = chunk_prefix + (uint64_t)blockIdx.x * tiles;
-    for (uint32_t t = threadIdx.x; t < tiles; t += blockDim.x) cursor[t] = tile_start[t] + pre[t];
-    __syncthreads();
-    const uint64_t lo = (uint64_t)blockIdx.x * chunk, hi = min(n, lo + chunk);
-    for (uint64_t r = lo + threadIdx.x; r < hi; r += blockDim.x) {
-        uint32_t id, tx0, tx1, ty0, ty1;
-        if (!rank_box(rec, k32s, order, r, id, tx0, tx1, ty0, ty1)) continue;
-        for (uint32_t ty = ty0; ty <= ty1; ++ty)
-            for (uint32_t tx = tx0; tx <= tx1; ++tx) list[atomicAdd(cursor + ty * tiles_x + tx, 1u)] = (uint32_t)r;
-    }
-}
-
-// Warp bitonic sort of 32*R u32; element lane + 32*r lives in v[r] of `lane`.
-template <int R>
-__device__ __forceinline__ void warp_bitonic(uint32_t (&v)[R], uint32_t lane) {
-#pragma unroll
-    for (uint32_t k = 2; k <= 32u * R; k <<= 1) {
-#pragma unroll
-        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-            if (j >= 32) {
-                const uint32_t jr = j >> 5;
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    if ((r & jr) != 0) continue;
-                    const bool asc = ((lane + 32u * r) & k) == 0;
-                    const uint32_t lo = min(v[r], v[r | jr]), hi = max(v[r], v[r | jr]);
-                    v[r] = asc ? lo : hi;
-                    v[r | jr] = asc ? hi : lo;
-                }
-            } else {
-                const bool lower = (lane & j) == 0;
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    const uint32_t pv = __shfl_xor_sync(0xffffffffu, v[r], j);
-                    const bool asc = ((lane + 32u * r) & k) == 0;
-                    v[r] = (lower == asc) ? min(v[r], pv) : max(v[r], pv);
-                }
-            }
+    if (k32s[r] == 0xffffffffu) return;
+    const uint32_t id = order[r];
+    const uint2 box = __ldg(reinterpret_cast<const uint2*>(&rec[id].x0));
+    uint32_t o = offsets[r];
+    for (uint32_t ty = (box.y & 0xffffu) / kTile; ty <= (box.y >> 16) / kTile; ++ty)
+        for (uint32_t tx = (box.x & 0xffffu) / kTile; tx <= (box.x >> 16) / kTile; ++tx) {
+            keys[o] = (K)(ty * tiles_x + tx);
+            vals[o] = id;
+            ++o;
         }
-    }
 }
 
-template <int R>
-__device__ __forceinline__ void warp_sort_segment(uint32_t* seg, uint32_t m, uint32_t lane) {
-    uint32_t v[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) v[r] = lane + 32u * r < m ? seg[lane + 32u * r] : 0xffffffffu;
-    warp_bitonic<R>(v, lane);
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-        if (lane + 32u * r < m) seg[lane + 32u * r] = v[r];
+// Pad [I_v, cap) with the largest key so a fixed-size sort leaves it last.
+template <typename K>
+__global__ void pad_keys_kernel(const uint32_t* offsets, uint64_t n, uint64_t cap, K* keys) {
+    const uint64_t iv = offsets[n];
+    for (uint64_t i = iv + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cap;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        keys[i] = (K)~(K)0;
 }
 
-// One CTA per tile: the tile's list (depth ranks, one segment per rank chunk,
-// segments already in chunk order) is loaded coalesced into shared memory,
-// each warp sorts segments with a register bitonic network of up to 512
-// (longer segments: insertion sort by one lane), and the ranks are replaced by
-// Gaussian ids (order[rank]) on the way out, so the compositor reads records
-// directly.  Tiles larger than the shared-memory slice sort in global memory.
-constexpr uint32_t kSegSmem = 12288; // ranks per tile held in shared memory (48 KB)
-__global__ void __launch_bounds__(512) segment_sort_kernel(const uint32_t* chunk_prefix, uint32_t n_chunks,
-                                                           uint32_t tiles, const uint32_t* tile_start,
-                                                           const uint32_t* order, uint32_t* list,
-                                                           const ViewInfo* info) {
-    extern __shared__ uint32_t sl[];
-    const uint32_t t = blockIdx.x;
-    const uint32_t ts = tile_start[t], n = tile_start[t + 1] - ts;
-    if (n == 0 || info->overflow) return;
-    const bool in_smem = n <= kSegSmem;
-    uint32_t* base = in_smem ? sl : list + ts;
-    if (in_smem) {
-        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) sl[i] = list[ts + i];
-        __syncthreads();
-    }
-    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (uint32_t c = warp; c < n_chunks; c += nw) {
-        const uint32_t s0 = chunk_prefix[(uint64_t)c * tiles + t];
-        const uint32_t s1 = c + 1 < n_chunks ? chunk_prefix[(uint64_t)(c + 1) * tiles + t] : n;
-        const uint32_t m = s1 - s0;
-        if (m < 2) continue;
-        if (m <= 64) {
-            warp_sort_segment<2>(base + s0, m, lane);
-        } else if (m <= 128) {
-            warp_sort_segment<4>(base + s0, m, lane);
-        } else if (m <= 256) {
-            warp_sort_segment<8>(base + s0, m, lane);
-        } else if (m <= 512) {
-            warp_sort_segment<16>(base + s0, m, lane);
-        } else if (lane == 0) {
-            for (uint32_t x = s0 + 1; x < s1; ++x) {
-                const uint32_t r = base[x];
-                uint32_t y = x;
-                while (y > s0 && base[y - 1] > r) {
-                    base[y] = base[y - 1];
-                    --y;
-                }
-                base[y] = r;
-            }
-        }
-        __syncwarp();
-    }
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) list[ts + i] = __ldg(order + base[i]);
+template <typename K>
+__global__ void tile_ranges_kernel(const K* keys, const uint32_t* offsets, uint64_t n, uint32_t* start,
+                                   uint32_t* end, ViewInfo* info) {
+    const uint64_t iv = offsets[n];
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) info->n_instances = iv;
+    if (i >= iv || info->overflow) return;
+    const uint32_t k = keys[i];
+    if (i == 0 || keys[i - 1] != k) start[k] = (uint32_t)i;
+    if (i == iv - 1 || keys[i + 1] != k) end[k] = (uint32_t)(i + 1);
 }
 
 // --------------------------------------------------------- contraction
@@ -614,15 +485,6 @@ cudaError_t launch_resample_bits(const uint32_t* src, uint32_t sw, uint32_t sh, 
     resample_bits_kernel<<<blocks_for(n, 256), 256, 0, s>>>(src, sw, sh, dst, tw, th, words);
     return cudaGetLastError();
 }
-uint32_t tile_chunks(uint64_t n, uint64_t* chunk) {
-    // ~128 rank chunks: per-chunk tile histograms stay small and the
-    // per-tile segments short
-    uint64_t c = (n + 127) / 128;
-    c = std::max<uint64_t>(1024, (c + 1023) / 1024 * 1024);
-    *chunk = c;
-    return (uint32_t)std::max<uint64_t>(1, (n + c - 1) / c);
-}
-
 cudaError_t launch_narrow_keys(const unsigned long long* keys, uint64_t n, const ViewInfo* info, uint32_t* k32,
                                cudaStream_t s) {
     if (!n) return cudaSuccess;
@@ -637,31 +499,40 @@ cudaError_t launch_tie_fixup(const uint32_t* k32s, uint64_t n, const unsigned lo
     return cudaGetLastError();
 }
 
-cudaError_t launch_tile_bins(const SplatRec* rec, const uint32_t* k32s, const uint32_t* order,
-                             const unsigned long long* keys, uint64_t n, uint32_t tiles, uint32_t tiles_x,
-                             uint32_t* chunk_counts, uint32_t* totals, uint32_t* tile_start, uint32_t* list,
-                             uint64_t cap, ViewInfo* info, cudaStream_t s) {
-    uint64_t chunk = 0;
-    const uint32_t nch = tile_chunks(n, &chunk);
-    const size_t smem = (size_t)tiles * 4;
-    // raise the dynamic shared-memory limit once per device (the call is not free)
-    static thread_local int configured_dev = -1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (configured_dev != dev) {
-        const int lim = 50000 * 4;
-        cudaError_t e = cudaFuncSetAttribute(tile_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(tile_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-        if (e != cudaSuccess) return e;
-        configured_dev = dev;
+cudaError_t launch_instance_offsets(const SplatRec* rec, const uint32_t* k32s, const uint32_t* order, uint64_t n,
+                                    uint32_t* offsets, void* tmp, size_t* tmp_bytes, cudaStream_t s) {
+    cub::CountingInputIterator<uint64_t> ranks(0);
+    cub::TransformInputIterator<uint32_t, RankTiles, cub::CountingInputIterator<uint64_t>> it(
+        ranks, RankTiles{rec, k32s, order, n});
+    return cub::DeviceScan::ExclusiveSum(tmp, *tmp_bytes, it, offsets, (int)(n + 1), s);
+}
+
+cudaError_t launch_emit_instances(const SplatRec* rec, const uint32_t* k32s, const uint32_t* order, uint64_t n,
+                                  const uint32_t* offsets, uint32_t tiles_x, uint64_t cap, void* keys, bool k16,
+                                  uint32_t* vals, ViewInfo* info, cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    const unsigned g = (unsigned)std::min<uint64_t>(blocks_for(cap, 256), 148u * 16u);
+    if (k16) {
+        emit_instances_kernel<uint16_t><<<blocks_for(n, 256), 256, 0, s>>>(rec, k32s, order, n, offsets, tiles_x, cap,
+                                                                            static_cast<uint16_t*>(keys), vals, info);
+        pad_keys_kernel<uint16_t><<<g, 256, 0, s>>>(offsets, n, cap, static_cast<uint16_t*>(keys));
+    } else {
+        emit_instances_kernel<uint32_t><<<blocks_for(n, 256), 256, 0, s>>>(rec, k32s, order, n, offsets, tiles_x, cap,
+                                                                            static_cast<uint32_t*>(keys), vals, info);
+        pad_keys_kernel<uint32_t><<<g, 256, 0, s>>>(offsets, n, cap, static_cast<uint32_t*>(keys));
     }
-    tile_count_kernel<<<nch, 1024, smem, s>>>(rec, k32s, order, n, chunk, tiles, tiles_x, chunk_counts);
-    tile_column_prefix_kernel<<<blocks_for(tiles, 128), 128, 0, s>>>(chunk_counts, nch, tiles, totals);
-    tile_scan_kernel<<<1, 1024, 0, s>>>(totals, tiles, tile_start, info);
-    tile_scatter_kernel<<<nch, 1024, smem, s>>>(rec, k32s, order, n, chunk, tiles, tiles_x, chunk_counts, tile_start,
-                                                list, cap, info);
-    segment_sort_kernel<<<tiles, 512, kSegSmem * 4, s>>>(chunk_counts, nch, tiles, tile_start, order, list, info);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tile_ranges(const void* keys, bool k16, const uint32_t* offsets, uint64_t n, uint64_t cap,
+                               uint32_t* start, uint32_t* end, ViewInfo* info, cudaStream_t s) {
+    // the instance count lives on the device; cover the capacity, threads past it exit
+    if (k16)
+        tile_ranges_kernel<uint16_t><<<blocks_for(cap, 256), 256, 0, s>>>(static_cast<const uint16_t*>(keys), offsets,
+                                                                           n, start, end, info);
+    else
+        tile_ranges_kernel<uint32_t><<<blocks_for(cap, 256), 256, 0, s>>>(static_cast<const uint32_t*>(keys), offsets,
+                                                                           n, start, end, info);
     return cudaGetLastError();
 }
 

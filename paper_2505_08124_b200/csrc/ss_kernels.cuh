@@ -22,15 +22,17 @@ cudaError_t launch_rle_to_bits(const uint32_t* runs, const uint64_t* run_offsets
                                uint32_t* bits, uint4* spans, unsigned int* n_spans, cudaStream_t s);
 cudaError_t launch_resample_bits(const uint32_t* src, uint32_t sw, uint32_t sh, uint32_t* dst, uint32_t tw,
                                  uint32_t th, uint32_t words, cudaStream_t s);
-uint32_t tile_chunks(uint64_t n, uint64_t* chunk);
 cudaError_t launch_narrow_keys(const unsigned long long* keys, uint64_t n, const ViewInfo* info, uint32_t* k32,
                                cudaStream_t s);
 cudaError_t launch_tie_fixup(const uint32_t* k32s, uint64_t n, const unsigned long long* keys, uint32_t* order,
                              cudaStream_t s);
-cudaError_t launch_tile_bins(const SplatRec* rec, const uint32_t* k32s, const uint32_t* order,
-                             const unsigned long long* keys, uint64_t n, uint32_t tiles, uint32_t tiles_x,
-                             uint32_t* chunk_counts, uint32_t* totals, uint32_t* tile_start, uint32_t* list,
-                             uint64_t cap, ViewInfo* info, cudaStream_t s);
+cudaError_t launch_instance_offsets(const SplatRec* rec, const uint32_t* k32s, const uint32_t* order, uint64_t n,
+                                    uint32_t* offsets, void* tmp, size_t* tmp_bytes, cudaStream_t s);
+cudaError_t launch_emit_instances(const SplatRec* rec, const uint32_t* k32s, const uint32_t* order, uint64_t n,
+                                  const uint32_t* offsets, uint32_t tiles_x, uint64_t cap, void* keys, bool k16,
+                                  uint32_t* vals, ViewInfo* info, cudaStream_t s);
+cudaError_t launch_tile_ranges(const void* keys, bool k16, const uint32_t* offsets, uint64_t n, uint64_t cap,
+                               uint32_t* start, uint32_t* end, ViewInfo* info, cudaStream_t s);
 cudaError_t launch_contract(const ContractParams& p, uint64_t max_touched, cudaStream_t s);
 cudaError_t launch_normalize(const float* sums, const float* totals, uint64_t n, uint32_t dim, float* rows,
                              float* coverage, cudaStream_t s);
