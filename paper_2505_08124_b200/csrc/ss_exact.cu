@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(256) project_kernel(ProjectParams p) {
                 r.a = dd(cyy, det);
                 r.b2 = dm(2.0, dd(-cxy, det));
                 r.c = dd(cxx, det);
-                r.opacity = mo.w;
+                r.opacity = (double)mo.w;
                 r.gid = (uint32_t)id;
                 const double rx = da(dm(3.0, __dsqrt_rn(cxx)), 1.0);
                 const double ry = da(dm(3.0, __dsqrt_rn(cyy)), 1.0);
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(256) project_kernel(ProjectParams p) {
                     r.x1 = (uint16_t)x1;
                     r.y0 = (uint16_t)y0;
                     r.y1 = (uint16_t)y1;
-                    r.pad0 = r.pad1 = 0;
+                    r.pad = 0;
                     p.rec[id] = r;
                     survive = true;
                     key = (unsigned long long)__double_as_longlong(z);
@@ -232,8 +232,10 @@ __device__ __forceinline__ bool composite_one(PixelState& ps, const SplatRec& s,
         }
         return false;
     } else {
-        const double og = dm((double)s.opacity, g);
-        const double alpha = og < kAlphaMax ? og : kAlphaMax;
+        const double og = dm(s.opacity, g);
+        // std::min(kAlphaMax, og) == (og < kAlphaMax ? og : kAlphaMax); og >= 0, and for
+        // NaN both forms give kAlphaMax, so one DMNMX suffices
+        const double alpha = fmin(og, kAlphaMax);
         if (alpha < kAlphaSkip) return false;
         const double w = dm(alpha, ps.T);
         const bool emit = w >= kWeightCutoff;
@@ -412,7 +414,7 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
                 ps.count += c ? 1u : 0u;
             } else if constexpr (KIND == 1) {
                 if (c) {
-                    p.entries[ps.out++] = ss_weight_entry{s.gid, ps.pixel, wf};
+                    p.entries[ps.out++] = ss_weight_entry{wgid[j], ps.pixel, wf};
                     ps.total = da(ps.total, (double)wf);
                 }
             } else {

@@ -17,11 +17,11 @@ constexpr int kMaxMaskWords = 4;        // up to 128 masks per view
 // Fields are the reference's SplatRecord (rasterizer.hpp:99-106) minus color.
 struct __align__(16) SplatRec {
     double mu_x, mu_y; // rasterizer.hpp:101
-    double a, b2, c;   // conic (rasterizer.hpp:66-71); b2 = 2*b (exact)
-    float opacity;     // widened to f64 at use, as SplatRecord::opacity
-    uint32_t gid;
+    double a, b2;      // conic (rasterizer.hpp:66-71); b2 = 2*b (exact)
+    double c;
+    double opacity;    // SplatRecord::opacity: the f32 opacity widened once
     uint16_t x0, x1, y0, y1; // inclusive padded 3-sigma box (rasterizer.hpp:171-176)
-    uint32_t pad0, pad1;
+    uint32_t gid, pad;
 };
 static_assert(sizeof(SplatRec) == 64, "SplatRec must stay 64 B");
 
