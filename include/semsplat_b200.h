@@ -90,8 +90,11 @@ int ss_last_error_kind(void);
 int ss_set_stream(ss_ctx* ctx, uintptr_t stream);
 int ss_synchronize(ss_ctx* ctx);
 /* Tuning options.  SS_OPT_LANES: per-view pipeline lanes (1 or 2, default 2);
- * 1 serialises views, which the bench uses for exclusive per-kernel timing. */
-enum ss_option { SS_OPT_LANES = 1 };
+ * 1 serialises views, which the bench uses for exclusive per-kernel timing.
+ * SS_OPT_QUERY_PATH: 0 = auto (tensor-core coarse scoring + exact rescoring
+ * for stores of >= 16384 rows with dim % 64 == 0), 1 = exact scan only,
+ * 2 = tensor-core path whenever dim allows.  Results are identical. */
+enum ss_option { SS_OPT_LANES = 1, SS_OPT_QUERY_PATH = 2 };
 int ss_set_option(ss_ctx* ctx, int option, int64_t value);
 
 /* ---- scene (GaussianScene, scene.hpp:54-76) --------------------------- */

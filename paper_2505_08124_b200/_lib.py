@@ -160,6 +160,10 @@ class Context:
     def set_lanes(self, n: int):
         check(self._L.ss_set_option(self.h, 1, int(n)))
 
+    def set_query_path(self, path: int):
+        """0 = auto, 1 = exact scan, 2 = tensor-core coarse + exact rescore."""
+        check(self._L.ss_set_option(self.h, 2, int(path)))
+
     def synchronize(self):
         check(self._L.ss_synchronize(self.h))
 

@@ -23,6 +23,7 @@ UNITS = [
     ("ss_exact.cu", ["-fmad=false"]),
     ("ss_kernels.cu", []),
     ("ss_api.cu", []),
+    ("ss_query_tc.cu", []),
     ("ss_synth.cpp", []),
 ]
 

@@ -23,6 +23,7 @@
 #include <cub/iterator/counting_input_iterator.cuh>
 
 #include "ss_kernels.cuh"
+#include "ss_query_tc.cuh"
 
 namespace ss {
 namespace {
@@ -180,6 +181,11 @@ struct ss_ctx {
         thr_ids, thr_ids_sorted, zero_flag;
     uint64_t store_count = 0;
     uint32_t store_dim = 0;
+    // tensor-core query path: fp16 copy of the store, coarse scores, candidates
+    ss::DevBuf store_half, qhalf, tc_scores, cand, cand_count, cand_sim;
+    bool store_half_ok = false;
+    int query_path = 0; // SS_OPT_QUERY_PATH
+    int num_sms = 0;
 
     // instrumentation
     ss::ProfState prof;
@@ -645,7 +651,8 @@ void ss_destroy(ss_ctx* c) {
                           &c->pix_offset, &c->entries, &c->per_pixel_total, &c->alpha, &c->counters, &c->sums_buf,
                           &c->totals_buf, &c->store_rows, &c->store_ids, &c->qbuf, &c->qnorm, &c->scores,
                           &c->topk_ids, &c->topk_sims, &c->sel_flags, &c->thr_keys, &c->thr_keys_sorted, &c->thr_ids,
-                          &c->thr_ids_sorted, &c->zero_flag};
+                          &c->thr_ids_sorted, &c->zero_flag, &c->store_half, &c->qhalf, &c->tc_scores,
+                          &c->cand, &c->cand_count, &c->cand_sim};
     for (auto* b : bufs) b->release();
     for (auto e : c->prof.pool) cudaEventDestroy(e);
     for (auto& pe : c->prof.pending) {
@@ -673,6 +680,9 @@ int ss_set_option(ss_ctx* c, int option, int64_t value) {
         if (option == SS_OPT_LANES) {
             if (value < 1 || value > 2) throw Error(SS_ERR_CONTRACT, "SS_OPT_LANES must be 1 or 2");
             c->n_lanes = (uint32_t)value;
+        } else if (option == SS_OPT_QUERY_PATH) {
+            if (value < 0 || value > 2) throw Error(SS_ERR_CONTRACT, "SS_OPT_QUERY_PATH must be 0, 1 or 2");
+            c->query_path = (int)value;
         } else {
             throw Error(SS_ERR_CONTRACT, "unknown option");
         }
@@ -935,6 +945,7 @@ int ss_store_set(ss_ctx* c, const uint32_t* ids, const float* unit_rows, uint64_
         set_device(c);
         c->store_count = count;
         c->store_dim = dim;
+        c->store_half_ok = false;
         SS_CUDA(cudaMemcpy(c->store_ids.ensure(std::max<uint64_t>(count, 1) * 4), ids, count * 4,
                            cudaMemcpyHostToDevice));
         SS_CUDA(cudaMemcpy(c->store_rows.ensure(std::max<uint64_t>(count, 1) * dim * 4), unit_rows,
@@ -975,6 +986,7 @@ int ss_store_build(ss_ctx* c, const float* rows, const float* coverage, uint64_t
         if (c->h_u32[0]) throw Error(SS_ERR_DATA, "build_store: a covered gaussian has a zero embedding row");
         c->store_count = count;
         c->store_dim = dim;
+        c->store_half_ok = false;
         if (count_out) *count_out = count;
     });
 }
@@ -1007,6 +1019,76 @@ float* prepare_queries(ss_ctx* c, const float* queries, uint32_t nq) {
 }
 } // namespace
 
+namespace {
+// Exact scan: every (query, row) score with the exact dot_lanes, per-query
+// top-k by (sim desc, id asc).  Rows of out are [q][k].
+void topk_exact(ss_ctx* c, const float* d_qn, uint32_t nq, uint32_t k, uint32_t* oid, float* osim) {
+    cudaStream_t s = c->stream;
+    const uint64_t count = c->store_count;
+    const uint32_t qt = (uint32_t)score_query_tile();
+    const uint32_t tile = std::max<uint32_t>(qt, 64);
+    auto* sc_buf = static_cast<float*>(c->scores.ensure((size_t)tile * count * 4));
+    for (uint32_t q0 = 0; q0 < nq; q0 += tile) {
+        const uint32_t nt = std::min(tile, nq - q0);
+        for (uint32_t t = 0; t < nt; t += qt)
+            own_launch(c, launch_score(c->store_rows.as<float>(), count, c->store_dim, d_qn, q0 + std::min(nt, t + qt),
+                                       q0 + t, sc_buf + (size_t)t * count, s),
+                       SS_K_QUERY);
+        own_launch(c, launch_topk(sc_buf, c->store_ids.as<uint32_t>(), count, k, nt, q0, oid, osim, s), SS_K_QUERY);
+    }
+}
+
+constexpr uint32_t kQueryChunk = 1024; // queries per coarse-score pass
+constexpr uint32_t kCandCap = 4096;    // candidates kept per query
+
+// Tensor-core path: fp16 coarse scores (tcgen05), candidate selection with a
+// proven margin, exact rescoring.  Returns false when some query's candidate
+// set is unusable (overflow, or fewer than k finite candidates); the caller
+// then answers with the exact scan.
+bool topk_tensor(ss_ctx* c, const float* d_qn, uint32_t nq, uint32_t k, uint32_t* oid, float* osim) {
+    cudaStream_t s = c->stream;
+    const uint64_t count = c->store_count;
+    const uint32_t dim = c->store_dim;
+    if (!c->num_sms) SS_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
+    if (!c->store_half_ok) {
+        void* h = c->store_half.ensure(count * dim * 2);
+        own_launch(c, ss::launch_to_half(c->store_rows.as<float>(), count * dim, h, s), SS_K_QUERY);
+        c->store_half_ok = true;
+    }
+    void* qh = c->qhalf.ensure((uint64_t)nq * dim * 2);
+    own_launch(c, ss::launch_to_half(d_qn, (uint64_t)nq * dim, qh, s), SS_K_QUERY);
+    const uint64_t ld = (count + 7) / 8 * 8;
+    const uint32_t chunk = std::min(nq, kQueryChunk);
+    void* scores = c->tc_scores.ensure((uint64_t)chunk * ld * 2);
+    auto* cand = static_cast<uint32_t*>(c->cand.ensure((uint64_t)nq * kCandCap * 4));
+    auto* ccount = static_cast<uint32_t*>(c->cand_count.ensure((uint64_t)nq * 4));
+    auto* csim = static_cast<float*>(c->cand_sim.ensure((uint64_t)nq * kCandCap * 4));
+    for (uint32_t q0 = 0; q0 < nq; q0 += chunk) {
+        const uint32_t nt = std::min(chunk, nq - q0);
+        own_launch(c,
+                   ss::launch_coarse_scores(c->store_half.p, (uint32_t)count,
+                                            static_cast<const char*>(qh) + (uint64_t)q0 * dim * 2, nt, dim, scores, ld,
+                                            c->num_sms, s),
+                   SS_K_QUERY);
+        own_launch(c,
+                   ss::launch_select_candidates(scores, ld, (uint32_t)count, nt, k, 2.0f * ss::kCoarseEps,
+                                                cand + (uint64_t)q0 * kCandCap, kCandCap, ccount + q0, s),
+                   SS_K_QUERY);
+    }
+    own_launch(c,
+               ss::launch_rescore(c->store_rows.as<float>(), c->store_ids.as<uint32_t>(), dim, d_qn, nq, cand,
+                                  kCandCap, ccount, k, csim, oid, osim, s),
+               SS_K_QUERY);
+    std::vector<uint32_t> hc(nq);
+    SS_CUDA(cudaMemcpyAsync(hc.data(), ccount, (size_t)nq * 4, cudaMemcpyDeviceToHost, s));
+    SS_CUDA(cudaStreamSynchronize(s));
+    const uint64_t take = std::min<uint64_t>(k, count);
+    for (uint32_t q = 0; q < nq; ++q)
+        if (hc[q] > kCandCap || hc[q] < take) return false;
+    return true;
+}
+} // namespace
+
 int ss_query_topk(ss_ctx* c, const float* queries, uint32_t nq, uint32_t k, uint32_t* out_ids, float* out_sims,
                   uint64_t* out_counts) {
     return guarded([&] {
@@ -1020,20 +1102,12 @@ int ss_query_topk(ss_ctx* c, const float* queries, uint32_t nq, uint32_t k, uint
         cudaStream_t s = c->stream;
         Scope sc(c, s, SS_K_QUERY);
         const float* d_qn = prepare_queries(c, queries, nq);
-        const uint32_t qt = (uint32_t)score_query_tile();
-        const uint32_t tile = std::max<uint32_t>(qt, 64);
-        auto* sc_buf = static_cast<float*>(c->scores.ensure((size_t)tile * count * 4));
         auto* oid = static_cast<uint32_t*>(c->topk_ids.ensure((size_t)nq * k * 4));
         auto* osim = static_cast<float*>(c->topk_sims.ensure((size_t)nq * k * 4));
-        for (uint32_t q0 = 0; q0 < nq; q0 += tile) {
-            const uint32_t nt = std::min(tile, nq - q0);
-            for (uint32_t t = 0; t < nt; t += qt)
-                own_launch(c, launch_score(c->store_rows.as<float>(), count, c->store_dim, d_qn, q0 + std::min(nt, t + qt),
-                                           q0 + t, sc_buf + (size_t)t * count, s),
-                           SS_K_QUERY);
-            own_launch(c, launch_topk(sc_buf, c->store_ids.as<uint32_t>(), count, k, nt, q0, oid, osim, s), SS_K_QUERY);
-        }
-        // rows written by topk are [q][k] with k stride; take <= k
+        const bool tc_ok = c->store_dim % 64 == 0 && c->store_dim <= 4096 && count < (1ull << 31) &&
+                           (c->query_path == 2 || (c->query_path == 0 && count >= 16384));
+        if (!(tc_ok && topk_tensor(c, d_qn, nq, k, oid, osim))) topk_exact(c, d_qn, nq, k, oid, osim);
+        // rows written are [q][k] with k stride; take <= k
         std::vector<uint32_t> hid((size_t)nq * k);
         std::vector<float> hsim((size_t)nq * k);
         SS_CUDA(cudaMemcpyAsync(hid.data(), oid, hid.size() * 4, cudaMemcpyDeviceToHost, s));

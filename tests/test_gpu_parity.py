@@ -223,7 +223,15 @@ def test_store_build_bitwise_vs_oracle(gpu_ctx, oracle):
         assert unit[j].tobytes() == oracle.normalized_copy(rows[k]).tobytes()
 
 
-def test_query_topk_vs_reference_golden(gpu_ctx):
+@pytest.fixture
+def query_path(gpu_ctx, request):
+    gpu_ctx.set_query_path(request.param)
+    yield request.param
+    gpu_ctx.set_query_path(0)
+
+
+@pytest.mark.parametrize("query_path", [1, 2], indirect=True)
+def test_query_topk_vs_reference_golden(gpu_ctx, query_path):
     z = golden("query")
     gpu_ctx.store_set(z["ids"], z["rows"])
     ids, sims, cnt = gpu_ctx.query_topk(z["queries"], 37)
@@ -247,7 +255,8 @@ def test_query_edge_cases(gpu_ctx):
         gpu_ctx.query_topk(np.array([0.0, 0.0], np.float32), 1)
 
 
-def test_query_random_large_vs_oracle(gpu_ctx, oracle):
+@pytest.mark.parametrize("query_path", [1, 2], indirect=True)
+def test_query_random_large_vs_oracle(gpu_ctx, oracle, query_path):
     rng = np.random.default_rng(11)
     raw = rng.uniform(-0.5, 0.5, (20000, 512)).astype(np.float32)
     cnt = gpu_ctx.store_build(raw, np.ones(20000, np.float32))
@@ -256,3 +265,57 @@ def test_query_random_large_vs_oracle(gpu_ctx, oracle):
     gi, gs, gc = gpu_ctx.query_topk(q, 10)
     oi, os_, oc = oracle.query_topk(ids, unit, q, 10, threads=8)
     assert np.array_equal(gi, oi) and gs.tobytes() == os_.tobytes()
+
+
+def _tc_vs_oracle(ctx, oracle, ids, unit, q, k):
+    ctx.store_set(ids, unit)
+    ctx.set_query_path(2)
+    try:
+        gi, gs, gc = ctx.query_topk(q, k)
+    finally:
+        ctx.set_query_path(0)
+    oi, os_, oc = oracle.query_topk(ids, unit, q, k, threads=8)
+    assert np.array_equal(gc, oc)
+    assert np.array_equal(gi, oi)
+    assert gs.tobytes() == os_.tobytes()
+
+
+def _unit_rows(oracle, raw):
+    return np.stack([oracle.normalized_copy(r) for r in raw]).astype(np.float32)
+
+
+def test_query_tensor_core_chunked_ragged_vs_oracle(gpu_ctx, oracle):
+    # > 1024 queries (two coarse-score passes), a row count that is not a
+    # multiple of the 128-row tile nor of 8, and k at the device maximum
+    rng = np.random.default_rng(21)
+    raw = rng.standard_normal((5003, 128)).astype(np.float32)
+    unit = _unit_rows(oracle, raw)
+    ids = rng.permutation(1 << 20)[:5003].astype(np.uint32)
+    q = rng.standard_normal((1100, 128)).astype(np.float32)
+    _tc_vs_oracle(gpu_ctx, oracle, ids, unit, q, 64)
+
+
+def test_query_tensor_core_duplicates_and_near_ties(gpu_ctx, oracle):
+    # clusters of exact duplicates (ties by ascending id) and near-duplicates
+    # closer than fp16 resolution: the coarse scores cannot order them, the
+    # exact rescoring must
+    rng = np.random.default_rng(22)
+    base = rng.standard_normal((400, 256)).astype(np.float32)
+    raw = np.repeat(base, 20, axis=0)
+    raw[1::2] += rng.standard_normal((raw.shape[0] // 2, 256)).astype(np.float32) * 1e-4
+    unit = _unit_rows(oracle, raw)
+    ids = rng.permutation(raw.shape[0]).astype(np.uint32)
+    q = np.concatenate([base[:40], rng.standard_normal((40, 256)).astype(np.float32)])
+    _tc_vs_oracle(gpu_ctx, oracle, ids, unit, q, 25)
+
+
+def test_query_tensor_core_candidate_overflow_falls_back_exactly(gpu_ctx, oracle):
+    # 6000 identical rows: every row is a candidate (> the per-query cap), the
+    # batch is answered by the exact scan and must still match
+    rng = np.random.default_rng(23)
+    raw = np.repeat(rng.standard_normal((1, 64)).astype(np.float32), 6000, axis=0)
+    raw[::7] = rng.standard_normal((len(raw[::7]), 64)).astype(np.float32)
+    unit = _unit_rows(oracle, raw)
+    ids = np.arange(6000, dtype=np.uint32)[::-1].copy()
+    q = np.concatenate([raw[:2], rng.standard_normal((3, 64)).astype(np.float32)])
+    _tc_vs_oracle(gpu_ctx, oracle, ids, unit, q, 10)
