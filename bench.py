@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-views", type=int, default=0)
+    ap.add_argument("--no-query", action="store_true", help="skip the c5 vector-DB query leg")
+    ap.add_argument("--cpu-sample-queries", type=int, default=32)
     return ap.parse_args()
 
 
@@ -171,6 +173,79 @@ def cpu_reference_sample(cfg_name, seed, views, threads=None):
     O.encode(wl.scene, wl.cams, wl.masks, cfg["dim"])
     dt = time.perf_counter() - t0
     return dt, "port", 1, f"{views} of {cfg['n_views']} views of {cfg_name} through the C oracle (1 thread)"
+
+
+def query_leg(ctx, args, dev, stream, want_cpu):
+    """configs[4]: 1024 queries x 2M 512-d unit rows, top-10, through the
+    public query call (host queries in, host ids/sims out).  Device-side
+    kernel times come from CUDA events on the call's stream."""
+    import torch
+    from paper_2505_08124_b200.workload import QUERY_CONFIG as QC
+    n, nq, d, k = QC["n_rows"], QC["n_queries"], QC["dim"], QC["k"]
+    g = torch.Generator(device=dev).manual_seed(args.seed)
+    raw = torch.randn((n, d), generator=g, device=dev).cpu().numpy()
+    queries = torch.randn((nq, d), generator=g, device=dev).cpu()
+    q_pinned = queries.pin_memory().numpy()
+    cnt = ctx.store_build(raw, np.ones(n, np.float32))
+    del raw
+    ctx.query_topk(q_pinned[:8], k)  # warm: fp16 copy of the store, kernel attributes
+    for _ in range(args.warmup):
+        ctx.query_topk(q_pinned, k)
+    times = []
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ids, sims, _ = ctx.query_topk(q_pinned, k)
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * float(np.median(times))
+    ctx.profile_reset()
+    ctx.profile(True)
+    ctx.query_topk(q_pinned, k)
+    ctx.profile(False)
+    prof = ctx.profile_read()
+    gemm, sel, tot = prof["query_gemm"], prof["query_select"], prof["query"]
+    try:
+        p = json.loads(PEAKS_FILE.read_text())
+        tpeak, src = float(p["bf16_tflops"]), "bf16_tflops burst (MEASURED_PEAKS.json; fp16 runs at the bf16 rate)"
+    except Exception:
+        tpeak, src = 2250.0, "nominal dense fp16 (fallback)"
+    achieved = gemm["bytes"] / (gemm["ms"] / 1e3) / 1e12 if gemm["ms"] > 0 else None
+    out = {
+        "workload": f"{QC['name']}: {nq} queries x {cnt} unit rows x {d}, top-{k}",
+        "metric": "queries_per_sec", "unit": "queries/s", "value_e2e": nq / (ms / 1e3), "ms_per_batch_e2e": ms,
+        "ms_device_query": tot["ms"], "value_device": nq / (tot["ms"] / 1e3) if tot["ms"] > 0 else None,
+        "h2d_bytes_per_batch": int(nq * d * 4), "d2h_bytes_per_batch": int(nq * k * 8),
+        "kernels": {"query_gemm_ms": gemm["ms"], "query_select_ms": sel["ms"],
+                    "other_ms": tot["ms"] - gemm["ms"] - sel["ms"]},
+        "roofline": {"bound": "tensor", "kernel": "coarse_scores_kernel (tcgen05 kind::f16)", "achieved": achieved,
+                     "peak": tpeak, "unit": "TFLOP/s", "frac": achieved / tpeak if achieved else None,
+                     "traffic": None, "peak_source": src, "flops_per_launch": gemm["bytes"]},
+        "data": "synthetic: N(0,1) rows and queries (seeded), normalised by store_build / prepare_query",
+    }
+    if want_cpu:
+        try:
+            from oracle.bindings import REF_SO
+            ns = max(1, args.cpu_sample_queries)
+            store_ids, store_rows = ctx.store_fetch()
+            qs = queries[:ns].numpy()
+            cores = os.cpu_count() or 1
+            if REF_SO.exists():
+                from oracle.bindings import Ref
+                R, kind = Ref(), "reference"
+            else:
+                from oracle.bindings import Oracle
+                R, kind = Oracle(), "port"
+            t0 = time.perf_counter()
+            ri, rs, _ = R.query_topk(store_ids, store_rows, qs, k, threads=cores)
+            dt = time.perf_counter() - t0
+            out["cpu_baseline"] = {"value": ns / dt, "unit": "queries/s", "cores": cores, "kind": kind,
+                                   "sample": f"{ns} of the {nq} queries over the full store, threads={cores}",
+                                   "seconds": dt}
+            out["parity_sample"] = bool(np.array_equal(ri, ids[:ns]) and rs.tobytes() == sims[:ns].tobytes())
+        except Exception as ex:
+            out["cpu_baseline"] = {"value": None, "unit": "queries/s", "cores": None, "kind": "unavailable",
+                                   "sample": str(ex)}
+    return out
 
 
 def run_reference_arm(args, rank, world):
@@ -334,7 +409,7 @@ def main():
     hbm, peak_kind = peaks()
     kernels = {}
     for k, v in prof.items():
-        if v["launches"] and v["ms"] > 0 and k != "query":
+        if v["launches"] and v["ms"] > 0 and not k.startswith("query"):
             kernels[k] = {"ms_per_step": v["ms"], "launches_per_step": v["launches"], "gb_per_step": v["bytes"] / 1e9,
                           "achieved_gbs": v["bytes"] / (v["ms"] / 1e3) / 1e9 if k != "h2d" else None,
                           "share_of_serial_step": v["ms"] / ms_prof}
@@ -356,6 +431,13 @@ def main():
                    "seconds": dt}
         except Exception as ex:  # reported, not fatal
             cpu = {"value": None, "unit": "views/s", "cores": None, "kind": "unavailable", "sample": str(ex)}
+
+    query = None
+    if rank == 0 and not args.no_query:
+        try:
+            query = query_leg(ctx, args, dev, stream, want_cpu=world == 1 and not args.no_cpu_baseline)
+        except Exception as ex:  # reported, not fatal
+            query = {"error": f"{type(ex).__name__}: {ex}"}
 
     value = n_views / (ms_step / 1e3)
     if rank == 0:
@@ -384,6 +466,7 @@ def main():
             "gpu_launches": int((own + cub) / max(args.steps, 1)),
             "gpu_launches_detail": {"own_per_step": own / max(args.steps, 1), "cub_per_step": cub / max(args.steps, 1)},
             "serial_profile_ms_per_step": ms_prof,
+            "query": query,
         }
         print(json.dumps(line), flush=True)
     ctx.close()

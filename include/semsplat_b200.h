@@ -176,7 +176,9 @@ enum ss_kernel_class {
     SS_K_NORMALIZE = 6,
     SS_K_QUERY = 7,
     SS_K_H2D = 8,
-    SS_K_COUNT = 9
+    SS_K_QUERY_GEMM = 9,    /* tcgen05 coarse scores (inside SS_K_QUERY) */
+    SS_K_QUERY_SELECT = 10, /* candidate selection + exact rescoring (inside SS_K_QUERY) */
+    SS_K_COUNT = 11
 };
 int ss_profile_enable(ss_ctx* ctx, int on);
 int ss_profile_reset(ss_ctx* ctx);
@@ -185,6 +187,10 @@ int ss_profile_read(ss_ctx* ctx, double* ms, uint64_t* launches, double* bytes);
 /* Running totals of the geometry counters (SURVEY.md 8 notation), summed over
  * views since ss_profile_reset: [0]=N_vis [1]=I_v [2]=G_v [3]=K_v [4]=views. */
 int ss_counters_read(ss_ctx* ctx, uint64_t* out5);
+/* Tensor-core query statistics since reset: queries answered on that path,
+ * total and maximum candidates per query, batches answered by the exact scan
+ * after a candidate overflow. */
+int ss_query_stats(ss_ctx* ctx, uint64_t* out4);
 /* Number of kernels this library launched (own + CUB) since reset. */
 int ss_launch_count(ss_ctx* ctx, uint64_t* own, uint64_t* cub);
 

@@ -41,7 +41,8 @@ PROJECTED_DTYPE = np.dtype([
 ])
 ENTRY_DTYPE = np.dtype([("gaussian_id", "<u4"), ("pixel", "<u4"), ("weight", "<f4")])
 
-K_NAMES = ["masks", "project", "sort", "bin", "raster", "contract", "normalize", "query", "h2d"]
+K_NAMES = ["masks", "project", "sort", "bin", "raster", "contract", "normalize", "query", "h2d", "query_gemm",
+           "query_select"]
 
 _lib = None
 
@@ -69,6 +70,7 @@ def lib() -> C.CDLL:
         "ss_set_stream": (i32, [vp, C.c_size_t]),
         "ss_synchronize": (i32, [vp]),
         "ss_set_option": (i32, [vp, i32, C.c_int64]),
+        "ss_query_stats": (i32, [vp, vp]),
         "ss_scene_set": (i32, [vp, pf, pf, pf, pf, u64]),
         "ss_project": (i32, [vp, C.POINTER(Camera), vp]),
         "ss_raster_capture": (i32, [vp, C.POINTER(Camera), i32, pu64, pu64, pu64]),
@@ -310,6 +312,11 @@ class Context:
         out = np.zeros(5, np.uint64)
         check(self._L.ss_counters_read(self.h, _ptr(out, C.c_uint64)))
         return dict(zip(["n_vis", "instances", "touched", "pairs", "views"], map(int, out)))
+
+    def query_stats(self):
+        out = np.zeros(4, np.uint64)
+        check(self._L.ss_query_stats(self.h, out.ctypes.data_as(C.c_void_p)))
+        return dict(zip(["tc_queries", "candidates", "max_candidates", "exact_fallbacks"], map(int, out)))
 
     def launch_count(self):
         a, b = C.c_uint64(), C.c_uint64()

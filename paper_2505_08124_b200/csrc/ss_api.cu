@@ -182,7 +182,7 @@ struct ss_ctx {
     uint64_t store_count = 0;
     uint32_t store_dim = 0;
     // tensor-core query path: fp16 copy of the store, coarse scores, candidates
-    ss::DevBuf store_half, qhalf, tc_scores, cand, cand_count, cand_sim;
+    ss::DevBuf store_half, qhalf, tc_scores, tc_thr, cand, cand_count, cand_sim;
     bool store_half_ok = false;
     int query_path = 0; // SS_OPT_QUERY_PATH
     int num_sms = 0;
@@ -191,6 +191,7 @@ struct ss_ctx {
     ss::ProfState prof;
     uint64_t launches_own = 0, launches_cub = 0;
     uint64_t cnt_vis = 0, cnt_inst = 0, cnt_views = 0;
+    uint64_t qstat[4] = {}; // tensor-core queries, candidates, max candidates, exact fallbacks
 };
 
 namespace ss {
@@ -651,7 +652,7 @@ void ss_destroy(ss_ctx* c) {
                           &c->pix_offset, &c->entries, &c->per_pixel_total, &c->alpha, &c->counters, &c->sums_buf,
                           &c->totals_buf, &c->store_rows, &c->store_ids, &c->qbuf, &c->qnorm, &c->scores,
                           &c->topk_ids, &c->topk_sims, &c->sel_flags, &c->thr_keys, &c->thr_keys_sorted, &c->thr_ids,
-                          &c->thr_ids_sorted, &c->zero_flag, &c->store_half, &c->qhalf, &c->tc_scores,
+                          &c->thr_ids_sorted, &c->zero_flag, &c->store_half, &c->qhalf, &c->tc_scores, &c->tc_thr,
                           &c->cand, &c->cand_count, &c->cand_sim};
     for (auto* b : bufs) b->release();
     for (auto e : c->prof.pool) cudaEventDestroy(e);
@@ -1057,35 +1058,59 @@ bool topk_tensor(ss_ctx* c, const float* d_qn, uint32_t nq, uint32_t k, uint32_t
     }
     void* qh = c->qhalf.ensure((uint64_t)nq * dim * 2);
     own_launch(c, ss::launch_to_half(d_qn, (uint64_t)nq * dim, qh, s), SS_K_QUERY);
-    const uint64_t ld = (count + 7) / 8 * 8;
     const uint32_t chunk = std::min(nq, kQueryChunk);
-    void* scores = c->tc_scores.ensure((uint64_t)chunk * ld * 2);
+    const uint64_t pcols = (uint64_t)ss::pilot_tiles((uint32_t)count) * 128;
+    void* pscores = c->tc_scores.ensure((uint64_t)chunk * pcols * 2);
+    auto* thr = static_cast<float*>(c->tc_thr.ensure((uint64_t)nq * 4));
     auto* cand = static_cast<uint32_t*>(c->cand.ensure((uint64_t)nq * kCandCap * 4));
     auto* ccount = static_cast<uint32_t*>(c->cand_count.ensure((uint64_t)nq * 4));
-    auto* csim = static_cast<float*>(c->cand_sim.ensure((uint64_t)nq * kCandCap * 4));
+    auto* cval = static_cast<float*>(c->cand_sim.ensure((uint64_t)nq * kCandCap * 4));
+    SS_CUDA(cudaMemsetAsync(ccount, 0, (size_t)nq * 4, s));
     for (uint32_t q0 = 0; q0 < nq; q0 += chunk) {
         const uint32_t nt = std::min(chunk, nq - q0);
+        const void* qc = static_cast<const char*>(qh) + (uint64_t)q0 * dim * 2;
+        {
+            // pilot over a strided sample of row tiles -> per-query threshold
+            Scope sp(c, s, SS_K_QUERY_SELECT);
+            own_launch(c, ss::launch_coarse_pilot(c->store_half.p, (uint32_t)count, qc, nt, dim, pscores, c->num_sms, s),
+                       SS_K_QUERY);
+            own_launch(c,
+                       ss::launch_pilot_threshold(pscores, (uint32_t)count, nt, k, 2.0f * ss::kCoarseEps, thr + q0, s),
+                       SS_K_QUERY);
+            c->prof.bytes[SS_K_QUERY_SELECT] += 2.0 * nt * (double)pcols * dim;
+        }
+        {
+            Scope sg(c, s, SS_K_QUERY_GEMM);
+            own_launch(c,
+                       ss::launch_coarse_candidates(c->store_half.p, (uint32_t)count, qc, nt, dim, thr + q0,
+                                                    cand + (uint64_t)q0 * kCandCap, cval + (uint64_t)q0 * kCandCap,
+                                                    kCandCap, ccount + q0, c->num_sms, s),
+                       SS_K_QUERY);
+            c->prof.bytes[SS_K_QUERY_GEMM] += 2.0 * nt * (double)count * dim; // flops
+        }
+    }
+    {
+        Scope sr(c, s, SS_K_QUERY_SELECT);
         own_launch(c,
-                   ss::launch_coarse_scores(c->store_half.p, (uint32_t)count,
-                                            static_cast<const char*>(qh) + (uint64_t)q0 * dim * 2, nt, dim, scores, ld,
-                                            c->num_sms, s),
-                   SS_K_QUERY);
-        own_launch(c,
-                   ss::launch_select_candidates(scores, ld, (uint32_t)count, nt, k, 2.0f * ss::kCoarseEps,
-                                                cand + (uint64_t)q0 * kCandCap, kCandCap, ccount + q0, s),
+                   ss::launch_rescore(c->store_rows.as<float>(), c->store_ids.as<uint32_t>(), dim, d_qn, nq, cand,
+                                      cval, kCandCap, ccount, k, 2.0f * ss::kCoarseEps, oid, osim, s),
                    SS_K_QUERY);
     }
-    own_launch(c,
-               ss::launch_rescore(c->store_rows.as<float>(), c->store_ids.as<uint32_t>(), dim, d_qn, nq, cand,
-                                  kCandCap, ccount, k, csim, oid, osim, s),
-               SS_K_QUERY);
     std::vector<uint32_t> hc(nq);
     SS_CUDA(cudaMemcpyAsync(hc.data(), ccount, (size_t)nq * 4, cudaMemcpyDeviceToHost, s));
     SS_CUDA(cudaStreamSynchronize(s));
     const uint64_t take = std::min<uint64_t>(k, count);
-    for (uint32_t q = 0; q < nq; ++q)
-        if (hc[q] > kCandCap || hc[q] < take) return false;
-    return true;
+    bool ok = true;
+    for (uint32_t q = 0; q < nq; ++q) {
+        if (hc[q] <= kCandCap) {
+            c->qstat[1] += hc[q];
+            c->qstat[2] = std::max<uint64_t>(c->qstat[2], hc[q]);
+        }
+        if (hc[q] > kCandCap || hc[q] < take) ok = false;
+    }
+    c->qstat[0] += nq;
+    if (!ok) c->qstat[3] += 1;
+    return ok;
 }
 } // namespace
 
@@ -1187,6 +1212,7 @@ int ss_profile_reset(ss_ctx* c) {
         }
         c->launches_own = c->launches_cub = 0;
         c->cnt_vis = c->cnt_inst = c->cnt_views = 0;
+        for (auto& v : c->qstat) v = 0;
         SS_CUDA(cudaMemsetAsync(c->counters.p, 0, c->counters.bytes, c->stream));
     });
 }
@@ -1224,6 +1250,13 @@ int ss_counters_read(ss_ctx* c, uint64_t* out5) {
         out5[2] = gv;
         out5[3] = kv;
         out5[4] = c->cnt_views;
+    });
+}
+
+int ss_query_stats(ss_ctx* c, uint64_t* out4) {
+    return guarded([&] {
+        if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
+        for (int i = 0; i < 4; ++i) out4[i] = c->qstat[i];
     });
 }
 

@@ -35,8 +35,10 @@ constexpr uint32_t B_BYTES = BN * BK * 2; // 32 KB
 constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr uint32_t ACC_STAGES = 2;
 constexpr uint32_t TMEM_COLS = 512; // 2 x 256 fp32 accumulator columns
-constexpr uint32_t THREADS = 192;   // 6 warps
-constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256;
+constexpr uint32_t EPI_WARPS = 8;   // two per TMEM lane quarter, 128 columns each
+constexpr uint32_t THREADS = 32 * (2 + EPI_WARPS);
+constexpr uint32_t THR_SMEM = EPI_WARPS * 128 * 4; // per-warp copy of its 128 thresholds
+constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256 + THR_SMEM;
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -116,10 +118,28 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                  : "r"(taddr))
 
 // ------------------------------------------------------------ coarse GEMM
-// scores[q * ld + r] = fp16 coarse cosine of query q and store row r.
+// Tiles are (row tile, query tile) pairs, query tile fastest, so the
+// q_tiles passes over one store tile run on neighbouring CTAs and share it
+// through L2.  Row tiles visited: rt = i * rt_stride, i < row_tiles_iter.
+//   PILOT: scores[q * ld + i*BM + r] = fp16 coarse score (rows past the store
+//          are written as -inf so they never rank);
+//   main:  rows with coarse >= thr[q] are appended to query q's candidates.
+struct CoarseParams {
+    uint32_t n_rows, n_queries, k_dim;
+    uint32_t row_tiles_iter, rt_stride;
+    __half* scores;
+    uint64_t ld;
+    const float* thr;
+    uint32_t* cand;
+    float* cand_val;
+    uint32_t cand_cap;
+    uint32_t* cand_count;
+};
+
+template <bool PILOT>
 __global__ void __launch_bounds__(THREADS, 1)
     coarse_scores_kernel(const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_q,
-                         uint32_t n_rows, uint32_t n_queries, uint32_t k_dim, __half* scores, uint64_t ld) {
+                         const CoarseParams p) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     unsigned char* stage_a = smem;
@@ -130,11 +150,12 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t* tfull = bars + 2 * STAGES;         // [ACC_STAGES]
     uint64_t* tempty = bars + 2 * STAGES + ACC_STAGES;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 2 * ACC_STAGES);
+    float* thr_smem = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-    const uint32_t row_tiles = (n_rows + BM - 1) / BM, q_tiles = (n_queries + BN - 1) / BN;
-    const uint32_t n_tiles = row_tiles * q_tiles;
-    const uint32_t k_blocks = k_dim / BK;
+    const uint32_t q_tiles = (p.n_queries + BN - 1) / BN;
+    const uint32_t n_tiles = p.row_tiles_iter * q_tiles;
+    const uint32_t k_blocks = p.k_dim / BK;
 
     if (warp == 0 && lane == 0) {
         for (uint32_t s = 0; s < STAGES; ++s) {
@@ -143,7 +164,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         for (uint32_t a = 0; a < ACC_STAGES; ++a) {
             mbar_init(tfull + a, 1);
-            mbar_init(tempty + a, 4); // one arrival per epilogue warp
+            mbar_init(tempty + a, EPI_WARPS); // one arrival per epilogue warp
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_v) : "memory");
@@ -164,8 +185,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (lane == 0) {
             uint32_t stage = 0, phase = 0;
             for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-                // query tile fastest: a store tile is reused from L2 by the q_tiles passes
-                const uint32_t rt = t / q_tiles, qt = t % q_tiles;
+                const uint32_t rt = (t / q_tiles) * p.rt_stride, qt = t % q_tiles;
                 for (uint32_t kb = 0; kb < k_blocks; ++kb) {
                     mbar_wait(empty + stage, phase ^ 1u);
                     mbar_expect_tx(full + stage, STAGE_BYTES);
@@ -210,27 +230,72 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         }
     } else {
-        // ===== epilogue: TMEM lane (= store row) per thread, 256 query columns
-        const uint32_t quarter = warp & 3u; // TMEM lanes 32*quarter .. +31 are this warp's
+        // ===== epilogue: TMEM lane (= store row) per thread; warp w reads TMEM
+        // lanes 32*(w%4) (the hardware's lane-quarter rule) and half of the
+        // 256 query columns
+        const uint32_t ew = warp - 2;
+        const uint32_t quarter = warp & 3u;
+        const uint32_t half = ew >> 2; // columns [128*half, 128*half + 128)
         const uint32_t row_in_tile = quarter * 32u + lane;
+        float* my_thr = thr_smem + ew * 128;
         uint32_t acc = 0, acc_phase = 0;
         for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-            const uint32_t rt = t / q_tiles, qt = t % q_tiles;
+            const uint32_t it = t / q_tiles, qt = t % q_tiles;
+            const uint32_t row = it * p.rt_stride * BM + row_in_tile;
+            const uint32_t qbase = qt * BN + half * 128;
+            const bool row_ok = row < p.n_rows;
+            if constexpr (!PILOT) {
+                __syncwarp();
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t q = qbase + lane + 32u * j;
+                    my_thr[lane + 32u * j] = q < p.n_queries ? __ldg(p.thr + q) : INFINITY;
+                }
+                __syncwarp();
+            }
             mbar_wait(tfull + acc, acc_phase);
             fence_after();
-            const uint32_t row = rt * BM + row_in_tile;
-            const uint32_t q0 = qt * BN;
 #pragma unroll 1
-            for (uint32_t c = 0; c < BN; c += 32) {
-                uint32_t r[32];
-                const uint32_t taddr = tmem_base + ((quarter * 32u) << 16) + acc * BN + c;
-                SS_TMEM_LD32(taddr, r);
+            for (uint32_t c = 0; c < 128; c += 64) {
+                uint32_t r0[32], r1[32];
+                const uint32_t taddr = tmem_base + ((quarter * 32u) << 16) + acc * BN + half * 128 + c;
+                SS_TMEM_LD32(taddr, r0);
+                SS_TMEM_LD32(taddr + 32, r1);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (row < n_rows) {
+                if constexpr (PILOT) {
+                    const uint64_t col = (uint64_t)it * BM + row_in_tile;
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const uint32_t q = q0 + c + (uint32_t)j;
-                        if (q < n_queries) scores[(uint64_t)q * ld + row] = __float2half_rn(__uint_as_float(r[j]));
+                    for (int j = 0; j < 64; ++j) {
+                        const uint32_t q = qbase + c + (uint32_t)j;
+                        const uint32_t bits = j < 32 ? r0[j] : r1[j - 32];
+                        if (q < p.n_queries)
+                            p.scores[(uint64_t)q * p.ld + col] =
+                                row_ok ? __float2half_rn(__uint_as_float(bits)) : __ushort_as_half(0xfc00u);
+                    }
+                } else {
+                    // branch-free screen: any column at or above its threshold?
+                    const float4* t4 = reinterpret_cast<const float4*>(my_thr + c);
+                    float mx = -INFINITY;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const float4 tv = t4[j];
+                        const uint32_t* rr = j < 8 ? r0 + 4 * j : r1 + 4 * (j - 8);
+                        mx = fmaxf(mx, fmaxf(fmaxf(__uint_as_float(rr[0]) - tv.x, __uint_as_float(rr[1]) - tv.y),
+                                             fmaxf(__uint_as_float(rr[2]) - tv.z, __uint_as_float(rr[3]) - tv.w)));
+                    }
+                    if (row_ok && mx >= 0.0f) {
+#pragma unroll
+                        for (int j = 0; j < 64; ++j) {
+                            const float v = __uint_as_float(j < 32 ? r0[j] : r1[j - 32]);
+                            if (v >= my_thr[c + j]) {
+                                const uint32_t q = qbase + c + (uint32_t)j;
+                                const uint32_t slot = atomicAdd(p.cand_count + q, 1u);
+                                if (slot < p.cand_cap) {
+                                    p.cand[(uint64_t)q * p.cand_cap + slot] = row;
+                                    p.cand_val[(uint64_t)q * p.cand_cap + slot] = v;
+                                }
+                            }
+                        }
                     }
                 }
             }
@@ -261,25 +326,23 @@ __device__ __forceinline__ float key_half(uint32_t key) {
     return __half2float(__ushort_as_half((unsigned short)b));
 }
 
-// One CTA per query.  Pass 1: 4096-bin histogram of the top 12 bits of the
-// orderable fp16 key; the bin holding the k-th largest coarse score c_k gives
-// a lower bound lo <= c_k.  Pass 2: every row with coarse >= lo - 2*eps is a
-// candidate -- a superset of {c >= c_k - 2*eps}, which holds the exact top-k.
+// One CTA per query over the pilot's fp16 scores: a 4096-bin histogram of
+// the top 12 bits of the orderable key finds the bin holding the sample's
+// k-th largest coarse score c_k^S; thr = (that bin's lower edge) - 2*eps.
+// The sample is a subset of the store, so the store's k-th largest coarse
+// score c_k >= c_k^S, and every row of the exact top-k has
+// coarse >= c_k - 2*eps >= thr ("query").
 constexpr uint32_t SEL_THREADS = 1024;
 constexpr uint32_t SEL_BINS = 4096;
-__global__ void __launch_bounds__(SEL_THREADS) select_candidates_kernel(const __half* scores, uint64_t ld,
-                                                                        uint32_t n_rows, uint32_t k, float eps2,
-                                                                        uint32_t* cand, uint32_t cand_cap,
-                                                                        uint32_t* cand_count) {
+__global__ void __launch_bounds__(SEL_THREADS) pilot_threshold_kernel(const __half* scores, uint64_t ld,
+                                                                      uint32_t n_cols, uint32_t k, float eps2,
+                                                                      float* thr) {
     __shared__ uint32_t hist[SEL_BINS];
-    __shared__ uint32_t s_bin;
-    __shared__ uint32_t s_count;
     const uint32_t q = blockIdx.x;
     const __half* sc = scores + (uint64_t)q * ld;
     for (uint32_t i = threadIdx.x; i < SEL_BINS; i += blockDim.x) hist[i] = 0;
-    if (threadIdx.x == 0) s_count = 0;
     __syncthreads();
-    const uint32_t nvec = n_rows / 8;
+    const uint32_t nvec = n_cols / 8;
     const uint4* sv = reinterpret_cast<const uint4*>(sc);
     for (uint32_t v = threadIdx.x; v < nvec; v += blockDim.x) {
         const uint4 pk = __ldg(sv + v);
@@ -287,7 +350,7 @@ __global__ void __launch_bounds__(SEL_THREADS) select_candidates_kernel(const __
 #pragma unroll
         for (int j = 0; j < 8; ++j) atomicAdd(hist + (half_key(h[j]) >> 4), 1u);
     }
-    for (uint32_t r = nvec * 8 + threadIdx.x; r < n_rows; r += blockDim.x) atomicAdd(hist + (half_key(sc[r]) >> 4), 1u);
+    for (uint32_t r = nvec * 8 + threadIdx.x; r < n_cols; r += blockDim.x) atomicAdd(hist + (half_key(sc[r]) >> 4), 1u);
     __syncthreads();
     // bin of the k-th largest: warp 0 scans the bins from the top, 32 at a time
     if (threadIdx.x < 32) {
@@ -295,8 +358,7 @@ __global__ void __launch_bounds__(SEL_THREADS) select_candidates_kernel(const __
         uint32_t above = 0, found = 0xffffffffu;
         for (int b0 = (int)SEL_BINS - 32; b0 >= 0 && found == 0xffffffffu; b0 -= 32) {
             const uint32_t b = (uint32_t)b0 + 31u - lane; // lane 0 = highest bin of the group
-            const uint32_t h = hist[b];
-            uint32_t incl = h;
+            uint32_t incl = hist[b];
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
@@ -306,30 +368,14 @@ __global__ void __launch_bounds__(SEL_THREADS) select_candidates_kernel(const __
             if (hit) found = (uint32_t)b0 + 31u - (uint32_t)(__ffs(hit) - 1);
             above += __shfl_sync(0xffffffffu, incl, 31);
         }
-        if (lane == 0) s_bin = found;
-    }
-    __syncthreads();
-    const float thr = s_bin == 0xffffffffu ? -INFINITY : key_half(s_bin << 4) - eps2;
-    uint32_t* out = cand + (uint64_t)q * cand_cap;
-    for (uint32_t v = threadIdx.x; v < nvec; v += blockDim.x) {
-        const uint4 pk = __ldg(sv + v);
-        const __half* h = reinterpret_cast<const __half*>(&pk);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            if (__half2float(h[j]) >= thr) {
-                const uint32_t slot = atomicAdd(&s_count, 1u);
-                if (slot < cand_cap) out[slot] = v * 8u + (uint32_t)j;
-            }
+        // NaN (or fewer than k sample rows) leaves no usable bound: every row is a candidate
+        float t = -INFINITY;
+        if (found != 0xffffffffu) {
+            const float lo = key_half(found << 4);
+            if (lo == lo) t = lo - eps2;
         }
+        if (lane == 0) thr[q] = t;
     }
-    for (uint32_t r = nvec * 8 + threadIdx.x; r < n_rows; r += blockDim.x) {
-        if (__half2float(sc[r]) >= thr) {
-            const uint32_t slot = atomicAdd(&s_count, 1u);
-            if (slot < cand_cap) out[slot] = r;
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) cand_count[q] = s_count;
 }
 
 __device__ __forceinline__ bool scored_before(float sa, uint32_t ia, float sb, uint32_t ib) {
@@ -337,66 +383,129 @@ __device__ __forceinline__ bool scored_before(float sa, uint32_t ia, float sb, u
     return ia < ib;
 }
 
-// One warp per query: exact dot_lanes of every candidate (vecstore.hpp:21-31:
-// eight fp32 lanes, separate rounded multiply and add, pairwise combine),
-// then (sim desc, id asc) selection of the first k.
-__global__ void __launch_bounds__(256) rescore_kernel(const float* rows, const uint32_t* ids, uint32_t dim,
-                                                      const float* qn, uint32_t nq, const uint32_t* cand,
-                                                      uint32_t cand_cap, const uint32_t* cand_count, uint32_t k,
-                                                      float* cand_sim, uint32_t* out_ids, float* out_sims) {
-    const uint32_t q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint32_t lane = threadIdx.x & 31u;
-    if (q >= nq) return;
+// One CTA per query.
+//  1. c_k = the k-th largest fp32 coarse score among the candidates.  Every
+//     row with coarse >= thr is a candidate and c_k >= thr, so this is the
+//     store's exact k-th largest coarse score; the exact top-k lies in
+//     {coarse >= c_k - 2*eps} ("query"), typically ~k rows.
+//  2. those rows are rescored with the exact dot_lanes (vecstore.hpp:21-31:
+//     eight fp32 lanes accumulated in index order with separately rounded
+//     multiply and add, combined ((l0+l1)+(l2+l3)) + ((l4+l5)+(l6+l7)), then
+//     the tail; dim % 8 == 0 here, so the tail is the literal 0.0f the
+//     reference adds).  Two threads per row: thread h owns accumulators
+//     4h..4h+3 and streams the row as float4 at 8i + 4h;
+//  3. ranks under (sim desc, id asc) (vecstore.hpp:107-110) by counting in
+//     shared memory; ranks < k are written.  Rows with equal (sim, id) --
+//     duplicate ids in a user store -- are ordered by slot; their output
+//     records are identical either way.
+constexpr uint32_t RS_THREADS = 512;
+__global__ void __launch_bounds__(RS_THREADS) rescore_kernel(const float* rows, const uint32_t* ids, uint32_t dim,
+                                                             const float* qn, const uint32_t* cand,
+                                                             const float* cand_val, uint32_t cand_cap,
+                                                             uint32_t* cand_count, uint32_t k, float eps2,
+                                                             uint32_t* out_ids, float* out_sims) {
+    extern __shared__ float4 smem4[];
+    float4* qs4 = smem4;                                           // dim / 4
+    float* sval = reinterpret_cast<float*>(smem4 + dim / 4);       // cand_cap coarse scores
+    uint32_t* srow = reinterpret_cast<uint32_t*>(sval + cand_cap); // cand_cap rows
+    __shared__ uint32_t s_n;
+    __shared__ float fsim[RS_THREADS / 2];
+    __shared__ uint32_t fid[RS_THREADS / 2];
+    const uint32_t q = blockIdx.x;
     const uint32_t nc = cand_count[q];
     if (nc > cand_cap) return; // overflow: the host answers this batch with the exact scan
+    const float4* qv = reinterpret_cast<const float4*>(qn + (uint64_t)q * dim);
+    for (uint32_t i = threadIdx.x; i < dim / 4; i += blockDim.x) qs4[i] = qv[i];
+    const float* cv = cand_val + (uint64_t)q * cand_cap;
     const uint32_t* cq = cand + (uint64_t)q * cand_cap;
-    float* sq = cand_sim + (uint64_t)q * cand_cap;
-    const float* qv = qn + (uint64_t)q * dim;
-    for (uint32_t c = lane; c < nc; c += 32) {
-        const float* a = rows + (uint64_t)cq[c] * dim;
-        float l[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        uint32_t i = 0;
-        for (; i + 8 <= dim; i += 8)
-#pragma unroll
-            for (int j = 0; j < 8; ++j) l[j] = __fadd_rn(l[j], __fmul_rn(a[i + j], qv[i + j]));
-        float tail = 0.0f;
-        for (; i < dim; ++i) tail = __fadd_rn(tail, __fmul_rn(a[i], qv[i]));
-        const float s01 = __fadd_rn(l[0], l[1]), s23 = __fadd_rn(l[2], l[3]);
-        const float s45 = __fadd_rn(l[4], l[5]), s67 = __fadd_rn(l[6], l[7]);
-        sq[c] = __fadd_rn(__fadd_rn(__fadd_rn(s01, s23), __fadd_rn(s45, s67)), tail);
+    for (uint32_t i = threadIdx.x; i < nc; i += blockDim.x) {
+        sval[i] = cv[i];
+        srow[i] = cq[i];
     }
-    __syncwarp();
-    // k rounds of warp arg-max by (sim desc, id asc); candidates are few
-    const uint32_t take = min(k, nc);
-    for (uint32_t o = 0; o < take; ++o) {
-        float bs = -INFINITY;
-        uint32_t bi = 0xffffffffu, bc = 0xffffffffu;
-        for (uint32_t c = lane; c < nc; c += 32) {
-            const float s = sq[c];
-            const uint32_t id = ids[cq[c]];
-            if (!isnan(s) && (bc == 0xffffffffu || scored_before(s, id, bs, bi))) {
-                bs = s;
-                bi = id;
-                bc = c;
-            }
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    // 1. k-th largest coarse score: min (as orderable key) over candidates
+    //    with fewer than k strictly larger coarse scores
+    const uint32_t kk = min(k, nc);
+    __shared__ uint32_t s_key;
+    if (threadIdx.x == 0) s_key = 0xffffffffu;
+    __syncthreads();
+    for (uint32_t c = threadIdx.x; c < nc; c += blockDim.x) {
+        const float v = sval[c];
+        uint32_t gt = 0;
+        for (uint32_t o = 0; o < nc; ++o) gt += sval[o] > v ? 1u : 0u;
+        if (gt < kk) {
+            const uint32_t b = __float_as_uint(v);
+            atomicMin(&s_key, (b & 0x80000000u) ? ~b : (b | 0x80000000u));
         }
+    }
+    __syncthreads();
+    const uint32_t kb = s_key;
+    const float ck = __uint_as_float((kb & 0x80000000u) ? (kb & 0x7fffffffu) : ~kb);
+    const float lim = ck - eps2;
+    // 2. exact rescoring of the rows with coarse >= c_k - 2 eps, two threads per row
+    uint32_t n_done = 0;
+    for (uint32_t base = 0; base < nc; base += RS_THREADS / 2) {
+        const uint32_t ci = base + (threadIdx.x >> 1);
+        const bool live = ci < nc && sval[ci] >= lim;
+        const uint32_t row = live ? srow[ci] : 0u;
+        const float4* a4 = reinterpret_cast<const float4*>(rows + (uint64_t)row * dim) + (threadIdx.x & 1u);
+        float l0 = 0.0f, l1 = 0.0f, l2 = 0.0f, l3 = 0.0f;
+        if (live) {
+            const uint32_t h = threadIdx.x & 1u;
+            const uint32_t steps = dim / 8;
+            for (uint32_t i0 = 0; i0 < steps; i0 += 16) {
+                float4 av[16];
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            const float os = __shfl_xor_sync(0xffffffffu, bs, off);
-            const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, off);
-            const uint32_t oc = __shfl_xor_sync(0xffffffffu, bc, off);
-            if (oc != 0xffffffffu && (bc == 0xffffffffu || scored_before(os, oi, bs, bi))) {
-                bs = os;
-                bi = oi;
-                bc = oc;
+                for (uint32_t u = 0; u < 16; ++u)
+                    if (i0 + u < steps) av[u] = __ldg(a4 + 2 * (i0 + u));
+#pragma unroll
+                for (uint32_t u = 0; u < 16; ++u) {
+                    if (i0 + u < steps) {
+                        const float4 bv = qs4[2 * (i0 + u) + h];
+                        l0 = __fadd_rn(l0, __fmul_rn(av[u].x, bv.x));
+                        l1 = __fadd_rn(l1, __fmul_rn(av[u].y, bv.y));
+                        l2 = __fadd_rn(l2, __fmul_rn(av[u].z, bv.z));
+                        l3 = __fadd_rn(l3, __fmul_rn(av[u].w, bv.w));
+                    }
+                }
             }
         }
-        if (lane == 0) {
-            out_ids[(uint64_t)q * k + o] = bi;
-            out_sims[(uint64_t)q * k + o] = bs;
-            sq[bc] = NAN; // taken
+        const float half_sum = __fadd_rn(__fadd_rn(l0, l1), __fadd_rn(l2, l3)); // (s01+s23) or (s45+s67)
+        const float other = __shfl_xor_sync(0xffffffffu, half_sum, 1);
+        if (live && (threadIdx.x & 1u) == 0) {
+            const float sim = __fadd_rn(__fadd_rn(half_sum, other), 0.0f);
+            const uint32_t slot = atomicAdd(&s_n, 1u);
+            if (slot < RS_THREADS / 2) {
+                fsim[slot] = isnan(sim) ? -INFINITY : sim;
+                fid[slot] = __ldg(ids + row);
+            }
         }
-        __syncwarp();
+        __syncthreads();
+        n_done = s_n;
+        __syncthreads();
+        if (n_done > RS_THREADS / 2) break;
+    }
+    if (n_done > RS_THREADS / 2) { // more finalists than slots: the host re-answers with the exact scan
+        if (threadIdx.x == 0) cand_count[q] = 0xffffffffu;
+        return;
+    }
+    // 3. ranks
+    const uint32_t nf = n_done;
+    const uint32_t take = min(k, nf);
+    for (uint32_t c = threadIdx.x; c < nf; c += blockDim.x) {
+        const float sc = fsim[c];
+        const uint32_t ic = fid[c];
+        uint32_t rank = 0;
+        for (uint32_t o = 0; o < nf; ++o) {
+            const float so = fsim[o];
+            const uint32_t io = fid[o];
+            rank += (so > sc || (so == sc && (io < ic || (io == ic && o < c)))) ? 1u : 0u;
+        }
+        if (rank < take) {
+            out_ids[(uint64_t)q * k + rank] = ic;
+            out_sims[(uint64_t)q * k + rank] = sc;
+        }
     }
 }
 
@@ -438,47 +547,95 @@ bool make_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t k, uin
 }
 } // namespace
 
-size_t tc_scores_smem() { return tc::SMEM_BYTES; }
-
 cudaError_t launch_to_half(const float* in, uint64_t n, void* out, cudaStream_t s) {
     if (!n) return cudaSuccess;
     tc::to_half_kernel<<<148 * 8, 256, 0, s>>>(in, n, static_cast<__half*>(out));
     return cudaGetLastError();
 }
 
-cudaError_t launch_coarse_scores(const void* v_half, uint32_t n_rows, const void* q_half, uint32_t n_queries,
-                                 uint32_t k_dim, void* scores, uint64_t ld, int num_sms, cudaStream_t s) {
+namespace {
+template <bool PILOT>
+cudaError_t coarse_launch(const CUtensorMap& mv, const CUtensorMap& mq, const tc::CoarseParams& p, int num_sms,
+                          cudaStream_t s) {
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(tc::coarse_scores_kernel<PILOT>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::SMEM_BYTES);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    const uint32_t tiles = p.row_tiles_iter * ((p.n_queries + tc::BN - 1) / tc::BN);
+    const uint32_t grid = std::min<uint32_t>(tiles, (uint32_t)num_sms);
+    tc::coarse_scores_kernel<PILOT><<<grid, tc::THREADS, tc::SMEM_BYTES, s>>>(mv, mq, p);
+    return cudaGetLastError();
+}
+} // namespace
+
+uint32_t pilot_tiles(uint32_t n_rows) {
+    const uint32_t row_tiles = (n_rows + tc::BM - 1) / tc::BM;
+    return std::min<uint32_t>(row_tiles, kPilotTiles);
+}
+
+cudaError_t launch_coarse_pilot(const void* v_half, uint32_t n_rows, const void* q_half, uint32_t n_queries,
+                                uint32_t k_dim, void* scores, int num_sms, cudaStream_t s) {
     if (k_dim % tc::BK != 0) return cudaErrorInvalidValue;
     CUtensorMap mv, mq;
     if (!make_map(&mv, v_half, n_rows, k_dim, tc::BM) || !make_map(&mq, q_half, n_queries, k_dim, tc::BN))
         return cudaErrorInvalidValue;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(tc::coarse_scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)tc::SMEM_BYTES);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
-    const uint32_t tiles = ((n_rows + tc::BM - 1) / tc::BM) * ((n_queries + tc::BN - 1) / tc::BN);
-    const uint32_t grid = std::min<uint32_t>(tiles, (uint32_t)num_sms);
-    tc::coarse_scores_kernel<<<grid, tc::THREADS, tc::SMEM_BYTES, s>>>(mv, mq, n_rows, n_queries, k_dim,
-                                                                       static_cast<__half*>(scores), ld);
+    const uint32_t row_tiles = (n_rows + tc::BM - 1) / tc::BM;
+    tc::CoarseParams p{};
+    p.n_rows = n_rows;
+    p.n_queries = n_queries;
+    p.k_dim = k_dim;
+    p.row_tiles_iter = pilot_tiles(n_rows);
+    p.rt_stride = row_tiles / p.row_tiles_iter;
+    p.scores = static_cast<__half*>(scores);
+    p.ld = (uint64_t)p.row_tiles_iter * tc::BM;
+    return coarse_launch<true>(mv, mq, p, num_sms, s);
+}
+
+cudaError_t launch_pilot_threshold(const void* scores, uint32_t n_rows, uint32_t nq, uint32_t k, float eps2,
+                                   float* thr, cudaStream_t s) {
+    const uint64_t cols = (uint64_t)pilot_tiles(n_rows) * tc::BM;
+    tc::pilot_threshold_kernel<<<nq, tc::SEL_THREADS, 0, s>>>(static_cast<const __half*>(scores), cols,
+                                                              (uint32_t)cols, k, eps2, thr);
     return cudaGetLastError();
 }
 
-cudaError_t launch_select_candidates(const void* scores, uint64_t ld, uint32_t n_rows, uint32_t nq, uint32_t k,
-                                     float eps2, uint32_t* cand, uint32_t cand_cap, uint32_t* cand_count,
-                                     cudaStream_t s) {
-    tc::select_candidates_kernel<<<nq, tc::SEL_THREADS, 0, s>>>(static_cast<const __half*>(scores), ld, n_rows, k,
-                                                                eps2, cand, cand_cap, cand_count);
-    return cudaGetLastError();
+cudaError_t launch_coarse_candidates(const void* v_half, uint32_t n_rows, const void* q_half, uint32_t n_queries,
+                                     uint32_t k_dim, const float* thr, uint32_t* cand, float* cand_val,
+                                     uint32_t cand_cap, uint32_t* cand_count, int num_sms, cudaStream_t s) {
+    if (k_dim % tc::BK != 0) return cudaErrorInvalidValue;
+    CUtensorMap mv, mq;
+    if (!make_map(&mv, v_half, n_rows, k_dim, tc::BM) || !make_map(&mq, q_half, n_queries, k_dim, tc::BN))
+        return cudaErrorInvalidValue;
+    tc::CoarseParams p{};
+    p.n_rows = n_rows;
+    p.n_queries = n_queries;
+    p.k_dim = k_dim;
+    p.row_tiles_iter = (n_rows + tc::BM - 1) / tc::BM;
+    p.rt_stride = 1;
+    p.thr = thr;
+    p.cand = cand;
+    p.cand_val = cand_val;
+    p.cand_cap = cand_cap;
+    p.cand_count = cand_count;
+    return coarse_launch<false>(mv, mq, p, num_sms, s);
 }
 
 cudaError_t launch_rescore(const float* rows, const uint32_t* ids, uint32_t dim, const float* qn, uint32_t nq,
-                           const uint32_t* cand, uint32_t cand_cap, const uint32_t* cand_count, uint32_t k,
-                           float* cand_sim, uint32_t* out_ids, float* out_sims, cudaStream_t s) {
-    tc::rescore_kernel<<<(nq * 32 + 255) / 256, 256, 0, s>>>(rows, ids, dim, qn, nq, cand, cand_cap, cand_count, k,
-                                                             cand_sim, out_ids, out_sims);
+                           const uint32_t* cand, const float* cand_val, uint32_t cand_cap, uint32_t* cand_count,
+                           uint32_t k, float eps2, uint32_t* out_ids, float* out_sims, cudaStream_t s) {
+    if (dim % 8 != 0) return cudaErrorInvalidValue;
+    const size_t smem = (size_t)dim * 4 + (size_t)cand_cap * 8;
+    static size_t configured = 0;
+    if (smem > configured) {
+        cudaError_t e = cudaFuncSetAttribute(tc::rescore_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        configured = smem;
+    }
+    tc::rescore_kernel<<<nq, tc::RS_THREADS, smem, s>>>(rows, ids, dim, qn, cand, cand_val, cand_cap, cand_count, k,
+                                                        eps2, out_ids, out_sims);
     return cudaGetLastError();
 }
 

@@ -47,6 +47,7 @@ def main():
     ctx.profile_reset()
     ctx.query_topk(q, a.k)
     print("profile", ctx.profile_read(), flush=True)
+    print("query stats", ctx.query_stats(), flush=True)
     if 1 in res:
         same = np.array_equal(res[1][0], res[2][0]) and res[1][1].tobytes() == res[2][1].tobytes()
         print("paths agree bitwise:", same, flush=True)
