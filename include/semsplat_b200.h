@@ -92,7 +92,8 @@ int ss_synchronize(ss_ctx* ctx);
 /* Tuning options.  SS_OPT_LANES: per-view pipeline lanes (1 or 2, default 2);
  * 1 serialises views, which the bench uses for exclusive per-kernel timing.
  * SS_OPT_QUERY_PATH: 0 = auto (tensor-core coarse scoring + exact rescoring
- * for stores of >= 16384 rows with dim % 64 == 0), 1 = exact scan only,
+ * for stores of >= 16384 rows with dim % 64 == 0 and dim <= 512), 1 = exact
+ * scan only,
  * 2 = tensor-core path whenever dim allows.  Results are identical. */
 enum ss_option { SS_OPT_LANES = 1, SS_OPT_QUERY_PATH = 2 };
 int ss_set_option(ss_ctx* ctx, int option, int64_t value);

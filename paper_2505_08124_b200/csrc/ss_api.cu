@@ -1059,7 +1059,7 @@ bool topk_tensor(ss_ctx* c, const float* d_qn, uint32_t nq, uint32_t k, uint32_t
     void* qh = c->qhalf.ensure((uint64_t)nq * dim * 2);
     own_launch(c, ss::launch_to_half(d_qn, (uint64_t)nq * dim, qh, s), SS_K_QUERY);
     const uint32_t chunk = std::min(nq, kQueryChunk);
-    const uint64_t pcols = (uint64_t)ss::pilot_tiles((uint32_t)count) * 128;
+    const uint64_t pcols = ss::pilot_cols((uint32_t)count);
     void* pscores = c->tc_scores.ensure((uint64_t)chunk * pcols * 2);
     auto* thr = static_cast<float*>(c->tc_thr.ensure((uint64_t)nq * 4));
     auto* cand = static_cast<uint32_t*>(c->cand.ensure((uint64_t)nq * kCandCap * 4));
@@ -1129,7 +1129,7 @@ int ss_query_topk(ss_ctx* c, const float* queries, uint32_t nq, uint32_t k, uint
         const float* d_qn = prepare_queries(c, queries, nq);
         auto* oid = static_cast<uint32_t*>(c->topk_ids.ensure((size_t)nq * k * 4));
         auto* osim = static_cast<float*>(c->topk_sims.ensure((size_t)nq * k * 4));
-        const bool tc_ok = c->store_dim % 64 == 0 && c->store_dim <= 4096 && count < (1ull << 31) &&
+        const bool tc_ok = c->store_dim % 64 == 0 && c->store_dim <= 512 && count < (1ull << 31) &&
                            (c->query_path == 2 || (c->query_path == 0 && count >= 16384));
         if (!(tc_ok && topk_tensor(c, d_qn, nq, k, oid, osim))) topk_exact(c, d_qn, nq, k, oid, osim);
         // rows written are [q][k] with k stride; take <= k

@@ -25,20 +25,40 @@
 namespace ss {
 namespace tc {
 
-constexpr uint32_t BM = 128;        // store rows per tile (UMMA M)
-constexpr uint32_t BN = 256;        // queries per tile (UMMA N)
+// CTA pair (cta_group::2): the pair computes a 256-row x 256-query tile with
+// M=256 MMAs issued by the leader.  Each CTA stages its own 128 store rows
+// (A, streamed) and keeps its 128-query half of B resident in shared memory,
+// so per 64-wide k-block a CTA receives 16 KB from L2 and the tensor core
+// reads 64 B/clk of operands from each SM's shared memory -- half of what a
+// single-CTA M=128 tile needs, which is what bounds the single-CTA kernel.
+constexpr uint32_t BM = 128;        // store rows per CTA (pair: 256)
+constexpr uint32_t BN = 256;        // queries per pair tile (UMMA N)
+constexpr uint32_t BN_HALF = 128;   // resident B rows per CTA
 constexpr uint32_t BK = 64;         // fp16 per 128-byte swizzle row
 constexpr uint32_t UK = 16;         // UMMA K for kind::f16
-constexpr uint32_t STAGES = 4;
-constexpr uint32_t A_BYTES = BM * BK * 2; // 16 KB
-constexpr uint32_t B_BYTES = BN * BK * 2; // 32 KB
-constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr uint32_t MAX_K = 512;     // resident B half: 128 queries x 512 fp16 = 128 KB
+constexpr uint32_t STAGES = 5;
+constexpr uint32_t A_BYTES = BM * BK * 2;         // 16 KB
+constexpr uint32_t BKB_BYTES = BN_HALF * BK * 2;  // 16 KB per resident k-block of B
+constexpr uint32_t B_RES_BYTES = (MAX_K / BK) * BKB_BYTES;
 constexpr uint32_t ACC_STAGES = 2;
 constexpr uint32_t TMEM_COLS = 512; // 2 x 256 fp32 accumulator columns
-constexpr uint32_t EPI_WARPS = 8;   // two per TMEM lane quarter, 128 columns each
+#ifndef SS_QTC_EPI_WARPS
+#define SS_QTC_EPI_WARPS 8
+#endif
+constexpr uint32_t EPI_WARPS = SS_QTC_EPI_WARPS; // 4, 8 or 16: 1, 2 or 4 per TMEM lane quarter
+constexpr uint32_t EPI_COLS = BN / (EPI_WARPS / 4);
+#ifndef SS_QTC_EPI_ROUND
+#define SS_QTC_EPI_ROUND 16
+#endif
+// TMEM columns per tcgen05.ld round (8, 16, 32 or 64).  Measured on B200 for
+// the c5 query (GEMM only): 8 warps x16 1.63 ms, x8 1.70, x32 1.72, x64 1.90;
+// 4 warps x16 2.00, 16 warps x16 1.75; no TMEM reads at all 1.48.
+constexpr uint32_t EPI_ROUND = SS_QTC_EPI_ROUND;
 constexpr uint32_t THREADS = 32 * (2 + EPI_WARPS);
-constexpr uint32_t THR_SMEM = EPI_WARPS * 128 * 4; // per-warp copy of its 128 thresholds
-constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256 + THR_SMEM;
+constexpr uint32_t BAR_BYTES = 256;
+constexpr uint32_t THR_SMEM = EPI_WARPS * EPI_COLS * 4; // per-warp copy of its thresholds
+constexpr size_t SMEM_BYTES = 1024 + STAGES * A_BYTES + B_RES_BYTES + BAR_BYTES + THR_SMEM;
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -72,6 +92,35 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
 }
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of this CTA's variable at `local` in CTA `rank`
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t local, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+    return r;
+}
+// Arrive on the leader's barrier from either CTA.  Only tcgen05.ld results
+// are being handed over (ordered by tcgen05.wait::ld + fence::before_thread_sync),
+// so no cluster-scope release -- which would cost a GPU-wide MEMBAR per tile.
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// pair TMA: data into this CTA's shared memory, completion to the leader's barrier
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int32_t x,
+                                                 int32_t y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+        "%4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(bar_cluster), "r"(x), "r"(y)
+        : "memory");
+}
 
 // K-major, 128B-swizzled operand tile: 8-row atoms of 128 B, atoms 1024 B apart
 __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
@@ -84,13 +133,13 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
     return d;
 }
 
-// kind::f16 instruction descriptor: D fp32, A/B fp16, both K-major, M=128, N=256
+// kind::f16 instruction descriptor: D fp32, A/B fp16, both K-major, M=256 (pair), N=256
 __host__ __device__ constexpr uint32_t instr_desc() {
     return (1u << 4)            // c_format = F32
            | (0u << 7)          // a_format = F16
            | (0u << 10)         // b_format = F16
            | ((BN >> 3) << 17)  // N >> 3
-           | ((BM >> 4) << 24); // M >> 4
+           | (((2 * BM) >> 4) << 24); // M >> 4
 }
 
 __device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
@@ -98,12 +147,16 @@ __device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
+// arrives on the barrier at this offset in both CTAs of the pair
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-                 : "memory");
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((unsigned short)3)
+        : "memory");
 }
 
 #define SS_TMEM_LD32(taddr, r)                                                                                       \
@@ -115,6 +168,19 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                    "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),      \
                    "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),      \
                    "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                                                           \
+                 : "r"(taddr))
+
+#define SS_TMEM_LD16(taddr, r)                                                                                       \
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 "                                                           \
+                 "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"                                   \
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), \
+                   "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),        \
+                   "=r"(r[15])                                                                                     \
+                 : "r"(taddr))
+
+#define SS_TMEM_LD8(taddr, r)                                                                                        \
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"                           \
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])  \
                  : "r"(taddr))
 
 // ------------------------------------------------------------ coarse GEMM
@@ -136,25 +202,38 @@ struct CoarseParams {
     uint32_t* cand_count;
 };
 
+// Pair tile t (qt-major: t = qt * row_tiles_iter + it) covers store rows
+// [rt*2BM, rt*2BM + 2BM) with rt = it * rt_stride (CTA r of the pair owns
+// rows rt*2BM + r*BM + [0, BM)) and queries [qt*BN, qt*BN + BN) (CTA r keeps
+// queries qt*BN + r*BN_HALF + [0, BN_HALF) resident).  Pair c of G runs the
+// contiguous tile range [c*T/G, (c+1)*T/G), so it changes query block (and
+// reloads B) at most a few times.  TMEM of CTA r holds its BM rows x BN
+// queries of the accumulator.
 template <bool PILOT>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     coarse_scores_kernel(const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_q,
                          const CoarseParams p) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     unsigned char* stage_a = smem;
-    unsigned char* stage_b = smem + STAGES * A_BYTES;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-    uint64_t* full = bars;                       // [STAGES]
-    uint64_t* empty = bars + STAGES;             // [STAGES]
-    uint64_t* tfull = bars + 2 * STAGES;         // [ACC_STAGES]
-    uint64_t* tempty = bars + 2 * STAGES + ACC_STAGES;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 2 * ACC_STAGES);
-    float* thr_smem = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);
+    unsigned char* b_res = smem + STAGES * A_BYTES;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(b_res + B_RES_BYTES);
+    uint64_t* full = bars;                       // [STAGES]   leader: both CTAs' A landed
+    uint64_t* empty = bars + STAGES;             // [STAGES]   MMAs done with the slot (both CTAs)
+    uint64_t* tfull = bars + 2 * STAGES;         // [ACC_STAGES] accumulator ready (both CTAs)
+    uint64_t* tempty = tfull + ACC_STAGES;       // [ACC_STAGES] leader: both epilogues drained it
+    uint64_t* bfull = tempty + ACC_STAGES;       // leader: both resident B halves loaded
+    uint64_t* bempty = bfull + 1;                // MMAs done with the resident B (both CTAs)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bempty + 1);
+    float* thr_smem = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(bars) + BAR_BYTES);
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    const uint32_t rank = cluster_rank();
+    const uint32_t pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
     const uint32_t q_tiles = (p.n_queries + BN - 1) / BN;
-    const uint32_t n_tiles = p.row_tiles_iter * q_tiles;
+    const uint64_t n_tiles = (uint64_t)p.row_tiles_iter * q_tiles;
+    const uint32_t t_begin = (uint32_t)(n_tiles * pair / n_pairs);
+    const uint32_t t_end = (uint32_t)(n_tiles * (pair + 1) / n_pairs);
     const uint32_t k_blocks = p.k_dim / BK;
 
     if (warp == 0 && lane == 0) {
@@ -164,35 +243,47 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         for (uint32_t a = 0; a < ACC_STAGES; ++a) {
             mbar_init(tfull + a, 1);
-            mbar_init(tempty + a, EPI_WARPS); // one arrival per epilogue warp
+            mbar_init(tempty + a, 2 * EPI_WARPS); // one arrival per epilogue warp of either CTA
         }
+        mbar_init(bfull, 1);
+        mbar_init(bempty, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_v) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_q) : "memory");
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "n"(TMEM_COLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
     }
     fence_before();
-    __syncthreads();
+    cluster_sync_all(); // barriers of both CTAs initialised, TMEM allocated
     fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        // ===== TMA producer
+        // ===== TMA producer (both CTAs; completions land on the leader's barriers)
         if (lane == 0) {
-            uint32_t stage = 0, phase = 0;
-            for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-                const uint32_t rt = (t / q_tiles) * p.rt_stride, qt = t % q_tiles;
+            const uint32_t full0 = map_to_rank(smem_u32(full), 0), bfull0 = map_to_rank(smem_u32(bfull), 0);
+            uint32_t stage = 0, phase = 0, cur_qt = 0xffffffffu, be_phase = 0;
+            for (uint32_t t = t_begin; t < t_end; ++t) {
+                const uint32_t qt = t / p.row_tiles_iter, rt = (t % p.row_tiles_iter) * p.rt_stride;
+                if (qt != cur_qt) {
+                    if (cur_qt != 0xffffffffu) {
+                        mbar_wait(bempty, be_phase);
+                        be_phase ^= 1u;
+                    }
+                    if (rank == 0) mbar_expect_tx(bfull, 2 * k_blocks * BKB_BYTES);
+                    for (uint32_t kb = 0; kb < k_blocks; ++kb)
+                        tma_load_2d_pair(b_res + kb * BKB_BYTES, &map_q, bfull0, (int32_t)(kb * BK),
+                                         (int32_t)(qt * BN + rank * BN_HALF));
+                    cur_qt = qt;
+                }
                 for (uint32_t kb = 0; kb < k_blocks; ++kb) {
                     mbar_wait(empty + stage, phase ^ 1u);
-                    mbar_expect_tx(full + stage, STAGE_BYTES);
-                    tma_load_2d(stage_a + stage * A_BYTES, &map_v, full + stage, (int32_t)(kb * BK),
-                                (int32_t)(rt * BM));
-                    tma_load_2d(stage_b + stage * B_BYTES, &map_q, full + stage, (int32_t)(kb * BK),
-                                (int32_t)(qt * BN));
+                    if (rank == 0) mbar_expect_tx(full + stage, 2 * A_BYTES);
+                    tma_load_2d_pair(stage_a + stage * A_BYTES, &map_v, full0 + stage * 8, (int32_t)(kb * BK),
+                                     (int32_t)((rt * 2 + rank) * BM));
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1u;
@@ -201,28 +292,36 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         }
     } else if (warp == 1) {
-        // ===== MMA issuer (one thread)
-        if (lane == 0) {
+        // ===== MMA issuer (leader CTA, one thread)
+        if (rank == 0 && lane == 0) {
             constexpr uint32_t idesc = instr_desc();
-            uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
-            for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+            uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0, cur_qt = 0xffffffffu, bf_phase = 0;
+            for (uint32_t t = t_begin; t < t_end; ++t) {
+                const uint32_t qt = t / p.row_tiles_iter;
+                if (qt != cur_qt) {
+                    if (cur_qt != 0xffffffffu) mma_commit(bempty); // fires once the old B's MMAs retire
+                    mbar_wait(bfull, bf_phase);
+                    bf_phase ^= 1u;
+                    fence_after();
+                    cur_qt = qt;
+                }
                 mbar_wait(tempty + acc, acc_phase ^ 1u);
                 fence_after();
                 const uint32_t d = tmem_base + acc * BN;
                 for (uint32_t kb = 0; kb < k_blocks; ++kb) {
                     mbar_wait(full + stage, phase);
                     fence_after();
-                    const uint32_t a0 = smem_u32(stage_a + stage * A_BYTES), b0 = smem_u32(stage_b + stage * B_BYTES);
+                    const uint32_t a0 = smem_u32(stage_a + stage * A_BYTES), b0 = smem_u32(b_res + kb * BKB_BYTES);
 #pragma unroll
                     for (uint32_t k = 0; k < BK / UK; ++k)
                         mma_f16(d, smem_desc(a0 + k * UK * 2), smem_desc(b0 + k * UK * 2), idesc, (kb | k) != 0);
-                    mma_commit(empty + stage); // frees the smem slot once these MMAs retire
+                    mma_commit(empty + stage); // frees the slot in both CTAs once these MMAs retire
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1u;
                     }
                 }
-                mma_commit(tfull + acc); // accumulator ready for the epilogue
+                mma_commit(tfull + acc); // accumulator ready for both epilogues
                 if (++acc == ACC_STAGES) {
                     acc = 0;
                     acc_phase ^= 1u;
@@ -232,63 +331,84 @@ __global__ void __launch_bounds__(THREADS, 1)
     } else {
         // ===== epilogue: TMEM lane (= store row) per thread; warp w reads TMEM
         // lanes 32*(w%4) (the hardware's lane-quarter rule) and half of the
-        // 256 query columns
+        // tile's query columns
         const uint32_t ew = warp - 2;
         const uint32_t quarter = warp & 3u;
-        const uint32_t half = ew >> 2; // columns [128*half, 128*half + 128)
-        const uint32_t row_in_tile = quarter * 32u + lane;
-        float* my_thr = thr_smem + ew * 128;
-        uint32_t acc = 0, acc_phase = 0;
-        for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-            const uint32_t it = t / q_tiles, qt = t % q_tiles;
-            const uint32_t row = it * p.rt_stride * BM + row_in_tile;
-            const uint32_t qbase = qt * BN + half * 128;
+        const uint32_t half = ew >> 2; // column slice [EPI_COLS*half, EPI_COLS*half + EPI_COLS)
+        const uint32_t row_in_tile = rank * BM + quarter * 32u + lane;
+        const uint32_t tempty0 = map_to_rank(smem_u32(tempty), 0);
+        float* my_thr = thr_smem + ew * EPI_COLS;
+        uint32_t acc = 0, acc_phase = 0, cur_qt = 0xffffffffu;
+        for (uint32_t t = t_begin; t < t_end; ++t) {
+            const uint32_t qt = t / p.row_tiles_iter, it = t % p.row_tiles_iter;
+            const uint32_t row = it * p.rt_stride * (2 * BM) + row_in_tile;
+            const uint32_t qbase = qt * BN + half * EPI_COLS;
             const bool row_ok = row < p.n_rows;
             if constexpr (!PILOT) {
-                __syncwarp();
+                if (qt != cur_qt) {
+                    __syncwarp();
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const uint32_t q = qbase + lane + 32u * j;
-                    my_thr[lane + 32u * j] = q < p.n_queries ? __ldg(p.thr + q) : INFINITY;
+                    for (uint32_t j = 0; j < EPI_COLS / 32; ++j) {
+                        const uint32_t q = qbase + lane + 32u * j;
+                        my_thr[lane + 32u * j] = q < p.n_queries ? __ldg(p.thr + q) : INFINITY;
+                    }
+                    __syncwarp();
+                    cur_qt = qt;
                 }
-                __syncwarp();
             }
             mbar_wait(tfull + acc, acc_phase);
             fence_after();
+            // ROUND columns at a time; the accumulator goes back to the MMA warp
+            // right after the last tcgen05.ld.  (tcgen05.ld shares TMEM
+            // bandwidth with the MMAs accumulating the other stage: more
+            // loads in flight slow the MMAs down more than they gain.)
 #pragma unroll 1
-            for (uint32_t c = 0; c < 128; c += 64) {
-                uint32_t r0[32], r1[32];
-                const uint32_t taddr = tmem_base + ((quarter * 32u) << 16) + acc * BN + half * 128 + c;
-                SS_TMEM_LD32(taddr, r0);
-                SS_TMEM_LD32(taddr + 32, r1);
+            for (uint32_t c = 0; c < EPI_COLS; c += EPI_ROUND) {
+                uint32_t r[EPI_ROUND];
+                const uint32_t taddr = tmem_base + ((quarter * 32u) << 16) + acc * BN + half * EPI_COLS + c;
+                if constexpr (EPI_ROUND == 8) {
+                    SS_TMEM_LD8(taddr, r);
+                } else if constexpr (EPI_ROUND == 16) {
+                    SS_TMEM_LD16(taddr, r);
+                } else {
+                    SS_TMEM_LD32(taddr, r);
+                    if constexpr (EPI_ROUND == 64) SS_TMEM_LD32(taddr + 32, (r + 32));
+                }
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (c + EPI_ROUND >= EPI_COLS) {
+                    fence_before();
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (rank == 0) mbar_arrive(tempty + acc);
+                        else mbar_arrive_remote(tempty0 + acc * 8);
+                    }
+                }
                 if constexpr (PILOT) {
-                    const uint64_t col = (uint64_t)it * BM + row_in_tile;
+                    const uint64_t col = (uint64_t)it * (2 * BM) + row_in_tile;
 #pragma unroll
-                    for (int j = 0; j < 64; ++j) {
-                        const uint32_t q = qbase + c + (uint32_t)j;
-                        const uint32_t bits = j < 32 ? r0[j] : r1[j - 32];
+                    for (uint32_t j = 0; j < EPI_ROUND; ++j) {
+                        const uint32_t q = qbase + c + j;
                         if (q < p.n_queries)
                             p.scores[(uint64_t)q * p.ld + col] =
-                                row_ok ? __float2half_rn(__uint_as_float(bits)) : __ushort_as_half(0xfc00u);
+                                row_ok ? __float2half_rn(__uint_as_float(r[j])) : __ushort_as_half(0xfc00u);
                     }
                 } else {
                     // branch-free screen: any column at or above its threshold?
                     const float4* t4 = reinterpret_cast<const float4*>(my_thr + c);
                     float mx = -INFINITY;
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
+                    for (uint32_t j = 0; j < EPI_ROUND / 4; ++j) {
                         const float4 tv = t4[j];
-                        const uint32_t* rr = j < 8 ? r0 + 4 * j : r1 + 4 * (j - 8);
-                        mx = fmaxf(mx, fmaxf(fmaxf(__uint_as_float(rr[0]) - tv.x, __uint_as_float(rr[1]) - tv.y),
-                                             fmaxf(__uint_as_float(rr[2]) - tv.z, __uint_as_float(rr[3]) - tv.w)));
+                        mx = fmaxf(mx, fmaxf(fmaxf(__uint_as_float(r[4 * j]) - tv.x, __uint_as_float(r[4 * j + 1]) - tv.y),
+                                             fmaxf(__uint_as_float(r[4 * j + 2]) - tv.z,
+                                                   __uint_as_float(r[4 * j + 3]) - tv.w)));
                     }
                     if (row_ok && mx >= 0.0f) {
 #pragma unroll
-                        for (int j = 0; j < 64; ++j) {
-                            const float v = __uint_as_float(j < 32 ? r0[j] : r1[j - 32]);
+                        for (uint32_t j = 0; j < EPI_ROUND; ++j) {
+                            const float v = __uint_as_float(r[j]);
                             if (v >= my_thr[c + j]) {
-                                const uint32_t q = qbase + c + (uint32_t)j;
+                                const uint32_t q = qbase + c + j;
                                 const uint32_t slot = atomicAdd(p.cand_count + q, 1u);
                                 if (slot < p.cand_cap) {
                                     p.cand[(uint64_t)q * p.cand_cap + slot] = row;
@@ -299,9 +419,6 @@ __global__ void __launch_bounds__(THREADS, 1)
                     }
                 }
             }
-            fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(tempty + acc);
             if (++acc == ACC_STAGES) {
                 acc = 0;
                 acc_phase ^= 1u;
@@ -309,10 +426,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
     }
     fence_before();
-    __syncthreads();
+    cluster_sync_all(); // the pair's MMAs and remote arrivals are done
     fence_after();
     if (warp == 1)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS));
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS));
 }
 
 // ---------------------------------------------------------- selection
@@ -564,25 +681,28 @@ cudaError_t coarse_launch(const CUtensorMap& mv, const CUtensorMap& mq, const tc
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    const uint32_t tiles = p.row_tiles_iter * ((p.n_queries + tc::BN - 1) / tc::BN);
-    const uint32_t grid = std::min<uint32_t>(tiles, (uint32_t)num_sms);
+    if (p.k_dim > tc::MAX_K) return cudaErrorInvalidValue;
+    const uint64_t tiles = (uint64_t)p.row_tiles_iter * ((p.n_queries + tc::BN - 1) / tc::BN);
+    const uint32_t grid = 2u * (uint32_t)std::min<uint64_t>(tiles, (uint64_t)(num_sms / 2));
     tc::coarse_scores_kernel<PILOT><<<grid, tc::THREADS, tc::SMEM_BYTES, s>>>(mv, mq, p);
     return cudaGetLastError();
 }
 } // namespace
 
 uint32_t pilot_tiles(uint32_t n_rows) {
-    const uint32_t row_tiles = (n_rows + tc::BM - 1) / tc::BM;
+    const uint32_t row_tiles = (n_rows + 2 * tc::BM - 1) / (2 * tc::BM);
     return std::min<uint32_t>(row_tiles, kPilotTiles);
 }
+
+uint64_t pilot_cols(uint32_t n_rows) { return (uint64_t)pilot_tiles(n_rows) * 2 * tc::BM; }
 
 cudaError_t launch_coarse_pilot(const void* v_half, uint32_t n_rows, const void* q_half, uint32_t n_queries,
                                 uint32_t k_dim, void* scores, int num_sms, cudaStream_t s) {
     if (k_dim % tc::BK != 0) return cudaErrorInvalidValue;
     CUtensorMap mv, mq;
-    if (!make_map(&mv, v_half, n_rows, k_dim, tc::BM) || !make_map(&mq, q_half, n_queries, k_dim, tc::BN))
+    if (!make_map(&mv, v_half, n_rows, k_dim, tc::BM) || !make_map(&mq, q_half, n_queries, k_dim, tc::BN_HALF))
         return cudaErrorInvalidValue;
-    const uint32_t row_tiles = (n_rows + tc::BM - 1) / tc::BM;
+    const uint32_t row_tiles = (n_rows + 2 * tc::BM - 1) / (2 * tc::BM);
     tc::CoarseParams p{};
     p.n_rows = n_rows;
     p.n_queries = n_queries;
@@ -590,13 +710,13 @@ cudaError_t launch_coarse_pilot(const void* v_half, uint32_t n_rows, const void*
     p.row_tiles_iter = pilot_tiles(n_rows);
     p.rt_stride = row_tiles / p.row_tiles_iter;
     p.scores = static_cast<__half*>(scores);
-    p.ld = (uint64_t)p.row_tiles_iter * tc::BM;
+    p.ld = pilot_cols(n_rows);
     return coarse_launch<true>(mv, mq, p, num_sms, s);
 }
 
 cudaError_t launch_pilot_threshold(const void* scores, uint32_t n_rows, uint32_t nq, uint32_t k, float eps2,
                                    float* thr, cudaStream_t s) {
-    const uint64_t cols = (uint64_t)pilot_tiles(n_rows) * tc::BM;
+    const uint64_t cols = pilot_cols(n_rows);
     tc::pilot_threshold_kernel<<<nq, tc::SEL_THREADS, 0, s>>>(static_cast<const __half*>(scores), cols,
                                                               (uint32_t)cols, k, eps2, thr);
     return cudaGetLastError();
@@ -607,13 +727,13 @@ cudaError_t launch_coarse_candidates(const void* v_half, uint32_t n_rows, const 
                                      uint32_t cand_cap, uint32_t* cand_count, int num_sms, cudaStream_t s) {
     if (k_dim % tc::BK != 0) return cudaErrorInvalidValue;
     CUtensorMap mv, mq;
-    if (!make_map(&mv, v_half, n_rows, k_dim, tc::BM) || !make_map(&mq, q_half, n_queries, k_dim, tc::BN))
+    if (!make_map(&mv, v_half, n_rows, k_dim, tc::BM) || !make_map(&mq, q_half, n_queries, k_dim, tc::BN_HALF))
         return cudaErrorInvalidValue;
     tc::CoarseParams p{};
     p.n_rows = n_rows;
     p.n_queries = n_queries;
     p.k_dim = k_dim;
-    p.row_tiles_iter = (n_rows + tc::BM - 1) / tc::BM;
+    p.row_tiles_iter = (n_rows + 2 * tc::BM - 1) / (2 * tc::BM);
     p.rt_stride = 1;
     p.thr = thr;
     p.cand = cand;

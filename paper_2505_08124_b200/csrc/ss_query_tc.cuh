@@ -10,12 +10,13 @@ namespace ss {
 // rounding of the coarse score, and the exact scorer's own fp32 rounding.
 constexpr float kCoarseEps = 2.0e-3f;
 
-// Pilot: row tiles sampled with a uniform stride, at most this many (128 rows each).
-constexpr uint32_t kPilotTiles = 1024;
+// Pilot: row tiles sampled with a uniform stride, at most this many (256 rows each).
+constexpr uint32_t kPilotTiles = 512;
 
 cudaError_t launch_to_half(const float* in, uint64_t n, void* out, cudaStream_t s);
 uint32_t pilot_tiles(uint32_t n_rows);
-// fp16 coarse scores of the pilot sample, [nq][pilot_tiles(n_rows) * 128]
+uint64_t pilot_cols(uint32_t n_rows);
+// fp16 coarse scores of the pilot sample, [nq][pilot_cols(n_rows)]
 cudaError_t launch_coarse_pilot(const void* v_half, uint32_t n_rows, const void* q_half, uint32_t n_queries,
                                 uint32_t k_dim, void* scores, int num_sms, cudaStream_t s);
 // per-query candidate threshold from the pilot scores
