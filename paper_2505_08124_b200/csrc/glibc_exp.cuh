@@ -78,11 +78,18 @@ __device__ __constant__ static const unsigned long long kExpTab[256] = {
 };
 
 // tab: the 256-entry table staged in shared memory by the caller.
+// The polynomial/reduction constants live in the constant bank so DFMA takes
+// them as c[][] operands instead of re-materialising 64-bit literals in the
+// compositor's inner loop (non-const: the compiler may not fold them back).
+__device__ __constant__ double kExpConst[8] = {
+    0x1.71547652b82fep0 * 128, 0x1.8p52, -0x1.62e42fefa0000p-8, -0x1.cf79abc9e3b3ap-47,
+    0x1.ffffffffffdbdp-2,      0x1.555555555543cp-3, 0x1.55555cf172b91p-5, 0x1.1111167a4d017p-7};
+
 __device__ __forceinline__ double glibc_exp(double x, const unsigned long long* tab) {
-    const double InvLn2N = 0x1.71547652b82fep0 * 128, Shift = 0x1.8p52;
-    const double NegLn2hiN = -0x1.62e42fefa0000p-8, NegLn2loN = -0x1.cf79abc9e3b3ap-47;
-    const double C2 = 0x1.ffffffffffdbdp-2, C3 = 0x1.555555555543cp-3;
-    const double C4 = 0x1.55555cf172b91p-5, C5 = 0x1.1111167a4d017p-7;
+    const double InvLn2N = kExpConst[0], Shift = kExpConst[1];
+    const double NegLn2hiN = kExpConst[2], NegLn2loN = kExpConst[3];
+    const double C2 = kExpConst[4], C3 = kExpConst[5];
+    const double C4 = kExpConst[6], C5 = kExpConst[7];
     const unsigned long long ix = (unsigned long long)__double_as_longlong(x);
     const uint32_t abstop = (uint32_t)(ix >> 52) & 0x7ffu;
     if (abstop - 0x3c9u >= 0x3fu) {

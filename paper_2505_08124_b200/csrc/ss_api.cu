@@ -116,7 +116,7 @@ struct ProfState {
 struct Lane {
     cudaStream_t stream = nullptr;
     cudaEvent_t contract_done = nullptr, done = nullptr;
-    DevBuf rec, keys, k32, k32s, order, iota, offsets, tkeys, tkeys_sorted, tvals, tile_start, tile_end, list;
+    DevBuf rec, boxes, keys, k32, k32s, order, iota, offsets, tkeys, tkeys_sorted, tvals, tile_start, tile_end, list;
     uint64_t iota_n = 0;           // entries of the 0..n-1 sequence in `iota`
     uint64_t list_cap = 0;         // entries of `list`
     DevBuf cub_tmp, info;
@@ -126,7 +126,7 @@ struct Lane {
     ViewInfo* h_info = nullptr;    // pinned
     uint32_t* h_u32 = nullptr;     // pinned scratch
     void release_all() {
-        DevBuf* b[] = {&rec, &keys, &k32, &k32s, &order, &iota, &offsets, &tkeys, &tkeys_sorted, &tvals, &tile_start,
+        DevBuf* b[] = {&rec, &boxes, &keys, &k32, &k32s, &order, &iota, &offsets, &tkeys, &tkeys_sorted, &tvals, &tile_start,
                        &tile_end, &list, &cub_tmp, &info, &pix_bits, &mask_bits,
                        &runs, &run_offsets, &clip, &spans, &acc, &touched, &touched_list};
         for (auto* x : b) x->release();
@@ -264,6 +264,7 @@ Geometry run_geometry(ss_ctx* c, Lane& L, cudaStream_t s, const ss_camera& cam) 
     g.tiles = g.tiles_x * g.tiles_y;
 
     auto* rec = static_cast<SplatRec*>(L.rec.ensure(std::max<uint64_t>(N, 1) * sizeof(SplatRec)));
+    auto* boxes = static_cast<uint2*>(L.boxes.ensure(std::max<uint64_t>(N, 1) * sizeof(uint2)));
     auto* keys = static_cast<unsigned long long*>(L.keys.ensure(std::max<uint64_t>(N, 1) * 8));
     if (g.tiles > 50000u) throw Error(SS_ERR_CONTRACT, "raster resolution too large (more than 50000 16x16 tiles)");
     auto* tstart = static_cast<uint32_t*>(L.tile_start.ensure((g.tiles + 1ull) * 4));
@@ -286,6 +287,7 @@ Geometry run_geometry(ss_ctx* c, Lane& L, cudaStream_t s, const ss_camera& cam) 
         p.n = N;
         p.cam = cam;
         p.rec = rec;
+        p.boxes = boxes;
         p.keys = keys;
         p.tile_count = nullptr;
         p.tiles_x = g.tiles_x;
@@ -321,14 +323,14 @@ Geometry run_geometry(ss_ctx* c, Lane& L, cudaStream_t s, const ss_camera& cam) 
         Scope sc(c, s, SS_K_BIN);
         auto* offsets = static_cast<uint32_t*>(L.offsets.ensure((N + 1) * 4));
         size_t tb = 0;
-        SS_CUDA(launch_instance_offsets(rec, k32s, order, N, offsets, nullptr, &tb, s));
+        SS_CUDA(launch_instance_offsets(boxes, k32s, order, N, offsets, nullptr, &tb, s));
         void* tmp = L.cub_tmp.ensure(tb);
         tb = L.cub_tmp.bytes;
-        SS_CUDA(launch_instance_offsets(rec, k32s, order, N, offsets, tmp, &tb, s));
+        SS_CUDA(launch_instance_offsets(boxes, k32s, order, N, offsets, tmp, &tb, s));
         c->launches_cub += 1;
         c->prof.launches[SS_K_BIN] += 1;
         own_launch(c,
-                   launch_emit_instances(rec, k32s, order, N, offsets, g.tiles_x, L.list_cap, L.tkeys.p, g.k16,
+                   launch_emit_instances(boxes, k32s, order, N, offsets, g.tiles_x, L.list_cap, L.tkeys.p, g.k16,
                                          L.tvals.as<uint32_t>(), info, s),
                    SS_K_BIN, 2);
     }
@@ -373,6 +375,7 @@ RasterParams raster_params(ss_ctx* c, Lane& L, const ss_camera& cam, const Geome
     RasterParams p;
     std::memset(&p, 0, sizeof(p));
     p.rec = L.rec.as<SplatRec>();
+    p.boxes = L.boxes.as<uint2>();
     p.tile_list = L.list.as<uint32_t>();
     p.tile_start = L.tile_start.as<uint32_t>();
     p.tile_end = L.tile_end.as<uint32_t>();
@@ -743,6 +746,7 @@ int ss_project(ss_ctx* c, const ss_camera* cam, ss_projected* out) {
         p.n = N;
         p.cam = *cam;
         p.rec = static_cast<SplatRec*>(L.rec.ensure(N * sizeof(SplatRec)));
+        p.boxes = static_cast<uint2*>(L.boxes.ensure(N * sizeof(uint2)));
         p.keys = static_cast<unsigned long long*>(L.keys.ensure(N * 8));
         p.tile_count = nullptr;
         p.tiles_x = 0;

@@ -33,6 +33,9 @@ constexpr double kAlphaMax = 0.99;         // rasterizer.hpp:19
 constexpr double kAlphaSkip = 1.0 / 255.0; // rasterizer.hpp:21
 constexpr double kTransmittanceFloor = 1e-4; // rasterizer.hpp:23
 constexpr double kMahalanobisSqCutoff = 9.0; // rasterizer.hpp:26
+// kAlphaMax, kAlphaSkip, kWeightCutoff, kTransmittanceFloor for the compositor's
+// inner loop (non-const so they stay constant-bank operands)
+__device__ __constant__ double kCompositeConst[4] = {kAlphaMax, kAlphaSkip, kWeightCutoff, kTransmittanceFloor};
 
 // ---------------------------------------------------------------- project
 // One thread per Gaussian (id order).  scene.hpp:33-37 covariance3d +
@@ -160,6 +163,7 @@ __global__ void __launch_bounds__(256) project_kernel(ProjectParams p) {
                     r.y1 = (uint16_t)y1;
                     r.pad = 0;
                     p.rec[id] = r;
+                    p.boxes[id] = make_uint2((uint32_t)x0 | ((uint32_t)x1 << 16), (uint32_t)y0 | ((uint32_t)y1 << 16));
                     survive = true;
                     key = (unsigned long long)__double_as_longlong(z);
                 }
@@ -233,15 +237,17 @@ __device__ __forceinline__ bool composite_one(PixelState& ps, const SplatRec& s,
         return false;
     } else {
         const double og = dm(s.opacity, g);
-        // std::min(kAlphaMax, og) == (og < kAlphaMax ? og : kAlphaMax); og >= 0, and for
-        // NaN both forms give kAlphaMax, so one DMNMX suffices
-        const double alpha = fmin(og, kAlphaMax);
-        if (alpha < kAlphaSkip) return false;
+        // std::min(kAlphaMax, og) (rasterizer.hpp:124): (og < max) ? og : max, NaN -> max.
+        // The thresholds come from the constant bank (kCompositeConst) so the
+        // loop does not re-materialise 64-bit literals.
+        const double amax = kCompositeConst[0];
+        const double alpha = og < amax ? og : amax;
+        if (alpha < kCompositeConst[1]) return false;
         const double w = dm(alpha, ps.T);
-        const bool emit = w >= kWeightCutoff;
+        const bool emit = w >= kCompositeConst[2];
         if (emit) wf = __double2float_rn(w);
         ps.T = dm(ps.T, ds(1.0, alpha));
-        if (ps.T < kTransmittanceFloor) ps.done = true;
+        if (ps.T < kCompositeConst[3]) ps.done = true;
         return emit;
     }
 }
@@ -374,7 +380,7 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
     uint2 nbox = make_uint2(0u, 0u);
     if (start + lane < end) {
         nr = __ldg(p.tile_list + start + lane);
-        nbox = __ldg(reinterpret_cast<const uint2*>(&p.rec[nr].x0));
+        nbox = __ldg(p.boxes + nr);
     }
     const uint32_t lane_bit = 1u << lane;
     for (uint32_t base = start; base < end; base += 32u) {
@@ -385,7 +391,7 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
         const uint2 box = nbox;
         if (i + 32u < end) { // software prefetch of the next chunk
             nr = __ldg(p.tile_list + i + 32u);
-            nbox = __ldg(reinterpret_cast<const uint2*>(&p.rec[nr].x0));
+            nbox = __ldg(p.boxes + nr);
         }
         const uint32_t sx0 = box.x & 0xffffu, sx1 = box.x >> 16, sy0 = box.y & 0xffffu, sy1 = box.y >> 16;
         // pixels of the block inside the box that are still compositing

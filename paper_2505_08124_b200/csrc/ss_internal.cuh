@@ -46,6 +46,7 @@ struct ProjectParams {
     uint64_t n;
     ss_camera cam;
     SplatRec* rec;        // [n] by gid
+    uint2* boxes;         // [n] by gid: (x0 | x1 << 16, y0 | y1 << 16), L2-resident copy of the records' boxes
     unsigned long long* keys; // [n] depth bits (~0 when culled)
     uint32_t* tile_count; // [tiles] instances per tile (atomic), or null
     uint32_t tiles_x;
@@ -55,6 +56,7 @@ struct ProjectParams {
 
 struct RasterParams {
     const SplatRec* rec;        // by Gaussian id
+    const uint2* boxes;         // by Gaussian id (compact copy of rec[].x0..y1)
     const uint32_t* tile_list;  // per tile: Gaussian ids in (depth, id) order
     const uint32_t* tile_start; // tile t is tile_list[start[t], end[t])
     const uint32_t* tile_end;

@@ -137,14 +137,14 @@ __global__ void tie_fixup_kernel(const uint32_t* k32, uint64_t n, const unsigned
 
 // Tiles covered by the splat of depth rank r (0 for culled Gaussians).
 struct RankTiles {
-    const SplatRec* rec;
+    const uint2* boxes;
     const uint32_t* k32s;
     const uint32_t* order;
     uint64_t n;
     __host__ __device__ __forceinline__ uint32_t operator()(uint64_t r) const {
 #ifdef __CUDA_ARCH__
         if (r >= n || k32s[r] == 0xffffffffu) return 0u;
-        const uint2 box = __ldg(reinterpret_cast<const uint2*>(&rec[order[r]].x0));
+        const uint2 box = __ldg(boxes + order[r]);
         return ((box.x >> 16) / kTile - (box.x & 0xffffu) / kTile + 1u) *
                ((box.y >> 16) / kTile - (box.y & 0xffffu) / kTile + 1u);
 #else
@@ -157,7 +157,7 @@ struct RankTiles {
 // tile its box covers at offsets[r] (exclusive scan of RankTiles).  A stable
 // sort by tile then yields each tile's list in depth order.
 template <typename K>
-__global__ void emit_instances_kernel(const SplatRec* rec, const uint32_t* k32s, const uint32_t* order, uint64_t n,
+__global__ void emit_instances_kernel(const uint2* boxes, const uint32_t* k32s, const uint32_t* order, uint64_t n,
                                       const uint32_t* offsets, uint32_t tiles_x, uint64_t cap, K* keys, uint32_t* vals,
                                       ViewInfo* info) {
     const uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -168,7 +168,7 @@ __global__ void emit_instances_kernel(const SplatRec* rec, const uint32_t* k32s,
     }
     if (k32s[r] == 0xffffffffu) return;
     const uint32_t id = order[r];
-    const uint2 box = __ldg(reinterpret_cast<const uint2*>(&rec[id].x0));
+    const uint2 box = __ldg(boxes + id);
     uint32_t o = offsets[r];
     for (uint32_t ty = (box.y & 0xffffu) / kTile; ty <= (box.y >> 16) / kTile; ++ty)
         for (uint32_t tx = (box.x & 0xffffu) / kTile; tx <= (box.x >> 16) / kTile; ++tx) {
@@ -499,25 +499,25 @@ cudaError_t launch_tie_fixup(const uint32_t* k32s, uint64_t n, const unsigned lo
     return cudaGetLastError();
 }
 
-cudaError_t launch_instance_offsets(const SplatRec* rec, const uint32_t* k32s, const uint32_t* order, uint64_t n,
+cudaError_t launch_instance_offsets(const uint2* boxes, const uint32_t* k32s, const uint32_t* order, uint64_t n,
                                     uint32_t* offsets, void* tmp, size_t* tmp_bytes, cudaStream_t s) {
     cub::CountingInputIterator<uint64_t> ranks(0);
     cub::TransformInputIterator<uint32_t, RankTiles, cub::CountingInputIterator<uint64_t>> it(
-        ranks, RankTiles{rec, k32s, order, n});
+        ranks, RankTiles{boxes, k32s, order, n});
     return cub::DeviceScan::ExclusiveSum(tmp, *tmp_bytes, it, offsets, (int)(n + 1), s);
 }
 
-cudaError_t launch_emit_instances(const SplatRec* rec, const uint32_t* k32s, const uint32_t* order, uint64_t n,
+cudaError_t launch_emit_instances(const uint2* boxes, const uint32_t* k32s, const uint32_t* order, uint64_t n,
                                   const uint32_t* offsets, uint32_t tiles_x, uint64_t cap, void* keys, bool k16,
                                   uint32_t* vals, ViewInfo* info, cudaStream_t s) {
     if (!n) return cudaSuccess;
     const unsigned g = (unsigned)std::min<uint64_t>(blocks_for(cap, 256), 148u * 16u);
     if (k16) {
-        emit_instances_kernel<uint16_t><<<blocks_for(n, 256), 256, 0, s>>>(rec, k32s, order, n, offsets, tiles_x, cap,
+        emit_instances_kernel<uint16_t><<<blocks_for(n, 256), 256, 0, s>>>(boxes, k32s, order, n, offsets, tiles_x, cap,
                                                                             static_cast<uint16_t*>(keys), vals, info);
         pad_keys_kernel<uint16_t><<<g, 256, 0, s>>>(offsets, n, cap, static_cast<uint16_t*>(keys));
     } else {
-        emit_instances_kernel<uint32_t><<<blocks_for(n, 256), 256, 0, s>>>(rec, k32s, order, n, offsets, tiles_x, cap,
+        emit_instances_kernel<uint32_t><<<blocks_for(n, 256), 256, 0, s>>>(boxes, k32s, order, n, offsets, tiles_x, cap,
                                                                             static_cast<uint32_t*>(keys), vals, info);
         pad_keys_kernel<uint32_t><<<g, 256, 0, s>>>(offsets, n, cap, static_cast<uint32_t*>(keys));
     }
