@@ -38,6 +38,9 @@ PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
 FALLBACK_HBM = 6650.0
 
 
+DEFAULT_LANES = 4
+
+
 def peaks():
     try:
         p = json.loads(PEAKS_FILE.read_text())
@@ -59,6 +62,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-views", type=int, default=0)
     ap.add_argument("--no-query", action="store_true", help="skip the c5 vector-DB query leg")
+    ap.add_argument("--lanes", type=int, default=0, help="pipeline lanes (0 = library default)")
     ap.add_argument("--cpu-sample-queries", type=int, default=32)
     return ap.parse_args()
 
@@ -308,6 +312,8 @@ def main():
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
     ctx.set_scene(wl.scene.mean, wl.scene.scale, wl.scene.quat_xyzw, wl.scene.opacity)
+    lanes = args.lanes or DEFAULT_LANES
+    ctx.set_lanes(lanes)
 
     # device-resident inputs for `value`
     dev = torch.device("cuda", local)
@@ -405,7 +411,7 @@ def main():
     ms_prof = timed(step_device, 1)
     ctx.profile(False)
     prof = ctx.profile_read()
-    ctx.set_lanes(2)
+    ctx.set_lanes(lanes)
     hbm, peak_kind = peaks()
     kernels = {}
     for k, v in prof.items():

@@ -155,9 +155,10 @@ struct ss_ctx {
     ss::DevBuf mean_op, scale, quat;
 
     // per-view pipeline lanes (scratch + stream each)
-    ss::Lane lanes[2];
+    static constexpr uint32_t kMaxLanes = 4;
+    ss::Lane lanes[kMaxLanes];
     uint32_t next_lane = 0;
-    uint32_t n_lanes = 2;
+    uint32_t n_lanes = 4;
     cudaEvent_t ev_user = nullptr;
     ss::DevBuf cub_tmp, num_sel, info; // store / query scratch
     ss::DevBuf vstat; // per-view status of the last batch
@@ -543,10 +544,11 @@ void encode_batch(ss_ctx* c, uint32_t nviews, const ss_camera* cams, const ss_vi
                 }
             } join{c};
             for (uint32_t v : todo) {
-                const uint32_t li = c->n_lanes > 1 ? c->next_lane : 0u;
+                // view v runs on lane v mod n; its contraction follows the previous view's
+                const uint32_t li = c->next_lane % c->n_lanes;
                 Lane& L = c->lanes[li];
-                Lane& prev = c->lanes[li ^ 1u];
-                c->next_lane ^= 1u;
+                Lane& prev = c->lanes[(li + c->n_lanes - 1) % c->n_lanes];
+                c->next_lane = (li + 1) % c->n_lanes;
                 encode_one(c, L, prev, cams[v], masks ? &masks[v] : nullptr, mode, vstat + v);
             }
         }
@@ -682,7 +684,8 @@ int ss_set_option(ss_ctx* c, int option, int64_t value) {
     return guarded([&] {
         if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
         if (option == SS_OPT_LANES) {
-            if (value < 1 || value > 2) throw Error(SS_ERR_CONTRACT, "SS_OPT_LANES must be 1 or 2");
+            if (value < 1 || value > (int64_t)ss_ctx::kMaxLanes)
+                throw Error(SS_ERR_CONTRACT, "SS_OPT_LANES must be between 1 and 4");
             c->n_lanes = (uint32_t)value;
         } else if (option == SS_OPT_QUERY_PATH) {
             if (value < 0 || value > 2) throw Error(SS_ERR_CONTRACT, "SS_OPT_QUERY_PATH must be 0, 1 or 2");

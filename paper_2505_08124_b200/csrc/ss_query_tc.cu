@@ -205,9 +205,10 @@ struct CoarseParams {
 // Pair tile t (qt-major: t = qt * row_tiles_iter + it) covers store rows
 // [rt*2BM, rt*2BM + 2BM) with rt = it * rt_stride (CTA r of the pair owns
 // rows rt*2BM + r*BM + [0, BM)) and queries [qt*BN, qt*BN + BN) (CTA r keeps
-// queries qt*BN + r*BN_HALF + [0, BN_HALF) resident).  Pair c of G runs the
-// contiguous tile range [c*T/G, (c+1)*T/G), so it changes query block (and
-// reloads B) at most a few times.  TMEM of CTA r holds its BM rows x BN
+// queries qt*BN + r*BN_HALF + [0, BN_HALF) resident).  With at most as many
+// query tiles as pairs, each pair owns one query tile and a contiguous range
+// of row tiles shared with the other query tiles' pairs; otherwise pair c of G
+// runs the contiguous tile range [c*T/G, (c+1)*T/G).  TMEM of CTA r holds its BM rows x BN
 // queries of the accumulator.
 template <bool PILOT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
@@ -231,9 +232,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const uint32_t rank = cluster_rank();
     const uint32_t pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
     const uint32_t q_tiles = (p.n_queries + BN - 1) / BN;
-    const uint64_t n_tiles = (uint64_t)p.row_tiles_iter * q_tiles;
-    const uint32_t t_begin = (uint32_t)(n_tiles * pair / n_pairs);
-    const uint32_t t_end = (uint32_t)(n_tiles * (pair + 1) / n_pairs);
+    uint32_t t_begin, t_end;
+    if (q_tiles <= n_pairs) {
+        // pair -> (query tile, row group): the q_tiles pairs of a group walk the
+        // same store rows side by side, so each store tile comes from HBM once
+        // and from L2 for the other query tiles
+        const uint32_t groups = n_pairs / q_tiles, qt = pair % q_tiles, grp = pair / q_tiles;
+        const uint32_t rt_lo = grp < groups ? (uint32_t)((uint64_t)p.row_tiles_iter * grp / groups) : 0u;
+        const uint32_t rt_hi = grp < groups ? (uint32_t)((uint64_t)p.row_tiles_iter * (grp + 1) / groups) : 0u;
+        t_begin = qt * p.row_tiles_iter + rt_lo;
+        t_end = qt * p.row_tiles_iter + rt_hi;
+    } else {
+        const uint64_t n_tiles = (uint64_t)p.row_tiles_iter * q_tiles;
+        t_begin = (uint32_t)(n_tiles * pair / n_pairs);
+        t_end = (uint32_t)(n_tiles * (pair + 1) / n_pairs);
+    }
     const uint32_t k_blocks = p.k_dim / BK;
 
     if (warp == 0 && lane == 0) {
