@@ -41,6 +41,15 @@ FALLBACK_HBM = 6650.0
 DEFAULT_LANES = 4
 
 
+def ncu_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture, or None."""
+    try:
+        t = json.loads((Path(__file__).resolve().parent / "profiles" / "ncu_traffic.json").read_text())
+        return t[kernel]["bytes_per_launch"]
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         p = json.loads(PEAKS_FILE.read_text())
@@ -223,7 +232,7 @@ def query_leg(ctx, args, dev, stream, want_cpu):
                     "other_ms": tot["ms"] - gemm["ms"] - sel["ms"]},
         "roofline": {"bound": "tensor", "kernel": "coarse_scores_kernel (tcgen05 kind::f16)", "achieved": achieved,
                      "peak": tpeak, "unit": "TFLOP/s", "frac": achieved / tpeak if achieved else None,
-                     "traffic": None, "peak_source": src, "flops_per_launch": gemm["bytes"]},
+                     "traffic": ncu_traffic("query_gemm"), "peak_source": src, "flops_per_launch": gemm["bytes"]},
         "data": "synthetic: N(0,1) rows and queries (seeded), normalised by store_build / prepare_query",
     }
     if want_cpu:
@@ -422,7 +431,8 @@ def main():
     dom = max((k for k in kernels if k not in ("h2d",)), key=lambda k: kernels[k]["ms_per_step"])
     dk = kernels[dom]
     roofline = {"bound": "hbm", "kernel": dom, "achieved": dk["achieved_gbs"], "peak": hbm, "unit": "GB/s",
-                "frac": dk["achieved_gbs"] / hbm, "traffic": None, "peak_source": f"{peak_kind} (MEASURED_PEAKS.json)",
+                "frac": dk["achieved_gbs"] / hbm, "traffic": ncu_traffic(dom),
+                "algorithmic_bytes_per_launch": dk["gb_per_step"] * 1e9 / max(dk["launches_per_step"], 1), "peak_source": f"{peak_kind} (MEASURED_PEAKS.json)",
                 "share_of_step": dk["share_of_serial_step"],
                 "timing": "CUDA events around each launch on its stream, one extra pass with lanes serialised"}
     steps = 1
