@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -195,11 +196,13 @@ def query_leg(ctx, args, dev, stream, want_cpu):
     import torch
     from paper_2505_08124_b200.workload import QUERY_CONFIG as QC
     n, nq, d, k = QC["n_rows"], QC["n_queries"], QC["dim"], QC["k"]
-    g = torch.Generator(device=dev).manual_seed(args.seed)
-    raw = torch.randn((n, d), generator=g, device=dev).cpu().numpy()
-    queries = torch.randn((nq, d), generator=g, device=dev).cpu()
+    from paper_2505_08124_b200.workload import query_workload
+    t_gen = time.perf_counter()
+    raw, qraw = query_workload(args.seed, n, nq, d)  # cmd_bench's store + queries (main.cpp:440-450)
+    gen_s = time.perf_counter() - t_gen
+    queries = torch.from_numpy(qraw.copy())
     q_pinned = queries.pin_memory().numpy()
-    cnt = ctx.store_build(raw, np.ones(n, np.float32))
+    cnt = ctx.store_build(raw, np.ones(n, np.float32))  # normalized_copy per row on the device
     del raw
     ctx.query_topk(q_pinned[:8], k)  # warm: fp16 copy of the store, kernel attributes
     for _ in range(args.warmup):
@@ -223,8 +226,28 @@ def query_leg(ctx, args, dev, stream, want_cpu):
     except Exception:
         tpeak, src = 2250.0, "nominal dense fp16 (fallback)"
     achieved = gemm["bytes"] / (gemm["ms"] / 1e3) / 1e12 if gemm["ms"] > 0 else None
+    # threshold mode of cmd_bench: tau so that a random query returns about k rows
+    frac = min(0.5, k / float(cnt))
+    z = 1.0
+    for _ in range(40):
+        z -= (math.erfc(z) - 2.0 * frac) / (-2.0 / math.sqrt(math.pi) * math.exp(-z * z))
+    tau = float(np.float32(math.sqrt(2.0) * z / math.sqrt(float(d))))
+    n_thr = min(nq, 64)
+    ctx.query_threshold(q_pinned[0], tau)
+    t0 = time.perf_counter()
+    returned = 0
+    thr_results = []
+    for i in range(n_thr):
+        ti, ts = ctx.query_threshold(q_pinned[i], tau)
+        returned += len(ti)
+        thr_results.append((ti, ts))
+    thr_ms = 1e3 * (time.perf_counter() - t0) / n_thr
     out = {
-        "workload": f"{QC['name']}: {nq} queries x {cnt} unit rows x {d}, top-{k}",
+        "workload": f"{QC['name']}: {nq} queries x {cnt} unit rows x {d}, top-{k} "
+                    f"(cmd_bench generator, seed {args.seed} ^ 0xbe9c)",
+        "dataset_gen_seconds": gen_s,
+        "threshold": {"tau": tau, "ms_per_query_e2e": thr_ms, "queries": n_thr,
+                      "avg_returned": returned / n_thr},
         "metric": "queries_per_sec", "unit": "queries/s", "value_e2e": nq / (ms / 1e3), "ms_per_batch_e2e": ms,
         "ms_device_query": tot["ms"], "value_device": nq / (tot["ms"] / 1e3) if tot["ms"] > 0 else None,
         "h2d_bytes_per_batch": int(nq * d * 4), "d2h_bytes_per_batch": int(nq * k * 8),
@@ -233,7 +256,8 @@ def query_leg(ctx, args, dev, stream, want_cpu):
         "roofline": {"bound": "tensor", "kernel": "coarse_scores_kernel (tcgen05 kind::f16)", "achieved": achieved,
                      "peak": tpeak, "unit": "TFLOP/s", "frac": achieved / tpeak if achieved else None,
                      "traffic": ncu_traffic("query_gemm"), "peak_source": src, "flops_per_launch": gemm["bytes"]},
-        "data": "synthetic: N(0,1) rows and queries (seeded), normalised by store_build / prepare_query",
+        "data": "synthetic: U(-0.5,0.5)^512 rows and queries from std::mt19937_64 as in cmd_bench, normalised "
+                "by store_build / prepare_query",
     }
     if want_cpu:
         try:
@@ -251,6 +275,18 @@ def query_leg(ctx, args, dev, stream, want_cpu):
             t0 = time.perf_counter()
             ri, rs, _ = R.query_topk(store_ids, store_rows, qs, k, threads=cores)
             dt = time.perf_counter() - t0
+            # threshold mode on the reference (single-threaded, as the reference API is)
+            nt = min(4, n_thr)
+            t1 = time.perf_counter()
+            thr_ok = True
+            for i in range(nt):
+                rti, rts = R.query_threshold(store_ids, store_rows, qs[i] if i < ns else queries[i].numpy(), tau)
+                gi, gs = thr_results[i]
+                thr_ok = thr_ok and np.array_equal(rti, gi) and rts.tobytes() == gs.tobytes()
+            out["threshold"]["cpu_baseline"] = {"value": 1e3 * (time.perf_counter() - t1) / nt,
+                                                "unit": "ms/query", "cores": 1, "kind": kind,
+                                                "sample": f"{nt} threshold queries over the full store"}
+            out["threshold"]["parity_sample"] = bool(thr_ok)
             out["cpu_baseline"] = {"value": ns / dt, "unit": "queries/s", "cores": cores, "kind": kind,
                                    "sample": f"{ns} of the {nq} queries over the full store, threads={cores}",
                                    "seconds": dt}

@@ -207,6 +207,9 @@ int ss_synth_embedding(const char* label, uint32_t dim, float* out);
 /* Random-rectangle masks for one view (main.cpp:386-396) from the rng state
  * seeded by seed; writes RLE runs (capacity >= n_masks*(2*height+2)) and
  * run_offsets (n_masks+1). */
+/* main.cpp:440-450: the bench query store/queries, U(-0.5, 0.5) per element
+ * from std::mt19937_64(seed) (cmd_bench seeds it with seed ^ 0xbe9c). */
+int ss_synth_uniform(uint64_t seed, uint64_t count, float* out);
 int ss_synth_rect_masks(uint64_t seed, uint32_t width, uint32_t height, uint32_t n_masks, uint32_t* runs,
                         uint64_t* run_offsets);
 

@@ -112,6 +112,9 @@ class Oracle:
         L.sso_dot_lanes.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64]
         L.sso_normalized_copy.restype = C.c_int
         L.sso_normalized_copy.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p]
+        L.sso_query_threshold.restype = C.c_int
+        L.sso_query_threshold.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p, C.c_float,
+                                          C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]
         L.sso_query_topk.restype = C.c_int
         L.sso_query_topk.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p, C.c_uint32,
                                      C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p]
@@ -254,6 +257,22 @@ class Oracle:
         if st == 3:
             raise OracleNumericError("cannot normalize a zero vector")
         return oid, osim, cnt
+
+
+    def query_threshold(self, ids, rows, q, tau):
+        ids = np.ascontiguousarray(ids, np.uint32)
+        rows = np.ascontiguousarray(rows, np.float32)
+        q = np.ascontiguousarray(q, np.float32)
+        oid = np.zeros(max(ids.shape[0], 1), np.uint32)
+        osim = np.zeros(max(ids.shape[0], 1), np.float32)
+        cnt = C.c_uint64()
+        st = self.L.sso_query_threshold(_p(ids), _p(rows), ids.shape[0], rows.shape[1], _p(q), C.c_float(tau),
+                                        _p(oid), _p(osim), oid.shape[0], C.byref(cnt))
+        if st == 3:
+            raise OracleNumericError("cannot normalize a zero vector")
+        if st == 1:
+            raise ValueError("cosine threshold must lie in [-1, 1]")
+        return oid[:cnt.value].copy(), osim[:cnt.value].copy()
 
 
 class RefError(Exception):

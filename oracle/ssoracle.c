@@ -706,3 +706,42 @@ int sso_query_topk(const uint32_t* ids, const float* rows, uint64_t count, uint3
     free(th);
     return st;
 }
+
+static int cmp_scored(const void* a, const void* b) {
+    const scored_t x = *(const scored_t*)a, y = *(const scored_t*)b;
+    if (before(x, y)) return -1;
+    if (before(y, x)) return 1;
+    return 0;
+}
+
+/* vecstore.hpp:135-146 query_threshold: tau in [-1, 1] (ContractError = 1
+ * otherwise), q normalised (NumericError = 3 on zero norm), every record with
+ * sim >= tau, ordered by scored_before.  Writes min(n, capacity) records and
+ * returns n in *out_count. */
+int sso_query_threshold(const uint32_t* ids, const float* rows, uint64_t count, uint32_t dim, const float* query,
+                        float tau, uint32_t* out_ids, float* out_sims, uint64_t capacity, uint64_t* out_count) {
+    *out_count = 0;
+    if (!(tau >= -1.0f && tau <= 1.0f)) return 1;
+    if (count == 0) return 0; /* before prepare_query, as the reference */
+    float* qn = (float*)malloc((dim ? dim : 1) * sizeof(float));
+    if (sso_normalized_copy(query, dim, qn)) {
+        free(qn);
+        return 3;
+    }
+    scored_t* all = (scored_t*)malloc((count ? count : 1) * sizeof(scored_t));
+    uint64_t n = 0;
+    for (uint64_t i = 0; i < count; ++i) {
+        const float sim = sso_dot_lanes(rows + i * dim, qn, dim);
+        if (sim >= tau) all[n++] = (scored_t){ids[i], sim};
+    }
+    qsort(all, n, sizeof(scored_t), cmp_scored);
+    for (uint64_t i = 0; i < n && i < capacity; ++i) {
+        out_ids[i] = all[i].id;
+        out_sims[i] = all[i].sim;
+    }
+    *out_count = n;
+    free(all);
+    free(qn);
+    return 0;
+}
+

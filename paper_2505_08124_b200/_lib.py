@@ -94,6 +94,7 @@ def lib() -> C.CDLL:
         "ss_synth_look_at": (i32, [pd, pd, u32, u32, C.c_double, C.POINTER(Camera)]),
         "ss_synth_embedding": (i32, [C.c_char_p, u32, pf]),
         "ss_synth_rect_masks": (i32, [u64, u32, u32, u32, pu32, pu64]),
+        "ss_synth_uniform": (i32, [u64, u64, pf]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -1121,6 +1121,73 @@ bool topk_tensor(ss_ctx* c, const float* d_qn, uint32_t nq, uint32_t k, uint32_t
 }
 } // namespace
 
+namespace {
+bool tc_eligible(const ss_ctx* c) {
+    return c->store_dim % 64 == 0 && c->store_dim <= 512 && c->store_count < (1ull << 31) &&
+           (c->query_path == 2 || (c->query_path == 0 && c->store_count >= 16384));
+}
+
+// query_threshold on the tensor cores: candidates with coarse >= tau - eps
+// (a superset of {exact >= tau}), exact rescoring, (sim desc, id asc) order.
+// False when the candidates overflow; the caller then runs the exact scan.
+bool threshold_tensor(ss_ctx* c, const float* d_qn, float tau, uint32_t* out_ids, float* out_sims, uint64_t capacity,
+                      uint64_t* out_count) {
+    cudaStream_t s = c->stream;
+    const uint64_t count = c->store_count;
+    const uint32_t dim = c->store_dim;
+    if (!c->num_sms) SS_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
+    if (!c->store_half_ok) {
+        void* h = c->store_half.ensure(count * dim * 2);
+        own_launch(c, ss::launch_to_half(c->store_rows.as<float>(), count * dim, h, s), SS_K_QUERY);
+        c->store_half_ok = true;
+    }
+    void* qh = c->qhalf.ensure((uint64_t)dim * 2);
+    own_launch(c, ss::launch_to_half(d_qn, dim, qh, s), SS_K_QUERY);
+    auto* thr = static_cast<float*>(c->tc_thr.ensure(64));
+    auto* cand = static_cast<uint32_t*>(c->cand.ensure((uint64_t)kCandCap * 4));
+    auto* cval = static_cast<float*>(c->cand_sim.ensure((uint64_t)kCandCap * 4));
+    auto* ccount = static_cast<uint32_t*>(c->cand_count.ensure(64));
+    auto* oid = static_cast<uint32_t*>(c->topk_ids.ensure((uint64_t)kCandCap * 4));
+    auto* osim = static_cast<float*>(c->topk_sims.ensure((uint64_t)kCandCap * 4));
+    c->h_u32[0] = 0;
+    float h_thr = tau - ss::kCoarseEps;
+    SS_CUDA(cudaMemcpyAsync(thr, &h_thr, 4, cudaMemcpyHostToDevice, s));
+    SS_CUDA(cudaMemsetAsync(ccount, 0, 8, s));
+    {
+        Scope sg(c, s, SS_K_QUERY_GEMM);
+        own_launch(c,
+                   ss::launch_coarse_candidates(c->store_half.p, (uint32_t)count, qh, 1, dim, thr, cand, cval,
+                                                kCandCap, ccount, c->num_sms, s),
+                   SS_K_QUERY);
+    }
+    {
+        Scope sr(c, s, SS_K_QUERY_SELECT);
+        own_launch(c,
+                   ss::launch_threshold_rescore(c->store_rows.as<float>(), c->store_ids.as<uint32_t>(), dim, d_qn,
+                                                cand, kCandCap, ccount, tau, oid, osim, kCandCap, ccount + 1, s),
+                   SS_K_QUERY);
+    }
+    uint32_t hc[2];
+    SS_CUDA(cudaMemcpyAsync(hc, ccount, 8, cudaMemcpyDeviceToHost, s));
+    SS_CUDA(cudaStreamSynchronize(s));
+    if (hc[0] > kCandCap) {
+        c->qstat[3] += 1;
+        return false;
+    }
+    const uint64_t m = hc[1], out = std::min<uint64_t>(m, capacity);
+    if (out) {
+        SS_CUDA(cudaMemcpyAsync(out_ids, oid, out * 4, cudaMemcpyDeviceToHost, s));
+        SS_CUDA(cudaMemcpyAsync(out_sims, osim, out * 4, cudaMemcpyDeviceToHost, s));
+        SS_CUDA(cudaStreamSynchronize(s));
+    }
+    c->qstat[0] += 1;
+    c->qstat[1] += hc[0];
+    c->qstat[2] = std::max<uint64_t>(c->qstat[2], hc[0]);
+    *out_count = m;
+    return true;
+}
+} // namespace
+
 int ss_query_topk(ss_ctx* c, const float* queries, uint32_t nq, uint32_t k, uint32_t* out_ids, float* out_sims,
                   uint64_t* out_counts) {
     return guarded([&] {
@@ -1136,9 +1203,7 @@ int ss_query_topk(ss_ctx* c, const float* queries, uint32_t nq, uint32_t k, uint
         const float* d_qn = prepare_queries(c, queries, nq);
         auto* oid = static_cast<uint32_t*>(c->topk_ids.ensure((size_t)nq * k * 4));
         auto* osim = static_cast<float*>(c->topk_sims.ensure((size_t)nq * k * 4));
-        const bool tc_ok = c->store_dim % 64 == 0 && c->store_dim <= 512 && count < (1ull << 31) &&
-                           (c->query_path == 2 || (c->query_path == 0 && count >= 16384));
-        if (!(tc_ok && topk_tensor(c, d_qn, nq, k, oid, osim))) topk_exact(c, d_qn, nq, k, oid, osim);
+        if (!(tc_eligible(c) && topk_tensor(c, d_qn, nq, k, oid, osim))) topk_exact(c, d_qn, nq, k, oid, osim);
         // rows written are [q][k] with k stride; take <= k
         std::vector<uint32_t> hid((size_t)nq * k);
         std::vector<float> hsim((size_t)nq * k);
@@ -1162,6 +1227,7 @@ int ss_query_threshold(ss_ctx* c, const float* query, float tau, uint32_t* out_i
         if (count == 0) return;
         cudaStream_t s = c->stream;
         const float* d_qn = prepare_queries(c, query, 1);
+        if (tc_eligible(c) && threshold_tensor(c, d_qn, tau, out_ids, out_sims, capacity, out_count)) return;
         auto* sc_buf = static_cast<float*>(c->scores.ensure(count * 4));
         own_launch(c, launch_score(c->store_rows.as<float>(), count, c->store_dim, d_qn, 1, 0, sc_buf, s), SS_K_QUERY);
         auto* keys = static_cast<unsigned long long*>(c->thr_keys.ensure(count * 8));

@@ -513,6 +513,41 @@ __device__ __forceinline__ bool scored_before(float sa, uint32_t ia, float sb, u
     return ia < ib;
 }
 
+// dot_lanes (vecstore.hpp:21-31) of store row `row` with the query held in
+// shared memory, by a pair of threads (h = threadIdx.x & 1): thread h owns
+// accumulators 4h..4h+3 and streams the row as float4 at 8i + 4h, 16 loads in
+// flight; the pair combines ((l0+l1)+(l2+l3)) + ((l4+l5)+(l6+l7)), then adds
+// the tail -- the literal 0.0f here, dim % 8 == 0.  Both threads return the sum.
+__device__ __forceinline__ float pair_dot_lanes(const float* rows, uint32_t row, uint32_t dim, const float4* qs4,
+                                                bool live) {
+    const uint32_t h = threadIdx.x & 1u;
+    const float4* a4 = reinterpret_cast<const float4*>(rows + (uint64_t)row * dim) + h;
+    float l0 = 0.0f, l1 = 0.0f, l2 = 0.0f, l3 = 0.0f;
+    if (live) {
+        const uint32_t steps = dim / 8;
+        for (uint32_t i0 = 0; i0 < steps; i0 += 16) {
+            float4 av[16];
+#pragma unroll
+            for (uint32_t u = 0; u < 16; ++u)
+                if (i0 + u < steps) av[u] = __ldg(a4 + 2 * (i0 + u));
+#pragma unroll
+            for (uint32_t u = 0; u < 16; ++u) {
+                if (i0 + u < steps) {
+                    const float4 bv = qs4[2 * (i0 + u) + h];
+                    l0 = __fadd_rn(l0, __fmul_rn(av[u].x, bv.x));
+                    l1 = __fadd_rn(l1, __fmul_rn(av[u].y, bv.y));
+                    l2 = __fadd_rn(l2, __fmul_rn(av[u].z, bv.z));
+                    l3 = __fadd_rn(l3, __fmul_rn(av[u].w, bv.w));
+                }
+            }
+        }
+    }
+    const float half_sum = __fadd_rn(__fadd_rn(l0, l1), __fadd_rn(l2, l3)); // (s01+s23) or (s45+s67)
+    const float other = __shfl_xor_sync(0xffffffffu, half_sum, 1);
+    const float lo = h ? other : half_sum, hi = h ? half_sum : other;
+    return __fadd_rn(__fadd_rn(lo, hi), 0.0f);
+}
+
 // One CTA per query.
 //  1. c_k = the k-th largest fp32 coarse score among the candidates.  Every
 //     row with coarse >= thr is a candidate and c_k >= thr, so this is the
@@ -579,32 +614,8 @@ __global__ void __launch_bounds__(RS_THREADS) rescore_kernel(const float* rows, 
         const uint32_t ci = base + (threadIdx.x >> 1);
         const bool live = ci < nc && sval[ci] >= lim;
         const uint32_t row = live ? srow[ci] : 0u;
-        const float4* a4 = reinterpret_cast<const float4*>(rows + (uint64_t)row * dim) + (threadIdx.x & 1u);
-        float l0 = 0.0f, l1 = 0.0f, l2 = 0.0f, l3 = 0.0f;
-        if (live) {
-            const uint32_t h = threadIdx.x & 1u;
-            const uint32_t steps = dim / 8;
-            for (uint32_t i0 = 0; i0 < steps; i0 += 16) {
-                float4 av[16];
-#pragma unroll
-                for (uint32_t u = 0; u < 16; ++u)
-                    if (i0 + u < steps) av[u] = __ldg(a4 + 2 * (i0 + u));
-#pragma unroll
-                for (uint32_t u = 0; u < 16; ++u) {
-                    if (i0 + u < steps) {
-                        const float4 bv = qs4[2 * (i0 + u) + h];
-                        l0 = __fadd_rn(l0, __fmul_rn(av[u].x, bv.x));
-                        l1 = __fadd_rn(l1, __fmul_rn(av[u].y, bv.y));
-                        l2 = __fadd_rn(l2, __fmul_rn(av[u].z, bv.z));
-                        l3 = __fadd_rn(l3, __fmul_rn(av[u].w, bv.w));
-                    }
-                }
-            }
-        }
-        const float half_sum = __fadd_rn(__fadd_rn(l0, l1), __fadd_rn(l2, l3)); // (s01+s23) or (s45+s67)
-        const float other = __shfl_xor_sync(0xffffffffu, half_sum, 1);
+        const float sim = pair_dot_lanes(rows, row, dim, qs4, live);
         if (live && (threadIdx.x & 1u) == 0) {
-            const float sim = __fadd_rn(__fadd_rn(half_sum, other), 0.0f);
             const uint32_t slot = atomicAdd(&s_n, 1u);
             if (slot < RS_THREADS / 2) {
                 fsim[slot] = isnan(sim) ? -INFINITY : sim;
@@ -637,6 +648,58 @@ __global__ void __launch_bounds__(RS_THREADS) rescore_kernel(const float* rows, 
             out_sims[(uint64_t)q * k + rank] = sc;
         }
     }
+}
+
+// query_threshold (vecstore.hpp:135-146) for one query: every candidate of
+// the coarse pass with thr = tau - eps (a superset of {exact >= tau}) is
+// rescored with the exact dot_lanes; those with sim >= tau are ranked by
+// (sim desc, id asc) in shared memory.  out_count gets the full count; at
+// most out_cap records are written.
+__global__ void __launch_bounds__(RS_THREADS) threshold_rescore_kernel(const float* rows, const uint32_t* ids,
+                                                                       uint32_t dim, const float* qn,
+                                                                       const uint32_t* cand, uint32_t cand_cap,
+                                                                       const uint32_t* cand_count, float tau,
+                                                                       uint32_t* out_ids, float* out_sims,
+                                                                       uint64_t out_cap, uint32_t* out_count) {
+    extern __shared__ float4 smem4[];
+    float4* qs4 = smem4;                                          // dim / 4
+    float* ksim = reinterpret_cast<float*>(smem4 + dim / 4);      // cand_cap
+    uint32_t* kid = reinterpret_cast<uint32_t*>(ksim + cand_cap); // cand_cap
+    __shared__ uint32_t s_n;
+    const uint32_t nc = cand_count[0];
+    if (nc > cand_cap) return; // overflow: the host answers with the exact scan
+    const float4* qv = reinterpret_cast<const float4*>(qn);
+    for (uint32_t i = threadIdx.x; i < dim / 4; i += blockDim.x) qs4[i] = qv[i];
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    for (uint32_t base = 0; base < nc; base += RS_THREADS / 2) {
+        const uint32_t ci = base + (threadIdx.x >> 1);
+        const bool live = ci < nc;
+        const uint32_t row = live ? __ldg(cand + ci) : 0u;
+        const float sim = pair_dot_lanes(rows, row, dim, qs4, live);
+        if (live && (threadIdx.x & 1u) == 0 && sim >= tau) {
+            const uint32_t slot = atomicAdd(&s_n, 1u);
+            ksim[slot] = sim;
+            kid[slot] = __ldg(ids + row);
+        }
+    }
+    __syncthreads();
+    const uint32_t n = s_n;
+    for (uint32_t c = threadIdx.x; c < n; c += blockDim.x) {
+        const float sc = ksim[c];
+        const uint32_t ic = kid[c];
+        uint32_t rank = 0;
+        for (uint32_t o = 0; o < n; ++o) {
+            const float so = ksim[o];
+            const uint32_t io = kid[o];
+            rank += (so > sc || (so == sc && (io < ic || (io == ic && o < c)))) ? 1u : 0u;
+        }
+        if (rank < out_cap) {
+            out_ids[rank] = ic;
+            out_sims[rank] = sc;
+        }
+    }
+    if (threadIdx.x == 0) *out_count = n;
 }
 
 __global__ void to_half_kernel(const float* in, uint64_t n, __half* out) {
@@ -769,6 +832,24 @@ cudaError_t launch_rescore(const float* rows, const uint32_t* ids, uint32_t dim,
     }
     tc::rescore_kernel<<<nq, tc::RS_THREADS, smem, s>>>(rows, ids, dim, qn, cand, cand_val, cand_cap, cand_count, k,
                                                         eps2, out_ids, out_sims);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_threshold_rescore(const float* rows, const uint32_t* ids, uint32_t dim, const float* qn,
+                                     const uint32_t* cand, uint32_t cand_cap, const uint32_t* cand_count, float tau,
+                                     uint32_t* out_ids, float* out_sims, uint64_t out_cap, uint32_t* out_count,
+                                     cudaStream_t s) {
+    if (dim % 8 != 0) return cudaErrorInvalidValue;
+    const size_t smem = (size_t)dim * 4 + (size_t)cand_cap * 8;
+    static size_t configured = 0;
+    if (smem > configured) {
+        cudaError_t e = cudaFuncSetAttribute(tc::threshold_rescore_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        configured = smem;
+    }
+    tc::threshold_rescore_kernel<<<1, tc::RS_THREADS, smem, s>>>(rows, ids, dim, qn, cand, cand_cap, cand_count, tau,
+                                                                 out_ids, out_sims, out_cap, out_count);
     return cudaGetLastError();
 }
 

@@ -31,5 +31,10 @@ cudaError_t launch_coarse_candidates(const void* v_half, uint32_t n_rows, const 
 cudaError_t launch_rescore(const float* rows, const uint32_t* ids, uint32_t dim, const float* qn, uint32_t nq,
                            const uint32_t* cand, const float* cand_val, uint32_t cand_cap, uint32_t* cand_count,
                            uint32_t k, float eps2, uint32_t* out_ids, float* out_sims, cudaStream_t s);
+// query_threshold: exact rescoring of the tau - eps candidates of one query
+cudaError_t launch_threshold_rescore(const float* rows, const uint32_t* ids, uint32_t dim, const float* qn,
+                                     const uint32_t* cand, uint32_t cand_cap, const uint32_t* cand_count, float tau,
+                                     uint32_t* out_ids, float* out_sims, uint64_t out_cap, uint32_t* out_count,
+                                     cudaStream_t s);
 
 } // namespace ss

@@ -172,4 +172,14 @@ int ss_synth_rect_masks(uint64_t seed, uint32_t width, uint32_t height, uint32_t
     return 0;
 }
 
+// main.cpp:440-450 (cmd_bench query store): x = f32((rng() >> 11) + 0.5) * 2^-53 - 0.5)
+// for every element, store rows first, then the query vectors, from
+// std::mt19937_64(seed) -- the caller passes cfg.seed ^ 0xbe9c.
+int ss_synth_uniform(uint64_t seed, uint64_t count, float* out) {
+    std::mt19937_64 rng(seed);
+    for (uint64_t i = 0; i < count; ++i)
+        out[i] = static_cast<float>((static_cast<double>(rng() >> 11) + 0.5) * 0x1.0p-53 - 0.5);
+    return 0;
+}
+
 } // extern "C"

@@ -51,6 +51,29 @@ def test_synth_embedding_matches_reference_golden():
         assert synth_embedding(str(label), 512).tobytes() == vec.tobytes()
 
 
+def test_mt19937_64_known_answer():
+    """std::mt19937_64 default seed: the 10000th output is 9981545732273789042
+    (C++11 [rand.predef]); the first is 14514284786278117030."""
+    from tests.util import MT19937_64
+    m = MT19937_64(5489)
+    assert m() == 14514284786278117030
+    for _ in range(9998):
+        m()
+    assert m() == 9981545732273789042
+
+
+def test_query_store_generator_matches_cmd_bench():
+    """main.cpp:440-450: store rows then queries, f32((rng()>>11)+0.5)*2^-53-0.5,
+    from std::mt19937_64(seed ^ 0xbe9c)."""
+    from paper_2505_08124_b200.workload import query_workload
+    from tests.util import MT19937_64
+    rows, queries = query_workload(2505, 5, 3, 16)
+    m = MT19937_64(2505 ^ 0xBE9C)
+    exp = np.array([np.float32(((m() >> 11) + 0.5) * 2.0 ** -53 - 0.5) for _ in range(8 * 16)], np.float32)
+    assert rows.shape == (5, 16) and queries.shape == (3, 16)
+    assert np.concatenate([rows.ravel(), queries.ravel()]).tobytes() == exp.tobytes()
+
+
 def test_look_at_matches_reference(ref):
     from paper_2505_08124_b200.workload import orbit_camera
     for v in (0, 7, 333):

@@ -335,3 +335,44 @@ def test_query_tensor_core_candidate_overflow_falls_back_exactly(gpu_ctx, oracle
     ids = np.arange(6000, dtype=np.uint32)[::-1].copy()
     q = np.concatenate([raw[:2], rng.standard_normal((3, 64)).astype(np.float32)])
     _tc_vs_oracle(gpu_ctx, oracle, ids, unit, q, 10)
+
+
+@pytest.mark.parametrize("tau", [0.12, 0.18, 0.3])
+def test_query_threshold_tensor_core_vs_oracle(gpu_ctx, oracle, tau):
+    """Tensor-core threshold path (candidates >= tau - eps, exact rescoring)
+    against the oracle restatement of query_threshold."""
+    rng = np.random.default_rng(31)
+    raw = rng.uniform(-0.5, 0.5, (30001, 128)).astype(np.float32)
+    unit = _unit_rows(oracle, raw)
+    ids = rng.permutation(1 << 22)[:30001].astype(np.uint32)
+    gpu_ctx.store_set(ids, unit)
+    gpu_ctx.set_query_path(2)
+    try:
+        for i in range(4):
+            q = raw[i * 7] + rng.uniform(-0.2, 0.2, 128).astype(np.float32) if i < 2 else \
+                rng.uniform(-0.5, 0.5, 128).astype(np.float32)
+            gi, gs = gpu_ctx.query_threshold(q, tau)
+            oi, os_ = oracle.query_threshold(ids, unit, q, tau)
+            assert np.array_equal(gi, oi) and gs.tobytes() == os_.tobytes(), (i, len(gi), len(oi))
+    finally:
+        gpu_ctx.set_query_path(0)
+
+
+def test_query_threshold_tensor_core_overflow_falls_back(gpu_ctx, oracle):
+    """tau low enough that more rows qualify than the candidate cap: the exact
+    scan answers, with the same result."""
+    rng = np.random.default_rng(32)
+    raw = rng.uniform(-0.5, 0.5, (20000, 64)).astype(np.float32)
+    unit = _unit_rows(oracle, raw)
+    ids = np.arange(20000, dtype=np.uint32)
+    gpu_ctx.store_set(ids, unit)
+    gpu_ctx.set_query_path(2)
+    try:
+        q = rng.uniform(-0.5, 0.5, 64).astype(np.float32)
+        gi, gs = gpu_ctx.query_threshold(q, -0.05)
+        oi, os_ = oracle.query_threshold(ids, unit, q, -0.05)
+        assert len(oi) > 4096
+        assert np.array_equal(gi, oi) and gs.tobytes() == os_.tobytes()
+    finally:
+        gpu_ctx.set_query_path(0)
+
