@@ -87,3 +87,67 @@ def test_two_rank_combine_matches_single_worker():
     rel = np.sqrt(((e - g) ** 2).sum(1)) / np.where(den > 0, den, 1)
     assert rel.max() <= 1e-5
     np.testing.assert_allclose(cov, ec, rtol=1e-6)
+
+
+def _query_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import torch.distributed as dist
+
+    from oracle.bindings import Oracle
+    from paper_2505_08124_b200.multigpu import shard_rows, sharded_query_topk
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(44)
+    n, d = 3001, 32
+    O = Oracle()
+    raw = rng.uniform(-0.5, 0.5, (n, d)).astype(np.float32)
+    raw[1500:1510] = raw[7]  # exact ties across the shard boundary
+    unit = np.stack([O.normalized_copy(r) for r in raw])
+    ids = rng.permutation(n).astype(np.uint32)
+    queries = np.concatenate([raw[[7, 100]], rng.uniform(-0.5, 0.5, (4, d)).astype(np.float32)])
+    lo, hi = shard_rows(n, world, rank)
+
+    def local(qs, k):  # this rank's rows (the GPU product uses Context.query_topk)
+        return O.query_topk(ids[lo:hi], unit[lo:hi], qs, k)
+
+    for k in (1, 12, 5000):
+        mi, ms, mc = sharded_query_topk(local, queries, k)
+        q.put((rank, k, mi, ms, mc))
+    dist.destroy_process_group()
+
+
+def test_two_rank_sharded_query_matches_single_store():
+    """§8(e) query: per-rank top-k over row shards + all_gather + merge equals
+    the single-store answer bit for bit (ids, sims, counts; k > count too)."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_query_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=300) for _ in range(6)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    from oracle.bindings import Oracle
+    rng = np.random.default_rng(44)
+    n, d = 3001, 32
+    O = Oracle()
+    raw = rng.uniform(-0.5, 0.5, (n, d)).astype(np.float32)
+    raw[1500:1510] = raw[7]
+    unit = np.stack([O.normalized_copy(r) for r in raw])
+    ids = rng.permutation(n).astype(np.uint32)
+    queries = np.concatenate([raw[[7, 100]], rng.uniform(-0.5, 0.5, (4, d)).astype(np.float32)])
+    for rank, k, mi, ms, mc in got:
+        ei, es, ec = O.query_topk(ids, unit, queries, k)
+        kk = min(k, n)
+        assert np.array_equal(mc, ec), (rank, k)
+        assert np.array_equal(mi[:, :kk], ei[:, :kk]), (rank, k)
+        assert ms[:, :kk].tobytes() == es[:, :kk].tobytes(), (rank, k)
