@@ -116,7 +116,7 @@ struct ProfState {
 struct Lane {
     cudaStream_t stream = nullptr;
     cudaEvent_t contract_done = nullptr, done = nullptr;
-    DevBuf rec, boxes, keys, k32, k32s, order, iota, offsets, tkeys, tkeys_sorted, tvals, tile_start, tile_end, list;
+    DevBuf rec, boxes, rbox, keys, k32, k32s, order, iota, offsets, tkeys, tkeys_sorted, tvals, tile_start, tile_end, list;
     uint64_t iota_n = 0;           // entries of the 0..n-1 sequence in `iota`
     uint64_t list_cap = 0;         // entries of `list`
     DevBuf cub_tmp, info;
@@ -126,7 +126,7 @@ struct Lane {
     ViewInfo* h_info = nullptr;    // pinned
     uint32_t* h_u32 = nullptr;     // pinned scratch
     void release_all() {
-        DevBuf* b[] = {&rec, &boxes, &keys, &k32, &k32s, &order, &iota, &offsets, &tkeys, &tkeys_sorted, &tvals, &tile_start,
+        DevBuf* b[] = {&rec, &boxes, &rbox, &keys, &k32, &k32s, &order, &iota, &offsets, &tkeys, &tkeys_sorted, &tvals, &tile_start,
                        &tile_end, &list, &cub_tmp, &info, &pix_bits, &mask_bits,
                        &runs, &run_offsets, &clip, &spans, &acc, &touched, &touched_list};
         for (auto* x : b) x->release();
@@ -323,15 +323,17 @@ Geometry run_geometry(ss_ctx* c, Lane& L, cudaStream_t s, const ss_camera& cam) 
     {
         Scope sc(c, s, SS_K_BIN);
         auto* offsets = static_cast<uint32_t*>(L.offsets.ensure((N + 1) * 4));
+        auto* rbox = static_cast<uint2*>(L.rbox.ensure(std::max<uint64_t>(N, 1) * sizeof(uint2)));
+        own_launch(c, launch_gather_boxes(boxes, k32s, order, N, rbox, s), SS_K_BIN);
         size_t tb = 0;
-        SS_CUDA(launch_instance_offsets(boxes, k32s, order, N, offsets, nullptr, &tb, s));
+        SS_CUDA(launch_instance_offsets(rbox, N, offsets, nullptr, &tb, s));
         void* tmp = L.cub_tmp.ensure(tb);
         tb = L.cub_tmp.bytes;
-        SS_CUDA(launch_instance_offsets(boxes, k32s, order, N, offsets, tmp, &tb, s));
+        SS_CUDA(launch_instance_offsets(rbox, N, offsets, tmp, &tb, s));
         c->launches_cub += 1;
         c->prof.launches[SS_K_BIN] += 1;
         own_launch(c,
-                   launch_emit_instances(boxes, k32s, order, N, offsets, g.tiles_x, L.list_cap, L.tkeys.p, g.k16,
+                   launch_emit_instances(rbox, order, N, offsets, g.tiles_x, L.list_cap, L.tkeys.p, g.k16,
                                          L.tvals.as<uint32_t>(), info, s),
                    SS_K_BIN, 2);
     }

@@ -135,18 +135,29 @@ __global__ void tie_fixup_kernel(const uint32_t* k32, uint64_t n, const unsigned
     }
 }
 
+// Boxes in depth-rank order, gathered once: rbox[r] = boxes[order[r]], or
+// kCulledBox for the culled tail (a real box has x0 <= x1 < 65535).
+constexpr uint32_t kCulledBox = 0xffffffffu;
+__global__ void gather_boxes_kernel(const uint2* boxes, const uint32_t* k32s, const uint32_t* order, uint64_t n,
+                                    uint2* rbox) {
+    const uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    rbox[r] = k32s[r] == 0xffffffffu ? make_uint2(kCulledBox, kCulledBox) : __ldg(boxes + order[r]);
+}
+
+__device__ __forceinline__ uint32_t box_tiles(uint2 box) {
+    if (box.x == kCulledBox) return 0u;
+    return ((box.x >> 16) / kTile - (box.x & 0xffffu) / kTile + 1u) *
+           ((box.y >> 16) / kTile - (box.y & 0xffffu) / kTile + 1u);
+}
+
 // Tiles covered by the splat of depth rank r (0 for culled Gaussians).
 struct RankTiles {
-    const uint2* boxes;
-    const uint32_t* k32s;
-    const uint32_t* order;
+    const uint2* rbox;
     uint64_t n;
     __host__ __device__ __forceinline__ uint32_t operator()(uint64_t r) const {
 #ifdef __CUDA_ARCH__
-        if (r >= n || k32s[r] == 0xffffffffu) return 0u;
-        const uint2 box = __ldg(boxes + order[r]);
-        return ((box.x >> 16) / kTile - (box.x & 0xffffu) / kTile + 1u) *
-               ((box.y >> 16) / kTile - (box.y & 0xffffu) / kTile + 1u);
+        return r < n ? box_tiles(rbox[r]) : 0u;
 #else
         return 0u;
 #endif
@@ -157,18 +168,17 @@ struct RankTiles {
 // tile its box covers at offsets[r] (exclusive scan of RankTiles).  A stable
 // sort by tile then yields each tile's list in depth order.
 template <typename K>
-__global__ void emit_instances_kernel(const uint2* boxes, const uint32_t* k32s, const uint32_t* order, uint64_t n,
-                                      const uint32_t* offsets, uint32_t tiles_x, uint64_t cap, K* keys, uint32_t* vals,
-                                      ViewInfo* info) {
+__global__ void emit_instances_kernel(const uint2* rbox, const uint32_t* order, uint64_t n, const uint32_t* offsets,
+                                      uint32_t tiles_x, uint64_t cap, K* keys, uint32_t* vals, ViewInfo* info) {
     const uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
     if (offsets[n] > cap) { // lists do not fit: the host re-runs the view
         if (r == 0) info->overflow = 1u;
         return;
     }
-    if (k32s[r] == 0xffffffffu) return;
+    const uint2 box = rbox[r];
+    if (box.x == kCulledBox) return;
     const uint32_t id = order[r];
-    const uint2 box = __ldg(boxes + id);
     uint32_t o = offsets[r];
     for (uint32_t ty = (box.y & 0xffffu) / kTile; ty <= (box.y >> 16) / kTile; ++ty)
         for (uint32_t tx = (box.x & 0xffffu) / kTile; tx <= (box.x >> 16) / kTile; ++tx) {
@@ -190,13 +200,25 @@ __global__ void pad_keys_kernel(const uint32_t* offsets, uint64_t n, uint64_t ca
 template <typename K>
 __global__ void tile_ranges_kernel(const K* keys, const uint32_t* offsets, uint64_t n, uint32_t* start,
                                    uint32_t* end, ViewInfo* info) {
+    // each thread checks the boundaries of 16 bytes of sorted keys (one uint4)
+    constexpr uint32_t PER = 16 / sizeof(K);
     const uint64_t iv = offsets[n];
-    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i == 0) info->n_instances = iv;
-    if (i >= iv || info->overflow) return;
-    const uint32_t k = keys[i];
-    if (i == 0 || keys[i - 1] != k) start[k] = (uint32_t)i;
-    if (i == iv - 1 || keys[i + 1] != k) end[k] = (uint32_t)(i + 1);
+    const uint64_t i0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * PER;
+    if (i0 == 0) info->n_instances = iv;
+    if (i0 >= iv || info->overflow) return;
+    K k[PER];
+    *reinterpret_cast<uint4*>(k) = __ldg(reinterpret_cast<const uint4*>(keys + i0));
+    uint32_t prev = i0 == 0 ? 0xffffffffu : (uint32_t)__ldg(keys + i0 - 1);
+#pragma unroll
+    for (uint32_t j = 0; j < PER; ++j) {
+        const uint64_t i = i0 + j;
+        if (i >= iv) break;
+        const uint32_t kj = k[j];
+        if (i == 0 || prev != kj) start[kj] = (uint32_t)i;
+        const uint32_t next = j + 1 < PER ? (uint32_t)k[j + 1] : (i + 1 < iv ? (uint32_t)__ldg(keys + i + 1) : 0u);
+        if (i == iv - 1 || next != kj) end[kj] = (uint32_t)(i + 1);
+        prev = kj;
+    }
 }
 
 // --------------------------------------------------------- contraction
@@ -499,25 +521,31 @@ cudaError_t launch_tie_fixup(const uint32_t* k32s, uint64_t n, const unsigned lo
     return cudaGetLastError();
 }
 
-cudaError_t launch_instance_offsets(const uint2* boxes, const uint32_t* k32s, const uint32_t* order, uint64_t n,
-                                    uint32_t* offsets, void* tmp, size_t* tmp_bytes, cudaStream_t s) {
+cudaError_t launch_gather_boxes(const uint2* boxes, const uint32_t* k32s, const uint32_t* order, uint64_t n,
+                                uint2* rbox, cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    gather_boxes_kernel<<<blocks_for(n, 256), 256, 0, s>>>(boxes, k32s, order, n, rbox);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_instance_offsets(const uint2* rbox, uint64_t n, uint32_t* offsets, void* tmp, size_t* tmp_bytes,
+                                    cudaStream_t s) {
     cub::CountingInputIterator<uint64_t> ranks(0);
-    cub::TransformInputIterator<uint32_t, RankTiles, cub::CountingInputIterator<uint64_t>> it(
-        ranks, RankTiles{boxes, k32s, order, n});
+    cub::TransformInputIterator<uint32_t, RankTiles, cub::CountingInputIterator<uint64_t>> it(ranks, RankTiles{rbox, n});
     return cub::DeviceScan::ExclusiveSum(tmp, *tmp_bytes, it, offsets, (int)(n + 1), s);
 }
 
-cudaError_t launch_emit_instances(const uint2* boxes, const uint32_t* k32s, const uint32_t* order, uint64_t n,
-                                  const uint32_t* offsets, uint32_t tiles_x, uint64_t cap, void* keys, bool k16,
-                                  uint32_t* vals, ViewInfo* info, cudaStream_t s) {
+cudaError_t launch_emit_instances(const uint2* rbox, const uint32_t* order, uint64_t n, const uint32_t* offsets,
+                                  uint32_t tiles_x, uint64_t cap, void* keys, bool k16, uint32_t* vals, ViewInfo* info,
+                                  cudaStream_t s) {
     if (!n) return cudaSuccess;
     const unsigned g = (unsigned)std::min<uint64_t>(blocks_for(cap, 256), 148u * 16u);
     if (k16) {
-        emit_instances_kernel<uint16_t><<<blocks_for(n, 256), 256, 0, s>>>(boxes, k32s, order, n, offsets, tiles_x, cap,
+        emit_instances_kernel<uint16_t><<<blocks_for(n, 256), 256, 0, s>>>(rbox, order, n, offsets, tiles_x, cap,
                                                                             static_cast<uint16_t*>(keys), vals, info);
         pad_keys_kernel<uint16_t><<<g, 256, 0, s>>>(offsets, n, cap, static_cast<uint16_t*>(keys));
     } else {
-        emit_instances_kernel<uint32_t><<<blocks_for(n, 256), 256, 0, s>>>(boxes, k32s, order, n, offsets, tiles_x, cap,
+        emit_instances_kernel<uint32_t><<<blocks_for(n, 256), 256, 0, s>>>(rbox, order, n, offsets, tiles_x, cap,
                                                                             static_cast<uint32_t*>(keys), vals, info);
         pad_keys_kernel<uint32_t><<<g, 256, 0, s>>>(offsets, n, cap, static_cast<uint32_t*>(keys));
     }
@@ -528,11 +556,11 @@ cudaError_t launch_tile_ranges(const void* keys, bool k16, const uint32_t* offse
                                uint32_t* start, uint32_t* end, ViewInfo* info, cudaStream_t s) {
     // the instance count lives on the device; cover the capacity, threads past it exit
     if (k16)
-        tile_ranges_kernel<uint16_t><<<blocks_for(cap, 256), 256, 0, s>>>(static_cast<const uint16_t*>(keys), offsets,
-                                                                           n, start, end, info);
+        tile_ranges_kernel<uint16_t><<<blocks_for((cap + 7) / 8, 256), 256, 0, s>>>(
+            static_cast<const uint16_t*>(keys), offsets, n, start, end, info);
     else
-        tile_ranges_kernel<uint32_t><<<blocks_for(cap, 256), 256, 0, s>>>(static_cast<const uint32_t*>(keys), offsets,
-                                                                           n, start, end, info);
+        tile_ranges_kernel<uint32_t><<<blocks_for((cap + 3) / 4, 256), 256, 0, s>>>(
+            static_cast<const uint32_t*>(keys), offsets, n, start, end, info);
     return cudaGetLastError();
 }
 
