@@ -73,6 +73,7 @@ def parse():
     ap.add_argument("--cpu-sample-views", type=int, default=0)
     ap.add_argument("--no-query", action="store_true", help="skip the c5 vector-DB query leg")
     ap.add_argument("--lanes", type=int, default=0, help="pipeline lanes (0 = library default)")
+    ap.add_argument("--group", type=int, default=0, help="views per contraction group (0 = library default)")
     ap.add_argument("--cpu-sample-queries", type=int, default=32)
     return ap.parse_args()
 
@@ -359,6 +360,8 @@ def main():
     ctx.set_scene(wl.scene.mean, wl.scene.scale, wl.scene.quat_xyzw, wl.scene.opacity)
     lanes = args.lanes or DEFAULT_LANES
     ctx.set_lanes(lanes)
+    if args.group:
+        ctx.set_contract_group(args.group)
 
     # device-resident inputs for `value`
     dev = torch.device("cuda", local)

@@ -94,8 +94,11 @@ int ss_synchronize(ss_ctx* ctx);
  * SS_OPT_QUERY_PATH: 0 = auto (tensor-core coarse scoring + exact rescoring
  * for stores of >= 16384 rows with dim % 64 == 0 and dim <= 512), 1 = exact
  * scan only,
- * 2 = tensor-core path whenever dim allows.  Results are identical. */
-enum ss_option { SS_OPT_LANES = 1, SS_OPT_QUERY_PATH = 2 };
+ * 2 = tensor-core path whenever dim allows.  Results are identical.
+ * SS_OPT_CONTRACT_GROUP: views contracted together (1..4, default 1): each
+ * touched Gaussian's row is read and written once per group; the fp32
+ * operation order per row is the same for every group size. */
+enum ss_option { SS_OPT_LANES = 1, SS_OPT_QUERY_PATH = 2, SS_OPT_CONTRACT_GROUP = 3 };
 int ss_set_option(ss_ctx* ctx, int option, int64_t value);
 
 /* ---- scene (GaussianScene, scene.hpp:54-76) --------------------------- */

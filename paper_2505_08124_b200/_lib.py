@@ -163,6 +163,9 @@ class Context:
     def set_lanes(self, n: int):
         check(self._L.ss_set_option(self.h, 1, int(n)))
 
+    def set_contract_group(self, n: int):
+        check(self._L.ss_set_option(self.h, 3, int(n)))
+
     def set_query_path(self, path: int):
         """0 = auto, 1 = exact scan, 2 = tensor-core coarse + exact rescore."""
         check(self._L.ss_set_option(self.h, 2, int(path)))

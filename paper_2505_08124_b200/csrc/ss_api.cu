@@ -113,23 +113,49 @@ struct ProfState {
 // alternate between two lanes so one view's sorts and host handshakes overlap
 // the previous view's compositor; the contraction into the shared N x D sums
 // stays in view order through an event chain.
+// What a view leaves for the group contraction: per-(Gaussian, mask) scalars,
+// the touched list/stamps/count and its CLIP rows.  Two per lane, alternating
+// by group, so a lane's next view never waits for the previous group's
+// contraction.
+struct ContractSet {
+    DevBuf acc, touched, touched_list, clip, tcount;
+    uint64_t acc_elems = 0;        // zero-initialised elements of acc
+    uint32_t gen = 0;              // last stamp handed out
+    cudaEvent_t free_ev = nullptr; // recorded after the contraction that consumed this set
+    bool pending = false;          // a contraction reading this set has been issued
+    bool in_group = false;         // part of the group being formed
+    void release() {
+        DevBuf* b[] = {&acc, &touched, &touched_list, &clip, &tcount};
+        for (auto* x : b) x->release();
+        if (free_ev) cudaEventDestroy(free_ev);
+        free_ev = nullptr;
+        acc_elems = 0;
+        gen = 0;
+        pending = false;
+        in_group = false;
+    }
+};
+
 struct Lane {
     cudaStream_t stream = nullptr;
-    cudaEvent_t contract_done = nullptr, done = nullptr;
+    cudaEvent_t contract_done = nullptr, done = nullptr, raster_done = nullptr;
+    ContractSet sets[2];
+    uint32_t set_next = 0;
     DevBuf rec, boxes, rbox, keys, k32, k32s, order, iota, offsets, tkeys, tkeys_sorted, tvals, tile_start, tile_end, list;
     uint64_t iota_n = 0;           // entries of the 0..n-1 sequence in `iota`
     uint64_t list_cap = 0;         // entries of `list`
     DevBuf cub_tmp, info;
-    DevBuf pix_bits, mask_bits, runs, run_offsets, clip, spans;
-    DevBuf acc, touched, touched_list;
-    uint64_t acc_elems = 0;        // zero-initialised elements of acc
+    DevBuf pix_bits, mask_bits, runs, run_offsets, spans;
     ViewInfo* h_info = nullptr;    // pinned
     uint32_t* h_u32 = nullptr;     // pinned scratch
     void release_all() {
         DevBuf* b[] = {&rec, &boxes, &rbox, &keys, &k32, &k32s, &order, &iota, &offsets, &tkeys, &tkeys_sorted, &tvals, &tile_start,
                        &tile_end, &list, &cub_tmp, &info, &pix_bits, &mask_bits,
-                       &runs, &run_offsets, &clip, &spans, &acc, &touched, &touched_list};
+                       &runs, &run_offsets, &spans};
         for (auto* x : b) x->release();
+        for (auto& cs : sets) cs.release();
+        if (raster_done) cudaEventDestroy(raster_done);
+        raster_done = nullptr;
         if (h_info) cudaFreeHost(h_info);
         if (h_u32) cudaFreeHost(h_u32);
         if (contract_done) cudaEventDestroy(contract_done);
@@ -140,6 +166,13 @@ struct Lane {
         contract_done = done = nullptr;
         stream = nullptr;
     }
+};
+
+struct GroupMember {
+    Lane* lane;
+    ContractSet* set;
+    uint32_t n_masks;
+    const float* clip;
 };
 
 } // namespace
@@ -160,6 +193,12 @@ struct ss_ctx {
     uint32_t next_lane = 0;
     uint32_t n_lanes = 4;
     cudaEvent_t ev_user = nullptr;
+    // contraction group: consecutive views whose contraction is issued together
+    std::vector<ss::GroupMember> group;
+    cudaStream_t cstream = nullptr;      // group contractions (keeps lanes free)
+    uint32_t group_max = 1;              // SS_OPT_CONTRACT_GROUP
+    cudaEvent_t group_done = nullptr;
+    bool group_done_valid = false;
     ss::DevBuf cub_tmp, num_sel, info; // store / query scratch
     ss::DevBuf vstat; // per-view status of the last batch
     uint64_t cap_n_surv = 0;
@@ -451,17 +490,67 @@ void build_mask_bits(ss_ctx* c, Lane& L, cudaStream_t s, const ss_camera& cam, c
     c->prof.bytes[SS_K_MASKS] += nr * 4.0 + (double)P * ((M + 7) / 8);
 }
 
-void encode_one(ss_ctx* c, Lane& L, Lane& prev, const ss_camera& cam, const ss_view_masks* vm, int mode,
+// Issues the contraction of the views gathered in c->group on the stream of
+// the last one: after every member's compositor and after the previous
+// group's contraction (the shared sums are updated in view order).
+void flush_group(ss_ctx* c) {
+    if (c->group.empty()) return;
+    cudaStream_t st = c->cstream; // in order: groups contract one after another
+    for (auto& g : c->group) SS_CUDA(cudaStreamWaitEvent(st, g.lane->raster_done, 0));
+    ContractParams q;
+    std::memset(&q, 0, sizeof(q));
+    q.n_members = (uint32_t)c->group.size();
+    for (uint32_t i = 0; i < q.n_members; ++i) {
+        const GroupMember& g = c->group[i];
+        q.m[i].touched_list = g.set->touched_list.as<uint32_t>();
+        q.m[i].touched_count = g.set->tcount.as<unsigned long long>();
+        q.m[i].touched = g.set->touched.as<uint32_t>();
+        q.m[i].gen = g.set->gen;
+        q.m[i].acc = g.set->acc.as<float>();
+        q.m[i].n_masks = g.n_masks;
+        q.m[i].clip = g.clip;
+        c->prof.bytes[SS_K_CONTRACT] += (double)g.n_masks * c->dim * 4;
+    }
+    q.dim = c->dim;
+    q.sums = c->sums;
+    q.totals = c->totals;
+    q.count_pairs = 1;
+    q.cum = c->counters.as<unsigned long long>();
+    {
+        Scope sc(c, st, SS_K_CONTRACT);
+        own_launch(c, launch_contract(q, c->n * q.n_members, st), SS_K_CONTRACT);
+    }
+    SS_CUDA(cudaEventRecord(c->group_done, st));
+    c->group_done_valid = true;
+    for (auto& g : c->group) {
+        SS_CUDA(cudaEventRecord(g.set->free_ev, st));
+        g.set->pending = true;
+        g.set->in_group = false;
+    }
+    c->group.clear();
+}
+
+void encode_one(ss_ctx* c, Lane& L, const ss_camera& cam, const ss_view_masks* vm, int mode,
                 ViewInfo* vstat_slot) {
     check_camera(&cam);
     const uint32_t M = vm ? vm->n_masks : 0;
     if (M > 128) throw Error(SS_ERR_CONTRACT, "at most 128 masks per view are supported");
     const uint32_t words = mask_words_for(M);
     cudaStream_t s = L.stream;
-    if (M) build_mask_bits(c, L, s, cam, vm, words, cam.image_id);
+    ContractSet* S = nullptr;
+    if (M) {
+        S = &L.sets[L.set_next];
+        L.set_next ^= 1u;
+        if (S->in_group) flush_group(c); // the set is needed again before its group closed
+        if (S->pending) {                // its last contraction must be done before we overwrite it
+            SS_CUDA(cudaStreamWaitEvent(s, S->free_ev, 0));
+            S->pending = false;
+        }
+        build_mask_bits(c, L, s, cam, vm, words, cam.image_id);
+    }
     const float* d_clip = vm && (vm->flags & SS_MASKS_ON_DEVICE) ? vm->clip : nullptr;
     if (M && !d_clip) {
-        auto* dc = static_cast<float*>(L.clip.ensure(std::max<uint64_t>((uint64_t)M * c->dim, 1) * 4));
+        auto* dc = static_cast<float*>(S->clip.ensure(std::max<uint64_t>((uint64_t)M * c->dim, 1) * 4));
         d_clip = dc;
         Scope h(c, s, SS_K_H2D);
         SS_CUDA(cudaMemcpyAsync(dc, vm->clip, (size_t)M * c->dim * 4, cudaMemcpyHostToDevice, s));
@@ -471,52 +560,41 @@ void encode_one(ss_ctx* c, Lane& L, Lane& prev, const ss_camera& cam, const ss_v
     if (M) {
         // per-(Gaussian, mask) scalars: grow-only and kept zero by consume-and-clear
         const uint64_t need = c->n * (uint64_t)M;
-        if (need > L.acc_elems) {
-            L.acc.release();
-            L.acc.ensure(need * 4);
-            SS_CUDA(cudaMemsetAsync(L.acc.p, 0, L.acc.bytes, s));
-            L.acc_elems = L.acc.bytes / 4;
+        if (need > S->acc_elems) {
+            S->acc.release();
+            S->acc.ensure(need * 4);
+            SS_CUDA(cudaMemsetAsync(S->acc.p, 0, S->acc.bytes, s));
+            S->acc_elems = S->acc.bytes / 4;
         }
-        auto* touched = static_cast<uint32_t*>(L.touched.p);
-        if (L.touched.bytes < c->n * 4) {
-            L.touched.release();
-            touched = static_cast<uint32_t*>(L.touched.ensure(c->n * 4));
-            SS_CUDA(cudaMemsetAsync(touched, 0, L.touched.bytes, s));
+        if (S->touched.bytes < c->n * 4 || S->gen == 0xffffffffu) {
+            S->touched.release();
+            S->touched.ensure(c->n * 4);
+            SS_CUDA(cudaMemsetAsync(S->touched.p, 0, S->touched.bytes, s));
+            S->gen = 0;
         }
-        auto* tlist = static_cast<uint32_t*>(L.touched_list.ensure(c->n * 4));
+        S->gen += 1;
+        auto* tlist = static_cast<uint32_t*>(S->touched_list.ensure(c->n * 4));
+        auto* tcount = static_cast<unsigned long long*>(S->tcount.ensure(16));
+        SS_CUDA(cudaMemsetAsync(tcount, 0, 8, s));
         {
             Scope sc(c, s, SS_K_RASTER);
             RasterParams p = raster_params(c, L, cam, g);
             p.pix_bits = L.pix_bits.as<uint32_t>();
             p.mask_words = words;
             p.n_masks = M;
-            p.acc = L.acc.as<float>();
-            p.touched = touched;
+            p.acc = S->acc.as<float>();
+            p.touched = S->touched.as<uint32_t>();
             p.touched_list = tlist;
+            p.touched_count = tcount;
+            p.gen = S->gen;
             own_launch(c, launch_raster_fused(p, mode, g.tiles, s), SS_K_RASTER);
         }
-        // contractions into the shared sums run in view order across the lanes
-        SS_CUDA(cudaStreamWaitEvent(s, prev.contract_done, 0));
-        {
-            Scope sc(c, s, SS_K_CONTRACT);
-            ContractParams q;
-            q.touched_list = tlist;
-            q.touched = touched;
-            q.acc = L.acc.as<float>();
-            q.n_masks = M;
-            q.clip = d_clip;
-            q.dim = c->dim;
-            q.sums = c->sums;
-            q.totals = c->totals;
-            q.info = L.info.as<ViewInfo>();
-            q.count_pairs = 1;
-            q.cum = c->counters.as<unsigned long long>();
-            own_launch(c, launch_contract(q, c->n, s), SS_K_CONTRACT);
-            c->prof.bytes[SS_K_CONTRACT] += (double)M * c->dim * 4;
-        }
-        SS_CUDA(cudaEventRecord(L.contract_done, s));
+        SS_CUDA(cudaEventRecord(L.raster_done, s));
+        S->in_group = true;
+        c->group.push_back(GroupMember{&L, S, M, d_clip});
     }
     SS_CUDA(cudaMemcpyAsync(vstat_slot, L.info.p, sizeof(ViewInfo), cudaMemcpyDeviceToDevice, s));
+    if (c->group.size() >= std::min<uint32_t>(c->group_max, kMaxGroup)) flush_group(c);
 }
 
 // Encodes a batch of views with no per-view host synchronisation; the host
@@ -534,25 +612,32 @@ void encode_batch(ss_ctx* c, uint32_t nviews, const ss_camera* cams, const ss_vi
         // lanes start after everything already queued on the user stream
         SS_CUDA(cudaEventRecord(c->ev_user, c->stream));
         for (auto& L : c->lanes) SS_CUDA(cudaStreamWaitEvent(L.stream, c->ev_user, 0));
+        SS_CUDA(cudaStreamWaitEvent(c->cstream, c->ev_user, 0));
         {
             struct Join {
                 ss_ctx* c;
                 ~Join() {
-                    // the user stream resumes after both lanes drain (also on errors)
+                    // the user stream resumes after all lanes drain (also on errors;
+                    // a group left open by an error contributes nothing)
+                    for (auto& g : c->group) g.set->in_group = false;
+                    c->group.clear();
                     for (auto& L : c->lanes) {
                         cudaEventRecord(L.done, L.stream);
                         cudaStreamWaitEvent(c->stream, L.done, 0);
                     }
+                    cudaEventRecord(c->group_done, c->cstream);
+                    cudaStreamWaitEvent(c->stream, c->group_done, 0);
                 }
             } join{c};
             for (uint32_t v : todo) {
-                // view v runs on lane v mod n; its contraction follows the previous view's
+                // view v runs on lane v mod n; contractions run per group of
+                // consecutive views, groups in view order
                 const uint32_t li = c->next_lane % c->n_lanes;
                 Lane& L = c->lanes[li];
-                Lane& prev = c->lanes[(li + c->n_lanes - 1) % c->n_lanes];
                 c->next_lane = (li + 1) % c->n_lanes;
-                encode_one(c, L, prev, cams[v], masks ? &masks[v] : nullptr, mode, vstat + v);
+                encode_one(c, L, cams[v], masks ? &masks[v] : nullptr, mode, vstat + v);
             }
+            flush_group(c);
         }
         SS_CUDA(cudaMemcpyAsync(hstat.data(), vstat, (uint64_t)nviews * sizeof(ViewInfo), cudaMemcpyDeviceToHost,
                                 c->stream));
@@ -592,6 +677,7 @@ void profile_drain(ss_ctx* c) {
     if (c->prof.pending.empty()) return;
     SS_CUDA(cudaStreamSynchronize(c->stream));
     for (auto& L : c->lanes) SS_CUDA(cudaStreamSynchronize(L.stream));
+    SS_CUDA(cudaStreamSynchronize(c->cstream));
     for (auto& pe : c->prof.pending) {
         float ms = 0;
         SS_CUDA(cudaEventElapsedTime(&ms, pe.second.first, pe.second.second));
@@ -632,10 +718,14 @@ int ss_create(int device, ss_ctx** out) {
         SS_CUDA(cudaMallocHost(&c->h_init, sizeof(ViewInfo)));
         SS_CUDA(cudaMallocHost(&c->h_u32, 64));
         SS_CUDA(cudaEventCreateWithFlags(&c->ev_user, cudaEventDisableTiming));
+        SS_CUDA(cudaEventCreateWithFlags(&c->group_done, cudaEventDisableTiming));
+        SS_CUDA(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
         for (auto& L : c->lanes) {
             SS_CUDA(cudaStreamCreateWithFlags(&L.stream, cudaStreamNonBlocking));
             SS_CUDA(cudaEventCreateWithFlags(&L.contract_done, cudaEventDisableTiming));
             SS_CUDA(cudaEventCreateWithFlags(&L.done, cudaEventDisableTiming));
+            SS_CUDA(cudaEventCreateWithFlags(&L.raster_done, cudaEventDisableTiming));
+            for (auto& cs : L.sets) SS_CUDA(cudaEventCreateWithFlags(&cs.free_ev, cudaEventDisableTiming));
             SS_CUDA(cudaMallocHost(&L.h_info, sizeof(ViewInfo)));
             SS_CUDA(cudaMallocHost(&L.h_u32, 64));
             L.info.ensure(sizeof(ViewInfo));
@@ -655,6 +745,7 @@ void ss_destroy(ss_ctx* c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     for (auto& L : c->lanes) cudaStreamSynchronize(L.stream);
+    if (c->cstream) cudaStreamSynchronize(c->cstream);
     ss::DevBuf* bufs[] = {&c->mean_op, &c->scale, &c->quat, &c->cub_tmp, &c->num_sel, &c->info, &c->vstat, &c->pix_count,
                           &c->pix_offset, &c->entries, &c->per_pixel_total, &c->alpha, &c->counters, &c->sums_buf,
                           &c->totals_buf, &c->store_rows, &c->store_ids, &c->qbuf, &c->qnorm, &c->scores,
@@ -669,6 +760,11 @@ void ss_destroy(ss_ctx* c) {
     }
     for (auto& L : c->lanes) L.release_all();
     if (c->ev_user) cudaEventDestroy(c->ev_user);
+    if (c->group_done) cudaEventDestroy(c->group_done);
+    if (c->cstream) {
+        cudaStreamSynchronize(c->cstream);
+        cudaStreamDestroy(c->cstream);
+    }
     if (c->h_init) cudaFreeHost(c->h_init);
     if (c->h_u32) cudaFreeHost(c->h_u32);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
@@ -689,6 +785,10 @@ int ss_set_option(ss_ctx* c, int option, int64_t value) {
             if (value < 1 || value > (int64_t)ss_ctx::kMaxLanes)
                 throw Error(SS_ERR_CONTRACT, "SS_OPT_LANES must be between 1 and 4");
             c->n_lanes = (uint32_t)value;
+        } else if (option == SS_OPT_CONTRACT_GROUP) {
+            if (value < 1 || value > (int64_t)kMaxGroup)
+                throw Error(SS_ERR_CONTRACT, "SS_OPT_CONTRACT_GROUP must be between 1 and 4");
+            c->group_max = (uint32_t)value;
         } else if (option == SS_OPT_QUERY_PATH) {
             if (value < 0 || value > 2) throw Error(SS_ERR_CONTRACT, "SS_OPT_QUERY_PATH must be 0, 1 or 2");
             c->query_path = (int)value;

@@ -292,9 +292,11 @@ __device__ __forceinline__ void gate_and_accumulate(const RasterParams& p, bool 
         rem &= ~gm;
     }
     if ((int)lane == __ffs(em) - 1) {
-        // first toucher of this Gaussian appends it to the contraction list
-        if (*reinterpret_cast<volatile uint32_t*>(p.touched + gid) == 0u && atomicExch(p.touched + gid, 1u) == 0u) {
-            const unsigned long long slot = atomicAdd(&p.info->n_touched, 1ull);
+        // first toucher of this Gaussian in this view appends it to the
+        // contraction list (stamps, never cleared: the next view uses gen + 1)
+        if (*reinterpret_cast<volatile uint32_t*>(p.touched + gid) != p.gen &&
+            atomicExch(p.touched + gid, p.gen) != p.gen) {
+            const unsigned long long slot = atomicAdd(p.touched_count, 1ull);
             p.touched_list[slot] = gid;
         }
     }

@@ -71,8 +71,10 @@ struct RasterParams {
     const uint32_t* pix_bits;      // [P * mask_words]
     uint32_t mask_words, n_masks;
     float* acc;                    // [N * n_masks] per-(Gaussian, mask) scalars
-    uint32_t* touched;             // [N] 0/1
-    uint32_t* touched_list;        // [N] Gaussian ids
+    uint32_t* touched;             // [N] generation stamp of the last view that touched the Gaussian
+    uint32_t* touched_list;        // [N] Gaussian ids touched in this view
+    unsigned long long* touched_count; // entries of touched_list
+    uint32_t gen;                  // this view's stamp (never 0)
     ViewInfo* info;
 };
 

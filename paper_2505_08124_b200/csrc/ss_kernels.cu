@@ -222,72 +222,100 @@ __global__ void tile_ranges_kernel(const K* keys, const uint32_t* offsets, uint6
 }
 
 // --------------------------------------------------------- contraction
-// pipeline.hpp:70-80 accumulate, per view: for every rank the compositor
-// touched, row[gid] += sum_m acc[rank, m] * CLIP_m and total[gid] +=
-// sum_m acc[rank, m]; then the scalars are cleared for the next view.  One
-// warp per touched Gaussian; the 2 KB fp32 row moves as four coalesced
-// float4 sweeps; CLIP rows stay L1/L2-resident (M x 2 KB per view).
+// pipeline.hpp:70-80 accumulate for a group of up to four consecutive views:
+// for every Gaussian touched in any of them, row[gid] += sum_m acc_v[gid, m] *
+// CLIP_v,m and total[gid] += sum_m acc_v[gid, m], view by view in view order
+// and mask by mask in mask order -- the same fp32 operation sequence as one
+// contraction per view, but the 2 KB row is read and written once per group
+// (consecutive views touch ~95 % the same Gaussians).  A Gaussian is handled
+// by the first member whose list holds it; later members skip it.  One warp
+// per (member, list entry); CLIP rows stay L1/L2-resident.
+template <bool DIM512>
+__device__ __forceinline__ void contract_member(const ContractMember& m, uint32_t gid, uint32_t lane, uint32_t dim,
+                                                float* row, float4 (&racc)[4], float& wsum,
+                                                unsigned long long& pairs) {
+    float* accrow = m.acc + (size_t)gid * m.n_masks;
+    float vsum = 0.0f;
+    for (uint32_t c = 0; c < m.n_masks; c += 32) {
+        const uint32_t mi = c + lane;
+        float v = 0.0f;
+        if (mi < m.n_masks) {
+            v = accrow[mi];
+            if (v != 0.0f) accrow[mi] = 0.0f;
+        }
+        vsum += v;
+        uint32_t bal = __ballot_sync(0xffffffffu, v != 0.0f);
+        pairs += __popc(bal);
+        while (bal) {
+            const int src = __ffs(bal) - 1;
+            bal &= bal - 1;
+            const float w = __shfl_sync(0xffffffffu, v, src);
+            const float* e = m.clip + (size_t)(c + src) * dim;
+            if constexpr (DIM512) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float4 ev = __ldg(reinterpret_cast<const float4*>(e) + lane + 32 * q);
+                    racc[q].x += w * ev.x;
+                    racc[q].y += w * ev.y;
+                    racc[q].z += w * ev.z;
+                    racc[q].w += w * ev.w;
+                }
+            } else {
+                for (uint32_t d = lane; d < dim; d += 32) row[d] += w * __ldg(e + d);
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) vsum += __shfl_xor_sync(0xffffffffu, vsum, o);
+    wsum += vsum; // totals[gid] += this view's sum, in view order
+}
+
 template <bool DIM512>
 __global__ void __launch_bounds__(256) contract_kernel(ContractParams p) {
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const unsigned long long n_touched = p.info->n_touched;
+    unsigned long long cnt[kMaxGroup], total = 0;
+#pragma unroll
+    for (uint32_t i = 0; i < kMaxGroup; ++i) {
+        cnt[i] = i < p.n_members ? *p.m[i].touched_count : 0ull;
+        total += cnt[i];
+    }
     unsigned long long pairs = 0;
-    for (uint64_t t = warp0; t < n_touched; t += nwarps) {
-        const uint32_t gid = p.touched_list[t];
-        float* accrow = p.acc + (size_t)gid * p.n_masks;
+    for (uint64_t t = warp0; t < total; t += nwarps) {
+        uint32_t i = 0;
+        uint64_t tt = t;
+        while (tt >= cnt[i]) {
+            tt -= cnt[i];
+            ++i;
+        }
+        const uint32_t gid = p.m[i].touched_list[tt];
+        bool earlier = false;
+        for (uint32_t j = 0; j < i; ++j) earlier |= __ldg(p.m[j].touched + gid) == p.m[j].gen;
+        if (earlier) continue; // handled with the earlier view's entry
         float* row = p.sums + (size_t)gid * p.dim;
         float4 racc[4];
         if constexpr (DIM512) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) racc[q] = reinterpret_cast<const float4*>(row)[lane + 32 * q];
         }
-        float wsum = 0.0f;
-        for (uint32_t c = 0; c < p.n_masks; c += 32) {
-            const uint32_t mi = c + lane;
-            float v = 0.0f;
-            if (mi < p.n_masks) {
-                v = accrow[mi];
-                if (v != 0.0f) accrow[mi] = 0.0f;
-            }
-            wsum += v;
-            uint32_t bal = __ballot_sync(0xffffffffu, v != 0.0f);
-            pairs += __popc(bal);
-            while (bal) {
-                const int src = __ffs(bal) - 1;
-                bal &= bal - 1;
-                const float w = __shfl_sync(0xffffffffu, v, src);
-                const float* e = p.clip + (size_t)(c + src) * p.dim;
-                if constexpr (DIM512) {
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const float4 ev = __ldg(reinterpret_cast<const float4*>(e) + lane + 32 * q);
-                        racc[q].x += w * ev.x;
-                        racc[q].y += w * ev.y;
-                        racc[q].z += w * ev.z;
-                        racc[q].w += w * ev.w;
-                    }
-                } else {
-                    for (uint32_t d = lane; d < p.dim; d += 32) row[d] += w * __ldg(e + d);
-                }
-            }
+        float wsum = p.totals[gid];
+        for (uint32_t j = i; j < p.n_members; ++j) {
+            if (j != i && __ldg(p.m[j].touched + gid) != p.m[j].gen) continue;
+            float vs = 0.0f;
+            contract_member<DIM512>(p.m[j], gid, lane, p.dim, row, racc, vs, pairs);
+            wsum += vs;
         }
         if constexpr (DIM512) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) reinterpret_cast<float4*>(row)[lane + 32 * q] = racc[q];
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
-        if (lane == 0) {
-            p.totals[gid] += wsum;
-            p.touched[gid] = 0u;
-        }
+        if (lane == 0) p.totals[gid] = wsum;
     }
     if (p.count_pairs) {
         // pairs is warp-uniform (ballot popcounts); count once per warp
         if (lane == 0 && pairs) atomicAdd(p.cum + 1, pairs);
-        if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(p.cum, n_touched);
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(p.cum, total);
     }
 }
 

@@ -4,18 +4,28 @@
 
 namespace ss {
 
-struct ContractParams {
-    const uint32_t* touched_list;
-    uint32_t* touched;
-    float* acc;            // [N x n_masks]
+// One view of a contraction group: its compositor outputs and CLIP rows.
+struct ContractMember {
+    const uint32_t* touched_list;        // Gaussians touched in the view
+    const unsigned long long* touched_count;
+    const uint32_t* touched;             // generation stamps
+    uint32_t gen;                        // the view's stamp
+    float* acc;                          // [N x n_masks], consumed and cleared
     uint32_t n_masks;
-    const float* clip;     // [n_masks x dim]
+    const float* clip;                   // [n_masks x dim]
+};
+
+constexpr uint32_t kMaxGroup = 4;
+
+// Contraction of a group of consecutive views (view order = member order).
+struct ContractParams {
+    ContractMember m[kMaxGroup];
+    uint32_t n_members;
     uint32_t dim;
     float* sums;           // [N x dim]
     float* totals;         // [N]
-    ViewInfo* info;
     int count_pairs;
-    unsigned long long* cum; // running [G_v, K_v] totals
+    unsigned long long* cum; // running [G_v, K_v] totals (summed over views)
 };
 
 cudaError_t launch_rle_to_bits(const uint32_t* runs, const uint64_t* run_offsets, uint32_t n_masks, uint32_t words,
