@@ -191,16 +191,19 @@ def test_encode_bench_style_vs_oracle(gpu_ctx, oracle, n, views, w, h, m, dim):
     np.testing.assert_allclose(cov, ec, rtol=1e-5)
 
 
-@pytest.mark.parametrize("lanes", [1, 3, 4])
-def test_encode_lane_count_does_not_change_results(gpu_ctx, oracle, lanes):
-    """Views spread over 1..4 pipeline lanes (SS_OPT_LANES) contract in view
-    order; the result matches the oracle for every lane count."""
+@pytest.mark.parametrize("lanes,group", [(1, 1), (3, 1), (4, 1), (4, 2), (4, 4), (1, 4), (3, 4)])
+def test_encode_lane_count_does_not_change_results(gpu_ctx, oracle, lanes, group):
+    """Views spread over 1..4 pipeline lanes (SS_OPT_LANES) and contracted in
+    groups of 1..4 (SS_OPT_CONTRACT_GROUP) contract in view order; the result
+    matches the oracle for every combination (7 views: partial last group)."""
     wl = _bench_style(3000, 7, 64, 64, 24, 64, seed=91)
     gpu_ctx.set_lanes(lanes)
+    gpu_ctx.set_contract_group(group)
     try:
         rows, cov = _encode(gpu_ctx, wl.scene, wl.cams, wl.masks, 64)
     finally:
         gpu_ctx.set_lanes(4)
+        gpu_ctx.set_contract_group(1)
     er, ec = oracle.encode(wl.scene, wl.cams, wl.masks, 64)
     rel, cos = row_errors(rows, cov, er, ec)
     assert rel <= EMB_REL_TOL and cos >= EMB_COS_TOL, (lanes, rel, cos)
