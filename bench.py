@@ -303,7 +303,7 @@ def run_reference_arm(args, rank, world):
         return
     cfg = CONFIGS[args.config]
     cores = os.cpu_count() or 1
-    views = args.cpu_sample_views or max(1, min(cores, 8))
+    views = args.cpu_sample_views or max(1, min(cores, 16))
     times = []
     for i in range(args.warmup + args.steps):
         dt, kind, used, sample = cpu_reference_sample(args.config, args.seed, views, cores)
@@ -312,7 +312,7 @@ def run_reference_arm(args, rank, world):
     sec = float(np.mean(times))
     v = views / sec
     print(json.dumps({
-        "impl": "reference", "metric": "views_per_sec", "value": v, "unit": "views/s", "n_gpus": 0,
+        "impl": "reference", "metric": "views_per_sec", "value": v, "unit": "views/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "gaussians_embedded_per_sec": cfg["n_gaussians"] * v / cfg["n_views"],
@@ -480,7 +480,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            sample = args.cpu_sample_views or max(1, min(os.cpu_count() or 1, 8))
+            sample = args.cpu_sample_views or max(1, min(os.cpu_count() or 1, 16))
             dt, kind, cores, desc = cpu_reference_sample(args.config, args.seed, sample)
             cpu = {"value": sample / dt, "unit": "views/s", "cores": cores, "kind": kind, "sample": desc,
                    "seconds": dt}
