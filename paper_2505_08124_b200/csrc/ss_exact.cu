@@ -260,12 +260,9 @@ __device__ __forceinline__ uint32_t block_box_mask(uint32_t sx0, uint32_t sx1, u
     const int c0 = max((int)sx0 - (int)bx0, 0), c1 = min((int)sx1 - (int)bx0, 7);
     const int r0 = max((int)sy0 - (int)by0, 0), r1 = min((int)sy1 - (int)by0, 3);
     if (c0 > c1 || r0 > r1) return 0u;
-    const uint32_t row = (0xffu >> (7 - c1)) & (0xffu << c0);
-    uint32_t m = 0u;
-#pragma unroll
-    for (int r = 0; r < 4; ++r)
-        if (r >= r0 && r <= r1) m |= row << (8 * r);
-    return m;
+    const uint32_t row = (0xffu >> (7 - c1)) & (0xffu << c0);           // columns c0..c1 of one row
+    const uint32_t rows = (0xffffffffu >> (8 * (3 - r1))) & (0xffffffffu << (8 * r0)); // bytes r0..r1
+    return (row * 0x01010101u) & rows;                                   // row replicated, rows kept
 }
 
 // Fused-mode gating of one pixel slot's contribution: lanes with identical
@@ -413,20 +410,25 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
         }
         __syncwarp();
         const uint32_t nh = __popc(cand);
+        // staged splat j's pixel mask and id live in lane j's registers
+        const uint32_t smk = lane < nh ? wmask[lane] : 0u;
+        const uint32_t sgd = lane < nh ? wgid[lane] : 0u;
         for (uint32_t j = 0; j < nh; ++j) {
             const SplatRec& s = wrec[j];
+            const uint32_t mj = __shfl_sync(0xffffffffu, smk, j);
+            const uint32_t gj = __shfl_sync(0xffffffffu, sgd, j);
             float wf = 0.0f;
             bool c = false;
-            if ((wmask[j] & lane_bit) && !ps.done) c = composite_one<FALLOFF>(ps, s, stab, wf);
+            if ((mj & lane_bit) && !ps.done) c = composite_one<FALLOFF>(ps, s, stab, wf);
             if constexpr (KIND == 0) {
                 ps.count += c ? 1u : 0u;
             } else if constexpr (KIND == 1) {
                 if (c) {
-                    p.entries[ps.out++] = ss_weight_entry{wgid[j], ps.pixel, wf};
+                    p.entries[ps.out++] = ss_weight_entry{gj, ps.pixel, wf};
                     ps.total = da(ps.total, (double)wf);
                 }
             } else {
-                gate_and_accumulate<MW>(p, c, wf, grp, bits, wgid[j], lane);
+                gate_and_accumulate<MW>(p, c, wf, grp, bits, gj, lane);
             }
             if ((j & 7u) == 7u && __all_sync(0xffffffffu, ps.done)) break;
         }
