@@ -222,8 +222,8 @@ struct PixelState {
 // Evaluate one splat at one pixel: the reference's box test, Mahalanobis
 // cutoff, alpha clamp, skip rule, weight cutoff and transmittance floor, in
 // its exact fp64 operation order.  Returns whether an entry is emitted.
-template <bool FALLOFF>
-__device__ __forceinline__ bool composite_one(PixelState& ps, const SplatRec& s, const unsigned long long* stab,
+template <bool FALLOFF, typename Rec>
+__device__ __forceinline__ bool composite_one(PixelState& ps, const Rec& s, const unsigned long long* stab,
                                               float& wf) {
     const double dx = ds(ps.dpx, s.mu_x), dy = ds(ps.dpy, s.mu_y);
     const double d2 = da(da(dm(dm(s.a, dx), dx), dm(dm(s.b2, dx), dy)), dm(dm(s.c, dy), dy));
@@ -250,6 +250,19 @@ __device__ __forceinline__ bool composite_one(PixelState& ps, const SplatRec& s,
         if (ps.T < kCompositeConst[3]) ps.done = true;
         return emit;
     }
+}
+
+// The six doubles of a staged SplatRec (its first 48 bytes), read from a
+// 32-bit shared-window address.
+struct StagedSplat {
+    double mu_x, mu_y, a, b2, c, opacity;
+};
+__device__ __forceinline__ StagedSplat lds_splat(uint32_t addr) {
+    StagedSplat r;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(r.mu_x), "=d"(r.mu_y) : "r"(addr));
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2+16];" : "=d"(r.a), "=d"(r.b2) : "r"(addr));
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2+32];" : "=d"(r.c), "=d"(r.opacity) : "r"(addr));
+    return r;
 }
 
 // Bits of a warp's 8x4 block (lane l = column l&7, row l>>3) inside the
@@ -341,7 +354,9 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
     const uint32_t bx1 = bx0 + 7u, by1 = by0 + 3u;
     const uint32_t start = p.tile_start[tile], end = p.tile_end[tile];
     if (p.info->overflow) return; // tile lists incomplete: the view is re-run by the host
-    SplatRec* wrec = srec + 32u * warp;
+    const uint32_t wbase = 32u * warp;
+    SplatRec* wrec = srec + wbase;
+    uint32_t srec_addr = (uint32_t)__cvta_generic_to_shared(wrec);
     uint32_t* wgid = sgid + 32u * warp;
     uint32_t* wmask = smask + 32u * warp;
 
@@ -414,7 +429,10 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
         const uint32_t smk = lane < nh ? wmask[lane] : 0u;
         const uint32_t sgd = lane < nh ? wgid[lane] : 0u;
         for (uint32_t j = 0; j < nh; ++j) {
-            const SplatRec& s = wrec[j];
+            // keep the pixel coordinates and the staging address live instead of
+            // re-deriving them for every splat
+            asm volatile("" : "+d"(ps.dpx), "+d"(ps.dpy), "+r"(srec_addr));
+            const StagedSplat s = lds_splat(srec_addr + j * (uint32_t)sizeof(SplatRec));
             const uint32_t mj = __shfl_sync(0xffffffffu, smk, j);
             const uint32_t gj = __shfl_sync(0xffffffffu, sgd, j);
             float wf = 0.0f;
