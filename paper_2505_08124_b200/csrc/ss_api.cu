@@ -1122,10 +1122,16 @@ float* prepare_queries(ss_ctx* c, const float* queries, uint32_t nq) {
     auto* zf = static_cast<int*>(c->zero_flag.ensure(16));
     SS_CUDA(cudaMemsetAsync(zf, 0, 4, s));
     own_launch(c, launch_normalize_rows(d_q, nullptr, nq, dim, d_qn, zf, s), SS_K_QUERY);
-    SS_CUDA(cudaMemcpyAsync(c->h_u32, zf, 4, cudaMemcpyDeviceToHost, s));
-    SS_CUDA(cudaStreamSynchronize(s));
-    if (c->h_u32[0]) throw Error(SS_ERR_NUMERIC, "cannot normalize a zero vector");
+    // the zero-norm flag is read back with the results (no round trip here);
+    // check_query_norm() raises prepare_query's NumericError after the next sync
+    c->h_u32[1] = 0;
+    SS_CUDA(cudaMemcpyAsync(c->h_u32 + 1, zf, 4, cudaMemcpyDeviceToHost, s));
     return d_qn;
+}
+
+// vecstore.hpp:37 -- after a stream sync that followed prepare_queries
+void check_query_norm(ss_ctx* c) {
+    if (c->h_u32[1]) throw Error(SS_ERR_NUMERIC, "cannot normalize a zero vector");
 }
 } // namespace
 
@@ -1272,6 +1278,7 @@ bool threshold_tensor(ss_ctx* c, const float* d_qn, float tau, uint32_t* out_ids
     uint32_t hc[2];
     SS_CUDA(cudaMemcpyAsync(hc, ccount, 8, cudaMemcpyDeviceToHost, s));
     SS_CUDA(cudaStreamSynchronize(s));
+    check_query_norm(c);
     if (hc[0] > kCandCap) {
         c->qstat[3] += 1;
         return false;
@@ -1312,6 +1319,7 @@ int ss_query_topk(ss_ctx* c, const float* queries, uint32_t nq, uint32_t k, uint
         SS_CUDA(cudaMemcpyAsync(hid.data(), oid, hid.size() * 4, cudaMemcpyDeviceToHost, s));
         SS_CUDA(cudaMemcpyAsync(hsim.data(), osim, hsim.size() * 4, cudaMemcpyDeviceToHost, s));
         SS_CUDA(cudaStreamSynchronize(s));
+        check_query_norm(c);
         std::memcpy(out_ids, hid.data(), hid.size() * 4);
         std::memcpy(out_sims, hsim.data(), hsim.size() * 4);
         c->prof.bytes[SS_K_QUERY] += 2.0 * nq * (double)count * c->store_dim; // flops
@@ -1347,6 +1355,7 @@ int ss_query_threshold(ss_ctx* c, const float* query, float tau, uint32_t* out_i
         SS_CUDA(cub::DeviceSelect::Flagged(tmp, tb, keys, flags, ksel, num, (int)count, s));
         SS_CUDA(cudaMemcpyAsync(c->h_u32, num, 4, cudaMemcpyDeviceToHost, s));
         SS_CUDA(cudaStreamSynchronize(s));
+        check_query_norm(c);
         const uint64_t m = c->h_u32[0];
         tb = c->cub_tmp.bytes;
         SS_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, ksel, ksorted, (int)m, 0, 64, s));
