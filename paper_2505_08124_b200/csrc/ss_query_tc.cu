@@ -19,6 +19,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <atomic>
 
 #include "ss_query_tc.cuh"
 
@@ -747,16 +748,28 @@ cudaError_t launch_to_half(const float* in, uint64_t n, void* out, cudaStream_t 
 }
 
 namespace {
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device: remember the
+// largest size set for each (kernel, device) pair.
+template <typename K>
+cudaError_t ensure_smem(K kernel, size_t bytes) {
+    static std::atomic<size_t> done[64] = {};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    if (done[dev].load(std::memory_order_relaxed) >= bytes) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) done[dev].store(bytes, std::memory_order_relaxed);
+    return e;
+}
+} // namespace
+
+namespace {
 template <bool PILOT>
 cudaError_t coarse_launch(const CUtensorMap& mv, const CUtensorMap& mq, const tc::CoarseParams& p, int num_sms,
                           cudaStream_t s) {
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(tc::coarse_scores_kernel<PILOT>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::SMEM_BYTES);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    cudaError_t e = ensure_smem(tc::coarse_scores_kernel<PILOT>, tc::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
     if (p.k_dim > tc::MAX_K) return cudaErrorInvalidValue;
     const uint64_t tiles = (uint64_t)p.row_tiles_iter * ((p.n_queries + tc::BN - 1) / tc::BN);
     const uint32_t grid = 2u * (uint32_t)std::min<uint64_t>(tiles, (uint64_t)(num_sms / 2));
@@ -824,12 +837,8 @@ cudaError_t launch_rescore(const float* rows, const uint32_t* ids, uint32_t dim,
                            uint32_t k, float eps2, uint32_t* out_ids, float* out_sims, cudaStream_t s) {
     if (dim % 8 != 0) return cudaErrorInvalidValue;
     const size_t smem = (size_t)dim * 4 + (size_t)cand_cap * 8;
-    static size_t configured = 0;
-    if (smem > configured) {
-        cudaError_t e = cudaFuncSetAttribute(tc::rescore_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        configured = smem;
-    }
+    cudaError_t e = ensure_smem(tc::rescore_kernel, smem);
+    if (e != cudaSuccess) return e;
     tc::rescore_kernel<<<nq, tc::RS_THREADS, smem, s>>>(rows, ids, dim, qn, cand, cand_val, cand_cap, cand_count, k,
                                                         eps2, out_ids, out_sims);
     return cudaGetLastError();
@@ -841,13 +850,8 @@ cudaError_t launch_threshold_rescore(const float* rows, const uint32_t* ids, uin
                                      cudaStream_t s) {
     if (dim % 8 != 0) return cudaErrorInvalidValue;
     const size_t smem = (size_t)dim * 4 + (size_t)cand_cap * 8;
-    static size_t configured = 0;
-    if (smem > configured) {
-        cudaError_t e = cudaFuncSetAttribute(tc::threshold_rescore_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
-        configured = smem;
-    }
+    cudaError_t e = ensure_smem(tc::threshold_rescore_kernel, smem);
+    if (e != cudaSuccess) return e;
     tc::threshold_rescore_kernel<<<1, tc::RS_THREADS, smem, s>>>(rows, ids, dim, qn, cand, cand_cap, cand_count, tau,
                                                                  out_ids, out_sims, out_cap, out_count);
     return cudaGetLastError();
