@@ -749,10 +749,11 @@ cudaError_t launch_to_half(const float* in, uint64_t n, void* out, cudaStream_t 
 
 namespace {
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device: remember the
-// largest size set for each (kernel, device) pair.
+// largest size set for each (kernel, device) pair.  `done` is one array per
+// kernel (kernels of the same function type must not share it).
+using SmemDone = std::atomic<size_t>[64];
 template <typename K>
-cudaError_t ensure_smem(K kernel, size_t bytes) {
-    static std::atomic<size_t> done[64] = {};
+cudaError_t ensure_smem(K kernel, size_t bytes, SmemDone& done) {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
@@ -768,7 +769,8 @@ namespace {
 template <bool PILOT>
 cudaError_t coarse_launch(const CUtensorMap& mv, const CUtensorMap& mq, const tc::CoarseParams& p, int num_sms,
                           cudaStream_t s) {
-    cudaError_t e = ensure_smem(tc::coarse_scores_kernel<PILOT>, tc::SMEM_BYTES);
+    static SmemDone done = {};
+    cudaError_t e = ensure_smem(tc::coarse_scores_kernel<PILOT>, tc::SMEM_BYTES, done);
     if (e != cudaSuccess) return e;
     if (p.k_dim > tc::MAX_K) return cudaErrorInvalidValue;
     const uint64_t tiles = (uint64_t)p.row_tiles_iter * ((p.n_queries + tc::BN - 1) / tc::BN);
@@ -837,7 +839,8 @@ cudaError_t launch_rescore(const float* rows, const uint32_t* ids, uint32_t dim,
                            uint32_t k, float eps2, uint32_t* out_ids, float* out_sims, cudaStream_t s) {
     if (dim % 8 != 0) return cudaErrorInvalidValue;
     const size_t smem = (size_t)dim * 4 + (size_t)cand_cap * 8;
-    cudaError_t e = ensure_smem(tc::rescore_kernel, smem);
+    static SmemDone done = {};
+    cudaError_t e = ensure_smem(tc::rescore_kernel, smem, done);
     if (e != cudaSuccess) return e;
     tc::rescore_kernel<<<nq, tc::RS_THREADS, smem, s>>>(rows, ids, dim, qn, cand, cand_val, cand_cap, cand_count, k,
                                                         eps2, out_ids, out_sims);
@@ -850,7 +853,8 @@ cudaError_t launch_threshold_rescore(const float* rows, const uint32_t* ids, uin
                                      cudaStream_t s) {
     if (dim % 8 != 0) return cudaErrorInvalidValue;
     const size_t smem = (size_t)dim * 4 + (size_t)cand_cap * 8;
-    cudaError_t e = ensure_smem(tc::threshold_rescore_kernel, smem);
+    static SmemDone done = {};
+    cudaError_t e = ensure_smem(tc::threshold_rescore_kernel, smem, done);
     if (e != cudaSuccess) return e;
     tc::threshold_rescore_kernel<<<1, tc::RS_THREADS, smem, s>>>(rows, ids, dim, qn, cand, cand_cap, cand_count, tau,
                                                                  out_ids, out_sims, out_cap, out_count);
