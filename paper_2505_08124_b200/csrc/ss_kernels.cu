@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <atomic>
 
 #include <cub/block/block_scan.cuh>
 #include <cub/device/device_scan.cuh>
@@ -230,7 +231,7 @@ __global__ void tile_ranges_kernel(const K* keys, const uint32_t* offsets, uint6
 // (consecutive views touch ~95 % the same Gaussians).  A Gaussian is handled
 // by the first member whose list holds it; later members skip it.  One warp
 // per (member, list entry); CLIP rows stay L1/L2-resident.
-template <bool DIM512>
+template <bool DIM512, bool CLIP_SMEM = false>
 __device__ __forceinline__ void contract_member(const ContractMember& m, uint32_t gid, uint32_t lane, uint32_t dim,
                                                 float* row, float4 (&racc)[4], float& wsum,
                                                 unsigned long long& pairs) {
@@ -254,7 +255,8 @@ __device__ __forceinline__ void contract_member(const ContractMember& m, uint32_
             if constexpr (DIM512) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    const float4 ev = __ldg(reinterpret_cast<const float4*>(e) + lane + 32 * q);
+                    const float4 ev = CLIP_SMEM ? reinterpret_cast<const float4*>(e)[lane + 32 * q]
+                                                : __ldg(reinterpret_cast<const float4*>(e) + lane + 32 * q);
                     racc[q].x += w * ev.x;
                     racc[q].y += w * ev.y;
                     racc[q].z += w * ev.z;
@@ -314,6 +316,43 @@ __global__ void __launch_bounds__(256) contract_kernel(ContractParams p) {
     }
     if (p.count_pairs) {
         // pairs is warp-uniform (ballot popcounts); count once per warp
+        if (lane == 0 && pairs) atomicAdd(p.cum + 1, pairs);
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(p.cum, total);
+    }
+}
+
+// Single-view contraction with the view's CLIP rows (M <= 64, D = 512)
+// staged in shared memory: one 1024-thread CTA per SM, persistent over the
+// touched list.  Same per-row operation order as contract_kernel.
+__global__ void __launch_bounds__(1024, 1) contract_smem_kernel(ContractParams p) {
+    extern __shared__ float4 sclip4[]; // n_masks x 128 float4
+    const ContractMember& m = p.m[0];
+    const uint32_t n4 = m.n_masks * 128u;
+    const float4* g4 = reinterpret_cast<const float4*>(m.clip);
+    for (uint32_t i = threadIdx.x; i < n4; i += blockDim.x) sclip4[i] = __ldg(g4 + i);
+    __syncthreads();
+    ContractMember ms = m;
+    ms.clip = reinterpret_cast<const float*>(sclip4);
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const unsigned long long total = *m.touched_count;
+    unsigned long long pairs = 0;
+    for (uint64_t t = warp0; t < total; t += nwarps) {
+        const uint32_t gid = m.touched_list[t];
+        float* row = p.sums + (size_t)gid * p.dim;
+        float4 racc[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) racc[q] = reinterpret_cast<const float4*>(row)[lane + 32 * q];
+        float wsum = p.totals[gid];
+        float vs = 0.0f;
+        contract_member<true, true>(ms, gid, lane, p.dim, row, racc, vs, pairs);
+        wsum += vs;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) reinterpret_cast<float4*>(row)[lane + 32 * q] = racc[q];
+        if (lane == 0) p.totals[gid] = wsum;
+    }
+    if (p.count_pairs) {
         if (lane == 0 && pairs) atomicAdd(p.cum + 1, pairs);
         if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(p.cum, total);
     }
@@ -594,6 +633,21 @@ cudaError_t launch_tile_ranges(const void* keys, bool k16, const uint32_t* offse
 
 cudaError_t launch_contract(const ContractParams& p, uint64_t max_touched, cudaStream_t s) {
     if (!max_touched) return cudaSuccess;
+    if (p.n_members == 1 && p.dim == 512 && p.m[0].n_masks <= 64) {
+        const size_t smem = (size_t)p.m[0].n_masks * 512 * 4;
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        static std::atomic<int> configured[64] = {};
+        if (dev >= 0 && dev < 64 && !configured[dev].load()) {
+            cudaError_t e = cudaFuncSetAttribute(contract_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 64 * 512 * 4);
+            if (e != cudaSuccess) return e;
+            configured[dev].store(1);
+        }
+        contract_smem_kernel<<<sms, 1024, smem, s>>>(p);
+        return cudaGetLastError();
+    }
     if (p.dim == 512)
         contract_kernel<true><<<warp_grid(max_touched), 256, 0, s>>>(p);
     else
