@@ -166,27 +166,54 @@ struct RankTiles {
 };
 
 // Instances in depth-rank order: splat of rank r writes (tile, id) for every
-// tile its box covers at offsets[r] (exclusive scan of RankTiles).  A stable
-// sort by tile then yields each tile's list in depth order.
+// tile its box covers (row-major within the box) at offsets[r] (exclusive
+// scan of RankTiles).  A stable sort by tile then yields each tile's list in
+// depth order.  Warp-cooperative: the warp's 32 ranks own one contiguous
+// output range, written 32 consecutive slots per round; a slot's rank is
+// found by a binary search over the lanes' offsets (shuffles).
 template <typename K>
 __global__ void emit_instances_kernel(const uint2* rbox, const uint32_t* order, uint64_t n, const uint32_t* offsets,
                                       uint32_t tiles_x, uint64_t cap, K* keys, uint32_t* vals, ViewInfo* info) {
     const uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n) return;
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t r0 = r - lane;
+    if (r0 >= n) return;
     if (offsets[n] > cap) { // lists do not fit: the host re-runs the view
         if (r == 0) info->overflow = 1u;
         return;
     }
-    const uint2 box = rbox[r];
-    if (box.x == kCulledBox) return;
-    const uint32_t id = order[r];
-    uint32_t o = offsets[r];
-    for (uint32_t ty = (box.y & 0xffffu) / kTile; ty <= (box.y >> 16) / kTile; ++ty)
-        for (uint32_t tx = (box.x & 0xffffu) / kTile; tx <= (box.x >> 16) / kTile; ++tx) {
-            keys[o] = (K)(ty * tiles_x + tx);
-            vals[o] = id;
-            ++o;
+    const bool live = r < n;
+    const uint2 box = live ? rbox[r] : make_uint2(kCulledBox, kCulledBox);
+    const uint32_t cnt = box_tiles(box);
+    const uint32_t off = live ? offsets[r] : offsets[n];
+    const uint32_t tx0 = (box.x & 0xffffu) / kTile, ty0 = (box.y & 0xffffu) / kTile;
+    const uint32_t nx = box.x == kCulledBox ? 1u : (box.x >> 16) / kTile - tx0 + 1u;
+    const uint32_t id = live && cnt ? order[r] : 0u;
+    const uint32_t base = __shfl_sync(0xffffffffu, off, 0);
+    const uint32_t rel = off - base; // lane's first slot within the warp's range
+    const uint32_t total = __shfl_sync(0xffffffffu, rel + cnt, 31);
+    for (uint32_t p0 = 0; p0 < total; p0 += 32) {
+        const uint32_t pos = p0 + lane;
+        // owner: the last lane whose first slot is <= pos (empty lanes never own a slot)
+        uint32_t o = 0;
+#pragma unroll
+        for (uint32_t step = 16; step > 0; step >>= 1) {
+            const uint32_t rv = __shfl_sync(0xffffffffu, rel, o + step);
+            if (rv <= pos) o += step;
         }
+        const uint32_t o_rel = __shfl_sync(0xffffffffu, rel, o);
+        const uint32_t o_nx = __shfl_sync(0xffffffffu, nx, o);
+        const uint32_t o_tx0 = __shfl_sync(0xffffffffu, tx0, o);
+        const uint32_t o_ty0 = __shfl_sync(0xffffffffu, ty0, o);
+        const uint32_t o_id = __shfl_sync(0xffffffffu, id, o);
+        if (pos < total) {
+            const uint32_t k = pos - o_rel;
+            const uint32_t dy = k / o_nx, dx = k - dy * o_nx;
+            const uint64_t q = (uint64_t)base + pos;
+            keys[q] = (K)((o_ty0 + dy) * tiles_x + o_tx0 + dx);
+            vals[q] = o_id;
+        }
+    }
 }
 
 // Pad [I_v, cap) with the largest key so a fixed-size sort leaves it last.
