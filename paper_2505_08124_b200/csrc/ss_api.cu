@@ -141,7 +141,7 @@ struct Lane {
     cudaEvent_t contract_done = nullptr, done = nullptr, raster_done = nullptr;
     ContractSet sets[2];
     uint32_t set_next = 0;
-    DevBuf rec, boxes, rbox, keys, k32, k32s, order, iota, offsets, tkeys, tkeys_sorted, tvals, tile_start, tile_end, list;
+    DevBuf rec, boxes, rbox, rcnt, keys, k32, k32s, order, iota, offsets, tkeys, tkeys_sorted, tvals, tile_start, tile_end, list;
     uint64_t iota_n = 0;           // entries of the 0..n-1 sequence in `iota`
     uint64_t list_cap = 0;         // entries of `list`
     DevBuf cub_tmp, info;
@@ -149,7 +149,7 @@ struct Lane {
     ViewInfo* h_info = nullptr;    // pinned
     uint32_t* h_u32 = nullptr;     // pinned scratch
     void release_all() {
-        DevBuf* b[] = {&rec, &boxes, &rbox, &keys, &k32, &k32s, &order, &iota, &offsets, &tkeys, &tkeys_sorted, &tvals, &tile_start,
+        DevBuf* b[] = {&rec, &boxes, &rbox, &rcnt, &keys, &k32, &k32s, &order, &iota, &offsets, &tkeys, &tkeys_sorted, &tvals, &tile_start,
                        &tile_end, &list, &cub_tmp, &info, &pix_bits, &mask_bits,
                        &runs, &run_offsets, &spans};
         for (auto* x : b) x->release();
@@ -363,12 +363,13 @@ Geometry run_geometry(ss_ctx* c, Lane& L, cudaStream_t s, const ss_camera& cam) 
         Scope sc(c, s, SS_K_BIN);
         auto* offsets = static_cast<uint32_t*>(L.offsets.ensure((N + 1) * 4));
         auto* rbox = static_cast<uint2*>(L.rbox.ensure(std::max<uint64_t>(N, 1) * sizeof(uint2)));
-        own_launch(c, launch_gather_boxes(boxes, k32s, order, N, rbox, s), SS_K_BIN);
+        auto* rcnt = static_cast<uint32_t*>(L.rcnt.ensure((N + 1) * 4));
+        own_launch(c, launch_gather_boxes(boxes, k32s, order, N, rbox, rcnt, s), SS_K_BIN);
         size_t tb = 0;
-        SS_CUDA(launch_instance_offsets(rbox, N, offsets, nullptr, &tb, s));
+        SS_CUDA(launch_instance_offsets(rcnt, N, offsets, nullptr, &tb, s));
         void* tmp = L.cub_tmp.ensure(tb);
         tb = L.cub_tmp.bytes;
-        SS_CUDA(launch_instance_offsets(rbox, N, offsets, tmp, &tb, s));
+        SS_CUDA(launch_instance_offsets(rcnt, N, offsets, tmp, &tb, s));
         c->launches_cub += 1;
         c->prof.launches[SS_K_BIN] += 1;
         own_launch(c,

@@ -139,11 +139,20 @@ __global__ void tie_fixup_kernel(const uint32_t* k32, uint64_t n, const unsigned
 // Boxes in depth-rank order, gathered once: rbox[r] = boxes[order[r]], or
 // kCulledBox for the culled tail (a real box has x0 <= x1 < 65535).
 constexpr uint32_t kCulledBox = 0xffffffffu;
+__device__ __forceinline__ uint32_t box_tiles(uint2 box);
+
+// ... and the rank's tile count, cnt[n] = 0, for the offset scan.
 __global__ void gather_boxes_kernel(const uint2* boxes, const uint32_t* k32s, const uint32_t* order, uint64_t n,
-                                    uint2* rbox) {
+                                    uint2* rbox, uint32_t* cnt) {
     const uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n) return;
-    rbox[r] = k32s[r] == 0xffffffffu ? make_uint2(kCulledBox, kCulledBox) : __ldg(boxes + order[r]);
+    if (r > n) return;
+    if (r == n) {
+        cnt[n] = 0u;
+        return;
+    }
+    const uint2 b = k32s[r] == 0xffffffffu ? make_uint2(kCulledBox, kCulledBox) : __ldg(boxes + order[r]);
+    rbox[r] = b;
+    cnt[r] = box_tiles(b);
 }
 
 __device__ __forceinline__ uint32_t box_tiles(uint2 box) {
@@ -152,18 +161,6 @@ __device__ __forceinline__ uint32_t box_tiles(uint2 box) {
            ((box.y >> 16) / kTile - (box.y & 0xffffu) / kTile + 1u);
 }
 
-// Tiles covered by the splat of depth rank r (0 for culled Gaussians).
-struct RankTiles {
-    const uint2* rbox;
-    uint64_t n;
-    __host__ __device__ __forceinline__ uint32_t operator()(uint64_t r) const {
-#ifdef __CUDA_ARCH__
-        return r < n ? box_tiles(rbox[r]) : 0u;
-#else
-        return 0u;
-#endif
-    }
-};
 
 // Instances in depth-rank order: splat of rank r writes (tile, id) for every
 // tile its box covers (row-major within the box) at offsets[r] (exclusive
@@ -616,17 +613,14 @@ cudaError_t launch_tie_fixup(const uint32_t* k32s, uint64_t n, const unsigned lo
 }
 
 cudaError_t launch_gather_boxes(const uint2* boxes, const uint32_t* k32s, const uint32_t* order, uint64_t n,
-                                uint2* rbox, cudaStream_t s) {
-    if (!n) return cudaSuccess;
-    gather_boxes_kernel<<<blocks_for(n, 256), 256, 0, s>>>(boxes, k32s, order, n, rbox);
+                                uint2* rbox, uint32_t* cnt, cudaStream_t s) {
+    gather_boxes_kernel<<<blocks_for(n + 1, 256), 256, 0, s>>>(boxes, k32s, order, n, rbox, cnt);
     return cudaGetLastError();
 }
 
-cudaError_t launch_instance_offsets(const uint2* rbox, uint64_t n, uint32_t* offsets, void* tmp, size_t* tmp_bytes,
+cudaError_t launch_instance_offsets(const uint32_t* cnt, uint64_t n, uint32_t* offsets, void* tmp, size_t* tmp_bytes,
                                     cudaStream_t s) {
-    cub::CountingInputIterator<uint64_t> ranks(0);
-    cub::TransformInputIterator<uint32_t, RankTiles, cub::CountingInputIterator<uint64_t>> it(ranks, RankTiles{rbox, n});
-    return cub::DeviceScan::ExclusiveSum(tmp, *tmp_bytes, it, offsets, (int)(n + 1), s);
+    return cub::DeviceScan::ExclusiveSum(tmp, *tmp_bytes, cnt, offsets, (int)(n + 1), s);
 }
 
 cudaError_t launch_emit_instances(const uint2* rbox, const uint32_t* order, uint64_t n, const uint32_t* offsets,

@@ -37,8 +37,8 @@ cudaError_t launch_narrow_keys(const unsigned long long* keys, uint64_t n, const
 cudaError_t launch_tie_fixup(const uint32_t* k32s, uint64_t n, const unsigned long long* keys, uint32_t* order,
                              cudaStream_t s);
 cudaError_t launch_gather_boxes(const uint2* boxes, const uint32_t* k32s, const uint32_t* order, uint64_t n,
-                                uint2* rbox, cudaStream_t s);
-cudaError_t launch_instance_offsets(const uint2* rbox, uint64_t n, uint32_t* offsets, void* tmp, size_t* tmp_bytes,
+                                uint2* rbox, uint32_t* cnt, cudaStream_t s);
+cudaError_t launch_instance_offsets(const uint32_t* cnt, uint64_t n, uint32_t* offsets, void* tmp, size_t* tmp_bytes,
                                     cudaStream_t s);
 cudaError_t launch_emit_instances(const uint2* rbox, const uint32_t* order, uint64_t n, const uint32_t* offsets,
                                   uint32_t tiles_x, uint64_t cap, void* keys, bool k16, uint32_t* vals, ViewInfo* info,
