@@ -104,35 +104,65 @@ __device__ __forceinline__ bool depth_before(unsigned long long ka, uint32_t ia,
 }
 
 __global__ void narrow_keys_kernel(const unsigned long long* keys, uint64_t n, const ViewInfo* info, uint32_t* k32) {
-    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const unsigned long long k = keys[i];
-    if (k == ~0ull) {
-        k32[i] = 0xffffffffu;
-        return;
+    // four keys per thread (two 16-byte loads, one 16-byte store)
+    const uint64_t i0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    if (i0 >= n) return;
+    const unsigned long long mn = info->min_key;
+    const uint32_t sh = narrow_shift(info);
+    unsigned long long k[4];
+    if (i0 + 4 <= n) {
+        const ulonglong2 a = reinterpret_cast<const ulonglong2*>(keys + i0)[0];
+        const ulonglong2 b = reinterpret_cast<const ulonglong2*>(keys + i0)[1];
+        k[0] = a.x, k[1] = a.y, k[2] = b.x, k[3] = b.y;
+    } else {
+        for (int j = 0; j < 4; ++j) k[j] = i0 + j < n ? keys[i0 + j] : ~0ull;
     }
-    const uint32_t v = (uint32_t)((k - info->min_key) >> narrow_shift(info));
-    k32[i] = v == 0xffffffffu ? 0xfffffffeu : v; // culled Gaussians alone sort last
+    uint32_t v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t t = (uint32_t)((k[j] - mn) >> sh);
+        v[j] = k[j] == ~0ull ? 0xffffffffu : (t == 0xffffffffu ? 0xfffffffeu : t); // culled alone sort last
+    }
+    if (i0 + 4 <= n) {
+        reinterpret_cast<uint4*>(k32 + i0)[0] = make_uint4(v[0], v[1], v[2], v[3]);
+    } else {
+        for (int j = 0; j < 4; ++j)
+            if (i0 + j < n) k32[i0 + j] = v[j];
+    }
 }
 
 __global__ void tie_fixup_kernel(const uint32_t* k32, uint64_t n, const unsigned long long* keys, uint32_t* order) {
-    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i + 1 >= n) return;
-    const uint32_t k = k32[i];
-    if (k == 0xffffffffu) return;                // culled tail
-    if (i > 0 && k32[i - 1] == k) return;       // not a run start
-    if (k32[i + 1] != k) return;                // singleton
-    uint64_t e = i + 2;
-    while (e < n && k32[e] == k) ++e;
-    for (uint64_t a = i + 1; a < e; ++a) {      // insertion sort by (depth bits, id)
-        const uint32_t id = order[a];
-        const unsigned long long key = keys[id];
-        uint64_t b = a;
-        while (b > i && depth_before(key, id, keys[order[b - 1]], order[b - 1])) {
-            order[b] = order[b - 1];
-            --b;
+    // four sorted keys per thread: a run of equal narrowed keys is fixed by the
+    // thread owning its first element (almost always there is none)
+    const uint64_t i0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    if (i0 + 1 >= n) return;
+    uint32_t kk[5];
+    if (i0 + 5 <= n) {
+        const uint4 q = reinterpret_cast<const uint4*>(k32 + i0)[0];
+        kk[0] = q.x, kk[1] = q.y, kk[2] = q.z, kk[3] = q.w, kk[4] = k32[i0 + 4];
+    } else {
+        for (int j = 0; j < 5; ++j) kk[j] = i0 + j < n ? k32[i0 + j] : 0xffffffffu;
+    }
+    uint32_t prev = i0 > 0 ? k32[i0 - 1] : 0xffffffffu;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint64_t i = i0 + j;
+        const uint32_t k = kk[j];
+        const bool start = i + 1 < n && k != 0xffffffffu && (i == 0 || prev != k) && kk[j + 1] == k;
+        prev = k;
+        if (!start) continue;
+        uint64_t e = i + 2;
+        while (e < n && k32[e] == k) ++e;
+        for (uint64_t a = i + 1; a < e; ++a) { // insertion sort by (depth bits, id)
+            const uint32_t id = order[a];
+            const unsigned long long key = keys[id];
+            uint64_t b = a;
+            while (b > i && depth_before(key, id, keys[order[b - 1]], order[b - 1])) {
+                order[b] = order[b - 1];
+                --b;
+            }
+            order[b] = id;
         }
-        order[b] = id;
     }
 }
 
@@ -601,14 +631,14 @@ cudaError_t launch_resample_bits(const uint32_t* src, uint32_t sw, uint32_t sh, 
 cudaError_t launch_narrow_keys(const unsigned long long* keys, uint64_t n, const ViewInfo* info, uint32_t* k32,
                                cudaStream_t s) {
     if (!n) return cudaSuccess;
-    narrow_keys_kernel<<<blocks_for(n, 256), 256, 0, s>>>(keys, n, info, k32);
+    narrow_keys_kernel<<<blocks_for((n + 3) / 4, 256), 256, 0, s>>>(keys, n, info, k32);
     return cudaGetLastError();
 }
 
 cudaError_t launch_tie_fixup(const uint32_t* k32s, uint64_t n, const unsigned long long* keys, uint32_t* order,
                              cudaStream_t s) {
     if (n < 2) return cudaSuccess;
-    tie_fixup_kernel<<<blocks_for(n, 256), 256, 0, s>>>(k32s, n, keys, order);
+    tie_fixup_kernel<<<blocks_for((n + 3) / 4, 256), 256, 0, s>>>(k32s, n, keys, order);
     return cudaGetLastError();
 }
 
