@@ -496,8 +496,11 @@ void build_mask_bits(ss_ctx* c, Lane& L, cudaStream_t s, const ss_camera& cam, c
 // group's contraction (the shared sums are updated in view order).
 void flush_group(ss_ctx* c) {
     if (c->group.empty()) return;
-    cudaStream_t st = c->cstream; // in order: groups contract one after another
+    // in order: groups contract one after another on their own stream; with a
+    // single lane everything stays on that lane (serialised attribution pass)
+    cudaStream_t st = c->n_lanes > 1 ? c->cstream : c->group.back().lane->stream;
     for (auto& g : c->group) SS_CUDA(cudaStreamWaitEvent(st, g.lane->raster_done, 0));
+    if (c->n_lanes == 1 && c->group_done_valid) SS_CUDA(cudaStreamWaitEvent(st, c->group_done, 0));
     ContractParams q;
     std::memset(&q, 0, sizeof(q));
     q.n_members = (uint32_t)c->group.size();
