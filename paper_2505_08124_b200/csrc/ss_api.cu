@@ -612,6 +612,7 @@ void encode_batch(ss_ctx* c, uint32_t nviews, const ss_camera* cams, const ss_vi
     std::vector<ViewInfo> hstat(nviews);
     std::vector<uint32_t> todo(nviews);
     for (uint32_t v = 0; v < nviews; ++v) todo[v] = v;
+    uint64_t max_inst = 0; // largest tile-instance count of the views that fit
     for (int attempt = 0; attempt < 4 && !todo.empty(); ++attempt) {
         // lanes start after everything already queued on the user stream
         SS_CUDA(cudaEventRecord(c->ev_user, c->stream));
@@ -658,6 +659,7 @@ void encode_batch(ss_ctx* c, uint32_t nviews, const ss_camera* cams, const ss_vi
                 need = std::max<uint64_t>(need, st.n_instances);
                 continue;
             }
+            max_inst = std::max<uint64_t>(max_inst, st.n_instances);
             const double P = (double)cams[v].width * cams[v].height;
             const uint32_t M = masks ? masks[v].n_masks : 0;
             c->cnt_vis += st.n_surv;
@@ -675,6 +677,13 @@ void encode_batch(ss_ctx* c, uint32_t nviews, const ss_camera* cams, const ss_vi
         todo.swap(again);
     }
     if (!todo.empty()) throw Error(SS_ERR_CUDA, "tile-list buffer kept overflowing");
+    // the tile sort runs over the whole list capacity: track the views' actual
+    // sizes (+1/16; a view that overflows is re-run with a larger capacity)
+    if (max_inst) {
+        const uint64_t want = (max_inst + max_inst / 16 + 1023) / 1024 * 1024;
+        for (auto& L : c->lanes)
+            if (L.list_cap > want + want / 8) L.list_cap = want;
+    }
 }
 
 void profile_drain(ss_ctx* c) {
