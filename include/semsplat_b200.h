@@ -121,6 +121,15 @@ int ss_raster_capture(ss_ctx* ctx, const ss_camera* cam, int mode, uint64_t* n_e
  * splat_gid: n_splats, the depth-sorted, box-culled splat list
  * tile_offsets: tiles+1; tile_splats: n_tile_instances splat indices
  * (rasterizer.hpp:183-194 tile_bins, flattened). */
+/* rasterizer.hpp:261-264 rasterize: the capture above plus the rendered
+ * image.  Colors (scene.hpp:28, n x 3 RGB) are uploaded once per scene with
+ * ss_scene_set_color.  The WeightMap and alpha come from ss_raster_fetch; the
+ * image (row-major, 3 floats per pixel; black where the total weight is
+ * <= kRenderTotalEps) from ss_render_fetch_image. */
+int ss_scene_set_color(ss_ctx* ctx, const float* rgb, uint64_t n);
+int ss_render(ss_ctx* ctx, const ss_camera* raster_cam, int mode, uint64_t* n_entries, uint64_t* n_splats,
+              uint64_t* n_tile_instances);
+int ss_render_fetch_image(ss_ctx* ctx, float* rgb);
 int ss_raster_fetch(ss_ctx* ctx, ss_weight_entry* entries, float* per_pixel_total, float* alpha,
                     uint32_t* splat_gid, uint32_t* tile_offsets, uint32_t* tile_splats);
 

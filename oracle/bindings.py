@@ -304,6 +304,8 @@ class Ref:
         L.ssref_rasterize.argtypes = [C.c_void_p] * 5 + [C.c_uint64, C.POINTER(CCam), C.c_int, C.c_int,
                                                          C.POINTER(C.c_void_p), C.POINTER(C.c_uint64)]
         L.ssref_weightmap_fetch.argtypes = [C.c_void_p] * 4
+        L.ssref_image_fetch.argtypes = [C.c_void_p] * 2
+        L.ssref_image_fetch.restype = None
         L.ssref_weightmap_free.argtypes = [C.c_void_p]
         L.ssref_mask_weights.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p,
                                          C.c_void_p]
@@ -365,6 +367,9 @@ class Ref:
             out = {"entries": entries, "per_pixel_total": ppt}
             if full_render:
                 out["alpha"] = alpha
+                image = np.zeros(3 * P, np.float32)
+                self.L.ssref_image_fetch(h, _p(image))
+                out["image"] = image.reshape(int(cam.height), int(cam.width), 3)
             if masks is not None:
                 mw = []
                 for bits in masks:

@@ -132,6 +132,7 @@ void put_cam(const CameraPose& cam, ssref_camera* c) {
 struct WeightMapHandle {
     WeightMap wm;
     std::vector<float> alpha;
+    std::vector<float> image; // RenderResult::image.pixels (full_render)
 };
 
 } // namespace
@@ -186,6 +187,7 @@ int ssref_rasterize(const float* mean, const float* scale, const float* quat_xyz
             RenderResult r = rasterize(scene, c, wmode);
             h->wm = std::move(r.weights);
             h->alpha = std::move(r.alpha);
+            h->image = std::move(r.image.pixels);
         } else {
             h->wm = rasterize_weights_only(scene, c, wmode);
         }
@@ -201,6 +203,12 @@ void ssref_weightmap_fetch(void* handle, ssref_entry* entries, float* per_pixel_
     if (per_pixel_total)
         std::memcpy(per_pixel_total, h->wm.per_pixel_total.data(), h->wm.per_pixel_total.size() * sizeof(float));
     if (alpha && !h->alpha.empty()) std::memcpy(alpha, h->alpha.data(), h->alpha.size() * sizeof(float));
+}
+
+// RenderResult::image pixels (3 x width x height floats) of a full_render handle
+void ssref_image_fetch(void* handle, float* rgb) {
+    auto* h = static_cast<WeightMapHandle*>(handle);
+    if (rgb && !h->image.empty()) std::memcpy(rgb, h->image.data(), h->image.size() * sizeof(float));
 }
 
 void ssref_weightmap_free(void* handle) { delete static_cast<WeightMapHandle*>(handle); }

@@ -71,6 +71,9 @@ def lib() -> C.CDLL:
         "ss_synchronize": (i32, [vp]),
         "ss_set_option": (i32, [vp, i32, C.c_int64]),
         "ss_query_stats": (i32, [vp, vp]),
+        "ss_scene_set_color": (i32, [vp, vp, u64]),
+        "ss_render": (i32, [vp, C.POINTER(Camera), i32, pu64, pu64, pu64]),
+        "ss_render_fetch_image": (i32, [vp, vp]),
         "ss_scene_set": (i32, [vp, pf, pf, pf, pf, u64]),
         "ss_project": (i32, [vp, C.POINTER(Camera), vp]),
         "ss_raster_capture": (i32, [vp, C.POINTER(Camera), i32, pu64, pu64, pu64]),
@@ -180,10 +183,23 @@ class Context:
         check(self._L.ss_project(self.h, C.byref(c), out.ctypes.data_as(C.c_void_p)))
         return out
 
-    def raster_capture(self, cam, mode: int = 0):
+    def set_scene_color(self, rgb):
+        rgb = np.ascontiguousarray(rgb, np.float32).reshape(-1, 3)
+        check(self._L.ss_scene_set_color(self.h, rgb.ctypes.data_as(C.c_void_p), rgb.shape[0]))
+
+    def render(self, cam, mode: int = 0):
+        """rasterize (rasterizer.hpp:261): the capture dict plus "image" [H, W, 3]."""
+        out = self.raster_capture(cam, mode, _render=True)
+        img = np.zeros((int(cam.height), int(cam.width), 3), np.float32)
+        check(self._L.ss_render_fetch_image(self.h, img.ctypes.data_as(C.c_void_p)))
+        out["image"] = img
+        return out
+
+    def raster_capture(self, cam, mode: int = 0, _render: bool = False):
         c = camera_struct(cam)
         ne, ns, ni = C.c_uint64(), C.c_uint64(), C.c_uint64()
-        check(self._L.ss_raster_capture(self.h, C.byref(c), int(mode), C.byref(ne), C.byref(ns), C.byref(ni)))
+        fn = self._L.ss_render if _render else self._L.ss_raster_capture
+        check(fn(self.h, C.byref(c), int(mode), C.byref(ne), C.byref(ns), C.byref(ni)))
         P = int(cam.width) * int(cam.height)
         tiles = ((int(cam.width) + 15) // 16) * ((int(cam.height) + 15) // 16)
         entries = np.zeros(ne.value, ENTRY_DTYPE)

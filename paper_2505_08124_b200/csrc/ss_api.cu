@@ -205,8 +205,10 @@ struct ss_ctx {
     ss::ViewInfo* h_init = nullptr;    // pinned
     uint32_t* h_u32 = nullptr;         // pinned scratch
 
-    // capture
-    ss::DevBuf pix_count, pix_offset, entries, per_pixel_total, alpha;
+    // capture / render
+    ss::DevBuf pix_count, pix_offset, entries, per_pixel_total, alpha, color, image;
+    bool color_ok = false;     // colors uploaded for the current scene
+    bool cap_image = false;    // the last capture rendered an image
     uint64_t cap_entries = 0, cap_splats = 0, cap_instances = 0;
     uint32_t cap_width = 0, cap_height = 0, cap_tiles = 0;
     ss::DevBuf counters; // [0] G_v sum, [1] K_v sum
@@ -760,7 +762,7 @@ void ss_destroy(ss_ctx* c) {
     for (auto& L : c->lanes) cudaStreamSynchronize(L.stream);
     if (c->cstream) cudaStreamSynchronize(c->cstream);
     ss::DevBuf* bufs[] = {&c->mean_op, &c->scale, &c->quat, &c->cub_tmp, &c->num_sel, &c->info, &c->vstat, &c->pix_count,
-                          &c->pix_offset, &c->entries, &c->per_pixel_total, &c->alpha, &c->counters, &c->sums_buf,
+                          &c->pix_offset, &c->entries, &c->per_pixel_total, &c->alpha, &c->color, &c->image, &c->counters, &c->sums_buf,
                           &c->totals_buf, &c->store_rows, &c->store_ids, &c->qbuf, &c->qnorm, &c->scores,
                           &c->topk_ids, &c->topk_sims, &c->sel_flags, &c->thr_keys, &c->thr_keys_sorted, &c->thr_ids,
                           &c->thr_ids_sorted, &c->zero_flag, &c->store_half, &c->qhalf, &c->tc_scores, &c->tc_thr,
@@ -838,6 +840,7 @@ int ss_scene_set(ss_ctx* c, const float* mean, const float* scale, const float* 
             for (int i = 0; i < 4; ++i) q[4 * k + i] = quat_xyzw[4 * k + i];
         }
         c->n = n;
+        c->color_ok = false;
         const size_t bytes = std::max<uint64_t>(n, 1) * 16;
         SS_CUDA(cudaMemcpyAsync(c->mean_op.ensure(bytes), a.data(), n * 16, cudaMemcpyHostToDevice, c->stream));
         SS_CUDA(cudaMemcpyAsync(c->scale.ensure(bytes), b.data(), n * 16, cudaMemcpyHostToDevice, c->stream));
@@ -876,69 +879,119 @@ int ss_project(ss_ctx* c, const ss_camera* cam, ss_projected* out) {
     });
 }
 
+namespace {
+// rasterize_weights_only (rasterizer.hpp:268-271) or, with color, rasterize
+// (rasterizer.hpp:261-264): tile lists, then the counting and capture passes
+// of the compositor (the capture pass also forms the normalised pixel colors).
+void capture_view(ss_ctx* c, const ss_camera* cam, int mode, bool color, uint64_t* n_entries, uint64_t* n_splats,
+                  uint64_t* n_tile_instances) {
+    check_camera(cam);
+    set_device(c);
+    cudaStream_t s = c->stream;
+    const uint64_t P = (uint64_t)cam->width * cam->height;
+    const uint64_t N = c->n;
+    ss::Lane& L = c->lanes[0];
+    Geometry g;
+    for (int attempt = 0;; ++attempt) {
+        g = run_geometry(c, L, s, *cam);
+        SS_CUDA(cudaMemcpyAsync(L.h_info, L.info.p, sizeof(ViewInfo), cudaMemcpyDeviceToHost, s));
+        SS_CUDA(cudaStreamSynchronize(s));
+        if (!L.h_info->overflow) break;
+        if (attempt > 2) throw Error(SS_ERR_CUDA, "tile-list buffer kept overflowing");
+        L.list_cap = L.h_info->n_instances + L.h_info->n_instances / 16;
+    }
+    if (L.h_info->err_count)
+        throw Error(SS_ERR_NUMERIC, "singular screen covariance for gaussian " + std::to_string(L.h_info->err_gid));
+    const uint64_t n_surv = L.h_info->n_surv, n_inst = L.h_info->n_instances;
+    auto* cnt = static_cast<uint32_t*>(c->pix_count.ensure((P + 1) * 4));
+    auto* off = static_cast<uint32_t*>(c->pix_offset.ensure((P + 1) * 4));
+    auto* ppt = static_cast<float*>(c->per_pixel_total.ensure(P * 4));
+    auto* alp = static_cast<float*>(c->alpha.ensure(P * 4));
+    SS_CUDA(cudaMemsetAsync(cnt, 0, (P + 1) * 4, s));
+    SS_CUDA(cudaMemsetAsync(ppt, 0, P * 4, s));
+    SS_CUDA(cudaMemsetAsync(alp, 0, P * 4, s));
+    RasterParams p = raster_params(c, L, *cam, g);
+    if (n_surv) {
+        p.pix_count = cnt;
+        own_launch(c, launch_raster_count(p, mode, g.tiles, s), SS_K_RASTER);
+    }
+    size_t tb = 0;
+    SS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, (int)(P + 1), s));
+    void* tmp = c->cub_tmp.ensure(tb);
+    tb = c->cub_tmp.bytes;
+    SS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, off, (int)(P + 1), s));
+    c->launches_cub += 1;
+    SS_CUDA(cudaMemcpyAsync(c->h_u32, off + P, 4, cudaMemcpyDeviceToHost, s));
+    SS_CUDA(cudaStreamSynchronize(s));
+    const uint64_t E = c->h_u32[0];
+    auto* ent = static_cast<ss_weight_entry*>(c->entries.ensure(std::max<uint64_t>(E, 1) * sizeof(ss_weight_entry)));
+    if (color) {
+        auto* img = static_cast<float*>(c->image.ensure(std::max<uint64_t>(P, 1) * 12));
+        SS_CUDA(cudaMemsetAsync(img, 0, P * 12, s));
+        p.color = c->color.as<float4>();
+        p.image = img;
+    }
+    if (n_surv) {
+        p.pix_offset = off;
+        p.entries = ent;
+        p.per_pixel_total = ppt;
+        p.alpha = alp;
+        own_launch(c, color ? launch_raster_render(p, mode, g.tiles, s) : launch_raster_capture(p, mode, g.tiles, s),
+                   SS_K_RASTER);
+    }
+    SS_CUDA(cudaStreamSynchronize(s));
+    c->cap_entries = E;
+    c->cap_splats = n_surv;
+    c->cap_instances = n_inst;
+    c->cap_width = cam->width;
+    c->cap_height = cam->height;
+    c->cap_tiles = g.tiles;
+    c->cap_image = color;
+    if (n_entries) *n_entries = E;
+    if (n_splats) *n_splats = n_surv;
+    if (n_tile_instances) *n_tile_instances = n_inst;
+}
+} // namespace
+
 int ss_raster_capture(ss_ctx* c, const ss_camera* cam, int mode, uint64_t* n_entries, uint64_t* n_splats,
                       uint64_t* n_tile_instances) {
     return guarded([&] {
         if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
-        check_camera(cam);
+        capture_view(c, cam, mode, false, n_entries, n_splats, n_tile_instances);
+    });
+}
+
+int ss_scene_set_color(ss_ctx* c, const float* rgb, uint64_t n) {
+    return guarded([&] {
+        if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
+        if (n != c->n) throw Error(SS_ERR_CONTRACT, "ss_scene_set_color: count differs from the scene");
         set_device(c);
-        cudaStream_t s = c->stream;
-        const uint64_t P = (uint64_t)cam->width * cam->height;
-        const uint64_t N = c->n;
-        ss::Lane& L = c->lanes[0];
-        // rasterize_weights_only (rasterizer.hpp:268-271): tile lists, then the
-        // counting and capture passes of the compositor
-        Geometry g;
-        for (int attempt = 0;; ++attempt) {
-            g = run_geometry(c, L, s, *cam);
-            SS_CUDA(cudaMemcpyAsync(L.h_info, L.info.p, sizeof(ViewInfo), cudaMemcpyDeviceToHost, s));
-            SS_CUDA(cudaStreamSynchronize(s));
-            if (!L.h_info->overflow) break;
-            if (attempt > 2) throw Error(SS_ERR_CUDA, "tile-list buffer kept overflowing");
-            L.list_cap = L.h_info->n_instances + L.h_info->n_instances / 16;
-        }
-        if (L.h_info->err_count)
-            throw Error(SS_ERR_NUMERIC, "singular screen covariance for gaussian " + std::to_string(L.h_info->err_gid));
-        const uint64_t n_surv = L.h_info->n_surv, n_inst = L.h_info->n_instances;
-        auto* cnt = static_cast<uint32_t*>(c->pix_count.ensure((P + 1) * 4));
-        auto* off = static_cast<uint32_t*>(c->pix_offset.ensure((P + 1) * 4));
-        auto* ppt = static_cast<float*>(c->per_pixel_total.ensure(P * 4));
-        auto* alp = static_cast<float*>(c->alpha.ensure(P * 4));
-        SS_CUDA(cudaMemsetAsync(cnt, 0, (P + 1) * 4, s));
-        SS_CUDA(cudaMemsetAsync(ppt, 0, P * 4, s));
-        SS_CUDA(cudaMemsetAsync(alp, 0, P * 4, s));
-        RasterParams p = raster_params(c, L, *cam, g);
-        if (n_surv) {
-            p.pix_count = cnt;
-            own_launch(c, launch_raster_count(p, mode, g.tiles, s), SS_K_RASTER);
-        }
-        size_t tb = 0;
-        SS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, (int)(P + 1), s));
-        void* tmp = c->cub_tmp.ensure(tb);
-        tb = c->cub_tmp.bytes;
-        SS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, off, (int)(P + 1), s));
-        c->launches_cub += 1;
-        SS_CUDA(cudaMemcpyAsync(c->h_u32, off + P, 4, cudaMemcpyDeviceToHost, s));
-        SS_CUDA(cudaStreamSynchronize(s));
-        const uint64_t E = c->h_u32[0];
-        auto* ent = static_cast<ss_weight_entry*>(c->entries.ensure(std::max<uint64_t>(E, 1) * sizeof(ss_weight_entry)));
-        if (n_surv) {
-            p.pix_offset = off;
-            p.entries = ent;
-            p.per_pixel_total = ppt;
-            p.alpha = alp;
-            own_launch(c, launch_raster_capture(p, mode, g.tiles, s), SS_K_RASTER);
-        }
-        SS_CUDA(cudaStreamSynchronize(s));
-        c->cap_entries = E;
-        c->cap_splats = n_surv;
-        c->cap_instances = n_inst;
-        c->cap_width = cam->width;
-        c->cap_height = cam->height;
-        c->cap_tiles = g.tiles;
-        if (n_entries) *n_entries = E;
-        if (n_splats) *n_splats = n_surv;
-        if (n_tile_instances) *n_tile_instances = n_inst;
+        std::vector<float> a(std::max<uint64_t>(n, 1) * 4, 0.0f);
+        for (uint64_t k = 0; k < n; ++k)
+            for (int i = 0; i < 3; ++i) a[4 * k + i] = rgb[3 * k + i];
+        SS_CUDA(cudaMemcpyAsync(c->color.ensure(std::max<uint64_t>(n, 1) * 16), a.data(), n * 16,
+                                cudaMemcpyHostToDevice, c->stream));
+        SS_CUDA(cudaStreamSynchronize(c->stream));
+        c->color_ok = true;
+    });
+}
+
+int ss_render(ss_ctx* c, const ss_camera* cam, int mode, uint64_t* n_entries, uint64_t* n_splats,
+              uint64_t* n_tile_instances) {
+    return guarded([&] {
+        if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
+        if (!c->color_ok && c->n) throw Error(SS_ERR_CONTRACT, "ss_render: scene colors not set (ss_scene_set_color)");
+        capture_view(c, cam, mode, true, n_entries, n_splats, n_tile_instances);
+    });
+}
+
+int ss_render_fetch_image(ss_ctx* c, float* rgb) {
+    return guarded([&] {
+        if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
+        if (!c->cap_image) throw Error(SS_ERR_CONTRACT, "ss_render_fetch_image: the last capture was not a render");
+        set_device(c);
+        const uint64_t P = (uint64_t)c->cap_width * c->cap_height;
+        if (P) SS_CUDA(cudaMemcpy(rgb, c->image.p, P * 12, cudaMemcpyDeviceToHost));
     });
 }
 

@@ -372,7 +372,8 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
     ps.count = 0;
     ps.out = 0;
     ps.done = !ps.inside;
-    if constexpr (KIND == 1) {
+    double csum[3] = {0.0, 0.0, 0.0}; // render (KIND 3): color_sum, rasterizer.hpp:224
+    if constexpr (KIND == 1 || KIND == 3) {
         if (ps.inside) ps.out = p.pix_offset[ps.pixel];
     }
     uint32_t bits[MW];
@@ -440,10 +441,17 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
             if ((mj & lane_bit) && !ps.done) c = composite_one<FALLOFF>(ps, s, stab, wf);
             if constexpr (KIND == 0) {
                 ps.count += c ? 1u : 0u;
-            } else if constexpr (KIND == 1) {
+            } else if constexpr (KIND == 1 || KIND == 3) {
                 if (c) {
                     p.entries[ps.out++] = ss_weight_entry{gj, ps.pixel, wf};
                     ps.total = da(ps.total, (double)wf);
+                    if constexpr (KIND == 3) {
+                        // color_sum += double(wf) * color (rasterizer.hpp:231), per component
+                        const float4 col = __ldg(p.color + gj);
+                        csum[0] = da(csum[0], dm((double)wf, (double)col.x));
+                        csum[1] = da(csum[1], dm((double)wf, (double)col.y));
+                        csum[2] = da(csum[2], dm((double)wf, (double)col.z));
+                    }
                 }
             } else {
                 gate_and_accumulate<MW>(p, c, wf, grp, bits, gj, lane);
@@ -455,9 +463,17 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
     if (ps.inside) {
         if constexpr (KIND == 0) {
             p.pix_count[ps.pixel] = ps.count;
-        } else if constexpr (KIND == 1) {
+        } else if constexpr (KIND == 1 || KIND == 3) {
             p.per_pixel_total[ps.pixel] = __double2float_rn(ps.total);
             p.alpha[ps.pixel] = __double2float_rn(ds(1.0, ps.T));
+            if constexpr (KIND == 3) {
+                // rasterizer.hpp:236-243: normalised color, background kept below kRenderTotalEps
+                if (ps.total > 1e-6) {
+#pragma unroll
+                    for (int k = 0; k < 3; ++k)
+                        p.image[3ull * ps.pixel + k] = __double2float_rn(dd(csum[k], ps.total));
+                }
+            }
         }
     }
 }
@@ -486,6 +502,9 @@ cudaError_t launch_raster_count(const RasterParams& p, int mode, uint32_t tiles,
 }
 cudaError_t launch_raster_capture(const RasterParams& p, int mode, uint32_t tiles, cudaStream_t s) {
     return launch_raster<1>(p, mode, tiles, s);
+}
+cudaError_t launch_raster_render(const RasterParams& p, int mode, uint32_t tiles, cudaStream_t s) {
+    return launch_raster<3>(p, mode, tiles, s);
 }
 
 cudaError_t launch_raster_fused(const RasterParams& p, int mode, uint32_t tiles, cudaStream_t s) {

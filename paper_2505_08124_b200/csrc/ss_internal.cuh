@@ -67,6 +67,8 @@ struct RasterParams {
     ss_weight_entry* entries;      // pass 1 output
     float* per_pixel_total;        // pass 1 output [P]
     float* alpha;                  // pass 1 output [P]
+    const float4* color;           // render: Gaussian colors (r, g, b, -) by id
+    float* image;                  // render output [P * 3], zero where no weight
     // fused mode
     const uint32_t* pix_bits;      // [P * mask_words]
     uint32_t mask_words, n_masks;
@@ -82,6 +84,7 @@ struct RasterParams {
 cudaError_t launch_project(const ProjectParams& p, cudaStream_t s);
 cudaError_t launch_raster_count(const RasterParams& p, int mode, uint32_t tiles, cudaStream_t s);
 cudaError_t launch_raster_capture(const RasterParams& p, int mode, uint32_t tiles, cudaStream_t s);
+cudaError_t launch_raster_render(const RasterParams& p, int mode, uint32_t tiles, cudaStream_t s);
 cudaError_t launch_raster_fused(const RasterParams& p, int mode, uint32_t tiles, cudaStream_t s);
 
 } // namespace ss

@@ -379,3 +379,38 @@ def test_query_threshold_tensor_core_overflow_falls_back(gpu_ctx, oracle):
     finally:
         gpu_ctx.set_query_path(0)
 
+
+def test_render_bitwise_vs_reference_golden(gpu_ctx):
+    """rasterize (rasterizer.hpp:261-264): image, alpha, WeightMap and totals
+    bit-identical to the reference build's RenderResult (golden_render.npz)."""
+    z = golden("render")
+    for i in range(int(z["n"])):
+        s = g_scene(z, i)
+        mode = int(z[f"mode_{i}"])
+        gpu_ctx.set_scene(s.mean, s.scale, s.quat_xyzw, s.opacity)
+        gpu_ctx.set_scene_color(z[f"color_{i}"])
+        got = gpu_ctx.render(g_cams(z, i)[0], mode)
+        assert got["image"].tobytes() == z[f"image_{i}"].tobytes(), i
+        exp = {"entries": z[f"entries_{i}"], "per_pixel_total": z[f"ppt_{i}"], "alpha": z[f"alpha_{i}"]}
+        _assert_capture_equal(got, exp, mode)
+
+
+@pytest.mark.parametrize("seed,n,w,h,dist,mode", [(21, 600, 72, 60, 7.0, 0), (22, 800, 120, 90, 8.0, 1)])
+def test_render_bitwise_vs_reference_live(gpu_ctx, ref, seed, n, w, h, dist, mode):
+    s = random_scene(n, seed)
+    cam = make_test_camera(w, h, dist)
+    gpu_ctx.set_scene(s.mean, s.scale, s.quat_xyzw, s.opacity)
+    gpu_ctx.set_scene_color(s.color)
+    got = gpu_ctx.render(cam, mode)
+    exp = ref.rasterize(s, cam, mode, full_render=True)
+    assert got["image"].tobytes() == exp["image"].tobytes()
+    _assert_capture_equal(got, exp, mode)
+
+
+def test_render_requires_colors(gpu_ctx):
+    from paper_2505_08124_b200 import ContractError
+    s = random_scene(50, 23)
+    gpu_ctx.set_scene(s.mean, s.scale, s.quat_xyzw, s.opacity)
+    with pytest.raises(ContractError):
+        gpu_ctx.render(make_test_camera(32, 32, 7.0))
+
