@@ -7,6 +7,7 @@
 //
 //   semsplat::encode_scene(...)            pipeline.hpp:280   -> b200::encode_scene
 //   semsplat::rasterize_weights_only(...)  rasterizer.hpp:268 -> b200::rasterize_weights_only
+//   semsplat::rasterize(...)               rasterizer.hpp:261 -> b200::rasterize
 //   semsplat::project_gaussian(...)        projection.hpp:33  -> b200::project_all (batch)
 //   semsplat::build_store(...)             vecstore.hpp:88    -> b200::build_store
 //   semsplat::query_topk(...)              vecstore.hpp:121   -> b200::query_topk
@@ -80,6 +81,14 @@ public:
         }
         check(ss_scene_set(ctx_, mean.data(), scale.data(), quat.data(), op.data(), n));
     }
+    // Colors for rasterize (scene.hpp:28), after bind().
+    void bind_color(const GaussianScene& scene) {
+        const size_t n = scene.size();
+        std::vector<float> rgb(3 * n);
+        for (size_t k = 0; k < n; ++k)
+            for (int i = 0; i < 3; ++i) rgb[3 * k + i] = scene[k].color[i];
+        check(ss_scene_set_color(ctx_, rgb.data(), n));
+    }
     ~Device() { ss_destroy(ctx_); }
 
 private:
@@ -123,6 +132,35 @@ inline WeightMap rasterize_weights_only(const GaussianScene& scene, const Camera
     wm.entries.resize(ne);
     for (size_t i = 0; i < ne; ++i) wm.entries[i] = {e[i].gaussian_id, e[i].pixel, e[i].weight};
     return wm;
+}
+
+// rasterizer.hpp:261-264: image, WeightMap and alpha, bit-identical to the
+// reference's RenderResult
+inline RenderResult rasterize(const GaussianScene& scene, const CameraPose& cam,
+                              WeightMode mode = WeightMode::kAlphaComposited, int device = 0) {
+    Device& d = Device::get(device);
+    std::lock_guard<std::mutex> lock(d.mutex());
+    d.bind(scene);
+    d.bind_color(scene);
+    const ss_camera c = to_c(cam);
+    uint64_t ne = 0, ns = 0, ni = 0;
+    check(ss_render(d.ctx(), &c, mode == WeightMode::kFalloffOnly ? SS_FALLOFF_ONLY : SS_ALPHA_COMPOSITED, &ne, &ns,
+                    &ni));
+    RenderResult out;
+    out.image = ImageRGB(cam.image_id, cam.width, cam.height);
+    out.weights.image_id = cam.image_id;
+    out.weights.width = cam.width;
+    out.weights.height = cam.height;
+    const size_t P = static_cast<size_t>(cam.width) * cam.height;
+    out.weights.per_pixel_total.assign(P, 0.0f);
+    out.alpha.assign(P, 0.0f);
+    std::vector<ss_weight_entry> e(ne);
+    check(ss_raster_fetch(d.ctx(), e.data(), out.weights.per_pixel_total.data(), out.alpha.data(), nullptr, nullptr,
+                          nullptr));
+    check(ss_render_fetch_image(d.ctx(), out.image.pixels.data()));
+    out.weights.entries.resize(ne);
+    for (size_t i = 0; i < ne; ++i) out.weights.entries[i] = {e[i].gaussian_id, e[i].pixel, e[i].weight};
+    return out;
 }
 
 // projection.hpp:33-55 for every Gaussian of the scene

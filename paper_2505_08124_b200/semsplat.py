@@ -60,6 +60,15 @@ class WeightMap:
 
 
 @dataclass
+class RenderResult:
+    """RenderResult (rasterizer.hpp:55-59): RGB image [H, W, 3] (black where the
+    total weight is <= kRenderTotalEps), WeightMap and per-pixel alpha."""
+    image: np.ndarray
+    weights: WeightMap
+    alpha: np.ndarray
+
+
+@dataclass
 class EmbeddingTable:
     """EmbeddingTable (pipeline.hpp:103-116)."""
     embeddings: np.ndarray  # N x D f32
@@ -144,6 +153,18 @@ def rasterize_weights_only(scene: GaussianScene, cam: CameraPose, mode: int = AL
     cap = ctx.raster_capture(cam, mode)
     wm = WeightMap(int(cam.image_id), int(cam.width), int(cam.height), cap["entries"], cap["per_pixel_total"])
     return (wm, cap) if with_binning else wm
+
+
+def rasterize(scene: GaussianScene, cam: CameraPose, mode: int = ALPHA_COMPOSITED, device: int = 0) -> RenderResult:
+    """rasterizer.hpp:261-264 on the device; needs scene.color (N x 3)."""
+    if scene.color is None:
+        raise ContractError("rasterize: the scene has no colors")
+    ctx = device_context(device)
+    _bind_scene(ctx, scene)
+    ctx.set_scene_color(scene.color)
+    r = ctx.render(cam, mode)
+    wm = WeightMap(int(cam.image_id), int(cam.width), int(cam.height), r["entries"], r["per_pixel_total"])
+    return RenderResult(r["image"], wm, r["alpha"])
 
 
 def encode_scene(scene: GaussianScene, manifest: DatasetManifest, workers: int, chunk_rows: int,

@@ -88,6 +88,13 @@ int main() {
                       r.cov_xy == pa[k].cov_xy && r.cov_yy == pa[k].cov_yy && r.depth == pa[k].depth;
         }
         CHECK(pok);
+        // rasterize (rasterizer.hpp:261): RenderResult image, alpha and WeightMap bit-identical
+        const RenderResult ra = rasterize(scene, cam);
+        const RenderResult rb = b200::rasterize(scene, cam);
+        CHECK(ra.image.pixels == rb.image.pixels);
+        CHECK(ra.alpha == rb.alpha);
+        CHECK(ra.weights.entries.size() == rb.weights.entries.size());
+        CHECK(ra.weights.per_pixel_total == rb.weights.per_pixel_total);
     }
 
     // --- encode_scene vs the reference on its own fixtures (test_pipeline.cpp:283-354)

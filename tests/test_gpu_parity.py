@@ -414,3 +414,17 @@ def test_render_requires_colors(gpu_ctx):
     with pytest.raises(ContractError):
         gpu_ctx.render(make_test_camera(32, 32, 7.0))
 
+
+def test_render_through_the_reference_shaped_api(gpu_ctx, ref):
+    """semsplat.rasterize (the Python mirror of rasterizer.hpp:261) returns a
+    RenderResult equal to the reference's."""
+    from paper_2505_08124_b200.semsplat import GaussianScene, rasterize
+    s = random_scene(500, 24)
+    scene = GaussianScene(s.mean, s.scale, s.quat_xyzw, s.opacity, s.color)
+    cam = make_test_camera(70, 50, 7.5)
+    r = rasterize(scene, cam)
+    exp = ref.rasterize(s, cam, 0, full_render=True)
+    assert r.image.tobytes() == exp["image"].tobytes()
+    assert r.alpha.tobytes() == exp["alpha"].tobytes()
+    assert r.weights.entries.tobytes() == exp["entries"].tobytes()
+
