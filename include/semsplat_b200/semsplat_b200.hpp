@@ -12,6 +12,8 @@
 //   semsplat::build_store(...)             vecstore.hpp:88    -> b200::build_store
 //   semsplat::query_topk(...)              vecstore.hpp:121   -> b200::query_topk
 //   semsplat::query_threshold(...)         vecstore.hpp:135   -> b200::query_threshold
+//   semsplat::run_query(...)               query.hpp:102     -> b200::run_query
+//   (device store -> host VectorStore for partition_store / snapshots: b200::fetch_store)
 //
 // All compute runs in the sm_100a kernels behind the C ABI
 // (include/semsplat_b200.h); this header only marshals the reference's types.
@@ -21,11 +23,13 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../semsplat_b200.h"
 #include "semsplat/pipeline.hpp"
 #include "semsplat/providers.hpp"
+#include "semsplat/query.hpp"
 #include "semsplat/vecstore.hpp"
 
 namespace semsplat {
@@ -304,12 +308,14 @@ inline EmbeddingTable encode_scene(const GaussianScene& scene, const DatasetMani
     return table;
 }
 
-// A device-resident VectorStore: ids + unit rows (payloads stay on the host
-// side in the caller's scene).
+// A device-resident VectorStore: ids + unit rows on the device; the records'
+// payloads (the scene's Gaussians, in the store's record order) on the host.
 struct DeviceStore {
     int device = 0;
     uint64_t count = 0;
     uint32_t dim = 0;
+    std::vector<uint32_t> ids;          // record order (= device order)
+    std::vector<Gaussian3D> payloads;   // record order
 };
 
 // vecstore.hpp:88-103
@@ -320,7 +326,12 @@ inline DeviceStore build_store(const EmbeddingTable& table, const GaussianScene&
     uint64_t cnt = 0;
     check(ss_store_build(d.ctx(), table.embeddings.data(), table.coverage.data(), table.gaussian_count, table.dim,
                          &cnt));
-    return DeviceStore{device, cnt, table.dim};
+    DeviceStore st{device, cnt, table.dim, {}, {}};
+    st.ids.resize(cnt);
+    if (cnt) check(ss_store_fetch(d.ctx(), st.ids.data(), nullptr));
+    st.payloads.reserve(cnt);
+    for (uint32_t id : st.ids) st.payloads.push_back(scene[id]);
+    return st;
 }
 
 inline DeviceStore upload_store(const VectorStore& store, int device = 0) {
@@ -330,7 +341,27 @@ inline DeviceStore upload_store(const VectorStore& store, int device = 0) {
     for (size_t i = 0; i < store.count(); ++i)
         std::memcpy(rows.data() + i * store.dim(), store.vector_at(i), store.dim() * sizeof(float));
     check(ss_store_set(d.ctx(), store.ids().data(), rows.data(), store.count(), store.dim()));
-    return DeviceStore{device, store.count(), store.dim()};
+    DeviceStore st{device, store.count(), store.dim(), store.ids(), {}};
+    st.payloads.reserve(store.count());
+    for (size_t i = 0; i < store.count(); ++i) st.payloads.push_back(store.payload_at(i));
+    return st;
+}
+
+// The device store as the reference's host VectorStore (ids, unit rows,
+// payloads in record order), e.g. for partition_store / save_snapshot
+// (vecstore.hpp:160-328), which run on the host in the reference too.
+inline VectorStore fetch_store(const DeviceStore& store) {
+    Device& d = Device::get(store.device);
+    std::lock_guard<std::mutex> lock(d.mutex());
+    std::vector<uint32_t> ids(store.count);
+    std::vector<float> rows(store.count * store.dim);
+    if (store.count) check(ss_store_fetch(d.ctx(), ids.data(), rows.data()));
+    VectorStore out(store.dim);
+    out.reserve(store.count);
+    for (size_t i = 0; i < store.count; ++i)
+        out.add_record(ids[i], std::vector<float>(rows.begin() + i * store.dim, rows.begin() + (i + 1) * store.dim),
+                       store.payloads.size() == store.count ? store.payloads[i] : Gaussian3D{});
+    return out;
 }
 
 // vecstore.hpp:121-132
@@ -362,6 +393,51 @@ inline std::vector<ScoredId> query_threshold(const DeviceStore& store, const std
     std::vector<ScoredId> out(cnt);
     for (size_t i = 0; i < cnt; ++i) out[i] = {ids[i], sims[i]};
     return out;
+}
+
+// Batched query_topk: row q of the result is query_topk(store, queries[q], k)
+// (the device answers the whole batch in one pass).
+inline std::vector<std::vector<ScoredId>> query_topk_batch(const DeviceStore& store,
+                                                           const std::vector<std::vector<float>>& queries, size_t k) {
+    std::vector<std::vector<ScoredId>> out(queries.size());
+    if (k == 0 || store.count == 0 || queries.empty()) return out;
+    std::vector<float> q(queries.size() * store.dim);
+    for (size_t i = 0; i < queries.size(); ++i) {
+        if (queries[i].size() != store.dim) throw ContractError("query dimension differs from store dimension");
+        std::memcpy(q.data() + i * store.dim, queries[i].data(), store.dim * sizeof(float));
+    }
+    Device& d = Device::get(store.device);
+    std::lock_guard<std::mutex> lock(d.mutex());
+    std::vector<uint32_t> ids(queries.size() * k);
+    std::vector<float> sims(queries.size() * k);
+    std::vector<uint64_t> cnt(queries.size());
+    check(ss_query_topk(d.ctx(), q.data(), static_cast<uint32_t>(queries.size()), static_cast<uint32_t>(k), ids.data(),
+                        sims.data(), cnt.data()));
+    for (size_t i = 0; i < queries.size(); ++i) {
+        out[i].resize(cnt[i]);
+        for (size_t j = 0; j < cnt[i]; ++j) out[i][j] = {ids[i * k + j], sims[i * k + j]};
+    }
+    return out;
+}
+
+// query.hpp:102-122: encode_text + store search + payload assembly.
+inline QueryResult run_query(const DeviceStore& store, const std::string& text, const QueryMode& mode,
+                             const TextProvider& provider) {
+    QueryResult result;
+    result.text = text;
+    result.mode = mode;
+    result.query_vector = encode_text(text, provider);
+    std::vector<ScoredId> scored;
+    if (store.count > 0)
+        scored = (mode.kind == QueryMode::Kind::kTopK) ? query_topk(store, result.query_vector, mode.k)
+                                                       : query_threshold(store, result.query_vector, mode.tau);
+    std::unordered_map<uint32_t, size_t> index_by_id;
+    index_by_id.reserve(store.ids.size());
+    for (size_t i = 0; i < store.ids.size(); ++i) index_by_id[store.ids[i]] = i;
+    result.matches.reserve(scored.size());
+    for (const ScoredId& sc : scored)
+        result.matches.push_back({sc.gaussian_id, sc.similarity, store.payloads.at(index_by_id.at(sc.gaussian_id))});
+    return result;
 }
 
 } // namespace b200

@@ -1220,6 +1220,44 @@ void topk_exact(ss_ctx* c, const float* d_qn, uint32_t nq, uint32_t k, uint32_t*
     }
 }
 
+// k beyond the top-k kernels' 64: every record's exact score, a full radix
+// sort of the (sim desc, id asc) keys, the first k (vecstore.hpp:121-132).
+void topk_sorted(ss_ctx* c, const float* d_qn, uint32_t nq, uint32_t k, uint32_t* oid, float* osim) {
+    cudaStream_t s = c->stream;
+    const uint64_t count = c->store_count;
+    const uint64_t take = std::min<uint64_t>(k, count);
+    auto* sc_buf = static_cast<float*>(c->scores.ensure(count * 4));
+    auto* keys = static_cast<unsigned long long*>(c->thr_keys.ensure(count * 8));
+    auto* ksorted = static_cast<unsigned long long*>(c->thr_keys_sorted.ensure(count * 8));
+    auto* flags = static_cast<uint8_t*>(c->sel_flags.ensure(count));
+    size_t tb = 0;
+    SS_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys, ksorted, (int)count, 0, 64, s));
+    void* tmp = c->cub_tmp.ensure(tb);
+    tb = c->cub_tmp.bytes;
+    std::vector<unsigned long long> hk(take);
+    for (uint32_t q = 0; q < nq; ++q) {
+        own_launch(c, launch_score(c->store_rows.as<float>(), count, c->store_dim, d_qn, q + 1, q, sc_buf, s),
+                   SS_K_QUERY);
+        own_launch(c, launch_threshold_keys(sc_buf, c->store_ids.as<uint32_t>(), count, -INFINITY, keys, flags, s),
+                   SS_K_QUERY);
+        SS_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, keys, ksorted, (int)count, 0, 64, s));
+        c->launches_cub += 1;
+        SS_CUDA(cudaMemcpyAsync(hk.data(), ksorted, take * 8, cudaMemcpyDeviceToHost, s));
+        SS_CUDA(cudaStreamSynchronize(s));
+        std::vector<uint32_t> ids(take);
+        std::vector<float> sims(take);
+        for (uint64_t i = 0; i < take; ++i) {
+            ids[i] = (uint32_t)(hk[i] & 0xffffffffu);
+            uint32_t b = ~(uint32_t)(hk[i] >> 32);
+            b = (b & 0x80000000u) ? (b & 0x7fffffffu) : ~b;
+            std::memcpy(&sims[i], &b, 4);
+        }
+        SS_CUDA(cudaMemcpyAsync(oid + (uint64_t)q * k, ids.data(), take * 4, cudaMemcpyHostToDevice, s));
+        SS_CUDA(cudaMemcpyAsync(osim + (uint64_t)q * k, sims.data(), take * 4, cudaMemcpyHostToDevice, s));
+        SS_CUDA(cudaStreamSynchronize(s));
+    }
+}
+
 constexpr uint32_t kQueryChunk = 1024; // queries per coarse-score pass
 constexpr uint32_t kCandCap = 4096;    // candidates kept per query
 
@@ -1372,13 +1410,16 @@ int ss_query_topk(ss_ctx* c, const float* queries, uint32_t nq, uint32_t k, uint
         const uint64_t take = std::min<uint64_t>(k, count);
         for (uint32_t q = 0; q < nq; ++q) out_counts[q] = (k == 0 || count == 0) ? 0 : take;
         if (k == 0 || count == 0 || nq == 0) return; // vecstore.hpp:122
-        if (k > 64) throw Error(SS_ERR_CONTRACT, "query_topk: k above 64 is not supported on the device path");
+
         cudaStream_t s = c->stream;
         Scope sc(c, s, SS_K_QUERY);
         const float* d_qn = prepare_queries(c, queries, nq);
         auto* oid = static_cast<uint32_t*>(c->topk_ids.ensure((size_t)nq * k * 4));
         auto* osim = static_cast<float*>(c->topk_sims.ensure((size_t)nq * k * 4));
-        if (!(tc_eligible(c) && topk_tensor(c, d_qn, nq, k, oid, osim))) topk_exact(c, d_qn, nq, k, oid, osim);
+        if (k > 64)
+            topk_sorted(c, d_qn, nq, k, oid, osim);
+        else if (!(tc_eligible(c) && topk_tensor(c, d_qn, nq, k, oid, osim)))
+            topk_exact(c, d_qn, nq, k, oid, osim);
         // rows written are [q][k] with k stride; take <= k
         std::vector<uint32_t> hid((size_t)nq * k);
         std::vector<float> hsim((size_t)nq * k);

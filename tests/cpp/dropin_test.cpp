@@ -192,6 +192,64 @@ int main() {
             numeric = true;
         }
         CHECK(numeric);
+
+        // k beyond 64, batched queries, run_query payloads, fetch_store round trip
+        std::vector<std::vector<float>> qs;
+        bool big = true;
+        for (int t = 0; t < 5; ++t) {
+            std::vector<float> q(dim);
+            for (auto& x : q) x = float(urand(rng, -1, 1));
+            qs.push_back(q);
+            const auto a = query_topk(store, q, 300);
+            const auto b = b200::query_topk(ds, q, 300);
+            big = big && a.size() == b.size();
+            for (size_t i = 0; big && i < a.size(); ++i)
+                big = a[i].gaussian_id == b[i].gaussian_id && a[i].similarity == b[i].similarity;
+        }
+        CHECK(big);
+        const auto batch = b200::query_topk_batch(ds, qs, 20);
+        bool bok = batch.size() == qs.size();
+        for (size_t t = 0; bok && t < qs.size(); ++t) {
+            const auto a = query_topk(store, qs[t], 20);
+            bok = a.size() == batch[t].size();
+            for (size_t i = 0; bok && i < a.size(); ++i)
+                bok = a[i].gaussian_id == batch[t][i].gaussian_id && a[i].similarity == batch[t][i].similarity;
+        }
+        CHECK(bok);
+        const VectorStore back = b200::fetch_store(ds);
+        bool fok = back.count() == store.count() && back.dim() == store.dim();
+        for (size_t i = 0; fok && i < store.count(); ++i)
+            fok = back.id_at(i) == store.id_at(i) &&
+                  std::memcmp(back.vector_at(i), store.vector_at(i), dim * sizeof(float)) == 0;
+        CHECK(fok);
+    }
+
+    // --- run_query (query.hpp:102-122) on a store built from an encoded fixture
+    {
+        const uint32_t dim = 32;
+        std::mt19937_64 rng(77);
+        GaussianScene scene = random_scene(400, 9);
+        EmbeddingTable table(scene.size(), dim);
+        for (uint64_t k = 0; k < scene.size(); ++k) {
+            if (k % 3 == 0) continue; // uncovered rows stay out of the store
+            for (uint32_t d = 0; d < dim; ++d) table.embeddings[k * dim + d] = float(urand(rng, -1, 1));
+            table.coverage[k] = 1.0f;
+        }
+        const VectorStore hs = build_store(table, scene);
+        const b200::DeviceStore ds = b200::build_store(table, scene);
+        const TextProvider prov = TextProvider::synthetic(dim);
+        bool rq = true;
+        for (const QueryMode& mode : {QueryMode::topk(7), QueryMode::threshold(0.1f)}) {
+            const QueryResult a = run_query(hs, "a chair", mode, prov);
+            const QueryResult b = b200::run_query(ds, "a chair", mode, prov);
+            rq = rq && a.query_vector == b.query_vector && a.matches.size() == b.matches.size();
+            for (size_t i = 0; rq && i < a.matches.size(); ++i)
+                rq = a.matches[i].gaussian_id == b.matches[i].gaussian_id &&
+                     a.matches[i].similarity == b.matches[i].similarity &&
+                     a.matches[i].payload.mean == b.matches[i].payload.mean &&
+                     a.matches[i].payload.opacity == b.matches[i].payload.opacity;
+        }
+        CHECK(rq);
     }
 
     fs::remove_all(tmp);

@@ -428,3 +428,19 @@ def test_render_through_the_reference_shaped_api(gpu_ctx, ref):
     assert r.alpha.tobytes() == exp["alpha"].tobytes()
     assert r.weights.entries.tobytes() == exp["entries"].tobytes()
 
+
+def test_query_topk_k_above_64_vs_oracle(gpu_ctx, oracle):
+    """k beyond the top-k kernels' 64: full exact sort (vecstore.hpp:121-132)."""
+    rng = np.random.default_rng(41)
+    raw = rng.uniform(-0.5, 0.5, (6000, 64)).astype(np.float32)
+    unit = _unit_rows(oracle, raw)
+    ids = rng.permutation(6000).astype(np.uint32)
+    q = rng.uniform(-0.5, 0.5, (3, 64)).astype(np.float32)
+    gpu_ctx.store_set(ids, unit)
+    for k in (65, 500, 7000):
+        gi, gs, gc = gpu_ctx.query_topk(q, k)
+        oi, os_, oc = oracle.query_topk(ids, unit, q, k)
+        kk = min(k, 6000)
+        assert np.array_equal(gc, oc)
+        assert np.array_equal(gi[:, :kk], oi[:, :kk]) and gs[:, :kk].tobytes() == os_[:, :kk].tobytes()
+
