@@ -200,6 +200,14 @@ int ss_profile_read(ss_ctx* ctx, double* ms, uint64_t* launches, double* bytes);
 /* Running totals of the geometry counters (SURVEY.md 8 notation), summed over
  * views since ss_profile_reset: [0]=N_vis [1]=I_v [2]=G_v [3]=K_v [4]=views. */
 int ss_counters_read(ss_ctx* ctx, uint64_t* out5);
+/* eval.hpp:122-158 assign_classes: arg-max cosine class per covered row of an
+ * EmbeddingTable (uncovered rows -1 = kUnlabeled, ties to the lowest class
+ * id), bit-identical to the reference (sequential f64 dots).  rows (n x dim)
+ * and coverage (n) are host arrays, or device pointers with
+ * SS_ROWS_ON_DEVICE; label_vecs is n_labels x dim, label_ids n_labels. */
+#define SS_ROWS_ON_DEVICE 1
+int ss_assign_classes(ss_ctx* ctx, const float* rows, const float* coverage, uint64_t n, uint32_t dim,
+                      const int32_t* label_ids, const float* label_vecs, uint32_t n_labels, int32_t* out, int flags);
 /* Tensor-core query statistics since reset: queries answered on that path,
  * total and maximum candidates per query, batches answered by the exact scan
  * after a candidate overflow. */

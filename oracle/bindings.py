@@ -305,6 +305,8 @@ class Ref:
                                                          C.POINTER(C.c_void_p), C.POINTER(C.c_uint64)]
         L.ssref_weightmap_fetch.argtypes = [C.c_void_p] * 4
         L.ssref_image_fetch.argtypes = [C.c_void_p] * 2
+        L.ssref_assign_classes.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p,
+                                           C.c_uint32, C.c_void_p]
         L.ssref_image_fetch.restype = None
         L.ssref_weightmap_free.argtypes = [C.c_void_p]
         L.ssref_mask_weights.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p,
@@ -489,6 +491,16 @@ class Ref:
         self._chk(self.L.ssref_query_topk(_p(ids), _p(rows), ids.shape[0], rows.shape[1], _p(q), nq, k, threads,
                                           _p(oid), _p(osim), _p(cnt)))
         return oid, osim, cnt
+
+    def assign_classes(self, rows, coverage, label_ids, label_vecs):
+        rows = np.ascontiguousarray(rows, np.float32)
+        coverage = np.ascontiguousarray(coverage, np.float32)
+        lid = np.ascontiguousarray(label_ids, np.int32)
+        lv = np.ascontiguousarray(label_vecs, np.float32)
+        out = np.zeros(rows.shape[0], np.int32)
+        self._chk(self.L.ssref_assign_classes(_p(rows), _p(coverage), rows.shape[0], rows.shape[1], _p(lid), _p(lv),
+                                              lid.shape[0], _p(out)))
+        return out
 
     def query_threshold(self, ids, rows, q, tau):
         ids = np.ascontiguousarray(ids, np.uint32)

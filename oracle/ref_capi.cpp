@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "semsplat/core.hpp"
+#include "semsplat/eval.hpp"
 #include "semsplat/fixture.hpp"
 #include "semsplat/pipeline.hpp"
 #include "semsplat/projection.hpp"
@@ -212,6 +213,22 @@ void ssref_image_fetch(void* handle, float* rgb) {
 }
 
 void ssref_weightmap_free(void* handle) { delete static_cast<WeightMapHandle*>(handle); }
+
+// eval.hpp:122-158 assign_classes on an EmbeddingTable (rows n x dim, coverage n)
+int ssref_assign_classes(const float* rows, const float* coverage, uint64_t n, uint32_t dim, const int32_t* label_ids,
+                         const float* label_vecs, uint32_t n_labels, int32_t* out) {
+    return guarded([&] {
+        EmbeddingTable table(n, dim);
+        std::memcpy(table.embeddings.data(), rows, n * dim * sizeof(float));
+        std::memcpy(table.coverage.data(), coverage, n * sizeof(float));
+        std::vector<std::pair<int32_t, std::vector<float>>> labels;
+        for (uint32_t c = 0; c < n_labels; ++c)
+            labels.push_back({label_ids[c], std::vector<float>(label_vecs + (size_t)c * dim,
+                                                               label_vecs + (size_t)(c + 1) * dim)});
+        const std::vector<int32_t> cls = assign_classes(table, labels);
+        std::memcpy(out, cls.data(), cls.size() * sizeof(int32_t));
+    });
+}
 
 // pipeline.hpp:35 mask_weights on a WeightMap handle and a raster-resolution u8 bitmap.
 // Outputs (gid, sum) pairs sorted by gid; caller provides capacity >= n_entries.

@@ -74,6 +74,7 @@ def lib() -> C.CDLL:
         "ss_scene_set_color": (i32, [vp, vp, u64]),
         "ss_render": (i32, [vp, C.POINTER(Camera), i32, pu64, pu64, pu64]),
         "ss_render_fetch_image": (i32, [vp, vp]),
+        "ss_assign_classes": (i32, [vp, vp, vp, u64, u32, vp, vp, u32, vp, i32]),
         "ss_scene_set": (i32, [vp, pf, pf, pf, pf, u64]),
         "ss_project": (i32, [vp, C.POINTER(Camera), vp]),
         "ss_raster_capture": (i32, [vp, C.POINTER(Camera), i32, pu64, pu64, pu64]),
@@ -168,6 +169,18 @@ class Context:
 
     def set_contract_group(self, n: int):
         check(self._L.ss_set_option(self.h, 3, int(n)))
+
+    def assign_classes(self, rows, coverage, label_ids, label_vecs):
+        """eval.hpp:122-158 on the device: class id per row (-1 = unlabeled)."""
+        rows = np.ascontiguousarray(rows, np.float32)
+        coverage = np.ascontiguousarray(coverage, np.float32)
+        lid = np.ascontiguousarray(label_ids, np.int32)
+        lv = np.ascontiguousarray(label_vecs, np.float32).reshape(lid.shape[0], -1)
+        out = np.zeros(rows.shape[0], np.int32)
+        check(self._L.ss_assign_classes(self.h, rows.ctypes.data_as(C.c_void_p), coverage.ctypes.data_as(C.c_void_p),
+                                        rows.shape[0], rows.shape[1], lid.ctypes.data_as(C.c_void_p),
+                                        lv.ctypes.data_as(C.c_void_p), lid.shape[0], out.ctypes.data_as(C.c_void_p), 0))
+        return out
 
     def set_query_path(self, path: int):
         """0 = auto, 1 = exact scan, 2 = tensor-core coarse + exact rescore."""

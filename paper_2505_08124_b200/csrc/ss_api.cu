@@ -1167,6 +1167,41 @@ int ss_store_build(ss_ctx* c, const float* rows, const float* coverage, uint64_t
     });
 }
 
+// eval.hpp:122-158 assign_classes.  rows/coverage: host arrays, or device
+// pointers with SS_ROWS_ON_DEVICE (e.g. the shard ss_encode_finalize left on
+// the device); labels and out are host arrays.
+int ss_assign_classes(ss_ctx* c, const float* rows, const float* coverage, uint64_t n, uint32_t dim,
+                      const int32_t* label_ids, const float* label_vecs, uint32_t n_labels, int32_t* out, int flags) {
+    return guarded([&] {
+        if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
+        if (n_labels == 0) throw Error(SS_ERR_CONTRACT, "assign_classes: empty label set");
+        if (dim == 0) throw Error(SS_ERR_CONTRACT, "assign_classes: label vector dimension mismatch");
+        set_device(c);
+        cudaStream_t s = c->stream;
+        const float* d_rows = rows;
+        const float* d_cov = coverage;
+        if (!(flags & SS_ROWS_ON_DEVICE)) {
+            auto* buf = static_cast<float*>(c->scores.ensure(std::max<uint64_t>(n, 1) * (dim + 1) * 4));
+            SS_CUDA(cudaMemcpyAsync(buf, rows, n * dim * 4, cudaMemcpyHostToDevice, s));
+            SS_CUDA(cudaMemcpyAsync(buf + n * dim, coverage, n * 4, cudaMemcpyHostToDevice, s));
+            d_rows = buf;
+            d_cov = buf + n * dim;
+        }
+        auto* lab = static_cast<char*>(c->qbuf.ensure((uint64_t)n_labels * (2ull * dim * 4 + 8 + 4) + 256));
+        float* d_lv = reinterpret_cast<float*>(lab);
+        float* d_lt = d_lv + (size_t)n_labels * dim;
+        double* d_ln = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(d_lt + (size_t)n_labels * dim) + 15) & ~uintptr_t(15));
+        int32_t* d_lid = reinterpret_cast<int32_t*>(d_ln + n_labels);
+        SS_CUDA(cudaMemcpyAsync(d_lv, label_vecs, (size_t)n_labels * dim * 4, cudaMemcpyHostToDevice, s));
+        SS_CUDA(cudaMemcpyAsync(d_lid, label_ids, (size_t)n_labels * 4, cudaMemcpyHostToDevice, s));
+        auto* d_out = static_cast<int32_t*>(c->topk_ids.ensure(std::max<uint64_t>(n, 1) * 4));
+        own_launch(c, launch_assign_classes(d_rows, d_cov, n, dim, d_lid, d_lv, n_labels, d_lt, d_ln, d_out, s),
+                   SS_K_QUERY, 2);
+        if (n) SS_CUDA(cudaMemcpyAsync(out, d_out, n * 4, cudaMemcpyDeviceToHost, s));
+        SS_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
 int ss_store_fetch(ss_ctx* c, uint32_t* ids, float* unit_rows) {
     return guarded([&] {
         set_device(c);

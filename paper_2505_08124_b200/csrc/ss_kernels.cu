@@ -412,6 +412,83 @@ __global__ void __launch_bounds__(1024, 1) contract_smem_kernel(ContractParams p
     }
 }
 
+// eval.hpp:122-158 assign_classes.  Warp per row: the row is staged in
+// shared memory, lane l owns classes l, l+32, ...; every dot product and norm
+// is the reference's sequential f64 sum (products of f32 values are exact in
+// f64, explicit __dmul_rn/__dadd_rn keep FMA out), cos = dot / (|row| |label|)
+// or -1 for a zero denominator, and the arg max takes the lowest class id on
+// ties.  Labels arrive transposed ([dim][n_labels]) so lanes read them
+// coalesced.  Uncovered rows (coverage <= f32(1e-8)) get kUnlabeled = -1.
+__global__ void __launch_bounds__(256) assign_classes_kernel(const float* rows, const float* coverage, uint64_t n,
+                                                             uint32_t dim, const int32_t* label_ids,
+                                                             const float* labels_t, const double* label_norms,
+                                                             uint32_t n_labels, int32_t* out) {
+    extern __shared__ float srow[]; // 8 warps x dim
+    const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
+    float* row_s = srow + (size_t)wib * dim;
+    const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t k = warp0; k < n; k += nwarps) {
+        if (!(coverage[k] > 1e-8f)) {
+            if (lane == 0) out[k] = -1;
+            continue;
+        }
+        const float* row = rows + k * dim;
+        __syncwarp();
+        for (uint32_t d = lane; d < dim; d += 32) row_s[d] = row[d];
+        __syncwarp();
+        double rn = 0.0;
+        for (uint32_t d = 0; d < dim; ++d) rn = __dadd_rn(rn, __dmul_rn((double)row_s[d], (double)row_s[d]));
+        rn = __dsqrt_rn(rn);
+        double best = -2.0;
+        int32_t best_id = -1;
+        bool have = false;
+        for (uint32_t c = lane; c < n_labels; c += 32) {
+            double dot = 0.0;
+            for (uint32_t d = 0; d < dim; ++d)
+                dot = __dadd_rn(dot, __dmul_rn((double)row_s[d], (double)__ldg(labels_t + (size_t)d * n_labels + c)));
+            const double denom = __dmul_rn(rn, label_norms[c]);
+            const double cs = denom > 0.0 ? __ddiv_rn(dot, denom) : -1.0;
+            const int32_t id = label_ids[c];
+            // the reference's scan (best = -2 first, replace on cos > best or on an
+            // equal cos with a lower id) selects the max cos, lowest id among equals;
+            // a NaN cos never replaces
+            if (!isnan(cs) && (!have || cs > best || (cs == best && id < best_id))) {
+                best = cs;
+                best_id = id;
+                have = true;
+            }
+        }
+        // arg max over lanes by (cos desc, id asc); lanes without a candidate lose
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int32_t oi = __shfl_xor_sync(0xffffffffu, best_id, o);
+            const bool oh = __shfl_xor_sync(0xffffffffu, have, o);
+            if (oh && (!have || ob > best || (ob == best && oi < best_id))) {
+                best = ob;
+                best_id = oi;
+                have = true;
+            }
+        }
+        if (lane == 0) out[k] = have ? best_id : -1;
+    }
+}
+
+// label_norms[c] = sqrt(sum_d double(v)^2) sequentially; labels_t = transpose
+__global__ void label_prep_kernel(const float* labels, uint32_t dim, uint32_t n_labels, float* labels_t,
+                                  double* norms) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n_labels) return;
+    double nn = 0.0;
+    for (uint32_t d = 0; d < dim; ++d) {
+        const float v = labels[(size_t)c * dim + d];
+        nn = __dadd_rn(nn, __dmul_rn((double)v, (double)v));
+        labels_t[(size_t)d * n_labels + c] = v;
+    }
+    norms[c] = __dsqrt_rn(nn);
+}
+
 // pipeline.hpp:120-135 finalize_into: covered rows (total > 1e-8) become
 // sum/total, coverage = total; uncovered rows are exactly zero.
 __global__ void __launch_bounds__(256) normalize_kernel(const float* sums, const float* totals, uint64_t n,
@@ -715,6 +792,20 @@ cudaError_t launch_normalize_rows(const float* in, const uint32_t* select, uint6
                                   int* zero_flag, cudaStream_t s) {
     if (!n) return cudaSuccess;
     normalize_rows_kernel<<<warp_grid(n), 256, 0, s>>>(in, select, n, dim, out, zero_flag);
+    return cudaGetLastError();
+}
+cudaError_t launch_assign_classes(const float* rows, const float* coverage, uint64_t n, uint32_t dim,
+                                  const int32_t* label_ids, const float* labels, uint32_t n_labels, float* labels_t,
+                                  double* label_norms, int32_t* out, cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    label_prep_kernel<<<blocks_for(n_labels, 128), 128, 0, s>>>(labels, dim, n_labels, labels_t, label_norms);
+    const size_t smem = (size_t)8 * dim * sizeof(float);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(assign_classes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    assign_classes_kernel<<<warp_grid(n), 256, smem, s>>>(rows, coverage, n, dim, label_ids, labels_t, label_norms,
+                                                          n_labels, out);
     return cudaGetLastError();
 }
 cudaError_t launch_flag_covered(const float* coverage, uint64_t n, uint8_t* flags, cudaStream_t s) {

@@ -50,6 +50,10 @@ cudaError_t launch_normalize(const float* sums, const float* totals, uint64_t n,
                              float* coverage, cudaStream_t s);
 cudaError_t launch_normalize_rows(const float* in, const uint32_t* select, uint64_t n, uint32_t dim, float* out,
                                   int* zero_flag, cudaStream_t s);
+// eval.hpp:122-158 (labels [n_labels][dim]; labels_t, label_norms: scratch)
+cudaError_t launch_assign_classes(const float* rows, const float* coverage, uint64_t n, uint32_t dim,
+                                  const int32_t* label_ids, const float* labels, uint32_t n_labels, float* labels_t,
+                                  double* label_norms, int32_t* out, cudaStream_t s);
 cudaError_t launch_flag_covered(const float* coverage, uint64_t n, uint8_t* flags, cudaStream_t s);
 int score_query_tile();
 cudaError_t launch_score(const float* rows, uint64_t count, uint32_t dim, const float* queries, uint32_t nq,

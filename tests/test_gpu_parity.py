@@ -444,3 +444,20 @@ def test_query_topk_k_above_64_vs_oracle(gpu_ctx, oracle):
         assert np.array_equal(gc, oc)
         assert np.array_equal(gi[:, :kk], oi[:, :kk]) and gs[:, :kk].tobytes() == os_[:, :kk].tobytes()
 
+
+@pytest.mark.parametrize("n,dim,nl", [(3000, 512, 20), (1500, 64, 70), (700, 32, 1)])
+def test_assign_classes_bitwise_vs_reference(gpu_ctx, ref, n, dim, nl):
+    """eval.hpp:122-158: sequential f64 cosines, arg max, ties to the lowest id,
+    uncovered rows kUnlabeled -- identical to the reference."""
+    rng = np.random.default_rng(n + nl)
+    rows = rng.standard_normal((n, dim)).astype(np.float32)
+    cov = (rng.random(n) < 0.8).astype(np.float32) * rng.uniform(0.01, 3.0, n).astype(np.float32)
+    rows[5] = 0.0                                        # zero row: cos = -1 for every label
+    ids = rng.permutation(1000)[:nl].astype(np.int32) - 500
+    vecs = rng.standard_normal((nl, dim)).astype(np.float32)
+    if nl > 3:
+        vecs[2] = vecs[1]                                # exact tie: the lower id wins
+    got = gpu_ctx.assign_classes(rows, cov, ids, vecs)
+    exp = ref.assign_classes(rows, cov, ids, vecs)
+    assert np.array_equal(got, exp)
+
