@@ -487,6 +487,38 @@ def main():
         except Exception as ex:  # reported, not fatal
             cpu = {"value": None, "unit": "views/s", "cores": None, "kind": "unavailable", "sample": str(ex)}
 
+    # eval leg (eval.hpp:122-158): arg-max class per covered row of the table
+    # shard just produced (device-resident), 16 synthetic class embeddings
+    evl = None
+    if rank == 0 and not args.no_query:
+        try:
+            from paper_2505_08124_b200.workload import synth_embedding
+            n_local = max(0, min(shard, N - rank * shard))
+            lab_ids = np.arange(16, dtype=np.int32)
+            lab_vecs = np.stack([synth_embedding(f"class_{i}", D) for i in range(16)])
+            ctx.assign_classes_device(rows_out.data_ptr(), cov_out.data_ptr(), n_local, D, lab_ids, lab_vecs)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            cls = ctx.assign_classes_device(rows_out.data_ptr(), cov_out.data_ptr(), n_local, D, lab_ids, lab_vecs)
+            dt = time.perf_counter() - t0
+            evl = {"function": "assign_classes (eval.hpp:122-158)", "rows": int(n_local), "labels": 16,
+                   "covered": int((cls >= 0).sum()), "ms": 1e3 * dt, "rows_per_sec": n_local / dt}
+            if world == 1 and not args.no_cpu_baseline:
+                from oracle.bindings import REF_SO
+                if REF_SO.exists():
+                    from oracle.bindings import Ref
+                    ns = 20000
+                    hr = rows_out[:ns].cpu().numpy()
+                    hc = cov_out[:ns].cpu().numpy()
+                    t1 = time.perf_counter()
+                    rc = Ref().assign_classes(hr, hc, lab_ids, lab_vecs)
+                    dt1 = time.perf_counter() - t1
+                    evl["cpu_baseline"] = {"value": ns / dt1, "unit": "rows/s", "cores": 1, "kind": "reference",
+                                           "sample": f"first {ns} rows of the table"}
+                    evl["parity_sample"] = bool(np.array_equal(rc, cls[:ns]))
+        except Exception as ex:  # reported, not fatal
+            evl = {"error": f"{type(ex).__name__}: {ex}"}
+
     query = None
     if rank == 0 and not args.no_query:
         try:
@@ -522,6 +554,7 @@ def main():
             "gpu_launches_detail": {"own_per_step": own / max(args.steps, 1), "cub_per_step": cub / max(args.steps, 1)},
             "serial_profile_ms_per_step": ms_prof,
             "query": query,
+            "eval": evl,
         }
         print(json.dumps(line), flush=True)
     ctx.close()

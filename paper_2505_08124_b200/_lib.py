@@ -182,6 +182,16 @@ class Context:
                                         lv.ctypes.data_as(C.c_void_p), lid.shape[0], out.ctypes.data_as(C.c_void_p), 0))
         return out
 
+    def assign_classes_device(self, d_rows: int, d_coverage: int, n: int, dim: int, label_ids, label_vecs):
+        """assign_classes on device-resident rows/coverage (SS_ROWS_ON_DEVICE)."""
+        lid = np.ascontiguousarray(label_ids, np.int32)
+        lv = np.ascontiguousarray(label_vecs, np.float32).reshape(lid.shape[0], -1)
+        out = np.zeros(n, np.int32)
+        check(self._L.ss_assign_classes(self.h, C.c_void_p(d_rows), C.c_void_p(d_coverage), n, dim,
+                                        lid.ctypes.data_as(C.c_void_p), lv.ctypes.data_as(C.c_void_p), lid.shape[0],
+                                        out.ctypes.data_as(C.c_void_p), 1))
+        return out
+
     def set_query_path(self, path: int):
         """0 = auto, 1 = exact scan, 2 = tensor-core coarse + exact rescore."""
         check(self._L.ss_set_option(self.h, 2, int(path)))
