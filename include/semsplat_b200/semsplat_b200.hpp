@@ -215,8 +215,21 @@ inline EmbeddingTable encode_scene(const GaussianScene& scene, const DatasetMani
     std::vector<std::string> failures(workers);
     std::vector<size_t> worker_images(workers, 0);
     std::vector<double> worker_seconds(workers, 0.0);
+    std::vector<size_t> worker_entries(workers, 0);
+    const ss_weight_mode wmode = options.mode == WeightMode::kFalloffOnly ? SS_FALLOFF_ONLY : SS_ALPHA_COMPOSITED;
     for (uint32_t rank = 0; rank < workers; ++rank) {
         const auto ts = std::chrono::steady_clock::now();
+        // a worker's views go to the device as one batch (views overlap in the
+        // device's pipeline lanes); host-side decoding errors stop the worker
+        // at that image, as the reference's worker_body does
+        struct ViewData {
+            std::vector<uint32_t> runs;
+            std::vector<uint64_t> offs;
+            std::vector<float> clip;
+        };
+        std::vector<ViewData> data;
+        std::vector<ss_camera> cams;
+        std::vector<uint32_t> image_ids;
         for (size_t idx = 0; idx < n_img; ++idx) {
             const bool mine = options.contiguous_batching ? (idx / block == rank) : (idx % workers == rank);
             if (!mine) continue;
@@ -243,33 +256,22 @@ inline EmbeddingTable encode_scene(const GaussianScene& scene, const DatasetMani
                 }
                 std::sort(masks.begin(), masks.end(),
                           [](const auto& a, const auto& b) { return a.first < b.first; });
-                std::vector<uint32_t> runs;
-                std::vector<uint64_t> offs{0};
+                ViewData vd;
+                vd.offs.push_back(0);
                 for (auto& m : masks) {
-                    runs.insert(runs.end(), m.second.begin(), m.second.end());
-                    offs.push_back(runs.size());
+                    vd.runs.insert(vd.runs.end(), m.second.begin(), m.second.end());
+                    vd.offs.push_back(vd.runs.size());
                 }
                 const std::vector<MaskEmbedding> emb = load_mask_embeddings(manifest, entry.image_id, count);
-                std::vector<float> clip(static_cast<size_t>(count) * manifest.embedding_dim);
+                vd.clip.resize(static_cast<size_t>(count) * manifest.embedding_dim);
                 for (uint32_t j = 0; j < count; ++j)
-                    std::memcpy(clip.data() + static_cast<size_t>(j) * manifest.embedding_dim, emb[j].vector.data(),
-                                manifest.embedding_dim * sizeof(float));
+                    std::memcpy(vd.clip.data() + static_cast<size_t>(j) * manifest.embedding_dim,
+                                emb[j].vector.data(), manifest.embedding_dim * sizeof(float));
                 ss_camera c = to_c(raster_cam);
                 c.image_id = entry.image_id;
-                ss_view_masks vm{};
-                vm.n_masks = count;
-                vm.mask_width = mw;
-                vm.mask_height = mh;
-                vm.flags = 0;
-                vm.runs = runs.data();
-                vm.run_offsets = offs.data();
-                vm.clip = clip.data();
-                vm.n_runs = runs.size();
-                const int st = ss_encode_view(d.ctx(), &c, &vm,
-                                              options.mode == WeightMode::kFalloffOnly ? SS_FALLOFF_ONLY
-                                                                                        : SS_ALPHA_COMPOSITED);
-                if (st != SS_OK) raise_status(st);
-                worker_images[rank] += 1;
+                cams.push_back(c);
+                image_ids.push_back(entry.image_id);
+                data.push_back(std::move(vd));
             } catch (const std::exception& ex) {
                 std::string m = ex.what();
                 const std::string pre = "image " + std::to_string(entry.image_id) + ":";
@@ -278,6 +280,30 @@ inline EmbeddingTable encode_scene(const GaussianScene& scene, const DatasetMani
                 break;
             }
         }
+        std::vector<ss_view_masks> vms(data.size());
+        for (size_t v = 0; v < data.size(); ++v) {
+            vms[v] = ss_view_masks{};
+            vms[v].n_masks = static_cast<uint32_t>(data[v].offs.size() - 1);
+            vms[v].mask_width = manifest.mask_width;
+            vms[v].mask_height = manifest.mask_height;
+            vms[v].flags = 0;
+            vms[v].runs = data[v].runs.data();
+            vms[v].run_offsets = data[v].offs.data();
+            vms[v].clip = data[v].clip.data();
+            vms[v].n_runs = data[v].runs.size();
+        }
+        uint64_t before[5] = {}, after[5] = {};
+        check(ss_counters_read(d.ctx(), before));
+        if (!cams.empty()) {
+            const int st = ss_encode_views(d.ctx(), static_cast<uint32_t>(cams.size()), cams.data(), vms.data(), wmode);
+            if (st != SS_OK) {
+                // per-image errors already name the image ("image N: ...")
+                if (failures[rank].empty()) failures[rank] = ss_last_error();
+            }
+        }
+        check(ss_counters_read(d.ctx(), after));
+        worker_images[rank] = cams.size();
+        worker_entries[rank] = static_cast<size_t>(after[3] - before[3]); // masked-weight (gid, mask) entries
         worker_seconds[rank] = std::chrono::duration<double>(std::chrono::steady_clock::now() - ts).count();
     }
     bool failed = false;
@@ -303,7 +329,7 @@ inline EmbeddingTable encode_scene(const GaussianScene& scene, const DatasetMani
         stats_out->phase2_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
         stats_out->worker_seconds = worker_seconds;
         stats_out->worker_images = worker_images;
-        stats_out->worker_entries.assign(workers, 0);
+        stats_out->worker_entries = worker_entries;
     }
     return table;
 }

@@ -199,10 +199,14 @@ def encode_scene(scene: GaussianScene, manifest: DatasetManifest, workers: int, 
     ctx.encode_begin(dim)
     worker_images = [0] * workers
     worker_seconds = [0.0] * workers
+    worker_entries = [0] * workers
     failures = [""] * workers
     status = ["pending"] * workers
     for rank in range(workers):
         t0 = time.perf_counter()
+        # a worker's views go to the device as one batch (they overlap in the
+        # device's pipeline lanes); host-side decoding errors stop the worker
+        cams, sets, ids = [], [], []
         for idx, entry in enumerate(manifest.images):
             mine = (idx // block == rank) if options.contiguous_batching else (idx % workers == rank)
             if not mine:
@@ -214,10 +218,9 @@ def encode_scene(scene: GaussianScene, manifest: DatasetManifest, workers: int, 
                     raise DataError(f"mask {int(mr.mask_ids[0]) if mr.n_masks else 0} of image {entry.image_id} "
                                     "does not match the manifest mask resolution")
                 emb = formats.load_mask_embeddings(manifest.resolve(entry.embedding_path), dim, mr.n_masks)
-                cam = replace(cam, image_id=entry.image_id)
-                ctx.encode_views([cam], [(mr.n_masks, mr.width, mr.height, mr.runs, mr.offsets, emb)],
-                                 options.mode)
-                worker_images[rank] += 1
+                cams.append(replace(cam, image_id=entry.image_id))
+                sets.append((mr.n_masks, mr.width, mr.height, mr.runs, mr.offsets, emb))
+                ids.append(entry.image_id)
             except SemsplatError as ex:
                 msg = str(ex)
                 if not msg.startswith(f"image {entry.image_id}:"):
@@ -225,6 +228,15 @@ def encode_scene(scene: GaussianScene, manifest: DatasetManifest, workers: int, 
                 failures[rank] = msg
                 status[rank] = msg
                 break
+        before = ctx.counters()["pairs"]
+        if cams:
+            try:
+                ctx.encode_views(cams, sets, options.mode)
+            except SemsplatError as ex:
+                failures[rank] = failures[rank] or str(ex)  # per-image errors name the image
+                status[rank] = failures[rank]
+        worker_images[rank] = len(cams)
+        worker_entries[rank] = ctx.counters()["pairs"] - before  # masked-weight (gid, mask) entries
         if not failures[rank]:
             status[rank] = "ok"
         worker_seconds[rank] = time.perf_counter() - t0
@@ -252,7 +264,7 @@ def encode_scene(scene: GaussianScene, manifest: DatasetManifest, workers: int, 
         stats.phase2_seconds = time.perf_counter() - t2
         stats.worker_seconds = worker_seconds
         stats.worker_images = worker_images
-        stats.worker_entries = [0] * workers
+        stats.worker_entries = worker_entries
     return EmbeddingTable(rows, cov)
 
 

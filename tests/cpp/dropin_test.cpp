@@ -112,13 +112,15 @@ int main() {
         const GaussianScene scene = load_scene(manifest.resolve("scene.ply"));
         const EmbeddingTable ref = encode_scene(scene, manifest, 1, 0);
         for (uint32_t workers : {1u, 3u}) {
-            EncodeStats stats;
+            EncodeStats stats, ref_stats;
             const EmbeddingTable got = b200::encode_scene(scene, manifest, workers, 7, {}, &stats);
+            encode_scene(scene, manifest, workers, 7, {}, &ref_stats);
             CHECK(max_row_rel_diff(ref, got) <= 1e-4);
             bool cov = true;
             for (uint64_t k = 0; k < scene.size(); ++k) cov = cov && ref.covered(k) == got.covered(k);
             CHECK(cov);
-            CHECK(stats.worker_images.size() == workers);
+            CHECK(stats.worker_images == ref_stats.worker_images);
+            CHECK(stats.worker_entries == ref_stats.worker_entries); // (gid, mask) entries per worker
         }
     }
 

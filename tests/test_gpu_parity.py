@@ -461,3 +461,24 @@ def test_assign_classes_bitwise_vs_reference(gpu_ctx, ref, n, dim, nl):
     exp = ref.assign_classes(rows, cov, ids, vecs)
     assert np.array_equal(got, exp)
 
+
+@pytest.mark.parametrize("workers,contiguous", [(1, False), (2, False), (3, True)])
+def test_encode_scene_api_vs_reference(gpu_ctx, ref, tmp_path, workers, contiguous):
+    """semsplat.encode_scene (pipeline.hpp:280-470 mirror) on a reference-written
+    fixture: table within tolerance, identical covered set, and the per-worker
+    masked-weight entry counts summing to the reference's."""
+    from paper_2505_08124_b200 import formats
+    from paper_2505_08124_b200.semsplat import EncodeOptions, EncodeStats, GaussianScene, encode_scene
+    mp = ref.write_fixture(str(tmp_path / "fx"), objects=3, per_object=15, views=5, resolution=40, mask_scale=1,
+                           dim=24, seed=12)
+    man = formats.load_manifest(mp)
+    scene = GaussianScene.load(man.resolve("scene.ply"))
+    stats = EncodeStats()
+    table = encode_scene(scene, man, workers, 11, EncodeOptions(contiguous_batching=contiguous), stats)
+    er, ec, rstats = ref.encode(scene, mp, workers, 11, 0, contiguous)
+    rel, cos = row_errors(table.embeddings, table.coverage, er, ec)
+    assert rel <= EMB_REL_TOL and cos >= EMB_COS_TOL
+    assert np.array_equal(table.coverage > np.float32(1e-8), ec > np.float32(1e-8))
+    assert sum(stats.worker_images) == 5 and len(stats.worker_entries) == workers
+    assert sum(stats.worker_entries) == int(rstats[2])
+
