@@ -112,4 +112,39 @@ __device__ __forceinline__ double glibc_exp(double x, const unsigned long long* 
     return __fma_rn(scale, tmp, scale);
 }
 
+// Same function with the table addressed through a 32-bit shared-window
+// address (tab_addr = __cvta_generic_to_shared(table)): one ld.shared.v2.u64
+// per call, no per-call rebuild of the generic shared base.
+__device__ __forceinline__ double glibc_exp_s(double x, uint32_t tab_addr) {
+    // literal constants: the compiler keeps them in uniform registers, which
+    // costs no general registers in the compositor's loop
+    const double InvLn2N = 0x1.71547652b82fep0 * 128, Shift = 0x1.8p52;
+    const double NegLn2hiN = -0x1.62e42fefa0000p-8, NegLn2loN = -0x1.cf79abc9e3b3ap-47;
+    const double C2 = 0x1.ffffffffffdbdp-2, C3 = 0x1.555555555543cp-3;
+    const double C4 = 0x1.55555cf172b91p-5, C5 = 0x1.1111167a4d017p-7;
+    const unsigned long long ix = (unsigned long long)__double_as_longlong(x);
+    const uint32_t abstop = (uint32_t)(ix >> 52) & 0x7ffu;
+    if (abstop - 0x3c9u >= 0x3fu) {
+        if ((int32_t)(abstop - 0x3c9u) < 0) return __dadd_rn(1.0, x); // |x| < 2^-54
+        return exp(x); // |x| >= 512: unreachable on this path (x in [-4.5, 0])
+    }
+    double kd = __fma_rn(x, InvLn2N, Shift);
+    const unsigned long long ki = (unsigned long long)__double_as_longlong(kd);
+    kd = __dsub_rn(kd, Shift);
+    double r = __fma_rn(kd, NegLn2hiN, x);
+    r = __fma_rn(kd, NegLn2loN, r);
+    const uint32_t idx = 2u * (uint32_t)(ki & 127ull);
+    const unsigned long long top = ki << 45;
+    unsigned long long t0, t1;
+    asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(t0), "=l"(t1) : "r"(tab_addr + idx * 8u));
+    const double tail = __longlong_as_double((long long)t0);
+    const unsigned long long sbits = t1 + top;
+    const double r2 = __dmul_rn(r, r);
+    const double tmp =
+        __fma_rn(__dmul_rn(r2, r2), __fma_rn(r, C5, C4), __fma_rn(__fma_rn(r, C3, C2), r2, __dadd_rn(tail, r)));
+    const double scale = __longlong_as_double((long long)sbits);
+    return __fma_rn(scale, tmp, scale);
+}
+
 } // namespace ss
+

@@ -223,12 +223,11 @@ struct PixelState {
 // cutoff, alpha clamp, skip rule, weight cutoff and transmittance floor, in
 // its exact fp64 operation order.  Returns whether an entry is emitted.
 template <bool FALLOFF, typename Rec>
-__device__ __forceinline__ bool composite_one(PixelState& ps, const Rec& s, const unsigned long long* stab,
-                                              float& wf) {
+__device__ __forceinline__ bool composite_one(PixelState& ps, const Rec& s, uint32_t stab_addr, float& wf) {
     const double dx = ds(ps.dpx, s.mu_x), dy = ds(ps.dpy, s.mu_y);
     const double d2 = da(da(dm(dm(s.a, dx), dx), dm(dm(s.b2, dx), dy)), dm(dm(s.c, dy), dy));
     if (d2 > kMahalanobisSqCutoff) return false;
-    const double g = glibc_exp(dm(-0.5, d2), stab);
+    const double g = glibc_exp_s(dm(-0.5, d2), stab_addr);
     if constexpr (FALLOFF) {
         if (g >= kWeightCutoff) {
             wf = __double2float_rn(g);
@@ -357,6 +356,7 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
     const uint32_t wbase = 32u * warp;
     SplatRec* wrec = srec + wbase;
     uint32_t srec_addr = (uint32_t)__cvta_generic_to_shared(wrec);
+    uint32_t stab_addr = (uint32_t)__cvta_generic_to_shared(stab);
     uint32_t* wgid = sgid + 32u * warp;
     uint32_t* wmask = smask + 32u * warp;
 
@@ -430,15 +430,15 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
         const uint32_t smk = lane < nh ? wmask[lane] : 0u;
         const uint32_t sgd = lane < nh ? wgid[lane] : 0u;
         for (uint32_t j = 0; j < nh; ++j) {
-            // keep the pixel coordinates and the staging address live instead of
-            // re-deriving them for every splat
-            asm volatile("" : "+d"(ps.dpx), "+d"(ps.dpy), "+r"(srec_addr));
+            // keep the staging and exp-table addresses live instead of re-deriving
+            // the shared window base for every splat
+            asm volatile("" : "+r"(srec_addr), "+r"(stab_addr));
             const StagedSplat s = lds_splat(srec_addr + j * (uint32_t)sizeof(SplatRec));
             const uint32_t mj = __shfl_sync(0xffffffffu, smk, j);
             const uint32_t gj = __shfl_sync(0xffffffffu, sgd, j);
             float wf = 0.0f;
             bool c = false;
-            if ((mj & lane_bit) && !ps.done) c = composite_one<FALLOFF>(ps, s, stab, wf);
+            if ((mj & lane_bit) && !ps.done) c = composite_one<FALLOFF>(ps, s, stab_addr, wf);
             if constexpr (KIND == 0) {
                 ps.count += c ? 1u : 0u;
             } else if constexpr (KIND == 1 || KIND == 3) {
