@@ -74,6 +74,7 @@ def parse():
     ap.add_argument("--no-query", action="store_true", help="skip the c5 vector-DB query leg")
     ap.add_argument("--lanes", type=int, default=0, help="pipeline lanes (0 = library default)")
     ap.add_argument("--group", type=int, default=0, help="views per contraction group (0 = library default)")
+    ap.add_argument("--bin", type=int, default=0, help="tile binning: 0 auto, 1 key sort, 2 direct")
     ap.add_argument("--cpu-sample-queries", type=int, default=32)
     return ap.parse_args()
 
@@ -362,6 +363,8 @@ def main():
     ctx.set_lanes(lanes)
     if args.group:
         ctx.set_contract_group(args.group)
+    if args.bin:
+        ctx.set_bin_path(args.bin)
 
     # device-resident inputs for `value`
     dev = torch.device("cuda", local)

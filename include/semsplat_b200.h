@@ -97,8 +97,11 @@ int ss_synchronize(ss_ctx* ctx);
  * 2 = tensor-core path whenever dim allows.  Results are identical.
  * SS_OPT_CONTRACT_GROUP: views contracted together (1..4, default 1): each
  * touched Gaussian's row is read and written once per group; the fp32
- * operation order per row is the same for every group size. */
-enum ss_option { SS_OPT_LANES = 1, SS_OPT_QUERY_PATH = 2, SS_OPT_CONTRACT_GROUP = 3 };
+ * operation order per row is the same for every group size.
+ * SS_OPT_BIN_PATH: tile lists from 0 / 1 = stable key sort (default),
+ * 2 = direct count/scan/scatter binning (views of <= 18000 16x16 tiles;
+ * error above).  The tile lists are identical. */
+enum ss_option { SS_OPT_LANES = 1, SS_OPT_QUERY_PATH = 2, SS_OPT_CONTRACT_GROUP = 3, SS_OPT_BIN_PATH = 4 };
 int ss_set_option(ss_ctx* ctx, int option, int64_t value);
 
 /* ---- scene (GaussianScene, scene.hpp:54-76) --------------------------- */

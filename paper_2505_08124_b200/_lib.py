@@ -196,6 +196,10 @@ class Context:
         """0 = auto, 1 = exact scan, 2 = tensor-core coarse + exact rescore."""
         check(self._L.ss_set_option(self.h, 2, int(path)))
 
+    def set_bin_path(self, path: int):
+        """0/1 = stable key sort (default), 2 = direct count/scan/scatter binning."""
+        check(self._L.ss_set_option(self.h, 4, int(path)))
+
     def synchronize(self):
         check(self._L.ss_synchronize(self.h))
 

@@ -142,6 +142,7 @@ struct Lane {
     ContractSet sets[2];
     uint32_t set_next = 0;
     DevBuf rec, boxes, rbox, rcnt, keys, k32, k32s, order, iota, offsets, tkeys, tkeys_sorted, tvals, tile_start, tile_end, list;
+    DevBuf bin_counts, bin_slice, bin_tot, bin_done; // direct binning scratch
     uint64_t iota_n = 0;           // entries of the 0..n-1 sequence in `iota`
     uint64_t list_cap = 0;         // entries of `list`
     DevBuf cub_tmp, info;
@@ -150,7 +151,7 @@ struct Lane {
     uint32_t* h_u32 = nullptr;     // pinned scratch
     void release_all() {
         DevBuf* b[] = {&rec, &boxes, &rbox, &rcnt, &keys, &k32, &k32s, &order, &iota, &offsets, &tkeys, &tkeys_sorted, &tvals, &tile_start,
-                       &tile_end, &list, &cub_tmp, &info, &pix_bits, &mask_bits,
+                       &tile_end, &list, &cub_tmp, &info, &pix_bits, &mask_bits, &bin_counts, &bin_slice, &bin_tot, &bin_done,
                        &runs, &run_offsets, &spans};
         for (auto* x : b) x->release();
         for (auto& cs : sets) cs.release();
@@ -227,6 +228,7 @@ struct ss_ctx {
     ss::DevBuf store_half, qhalf, tc_scores, tc_thr, cand, cand_count, cand_sim;
     bool store_half_ok = false;
     int query_path = 0; // SS_OPT_QUERY_PATH
+    int bin_path = 0;   // SS_OPT_BIN_PATH
     int num_sms = 0;
 
     // instrumentation
@@ -314,9 +316,15 @@ Geometry run_geometry(ss_ctx* c, Lane& L, cudaStream_t s, const ss_camera& cam) 
     g.k16 = g.tiles <= 65535u;
     if (L.list_cap == 0) L.list_cap = std::max<uint64_t>(4 * N, 1u << 20);
     auto* list = static_cast<uint32_t*>(L.list.ensure(L.list_cap * 4));
-    L.tkeys.ensure(L.list_cap * (g.k16 ? 2 : 4));
-    L.tkeys_sorted.ensure(L.list_cap * (g.k16 ? 2 : 4));
-    L.tvals.ensure(L.list_cap * 4);
+    const uint32_t bin_warps = bin_scatter_warps(g.tiles);
+    if (c->bin_path == 2 && !bin_warps)
+        throw Error(SS_ERR_CONTRACT, "SS_OPT_BIN_PATH=2: too many tiles for the direct binning path");
+    const bool direct = c->bin_path == 2;
+    if (!direct) {
+        L.tkeys.ensure(L.list_cap * (g.k16 ? 2 : 4));
+        L.tkeys_sorted.ensure(L.list_cap * (g.k16 ? 2 : 4));
+        L.tvals.ensure(L.list_cap * 4);
+    }
     ViewInfo* info = L.info.as<ViewInfo>();
 
     reset_info(c, L, s);
@@ -360,6 +368,32 @@ Geometry run_geometry(ss_ctx* c, Lane& L, cudaStream_t s, const ss_camera& cam) 
         c->launches_cub += 1;
         c->prof.launches[SS_K_SORT] += 1;
         own_launch(c, launch_tie_fixup(k32s, N, keys, order, s), SS_K_SORT);
+    }
+    if (direct) {
+        // count / scan / scatter straight into the tile slices (no key sort)
+        Scope sc(c, s, SS_K_BIN);
+        if (!L.bin_done.p) {
+            L.bin_done.ensure(4);
+            SS_CUDA(cudaMemset(L.bin_done.p, 0, 4));
+        }
+        BinParams bp;
+        bp.boxes = boxes;
+        bp.order = order;
+        bp.n = N;
+        bp.tiles = g.tiles;
+        bp.tiles_x = g.tiles_x;
+        bp.rbox = static_cast<uint2*>(L.rbox.ensure(std::max<uint64_t>(N, 1) * sizeof(uint2)));
+        bp.counts = static_cast<uint32_t*>(L.bin_counts.ensure(std::max<size_t>(bin_counts_entries(N, g.tiles), 1) * 4));
+        bp.slice = static_cast<uint32_t*>(L.bin_slice.ensure(32ull * g.tiles * 4));
+        bp.tot = static_cast<uint32_t*>(L.bin_tot.ensure((g.tiles + 1ull) * 4));
+        bp.done = L.bin_done.as<uint32_t>();
+        bp.start = tstart;
+        bp.end = tend;
+        bp.list = list;
+        bp.cap = L.list_cap;
+        bp.info = info;
+        own_launch(c, launch_bin(bp, s), SS_K_BIN, 3);
+        return g;
     }
     {
         Scope sc(c, s, SS_K_BIN);
@@ -807,6 +841,9 @@ int ss_set_option(ss_ctx* c, int option, int64_t value) {
         } else if (option == SS_OPT_QUERY_PATH) {
             if (value < 0 || value > 2) throw Error(SS_ERR_CONTRACT, "SS_OPT_QUERY_PATH must be 0, 1 or 2");
             c->query_path = (int)value;
+        } else if (option == SS_OPT_BIN_PATH) {
+            if (value < 0 || value > 2) throw Error(SS_ERR_CONTRACT, "SS_OPT_BIN_PATH must be 0, 1 or 2");
+            c->bin_path = (int)value;
         } else {
             throw Error(SS_ERR_CONTRACT, "unknown option");
         }

@@ -276,6 +276,261 @@ __global__ void tile_ranges_kernel(const K* keys, const uint32_t* offsets, uint6
     }
 }
 
+// ------------------------------------------------ direct box binning
+// The same tile lists as steps 4-6 above (each tile's slice = the depth ranks
+// whose box covers it, ascending) without materialising (tile, id) keys or
+// sorting them: a counting sort whose one "digit" is the whole tile index.
+//  A. bin_count: chunk c = ranks [c*R, (c+1)*R); counts[c][t] = instances of
+//     tile t in the chunk (shared-memory histogram).  Also rbox[r].
+//  B. bin_scan: per tile, exclusive prefix over chunks (in 32 slices:
+//     counts[c][t] becomes the prefix inside its slice, slice[s][t] the slice
+//     base), tile totals; the last CTA scans the totals into tile_start /
+//     tile_end and sets n_instances / overflow.
+//  C. bin_scatter: chunk c's CTA holds cur[t] = start + slice + prefix; its
+//     warps own consecutive rank ranges, so a per-tile scan over the warps'
+//     own counts gives each warp its first slot; inside a warp the 32-slot
+//     rounds run in rank order and slots of one tile in a round belong to
+//     distinct ranks in lane order (a rank covers a tile at most once), so
+//     the rank inside the round is popc(match_any(tile) & lanes below).
+// Every step is deterministic; the result is bit-identical to the sort path.
+constexpr uint32_t kBinChunk = 4096;   // ranks per chunk
+constexpr uint32_t kBinSlices = 32;    // chunk slices of the prefix scan
+
+// Visit a warp's 32 boxes' tile instances in (lane, row-major tile) order, 32
+// slots per round: f(valid, tile, owner_lane) on every lane of every round.
+template <typename F>
+__device__ __forceinline__ void for_each_instance(uint2 box, uint32_t lane, uint32_t tiles_x, F&& f) {
+    const uint32_t cnt = box_tiles(box);
+    const uint32_t tx0 = (box.x & 0xffffu) / kTile, ty0 = (box.y & 0xffffu) / kTile;
+    const uint32_t nx = box.x == kCulledBox ? 1u : (box.x >> 16) / kTile - tx0 + 1u;
+    uint32_t incl = cnt;
+#pragma unroll
+    for (uint32_t d = 1; d < 32; d <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += v;
+    }
+    const uint32_t rel = incl - cnt;
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    for (uint32_t p0 = 0; p0 < total; p0 += 32) {
+        const uint32_t pos = p0 + lane;
+        uint32_t o = 0; // the last lane whose first slot is <= pos
+#pragma unroll
+        for (uint32_t step = 16; step > 0; step >>= 1) {
+            const uint32_t rv = __shfl_sync(0xffffffffu, rel, o + step);
+            if (rv <= pos) o += step;
+        }
+        const uint32_t o_rel = __shfl_sync(0xffffffffu, rel, o);
+        const uint32_t o_nx = __shfl_sync(0xffffffffu, nx, o);
+        const uint32_t o_tx0 = __shfl_sync(0xffffffffu, tx0, o);
+        const uint32_t o_ty0 = __shfl_sync(0xffffffffu, ty0, o);
+        const uint32_t k = pos - o_rel;
+        const uint32_t dy = k / o_nx, dx = k - dy * o_nx;
+        f(pos < total, (o_ty0 + dy) * tiles_x + o_tx0 + dx, o);
+    }
+}
+
+__device__ __forceinline__ uint32_t bin_chunks(const ViewInfo* info) {
+    return (uint32_t)((info->n_surv + kBinChunk - 1) / kBinChunk);
+}
+
+__global__ void __launch_bounds__(256) bin_count_kernel(BinParams p) {
+    extern __shared__ uint32_t hist[];
+    const uint64_t n_surv = p.info->n_surv;
+    const uint64_t base = (uint64_t)blockIdx.x * kBinChunk;
+    if (base >= n_surv) return;
+    for (uint32_t t = threadIdx.x; t < p.tiles; t += blockDim.x) hist[t] = 0u;
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    constexpr uint32_t groups = kBinChunk / 256u;
+    const uint64_t r0 = base + (uint64_t)warp * groups * 32u + lane;
+    auto load_id = [&](uint32_t g) {
+        return r0 + g * 32u < n_surv ? __ldg(p.order + r0 + g * 32u) : 0xffffffffu;
+    };
+    auto load_box = [&](uint32_t id) {
+        return id != 0xffffffffu ? __ldg(p.boxes + id) : make_uint2(kCulledBox, kCulledBox);
+    };
+    uint32_t id = load_id(0), id_next = load_id(1);
+    uint2 next = load_box(id);
+    for (uint32_t g = 0; g < groups; ++g) {
+        const uint2 box = next;
+        const uint32_t idg = id;
+        id = id_next;
+        if (g + 1 < groups) next = load_box(id);
+        if (g + 2 < groups) id_next = load_id(g + 2);
+        if (idg != 0xffffffffu) p.rbox[r0 + g * 32u] = box;
+        for_each_instance(box, lane, p.tiles_x, [&](bool valid, uint32_t t, uint32_t) {
+            if (valid) atomicAdd(hist + t, 1u);
+        });
+    }
+    __syncthreads();
+    uint32_t* row = p.counts + (size_t)blockIdx.x * p.tiles;
+    for (uint32_t t = threadIdx.x; t < p.tiles; t += blockDim.x) row[t] = hist[t];
+}
+
+__global__ void __launch_bounds__(1024) bin_scan_kernel(BinParams p) {
+    __shared__ uint32_t sm[32][33];
+    __shared__ uint32_t wsum[32];
+    __shared__ bool last;
+    const uint32_t tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32u + tx;
+    const uint32_t C = bin_chunks(p.info);
+    const uint32_t S = (C + kBinSlices - 1) / kBinSlices;
+    const uint32_t t = blockIdx.x * 32u + tx;
+    uint32_t sum = 0;
+    if (t < p.tiles) {
+        const uint32_t c1 = min(C, (ty + 1) * S);
+        for (uint32_t c = ty * S; c < c1; c += 8) { // eight loads in flight, then the stores
+            uint32_t v[8];
+#pragma unroll
+            for (uint32_t i = 0; i < 8; ++i) v[i] = c + i < c1 ? p.counts[(size_t)(c + i) * p.tiles + t] : 0u;
+#pragma unroll
+            for (uint32_t i = 0; i < 8; ++i) {
+                if (c + i < c1) p.counts[(size_t)(c + i) * p.tiles + t] = sum;
+                sum += v[i];
+            }
+        }
+    }
+    sm[ty][tx] = sum;
+    __syncthreads();
+    { // warp ty scans column ty over the 32 slices (lane = slice)
+        const uint32_t v = sm[tx][ty];
+        uint32_t incl = v;
+#pragma unroll
+        for (uint32_t d = 1; d < 32; d <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, incl, d);
+            if (tx >= d) incl += u;
+        }
+        sm[tx][ty] = incl - v;
+        const uint32_t tt = blockIdx.x * 32u + ty;
+        if (tx == 31u && tt < p.tiles) p.tot[tt] = incl;
+    }
+    __syncthreads();
+    if (t < p.tiles) p.slice[(size_t)ty * p.tiles + t] = sm[ty][tx];
+    // the last CTA to finish scans the tile totals
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) last = atomicAdd(p.done, 1u) == gridDim.x * gridDim.y - 1u;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const uint32_t seg = (p.tiles + 1023u) / 1024u;
+    const uint32_t t0 = min(p.tiles, tid * seg), t1 = min(p.tiles, t0 + seg);
+    uint32_t local = 0;
+    for (uint32_t u = t0; u < t1; ++u) local += __ldcg(p.tot + u);
+    uint32_t incl = local;
+#pragma unroll
+    for (uint32_t d = 1; d < 32; d <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, incl, d);
+        if (tx >= d) incl += u;
+    }
+    if (tx == 31u) wsum[ty] = incl;
+    __syncthreads();
+    if (ty == 0) {
+        const uint32_t v = wsum[tx];
+        uint32_t wi = v;
+#pragma unroll
+        for (uint32_t d = 1; d < 32; d <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, wi, d);
+            if (tx >= d) wi += u;
+        }
+        wsum[tx] = wi - v;
+    }
+    __syncthreads();
+    uint32_t run = wsum[ty] + incl - local;
+    for (uint32_t u = t0; u < t1; ++u) {
+        const uint32_t v = __ldcg(p.tot + u);
+        p.start[u] = run;
+        run += v;
+        p.end[u] = run;
+    }
+    if (tid == 1023u) {
+        p.info->n_instances = run;
+        if (run > p.cap) p.info->overflow = 1u;
+        *p.done = 0u;
+    }
+}
+
+template <uint32_t WARPS>
+__global__ void __launch_bounds__(WARPS * 32) bin_scatter_kernel(BinParams p) {
+    extern __shared__ uint32_t cur[];                                    // [tiles]
+    uint16_t* wh = reinterpret_cast<uint16_t*>(cur + p.tiles);           // [WARPS][tiles]
+    if (p.info->overflow) return;
+    const uint64_t n_surv = p.info->n_surv;
+    const uint64_t base = (uint64_t)blockIdx.x * kBinChunk;
+    if (base >= n_surv) return;
+    const uint32_t C = bin_chunks(p.info);
+    const uint32_t S = (C + kBinSlices - 1) / kBinSlices;
+    const uint32_t* row = p.counts + (size_t)blockIdx.x * p.tiles;
+    const uint32_t* sl = p.slice + (size_t)(blockIdx.x / S) * p.tiles;
+    for (uint32_t t = threadIdx.x; t < p.tiles; t += blockDim.x) cur[t] = p.start[t] + sl[t] + row[t];
+    for (uint32_t t = threadIdx.x; t < WARPS * p.tiles; t += blockDim.x) wh[t] = 0;
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    constexpr uint32_t groups = kBinChunk / (WARPS * 32u);
+    uint16_t* mine = wh + (size_t)warp * p.tiles;
+    const uint32_t below = (1u << lane) - 1u;
+    const uint32_t kbits = 32u - __clz(max(p.tiles, 2u) - 1u);
+    const uint64_t r0 = base + (uint64_t)warp * groups * 32u + lane;
+    auto load_box = [&](uint32_t g) {
+        return r0 + g * 32u < n_surv ? p.rbox[r0 + g * 32u] : make_uint2(kCulledBox, kCulledBox);
+    };
+    // lanes holding the same tile (ballots over the tile bits; cheaper than match.any)
+    auto peers = [&](bool valid, uint32_t t) {
+        uint32_t m = __ballot_sync(0xffffffffu, valid);
+        for (uint32_t b = 0; b < kbits; ++b) {
+            const uint32_t on = __ballot_sync(0xffffffffu, (t >> b) & 1u);
+            m &= ((t >> b) & 1u) ? on : ~on;
+        }
+        return m;
+    };
+    // 1. the warp's own per-tile counts
+    uint2 next = load_box(0);
+    for (uint32_t g = 0; g < groups; ++g) {
+        const uint2 box = next;
+        if (g + 1 < groups) next = load_box(g + 1); // one group ahead
+        for_each_instance(box, lane, p.tiles_x, [&](bool valid, uint32_t t, uint32_t) {
+            const uint32_t m = peers(valid, t);
+            if (valid && (m & below) == 0u) mine[t] = (uint16_t)(mine[t] + __popc(m));
+            __syncwarp();
+        });
+    }
+    __syncthreads();
+    // 2. warp offsets inside the chunk (a tile holds <= kBinChunk of its instances)
+    for (uint32_t t = threadIdx.x; t < p.tiles; t += blockDim.x) {
+        uint32_t run = 0;
+#pragma unroll
+        for (uint32_t w = 0; w < WARPS; ++w) {
+            const uint32_t v = wh[(size_t)w * p.tiles + t];
+            wh[(size_t)w * p.tiles + t] = (uint16_t)run;
+            run += v;
+        }
+    }
+    __syncthreads();
+    // 3. scatter in rank order
+    auto load_id = [&](uint32_t g) { return r0 + g * 32u < n_surv ? __ldg(p.order + r0 + g * 32u) : 0u; };
+    next = load_box(0);
+    uint32_t next_id = load_id(0);
+    for (uint32_t g = 0; g < groups; ++g) {
+        const uint2 box = next;
+        const uint32_t id = next_id;
+        if (g + 1 < groups) {
+            next = load_box(g + 1);
+            next_id = load_id(g + 1);
+        }
+        for_each_instance(box, lane, p.tiles_x, [&](bool valid, uint32_t t, uint32_t o) {
+            const uint32_t gid = __shfl_sync(0xffffffffu, id, o);
+            const uint32_t m = peers(valid, t);
+            uint32_t off = 0;
+            if (valid) {
+                off = mine[t];
+                p.list[cur[t] + off + __popc(m & below)] = gid;
+            }
+            __syncwarp();
+            if (valid && (m & below) == 0u) mine[t] = (uint16_t)(off + __popc(m));
+            __syncwarp();
+        });
+    }
+}
+
 // --------------------------------------------------------- contraction
 // pipeline.hpp:70-80 accumulate for a group of up to four consecutive views:
 // for every Gaussian touched in any of them, row[gid] += sum_m acc_v[gid, m] *
@@ -744,6 +999,50 @@ cudaError_t launch_emit_instances(const uint2* rbox, const uint32_t* order, uint
                                                                             static_cast<uint32_t*>(keys), vals, info);
         pad_keys_kernel<uint32_t><<<g, 256, 0, s>>>(offsets, n, cap, static_cast<uint32_t*>(keys));
     }
+    return cudaGetLastError();
+}
+
+uint32_t bin_scatter_warps(uint32_t tiles) {
+    if (20ull * tiles <= 112u * 1024u) return 8u; // two CTAs of 8 warps per SM
+    if (tiles <= 18000u) return 4u;              // 12 B per tile: <= 216 KB
+    return 0u;
+}
+
+size_t bin_counts_entries(uint64_t n, uint32_t tiles) {
+    return (size_t)((n + kBinChunk - 1) / kBinChunk) * tiles;
+}
+
+cudaError_t launch_bin(const BinParams& p, cudaStream_t s) {
+    const uint32_t warps = bin_scatter_warps(p.tiles);
+    if (!warps) return cudaErrorInvalidValue;
+    const unsigned chunks = (unsigned)std::max<uint64_t>((p.n + kBinChunk - 1) / kBinChunk, 1);
+    static bool attr_done[3] = {false, false, false};
+    const size_t count_smem = (size_t)p.tiles * 4u;
+    const size_t scatter_smem = (size_t)p.tiles * (4u + 2u * warps);
+    cudaError_t e;
+    if (!attr_done[0]) {
+        if ((e = cudaFuncSetAttribute(bin_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024)))
+            return e;
+        attr_done[0] = true;
+    }
+    if (warps == 8 && !attr_done[1]) {
+        if ((e = cudaFuncSetAttribute(bin_scatter_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      112 * 1024)))
+            return e;
+        attr_done[1] = true;
+    }
+    if (warps == 4 && !attr_done[2]) {
+        if ((e = cudaFuncSetAttribute(bin_scatter_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      220 * 1024)))
+            return e;
+        attr_done[2] = true;
+    }
+    bin_count_kernel<<<chunks, 256, count_smem, s>>>(p);
+    bin_scan_kernel<<<(p.tiles + 31) / 32, dim3(32, 32), 0, s>>>(p);
+    if (warps == 8)
+        bin_scatter_kernel<8><<<chunks, 256, scatter_smem, s>>>(p);
+    else
+        bin_scatter_kernel<4><<<chunks, 128, scatter_smem, s>>>(p);
     return cudaGetLastError();
 }
 

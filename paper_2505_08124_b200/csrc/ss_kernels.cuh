@@ -45,6 +45,29 @@ cudaError_t launch_emit_instances(const uint2* rbox, const uint32_t* order, uint
                                   cudaStream_t s);
 cudaError_t launch_tile_ranges(const void* keys, bool k16, const uint32_t* offsets, uint64_t n, uint64_t cap,
                                uint32_t* start, uint32_t* end, ViewInfo* info, cudaStream_t s);
+
+// Direct box binning (count / scan / scatter; ss_kernels.cu): tile lists and
+// ranges straight from the depth order, bit-identical to the sort path.
+struct BinParams {
+    const uint2* boxes;    // per Gaussian (projection)
+    const uint32_t* order; // depth order, survivors first
+    uint64_t n;            // Gaussians (grid size; survivors come from info)
+    uint32_t tiles, tiles_x;
+    uint2* rbox;           // [n] boxes in rank order (scratch)
+    uint32_t* counts;      // [bin_counts_entries] per-chunk tile counts / prefixes
+    uint32_t* slice;       // [32 x tiles] slice bases
+    uint32_t* tot;         // [tiles] tile totals
+    uint32_t* done;        // CTA counter, zero between launches
+    uint32_t* start;       // [tiles] tile ranges
+    uint32_t* end;
+    uint32_t* list;        // [cap] splat ids
+    uint64_t cap;
+    ViewInfo* info;
+};
+// warps per scatter CTA for a tile count (0: too many tiles, use the sort path)
+uint32_t bin_scatter_warps(uint32_t tiles);
+size_t bin_counts_entries(uint64_t n, uint32_t tiles);
+cudaError_t launch_bin(const BinParams& p, cudaStream_t s);
 cudaError_t launch_contract(const ContractParams& p, uint64_t max_touched, cudaStream_t s);
 cudaError_t launch_normalize(const float* sums, const float* totals, uint64_t n, uint32_t dim, float* rows,
                              float* coverage, cudaStream_t s);

@@ -137,6 +137,50 @@ def test_oversized_tiles_sort_exactly(gpu_ctx, oracle, n):
     _assert_capture_equal(got, oracle.rasterize(s, cam))
 
 
+@pytest.mark.parametrize("seed,n,w,h,dist,scale", [
+    (11, 50000, 1920, 1080, 9.0, 1.0),    # 13 chunks, 8160 tiles (4-warp scatter CTAs)
+    (12, 30000, 640, 480, 7.0, 6.0),      # large boxes: hundreds of tiles per splat
+    (13, 9000, 1152, 864, 8.0, 1.0),      # c4 geometry (8-warp scatter CTAs)
+    (14, 4097, 64, 64, 7.0, 1.0)])        # one rank past a chunk
+def test_direct_binning_equals_sort(gpu_ctx, oracle, seed, n, w, h, dist, scale):
+    """SS_OPT_BIN_PATH: the count/scan/scatter binning gives the key sort's
+    tile lists, ranges and contributor lists bit for bit."""
+    s = random_scene(n, seed)
+    s.scale[:] = (s.scale * np.float32(scale)).astype(np.float32)
+    cam = make_test_camera(w, h, dist)
+    try:
+        gpu_ctx.set_bin_path(1)
+        by_sort = _capture(gpu_ctx, s, cam)
+        gpu_ctx.set_bin_path(2)
+        direct = _capture(gpu_ctx, s, cam)
+    finally:
+        gpu_ctx.set_bin_path(0)
+    assert direct["tile_offsets"][-1] > 0
+    _assert_capture_equal(direct, by_sort)
+    if n <= 10000:
+        _assert_capture_equal(direct, oracle.rasterize(s, cam))
+
+
+def test_direct_binning_tile_limit(gpu_ctx, oracle):
+    """Forcing the direct path on a view with more than 18000 tiles is a
+    contract error; the sort path handles it."""
+    from paper_2505_08124_b200.errors import ContractError
+    s = random_scene(3000, 15)
+    cam = make_test_camera(3840, 2160, 8.0)
+    auto = _capture(gpu_ctx, s, cam)
+    try:
+        gpu_ctx.set_bin_path(2)
+        with pytest.raises(ContractError):
+            _capture(gpu_ctx, s, cam)
+    finally:
+        gpu_ctx.set_bin_path(0)
+    gpu_ctx.set_bin_path(1)
+    try:
+        _assert_capture_equal(auto, _capture(gpu_ctx, s, cam))
+    finally:
+        gpu_ctx.set_bin_path(0)
+
+
 def test_empty_and_culled_scenes(gpu_ctx, oracle):
     cam = plain_camera(50, 50, 16, 16, 32, 32)
     behind = scene_ns([[0, 0, -1], [0, 0, 0.005]], [[0.1] * 3] * 2, [[0, 0, 0, 1]] * 2, [0.5, 0.5])
