@@ -186,7 +186,7 @@ struct ss_ctx {
 
     // scene
     uint64_t n = 0;
-    ss::DevBuf mean_op, scale, quat;
+    ss::DevBuf mean_op, scale, quat, cov3; // cov3: [9][n] f64 3-D covariances (per scene)
 
     // per-view pipeline lanes (scratch + stream each)
     static constexpr uint32_t kMaxLanes = 4;
@@ -334,6 +334,7 @@ Geometry run_geometry(ss_ctx* c, Lane& L, cudaStream_t s, const ss_camera& cam) 
         p.mean_op = c->mean_op.as<float4>();
         p.scale = c->scale.as<float4>();
         p.quat = c->quat.as<float4>();
+        p.cov3 = c->cov3.as<double>();
         p.n = N;
         p.cam = cam;
         p.rec = rec;
@@ -795,7 +796,7 @@ void ss_destroy(ss_ctx* c) {
     cudaStreamSynchronize(c->stream);
     for (auto& L : c->lanes) cudaStreamSynchronize(L.stream);
     if (c->cstream) cudaStreamSynchronize(c->cstream);
-    ss::DevBuf* bufs[] = {&c->mean_op, &c->scale, &c->quat, &c->cub_tmp, &c->num_sel, &c->info, &c->vstat, &c->pix_count,
+    ss::DevBuf* bufs[] = {&c->mean_op, &c->scale, &c->quat, &c->cov3, &c->cub_tmp, &c->num_sel, &c->info, &c->vstat, &c->pix_count,
                           &c->pix_offset, &c->entries, &c->per_pixel_total, &c->alpha, &c->color, &c->image, &c->counters, &c->sums_buf,
                           &c->totals_buf, &c->store_rows, &c->store_ids, &c->qbuf, &c->qnorm, &c->scores,
                           &c->topk_ids, &c->topk_sims, &c->sel_flags, &c->thr_keys, &c->thr_keys_sorted, &c->thr_ids,
@@ -882,6 +883,8 @@ int ss_scene_set(ss_ctx* c, const float* mean, const float* scale, const float* 
         SS_CUDA(cudaMemcpyAsync(c->mean_op.ensure(bytes), a.data(), n * 16, cudaMemcpyHostToDevice, c->stream));
         SS_CUDA(cudaMemcpyAsync(c->scale.ensure(bytes), b.data(), n * 16, cudaMemcpyHostToDevice, c->stream));
         SS_CUDA(cudaMemcpyAsync(c->quat.ensure(bytes), q.data(), n * 16, cudaMemcpyHostToDevice, c->stream));
+        auto* cov = static_cast<double*>(c->cov3.ensure(std::max<uint64_t>(n, 1) * 72));
+        own_launch(c, launch_cov3d(c->scale.as<float4>(), c->quat.as<float4>(), n, cov, c->stream), SS_K_PROJECT);
         SS_CUDA(cudaStreamSynchronize(c->stream));
     });
 }
@@ -901,6 +904,7 @@ int ss_project(ss_ctx* c, const ss_camera* cam, ss_projected* out) {
         p.mean_op = c->mean_op.as<float4>();
         p.scale = c->scale.as<float4>();
         p.quat = c->quat.as<float4>();
+        p.cov3 = c->cov3.as<double>();
         p.n = N;
         p.cam = *cam;
         p.rec = static_cast<SplatRec*>(L.rec.ensure(N * sizeof(SplatRec)));

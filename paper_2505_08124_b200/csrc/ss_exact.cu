@@ -37,6 +37,51 @@ constexpr double kMahalanobisSqCutoff = 9.0; // rasterizer.hpp:26
 // inner loop (non-const so they stay constant-bank operands)
 __device__ __constant__ double kCompositeConst[4] = {kAlphaMax, kAlphaSkip, kWeightCutoff, kTransmittanceFloor};
 
+// ------------------------------------------------------- 3-D covariance
+// scene.hpp:33-37 covariance3d: Eigen quaternion normalize (2-wide redux) +
+// toRotationMatrix, then R * diag(s^2) * R^T.  It does not depend on the
+// camera, so it is evaluated once per scene (same operation order as the
+// reference) and projection reads the nine doubles (SoA, [9][n]).
+__global__ void __launch_bounds__(256) cov3d_kernel(const float4* __restrict__ scale, const float4* __restrict__ quat,
+                                                    uint64_t n, double* __restrict__ cov3) {
+    const uint64_t id = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= n) return;
+    const float4 q = quat[id];
+    double qx = q.x, qy = q.y, qz = q.z, qw = q.w;
+    const double n2 = da(da(dm(qx, qx), dm(qz, qz)), da(dm(qy, qy), dm(qw, qw)));
+    if (n2 > 0.0) {
+        const double nn = __dsqrt_rn(n2);
+        qx = dd(qx, nn);
+        qy = dd(qy, nn);
+        qz = dd(qz, nn);
+        qw = dd(qw, nn);
+    }
+    const double tx = dm(2.0, qx), ty = dm(2.0, qy), tz = dm(2.0, qz);
+    const double twx = dm(tx, qw), twy = dm(ty, qw), twz = dm(tz, qw);
+    const double txx = dm(tx, qx), txy = dm(ty, qx), txz = dm(tz, qx);
+    const double tyy = dm(ty, qy), tyz = dm(tz, qy), tzz = dm(tz, qz);
+    double R[9];
+    R[0] = ds(1.0, da(tyy, tzz));
+    R[1] = ds(txy, twz);
+    R[2] = da(txz, twy);
+    R[3] = da(txy, twz);
+    R[4] = ds(1.0, da(txx, tzz));
+    R[5] = ds(tyz, twx);
+    R[6] = ds(txz, twy);
+    R[7] = da(tyz, twx);
+    R[8] = ds(1.0, da(txx, tyy));
+    const float4 sc = scale[id];
+    const double s0 = sc.x, s1 = sc.y, s2c = sc.z;
+    const double s2[3] = {dm(s0, s0), dm(s1, s1), dm(s2c, s2c)};
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            cov3[(size_t)(3 * i + j) * n + id] = da(dm(dm(R[3 * i], s2[0]), R[3 * j]),
+                                                    da(dm(dm(R[3 * i + 1], s2[1]), R[3 * j + 1]),
+                                                       dm(dm(R[3 * i + 2], s2[2]), R[3 * j + 2])));
+}
+
 // ---------------------------------------------------------------- project
 // One thread per Gaussian (id order).  scene.hpp:33-37 covariance3d +
 // projection.hpp:33-55 project_gaussian + rasterizer.hpp:66-71 conic_of +
@@ -61,42 +106,10 @@ __global__ void __launch_bounds__(256) project_kernel(ProjectParams p) {
             const double mu_x = da(dd(dm(cam.fx, xc[0]), z), cam.cx);
             const double mu_y = da(dd(dm(cam.fy, xc[1]), z), cam.cy);
 
-            // quaternion normalize (Eigen 2-wide redux) + toRotationMatrix
-            const float4 q = p.quat[id];
-            double qx = q.x, qy = q.y, qz = q.z, qw = q.w;
-            const double n2 = da(da(dm(qx, qx), dm(qz, qz)), da(dm(qy, qy), dm(qw, qw)));
-            if (n2 > 0.0) {
-                const double nn = __dsqrt_rn(n2);
-                qx = dd(qx, nn);
-                qy = dd(qy, nn);
-                qz = dd(qz, nn);
-                qw = dd(qw, nn);
-            }
-            const double tx = dm(2.0, qx), ty = dm(2.0, qy), tz = dm(2.0, qz);
-            const double twx = dm(tx, qw), twy = dm(ty, qw), twz = dm(tz, qw);
-            const double txx = dm(tx, qx), txy = dm(ty, qx), txz = dm(tz, qx);
-            const double tyy = dm(ty, qy), tyz = dm(tz, qy), tzz = dm(tz, qz);
-            double R[9];
-            R[0] = ds(1.0, da(tyy, tzz));
-            R[1] = ds(txy, twz);
-            R[2] = da(txz, twy);
-            R[3] = da(txy, twz);
-            R[4] = ds(1.0, da(txx, tzz));
-            R[5] = ds(tyz, twx);
-            R[6] = ds(txz, twy);
-            R[7] = da(tyz, twx);
-            R[8] = ds(1.0, da(txx, tyy));
-            const float4 sc = p.scale[id];
-            const double s0 = sc.x, s1 = sc.y, s2c = sc.z;
-            const double s2[3] = {dm(s0, s0), dm(s1, s1), dm(s2c, s2c)};
+            // scene.hpp:33-37 covariance3d, cached per scene (cov3d_kernel)
             double S[9];
 #pragma unroll
-            for (int i = 0; i < 3; ++i)
-#pragma unroll
-                for (int j = 0; j < 3; ++j)
-                    S[3 * i + j] = da(dm(dm(R[3 * i], s2[0]), R[3 * j]),
-                                      da(dm(dm(R[3 * i + 1], s2[1]), R[3 * j + 1]),
-                                         dm(dm(R[3 * i + 2], s2[2]), R[3 * j + 2])));
+            for (int k = 0; k < 9; ++k) S[k] = __ldg(p.cov3 + (size_t)k * p.n + id);
             const double zz = dm(z, z);
             const double J00 = dd(cam.fx, z), J02 = dd(dm(-cam.fx, xc[0]), zz);
             const double J11 = dd(cam.fy, z), J12 = dd(dm(-cam.fy, xc[1]), zz);
@@ -489,6 +502,12 @@ cudaError_t launch_raster(const RasterParams& p, int mode, uint32_t tiles, cudaS
 }
 
 } // namespace
+
+cudaError_t launch_cov3d(const float4* scale, const float4* quat, uint64_t n, double* cov3, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    cov3d_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(scale, quat, n, cov3);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_project(const ProjectParams& p, cudaStream_t s) {
     if (p.n == 0) return cudaSuccess;

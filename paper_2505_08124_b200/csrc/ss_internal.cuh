@@ -43,6 +43,7 @@ struct ProjectParams {
     const float4* mean_op; // x, y, z, opacity
     const float4* scale;   // sx, sy, sz, -
     const float4* quat;    // x, y, z, w (Eigen coeffs order)
+    const double* cov3;    // [9][n] 3-D covariances (cov3d_kernel, per scene)
     uint64_t n;
     ss_camera cam;
     SplatRec* rec;        // [n] by gid
@@ -82,6 +83,7 @@ struct RasterParams {
 
 // Kernel launchers (return cudaError_t of the launch).
 cudaError_t launch_project(const ProjectParams& p, cudaStream_t s);
+cudaError_t launch_cov3d(const float4* scale, const float4* quat, uint64_t n, double* cov3, cudaStream_t s);
 cudaError_t launch_raster_count(const RasterParams& p, int mode, uint32_t tiles, cudaStream_t s);
 cudaError_t launch_raster_capture(const RasterParams& p, int mode, uint32_t tiles, cudaStream_t s);
 cudaError_t launch_raster_render(const RasterParams& p, int mode, uint32_t tiles, cudaStream_t s);
