@@ -95,9 +95,10 @@ int ss_synchronize(ss_ctx* ctx);
  * for stores of >= 16384 rows with dim % 64 == 0 and dim <= 512), 1 = exact
  * scan only,
  * 2 = tensor-core path whenever dim allows.  Results are identical.
- * SS_OPT_CONTRACT_GROUP: views contracted together (1..4, default 1): each
- * touched Gaussian's row is read and written once per group; the fp32
- * operation order per row is the same for every group size.
+ * SS_OPT_CONTRACT_GROUP: views contracted together (1..4; default 0 = auto:
+ * three consecutive views with D = 512 and <= 64 masks each, other views
+ * alone): each touched Gaussian's row is read and written once per group; the
+ * fp32 operation order per row is the same for every group size.
  * SS_OPT_BIN_PATH: tile lists from 0 / 1 = stable key sort (default),
  * 2 = direct count/scan/scatter binning (views of <= 18000 16x16 tiles;
  * error above).  The tile lists are identical. */

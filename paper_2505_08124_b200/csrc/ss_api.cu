@@ -197,11 +197,12 @@ struct ss_ctx {
     // contraction group: consecutive views whose contraction is issued together
     std::vector<ss::GroupMember> group;
     cudaStream_t cstream = nullptr;      // group contractions (keeps lanes free)
-    uint32_t group_max = 1;              // SS_OPT_CONTRACT_GROUP
+    uint32_t group_max = 0;              // SS_OPT_CONTRACT_GROUP (0 = auto)
     cudaEvent_t group_done = nullptr;
     bool group_done_valid = false;
     ss::DevBuf cub_tmp, num_sel, info; // store / query scratch
     ss::DevBuf vstat; // per-view status of the last batch
+    ss::DevBuf union_list, union_count; // group contraction scratch
     uint64_t cap_n_surv = 0;
     ss::ViewInfo* h_init = nullptr;    // pinned
     uint32_t* h_u32 = nullptr;         // pinned scratch
@@ -531,6 +532,8 @@ void build_mask_bits(ss_ctx* c, Lane& L, cudaStream_t s, const ss_camera& cam, c
 // Issues the contraction of the views gathered in c->group on the stream of
 // the last one: after every member's compositor and after the previous
 // group's contraction (the shared sums are updated in view order).
+constexpr uint32_t kAutoGroup = 3; // views per group under SS_OPT_CONTRACT_GROUP = 0
+
 void flush_group(ss_ctx* c) {
     if (c->group.empty()) return;
     // in order: groups contract one after another on their own stream; with a
@@ -557,6 +560,10 @@ void flush_group(ss_ctx* c) {
     q.totals = c->totals;
     q.count_pairs = 1;
     q.cum = c->counters.as<unsigned long long>();
+    if (q.n_members > 1) {
+        q.union_list = static_cast<uint2*>(c->union_list.ensure(std::max<uint64_t>(c->n * q.n_members, 1) * 8));
+        q.union_count = static_cast<unsigned int*>(c->union_count.ensure(16));
+    }
     {
         Scope sc(c, st, SS_K_CONTRACT);
         own_launch(c, launch_contract(q, c->n * q.n_members, st), SS_K_CONTRACT);
@@ -631,11 +638,16 @@ void encode_one(ss_ctx* c, Lane& L, const ss_camera& cam, const ss_view_masks* v
             own_launch(c, launch_raster_fused(p, mode, g.tiles, s), SS_K_RASTER);
         }
         SS_CUDA(cudaEventRecord(L.raster_done, s));
+        // auto grouping: only views the shared-memory group kernel takes
+        // (D = 512, <= 64 masks) are contracted three at a time
+        if (c->group_max == 0 && !(c->dim == 512 && M <= 64)) flush_group(c);
         S->in_group = true;
         c->group.push_back(GroupMember{&L, S, M, d_clip});
     }
     SS_CUDA(cudaMemcpyAsync(vstat_slot, L.info.p, sizeof(ViewInfo), cudaMemcpyDeviceToDevice, s));
-    if (c->group.size() >= std::min<uint32_t>(c->group_max, kMaxGroup)) flush_group(c);
+    const uint32_t cap = c->group_max ? std::min<uint32_t>(c->group_max, kMaxGroup)
+                                      : (c->dim == 512 && M <= 64 ? kAutoGroup : 1u);
+    if (c->group.size() >= cap) flush_group(c);
 }
 
 // Encodes a batch of views with no per-view host synchronisation; the host
@@ -796,7 +808,7 @@ void ss_destroy(ss_ctx* c) {
     cudaStreamSynchronize(c->stream);
     for (auto& L : c->lanes) cudaStreamSynchronize(L.stream);
     if (c->cstream) cudaStreamSynchronize(c->cstream);
-    ss::DevBuf* bufs[] = {&c->mean_op, &c->scale, &c->quat, &c->cov3, &c->cub_tmp, &c->num_sel, &c->info, &c->vstat, &c->pix_count,
+    ss::DevBuf* bufs[] = {&c->mean_op, &c->scale, &c->quat, &c->cov3, &c->cub_tmp, &c->num_sel, &c->info, &c->vstat, &c->union_list, &c->union_count, &c->pix_count,
                           &c->pix_offset, &c->entries, &c->per_pixel_total, &c->alpha, &c->color, &c->image, &c->counters, &c->sums_buf,
                           &c->totals_buf, &c->store_rows, &c->store_ids, &c->qbuf, &c->qnorm, &c->scores,
                           &c->topk_ids, &c->topk_sims, &c->sel_flags, &c->thr_keys, &c->thr_keys_sorted, &c->thr_ids,
@@ -836,8 +848,8 @@ int ss_set_option(ss_ctx* c, int option, int64_t value) {
                 throw Error(SS_ERR_CONTRACT, "SS_OPT_LANES must be between 1 and 4");
             c->n_lanes = (uint32_t)value;
         } else if (option == SS_OPT_CONTRACT_GROUP) {
-            if (value < 1 || value > (int64_t)kMaxGroup)
-                throw Error(SS_ERR_CONTRACT, "SS_OPT_CONTRACT_GROUP must be between 1 and 4");
+            if (value < 0 || value > (int64_t)kMaxGroup)
+                throw Error(SS_ERR_CONTRACT, "SS_OPT_CONTRACT_GROUP must be between 0 (auto) and 4");
             c->group_max = (uint32_t)value;
         } else if (option == SS_OPT_QUERY_PATH) {
             if (value < 0 || value > 2) throw Error(SS_ERR_CONTRACT, "SS_OPT_QUERY_PATH must be 0, 1 or 2");

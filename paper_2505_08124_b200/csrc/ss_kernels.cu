@@ -630,40 +630,268 @@ __global__ void __launch_bounds__(256) contract_kernel(ContractParams p) {
     }
 }
 
+constexpr uint32_t kContractThreads = 768; // 24 warps x <= 85 registers (row + prefetched row)
+
 // Single-view contraction with the view's CLIP rows (M <= 64, D = 512)
-// staged in shared memory: one 1024-thread CTA per SM, persistent over the
-// touched list.  Same per-row operation order as contract_kernel.
-__global__ void __launch_bounds__(1024, 1) contract_smem_kernel(ContractParams p) {
+// staged in shared memory: one 768-thread CTA per SM, persistent over the
+// touched list.  Same per-row operation order as contract_kernel.  Software
+// pipelined: a warp's next 32 list entries are loaded one per lane, and the
+// next Gaussian's row, total and mask weights are in flight while the
+// current one is contracted (every Gaussian appears once in the list, so no
+// other warp touches a prefetched row).
+__global__ void __launch_bounds__(kContractThreads, 1) contract_smem_kernel(ContractParams p) {
     extern __shared__ float4 sclip4[]; // n_masks x 128 float4
     const ContractMember& m = p.m[0];
     const uint32_t n4 = m.n_masks * 128u;
     const float4* g4 = reinterpret_cast<const float4*>(m.clip);
     for (uint32_t i = threadIdx.x; i < n4; i += blockDim.x) sclip4[i] = __ldg(g4 + i);
     __syncthreads();
-    ContractMember ms = m;
-    ms.clip = reinterpret_cast<const float*>(sclip4);
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const unsigned long long total = *m.touched_count;
+    const uint32_t M = m.n_masks;
     unsigned long long pairs = 0;
-    for (uint64_t t = warp0; t < total; t += nwarps) {
-        const uint32_t gid = m.touched_list[t];
-        float* row = p.sums + (size_t)gid * p.dim;
+    auto batch = [&](uint64_t t0) { // lane i: the entry of iteration t0 + i * nwarps
+        const uint64_t tt = t0 + (uint64_t)lane * nwarps;
+        return tt < total ? __ldg(m.touched_list + tt) : 0u;
+    };
+    auto fetch = [&](uint32_t gid, float4 (&r)[4], float& w, float& v0, float& v1) {
+        const float4* row = reinterpret_cast<const float4*>(p.sums + (size_t)gid * 512u);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) r[q] = row[lane + 32 * q];
+        w = p.totals[gid];
+        const float* accrow = m.acc + (size_t)gid * M;
+        v0 = lane < M ? accrow[lane] : 0.0f;
+        v1 = lane + 32u < M ? accrow[lane + 32u] : 0.0f;
+    };
+    uint64_t t = warp0;
+    if (t < total) {
+        uint32_t gb = batch(t), k = 0;
+        uint32_t gid = __shfl_sync(0xffffffffu, gb, 0);
         float4 racc[4];
+        float wsum, v0, v1;
+        fetch(gid, racc, wsum, v0, v1);
+        for (; t < total; t += nwarps) {
+            const uint64_t tn = t + nwarps;
+            if (++k == 32u) {
+                gb = batch(tn);
+                k = 0;
+            }
+            const uint32_t ngid = __shfl_sync(0xffffffffu, gb, k);
+            float4 nacc[4];
+            float nw = 0.0f, nv0 = 0.0f, nv1 = 0.0f;
+            if (tn < total) fetch(ngid, nacc, nw, nv0, nv1);
+            // contract_member<true, true> on the prefetched mask weights
+            float* accrow = m.acc + (size_t)gid * M;
+            float vsum = 0.0f;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) racc[q] = reinterpret_cast<const float4*>(row)[lane + 32 * q];
-        float wsum = p.totals[gid];
-        float vs = 0.0f;
-        contract_member<true, true>(ms, gid, lane, p.dim, row, racc, vs, pairs);
-        wsum += vs;
+            for (uint32_t c = 0; c < 64u; c += 32u) {
+                if (c >= M) break;
+                const float v = c == 0 ? v0 : v1;
+                if (v != 0.0f) accrow[c + lane] = 0.0f;
+                vsum += v;
+                uint32_t bal = __ballot_sync(0xffffffffu, v != 0.0f);
+                pairs += __popc(bal);
+                while (bal) {
+                    const int src = __ffs(bal) - 1;
+                    bal &= bal - 1;
+                    const float w = __shfl_sync(0xffffffffu, v, src);
+                    const float4* e = sclip4 + (size_t)(c + src) * 128u;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) reinterpret_cast<float4*>(row)[lane + 32 * q] = racc[q];
-        if (lane == 0) p.totals[gid] = wsum;
+                    for (int q = 0; q < 4; ++q) {
+                        const float4 ev = e[lane + 32 * q];
+                        racc[q].x += w * ev.x;
+                        racc[q].y += w * ev.y;
+                        racc[q].z += w * ev.z;
+                        racc[q].w += w * ev.w;
+                    }
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) vsum += __shfl_xor_sync(0xffffffffu, vsum, o);
+            wsum += vsum;
+            float4* row = reinterpret_cast<float4*>(p.sums + (size_t)gid * 512u);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) row[lane + 32 * q] = racc[q];
+            if (lane == 0) p.totals[gid] = wsum;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) racc[q] = nacc[q];
+            gid = ngid;
+            wsum = nw;
+            v0 = nv0;
+            v1 = nv1;
+        }
     }
     if (p.count_pairs) {
         if (lane == 0 && pairs) atomicAdd(p.cum + 1, pairs);
         if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(p.cum, total);
+    }
+}
+
+// Group contraction (2-3 consecutive views, D = 512, M <= 64 each).
+//  1. group_union_kernel: one thread per (member, list entry); an entry whose
+//     Gaussian no earlier member touched becomes one union entry (gid, mask of
+//     the members that touched it) -- the union of the lists, each Gaussian once.
+//  2. contract_group_pass_kernel<H>, H = 0, 1: the members' CLIP rows for D-half
+//     H staged in shared memory (3 x 64 masks x 1 KB = 192 KB), one warp per
+//     union entry with the next entry's half row and mask weights in flight;
+//     every touched half row is read and written once for the whole group.
+// Per element the fp32 sequence is the single-view one (views in order, masks
+// in order within a view), so the sums are bit-identical to contracting the
+// views one by one.  Mask weights are cleared and totals updated in pass 1.
+__global__ void __launch_bounds__(256) group_union_kernel(ContractParams p, uint2* ulist, unsigned int* ucount) {
+    const uint32_t nm = p.n_members;
+    unsigned long long cnt[kMaxGroup - 1], all = 0;
+#pragma unroll
+    for (uint32_t j = 0; j < kMaxGroup - 1; ++j) {
+        cnt[j] = j < nm ? *p.m[j].touched_count : 0ull;
+        all += cnt[j];
+    }
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < all; base += stride) {
+        uint64_t e = base + lane;
+        uint32_t gid = 0, mask = 0;
+        if (e < all) {
+            uint32_t j = 0;
+#pragma unroll
+            for (uint32_t k = 0; k < kMaxGroup - 2; ++k)
+                if (j == k && e >= cnt[k]) {
+                    e -= cnt[k];
+                    j = k + 1;
+                }
+            gid = __ldg(p.m[j].touched_list + e);
+            mask = 1u << j;
+            for (uint32_t k = 0; k < nm; ++k) {
+                if (k == j || __ldg(p.m[k].touched + gid) != p.m[k].gen) continue;
+                if (k < j) { // an earlier member owns it
+                    mask = 0;
+                    break;
+                }
+                mask |= 1u << k;
+            }
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, mask != 0u);
+        if (!bal) continue;
+        const uint32_t leader = __ffs(bal) - 1;
+        uint32_t slot = 0;
+        if (lane == leader) slot = atomicAdd(ucount, (unsigned int)__popc(bal));
+        slot = __shfl_sync(0xffffffffu, slot, leader);
+        if (mask) ulist[slot + __popc(bal & ((1u << lane) - 1u))] = make_uint2(gid, mask);
+    }
+}
+
+template <uint32_t H>
+__global__ void __launch_bounds__(1024, 1) contract_group_pass_kernel(ContractParams p, const uint2* ulist,
+                                                                     const unsigned int* ucount) {
+    extern __shared__ float4 sclip4[]; // per member: n_masks x 64 float4 (D-half H)
+    __shared__ uint32_t soff[kMaxGroup];
+    const uint32_t nm = p.n_members;
+    if (threadIdx.x == 0) {
+        uint32_t off = 0;
+        for (uint32_t i = 0; i < kMaxGroup; ++i) {
+            soff[i] = off;
+            off += i < nm ? p.m[i].n_masks * 64u : 0u;
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = 0; i < nm; ++i) {
+        const float4* g4 = reinterpret_cast<const float4*>(p.m[i].clip);
+        const uint32_t n = p.m[i].n_masks * 64u;
+        for (uint32_t e = threadIdx.x; e < n; e += blockDim.x)
+            sclip4[soff[i] + e] = __ldg(g4 + (size_t)(e >> 6) * 128u + H * 64u + (e & 63u));
+    }
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t total = *ucount;
+    unsigned long long pairs = 0;
+    // one union entry's inputs: half row, total (pass 1), two mask-weight words per member
+    struct In {
+        float4 r[2];
+        float w;
+        float v[kMaxGroup - 1][2];
+    };
+    auto fetch = [&](uint2 u, In& x) {
+        const float4* row = reinterpret_cast<const float4*>(p.sums + (size_t)u.x * 512u) + H * 64u;
+        x.r[0] = row[lane];
+        x.r[1] = row[lane + 32];
+        x.w = H ? p.totals[u.x] : 0.0f;
+#pragma unroll
+        for (uint32_t j = 0; j < kMaxGroup - 1; ++j) {
+            x.v[j][0] = x.v[j][1] = 0.0f;
+            if (j < nm && ((u.y >> j) & 1u)) {
+                const float* accrow = p.m[j].acc + (size_t)u.x * p.m[j].n_masks;
+                if (lane < p.m[j].n_masks) x.v[j][0] = accrow[lane];
+                if (lane + 32u < p.m[j].n_masks) x.v[j][1] = accrow[lane + 32u];
+            }
+        }
+    };
+    uint64_t t = warp0;
+    if (t < total) {
+        uint2 u = ulist[t];
+        In cur;
+        fetch(u, cur);
+        for (; t < total; t += nwarps) {
+            const uint64_t tn = t + nwarps;
+            uint2 un = make_uint2(0u, 0u);
+            In nxt;
+            if (tn < total) {
+                un = ulist[tn];
+                fetch(un, nxt);
+            }
+            float wsum = cur.w;
+#pragma unroll
+            for (uint32_t j = 0; j < kMaxGroup - 1; ++j) {
+                if (j >= nm || !((u.y >> j) & 1u)) continue;
+                const uint32_t M = p.m[j].n_masks;
+                float* accrow = p.m[j].acc + (size_t)u.x * M;
+                const float4* clip = sclip4 + soff[j];
+                float vsum = 0.0f;
+#pragma unroll
+                for (uint32_t c = 0; c < 2u; ++c) {
+                    if (32u * c >= M) break;
+                    const float v = cur.v[j][c];
+                    if (H && v != 0.0f) accrow[32u * c + lane] = 0.0f;
+                    vsum += v;
+                    uint32_t bal = __ballot_sync(0xffffffffu, v != 0.0f);
+                    if (H) pairs += __popc(bal);
+                    while (bal) {
+                        const int src = __ffs(bal) - 1;
+                        bal &= bal - 1;
+                        const float w = __shfl_sync(0xffffffffu, v, src);
+                        const float4* e = clip + (size_t)(32u * c + src) * 64u;
+#pragma unroll
+                        for (int q = 0; q < 2; ++q) {
+                            const float4 ev = e[lane + 32 * q];
+                            cur.r[q].x += w * ev.x;
+                            cur.r[q].y += w * ev.y;
+                            cur.r[q].z += w * ev.z;
+                            cur.r[q].w += w * ev.w;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) vsum += __shfl_xor_sync(0xffffffffu, vsum, o);
+                wsum += vsum;
+            }
+            float4* row = reinterpret_cast<float4*>(p.sums + (size_t)u.x * 512u) + H * 64u;
+            row[lane] = cur.r[0];
+            row[lane + 32] = cur.r[1];
+            if (H && lane == 0) p.totals[u.x] = wsum;
+            u = un;
+            cur = nxt;
+        }
+    }
+    if (H && p.count_pairs) {
+        if (lane == 0 && pairs) atomicAdd(p.cum + 1, pairs);
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            unsigned long long all = 0;
+            for (uint32_t i = 0; i < nm; ++i) all += *p.m[i].touched_count;
+            atomicAdd(p.cum, all);
+        }
     }
 }
 
@@ -1072,7 +1300,35 @@ cudaError_t launch_contract(const ContractParams& p, uint64_t max_touched, cudaS
             if (e != cudaSuccess) return e;
             configured[dev].store(1);
         }
-        contract_smem_kernel<<<sms, 1024, smem, s>>>(p);
+        contract_smem_kernel<<<sms, kContractThreads, smem, s>>>(p);
+        return cudaGetLastError();
+    }
+    uint32_t group_masks = 0;
+    bool small = true;
+    for (uint32_t i = 0; i < p.n_members; ++i) {
+        group_masks += p.m[i].n_masks;
+        small = small && p.m[i].n_masks <= 64;
+    }
+    if (p.n_members >= 2 && p.n_members < kMaxGroup && p.dim == 512 && small && group_masks <= 192 && p.union_list) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        static std::atomic<int> configured_g[64] = {};
+        if (dev >= 0 && dev < 64 && !configured_g[dev].load()) {
+            cudaError_t e = cudaFuncSetAttribute(contract_group_pass_kernel<0>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 192 * 1024);
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(contract_group_pass_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         192 * 1024);
+            if (e != cudaSuccess) return e;
+            configured_g[dev].store(1);
+        }
+        cudaError_t e = cudaMemsetAsync(p.union_count, 0, sizeof(unsigned int), s);
+        if (e != cudaSuccess) return e;
+        group_union_kernel<<<(unsigned)sms * 4u, 256, 0, s>>>(p, p.union_list, p.union_count);
+        const size_t smem = (size_t)group_masks * 1024u;
+        contract_group_pass_kernel<0><<<sms, 1024, smem, s>>>(p, p.union_list, p.union_count);
+        contract_group_pass_kernel<1><<<sms, 1024, smem, s>>>(p, p.union_list, p.union_count);
         return cudaGetLastError();
     }
     if (p.dim == 512)

@@ -26,6 +26,8 @@ struct ContractParams {
     float* totals;         // [N]
     int count_pairs;
     unsigned long long* cum; // running [G_v, K_v] totals (summed over views)
+    uint2* union_list;       // group scratch: (gid, member mask), sum of the members' lists
+    unsigned int* union_count;
 };
 
 cudaError_t launch_rle_to_bits(const uint32_t* runs, const uint64_t* run_offsets, uint32_t n_masks, uint32_t words,
