@@ -39,7 +39,7 @@ PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
 FALLBACK_HBM = 6650.0
 
 
-DEFAULT_LANES = 4
+DEFAULT_LANES = 5
 
 
 def ncu_traffic(kernel):

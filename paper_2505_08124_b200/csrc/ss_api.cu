@@ -189,10 +189,10 @@ struct ss_ctx {
     ss::DevBuf mean_op, scale, quat, cov3; // cov3: [9][n] f64 3-D covariances (per scene)
 
     // per-view pipeline lanes (scratch + stream each)
-    static constexpr uint32_t kMaxLanes = 4;
+    static constexpr uint32_t kMaxLanes = 6;
     ss::Lane lanes[kMaxLanes];
     uint32_t next_lane = 0;
-    uint32_t n_lanes = 4;
+    uint32_t n_lanes = 5;
     cudaEvent_t ev_user = nullptr;
     // contraction group: consecutive views whose contraction is issued together
     std::vector<ss::GroupMember> group;
@@ -845,7 +845,7 @@ int ss_set_option(ss_ctx* c, int option, int64_t value) {
         if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
         if (option == SS_OPT_LANES) {
             if (value < 1 || value > (int64_t)ss_ctx::kMaxLanes)
-                throw Error(SS_ERR_CONTRACT, "SS_OPT_LANES must be between 1 and 4");
+                throw Error(SS_ERR_CONTRACT, "SS_OPT_LANES must be between 1 and 6");
             c->n_lanes = (uint32_t)value;
         } else if (option == SS_OPT_CONTRACT_GROUP) {
             if (value < 0 || value > (int64_t)kMaxGroup)
