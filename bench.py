@@ -42,11 +42,11 @@ FALLBACK_HBM = 6650.0
 DEFAULT_LANES = 5
 
 
-def ncu_traffic(kernel):
-    """DRAM bytes per launch of `kernel` from the committed ncu capture, or None."""
+def ncu_traffic(kernel, field="bytes_per_launch"):
+    """DRAM bytes (or another per-launch count) of `kernel` from the committed ncu capture, or None."""
     try:
         t = json.loads((Path(__file__).resolve().parent / "profiles" / "ncu_traffic.json").read_text())
-        return t[kernel]["bytes_per_launch"]
+        return t[kernel][field]
     except Exception:
         return None
 
@@ -477,6 +477,19 @@ def main():
                 "algorithmic_bytes_per_launch": dk["gb_per_step"] * 1e9 / max(dk["launches_per_step"], 1), "peak_source": f"{peak_kind} (MEASURED_PEAKS.json)",
                 "share_of_step": dk["share_of_serial_step"],
                 "timing": "CUDA events around each launch on its stream, one extra pass with lanes serialised"}
+    # the compositor is bound by the fp64 pipe, not HBM; its fp64
+    # operation count per c4 launch comes from the committed ncu capture, the
+    # peak from a DFMA probe run here
+    roofline_fp64 = None
+    ops = ncu_traffic(dom, "fp64_ops_per_launch") if args.config == "c4" else None
+    if ops:
+        t_launch = dk["ms_per_step"] / max(dk["launches_per_step"], 1) / 1e3
+        peak64 = ctx.probe_fp64_rate()
+        roofline_fp64 = {"bound": "fp64", "kernel": dom, "achieved": ops / t_launch / 1e12, "peak": peak64 / 1e12,
+                         "unit": "T fp64 lane-ops/s (DADD, DMUL, DFMA: one each)",
+                         "frac": ops / t_launch / peak64, "ops_per_launch": ops,
+                         "ops_source": "profiles/ncu_traffic.json (smsp__sass_thread_inst_executed_op_d{add,mul,fma})",
+                         "peak_source": "ss_probe_fp64_rate: eight DFMA chains per thread on every SM, this run"}
     steps = 1
     pass_bytes = sum(v["bytes"] for k, v in prof.items() if k not in ("h2d", "query"))
 
@@ -545,6 +558,7 @@ def main():
                        "l2": "inputs larger than L2 (N x 512 fp32 sums = %.1f GB RMW per pass)" % (N * D * 4 / 1e9),
                        "dataset_gen_seconds": gen_s},
             "roofline": roofline,
+            "roofline_fp64": roofline_fp64,
             "pass_algorithmic_gb": pass_bytes / 1e9,
             "pass_hbm_frac": pass_bytes / (ms_step / 1e3) / 1e9 / hbm,
             "kernels": kernels,

@@ -216,6 +216,10 @@ int ss_assign_classes(ss_ctx* ctx, const float* rows, const float* coverage, uin
  * total and maximum candidates per query, batches answered by the exact scan
  * after a candidate overflow. */
 int ss_query_stats(ss_ctx* ctx, uint64_t* out4);
+/* Measurement helper: the device's fp64 pipe rate in DFMA lane-operations
+ * per second (eight independent chains per thread on every SM), the
+ * denominator of the compositor's fp64 roofline in bench.py. */
+int ss_probe_fp64_rate(ss_ctx* ctx, double* lane_ops_per_s);
 /* Number of kernels this library launched (own + CUB) since reset. */
 int ss_launch_count(ss_ctx* ctx, uint64_t* own, uint64_t* cub);
 

@@ -71,6 +71,7 @@ def lib() -> C.CDLL:
         "ss_synchronize": (i32, [vp]),
         "ss_set_option": (i32, [vp, i32, C.c_int64]),
         "ss_query_stats": (i32, [vp, vp]),
+        "ss_probe_fp64_rate": (i32, [vp, vp]),
         "ss_scene_set_color": (i32, [vp, vp, u64]),
         "ss_render": (i32, [vp, C.POINTER(Camera), i32, pu64, pu64, pu64]),
         "ss_render_fetch_image": (i32, [vp, vp]),
@@ -364,6 +365,12 @@ class Context:
         out = np.zeros(4, np.uint64)
         check(self._L.ss_query_stats(self.h, out.ctypes.data_as(C.c_void_p)))
         return dict(zip(["tc_queries", "candidates", "max_candidates", "exact_fallbacks"], map(int, out)))
+
+    def probe_fp64_rate(self) -> float:
+        """DFMA lane-operations per second on this device (fp64 pipe peak)."""
+        out = C.c_double(0.0)
+        check(self._L.ss_probe_fp64_rate(self.h, C.byref(out)))
+        return float(out.value)
 
     def launch_count(self):
         a, b = C.c_uint64(), C.c_uint64()

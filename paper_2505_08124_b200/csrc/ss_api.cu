@@ -1639,6 +1639,14 @@ int ss_query_stats(ss_ctx* c, uint64_t* out4) {
     });
 }
 
+int ss_probe_fp64_rate(ss_ctx* c, double* lane_ops_per_s) {
+    return guarded([&] {
+        if (!c || !lane_ops_per_s) throw Error(SS_ERR_CONTRACT, "ctx or output is null");
+        set_device(c);
+        SS_CUDA(ss::probe_fp64_rate(lane_ops_per_s));
+    });
+}
+
 int ss_launch_count(ss_ctx* c, uint64_t* own, uint64_t* cub) {
     if (own) *own = c->launches_own;
     if (cub) *cub = c->launches_cub;

@@ -503,6 +503,52 @@ cudaError_t launch_raster(const RasterParams& p, int mode, uint32_t tiles, cudaS
 
 } // namespace
 
+namespace {
+// fp64 pipe probe (the compositor's roofline denominator):
+// eight independent DFMA chains per thread, every SM full.
+__global__ void __launch_bounds__(256) fp64_probe_kernel(double* out, uint32_t iters) {
+    double a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = 1.0 + 1e-9 * (double)(threadIdx.x + 8 * k);
+    const double m = 0.9999999, c = 1e-7;
+    for (uint32_t i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) a[k] = __fma_rn(a[k], m, c);
+    }
+    double sum = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sum += a[k];
+    if (sum == -1.0) out[0] = sum; // keeps the chains live
+}
+} // namespace
+
+cudaError_t probe_fp64_rate(double* lane_ops_per_s) {
+    int dev = 0, sms = 148;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint32_t iters = 8192, blocks = (uint32_t)sms * 8u;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    double best = 0.0;
+    for (int rep = 0; rep < 4; ++rep) { // first launch warms up
+        cudaEventRecord(a);
+        fp64_probe_kernel<<<blocks, 256>>>(nullptr, iters);
+        cudaEventRecord(b);
+        if ((e = cudaEventSynchronize(b)) != cudaSuccess) break;
+        float ms = 0.0f;
+        cudaEventElapsedTime(&ms, a, b);
+        const double rate = (double)blocks * 256.0 * 8.0 * iters / (ms * 1e-3);
+        if (rep > 0 && rate > best) best = rate;
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    *lane_ops_per_s = best;
+    return e;
+}
+
 cudaError_t launch_cov3d(const float4* scale, const float4* quat, uint64_t n, double* cov3, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     cov3d_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(scale, quat, n, cov3);

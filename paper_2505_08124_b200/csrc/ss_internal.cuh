@@ -83,6 +83,7 @@ struct RasterParams {
 
 // Kernel launchers (return cudaError_t of the launch).
 cudaError_t launch_project(const ProjectParams& p, cudaStream_t s);
+cudaError_t probe_fp64_rate(double* lane_ops_per_s); // DFMA lane-operations per second, whole device
 cudaError_t launch_cov3d(const float4* scale, const float4* quat, uint64_t n, double* cov3, cudaStream_t s);
 cudaError_t launch_raster_count(const RasterParams& p, int mode, uint32_t tiles, cudaStream_t s);
 cudaError_t launch_raster_capture(const RasterParams& p, int mode, uint32_t tiles, cudaStream_t s);

@@ -556,3 +556,10 @@ def test_encode_scene_api_vs_reference(gpu_ctx, ref, tmp_path, workers, contiguo
     assert sum(stats.worker_images) == 5 and len(stats.worker_entries) == workers
     assert sum(stats.worker_entries) == int(rstats[2])
 
+
+
+def test_fp64_probe_rate_is_plausible(gpu_ctx):
+    """ss_probe_fp64_rate (the compositor's fp64 roofline denominator): a B200
+    runs 64 fp64 lanes per SM per clock, 148 SMs at up to ~2 GHz."""
+    rate = gpu_ctx.probe_fp64_rate()
+    assert 5e12 < rate < 2.2e13, rate
