@@ -782,7 +782,9 @@ __global__ void __launch_bounds__(256) group_union_kernel(ContractParams p, uint
     }
 }
 
-template <uint32_t H>
+// MEMBERS: views in the group (<= 3); CH: 32-mask chunks per view (2: M <= 64,
+// 4: M <= 128); DIRECT: a single view, walked through its own touched list.
+template <uint32_t H, uint32_t MEMBERS, uint32_t CH, bool DIRECT>
 __global__ void __launch_bounds__(1024, 1) contract_group_pass_kernel(ContractParams p, const uint2* ulist,
                                                                      const unsigned int* ucount) {
     extern __shared__ float4 sclip4[]; // per member: n_masks x 64 float4 (D-half H)
@@ -806,13 +808,16 @@ __global__ void __launch_bounds__(1024, 1) contract_group_pass_kernel(ContractPa
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const uint64_t total = *ucount;
+    const uint64_t total = DIRECT ? *p.m[0].touched_count : *ucount;
+    auto entry = [&](uint64_t i) {
+        return DIRECT ? make_uint2(__ldg(p.m[0].touched_list + i), 1u) : ulist[i];
+    };
     unsigned long long pairs = 0;
-    // one union entry's inputs: half row, total (pass 1), two mask-weight words per member
+    // one union entry's inputs: half row, total (pass 1), CH mask-weight words per member
     struct In {
         float4 r[2];
         float w;
-        float v[kMaxGroup - 1][2];
+        float v[MEMBERS][CH];
     };
     auto fetch = [&](uint2 u, In& x) {
         const float4* row = reinterpret_cast<const float4*>(p.sums + (size_t)u.x * 512u) + H * 64u;
@@ -820,18 +825,20 @@ __global__ void __launch_bounds__(1024, 1) contract_group_pass_kernel(ContractPa
         x.r[1] = row[lane + 32];
         x.w = H ? p.totals[u.x] : 0.0f;
 #pragma unroll
-        for (uint32_t j = 0; j < kMaxGroup - 1; ++j) {
-            x.v[j][0] = x.v[j][1] = 0.0f;
+        for (uint32_t j = 0; j < MEMBERS; ++j) {
+#pragma unroll
+            for (uint32_t c = 0; c < CH; ++c) x.v[j][c] = 0.0f;
             if (j < nm && ((u.y >> j) & 1u)) {
                 const float* accrow = p.m[j].acc + (size_t)u.x * p.m[j].n_masks;
-                if (lane < p.m[j].n_masks) x.v[j][0] = accrow[lane];
-                if (lane + 32u < p.m[j].n_masks) x.v[j][1] = accrow[lane + 32u];
+#pragma unroll
+                for (uint32_t c = 0; c < CH; ++c)
+                    if (32u * c + lane < p.m[j].n_masks) x.v[j][c] = accrow[32u * c + lane];
             }
         }
     };
     uint64_t t = warp0;
     if (t < total) {
-        uint2 u = ulist[t];
+        uint2 u = entry(t);
         In cur;
         fetch(u, cur);
         for (; t < total; t += nwarps) {
@@ -839,19 +846,19 @@ __global__ void __launch_bounds__(1024, 1) contract_group_pass_kernel(ContractPa
             uint2 un = make_uint2(0u, 0u);
             In nxt;
             if (tn < total) {
-                un = ulist[tn];
+                un = entry(tn);
                 fetch(un, nxt);
             }
             float wsum = cur.w;
 #pragma unroll
-            for (uint32_t j = 0; j < kMaxGroup - 1; ++j) {
+            for (uint32_t j = 0; j < MEMBERS; ++j) {
                 if (j >= nm || !((u.y >> j) & 1u)) continue;
                 const uint32_t M = p.m[j].n_masks;
                 float* accrow = p.m[j].acc + (size_t)u.x * M;
                 const float4* clip = sclip4 + soff[j];
                 float vsum = 0.0f;
 #pragma unroll
-                for (uint32_t c = 0; c < 2u; ++c) {
+                for (uint32_t c = 0; c < CH; ++c) {
                     if (32u * c >= M) break;
                     const float v = cur.v[j][c];
                     if (H && v != 0.0f) accrow[32u * c + lane] = 0.0f;
@@ -1309,26 +1316,35 @@ cudaError_t launch_contract(const ContractParams& p, uint64_t max_touched, cudaS
         group_masks += p.m[i].n_masks;
         small = small && p.m[i].n_masks <= 64;
     }
-    if (p.n_members >= 2 && p.n_members < kMaxGroup && p.dim == 512 && small && group_masks <= 192 && p.union_list) {
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        static std::atomic<int> configured_g[64] = {};
-        if (dev >= 0 && dev < 64 && !configured_g[dev].load()) {
-            cudaError_t e = cudaFuncSetAttribute(contract_group_pass_kernel<0>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 192 * 1024);
-            if (e == cudaSuccess)
-                e = cudaFuncSetAttribute(contract_group_pass_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         192 * 1024);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    static std::atomic<int> configured_g[64] = {};
+    if (dev >= 0 && dev < 64 && !configured_g[dev].load()) {
+        const void* ks[] = {(const void*)contract_group_pass_kernel<0, 3, 2, false>,
+                            (const void*)contract_group_pass_kernel<1, 3, 2, false>,
+                            (const void*)contract_group_pass_kernel<0, 1, 4, true>,
+                            (const void*)contract_group_pass_kernel<1, 1, 4, true>};
+        for (const void* k : ks) {
+            cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 192 * 1024);
             if (e != cudaSuccess) return e;
-            configured_g[dev].store(1);
         }
+        configured_g[dev].store(1);
+    }
+    if (p.n_members >= 2 && p.n_members < kMaxGroup && p.dim == 512 && small && group_masks <= 192 && p.union_list) {
         cudaError_t e = cudaMemsetAsync(p.union_count, 0, sizeof(unsigned int), s);
         if (e != cudaSuccess) return e;
         group_union_kernel<<<(unsigned)sms * 4u, 256, 0, s>>>(p, p.union_list, p.union_count);
         const size_t smem = (size_t)group_masks * 1024u;
-        contract_group_pass_kernel<0><<<sms, 1024, smem, s>>>(p, p.union_list, p.union_count);
-        contract_group_pass_kernel<1><<<sms, 1024, smem, s>>>(p, p.union_list, p.union_count);
+        contract_group_pass_kernel<0, 3, 2, false><<<sms, 1024, smem, s>>>(p, p.union_list, p.union_count);
+        contract_group_pass_kernel<1, 3, 2, false><<<sms, 1024, smem, s>>>(p, p.union_list, p.union_count);
+        return cudaGetLastError();
+    }
+    if (p.n_members == 1 && p.dim == 512 && p.m[0].n_masks <= 128) {
+        // one view with 65..128 masks: its CLIP half-rows (<= 128 KB) per pass
+        const size_t smem = (size_t)p.m[0].n_masks * 1024u;
+        contract_group_pass_kernel<0, 1, 4, true><<<sms, 1024, smem, s>>>(p, nullptr, nullptr);
+        contract_group_pass_kernel<1, 1, 4, true><<<sms, 1024, smem, s>>>(p, nullptr, nullptr);
         return cudaGetLastError();
     }
     if (p.dim == 512)
