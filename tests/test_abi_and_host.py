@@ -166,3 +166,17 @@ def test_encode_scene_contract_errors_before_device():
         encode_scene(None, DatasetManifest(raster_width=4, raster_height=4), 0, 0)
     with pytest.raises(DataError):
         encode_scene(None, DatasetManifest(), 1, 0)
+
+
+def test_library_has_no_unresolved_internal_symbols():
+    """Every ss:: function the library calls is defined in it (a missing
+    definition would only surface at the first call on a GPU box)."""
+    import shutil
+    import subprocess
+    from paper_2505_08124_b200._lib import LIB_PATH
+    nm = shutil.which("nm")
+    if nm is None:
+        pytest.skip("nm not available")
+    out = subprocess.run([nm, "-D", "--undefined-only", str(LIB_PATH)], capture_output=True, text=True).stdout
+    missing = [line.split()[-1] for line in out.splitlines() if line.split() and line.split()[-1].startswith("_ZN2ss")]
+    assert not missing, missing
