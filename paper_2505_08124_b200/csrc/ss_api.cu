@@ -320,7 +320,7 @@ Geometry run_geometry(ss_ctx* c, Lane& L, cudaStream_t s, const ss_camera& cam) 
     const uint32_t bin_warps = bin_scatter_warps(g.tiles);
     if (c->bin_path == 2 && !bin_warps)
         throw Error(SS_ERR_CONTRACT, "SS_OPT_BIN_PATH=2: too many tiles for the direct binning path");
-    const bool direct = c->bin_path == 2;
+    const bool direct = c->bin_path == 2 || (c->bin_path == 0 && bin_warps != 0);
     if (!direct) {
         L.tkeys.ensure(L.list_cap * (g.k16 ? 2 : 4));
         L.tkeys_sorted.ensure(L.list_cap * (g.k16 ? 2 : 4));

@@ -466,31 +466,24 @@ __global__ void __launch_bounds__(WARPS * 32) bin_scatter_kernel(BinParams p) {
     __syncthreads();
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     constexpr uint32_t groups = kBinChunk / (WARPS * 32u);
-    uint16_t* mine = wh + (size_t)warp * p.tiles;
     const uint32_t below = (1u << lane) - 1u;
-    const uint32_t kbits = 32u - __clz(max(p.tiles, 2u) - 1u);
     const uint64_t r0 = base + (uint64_t)warp * groups * 32u + lane;
     auto load_box = [&](uint32_t g) {
         return r0 + g * 32u < n_surv ? p.rbox[r0 + g * 32u] : make_uint2(kCulledBox, kCulledBox);
     };
-    // lanes holding the same tile (ballots over the tile bits; cheaper than match.any)
-    auto peers = [&](bool valid, uint32_t t) {
-        uint32_t m = __ballot_sync(0xffffffffu, valid);
-        for (uint32_t b = 0; b < kbits; ++b) {
-            const uint32_t on = __ballot_sync(0xffffffffu, (t >> b) & 1u);
-            m &= ((t >> b) & 1u) ? on : ~on;
-        }
-        return m;
-    };
-    // 1. the warp's own per-tile counts
+    // the warp's u16 counters, addressed as packed pairs for shared-memory atomics
+    uint32_t* mine32 = reinterpret_cast<uint32_t*>(wh);
+    const uint32_t mine0 = warp * p.tiles; // element index of (warp, tile 0)
+    // 1. the warp's own per-tile counts (order-free: plain atomics)
     uint2 next = load_box(0);
     for (uint32_t g = 0; g < groups; ++g) {
         const uint2 box = next;
         if (g + 1 < groups) next = load_box(g + 1); // one group ahead
         for_each_instance(box, lane, p.tiles_x, [&](bool valid, uint32_t t, uint32_t) {
-            const uint32_t m = peers(valid, t);
-            if (valid && (m & below) == 0u) mine[t] = (uint16_t)(mine[t] + __popc(m));
-            __syncwarp();
+            if (valid) {
+                const uint32_t e = mine0 + t;
+                atomicAdd(mine32 + (e >> 1), 1u << (16u * (e & 1u)));
+            }
         });
     }
     __syncthreads();
@@ -518,14 +511,20 @@ __global__ void __launch_bounds__(WARPS * 32) bin_scatter_kernel(BinParams p) {
         }
         for_each_instance(box, lane, p.tiles_x, [&](bool valid, uint32_t t, uint32_t o) {
             const uint32_t gid = __shfl_sync(0xffffffffu, id, o);
-            const uint32_t m = peers(valid, t);
+            // slot from an atomic on the warp's counter; lanes of one round
+            // sharing a tile (rare: different ranks) are then re-ranked in lane
+            // order = rank order
+            const uint32_t e = mine0 + t, sh = 16u * (e & 1u);
             uint32_t off = 0;
-            if (valid) {
-                off = mine[t];
-                p.list[cur[t] + off + __popc(m & below)] = gid;
-            }
+            if (valid) off = (atomicAdd(mine32 + (e >> 1), 1u << sh) >> sh) & 0xffffu;
             __syncwarp();
-            if (valid && (m & below) == 0u) mine[t] = (uint16_t)(off + __popc(m));
+            uint32_t now = 0;
+            if (valid) now = (mine32[e >> 1] >> sh) & 0xffffu;
+            if (__ballot_sync(0xffffffffu, valid && now != off + 1u)) {
+                const uint32_t m = __match_any_sync(0xffffffffu, valid ? t : 0xffffffffu);
+                if (valid && __popc(m) > 1) off = now - __popc(m) + __popc(m & below);
+            }
+            if (valid) p.list[cur[t] + off] = gid;
             __syncwarp();
         });
     }

@@ -162,8 +162,8 @@ def test_direct_binning_equals_sort(gpu_ctx, oracle, seed, n, w, h, dist, scale)
 
 
 def test_direct_binning_tile_limit(gpu_ctx, oracle):
-    """Forcing the direct path on a view with more than 18000 tiles is a
-    contract error; the sort path handles it."""
+    """Above 18000 tiles auto takes the key sort; forcing the direct path there
+    is a contract error."""
     from paper_2505_08124_b200.errors import ContractError
     s = random_scene(3000, 15)
     cam = make_test_camera(3840, 2160, 8.0)
