@@ -461,7 +461,17 @@ __global__ void __launch_bounds__(WARPS * 32) bin_scatter_kernel(BinParams p) {
     const uint32_t S = (C + kBinSlices - 1) / kBinSlices;
     const uint32_t* row = p.counts + (size_t)blockIdx.x * p.tiles;
     const uint32_t* sl = p.slice + (size_t)(blockIdx.x / S) * p.tiles;
-    for (uint32_t t = threadIdx.x; t < p.tiles; t += blockDim.x) cur[t] = p.start[t] + sl[t] + row[t];
+    for (uint32_t t0 = threadIdx.x; t0 < p.tiles; t0 += 4u * blockDim.x) { // four tiles' loads in flight
+        uint32_t v[4];
+#pragma unroll
+        for (uint32_t u = 0; u < 4; ++u) {
+            const uint32_t t = t0 + u * blockDim.x;
+            v[u] = t < p.tiles ? __ldg(p.start + t) + __ldg(sl + t) + __ldg(row + t) : 0u;
+        }
+#pragma unroll
+        for (uint32_t u = 0; u < 4; ++u)
+            if (t0 + u * blockDim.x < p.tiles) cur[t0 + u * blockDim.x] = v[u];
+    }
     for (uint32_t t = threadIdx.x; t < WARPS * p.tiles; t += blockDim.x) wh[t] = 0;
     __syncthreads();
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
