@@ -150,7 +150,6 @@ __global__ void __launch_bounds__(256) project_kernel(ProjectParams p) {
                 r.b2 = dm(2.0, dd(-cxy, det));
                 r.c = dd(cxx, det);
                 r.opacity = (double)mo.w;
-                r.gid = (uint32_t)id;
                 const double rx = da(dm(3.0, __dsqrt_rn(cxx)), 1.0);
                 const double ry = da(dm(3.0, __dsqrt_rn(cyy)), 1.0);
                 const int32_t W = (int32_t)cam.width, H = (int32_t)cam.height;
@@ -170,11 +169,6 @@ __global__ void __launch_bounds__(256) project_kernel(ProjectParams p) {
                             for (uint32_t tx = (uint32_t)x0 / kTile; tx <= (uint32_t)x1 / kTile; ++tx)
                                 atomicAdd(p.tile_count + ty * p.tiles_x + tx, 1u);
                     }
-                    r.x0 = (uint16_t)x0;
-                    r.x1 = (uint16_t)x1;
-                    r.y0 = (uint16_t)y0;
-                    r.y1 = (uint16_t)y1;
-                    r.pad = 0;
                     p.rec[id] = r;
                     p.boxes[id] = make_uint2((uint32_t)x0 | ((uint32_t)x1 << 16), (uint32_t)y0 | ((uint32_t)y1 << 16));
                     survive = true;

@@ -12,18 +12,18 @@ constexpr uint32_t kTile = 16;          // rasterizer.hpp:30 kTileSize
 constexpr int kRasterThreads = 256;     // pixels of a 16x16 tile
 constexpr int kMaxMaskWords = 4;        // up to 128 masks per view
 
-// Per-splat record staged through shared memory by the compositor.  64 B so a
-// batch of 256 is 16 KB and every record is one aligned 64 B segment.
-// Fields are the reference's SplatRecord (rasterizer.hpp:99-106) minus color.
+// Per-splat record staged through shared memory by the compositor: exactly
+// the six doubles it reads (48 B, three 16 B vectors; a batch of 256 is 12 KB).
+// Fields are the reference's SplatRecord (rasterizer.hpp:99-106) minus color,
+// id and box (the box is the separate `boxes` array, the id comes from the
+// tile list).
 struct __align__(16) SplatRec {
     double mu_x, mu_y; // rasterizer.hpp:101
     double a, b2;      // conic (rasterizer.hpp:66-71); b2 = 2*b (exact)
     double c;
     double opacity;    // SplatRecord::opacity: the f32 opacity widened once
-    uint16_t x0, x1, y0, y1; // inclusive padded 3-sigma box (rasterizer.hpp:171-176)
-    uint32_t gid, pad;
 };
-static_assert(sizeof(SplatRec) == 64, "SplatRec must stay 64 B");
+static_assert(sizeof(SplatRec) == 48, "SplatRec must stay 48 B");
 
 // Per-view scalars kept on the device; the host reads them only at batch
 // boundaries (copied into a per-view status array), never per view.
