@@ -235,7 +235,8 @@ def test_encode_bench_style_vs_oracle(gpu_ctx, oracle, n, views, w, h, m, dim):
     np.testing.assert_allclose(cov, ec, rtol=1e-5)
 
 
-def test_group_contraction_d512(gpu_ctx, oracle):
+@pytest.mark.parametrize("m", [48, 64])  # 64: three views fill the 192 KB of staged CLIP half-rows
+def test_group_contraction_d512(gpu_ctx, oracle, m):
     """D = 512 views with <= 64 masks are contracted in groups (auto: three at a
     time; the two-pass shared-memory group kernels), including a partial last
     group and a view with more masks that is contracted alone.  The per-row
@@ -243,7 +244,7 @@ def test_group_contraction_d512(gpu_ctx, oracle):
     into the per-(Gaussian, mask) scalars make runs differ in the last bits,
     so configurations agree to 1e-5 relative per row with identical covered
     sets, and each matches the oracle to the north-star tolerance."""
-    wl = _bench_style(4000, 8, 80, 64, 48, 512, seed=77)
+    wl = _bench_style(4000, 8, 80, 64, m, 512, seed=77)
     big = _bench_style(4000, 1, 80, 64, 100, 512, seed=78)
     cams = wl.cams[:5] + big.cams + wl.cams[5:]
     masks = wl.masks[:5] + big.masks + wl.masks[5:]
