@@ -100,9 +100,9 @@ int ss_synchronize(ss_ctx* ctx);
  * alone): each touched Gaussian's row is read and written once per group; the
  * fp32 operation order per row is the same for every group size.
  * SS_OPT_BIN_PATH: tile lists from 0 = auto (default: direct count/scan/
- * scatter binning for views of <= 18000 16x16 tiles, else the key sort),
- * 1 = stable key sort, 2 = direct binning (error above 18000 tiles).  The
- * tile lists are identical. */
+ * scatter binning for views of <= 5734 16x16 tiles, else the key sort),
+ * 1 = stable key sort, 2 = direct binning (up to 18000 tiles; error above).
+ * The tile lists are identical. */
 enum ss_option { SS_OPT_LANES = 1, SS_OPT_QUERY_PATH = 2, SS_OPT_CONTRACT_GROUP = 3, SS_OPT_BIN_PATH = 4 };
 int ss_set_option(ss_ctx* ctx, int option, int64_t value);
 

@@ -198,7 +198,7 @@ class Context:
         check(self._L.ss_set_option(self.h, 2, int(path)))
 
     def set_bin_path(self, path: int):
-        """0 = auto (direct binning up to 18000 tiles), 1 = stable key sort, 2 = direct count/scan/scatter."""
+        """0 = auto (direct binning up to 5734 tiles), 1 = stable key sort, 2 = direct count/scan/scatter."""
         check(self._L.ss_set_option(self.h, 4, int(path)))
 
     def synchronize(self):
