@@ -17,6 +17,7 @@
 #include <string>
 #include <vector>
 
+#include <thrust/iterator/counting_iterator.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
@@ -272,11 +273,6 @@ void set_device(ss_ctx* c) { SS_CUDA(cudaSetDevice(c->device)); }
 
 void reset_info(ss_ctx* c, Lane& L, cudaStream_t s) {
     SS_CUDA(cudaMemcpyAsync(L.info.p, c->h_init, sizeof(ViewInfo), cudaMemcpyHostToDevice, s));
-}
-
-void sync_info(Lane& L, cudaStream_t s) {
-    SS_CUDA(cudaMemcpyAsync(L.h_info, L.info.p, sizeof(ViewInfo), cudaMemcpyDeviceToHost, s));
-    SS_CUDA(cudaStreamSynchronize(s));
 }
 
 uint32_t bits_for(uint64_t v) { // number of bits to represent v (v >= 1 -> >= 1)
@@ -944,7 +940,6 @@ void capture_view(ss_ctx* c, const ss_camera* cam, int mode, bool color, uint64_
     set_device(c);
     cudaStream_t s = c->stream;
     const uint64_t P = (uint64_t)cam->width * cam->height;
-    const uint64_t N = c->n;
     ss::Lane& L = c->lanes[0];
     Geometry g;
     for (int attempt = 0;; ++attempt) {
@@ -1199,7 +1194,7 @@ int ss_store_build(ss_ctx* c, const float* rows, const float* coverage, uint64_t
         auto* num = static_cast<int*>(c->num_sel.ensure(16));
         own_launch(c, launch_flag_covered(d_cov, n, flags, s), SS_K_QUERY);
         size_t tb = 0;
-        cub::CountingInputIterator<uint32_t> it(0);
+        thrust::counting_iterator<uint32_t> it(0);
         SS_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, it, flags, ids, num, (int)n, s));
         void* tmp = c->cub_tmp.ensure(tb);
         tb = c->cub_tmp.bytes;

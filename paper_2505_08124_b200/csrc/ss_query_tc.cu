@@ -56,6 +56,7 @@ constexpr uint32_t EPI_COLS = BN / (EPI_WARPS / 4);
 // the c5 query (GEMM only): 8 warps x16 1.63 ms, x8 1.70, x32 1.72, x64 1.90;
 // 4 warps x16 2.00, 16 warps x16 1.75; no TMEM reads at all 1.48.
 constexpr uint32_t EPI_ROUND = SS_QTC_EPI_ROUND;
+static_assert(EPI_ROUND == 8 || EPI_ROUND == 16 || EPI_ROUND == 32, "SS_QTC_EPI_ROUND must be 8, 16 or 32");
 constexpr uint32_t THREADS = 32 * (2 + EPI_WARPS);
 constexpr uint32_t BAR_BYTES = 256;
 constexpr uint32_t THR_SMEM = EPI_WARPS * EPI_COLS * 4; // per-warp copy of its thresholds
@@ -386,7 +387,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                     SS_TMEM_LD16(taddr, r);
                 } else {
                     SS_TMEM_LD32(taddr, r);
-                    if constexpr (EPI_ROUND == 64) SS_TMEM_LD32(taddr + 32, (r + 32));
                 }
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 if (c + EPI_ROUND >= EPI_COLS) {
