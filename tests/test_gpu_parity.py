@@ -564,3 +564,26 @@ def test_fp64_probe_rate_is_plausible(gpu_ctx):
     runs 64 fp64 lanes per SM per clock, 148 SMs at up to ~2 GHz."""
     rate = gpu_ctx.probe_fp64_rate()
     assert 5e12 < rate < 2.2e13, rate
+
+
+@pytest.mark.parametrize("bin_path", [0, 1])
+def test_tile_list_overflow_reruns_exactly(oracle, bin_path):
+    """Views whose tile lists exceed the list buffer (it starts at max(4N, 2^20)
+    entries) are re-run with a larger one: captures and embeddings stay exact."""
+    from paper_2505_08124_b200 import _lib
+    s = random_scene(30000, 31)
+    s.scale[:] = (s.scale * np.float32(4.0)).astype(np.float32)  # boxes of most of the view
+    cam = make_test_camera(128, 128, 6.0)
+    ctx = _lib.Context(0)  # fresh: the list buffer has its initial size
+    ctx.set_bin_path(bin_path)
+    got = _capture(ctx, s, cam)
+    assert got["tile_offsets"][-1] > (1 << 20)
+    _assert_capture_equal(got, oracle.rasterize(s, cam))
+    wl = _bench_style(30000, 3, 96, 96, 8, 16, seed=33)
+    wl.scene.scale[:] = (wl.scene.scale * np.float32(6.0)).astype(np.float32)
+    ctx2 = _lib.Context(0)
+    ctx2.set_bin_path(bin_path)
+    rows, cov = _encode(ctx2, wl.scene, wl.cams, wl.masks, 16)
+    er, ec = oracle.encode(wl.scene, wl.cams, wl.masks, 16)
+    rel, cos = row_errors(rows, cov, er, ec)
+    assert rel <= EMB_REL_TOL and cos >= EMB_COS_TOL, (rel, cos)
