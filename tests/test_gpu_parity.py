@@ -587,3 +587,25 @@ def test_tile_list_overflow_reruns_exactly(oracle, bin_path):
     er, ec = oracle.encode(wl.scene, wl.cams, wl.masks, 16)
     rel, cos = row_errors(rows, cov, er, ec)
     assert rel <= EMB_REL_TOL and cos >= EMB_COS_TOL, (rel, cos)
+
+
+@pytest.mark.parametrize("lanes,group", [(5, 0), (1, 0), (4, 2)])
+def test_encode_views_without_masks_interleaved(gpu_ctx, oracle, lanes, group):
+    """Views with no masks contribute nothing and take no contraction; mixed
+    into groups of D = 512 views they must not disturb the grouping or the
+    per-row order (pipeline.hpp:320-350 skips them the same way)."""
+    wl = _bench_style(3000, 5, 80, 64, 48, 512, seed=81)
+    wl0 = _bench_style(3000, 3, 80, 64, 0, 512, seed=82)
+    cams = [wl.cams[0], wl0.cams[0], wl.cams[1], wl.cams[2], wl0.cams[1], wl0.cams[2], wl.cams[3], wl.cams[4]]
+    masks = [wl.masks[0], wl0.masks[0], wl.masks[1], wl.masks[2], wl0.masks[1], wl0.masks[2], wl.masks[3],
+             wl.masks[4]]
+    try:
+        gpu_ctx.set_lanes(lanes)
+        gpu_ctx.set_contract_group(group)
+        rows, cov = _encode(gpu_ctx, wl.scene, cams, masks, 512)
+    finally:
+        gpu_ctx.set_lanes(5)
+        gpu_ctx.set_contract_group(0)
+    er, ec = oracle.encode(wl.scene, cams, masks, 512)
+    rel, cos = row_errors(rows, cov, er, ec)
+    assert rel <= EMB_REL_TOL and cos >= EMB_COS_TOL, (rel, cos)
