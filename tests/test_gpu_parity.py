@@ -266,7 +266,7 @@ def test_group_contraction_d512(gpu_ctx, oracle, m):
         assert rel <= EMB_REL_TOL and cos >= EMB_COS_TOL, (key, rel, cos)
 
 
-@pytest.mark.parametrize("lanes,group", [(1, 1), (3, 1), (4, 1), (4, 2), (4, 4), (1, 4), (3, 4)])
+@pytest.mark.parametrize("lanes,group", [(1, 1), (3, 1), (4, 1), (4, 2), (4, 4), (1, 4), (3, 4), (6, 0), (5, 3)])
 def test_encode_lane_count_does_not_change_results(gpu_ctx, oracle, lanes, group):
     """Views spread over 1..4 pipeline lanes (SS_OPT_LANES) and contracted in
     groups of 1..4 (SS_OPT_CONTRACT_GROUP) contract in view order; the result
