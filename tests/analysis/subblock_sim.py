@@ -9,7 +9,7 @@ independently or synchronised at every 32-entry staging chunk.
 
 The per-pixel arithmetic is a float64 numpy model of rasterizer.hpp:112-133
 (exact enough to place early termination); the projection comes from the
-CPU oracle.  Usage: python tools/subblock_sim.py [--tiles 40] [--view 0]
+CPU oracle.  Usage: python tests/analysis/subblock_sim.py [--tiles 40] [--view 0]
 """
 import argparse
 import sys
@@ -17,7 +17,7 @@ from pathlib import Path
 
 import numpy as np
 
-sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
 from oracle.bindings import Oracle  # noqa: E402
 from paper_2505_08124_b200.workload import orbit_camera, synth_scene  # noqa: E402
 
