@@ -33,7 +33,7 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-from paper_2505_08124_b200.workload import CONFIGS, make_bench_workload  # noqa: E402
+from harness.workload import CONFIGS, make_bench_workload  # noqa: E402
 
 PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
 FALLBACK_HBM = 6650.0
@@ -196,9 +196,9 @@ def query_leg(ctx, args, dev, stream, want_cpu):
     public query call (host queries in, host ids/sims out).  Device-side
     kernel times come from CUDA events on the call's stream."""
     import torch
-    from paper_2505_08124_b200.workload import QUERY_CONFIG as QC
+    from harness.workload import QUERY_CONFIG as QC
     n, nq, d, k = QC["n_rows"], QC["n_queries"], QC["dim"], QC["k"]
-    from paper_2505_08124_b200.workload import query_workload
+    from harness.workload import query_workload
     t_gen = time.perf_counter()
     raw, qraw = query_workload(args.seed, n, nq, d)  # cmd_bench's store + queries (main.cpp:440-450)
     gen_s = time.perf_counter() - t_gen
@@ -302,6 +302,11 @@ def query_leg(ctx, args, dev, stream, want_cpu):
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return
+    # inputs from the oracle-side build of the harness generator: this process
+    # maps oracle/ libraries only, never libsemsplat_b200.so
+    from harness import workload
+    from oracle.build_oracle import GEN_SO
+    workload.use_generator(GEN_SO)
     cfg = CONFIGS[args.config]
     cores = os.cpu_count() or 1
     views = args.cpu_sample_views or max(1, min(cores, 16))
@@ -508,7 +513,7 @@ def main():
     evl = None
     if rank == 0 and not args.no_query:
         try:
-            from paper_2505_08124_b200.workload import synth_embedding
+            from harness.workload import synth_embedding
             n_local = max(0, min(shard, N - rank * shard))
             lab_ids = np.arange(16, dtype=np.int32)
             lab_vecs = np.stack([synth_embedding(f"class_{i}", D) for i in range(16)])

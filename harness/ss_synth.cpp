@@ -1,8 +1,9 @@
 // Synthetic workload generator: the B200 framework's counterpart of the
 // reference CLI's `bench` dataset writer (main.cpp:334-410) and of
 // synth_embedding (providers.hpp:381-400) / look_at (fixture.hpp:65-84).
-// Host code; produces the inputs the bench and the tests feed to BOTH the
-// device path and the CPU oracle.
+// BENCH/TEST HARNESS, not linked into libsemsplat_b200.so: host code that
+// produces the inputs the bench and the tests feed to BOTH the device path
+// and the CPU oracle (built as harness/libss_synth.so and oracle/libssgen.so).
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -10,7 +11,7 @@
 #include <string>
 #include <vector>
 
-#include "../../include/semsplat_b200.h"
+#include "ss_synth.h"
 
 namespace {
 
@@ -83,7 +84,7 @@ int ss_synth_scene(uint64_t seed, uint64_t n, double xy_extent, double z_extent,
 }
 
 int ss_synth_look_at(const double* eye, const double* target, uint32_t width, uint32_t height, double focal,
-                     ss_camera* out) {
+                     ss_synth_camera* out) {
     double fwd[3] = {target[0] - eye[0], target[1] - eye[1], target[2] - eye[2]};
     normalize3(fwd);
     double up[3] = {0, 1, 0};
@@ -114,7 +115,7 @@ int ss_synth_look_at(const double* eye, const double* target, uint32_t width, ui
 }
 
 int ss_synth_embedding(const char* label, uint32_t dim, float* out) {
-    if (dim < 2) return SS_ERR_CONTRACT;
+    if (dim < 2) return 1; // ContractError
     std::mt19937_64 rng(fnv1a64(label) ^ 0x9e3779b97f4a7c15ull);
     auto uniform01 = [&rng]() { return (static_cast<double>(rng() >> 11) + 0.5) * 0x1.0p-53; };
     std::vector<double> values(dim);

@@ -224,24 +224,6 @@ int ss_probe_fp64_rate(ss_ctx* ctx, double* lane_ops_per_s);
 /* Number of kernels this library launched (own + CUB) since reset. */
 int ss_launch_count(ss_ctx* ctx, uint64_t* own, uint64_t* cub);
 
-/* ---- synthetic workload (main.cpp:334-410 write_bench_dataset) --------- */
-/* Bench-style uniform scene (main.cpp:340-352) from std::mt19937_64(seed). */
-int ss_synth_scene(uint64_t seed, uint64_t n, double xy_extent, double z_extent, float* mean, float* scale,
-                   float* quat_xyzw, float* opacity, float* color);
-/* fixture.hpp:65-84 look_at */
-int ss_synth_look_at(const double* eye, const double* target, uint32_t width, uint32_t height, double focal,
-                     ss_camera* out);
-/* providers.hpp:381-400 synth_embedding */
-int ss_synth_embedding(const char* label, uint32_t dim, float* out);
-/* Random-rectangle masks for one view (main.cpp:386-396) from the rng state
- * seeded by seed; writes RLE runs (capacity >= n_masks*(2*height+2)) and
- * run_offsets (n_masks+1). */
-/* main.cpp:440-450: the bench query store/queries, U(-0.5, 0.5) per element
- * from std::mt19937_64(seed) (cmd_bench seeds it with seed ^ 0xbe9c). */
-int ss_synth_uniform(uint64_t seed, uint64_t count, float* out);
-int ss_synth_rect_masks(uint64_t seed, uint32_t width, uint32_t height, uint32_t n_masks, uint32_t* runs,
-                        uint64_t* run_offsets);
-
 #ifdef __cplusplus
 }
 #endif

@@ -1,6 +1,9 @@
 """Builds the parity checkers -- TEST INFRASTRUCTURE ONLY.
 
   oracle/libssoracle.so   the C restatement (oracle/ssoracle.c)
+  oracle/libssgen.so      the synthetic-input generator (harness/ss_synth.cpp),
+                          a second build used only by bench.py's reference
+                          arm so that process never maps the product library
   oracle/_ref/libssref.so the UNMODIFIED reference headers
                           (/root/reference/proj/include, only present in the
                           build container) + oracle/eigen_shim + ref_capi.cpp
@@ -18,6 +21,7 @@ from pathlib import Path
 HERE = Path(__file__).resolve().parent
 REF_INCLUDE = Path("/root/reference/proj/include")
 ORACLE_SO = HERE / "libssoracle.so"
+GEN_SO = HERE / "libssgen.so"
 REF_SO = HERE / "_ref" / "libssref.so"
 
 
@@ -33,6 +37,9 @@ def build(verbose: bool = False) -> None:
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
+    sys.path.insert(0, str(HERE.parent))
+    from harness.build import compile_generator
+    compile_generator(GEN_SO, verbose)
     if REF_INCLUDE.exists():
         REF_SO.parent.mkdir(exist_ok=True)
         deps = [HERE / "ref_capi.cpp", HERE / "eigen_shim" / "Eigen" / "Dense", HERE / "eigen_shim" / "Eigen" / "Geometry",

@@ -95,11 +95,6 @@ def lib() -> C.CDLL:
         "ss_profile_read": (i32, [vp, pd, pu64, pd]),
         "ss_counters_read": (i32, [vp, pu64]),
         "ss_launch_count": (i32, [vp, pu64, pu64]),
-        "ss_synth_scene": (i32, [u64, u64, C.c_double, C.c_double, pf, pf, pf, pf, pf]),
-        "ss_synth_look_at": (i32, [pd, pd, u32, u32, C.c_double, C.POINTER(Camera)]),
-        "ss_synth_embedding": (i32, [C.c_char_p, u32, pf]),
-        "ss_synth_rect_masks": (i32, [u64, u32, u32, u32, pu32, pu64]),
-        "ss_synth_uniform": (i32, [u64, u64, pf]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -24,7 +24,6 @@ UNITS = [
     ("ss_kernels.cu", []),
     ("ss_api.cu", []),
     ("ss_query_tc.cu", []),
-    ("ss_synth.cpp", []),
 ]
 
 

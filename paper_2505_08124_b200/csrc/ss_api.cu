@@ -125,6 +125,7 @@ struct ContractSet {
     cudaEvent_t free_ev = nullptr; // recorded after the contraction that consumed this set
     bool pending = false;          // a contraction reading this set has been issued
     bool in_group = false;         // part of the group being formed
+    bool dirty = false;            // rasterized into but never contracted (error path): acc must be zeroed
     void release() {
         DevBuf* b[] = {&acc, &touched, &touched_list, &clip, &tcount};
         for (auto* x : b) x->release();
@@ -134,6 +135,7 @@ struct ContractSet {
         gen = 0;
         pending = false;
         in_group = false;
+        dirty = false;
     }
 };
 
@@ -214,7 +216,7 @@ struct ss_ctx {
     bool cap_image = false;    // the last capture rendered an image
     uint64_t cap_entries = 0, cap_splats = 0, cap_instances = 0;
     uint32_t cap_width = 0, cap_height = 0, cap_tiles = 0;
-    ss::DevBuf counters; // [0] G_v sum, [1] K_v sum
+    ss::DevBuf counters; // [0] G_v sum, [1] K_v sum, [2] contraction rows RMW, [3] covered rows normalised
     // accumulators
     uint32_t dim = 0;
     float* sums = nullptr;
@@ -286,6 +288,26 @@ void check_camera(const ss_camera* cam) {
     if (cam->width == 0 || cam->height == 0) throw Error(SS_ERR_DATA, "camera has zero raster resolution");
     if (cam->width > 65535 || cam->height > 65535)
         throw Error(SS_ERR_CONTRACT, "raster resolution above 65535 is not supported");
+}
+
+// rasterizer.hpp:66-70,187-191: conic_of throws for the first singular
+// projection in depth order (it runs over the depth-sorted visible list before
+// any box cull).  The kernels only count singular covariances; on that (rare)
+// error path the view is projected again with the Projected2D dump and the
+// host picks the first (depth, id) one, so the error names the same Gaussian.
+uint32_t first_singular_gid(ss_ctx* c, const ss_camera& cam) {
+    const uint64_t N = c->n;
+    std::vector<ss_projected> h(N);
+    if (ss_project(c, &cam, h.data()) != SS_OK) throw Error(SS_ERR_CUDA, "re-projection failed: " + g_err);
+    uint64_t best = N;
+    for (uint64_t k = 0; k < N; ++k) {
+        const ss_projected& q = h[k];
+        if (!q.visible) continue;
+        const double det = q.cov_xx * q.cov_yy - q.cov_xy * q.cov_xy; // conic_of, no FMA (x86-64 baseline)
+        if (!(det < 1e-12)) continue;
+        if (best == N || q.depth < h[best].depth) best = k; // ids ascend: ties keep the lower id
+    }
+    return best == N ? 0xffffffffu : (uint32_t)best;
 }
 
 struct Geometry {
@@ -466,7 +488,12 @@ RasterParams raster_params(ss_ctx* c, Lane& L, const ss_camera& cam, const Geome
     return p;
 }
 
-uint32_t mask_words_for(uint32_t m) { return m <= 32 ? 1 : (m <= 64 ? 2 : 4); }
+// words per pixel of a view's mask bitsets: 1, 2 or 4 (one compositor pass),
+// or whole 128-mask windows of 4 words for views with more than 128 masks
+uint32_t mask_words_for(uint32_t m) {
+    if (m <= 128) return m <= 32 ? 1 : (m <= 64 ? 2 : 4);
+    return (m + 127) / 128 * 4;
+}
 
 // Upload one view's RLE masks + CLIP and build the raster-resolution bitsets.
 void build_mask_bits(ss_ctx* c, Lane& L, cudaStream_t s, const ss_camera& cam, const ss_view_masks* vm,
@@ -580,7 +607,6 @@ void encode_one(ss_ctx* c, Lane& L, const ss_camera& cam, const ss_view_masks* v
                 ViewInfo* vstat_slot) {
     check_camera(&cam);
     const uint32_t M = vm ? vm->n_masks : 0;
-    if (M > 128) throw Error(SS_ERR_CONTRACT, "at most 128 masks per view are supported");
     const uint32_t words = mask_words_for(M);
     cudaStream_t s = L.stream;
     ContractSet* S = nullptr;
@@ -591,6 +617,10 @@ void encode_one(ss_ctx* c, Lane& L, const ss_camera& cam, const ss_view_masks* v
         if (S->pending) {                // its last contraction must be done before we overwrite it
             SS_CUDA(cudaStreamWaitEvent(s, S->free_ev, 0));
             S->pending = false;
+        }
+        if (S->dirty) { // a view of an abandoned group left its per-(Gaussian, mask) scalars behind
+            if (S->acc.p) SS_CUDA(cudaMemsetAsync(S->acc.p, 0, S->acc.bytes, s));
+            S->dirty = false;
         }
         build_mask_bits(c, L, s, cam, vm, words, cam.image_id);
     }
@@ -626,14 +656,19 @@ void encode_one(ss_ctx* c, Lane& L, const ss_camera& cam, const ss_view_masks* v
             Scope sc(c, s, SS_K_RASTER);
             RasterParams p = raster_params(c, L, cam, g);
             p.pix_bits = L.pix_bits.as<uint32_t>();
-            p.mask_words = words;
             p.n_masks = M;
+            p.bits_stride = words;
             p.acc = S->acc.as<float>();
             p.touched = S->touched.as<uint32_t>();
             p.touched_list = tlist;
             p.touched_count = tcount;
             p.gen = S->gen;
-            own_launch(c, launch_raster_fused(p, mode, g.tiles, s), SS_K_RASTER);
+            // one pass per 128-mask window (a single pass for M <= 128)
+            for (uint32_t w0 = 0; w0 < words; w0 += kMaxMaskWords) {
+                p.mask_words = std::min<uint32_t>(words - w0, kMaxMaskWords);
+                p.mask_base = 32u * w0;
+                own_launch(c, launch_raster_fused(p, mode, g.tiles, s), SS_K_RASTER);
+            }
         }
         SS_CUDA(cudaEventRecord(L.raster_done, s));
         // auto grouping: only views the shared-memory group kernel takes
@@ -670,8 +705,12 @@ void encode_batch(ss_ctx* c, uint32_t nviews, const ss_camera* cams, const ss_vi
                 ss_ctx* c;
                 ~Join() {
                     // the user stream resumes after all lanes drain (also on errors;
-                    // a group left open by an error contributes nothing)
-                    for (auto& g : c->group) g.set->in_group = false;
+                    // a group left open by an error contributes nothing, and its
+                    // members' scalars are zeroed before the sets are used again)
+                    for (auto& g : c->group) {
+                        g.set->in_group = false;
+                        g.set->dirty = true;
+                    }
                     c->group.clear();
                     for (auto& L : c->lanes) {
                         cudaEventRecord(L.done, L.stream);
@@ -700,7 +739,8 @@ void encode_batch(ss_ctx* c, uint32_t nviews, const ss_camera* cams, const ss_vi
             const ViewInfo& st = hstat[v];
             if (st.err_count)
                 throw Error(SS_ERR_DATA, "image " + std::to_string(cams[v].image_id) +
-                                             ": singular screen covariance for gaussian " + std::to_string(st.err_gid));
+                                             ": singular screen covariance for gaussian " +
+                                             std::to_string(first_singular_gid(c, cams[v])));
             if (st.overflow) {
                 again.push_back(v);
                 need = std::max<uint64_t>(need, st.n_instances);
@@ -794,7 +834,7 @@ int ss_create(int device, ss_ctx** out) {
         c->h_init->min_key = ~0ull;
         c->h_init->err_gid = ~0u;
         c->info.ensure(sizeof(ViewInfo));
-        c->counters.ensure(16);
+        c->counters.ensure(32);
         SS_CUDA(cudaMemset(c->counters.p, 0, c->counters.bytes));
         *out = c;
     });
@@ -951,7 +991,8 @@ void capture_view(ss_ctx* c, const ss_camera* cam, int mode, bool color, uint64_
         L.list_cap = L.h_info->n_instances + L.h_info->n_instances / 16;
     }
     if (L.h_info->err_count)
-        throw Error(SS_ERR_NUMERIC, "singular screen covariance for gaussian " + std::to_string(L.h_info->err_gid));
+        throw Error(SS_ERR_NUMERIC, "singular screen covariance for gaussian " +
+                                        std::to_string(first_singular_gid(c, *cam)));
     const uint64_t n_surv = L.h_info->n_surv, n_inst = L.h_info->n_instances;
     auto* cnt = static_cast<uint32_t*>(c->pix_count.ensure((P + 1) * 4));
     auto* off = static_cast<uint32_t*>(c->pix_offset.ensure((P + 1) * 4));
@@ -1140,9 +1181,12 @@ int ss_encode_finalize(ss_ctx* c, uint64_t row_lo, uint64_t row_hi, float* rows_
         }
         {
             Scope sc(c, s, SS_K_NORMALIZE);
-            own_launch(c, launch_normalize(c->sums + row_lo * c->dim, c->totals + row_lo, n, c->dim, d_rows, d_cov, s),
+            own_launch(c,
+                       launch_normalize(c->sums + row_lo * c->dim, c->totals + row_lo, n, c->dim, d_rows, d_cov,
+                                        c->counters.as<unsigned long long>() + 3, s),
                        SS_K_NORMALIZE);
-            c->prof.bytes[SS_K_NORMALIZE] += (double)n * (8.0 * c->dim + 8.0);
+            // totals read + rows and coverage written; covered rows' sums (read) are added at readout
+            c->prof.bytes[SS_K_NORMALIZE] += (double)n * (4.0 * c->dim + 8.0);
         }
         if (!out_on_device) {
             SS_CUDA(cudaMemcpyAsync(rows_out, d_rows, n * c->dim * 4, cudaMemcpyDeviceToHost, s));
@@ -1158,9 +1202,11 @@ int ss_normalize_device(ss_ctx* c, const float* d_sums, const float* d_totals, u
         if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
         set_device(c);
         Scope sc(c, c->stream, SS_K_NORMALIZE);
-        own_launch(c, launch_normalize(d_sums, d_totals, n, dim, d_rows_out, d_coverage_out, c->stream),
+        own_launch(c,
+                   launch_normalize(d_sums, d_totals, n, dim, d_rows_out, d_coverage_out,
+                                    c->counters.as<unsigned long long>() + 3, c->stream),
                    SS_K_NORMALIZE);
-        c->prof.bytes[SS_K_NORMALIZE] += (double)n * (8.0 * dim + 8.0);
+        c->prof.bytes[SS_K_NORMALIZE] += (double)n * (4.0 * dim + 8.0);
     });
 }
 
@@ -1597,10 +1643,14 @@ int ss_profile_read(ss_ctx* c, double* ms, uint64_t* launches, double* bytes) {
     return guarded([&] {
         set_device(c);
         profile_drain(c);
-        // fold the device-side G_v / K_v counters into raster + contract bytes
-        unsigned long long h[2];
-        SS_CUDA(cudaMemcpy(h, c->counters.p, 16, cudaMemcpyDeviceToHost));
-        const double gv = (double)h[0], kv = (double)h[1];
+        // fold the device-side counters into raster / contract / normalize bytes:
+        // K_v pairs (8 B read-modify-write each, written by the compositor and
+        // read + cleared by the contraction), rows read and written by the
+        // contraction (once per group: the union of the members' touched
+        // sets), covered rows whose sums normalize reads
+        unsigned long long h[4];
+        SS_CUDA(cudaMemcpy(h, c->counters.p, 32, cudaMemcpyDeviceToHost));
+        const double kv = (double)h[1], rows = (double)h[2], covered = (double)h[3];
         for (int i = 0; i < SS_K_COUNT; ++i) {
             if (ms) ms[i] = c->prof.ms[i];
             if (launches) launches[i] = c->prof.launches[i];
@@ -1609,7 +1659,8 @@ int ss_profile_read(ss_ctx* c, double* ms, uint64_t* launches, double* bytes) {
         if (bytes) {
             const double D = c->dim ? c->dim : 512;
             bytes[SS_K_RASTER] += 8.0 * kv;
-            bytes[SS_K_CONTRACT] += 8.0 * kv + gv * (8.0 * D + 8.0);
+            bytes[SS_K_CONTRACT] += 8.0 * kv + rows * (8.0 * D + 8.0);
+            bytes[SS_K_NORMALIZE] += covered * 4.0 * D;
         }
     });
 }
@@ -1618,8 +1669,8 @@ int ss_counters_read(ss_ctx* c, uint64_t* out5) {
     return guarded([&] {
         set_device(c);
         SS_CUDA(cudaStreamSynchronize(c->stream));
-        unsigned long long h[2];
-        SS_CUDA(cudaMemcpy(h, c->counters.p, 16, cudaMemcpyDeviceToHost));
+        unsigned long long h[4];
+        SS_CUDA(cudaMemcpy(h, c->counters.p, 32, cudaMemcpyDeviceToHost));
         const uint64_t gv = h[0], kv = h[1];
         out5[0] = c->cnt_vis;
         out5[1] = c->cnt_inst;

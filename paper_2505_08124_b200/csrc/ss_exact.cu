@@ -293,7 +293,7 @@ __device__ __forceinline__ void gate_and_accumulate(const RasterParams& p, bool 
     const uint32_t em = __ballot_sync(0xffffffffu, contrib);
     if (!em) return;
     uint32_t rem = em;
-    float* row = p.acc + (size_t)gid * p.n_masks + lane;
+    float* row = p.acc + (size_t)gid * p.n_masks + p.mask_base + lane;
     while (rem) {
         const int leader = __ffs(rem) - 1;
         const uint32_t gm = __shfl_sync(0xffffffffu, grp, leader);
@@ -345,6 +345,9 @@ __device__ __forceinline__ uint32_t match_bits(const uint32_t (&bits)[MW]) {
 //         alpha = 1 - T_final.
 // KIND 2: fused -- gate each contribution by the pixel's SAM-mask bitset and
 //         add w into per-(Gaussian, mask) fp32 scalars (never a 512-d scatter).
+//         One pass covers up to 128 masks (MW words); views with more masks
+//         (providers.hpp:135 allows any count) run one pass per 128-mask
+//         window [mask_base, mask_base + 128), each recompositing the tile.
 template <int KIND, bool FALLOFF, int MW>
 __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) {
     __shared__ SplatRec srec[kRasterThreads]; // warp w stages its hits in srec[32w, 32w+32)
@@ -389,7 +392,7 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
         bool any = false;
 #pragma unroll
         for (int w = 0; w < MW; ++w) {
-            bits[w] = ps.inside ? p.pix_bits[(size_t)ps.pixel * MW + w] : 0u;
+            bits[w] = ps.inside ? p.pix_bits[(size_t)ps.pixel * p.bits_stride + (p.mask_base >> 5) + w] : 0u;
             any |= bits[w] != 0;
         }
         grp = match_bits<MW>(bits);

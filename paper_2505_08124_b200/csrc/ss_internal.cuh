@@ -10,7 +10,7 @@ namespace ss {
 
 constexpr uint32_t kTile = 16;          // rasterizer.hpp:30 kTileSize
 constexpr int kRasterThreads = 256;     // pixels of a 16x16 tile
-constexpr int kMaxMaskWords = 4;        // up to 128 masks per view
+constexpr int kMaxMaskWords = 4;        // masks per compositor pass: views with more run 128-mask windows
 
 // Per-splat record staged through shared memory by the compositor: exactly
 // the six doubles it reads (48 B, three 16 B vectors; a batch of 256 is 12 KB).
@@ -71,8 +71,10 @@ struct RasterParams {
     const float4* color;           // render: Gaussian colors (r, g, b, -) by id
     float* image;                  // render output [P * 3], zero where no weight
     // fused mode
-    const uint32_t* pix_bits;      // [P * mask_words]
-    uint32_t mask_words, n_masks;
+    const uint32_t* pix_bits;      // [P * bits_stride]
+    uint32_t mask_words, n_masks;  // words of this pass's window (1, 2 or 4); masks of the view
+    uint32_t bits_stride;          // words per pixel in pix_bits (= mask_words unless windowed)
+    uint32_t mask_base;            // first mask of the window (multiple of 128; word offset mask_base / 32)
     float* acc;                    // [N * n_masks] per-(Gaussian, mask) scalars
     uint32_t* touched;             // [N] generation stamp of the last view that touched the Gaussian
     uint32_t* touched_list;        // [N] Gaussian ids touched in this view

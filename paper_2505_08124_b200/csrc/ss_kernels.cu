@@ -601,7 +601,7 @@ __global__ void __launch_bounds__(256) contract_kernel(ContractParams p) {
         cnt[i] = i < p.n_members ? *p.m[i].touched_count : 0ull;
         total += cnt[i];
     }
-    unsigned long long pairs = 0;
+    unsigned long long pairs = 0, rows = 0;
     for (uint64_t t = warp0; t < total; t += nwarps) {
         uint32_t i = 0;
         uint64_t tt = t;
@@ -613,6 +613,7 @@ __global__ void __launch_bounds__(256) contract_kernel(ContractParams p) {
         bool earlier = false;
         for (uint32_t j = 0; j < i; ++j) earlier |= __ldg(p.m[j].touched + gid) == p.m[j].gen;
         if (earlier) continue; // handled with the earlier view's entry
+        ++rows;
         float* row = p.sums + (size_t)gid * p.dim;
         float4 racc[4];
         if constexpr (DIM512) {
@@ -635,6 +636,7 @@ __global__ void __launch_bounds__(256) contract_kernel(ContractParams p) {
     if (p.count_pairs) {
         // pairs is warp-uniform (ballot popcounts); count once per warp
         if (lane == 0 && pairs) atomicAdd(p.cum + 1, pairs);
+        if (lane == 0 && rows) atomicAdd(p.cum + 2, rows);
         if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(p.cum, total);
     }
 }
@@ -734,7 +736,10 @@ __global__ void __launch_bounds__(kContractThreads, 1) contract_smem_kernel(Cont
     }
     if (p.count_pairs) {
         if (lane == 0 && pairs) atomicAdd(p.cum + 1, pairs);
-        if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(p.cum, total);
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            atomicAdd(p.cum, total);
+            atomicAdd(p.cum + 2, total); // rows read and written (each touched row once)
+        }
     }
 }
 
@@ -907,6 +912,7 @@ __global__ void __launch_bounds__(1024, 1) contract_group_pass_kernel(ContractPa
             unsigned long long all = 0;
             for (uint32_t i = 0; i < nm; ++i) all += *p.m[i].touched_count;
             atomicAdd(p.cum, all);
+            atomicAdd(p.cum + 2, (unsigned long long)total); // union rows, each read and written once per group
         }
     }
 }
@@ -991,7 +997,9 @@ __global__ void label_prep_kernel(const float* labels, uint32_t dim, uint32_t n_
 // pipeline.hpp:120-135 finalize_into: covered rows (total > 1e-8) become
 // sum/total, coverage = total; uncovered rows are exactly zero.
 __global__ void __launch_bounds__(256) normalize_kernel(const float* sums, const float* totals, uint64_t n,
-                                                        uint32_t dim, float* rows, float* coverage) {
+                                                        uint32_t dim, float* rows, float* coverage,
+                                                        unsigned long long* covered) {
+    unsigned long long ncov = 0;
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -999,6 +1007,7 @@ __global__ void __launch_bounds__(256) normalize_kernel(const float* sums, const
     for (uint64_t k = warp0; k < n; k += nwarps) {
         const float t = totals[k];
         const bool cov = (double)t > 1e-8;
+        ncov += cov;
         const double inv = cov ? 1.0 / (double)t : 0.0;
         const float* s = sums + k * dim;
         float* o = rows + k * dim;
@@ -1020,6 +1029,7 @@ __global__ void __launch_bounds__(256) normalize_kernel(const float* sums, const
         }
         if (lane == 0) coverage[k] = cov ? t : 0.0f;
     }
+    if (covered && lane == 0 && ncov) atomicAdd(covered, ncov); // rows whose sums were read (roofline bytes)
 }
 
 // ---------------------------------------------------------------- query
@@ -1363,9 +1373,9 @@ cudaError_t launch_contract(const ContractParams& p, uint64_t max_touched, cudaS
     return cudaGetLastError();
 }
 cudaError_t launch_normalize(const float* sums, const float* totals, uint64_t n, uint32_t dim, float* rows,
-                             float* coverage, cudaStream_t s) {
+                             float* coverage, unsigned long long* covered, cudaStream_t s) {
     if (!n) return cudaSuccess;
-    normalize_kernel<<<warp_grid(n), 256, 0, s>>>(sums, totals, n, dim, rows, coverage);
+    normalize_kernel<<<warp_grid(n), 256, 0, s>>>(sums, totals, n, dim, rows, coverage, covered);
     return cudaGetLastError();
 }
 cudaError_t launch_normalize_rows(const float* in, const uint32_t* select, uint64_t n, uint32_t dim, float* out,

@@ -25,7 +25,7 @@ struct ContractParams {
     float* sums;           // [N x dim]
     float* totals;         // [N]
     int count_pairs;
-    unsigned long long* cum; // running [G_v, K_v] totals (summed over views)
+    unsigned long long* cum; // running totals: [0] G_v, [1] K_v (summed over views), [2] rows read+written
     uint2* union_list;       // group scratch: (gid, member mask), sum of the members' lists
     unsigned int* union_count;
 };
@@ -71,8 +71,9 @@ uint32_t bin_scatter_warps(uint32_t tiles);
 size_t bin_counts_entries(uint64_t n, uint32_t tiles);
 cudaError_t launch_bin(const BinParams& p, cudaStream_t s);
 cudaError_t launch_contract(const ContractParams& p, uint64_t max_touched, cudaStream_t s);
+// covered (optional): += rows with total > 1e-8 (their sums are read; the rest are only written)
 cudaError_t launch_normalize(const float* sums, const float* totals, uint64_t n, uint32_t dim, float* rows,
-                             float* coverage, cudaStream_t s);
+                             float* coverage, unsigned long long* covered, cudaStream_t s);
 cudaError_t launch_normalize_rows(const float* in, const uint32_t* select, uint64_t n, uint32_t dim, float* out,
                                   int* zero_flag, cudaStream_t s);
 // eval.hpp:122-158 (labels [n_labels][dim]; labels_t, label_norms: scratch)

@@ -19,7 +19,7 @@ import numpy as np
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
 from oracle.bindings import Oracle  # noqa: E402
-from paper_2505_08124_b200.workload import orbit_camera, synth_scene  # noqa: E402
+from harness.workload import orbit_camera, synth_scene  # noqa: E402
 
 W, H = 1152, 864
 

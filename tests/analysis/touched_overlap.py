@@ -8,7 +8,7 @@ import numpy as np
 sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
 from oracle.bindings import Oracle  # noqa: E402  (decoder for the experiment only)
 from paper_2505_08124_b200._lib import Context  # noqa: E402
-from paper_2505_08124_b200.workload import CONFIGS, make_bench_workload  # noqa: E402
+from harness.workload import CONFIGS, make_bench_workload  # noqa: E402
 
 cfg = CONFIGS["c4"]
 views = list(range(8))

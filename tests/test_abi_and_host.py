@@ -44,7 +44,7 @@ def test_no_device_fails_loudly():
 
 
 def test_synth_embedding_matches_reference_golden():
-    from paper_2505_08124_b200.workload import synth_embedding
+    from harness.workload import synth_embedding
     from tests.goldens import golden
     z = golden("synth")
     for label, vec in zip(z["labels"], z["vectors"]):
@@ -65,7 +65,7 @@ def test_mt19937_64_known_answer():
 def test_query_store_generator_matches_cmd_bench():
     """main.cpp:440-450: store rows then queries, f32((rng()>>11)+0.5)*2^-53-0.5,
     from std::mt19937_64(seed ^ 0xbe9c)."""
-    from paper_2505_08124_b200.workload import query_workload
+    from harness.workload import query_workload
     from tests.util import MT19937_64
     rows, queries = query_workload(2505, 5, 3, 16)
     m = MT19937_64(2505 ^ 0xBE9C)
@@ -75,7 +75,7 @@ def test_query_store_generator_matches_cmd_bench():
 
 
 def test_look_at_matches_reference(ref):
-    from paper_2505_08124_b200.workload import orbit_camera
+    from harness.workload import orbit_camera
     for v in (0, 7, 333):
         c = orbit_camera(v, 1000, 1152, 864)
         import math
@@ -86,7 +86,7 @@ def test_look_at_matches_reference(ref):
 
 def test_rect_masks_decode_to_rectangles(oracle):
     from paper_2505_08124_b200.formats import rle_runs_from_bitmap
-    from paper_2505_08124_b200.workload import rect_masks
+    from harness.workload import rect_masks
     runs, offs = rect_masks(99, 120, 90, 40)
     assert offs.shape[0] == 41
     for j in range(40):

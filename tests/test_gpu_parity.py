@@ -219,7 +219,7 @@ def test_encode_fixtures_vs_reference_golden(gpu_ctx):
 
 
 def _bench_style(n, views, w, h, m, dim, seed):
-    from paper_2505_08124_b200.workload import make_bench_workload
+    from harness.workload import make_bench_workload
     return make_bench_workload(n_gaussians=n, n_views=views, width=w, height=h, masks_per_view=m, dim=dim,
                                seed=seed, xy_extent=5.0)
 
@@ -609,3 +609,80 @@ def test_encode_views_without_masks_interleaved(gpu_ctx, oracle, lanes, group):
     er, ec = oracle.encode(wl.scene, cams, masks, 512)
     rel, cos = row_errors(rows, cov, er, ec)
     assert rel <= EMB_REL_TOL and cos >= EMB_COS_TOL, (rel, cos)
+
+
+def test_failed_encode_leaves_no_stale_weights(gpu_ctx, oracle):
+    """A batch that fails on view 2 (bad RLE length: FormatError, providers.hpp:97-107)
+    after views 0 and 1 were composited into an open contraction group must
+    not leak their per-(Gaussian, mask) scalars into the next encode, even when
+    that encode has a different mask count."""
+    from paper_2505_08124_b200 import FormatError
+    wl = _bench_style(3000, 4, 80, 64, 40, 512, seed=101)
+    bad = list(wl.masks)
+    n, w, h, runs, offs, clip = bad[2]
+    runs = runs.copy()
+    runs[0] += 1
+    bad[2] = (n, w, h, runs, offs, clip)
+    gpu_ctx.set_scene(wl.scene.mean, wl.scene.scale, wl.scene.quat_xyzw, wl.scene.opacity)
+    gpu_ctx.encode_begin(512)
+    with pytest.raises(FormatError):
+        gpu_ctx.encode_views(wl.cams, bad)
+    good = _bench_style(3000, 3, 80, 64, 24, 512, seed=102)
+    good.scene = wl.scene
+    rows, cov = _encode(gpu_ctx, wl.scene, good.cams, good.masks, 512)
+    er, ec = oracle.encode(wl.scene, good.cams, good.masks, 512)
+    rel, cos = row_errors(rows, cov, er, ec)
+    assert rel <= EMB_REL_TOL and cos >= EMB_COS_TOL, (rel, cos)
+
+
+def _singular_scene():
+    """Rank-one, huge (1e7) Gaussians rotated off the image axes: after
+    projection cov_xx * cov_yy - cov_xy^2 rounds below 1e-12 (rasterizer.hpp:66-69).
+    Four of them; 10 has the smallest id but the first in depth order is 120
+    (tied in depth with 250, so the id breaks the tie)."""
+    s = random_scene(300, 41)
+    c, sn = np.float32(np.cos(np.pi / 8)), np.float32(np.sin(np.pi / 8))
+    for gid, z in [(10, 1.0), (250, -2.0), (120, -2.0), (77, 2.5)]:
+        s.scale[gid] = [1e7, 1e-3, 1e-3]
+        s.quat_xyzw[gid] = [0, 0, sn, c]
+        s.mean[gid] = [0.1, 0.2, z]
+    return s
+
+
+def test_singular_covariance_names_first_in_depth_order(gpu_ctx, ref):
+    """NumericError from conic_of names the first singular projection in depth
+    order (rasterizer.hpp:66-69 inside the depth-sorted loop :187-191), as
+    the reference build does; the encode path wraps it as the reference's
+    per-image DataError (pipeline.hpp:350-351)."""
+    from paper_2505_08124_b200 import DataError, NumericError
+    from oracle.bindings import RefError
+    s = _singular_scene()
+    cam = make_test_camera(64, 48, 7.0, image_id=5)
+    with pytest.raises(RefError) as er:
+        ref.rasterize(s, cam)
+    assert "gaussian 120" in str(er.value)
+    gpu_ctx.set_scene(s.mean, s.scale, s.quat_xyzw, s.opacity)
+    with pytest.raises(NumericError) as eg:
+        gpu_ctx.raster_capture(cam, 0)
+    assert str(eg.value).endswith("singular screen covariance for gaussian 120"), str(eg.value)
+    from tests.util import rect_mask_runs
+    runs, _ = rect_mask_runs(64, 48, [(3, 4, 40, 30)])
+    masks = [(1, 64, 48, runs.astype(np.uint32), np.array([0, len(runs)], np.uint64),
+              np.ones((1, 8), np.float32))]
+    gpu_ctx.encode_begin(8)
+    with pytest.raises(DataError) as ed:
+        gpu_ctx.encode_views([cam], masks)
+    assert str(ed.value).endswith("image 5: singular screen covariance for gaussian 120"), str(ed.value)
+
+
+@pytest.mark.parametrize("m,dim", [(200, 512), (129, 64), (300, 16)])
+def test_encode_more_than_128_masks_vs_oracle(gpu_ctx, oracle, m, dim):
+    """Views with more SAM masks than one compositor pass holds (providers.hpp:135
+    reads any u32 count; pipeline.hpp:323-336 loops over all of them): 128-mask
+    windows, each a compositor pass, then the general contraction."""
+    wl = _bench_style(3000, 3, 96, 72, m, dim, seed=m + dim)
+    rows, cov = _encode(gpu_ctx, wl.scene, wl.cams, wl.masks, dim)
+    er, ec = oracle.encode(wl.scene, wl.cams, wl.masks, dim)
+    rel, cos = row_errors(rows, cov, er, ec)
+    assert rel <= EMB_REL_TOL and cos >= EMB_COS_TOL, (rel, cos)
+    np.testing.assert_allclose(cov, ec, rtol=1e-5)

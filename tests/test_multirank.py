@@ -29,7 +29,7 @@ def _worker(rank, world, port, q):
 
     from oracle.bindings import Oracle
     from paper_2505_08124_b200.multigpu import padded_rows, reduce_scatter_rows, shard_rows, shard_views
-    from paper_2505_08124_b200.workload import make_bench_workload
+    from harness.workload import make_bench_workload
 
     dist.init_process_group("gloo", rank=rank, world_size=world)
     wl = make_bench_workload(n_gaussians=1501, n_views=5, width=64, height=48, masks_per_view=12, dim=32, seed=3)
@@ -78,7 +78,7 @@ def test_two_rank_combine_matches_single_worker():
     from pathlib import Path
     sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
     from oracle.bindings import Oracle
-    from paper_2505_08124_b200.workload import make_bench_workload
+    from harness.workload import make_bench_workload
     wl = make_bench_workload(n_gaussians=1501, n_views=5, width=64, height=48, masks_per_view=12, dim=32, seed=3)
     er, ec = Oracle().encode(wl.scene, wl.cams, wl.masks, 32)
     assert np.array_equal(cov > 0, ec > 0)

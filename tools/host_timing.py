@@ -2,7 +2,7 @@
 import sys, time; sys.path.insert(0,'.')
 import numpy as np, torch
 from paper_2505_08124_b200._lib import Context
-from paper_2505_08124_b200.workload import make_bench_workload
+from harness.workload import make_bench_workload
 wl = make_bench_workload(2_000_000, 1000, 1152, 864, 64, 512, seed=1, views=list(range(48)))
 ctx = Context(0); ctx.set_scene(wl.scene.mean, wl.scene.scale, wl.scene.quat_xyzw, wl.scene.opacity)
 dev=torch.device('cuda',0)
