@@ -33,7 +33,7 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-from harness.workload import CONFIGS, make_bench_workload  # noqa: E402
+from harness.workload import CONFIGS, make_bench_workload, write_reference_dataset  # noqa: E402
 
 PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
 FALLBACK_HBM = 6650.0
@@ -137,32 +137,11 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------- reference arm
-def write_reference_dataset(wl, directory: str):
-    """The sample in the reference's on-disk formats (manifest/cameras/MRLE/EMBV)."""
-    from paper_2505_08124_b200 import formats
-    d = Path(directory)
-    (d / "masks").mkdir(parents=True, exist_ok=True)
-    (d / "embeddings").mkdir(exist_ok=True)
-    cams = []
-    m = formats.DatasetManifest(root=str(d), camera_file="cameras.txt", mask_width=wl.width, mask_height=wl.height,
-                                raster_width=wl.width, raster_height=wl.height, embedding_dim=wl.dim)
-    for cam, (n, w, h, runs, offs, clip) in zip(wl.cams, wl.masks):
-        cams.append(formats.CameraPose(image_id=cam.image_id, fx=cam.fx, fy=cam.fy, cx=cam.cx, cy=cam.cy,
-                                       rotation=cam.rotation, translation=cam.translation, width=w, height=h))
-        mr = formats.MaskRuns(cam.image_id, w, h, np.arange(n, dtype=np.uint32), runs, offs)
-        formats.save_maskset_runs(mr, str(d / "masks" / f"{cam.image_id}.rle"))
-        formats.save_mask_embeddings(clip, str(d / "embeddings" / f"{cam.image_id}.emb"))
-        m.images.append(formats.ImageEntry(cam.image_id, "-", cam.image_id, f"masks/{cam.image_id}.rle",
-                                           f"embeddings/{cam.image_id}.emb"))
-    formats.save_cameras(cams, str(d / "cameras.txt"))
-    formats.save_manifest(m, str(d / "manifest.txt"))
-    return str(d / "manifest.txt")
-
-
 def cpu_reference_sample(cfg_name, seed, views, threads=None):
     """Times the reference's encode_scene (oracle/_ref) -- or, where the
     reference build is absent, the oracle port -- on `views` views of the
-    config.  Returns (seconds, kind, cores, sample description)."""
+    config.  Returns (seconds, kind, cores, sample description, workload,
+    (rows, coverage) of the reference's table for the sample)."""
     cfg = CONFIGS[cfg_name]
     threads = threads or os.cpu_count() or 1
     wl = make_bench_workload(n_gaussians=cfg["n_gaussians"], n_views=cfg["n_views"], width=cfg["width"],
@@ -179,16 +158,45 @@ def cpu_reference_sample(cfg_name, seed, views, threads=None):
         # phase-2 partials are workers x chunk x D f64 (pipeline.hpp:417): bound them to ~8 GB
         chunk = int(max(4096, min(n, (8 << 30) // (workers * cfg["dim"] * 8))))
         t0 = time.perf_counter()
-        R.encode(wl.scene, mp, workers, chunk)
+        rows, cov, _ = R.encode(wl.scene, mp, workers, chunk)
         dt = time.perf_counter() - t0
         return dt, "reference", workers, (f"{views} of {cfg['n_views']} views of {cfg_name} through the reference "
-                                          f"encode_scene (workers={workers}, chunk_rows={chunk})")
+                                          f"encode_scene (workers={workers}, chunk_rows={chunk})"), wl, (rows, cov)
     from oracle.bindings import Oracle
     O = Oracle()
     t0 = time.perf_counter()
-    O.encode(wl.scene, wl.cams, wl.masks, cfg["dim"])
+    rows, cov = O.encode(wl.scene, wl.cams, wl.masks, cfg["dim"])
     dt = time.perf_counter() - t0
-    return dt, "port", 1, f"{views} of {cfg['n_views']} views of {cfg_name} through the C oracle (1 thread)"
+    return (dt, "port", 1, f"{views} of {cfg['n_views']} views of {cfg_name} through the C oracle (1 thread)", wl,
+            (rows, cov))
+
+
+PARITY_REL, PARITY_COS = 1e-4, 0.9999  # BASELINE.json north_star tolerance (per-row relative L2, cosine)
+
+
+def table_parity(rows, cov, ref_rows, ref_cov):
+    """Per-row relative L2 and cosine of the device table against the
+    reference's (oracles.hpp:129-160 definitions), over covered rows; the
+    covered sets must be identical."""
+    cg, ce = cov > np.float32(1e-8), ref_cov > np.float32(1e-8)
+    out = {"max_row_rel": 0.0, "min_cos": 1.0, "covered_equal": bool(np.array_equal(cg, ce)),
+           "covered_rows": int(ce.sum()), "uncovered_rows_zero": bool(not rows[~cg].any())}
+    for lo in range(0, rows.shape[0], 1 << 18):
+        sl = slice(lo, lo + (1 << 18))
+        m = ce[sl]
+        if not m.any():
+            continue
+        e = ref_rows[sl][m].astype(np.float64)
+        g = rows[sl][m].astype(np.float64)
+        den = np.sqrt((e * e).sum(1))
+        rel = np.sqrt(((e - g) ** 2).sum(1)) / np.where(den > 0, den, 1.0)
+        cos = (e * g).sum(1) / np.maximum(np.sqrt((e * e).sum(1) * (g * g).sum(1)), 1e-300)
+        out["max_row_rel"] = max(out["max_row_rel"], float(rel.max()))
+        out["min_cos"] = min(out["min_cos"], float(cos.min()))
+    out["ok"] = bool(out["covered_equal"] and out["uncovered_rows_zero"] and out["max_row_rel"] <= PARITY_REL
+                     and out["min_cos"] >= PARITY_COS)
+    out["tolerance"] = {"max_row_rel": PARITY_REL, "min_cos": PARITY_COS}
+    return out
 
 
 def query_leg(ctx, args, dev, stream, want_cpu):
@@ -312,7 +320,7 @@ def run_reference_arm(args, rank, world):
     views = args.cpu_sample_views or max(1, min(cores, 16))
     times = []
     for i in range(args.warmup + args.steps):
-        dt, kind, used, sample = cpu_reference_sample(args.config, args.seed, views, cores)
+        dt, kind, used, sample, _, _ = cpu_reference_sample(args.config, args.seed, views, cores)
         if i >= args.warmup:
             times.append(dt)
     sec = float(np.mean(times))
@@ -499,12 +507,21 @@ def main():
     pass_bytes = sum(v["bytes"] for k, v in prof.items() if k not in ("h2d", "query"))
 
     cpu = None
+    parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             sample = args.cpu_sample_views or max(1, min(os.cpu_count() or 1, 16))
-            dt, kind, cores, desc = cpu_reference_sample(args.config, args.seed, sample)
+            dt, kind, cores, desc, swl, (er, ec) = cpu_reference_sample(args.config, args.seed, sample)
             cpu = {"value": sample / dt, "unit": "views/s", "cores": cores, "kind": kind, "sample": desc,
                    "seconds": dt}
+            # parity at the benchmarked configuration: the same sample views
+            # through the device pass (context-owned accumulators, same C ABI)
+            ctx.encode_begin(D)
+            ctx.encode_views(swl.cams, swl.masks)
+            prow, pcov = ctx.encode_finalize()
+            parity = table_parity(prow, pcov, er, ec)
+            parity["sample"] = f"views 0..{sample - 1} of {args.config} vs the {kind} encode_scene table"
+            del prow, pcov, er, ec
         except Exception as ex:  # reported, not fatal
             cpu = {"value": None, "unit": "views/s", "cores": None, "kind": "unavailable", "sample": str(ex)}
 
@@ -571,6 +588,7 @@ def main():
                                   ("n_vis", "instances", "touched", "pairs")},
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "parity": parity,
             "clocks": clk.summary(),
             "gpu_launches": int((own + cub) / max(args.steps, 1)),
             "gpu_launches_detail": {"own_per_step": own / max(args.steps, 1), "cub_per_step": cub / max(args.steps, 1)},
@@ -582,6 +600,10 @@ def main():
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
+    if parity is not None and not parity["ok"]:
+        # loud: the bench configuration does not match the reference
+        print(f"PARITY FAILURE at {args.config}: {json.dumps(parity)}", file=sys.stderr, flush=True)
+        sys.exit(3)
 
 
 if __name__ == "__main__":
