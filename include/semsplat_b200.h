@@ -102,8 +102,20 @@ int ss_synchronize(ss_ctx* ctx);
  * SS_OPT_BIN_PATH: tile lists from 0 = auto (default: direct count/scan/
  * scatter binning for views of <= 5734 16x16 tiles, else the key sort),
  * 1 = stable key sort, 2 = direct binning (up to 18000 tiles; error above).
- * The tile lists are identical. */
-enum ss_option { SS_OPT_LANES = 1, SS_OPT_QUERY_PATH = 2, SS_OPT_CONTRACT_GROUP = 3, SS_OPT_BIN_PATH = 4 };
+ * The tile lists are identical.
+
+ * SS_OPT_RASTER: compositor schedule, 0 = staged evaluation (default: per
+ * staged chunk, the box test and Mahalanobis distance per splat, then exp and
+ * alpha dense over the surviving pairs, then the front-to-back transmittance
+ * walk), 1 = one splat per step for all pixels of a warp's block.  Identical
+ * bits. */
+enum ss_option {
+    SS_OPT_LANES = 1,
+    SS_OPT_QUERY_PATH = 2,
+    SS_OPT_CONTRACT_GROUP = 3,
+    SS_OPT_BIN_PATH = 4,
+    SS_OPT_RASTER = 5
+};
 int ss_set_option(ss_ctx* ctx, int option, int64_t value);
 
 /* ---- scene (GaussianScene, scene.hpp:54-76) --------------------------- */

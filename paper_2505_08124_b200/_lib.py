@@ -192,6 +192,10 @@ class Context:
         """0 = auto, 1 = exact scan, 2 = tensor-core coarse + exact rescore."""
         check(self._L.ss_set_option(self.h, 2, int(path)))
 
+    def set_raster_algo(self, algo: int):
+        """SS_OPT_RASTER: 0 = staged-evaluation compositor (default), 1 = per-step compositor (same bits)."""
+        check(self._L.ss_set_option(self.h, 5, int(algo)))
+
     def set_bin_path(self, path: int):
         """0 = auto (direct binning up to 5734 tiles), 1 = stable key sort, 2 = direct count/scan/scatter."""
         check(self._L.ss_set_option(self.h, 4, int(path)))

@@ -233,6 +233,7 @@ struct ss_ctx {
     bool store_half_ok = false;
     int query_path = 0; // SS_OPT_QUERY_PATH
     int bin_path = 0;   // SS_OPT_BIN_PATH
+    int raster_algo = 0; // SS_OPT_RASTER
     int num_sms = 0;
 
     // instrumentation
@@ -484,7 +485,7 @@ RasterParams raster_params(ss_ctx* c, Lane& L, const ss_camera& cam, const Geome
     p.height = cam.height;
     p.tiles_x = g.tiles_x;
     p.info = L.info.as<ViewInfo>();
-    (void)c;
+    p.algo = (uint32_t)c->raster_algo;
     return p;
 }
 
@@ -892,6 +893,9 @@ int ss_set_option(ss_ctx* c, int option, int64_t value) {
         } else if (option == SS_OPT_QUERY_PATH) {
             if (value < 0 || value > 2) throw Error(SS_ERR_CONTRACT, "SS_OPT_QUERY_PATH must be 0, 1 or 2");
             c->query_path = (int)value;
+        } else if (option == SS_OPT_RASTER) {
+            if (value < 0 || value > 1) throw Error(SS_ERR_CONTRACT, "SS_OPT_RASTER must be 0 or 1");
+            c->raster_algo = (int)value;
         } else if (option == SS_OPT_BIN_PATH) {
             if (value < 0 || value > 2) throw Error(SS_ERR_CONTRACT, "SS_OPT_BIN_PATH must be 0, 1 or 2");
             c->bin_path = (int)value;

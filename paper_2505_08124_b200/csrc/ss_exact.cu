@@ -488,13 +488,253 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
     }
 }
 
+// ------------------------------------------------- staged-evaluation compositor
+// Same tile / warp / block shaping and the same staging of 32 list entries as
+// raster_kernel, but the per-(splat, pixel) work of a staged chunk is split by
+// what depends on the transmittance:
+//   A1  for each staged splat j (SIMT over the block's pixels): the box test
+//       and d2 (rasterizer.hpp:115-121, fp64, reference order); the pairs with
+//       d2 <= 9 are appended, j-major, to the warp's compact list (d2, j);
+//   A2  dense over that list, all 32 lanes busy: g = exp(-d2/2) (glibc
+//       restated) and alpha = min(0.99, o*g) (rasterizer.hpp:120-124) -- none
+//       of it depends on T;
+//   B   front to back over the staged splats with at least one such pair:
+//       each pixel reads its alpha at off_j + rank, applies the skip rule,
+//       w = alpha*T, the emission cutoff, T *= 1 - alpha and the floor
+//       (rasterizer.hpp:125-131), then counts / captures / gates exactly as
+//       raster_kernel.
+// Every pixel still sees exactly its box's splats in depth order with the
+// same operations, so the bits are raster_kernel's; the exp -- most of the
+// fp64 work -- runs on full warps instead of the ~40 % of lanes a (splat,
+// block) step keeps busy.  A list round holds <= kEvalCap pairs; a chunk with
+// more is split into rounds (A1 stops before a splat could overflow it).
+constexpr uint32_t kEvalCap = 256; // compacted (splat, pixel) evaluations per warp round
+
+template <int KIND, bool FALLOFF, int MW>
+__global__ void __launch_bounds__(kRasterThreads) raster_staged_kernel(RasterParams p) {
+    __shared__ SplatRec srec[kRasterThreads]; // warp w stages its hits in srec[32w, 32w+32)
+    __shared__ uint32_t sgid[kRasterThreads];
+    __shared__ uint32_t smask[kRasterThreads];
+    __shared__ double sval[kRasterThreads / 32][kEvalCap]; // d2, then alpha (or g: falloff)
+    __shared__ uint8_t sjj[kRasterThreads / 32][kEvalCap];  // staged splat of each list entry
+    __shared__ unsigned long long stab[256];
+    stab[threadIdx.x] = kExpTab[threadIdx.x];
+
+    const uint32_t tile = blockIdx.x;
+    const uint32_t tx = tile % p.tiles_x, ty = tile / p.tiles_x;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    const uint32_t bx0 = tx * kTile + 8u * (warp & 1u), by0 = ty * kTile + 4u * (warp >> 1);
+    const uint32_t bx1 = bx0 + 7u, by1 = by0 + 3u;
+    const uint32_t start = p.tile_start[tile], end = p.tile_end[tile];
+    if (p.info->overflow) return; // tile lists incomplete: the view is re-run by the host
+    const uint32_t wbase = 32u * warp;
+    SplatRec* wrec = srec + wbase;
+    const uint32_t srec_addr = (uint32_t)__cvta_generic_to_shared(wrec);
+    uint32_t stab_addr = (uint32_t)__cvta_generic_to_shared(stab);
+    uint32_t* wgid = sgid + wbase;
+    uint32_t* wmask = smask + wbase;
+    double* wval = sval[warp];
+    uint8_t* wjj = sjj[warp];
+
+    PixelState ps;
+    ps.px = bx0 + (lane & 7u);
+    ps.py = by0 + (lane >> 3);
+    ps.inside = ps.px < p.width && ps.py < p.height;
+    ps.pixel = ps.py * p.width + ps.px;
+    ps.dpx = (double)(int32_t)ps.px;
+    ps.dpy = (double)(int32_t)ps.py;
+    ps.T = 1.0;
+    ps.total = 0.0;
+    ps.count = 0;
+    ps.out = 0;
+    ps.done = !ps.inside;
+    double csum[3] = {0.0, 0.0, 0.0}; // render (KIND 3): color_sum, rasterizer.hpp:224
+    if constexpr (KIND == 1 || KIND == 3) {
+        if (ps.inside) ps.out = p.pix_offset[ps.pixel];
+    }
+    uint32_t bits[MW];
+    uint32_t grp = 0;
+    if constexpr (KIND == 2) {
+        bool any = false;
+#pragma unroll
+        for (int w = 0; w < MW; ++w) {
+            bits[w] = ps.inside ? p.pix_bits[(size_t)ps.pixel * p.bits_stride + (p.mask_base >> 5) + w] : 0u;
+            any |= bits[w] != 0;
+        }
+        grp = match_bits<MW>(bits);
+        ps.done = ps.done || !any; // unmasked pixels contribute nothing
+    }
+    __syncthreads(); // exp table staged
+
+    uint32_t nr = 0;
+    uint2 nbox = make_uint2(0u, 0u);
+    if (start + lane < end) {
+        nr = __ldg(p.tile_list + start + lane);
+        nbox = __ldg(p.boxes + nr);
+    }
+    const uint32_t lane_bit = 1u << lane, below = lane_bit - 1u;
+    bool finished = false;
+    for (uint32_t base = start; base < end && !finished; base += 32u) {
+        const uint32_t live = ~__ballot_sync(0xffffffffu, ps.done);
+        if (live == 0u) break;
+        const uint32_t i = base + lane;
+        const uint32_t r = nr;
+        const uint2 box = nbox;
+        if (i + 32u < end) { // software prefetch of the next chunk
+            nr = __ldg(p.tile_list + i + 32u);
+            nbox = __ldg(p.boxes + nr);
+        }
+        const uint32_t sx0 = box.x & 0xffffu, sx1 = box.x >> 16, sy0 = box.y & 0xffffu, sy1 = box.y >> 16;
+        uint32_t m = 0u;
+        if (i < end && !(sx1 < bx0 || sx0 > bx1 || sy1 < by0 || sy0 > by1))
+            m = block_box_mask(sx0, sx1, sy0, sy1, bx0, by0) & live;
+        const uint32_t cand = __ballot_sync(0xffffffffu, m != 0u);
+        if (m) {
+            const uint32_t slot = __popc(cand & below);
+            const uint4* src = reinterpret_cast<const uint4*>(p.rec + r);
+            uint4* dst = reinterpret_cast<uint4*>(wrec + slot);
+            dst[0] = __ldg(src);
+            dst[1] = __ldg(src + 1);
+            dst[2] = __ldg(src + 2);
+            wgid[slot] = r;
+            wmask[slot] = m;
+        }
+        __syncwarp();
+        const uint32_t nh = __popc(cand);
+        // staged splat j's pixel mask and id live in lane j's registers
+        const uint32_t smk = lane < nh ? wmask[lane] : 0u;
+        const uint32_t sgd = lane < nh ? wgid[lane] : 0u;
+        for (uint32_t j0 = 0; j0 < nh && !finished;) {
+            // ---- A1: box test + d2 for the staged splats j0.., compacted
+            uint32_t ne = 0, e_reg = 0, off_reg = 0, j = j0;
+            for (; j < nh && ne + 32u <= kEvalCap; ++j) {
+                asm volatile("" : "+r"(stab_addr));
+                const uint32_t mj = __shfl_sync(0xffffffffu, smk, j);
+                bool pass = false;
+                double d2 = 0.0;
+                if ((mj & lane_bit) && !ps.done) {
+                    const uint32_t a = srec_addr + j * (uint32_t)sizeof(SplatRec);
+                    double mu_x, mu_y, ca, cb2, cc;
+                    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(mu_x), "=d"(mu_y) : "r"(a));
+                    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2+16];" : "=d"(ca), "=d"(cb2) : "r"(a));
+                    asm volatile("ld.shared.f64 %0, [%1+32];" : "=d"(cc) : "r"(a));
+                    const double dx = ds(ps.dpx, mu_x), dy = ds(ps.dpy, mu_y);
+                    d2 = da(da(dm(dm(ca, dx), dx), dm(dm(cb2, dx), dy)), dm(dm(cc, dy), dy));
+                    pass = !(d2 > kMahalanobisSqCutoff); // NaN continues, as in the reference
+                }
+                const uint32_t e = __ballot_sync(0xffffffffu, pass);
+                if (pass) {
+                    const uint32_t slot = ne + __popc(e & below);
+                    wval[slot] = d2;
+                    wjj[slot] = (uint8_t)j;
+                }
+                if (lane == j) {
+                    e_reg = e;
+                    off_reg = ne;
+                }
+                ne += __popc(e);
+            }
+            const uint32_t j1 = j;
+            __syncwarp();
+            // ---- A2: exp and alpha, dense over the list
+            for (uint32_t k = lane; k < ne; k += 32u) {
+                const double d2 = wval[k];
+                const double g = glibc_exp_s(dm(-0.5, d2), stab_addr);
+                if constexpr (FALLOFF) {
+                    wval[k] = g;
+                } else {
+                    double o;
+                    asm volatile("ld.shared.f64 %0, [%1+40];"
+                                 : "=d"(o)
+                                 : "r"(srec_addr + (uint32_t)wjj[k] * (uint32_t)sizeof(SplatRec)));
+                    const double og = dm(o, g);
+                    // std::min(kAlphaMax, og) (rasterizer.hpp:124): (og < max) ? og : max, NaN -> max
+                    const double amax = kCompositeConst[0];
+                    wval[k] = og < amax ? og : amax;
+                }
+            }
+            __syncwarp();
+            // ---- B: front to back over the splats with an evaluated pair
+            uint32_t todo = __ballot_sync(0xffffffffu, e_reg != 0u);
+            uint32_t steps = 0;
+            while (todo) {
+                const uint32_t jb = __ffs(todo) - 1u;
+                todo &= todo - 1u;
+                const uint32_t ej = __shfl_sync(0xffffffffu, e_reg, jb);
+                const uint32_t oj = __shfl_sync(0xffffffffu, off_reg, jb);
+                const uint32_t gj = __shfl_sync(0xffffffffu, sgd, jb);
+                float wf = 0.0f;
+                bool c = false;
+                if ((ej & lane_bit) && !ps.done) {
+                    const double v = wval[oj + __popc(ej & below)];
+                    if constexpr (FALLOFF) {
+                        if (v >= kWeightCutoff) {
+                            wf = __double2float_rn(v);
+                            c = true;
+                        }
+                    } else if (v >= kCompositeConst[1]) { // else: alpha < 1/255 skips, T untouched
+                        const double w = dm(v, ps.T);
+                        c = w >= kCompositeConst[2];
+                        if (c) wf = __double2float_rn(w);
+                        ps.T = dm(ps.T, ds(1.0, v));
+                        if (ps.T < kCompositeConst[3]) ps.done = true;
+                    }
+                }
+                if constexpr (KIND == 0) {
+                    ps.count += c ? 1u : 0u;
+                } else if constexpr (KIND == 1 || KIND == 3) {
+                    if (c) {
+                        p.entries[ps.out++] = ss_weight_entry{gj, ps.pixel, wf};
+                        ps.total = da(ps.total, (double)wf);
+                        if constexpr (KIND == 3) {
+                            const float4 col = __ldg(p.color + gj);
+                            csum[0] = da(csum[0], dm((double)wf, (double)col.x));
+                            csum[1] = da(csum[1], dm((double)wf, (double)col.y));
+                            csum[2] = da(csum[2], dm((double)wf, (double)col.z));
+                        }
+                    }
+                } else {
+                    gate_and_accumulate<MW>(p, c, wf, grp, bits, gj, lane);
+                }
+                if ((++steps & 7u) == 0u && __all_sync(0xffffffffu, ps.done)) {
+                    finished = true;
+                    break;
+                }
+            }
+            if (__all_sync(0xffffffffu, ps.done)) finished = true;
+            j0 = j1;
+            __syncwarp();
+        }
+        __syncwarp();
+    }
+    if (ps.inside) {
+        if constexpr (KIND == 0) {
+            p.pix_count[ps.pixel] = ps.count;
+        } else if constexpr (KIND == 1 || KIND == 3) {
+            p.per_pixel_total[ps.pixel] = __double2float_rn(ps.total);
+            p.alpha[ps.pixel] = __double2float_rn(ds(1.0, ps.T));
+            if constexpr (KIND == 3) {
+                if (ps.total > 1e-6) {
+#pragma unroll
+                    for (int k = 0; k < 3; ++k)
+                        p.image[3ull * ps.pixel + k] = __double2float_rn(dd(csum[k], ps.total));
+                }
+            }
+        }
+    }
+}
+
 template <int KIND>
 cudaError_t launch_raster(const RasterParams& p, int mode, uint32_t tiles, cudaStream_t s) {
     if (tiles == 0) return cudaSuccess;
-    if (mode == SS_FALLOFF_ONLY)
-        raster_kernel<KIND, true, 1><<<tiles, kRasterThreads, 0, s>>>(p);
-    else
-        raster_kernel<KIND, false, 1><<<tiles, kRasterThreads, 0, s>>>(p);
+    const bool fo = mode == SS_FALLOFF_ONLY;
+    if (p.algo == 1) {
+        if (fo) raster_kernel<KIND, true, 1><<<tiles, kRasterThreads, 0, s>>>(p);
+        else raster_kernel<KIND, false, 1><<<tiles, kRasterThreads, 0, s>>>(p);
+    } else {
+        if (fo) raster_staged_kernel<KIND, true, 1><<<tiles, kRasterThreads, 0, s>>>(p);
+        else raster_staged_kernel<KIND, false, 1><<<tiles, kRasterThreads, 0, s>>>(p);
+    }
     return cudaGetLastError();
 }
 
@@ -574,8 +814,13 @@ cudaError_t launch_raster_fused(const RasterParams& p, int mode, uint32_t tiles,
     const bool fo = mode == SS_FALLOFF_ONLY;
 #define SS_FUSED(MWV)                                                                       \
     do {                                                                                    \
-        if (fo) raster_kernel<2, true, MWV><<<tiles, kRasterThreads, 0, s>>>(p);           \
-        else raster_kernel<2, false, MWV><<<tiles, kRasterThreads, 0, s>>>(p);             \
+        if (p.algo == 1) {                                                                  \
+            if (fo) raster_kernel<2, true, MWV><<<tiles, kRasterThreads, 0, s>>>(p);       \
+            else raster_kernel<2, false, MWV><<<tiles, kRasterThreads, 0, s>>>(p);         \
+        } else {                                                                            \
+            if (fo) raster_staged_kernel<2, true, MWV><<<tiles, kRasterThreads, 0, s>>>(p); \
+            else raster_staged_kernel<2, false, MWV><<<tiles, kRasterThreads, 0, s>>>(p);   \
+        }                                                                                   \
     } while (0)
     switch (p.mask_words) {
     case 1: SS_FUSED(1); break;
