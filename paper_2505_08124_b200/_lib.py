@@ -197,7 +197,8 @@ class Context:
         check(self._L.ss_set_option(self.h, 5, int(algo)))
 
     def set_bin_path(self, path: int):
-        """0 = auto (direct binning up to 5734 tiles), 1 = stable key sort, 2 = direct count/scan/scatter."""
+        """0 = auto (tile-sort binning up to 16384 tiles, else direct / key sort), 1 = stable key sort,
+        2 = direct count/scan/scatter, 3 = tile-sort binning."""
         check(self._L.ss_set_option(self.h, 4, int(path)))
 
     def synchronize(self):

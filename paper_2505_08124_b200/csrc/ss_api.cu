@@ -146,6 +146,8 @@ struct Lane {
     uint32_t set_next = 0;
     DevBuf rec, boxes, rbox, rcnt, keys, k32, k32s, order, iota, offsets, tkeys, tkeys_sorted, tvals, tile_start, tile_end, list;
     DevBuf bin_counts, bin_slice, bin_tot, bin_done; // direct binning scratch
+    DevBuf ts_fill, ts_slab;       // tile-sort binning: per-tile fill counters, unordered (key, gid) slots
+    uint32_t ts_cap = 4096;        // tile-sort slots per tile (grown to the largest tile seen)
     uint64_t iota_n = 0;           // entries of the 0..n-1 sequence in `iota`
     uint64_t list_cap = 0;         // entries of `list`
     DevBuf cub_tmp, info;
@@ -155,7 +157,7 @@ struct Lane {
     void release_all() {
         DevBuf* b[] = {&rec, &boxes, &rbox, &rcnt, &keys, &k32, &k32s, &order, &iota, &offsets, &tkeys, &tkeys_sorted, &tvals, &tile_start,
                        &tile_end, &list, &cub_tmp, &info, &pix_bits, &mask_bits, &bin_counts, &bin_slice, &bin_tot, &bin_done,
-                       &runs, &run_offsets, &spans};
+                       &runs, &run_offsets, &spans, &ts_fill, &ts_slab};
         for (auto* x : b) x->release();
         for (auto& cs : sets) cs.release();
         if (raster_done) cudaEventDestroy(raster_done);
@@ -215,6 +217,7 @@ struct ss_ctx {
     bool color_ok = false;     // colors uploaded for the current scene
     bool cap_image = false;    // the last capture rendered an image
     uint64_t cap_entries = 0, cap_splats = 0, cap_instances = 0;
+    bool cap_tile_sort = false; // the last capture's lists are per-tile slot ranges
     uint32_t cap_width = 0, cap_height = 0, cap_tiles = 0;
     ss::DevBuf counters; // [0] G_v sum, [1] K_v sum, [2] contraction rows RMW, [3] covered rows normalised
     // accumulators
@@ -314,13 +317,23 @@ uint32_t first_singular_gid(ss_ctx* c, const ss_camera& cam) {
 struct Geometry {
     uint32_t tiles_x = 0, tiles_y = 0, tiles = 0;
     bool k16 = true; // 16-bit tile keys
+    bool tile_sort = false; // lists from the tile-sort binning (no global depth order)
 };
+
+// The fused pass bins by tile sort (SS_OPT_BIN_PATH 0 or 3) unless the view
+// needs the global depth order (captures report it) or was sent back to the
+// global path (bin_fallback 2).
+bool use_tile_sort(const ss_ctx* c, uint32_t tiles, bool force_global) {
+    if (force_global) return false;
+    return (c->bin_path == 0 || c->bin_path == 3) && tiles <= tile_sort_max_tiles();
+}
 
 // project (+ per-tile instance counts) -> scan -> scatter ids into tile
 // slices -> per-tile (depth, id) sort.  No host synchronisation: sizes,
 // offsets and key ranges stay on the device; a view whose tile lists would
 // overflow the list buffer raises info->overflow and its compositor skips.
-Geometry run_geometry(ss_ctx* c, Lane& L, cudaStream_t s, const ss_camera& cam) {
+Geometry run_geometry(ss_ctx* c, Lane& L, cudaStream_t s, const ss_camera& cam, bool force_global = false,
+                      bool need_order = false) {
     Geometry g;
     const uint64_t N = c->n;
     g.tiles_x = (cam.width + kTile - 1) / kTile;
@@ -341,8 +354,10 @@ Geometry run_geometry(ss_ctx* c, Lane& L, cudaStream_t s, const ss_camera& cam) 
         throw Error(SS_ERR_CONTRACT, "SS_OPT_BIN_PATH=2: too many tiles for the direct binning path");
     // auto: the direct path where its scatter runs 8-warp CTAs (<= 5734 tiles);
     // with 4-warp CTAs (larger views) the key sort is faster (c3: 1029 vs 989 views/s)
-    const bool direct = c->bin_path == 2 || (c->bin_path == 0 && bin_warps == 8);
-    if (!direct) {
+    const bool direct = c->bin_path == 2 || (c->bin_path != 1 && bin_warps == 8);
+    if (c->bin_path == 3 && g.tiles > tile_sort_max_tiles())
+        throw Error(SS_ERR_CONTRACT, "SS_OPT_BIN_PATH=3: too many tiles for the tile-sort binning");
+    if (!direct && !use_tile_sort(c, g.tiles, force_global)) {
         L.tkeys.ensure(L.list_cap * (g.k16 ? 2 : 4));
         L.tkeys_sorted.ensure(L.list_cap * (g.k16 ? 2 : 4));
         L.tvals.ensure(L.list_cap * 4);
@@ -369,6 +384,31 @@ Geometry run_geometry(ss_ctx* c, Lane& L, cudaStream_t s, const ss_camera& cam) 
         own_launch(c, launch_project(p, s), SS_K_PROJECT);
         c->prof.bytes[SS_K_PROJECT] += 44.0 * (double)N;
     }
+    g.tile_sort = use_tile_sort(c, g.tiles, force_global);
+    if (g.tile_sort) {
+        // tile-sort binning: unordered per-tile slots, then an exact per-tile sort
+        Scope sc(c, s, SS_K_BIN);
+        TileSortParams tp;
+        tp.boxes = boxes;
+        tp.keys = keys;
+        tp.n = N;
+        tp.tiles = g.tiles;
+        tp.tiles_x = g.tiles_x;
+        tp.cap = L.ts_cap;
+        const uint64_t slots = (uint64_t)g.tiles * L.ts_cap;
+        tp.fill = static_cast<uint32_t*>(L.ts_fill.ensure((g.tiles + 1ull) * 4));
+        tp.slab = static_cast<uint2*>(L.ts_slab.ensure(slots * 8));
+        if (L.list_cap < slots) {
+            L.list_cap = slots;
+            list = static_cast<uint32_t*>(L.list.ensure(L.list_cap * 4));
+        }
+        tp.list = list;
+        tp.start = tstart;
+        tp.end = tend;
+        tp.info = info;
+        own_launch(c, launch_tile_sort_bin(tp, s), SS_K_BIN, 2);
+        if (!need_order) return g;
+    }
     auto* k32 = static_cast<uint32_t*>(L.k32.ensure(std::max<uint64_t>(N, 1) * 4));
     auto* k32s = static_cast<uint32_t*>(L.k32s.ensure(std::max<uint64_t>(N, 1) * 4));
     auto* order = static_cast<uint32_t*>(L.order.ensure(std::max<uint64_t>(N, 1) * 4));
@@ -392,6 +432,7 @@ Geometry run_geometry(ss_ctx* c, Lane& L, cudaStream_t s, const ss_camera& cam) 
         c->prof.launches[SS_K_SORT] += 1;
         own_launch(c, launch_tie_fixup(k32s, N, keys, order, s), SS_K_SORT);
     }
+    if (g.tile_sort) return g; // the depth order was only wanted for reporting (captures)
     if (direct) {
         // count / scan / scatter straight into the tile slices (no key sort)
         Scope sc(c, s, SS_K_BIN);
@@ -604,8 +645,8 @@ void flush_group(ss_ctx* c) {
     c->group.clear();
 }
 
-void encode_one(ss_ctx* c, Lane& L, const ss_camera& cam, const ss_view_masks* vm, int mode,
-                ViewInfo* vstat_slot) {
+bool encode_one(ss_ctx* c, Lane& L, const ss_camera& cam, const ss_view_masks* vm, int mode,
+                ViewInfo* vstat_slot, bool force_global) {
     check_camera(&cam);
     const uint32_t M = vm ? vm->n_masks : 0;
     const uint32_t words = mask_words_for(M);
@@ -633,7 +674,7 @@ void encode_one(ss_ctx* c, Lane& L, const ss_camera& cam, const ss_view_masks* v
         SS_CUDA(cudaMemcpyAsync(dc, vm->clip, (size_t)M * c->dim * 4, cudaMemcpyHostToDevice, s));
         c->prof.bytes[SS_K_H2D] += (double)M * c->dim * 4;
     }
-    const Geometry g = run_geometry(c, L, s, cam);
+    const Geometry g = run_geometry(c, L, s, cam, force_global);
     if (M) {
         // per-(Gaussian, mask) scalars: grow-only and kept zero by consume-and-clear
         const uint64_t need = c->n * (uint64_t)M;
@@ -682,6 +723,7 @@ void encode_one(ss_ctx* c, Lane& L, const ss_camera& cam, const ss_view_masks* v
     const uint32_t cap = c->group_max ? std::min<uint32_t>(c->group_max, kMaxGroup)
                                       : (c->dim == 512 && M <= 64 ? kAutoGroup : 1u);
     if (c->group.size() >= cap) flush_group(c);
+    return g.tile_sort;
 }
 
 // Encodes a batch of views with no per-view host synchronisation; the host
@@ -695,7 +737,9 @@ void encode_batch(ss_ctx* c, uint32_t nviews, const ss_camera* cams, const ss_vi
     std::vector<ViewInfo> hstat(nviews);
     std::vector<uint32_t> todo(nviews);
     for (uint32_t v = 0; v < nviews; ++v) todo[v] = v;
+    std::vector<uint8_t> force_global(nviews, 0), tile_sorted(nviews, 0);
     uint64_t max_inst = 0; // largest tile-instance count of the views that fit
+    uint64_t ts_slots = 0; // list entries the tile-sort binning needs
     for (int attempt = 0; attempt < 4 && !todo.empty(); ++attempt) {
         // lanes start after everything already queued on the user stream
         SS_CUDA(cudaEventRecord(c->ev_user, c->stream));
@@ -727,7 +771,13 @@ void encode_batch(ss_ctx* c, uint32_t nviews, const ss_camera* cams, const ss_vi
                 const uint32_t li = c->next_lane % c->n_lanes;
                 Lane& L = c->lanes[li];
                 c->next_lane = (li + 1) % c->n_lanes;
-                encode_one(c, L, cams[v], masks ? &masks[v] : nullptr, mode, vstat + v);
+                tile_sorted[v] = encode_one(c, L, cams[v], masks ? &masks[v] : nullptr, mode, vstat + v,
+                                            force_global[v] != 0);
+                if (tile_sorted[v]) {
+                    const uint64_t tiles = (uint64_t)((cams[v].width + kTile - 1) / kTile) *
+                                           ((cams[v].height + kTile - 1) / kTile);
+                    ts_slots = std::max<uint64_t>(ts_slots, tiles * L.ts_cap);
+                }
             }
             flush_group(c);
         }
@@ -744,7 +794,16 @@ void encode_batch(ss_ctx* c, uint32_t nviews, const ss_camera* cams, const ss_vi
                                              std::to_string(first_singular_gid(c, cams[v])));
             if (st.overflow) {
                 again.push_back(v);
-                need = std::max<uint64_t>(need, st.n_instances);
+                if (st.bin_fallback == 1 && st.max_fill <= kTileSortMax) {
+                    // a tile outgrew its slots: every lane's capacity grows to the largest tile seen
+                    uint32_t cap = 1024;
+                    while (cap < st.max_fill) cap <<= 1;
+                    for (auto& L : c->lanes) L.ts_cap = std::max(L.ts_cap, cap);
+                } else if (st.bin_fallback) {
+                    force_global[v] = 1; // beyond the in-CTA tile sort: the global depth sort path
+                } else {
+                    need = std::max<uint64_t>(need, st.n_instances);
+                }
                 continue;
             }
             max_inst = std::max<uint64_t>(max_inst, st.n_instances);
@@ -754,8 +813,13 @@ void encode_batch(ss_ctx* c, uint32_t nviews, const ss_camera* cams, const ss_vi
             c->cnt_inst += st.n_instances;
             c->cnt_views += 1;
             c->prof.bytes[SS_K_PROJECT] += 76.0 * (double)st.n_surv;
-            c->prof.bytes[SS_K_BIN] += 8.0 * (double)st.n_surv + 4.0 * (double)st.n_instances;
-            c->prof.bytes[SS_K_SORT] += 16.0 * (double)st.n_instances;
+            if (tile_sorted[v]) {
+                // boxes by gid, survivors' depth keys; (key, gid) slots written and read; the list written
+                c->prof.bytes[SS_K_BIN] += 8.0 * (double)c->n + 8.0 * (double)st.n_surv + 20.0 * (double)st.n_instances;
+            } else {
+                c->prof.bytes[SS_K_BIN] += 8.0 * (double)st.n_surv + 4.0 * (double)st.n_instances;
+                c->prof.bytes[SS_K_SORT] += 16.0 * (double)st.n_instances;
+            }
             if (M) c->prof.bytes[SS_K_RASTER] += 64.0 * (double)st.n_instances + P * ((M + 7) / 8);
         }
         for (auto& L : c->lanes)
@@ -768,7 +832,7 @@ void encode_batch(ss_ctx* c, uint32_t nviews, const ss_camera* cams, const ss_vi
     // the tile sort runs over the whole list capacity: track the views' actual
     // sizes (+1/16; a view that overflows is re-run with a larger capacity)
     if (max_inst) {
-        const uint64_t want = (max_inst + max_inst / 16 + 1023) / 1024 * 1024;
+        const uint64_t want = std::max<uint64_t>((max_inst + max_inst / 16 + 1023) / 1024 * 1024, ts_slots);
         for (auto& L : c->lanes)
             if (L.list_cap > want + want / 8) L.list_cap = want;
     }
@@ -897,7 +961,7 @@ int ss_set_option(ss_ctx* c, int option, int64_t value) {
             if (value < 0 || value > 1) throw Error(SS_ERR_CONTRACT, "SS_OPT_RASTER must be 0 or 1");
             c->raster_algo = (int)value;
         } else if (option == SS_OPT_BIN_PATH) {
-            if (value < 0 || value > 2) throw Error(SS_ERR_CONTRACT, "SS_OPT_BIN_PATH must be 0, 1 or 2");
+            if (value < 0 || value > 3) throw Error(SS_ERR_CONTRACT, "SS_OPT_BIN_PATH must be 0, 1, 2 or 3");
             c->bin_path = (int)value;
         } else {
             throw Error(SS_ERR_CONTRACT, "unknown option");
@@ -986,14 +1050,24 @@ void capture_view(ss_ctx* c, const ss_camera* cam, int mode, bool color, uint64_
     const uint64_t P = (uint64_t)cam->width * cam->height;
     ss::Lane& L = c->lanes[0];
     Geometry g;
+    bool force_global = false;
     for (int attempt = 0;; ++attempt) {
-        g = run_geometry(c, L, s, *cam);
+        g = run_geometry(c, L, s, *cam, force_global, true);
         SS_CUDA(cudaMemcpyAsync(L.h_info, L.info.p, sizeof(ViewInfo), cudaMemcpyDeviceToHost, s));
         SS_CUDA(cudaStreamSynchronize(s));
         if (!L.h_info->overflow) break;
-        if (attempt > 2) throw Error(SS_ERR_CUDA, "tile-list buffer kept overflowing");
-        L.list_cap = L.h_info->n_instances + L.h_info->n_instances / 16;
+        if (attempt > 3) throw Error(SS_ERR_CUDA, "tile-list buffer kept overflowing");
+        if (L.h_info->bin_fallback == 1 && L.h_info->max_fill <= kTileSortMax) {
+            uint32_t cap = 1024;
+            while (cap < L.h_info->max_fill) cap <<= 1;
+            L.ts_cap = std::max(L.ts_cap, cap);
+        } else if (L.h_info->bin_fallback) {
+            force_global = true;
+        } else {
+            L.list_cap = L.h_info->n_instances + L.h_info->n_instances / 16;
+        }
     }
+    c->cap_tile_sort = g.tile_sort;
     if (L.h_info->err_count)
         throw Error(SS_ERR_NUMERIC, "singular screen covariance for gaussian " +
                                         std::to_string(first_singular_gid(c, *cam)));
@@ -1120,7 +1194,20 @@ int ss_raster_fetch(ss_ctx* c, ss_weight_entry* entries, float* per_pixel_total,
             // tile lists hold Gaussian ids; report them as indices into the
             // depth-sorted splat list, as the reference's tile_bins do
             std::vector<uint32_t> ids(c->cap_instances);
-            SS_CUDA(cudaMemcpy(ids.data(), c->lanes[0].list.p, c->cap_instances * 4, cudaMemcpyDeviceToHost));
+            if (c->cap_tile_sort) {
+                // per-tile slot ranges: gather them in tile order
+                std::vector<uint32_t> st(c->cap_tiles), en(c->cap_tiles);
+                SS_CUDA(cudaMemcpy(st.data(), c->lanes[0].tile_start.p, c->cap_tiles * 4, cudaMemcpyDeviceToHost));
+                SS_CUDA(cudaMemcpy(en.data(), c->lanes[0].tile_end.p, c->cap_tiles * 4, cudaMemcpyDeviceToHost));
+                const uint64_t span = en.empty() ? 0 : *std::max_element(en.begin(), en.end());
+                std::vector<uint32_t> all(span);
+                if (span) SS_CUDA(cudaMemcpy(all.data(), c->lanes[0].list.p, span * 4, cudaMemcpyDeviceToHost));
+                uint64_t k = 0;
+                for (uint32_t t = 0; t < c->cap_tiles; ++t)
+                    for (uint32_t i = st[t]; i < en[t]; ++i) ids[k++] = all[i];
+            } else {
+                SS_CUDA(cudaMemcpy(ids.data(), c->lanes[0].list.p, c->cap_instances * 4, cudaMemcpyDeviceToHost));
+            }
             std::vector<uint32_t> rank_of(c->n, 0xffffffffu);
             for (uint64_t r = 0; r < order.size(); ++r) rank_of[order[r]] = (uint32_t)r;
             for (uint64_t i = 0; i < ids.size(); ++i) tile_splats[i] = rank_of[ids[i]];

@@ -177,6 +177,7 @@ __global__ void __launch_bounds__(128) project_kernel(ProjectParams p) {
             }
         }
         p.keys[id] = key;
+        if (!survive) p.boxes[id] = make_uint2(0xffffffffu, 0xffffffffu); // no tile instances
     }
     // block-reduce survivors' count and key range, one atomic per block
     const unsigned long long kmin = survive ? key : ~0ull;

@@ -35,7 +35,10 @@ struct ViewInfo {
     unsigned int err_count;          // singular screen covariances
     unsigned int err_gid;            // smallest gid with one
     unsigned long long n_touched;    // G_v (Gaussians with any masked weight)
-    unsigned int overflow;           // tile-list capacity exceeded: view skipped
+    unsigned int overflow;           // tile lists unusable: compositor skips, the host re-runs the view
+    unsigned int bin_fallback;       // tile-sort binning: 1 = a tile outgrew its slot capacity (grow it),
+                                     // 2 = beyond the in-CTA sort (re-run with the global depth sort)
+    unsigned int max_fill;           // tile-sort binning: largest tile list
     unsigned int pad;
 };
 
@@ -48,6 +51,7 @@ struct ProjectParams {
     ss_camera cam;
     SplatRec* rec;        // [n] by gid
     uint2* boxes;         // [n] by gid: (x0 | x1 << 16, y0 | y1 << 16), L2-resident copy of the records' boxes
+                          // (0xffffffff, 0xffffffff) for Gaussians that do not survive
     unsigned long long* keys; // [n] depth bits (~0 when culled)
     uint32_t* tile_count; // [tiles] instances per tile (atomic), or null
     uint32_t tiles_x;

@@ -540,6 +540,208 @@ __global__ void __launch_bounds__(WARPS * 32) bin_scatter_kernel(BinParams p) {
     }
 }
 
+// ------------------------------------------------- tile-sort binning
+// rasterizer.hpp:181-194 (tile_bins) without a global depth sort.
+//  1. ts_scatter: CTA per chunk of kTsChunk Gaussians (id order).  A shared
+//     histogram counts the chunk's instances per tile; one atomicAdd per
+//     (chunk, tile) on fill[t] reserves the chunk's slots in tile t's
+//     fixed-capacity range; the instances are then written there, unordered,
+//     as (narrowed depth key, gid).  A tile outgrowing its capacity flags
+//     bin_fallback = 1 (the host grows the capacity and re-runs the view).
+//  2. tile_sort: CTA per tile.  The narrowed keys (monotone in the f64 depth
+//     bits) of the tile's instances are bucketed into B >= 2n buckets over the
+//     tile's own key range (shared-memory counting sort: histogram, scan,
+//     scatter); buckets holding several instances are put in exact (depth
+//     bits, id) order -- the reference's depth_sort comparator,
+//     projection.hpp:59-64 -- by insertion on the full keys.  The tile's list
+//     is then exactly its slice of the reference's tile_bins.  A tile beyond
+//     kTileSortMax instances or a bucket beyond kTsBucketMax (massive exact
+//     depth ties) flags bin_fallback = 2: the host re-runs the view on the
+//     global depth sort, whose tie fix-up handles any run length.
+constexpr uint32_t kTsChunk = 8192;   // Gaussians per scatter CTA
+constexpr uint32_t kTsBucketMax = 64; // instances per bucket the fix-up orders
+constexpr uint32_t kTsMaxTiles = 16384; // shared histogram of the scatter (64 KB)
+
+__global__ void __launch_bounds__(256) ts_scatter_kernel(TileSortParams p) {
+    extern __shared__ uint32_t hist[]; // [tiles]: counts, then cursors
+    const uint64_t base = (uint64_t)blockIdx.x * kTsChunk;
+    if (base >= p.n) return;
+    for (uint32_t t = threadIdx.x; t < p.tiles; t += blockDim.x) hist[t] = 0u;
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    constexpr uint32_t groups = kTsChunk / 256u;
+    const uint64_t r0 = base + (uint64_t)warp * groups * 32u + lane;
+    auto load_box = [&](uint32_t g) {
+        return r0 + g * 32u < p.n ? __ldg(p.boxes + r0 + g * 32u) : make_uint2(kCulledBox, kCulledBox);
+    };
+    uint2 next = load_box(0);
+    for (uint32_t g = 0; g < groups; ++g) {
+        const uint2 box = next;
+        if (g + 1 < groups) next = load_box(g + 1);
+        for_each_instance(box, lane, p.tiles_x, [&](bool valid, uint32_t t, uint32_t) {
+            if (valid) atomicAdd(hist + t, 1u);
+        });
+    }
+    __syncthreads();
+    // reserve each touched tile's slots: one global atomic per (chunk, tile)
+    uint32_t mine = 0, mfill = 0;
+    for (uint32_t t = threadIdx.x; t < p.tiles; t += blockDim.x) {
+        const uint32_t c = hist[t];
+        if (!c) continue;
+        mine += c;
+        const uint32_t b = atomicAdd(p.fill + t, c);
+        mfill = max(mfill, b + c);
+        hist[t] = b + c <= p.cap ? t * p.cap + b : 0xffffffffu;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mine += __shfl_xor_sync(0xffffffffu, mine, o);
+        mfill = max(mfill, __shfl_xor_sync(0xffffffffu, mfill, o));
+    }
+    if (lane == 0) {
+        if (mine) atomicAdd(&p.info->n_instances, (unsigned long long)mine);
+        if (mfill > p.cap) {
+            atomicMax(&p.info->max_fill, mfill);
+            atomicMax(&p.info->bin_fallback, 1u);
+            p.info->overflow = 1u;
+        }
+    }
+    __syncthreads();
+    const unsigned long long mn = p.info->min_key;
+    const uint32_t sh = narrow_shift(p.info);
+    auto load_id = [&](uint32_t g) { return r0 + g * 32u; };
+    next = load_box(0);
+    for (uint32_t g = 0; g < groups; ++g) {
+        const uint2 box = next;
+        if (g + 1 < groups) next = load_box(g + 1);
+        const uint64_t id = load_id(g);
+        const uint32_t k32 =
+            box.x != kCulledBox ? (uint32_t)((__ldg(p.keys + id) - mn) >> sh) : 0u; // monotone in the depth bits
+        for_each_instance(box, lane, p.tiles_x, [&](bool valid, uint32_t t, uint32_t o) {
+            const uint32_t ok = __shfl_sync(0xffffffffu, k32, o);
+            const uint32_t og = __shfl_sync(0xffffffffu, (uint32_t)id, o);
+            if (valid) {
+                const uint32_t cur = hist[t];
+                if (cur != 0xffffffffu) p.slab[atomicAdd(hist + t, 1u)] = make_uint2(ok, og);
+            }
+        });
+    }
+}
+
+__global__ void __launch_bounds__(256) tile_sort_kernel(TileSortParams p) {
+    extern __shared__ uint32_t sm[]; // cnt[kTileSortMax] then out[kTileSortMax]
+    uint32_t* cnt = sm;
+    uint32_t* out = sm + kTileSortMax;
+    __shared__ uint32_t red_min[8], red_max[8];
+    __shared__ uint32_t s_fail;
+    const uint32_t t = blockIdx.x;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    if (p.info->overflow) return; // the view is re-run
+    const uint32_t n = p.fill[t];
+    const size_t base = (size_t)t * p.cap;
+    if (tid == 0) {
+        p.start[t] = (uint32_t)base;
+        p.end[t] = (uint32_t)base + n;
+        s_fail = 0u;
+    }
+    if (n == 0) return;
+    if (n > kTileSortMax) {
+        if (tid == 0) {
+            atomicMax(&p.info->bin_fallback, 2u);
+            p.info->overflow = 1u;
+        }
+        return;
+    }
+    const uint2* src = p.slab + base;
+    // the tile's narrowed key range
+    uint32_t mn = 0xffffffffu, mx = 0u;
+    for (uint32_t i = tid; i < n; i += 256u) {
+        const uint32_t k = src[i].x;
+        mn = min(mn, k);
+        mx = max(mx, k);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (lane == 0) {
+        red_min[warp] = mn;
+        red_max[warp] = mx;
+    }
+    __syncthreads();
+    mn = red_min[0];
+    mx = red_max[0];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) {
+        mn = min(mn, red_min[w]);
+        mx = max(mx, red_max[w]);
+    }
+    // B = 2^lb >= 2n buckets (32 .. kTileSortMax) over [mn, mx]
+    uint32_t lb = 5;
+    while ((1u << lb) < 2u * n && (1u << lb) < kTileSortMax) ++lb;
+    const uint32_t B = 1u << lb;
+    const uint32_t span = mx - mn;
+    const uint32_t hb = span ? 32u - (uint32_t)__clz(span) : 0u;
+    const uint32_t sh = hb > lb ? hb - lb : 0u;
+    for (uint32_t b = tid; b < B; b += 256u) cnt[b] = 0u;
+    __syncthreads();
+    for (uint32_t i = tid; i < n; i += 256u) atomicAdd(cnt + ((src[i].x - mn) >> sh), 1u);
+    __syncthreads();
+    { // exclusive scan of cnt[0, B): per-thread runs of B/256, then a block scan of the run totals
+        using Scan = cub::BlockScan<uint32_t, 256>;
+        __shared__ typename Scan::TempStorage scan_tmp;
+        const uint32_t per = (B + 255u) / 256u, b0 = tid * per, b1 = min(B, b0 + per);
+        uint32_t run = 0;
+        for (uint32_t b = b0; b < b1; ++b) run += cnt[b];
+        uint32_t before = 0;
+        Scan(scan_tmp).ExclusiveSum(run, before);
+        for (uint32_t b = b0; b < b1; ++b) {
+            const uint32_t c = cnt[b];
+            cnt[b] = before;
+            before += c;
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = tid; i < n; i += 256u) {
+        const uint2 v = src[i];
+        out[atomicAdd(cnt + ((v.x - mn) >> sh), 1u)] = v.y;
+    }
+    __syncthreads();
+    // cnt[b] is now the end of bucket b (= the start of bucket b + 1)
+    for (uint32_t b = tid; b < B; b += 256u) {
+        const uint32_t s0 = b ? cnt[b - 1] : 0u, e0 = cnt[b];
+        if (e0 - s0 < 2u) continue;
+        if (e0 - s0 > kTsBucketMax) {
+            s_fail = 1u;
+            continue;
+        }
+        for (uint32_t a = s0 + 1; a < e0; ++a) { // insertion by (depth bits, id)
+            const uint32_t id = out[a];
+            const unsigned long long key = __ldg(p.keys + id);
+            uint32_t c = a;
+            while (c > s0) {
+                const uint32_t pid = out[c - 1];
+                if (!depth_before(key, id, __ldg(p.keys + pid), pid)) break;
+                out[c] = pid;
+                --c;
+            }
+            out[c] = id;
+        }
+    }
+    __syncthreads();
+    if (s_fail) {
+        if (tid == 0) {
+            atomicMax(&p.info->bin_fallback, 2u);
+            p.info->overflow = 1u;
+        }
+        return;
+    }
+    uint32_t* dst = p.list + base;
+    for (uint32_t i = tid; i < n; i += 256u) dst[i] = out[i];
+    if (tid == 0) atomicMax(&p.info->max_fill, n);
+}
+
 // --------------------------------------------------------- contraction
 // pipeline.hpp:70-80 accumulate for a group of up to four consecutive views:
 // for every Gaussian touched in any of them, row[gid] += sum_m acc_v[gid, m] *
@@ -1253,6 +1455,32 @@ cudaError_t launch_emit_instances(const uint2* rbox, const uint32_t* order, uint
                                                                             static_cast<uint32_t*>(keys), vals, info);
         pad_keys_kernel<uint32_t><<<g, 256, 0, s>>>(offsets, n, cap, static_cast<uint32_t*>(keys));
     }
+    return cudaGetLastError();
+}
+
+uint32_t tile_sort_max_tiles() { return kTsMaxTiles; }
+
+cudaError_t launch_tile_sort_bin(const TileSortParams& p, cudaStream_t s) {
+    if (p.tiles > kTsMaxTiles) return cudaErrorInvalidValue;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    static std::atomic<int> configured[64] = {};
+    if (dev >= 0 && dev < 64 && !configured[dev].load()) {
+        cudaError_t e = cudaFuncSetAttribute(ts_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)(kTsMaxTiles * 4));
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(tile_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(2 * kTileSortMax * 4));
+        if (e != cudaSuccess) return e;
+        configured[dev].store(1);
+    }
+    cudaError_t e = cudaMemsetAsync(p.fill, 0, (size_t)p.tiles * 4, s);
+    if (e != cudaSuccess) return e;
+    if (p.n) {
+        const unsigned chunks = (unsigned)((p.n + kTsChunk - 1) / kTsChunk);
+        ts_scatter_kernel<<<chunks, 256, (size_t)p.tiles * 4, s>>>(p);
+    }
+    tile_sort_kernel<<<p.tiles, 256, 2 * kTileSortMax * 4, s>>>(p);
     return cudaGetLastError();
 }
 

@@ -66,6 +66,29 @@ struct BinParams {
     uint64_t cap;
     ViewInfo* info;
 };
+// Tile-sort binning (ss_kernels.cu): each Gaussian's tile instances are
+// scattered, unordered, into fixed-capacity per-tile slots (chunk histograms in
+// shared memory reserve each tile's range with one global atomic per chunk),
+// then one CTA per tile orders its slots by (depth, id) with a shared-memory
+// bucket sort on the narrowed key plus an exact fix-up of shared buckets.  No
+// global depth sort is needed for the fused pass.
+struct TileSortParams {
+    const uint2* boxes;              // by gid (projection; culled: all ones)
+    const unsigned long long* keys;  // by gid: depth bits (~0 culled)
+    uint64_t n;                      // Gaussians
+    uint32_t tiles, tiles_x;
+    uint32_t cap;                    // slots per tile
+    uint32_t* fill;                  // [tiles], zero before the scatter
+    uint2* slab;                     // [tiles * cap] (narrowed key, gid), unordered
+    uint32_t* list;                  // [tiles * cap] gids in (depth, id) order
+    uint32_t* start;                 // [tiles] list ranges
+    uint32_t* end;
+    ViewInfo* info;
+};
+constexpr uint32_t kTileSortMax = 8192; // instances one CTA orders in shared memory
+uint32_t tile_sort_max_tiles();         // views with more tiles use the other paths
+cudaError_t launch_tile_sort_bin(const TileSortParams& p, cudaStream_t s);
+
 // warps per scatter CTA for a tile count (0: too many tiles, use the sort path)
 uint32_t bin_scatter_warps(uint32_t tiles);
 size_t bin_counts_entries(uint64_t n, uint32_t tiles);

@@ -153,10 +153,13 @@ def test_direct_binning_equals_sort(gpu_ctx, oracle, seed, n, w, h, dist, scale)
         by_sort = _capture(gpu_ctx, s, cam)
         gpu_ctx.set_bin_path(2)
         direct = _capture(gpu_ctx, s, cam)
+        gpu_ctx.set_bin_path(3)
+        tile_sorted = _capture(gpu_ctx, s, cam)
     finally:
         gpu_ctx.set_bin_path(0)
     assert direct["tile_offsets"][-1] > 0
     _assert_capture_equal(direct, by_sort)
+    _assert_capture_equal(tile_sorted, by_sort)
     if n <= 10000:
         _assert_capture_equal(direct, oracle.rasterize(s, cam))
 
