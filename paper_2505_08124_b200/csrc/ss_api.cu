@@ -147,7 +147,7 @@ struct Lane {
     DevBuf rec, boxes, rbox, rcnt, keys, k32, k32s, order, iota, offsets, tkeys, tkeys_sorted, tvals, tile_start, tile_end, list;
     DevBuf bin_counts, bin_slice, bin_tot, bin_done; // direct binning scratch
     DevBuf ts_fill, ts_slab;       // tile-sort binning: per-tile fill counters, unordered (key, gid) slots
-    uint32_t ts_cap = 4096;        // tile-sort slots per tile (grown to the largest tile seen)
+    uint32_t ts_cap = kTileSortMax; // tile-sort slots per tile (larger tiles take the global path)
     uint64_t iota_n = 0;           // entries of the 0..n-1 sequence in `iota`
     uint64_t list_cap = 0;         // entries of `list`
     DevBuf cub_tmp, info;

@@ -562,26 +562,33 @@ constexpr uint32_t kTsChunk = 8192;   // Gaussians per scatter CTA
 constexpr uint32_t kTsBucketMax = 64; // instances per bucket the fix-up orders
 constexpr uint32_t kTsMaxTiles = 16384; // shared histogram of the scatter (64 KB)
 
-__global__ void __launch_bounds__(256) ts_scatter_kernel(TileSortParams p) {
+constexpr uint32_t kTsThreads = 1024;  // scatter CTA: 32 warps, each 8 groups of 32 Gaussians
+
+__global__ void __launch_bounds__(kTsThreads) ts_scatter_kernel(TileSortParams p) {
     extern __shared__ uint32_t hist[]; // [tiles]: counts, then cursors
     const uint64_t base = (uint64_t)blockIdx.x * kTsChunk;
     if (base >= p.n) return;
     for (uint32_t t = threadIdx.x; t < p.tiles; t += blockDim.x) hist[t] = 0u;
     __syncthreads();
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    constexpr uint32_t groups = kTsChunk / 256u;
+    constexpr uint32_t groups = kTsChunk / kTsThreads;
     const uint64_t r0 = base + (uint64_t)warp * groups * 32u + lane;
-    auto load_box = [&](uint32_t g) {
-        return r0 + g * 32u < p.n ? __ldg(p.boxes + r0 + g * 32u) : make_uint2(kCulledBox, kCulledBox);
-    };
-    uint2 next = load_box(0);
-    for (uint32_t g = 0; g < groups; ++g) {
-        const uint2 box = next;
-        if (g + 1 < groups) next = load_box(g + 1);
-        for_each_instance(box, lane, p.tiles_x, [&](bool valid, uint32_t t, uint32_t) {
+    uint2 box[groups];
+#pragma unroll
+    for (uint32_t g = 0; g < groups; ++g) // all of the warp's boxes in flight at once
+        box[g] = r0 + g * 32u < p.n ? __ldg(p.boxes + r0 + g * 32u) : make_uint2(kCulledBox, kCulledBox);
+#pragma unroll
+    for (uint32_t g = 0; g < groups; ++g)
+        for_each_instance(box[g], lane, p.tiles_x, [&](bool valid, uint32_t t, uint32_t) {
             if (valid) atomicAdd(hist + t, 1u);
         });
-    }
+    // the narrowed depth keys for the scatter, loaded while the histogram settles
+    const unsigned long long mn = p.info->min_key;
+    const uint32_t sh = narrow_shift(p.info);
+    uint32_t k32[groups];
+#pragma unroll
+    for (uint32_t g = 0; g < groups; ++g)
+        k32[g] = box[g].x != kCulledBox ? (uint32_t)((__ldg(p.keys + r0 + g * 32u) - mn) >> sh) : 0u;
     __syncthreads();
     // reserve each touched tile's slots: one global atomic per (chunk, tile)
     uint32_t mine = 0, mfill = 0;
@@ -607,32 +614,25 @@ __global__ void __launch_bounds__(256) ts_scatter_kernel(TileSortParams p) {
         }
     }
     __syncthreads();
-    const unsigned long long mn = p.info->min_key;
-    const uint32_t sh = narrow_shift(p.info);
-    auto load_id = [&](uint32_t g) { return r0 + g * 32u; };
-    next = load_box(0);
+#pragma unroll
     for (uint32_t g = 0; g < groups; ++g) {
-        const uint2 box = next;
-        if (g + 1 < groups) next = load_box(g + 1);
-        const uint64_t id = load_id(g);
-        const uint32_t k32 =
-            box.x != kCulledBox ? (uint32_t)((__ldg(p.keys + id) - mn) >> sh) : 0u; // monotone in the depth bits
-        for_each_instance(box, lane, p.tiles_x, [&](bool valid, uint32_t t, uint32_t o) {
-            const uint32_t ok = __shfl_sync(0xffffffffu, k32, o);
-            const uint32_t og = __shfl_sync(0xffffffffu, (uint32_t)id, o);
-            if (valid) {
-                const uint32_t cur = hist[t];
-                if (cur != 0xffffffffu) p.slab[atomicAdd(hist + t, 1u)] = make_uint2(ok, og);
-            }
+        const uint32_t id = (uint32_t)(r0 + g * 32u);
+        for_each_instance(box[g], lane, p.tiles_x, [&](bool valid, uint32_t t, uint32_t o) {
+            const uint32_t ok = __shfl_sync(0xffffffffu, k32[g], o);
+            const uint32_t og = __shfl_sync(0xffffffffu, id, o);
+            if (valid && hist[t] != 0xffffffffu) p.slab[atomicAdd(hist + t, 1u)] = make_uint2(ok, og);
         });
     }
 }
 
-__global__ void __launch_bounds__(256) tile_sort_kernel(TileSortParams p) {
-    extern __shared__ uint32_t sm[]; // cnt[kTileSortMax] then out[kTileSortMax]
+constexpr uint32_t kTsSortThreads = 512;
+constexpr uint32_t kTsPer = kTileSortMax / kTsSortThreads; // slots per thread
+
+__global__ void __launch_bounds__(kTsSortThreads) tile_sort_kernel(TileSortParams p) {
+    extern __shared__ uint32_t sm[]; // cnt[kTileSortMax], then out[kTileSortMax] as (key, gid)
     uint32_t* cnt = sm;
-    uint32_t* out = sm + kTileSortMax;
-    __shared__ uint32_t red_min[8], red_max[8];
+    uint2* out = reinterpret_cast<uint2*>(sm + kTileSortMax);
+    __shared__ uint32_t red_min[kTsSortThreads / 32], red_max[kTsSortThreads / 32];
     __shared__ uint32_t s_fail;
     const uint32_t t = blockIdx.x;
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
@@ -652,13 +652,18 @@ __global__ void __launch_bounds__(256) tile_sort_kernel(TileSortParams p) {
         }
         return;
     }
+    // the tile's (key, gid) slots, strided over the threads, held in registers
     const uint2* src = p.slab + base;
-    // the tile's narrowed key range
+    uint2 v[kTsPer];
     uint32_t mn = 0xffffffffu, mx = 0u;
-    for (uint32_t i = tid; i < n; i += 256u) {
-        const uint32_t k = src[i].x;
-        mn = min(mn, k);
-        mx = max(mx, k);
+#pragma unroll
+    for (uint32_t k = 0; k < kTsPer; ++k) {
+        const uint32_t i = tid + k * kTsSortThreads;
+        v[k] = i < n ? src[i] : make_uint2(0u, 0u);
+        if (i < n) {
+            mn = min(mn, v[k].x);
+            mx = max(mx, v[k].x);
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -669,29 +674,30 @@ __global__ void __launch_bounds__(256) tile_sort_kernel(TileSortParams p) {
         red_min[warp] = mn;
         red_max[warp] = mx;
     }
+    // B = 2^lb >= n buckets (32 .. kTileSortMax) over [mn, mx]
+    uint32_t lb = 5;
+    while ((1u << lb) < n) ++lb;
+    const uint32_t B = 1u << lb;
+    for (uint32_t b = tid; b < B; b += kTsSortThreads) cnt[b] = 0u;
     __syncthreads();
     mn = red_min[0];
     mx = red_max[0];
 #pragma unroll
-    for (int w = 1; w < 8; ++w) {
+    for (int w = 1; w < (int)(kTsSortThreads / 32); ++w) {
         mn = min(mn, red_min[w]);
         mx = max(mx, red_max[w]);
     }
-    // B = 2^lb >= 2n buckets (32 .. kTileSortMax) over [mn, mx]
-    uint32_t lb = 5;
-    while ((1u << lb) < 2u * n && (1u << lb) < kTileSortMax) ++lb;
-    const uint32_t B = 1u << lb;
     const uint32_t span = mx - mn;
     const uint32_t hb = span ? 32u - (uint32_t)__clz(span) : 0u;
     const uint32_t sh = hb > lb ? hb - lb : 0u;
-    for (uint32_t b = tid; b < B; b += 256u) cnt[b] = 0u;
+#pragma unroll
+    for (uint32_t k = 0; k < kTsPer; ++k)
+        if (tid + k * kTsSortThreads < n) atomicAdd(cnt + ((v[k].x - mn) >> sh), 1u);
     __syncthreads();
-    for (uint32_t i = tid; i < n; i += 256u) atomicAdd(cnt + ((src[i].x - mn) >> sh), 1u);
-    __syncthreads();
-    { // exclusive scan of cnt[0, B): per-thread runs of B/256, then a block scan of the run totals
-        using Scan = cub::BlockScan<uint32_t, 256>;
+    { // exclusive scan of cnt[0, B): per-thread runs, then a block scan of the run totals
+        using Scan = cub::BlockScan<uint32_t, kTsSortThreads>;
         __shared__ typename Scan::TempStorage scan_tmp;
-        const uint32_t per = (B + 255u) / 256u, b0 = tid * per, b1 = min(B, b0 + per);
+        const uint32_t per = (B + kTsSortThreads - 1u) / kTsSortThreads, b0 = tid * per, b1 = min(B, b0 + per);
         uint32_t run = 0;
         for (uint32_t b = b0; b < b1; ++b) run += cnt[b];
         uint32_t before = 0;
@@ -703,30 +709,32 @@ __global__ void __launch_bounds__(256) tile_sort_kernel(TileSortParams p) {
         }
     }
     __syncthreads();
-    for (uint32_t i = tid; i < n; i += 256u) {
-        const uint2 v = src[i];
-        out[atomicAdd(cnt + ((v.x - mn) >> sh), 1u)] = v.y;
-    }
+#pragma unroll
+    for (uint32_t k = 0; k < kTsPer; ++k)
+        if (tid + k * kTsSortThreads < n) out[atomicAdd(cnt + ((v[k].x - mn) >> sh), 1u)] = v[k];
     __syncthreads();
-    // cnt[b] is now the end of bucket b (= the start of bucket b + 1)
-    for (uint32_t b = tid; b < B; b += 256u) {
+    // cnt[b] is now the end of bucket b (= the start of bucket b + 1); order
+    // each shared bucket by (key, then depth bits and id on equal keys)
+    for (uint32_t b = tid; b < B; b += kTsSortThreads) {
         const uint32_t s0 = b ? cnt[b - 1] : 0u, e0 = cnt[b];
         if (e0 - s0 < 2u) continue;
         if (e0 - s0 > kTsBucketMax) {
             s_fail = 1u;
             continue;
         }
-        for (uint32_t a = s0 + 1; a < e0; ++a) { // insertion by (depth bits, id)
-            const uint32_t id = out[a];
-            const unsigned long long key = __ldg(p.keys + id);
+        for (uint32_t a = s0 + 1; a < e0; ++a) {
+            const uint2 x = out[a];
             uint32_t c = a;
             while (c > s0) {
-                const uint32_t pid = out[c - 1];
-                if (!depth_before(key, id, __ldg(p.keys + pid), pid)) break;
-                out[c] = pid;
+                const uint2 y = out[c - 1];
+                bool before = x.x < y.x;
+                if (x.x == y.x) // equal narrowed keys: the full depth bits, then the id
+                    before = depth_before(__ldg(p.keys + x.y), x.y, __ldg(p.keys + y.y), y.y);
+                if (!before) break;
+                out[c] = y;
                 --c;
             }
-            out[c] = id;
+            out[c] = x;
         }
     }
     __syncthreads();
@@ -738,8 +746,7 @@ __global__ void __launch_bounds__(256) tile_sort_kernel(TileSortParams p) {
         return;
     }
     uint32_t* dst = p.list + base;
-    for (uint32_t i = tid; i < n; i += 256u) dst[i] = out[i];
-    if (tid == 0) atomicMax(&p.info->max_fill, n);
+    for (uint32_t i = tid; i < n; i += kTsSortThreads) dst[i] = out[i].y;
 }
 
 // --------------------------------------------------------- contraction
@@ -1470,7 +1477,7 @@ cudaError_t launch_tile_sort_bin(const TileSortParams& p, cudaStream_t s) {
                                              (int)(kTsMaxTiles * 4));
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(tile_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(2 * kTileSortMax * 4));
+                                     (int)(3 * kTileSortMax * 4));
         if (e != cudaSuccess) return e;
         configured[dev].store(1);
     }
@@ -1478,9 +1485,9 @@ cudaError_t launch_tile_sort_bin(const TileSortParams& p, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     if (p.n) {
         const unsigned chunks = (unsigned)((p.n + kTsChunk - 1) / kTsChunk);
-        ts_scatter_kernel<<<chunks, 256, (size_t)p.tiles * 4, s>>>(p);
+        ts_scatter_kernel<<<chunks, kTsThreads, (size_t)p.tiles * 4, s>>>(p);
     }
-    tile_sort_kernel<<<p.tiles, 256, 2 * kTileSortMax * 4, s>>>(p);
+    tile_sort_kernel<<<p.tiles, kTsSortThreads, 3 * kTileSortMax * 4, s>>>(p);
     return cudaGetLastError();
 }
 
