@@ -564,31 +564,42 @@ constexpr uint32_t kTsMaxTiles = 16384; // shared histogram of the scatter (64 K
 
 constexpr uint32_t kTsThreads = 1024;  // scatter CTA: 32 warps, each 8 groups of 32 Gaussians
 
+// f(tile) for every tile of a box, row-major (per lane; lanes diverge on box size)
+template <typename F>
+__device__ __forceinline__ void for_box_tiles(uint2 box, uint32_t tiles_x, F&& f) {
+    if (box.x == kCulledBox) return;
+    const uint32_t tx0 = (box.x & 0xffffu) / kTile, tx1 = (box.x >> 16) / kTile;
+    const uint32_t ty0 = (box.y & 0xffffu) / kTile, ty1 = (box.y >> 16) / kTile;
+    for (uint32_t ty = ty0; ty <= ty1; ++ty)
+        for (uint32_t tx = tx0; tx <= tx1; ++tx) f(ty * tiles_x + tx);
+}
+
 __global__ void __launch_bounds__(kTsThreads) ts_scatter_kernel(TileSortParams p) {
     extern __shared__ uint32_t hist[]; // [tiles]: counts, then cursors
     const uint64_t base = (uint64_t)blockIdx.x * kTsChunk;
     if (base >= p.n) return;
     for (uint32_t t = threadIdx.x; t < p.tiles; t += blockDim.x) hist[t] = 0u;
-    __syncthreads();
-    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint32_t lane = threadIdx.x & 31u;
     constexpr uint32_t groups = kTsChunk / kTsThreads;
-    const uint64_t r0 = base + (uint64_t)warp * groups * 32u + lane;
+    // thread i takes Gaussians base + i + g * kTsThreads (coalesced)
     uint2 box[groups];
 #pragma unroll
-    for (uint32_t g = 0; g < groups; ++g) // all of the warp's boxes in flight at once
-        box[g] = r0 + g * 32u < p.n ? __ldg(p.boxes + r0 + g * 32u) : make_uint2(kCulledBox, kCulledBox);
+    for (uint32_t g = 0; g < groups; ++g) {
+        const uint64_t id = base + threadIdx.x + (uint64_t)g * kTsThreads;
+        box[g] = id < p.n ? __ldg(p.boxes + id) : make_uint2(kCulledBox, kCulledBox);
+    }
+    __syncthreads();
 #pragma unroll
-    for (uint32_t g = 0; g < groups; ++g)
-        for_each_instance(box[g], lane, p.tiles_x, [&](bool valid, uint32_t t, uint32_t) {
-            if (valid) atomicAdd(hist + t, 1u);
-        });
+    for (uint32_t g = 0; g < groups; ++g) for_box_tiles(box[g], p.tiles_x, [&](uint32_t t) { atomicAdd(hist + t, 1u); });
     // the narrowed depth keys for the scatter, loaded while the histogram settles
     const unsigned long long mn = p.info->min_key;
     const uint32_t sh = narrow_shift(p.info);
     uint32_t k32[groups];
 #pragma unroll
-    for (uint32_t g = 0; g < groups; ++g)
-        k32[g] = box[g].x != kCulledBox ? (uint32_t)((__ldg(p.keys + r0 + g * 32u) - mn) >> sh) : 0u;
+    for (uint32_t g = 0; g < groups; ++g) {
+        const uint64_t id = base + threadIdx.x + (uint64_t)g * kTsThreads;
+        k32[g] = box[g].x != kCulledBox ? (uint32_t)((__ldg(p.keys + id) - mn) >> sh) : 0u; // monotone in depth
+    }
     __syncthreads();
     // reserve each touched tile's slots: one global atomic per (chunk, tile)
     uint32_t mine = 0, mfill = 0;
@@ -616,11 +627,10 @@ __global__ void __launch_bounds__(kTsThreads) ts_scatter_kernel(TileSortParams p
     __syncthreads();
 #pragma unroll
     for (uint32_t g = 0; g < groups; ++g) {
-        const uint32_t id = (uint32_t)(r0 + g * 32u);
-        for_each_instance(box[g], lane, p.tiles_x, [&](bool valid, uint32_t t, uint32_t o) {
-            const uint32_t ok = __shfl_sync(0xffffffffu, k32[g], o);
-            const uint32_t og = __shfl_sync(0xffffffffu, id, o);
-            if (valid && hist[t] != 0xffffffffu) p.slab[atomicAdd(hist + t, 1u)] = make_uint2(ok, og);
+        const uint32_t id = (uint32_t)(base + threadIdx.x + (uint64_t)g * kTsThreads);
+        const uint2 v = make_uint2(k32[g], id);
+        for_box_tiles(box[g], p.tiles_x, [&](uint32_t t) {
+            if (hist[t] != 0xffffffffu) p.slab[atomicAdd(hist + t, 1u)] = v;
         });
     }
 }
@@ -694,19 +704,30 @@ __global__ void __launch_bounds__(kTsSortThreads) tile_sort_kernel(TileSortParam
     for (uint32_t k = 0; k < kTsPer; ++k)
         if (tid + k * kTsSortThreads < n) atomicAdd(cnt + ((v[k].x - mn) >> sh), 1u);
     __syncthreads();
-    { // exclusive scan of cnt[0, B): per-thread runs, then a block scan of the run totals
-        using Scan = cub::BlockScan<uint32_t, kTsSortThreads>;
-        __shared__ typename Scan::TempStorage scan_tmp;
-        const uint32_t per = (B + kTsSortThreads - 1u) / kTsSortThreads, b0 = tid * per, b1 = min(B, b0 + per);
-        uint32_t run = 0;
-        for (uint32_t b = b0; b < b1; ++b) run += cnt[b];
-        uint32_t before = 0;
-        Scan(scan_tmp).ExclusiveSum(run, before);
-        for (uint32_t b = b0; b < b1; ++b) {
-            const uint32_t c = cnt[b];
-            cnt[b] = before;
-            before += c;
+    { // exclusive scan of cnt[0, B): warp w scans its contiguous segment 32
+      // counters per round (conflict-free), then the warp totals are scanned
+        __shared__ uint32_t wtot[kTsSortThreads / 32];
+        constexpr uint32_t W = kTsSortThreads / 32;
+        const uint32_t seg = B / W, s0 = warp * seg; // B >= 32 * W or seg < 32 (then lanes past seg idle)
+        uint32_t carry = 0;
+        for (uint32_t b = s0; b < s0 + seg; b += 32u) {
+            const uint32_t i = b + lane;
+            const uint32_t c = i < s0 + seg ? cnt[i] : 0u;
+            uint32_t incl = c;
+#pragma unroll
+            for (uint32_t d = 1; d < 32; d <<= 1) {
+                const uint32_t u = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += u;
+            }
+            if (i < s0 + seg) cnt[i] = carry + incl - c;
+            carry += __shfl_sync(0xffffffffu, incl, 31);
         }
+        if (lane == 0) wtot[warp] = carry;
+        __syncthreads();
+        uint32_t before = 0;
+        for (uint32_t w = 0; w < warp; ++w) before += wtot[w];
+        if (before)
+            for (uint32_t i = s0 + lane; i < s0 + seg; i += 32u) cnt[i] += before;
     }
     __syncthreads();
 #pragma unroll
