@@ -666,8 +666,10 @@ __global__ void __launch_bounds__(kTsSortThreads) tile_sort_kernel(TileSortParam
     const uint2* src = p.slab + base;
     uint2 v[kTsPer];
     uint32_t mn = 0xffffffffu, mx = 0u;
+    const uint32_t per = (n + kTsSortThreads - 1u) / kTsSortThreads; // slots per thread this tile
 #pragma unroll
     for (uint32_t k = 0; k < kTsPer; ++k) {
+        if (k >= per) break;
         const uint32_t i = tid + k * kTsSortThreads;
         v[k] = i < n ? src[i] : make_uint2(0u, 0u);
         if (i < n) {
@@ -701,8 +703,10 @@ __global__ void __launch_bounds__(kTsSortThreads) tile_sort_kernel(TileSortParam
     const uint32_t hb = span ? 32u - (uint32_t)__clz(span) : 0u;
     const uint32_t sh = hb > lb ? hb - lb : 0u;
 #pragma unroll
-    for (uint32_t k = 0; k < kTsPer; ++k)
+    for (uint32_t k = 0; k < kTsPer; ++k) {
+        if (k >= per) break;
         if (tid + k * kTsSortThreads < n) atomicAdd(cnt + ((v[k].x - mn) >> sh), 1u);
+    }
     __syncthreads();
     { // exclusive scan of cnt[0, B): warp w scans its contiguous segment 32
       // counters per round (conflict-free), then the warp totals are scanned
@@ -731,8 +735,10 @@ __global__ void __launch_bounds__(kTsSortThreads) tile_sort_kernel(TileSortParam
     }
     __syncthreads();
 #pragma unroll
-    for (uint32_t k = 0; k < kTsPer; ++k)
+    for (uint32_t k = 0; k < kTsPer; ++k) {
+        if (k >= per) break;
         if (tid + k * kTsSortThreads < n) out[atomicAdd(cnt + ((v[k].x - mn) >> sh), 1u)] = v[k];
+    }
     __syncthreads();
     // cnt[b] is now the end of bucket b (= the start of bucket b + 1); order
     // each shared bucket by (key, then depth bits and id on equal keys)
