@@ -76,6 +76,8 @@ def parse():
     ap.add_argument("--group", type=int, default=0, help="views per contraction group (0 = library default)")
     ap.add_argument("--bin", type=int, default=0, help="tile binning: 0 auto, 1 key sort, 2 direct")
     ap.add_argument("--raster", type=int, default=0, help="compositor: 0 staged evaluation, 1 per-step")
+    ap.add_argument("--combine-rows", type=int, default=0,
+                    help="rows per block of the block-cyclic combine (0 = contiguous shards)")
     ap.add_argument("--cpu-sample-queries", type=int, default=32)
     return ap.parse_args()
 
@@ -340,11 +342,27 @@ def run_reference_arm(args, rank, world):
 
 
 # ---------------------------------------------------------------- B200 arm
+def relaunch_under_torchrun(n: int) -> None:
+    """`bench.py --gpus N` (N > 1) outside a launcher: re-exec as N ranks, one
+    process per GPU, exactly as the driver launches it."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args.gpus)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; measuring {world} rank(s)", file=sys.stderr)
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
         return
@@ -366,13 +384,18 @@ def main():
                              seed=args.seed, views=mine)
     gen_s = time.perf_counter() - t_gen
     N, D = cfg["n_gaussians"], cfg["dim"]
-    n_pad = (N + world - 1) // world * world
-    shard = n_pad // world
 
     ctx = Context(local)
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
     ctx.set_scene(wl.scene.mean, wl.scene.scale, wl.scene.quat_xyzw, wl.scene.opacity)
+    if world > 1:
+        # the library's own NCCL communicator (the combine is one grouped
+        # reduce-scatter issued by libsemsplat_b200, not by torch)
+        uid = [Context.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx.comm_init(world, rank, uid[0])
+    ctx.set_combine_rows(args.combine_rows)
     lanes = args.lanes or DEFAULT_LANES
     ctx.set_lanes(lanes)
     if args.group:
@@ -394,22 +417,19 @@ def main():
     d_clip = [torch.from_numpy(np.ascontiguousarray(m[5], np.float32)).to(dev) for m in wl.masks]
     dev_masks = [(m[0], m[1], m[2], d_runs.data_ptr(), o.data_ptr(), c.data_ptr(), int(m[4][-1] - m[4][0]))
                  for m, o, c in zip(wl.masks, d_offs, d_clip)]
-    sums = torch.zeros((n_pad, D), dtype=torch.float32, device=dev)
-    totals = torch.zeros((n_pad,), dtype=torch.float32, device=dev)
-    sum_shard = torch.empty((shard, D), dtype=torch.float32, device=dev) if world > 1 else None
-    tot_shard = torch.empty((shard,), dtype=torch.float32, device=dev) if world > 1 else None
+    lay = ctx.combine_layout()
+    shard = lay["rank_rows"]  # rows this rank receives (block-cyclic rounds; padding included)
+    sums = torch.zeros((lay["rows_alloc"], D), dtype=torch.float32, device=dev)
+    totals = torch.zeros((lay["rows_alloc"],), dtype=torch.float32, device=dev)
     rows_out = torch.empty((shard, D), dtype=torch.float32, device=dev)
     cov_out = torch.empty((shard,), dtype=torch.float32, device=dev)
+    held = ctx.combine_rows_of(lay)
+    n_local = int((held < N).sum())  # real table rows this rank finalises
 
     def combine_and_normalize():
-        if world > 1:
-            dist.reduce_scatter_tensor(sum_shard, sums)
-            dist.reduce_scatter_tensor(tot_shard, totals)
-            s, t = sum_shard, tot_shard
-        else:
-            s, t = sums, totals
-        n_local = max(0, min(shard, N - rank * shard))
-        ctx.normalize_device(s.data_ptr(), t.data_ptr(), n_local, D, rows_out.data_ptr(), cov_out.data_ptr())
+        # combine_partials + finalize_into: one grouped NCCL reduce-scatter per
+        # round (sums and totals), then the shard's normalisation
+        ctx.combine_device(rows_out.data_ptr(), cov_out.data_ptr())
 
     def step_device():
         ctx.encode_begin(D, sums.data_ptr(), totals.data_ptr())
@@ -534,7 +554,6 @@ def main():
     if rank == 0 and not args.no_query:
         try:
             from harness.workload import synth_embedding
-            n_local = max(0, min(shard, N - rank * shard))
             lab_ids = np.arange(16, dtype=np.int32)
             lab_vecs = np.stack([synth_embedding(f"class_{i}", D) for i in range(16)])
             ctx.assign_classes_device(rows_out.data_ptr(), cov_out.data_ptr(), n_local, D, lab_ids, lab_vecs)
@@ -579,7 +598,12 @@ def main():
             "embed_seconds": ms_step / 1e3,
             "config": {"workload": f"{args.config}: {N} Gaussians, {n_views} views {cfg['width']}x{cfg['height']}, "
                                    f"{cfg['masks_per_view']} masks/view, D={D}",
-                       "parallelism": f"views round-robin over {world} GPU(s), NCCL reduce-scatter of N x D sums",
+                       "parallelism": f"views round-robin over {world} GPU(s); combine = the library's NCCL "
+                                      f"reduce-scatter of the N x D sums and N totals (one group per round, "
+                                      f"{lay['rounds']} round(s) of {lay['block_rows']} rows per rank), then "
+                                      f"per-rank normalisation of {n_local} rows",
+                       "nccl": {"nranks": world, "communicator": "libsemsplat_b200 (ss_comm_init)"} if world > 1
+                       else None,
                        "l2": "inputs larger than L2 (N x 512 fp32 sums = %.1f GB RMW per pass)" % (N * D * 4 / 1e9),
                        "dataset_gen_seconds": gen_s},
             "roofline": roofline,

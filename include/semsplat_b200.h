@@ -104,6 +104,8 @@ int ss_synchronize(ss_ctx* ctx);
  * 1 = stable key sort, 2 = direct binning (up to 18000 tiles; error above).
  * The tile lists are identical.
 
+ * SS_OPT_COMBINE_ROWS: rows per block of the block-cyclic combine (see the
+ * multi-GPU section; 0 = contiguous shards).  Set before ss_encode_begin.
  * SS_OPT_RASTER: compositor schedule, 0 = staged evaluation (default: per
  * staged chunk, the box test and Mahalanobis distance per splat, then exp and
  * alpha dense over the surviving pairs, then the front-to-back transmittance
@@ -114,7 +116,8 @@ enum ss_option {
     SS_OPT_QUERY_PATH = 2,
     SS_OPT_CONTRACT_GROUP = 3,
     SS_OPT_BIN_PATH = 4,
-    SS_OPT_RASTER = 5
+    SS_OPT_RASTER = 5,
+    SS_OPT_COMBINE_ROWS = 6
 };
 int ss_set_option(ss_ctx* ctx, int option, int64_t value);
 
@@ -174,6 +177,42 @@ int ss_encode_finalize(ss_ctx* ctx, uint64_t row_lo, uint64_t row_hi, float* row
 int ss_normalize_device(ss_ctx* ctx, const float* d_sums, const float* d_totals, uint64_t n, uint32_t dim,
                         float* d_rows_out, float* d_coverage_out);
 
+/* ---- multi-GPU combine (pipeline.hpp:90-100 combine_partials + :120-141) -
+ * Views shard across devices like the reference's workers
+ * (pipeline.hpp:306-316); every device accumulates a full N x dim fp32
+ * partial.  One NCCL reduce-scatter (sums and totals in one NCCL group) over
+ * NVLink combines them, and every rank normalises the rows it receives.
+ * Row ownership is block-cyclic with block B = SS_OPT_COMBINE_ROWS rows
+ * (0 = one contiguous shard of ceil(N / nranks) rows per rank; otherwise
+ * chunk_rows of encode_scene, pipeline.hpp:396-402): round q reduce-scatters
+ * rows [q*nranks*B, (q+1)*nranks*B) and rank r receives rows
+ * [q*nranks*B + r*B, q*nranks*B + (r+1)*B); the next round's collective
+ * overlaps this round's normalisation.  NCCL is loaded at run time (the copy
+ * already in the process, e.g. torch's, else libnccl.so.2). */
+#define SS_NCCL_UNIQUE_ID_BYTES 128
+/* A new NCCL unique id (rank 0 creates it; the caller ships it to the others). */
+int ss_comm_unique_id(unsigned char id[SS_NCCL_UNIQUE_ID_BYTES]);
+/* Join the communicator as `rank` of `nranks` (one process per device). */
+int ss_comm_init(ss_ctx* ctx, int nranks, int rank, const unsigned char id[SS_NCCL_UNIQUE_ID_BYTES]);
+/* One process driving several devices: ctxs[i] becomes rank i (ncclCommInitAll). */
+int ss_comm_init_all(ss_ctx* const* ctxs, int n);
+/* Accumulator rows to allocate (N padded to whole rounds), block rows B,
+ * rounds, and the rows this rank receives (rounds * B, padding included). */
+int ss_combine_layout(ss_ctx* ctx, uint64_t* rows_alloc, uint64_t* block_rows, uint64_t* rounds,
+                      uint64_t* rank_rows);
+/* The same layout for n rows over nranks ranks with SS_OPT_COMBINE_ROWS =
+ * combine_rows (no context or device needed). */
+int ss_combine_layout_for(uint64_t n, int nranks, uint64_t combine_rows, uint64_t* rows_alloc, uint64_t* block_rows,
+                          uint64_t* rounds);
+/* Reduce-scatter the accumulators of ss_encode_begin/ss_encode_views over the
+ * communicator (a plain pass-through without one) and finalize_into the
+ * received rows: rows_out (rank_rows x dim) and coverage_out (rank_rows), in
+ * round order; rows past N come out zero.  out_on_device: device pointers.
+ * With several ranks every rank must call it (collective). */
+int ss_encode_combine(ss_ctx* ctx, float* rows_out, float* coverage_out, int out_on_device);
+/* Number of CUDA devices visible to the library. */
+int ss_device_count(int* n);
+
 /* ---- vector store + query (vecstore.hpp:21-146) ----------------------- */
 /* build_store (vecstore.hpp:88-103): covered rows of a table -> unit rows
  * (normalized_copy, vecstore.hpp:34-42, f64 norm).  Keeps the store on the
@@ -208,7 +247,8 @@ enum ss_kernel_class {
     SS_K_H2D = 8,
     SS_K_QUERY_GEMM = 9,    /* tcgen05 coarse scores (inside SS_K_QUERY) */
     SS_K_QUERY_SELECT = 10, /* candidate selection + exact rescoring (inside SS_K_QUERY) */
-    SS_K_COUNT = 11
+    SS_K_COMBINE = 11,      /* NCCL reduce-scatter of the partials (bytes: sent per rank) */
+    SS_K_COUNT = 12
 };
 int ss_profile_enable(ss_ctx* ctx, int on);
 int ss_profile_reset(ss_ctx* ctx);

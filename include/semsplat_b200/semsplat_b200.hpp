@@ -23,6 +23,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -65,10 +66,38 @@ public:
         return *devs[device];
     }
     ss_ctx* ctx() { return ctx_; }
+    int device() const { return device_; }
     std::mutex& mutex() { return mu_; }
-    // Upload the scene (N x 48 B; cheap next to any call that uses it).  No
-    // caching by address: a caller may reuse the same object storage.
+    // Content key of a scene: size plus a 64-bit mix of every Gaussian's
+    // fields (a caller may reuse the same storage for another scene, so the
+    // address alone is not a key).
+    static uint64_t scene_key(const GaussianScene& scene) {
+        uint64_t h = 0x9e3779b97f4a7c15ull ^ scene.size();
+        for (size_t k = 0; k < scene.size(); ++k) {
+            const Gaussian3D& g = scene[k];
+            const float f[11] = {g.mean[0], g.mean[1], g.mean[2], g.scale[0], g.scale[1], g.scale[2],
+                                 g.rotation.x(), g.rotation.y(), g.rotation.z(), g.rotation.w(), g.opacity};
+            for (float v : f) {
+                uint32_t b;
+                std::memcpy(&b, &v, 4);
+                h = (h ^ b) * 0x100000001b3ull;
+                h ^= h >> 29;
+            }
+        }
+        return h;
+    }
+    // Upload the scene unless this device already holds it (same content
+    // key): per-view calls (eval.hpp:94, fixture.hpp:157) do not re-upload
+    // and re-derive the 3-D covariances of an unchanged scene.
     void bind(const GaussianScene& scene) {
+        const uint64_t key = scene_key(scene);
+        if (bound_ && key == key_) return;
+        upload(scene);
+        bound_ = true;
+        key_ = key;
+        color_bound_ = false;
+    }
+    void upload(const GaussianScene& scene) {
         const size_t n = scene.size();
         std::vector<float> mean(3 * n), scale(3 * n), quat(4 * n), op(n);
         for (size_t k = 0; k < n; ++k) {
@@ -87,19 +116,51 @@ public:
     }
     // Colors for rasterize (scene.hpp:28), after bind().
     void bind_color(const GaussianScene& scene) {
+        if (color_bound_) return;
         const size_t n = scene.size();
         std::vector<float> rgb(3 * n);
         for (size_t k = 0; k < n; ++k)
             for (int i = 0; i < 3; ++i) rgb[3 * k + i] = scene[k].color[i];
         check(ss_scene_set_color(ctx_, rgb.data(), n));
+        color_bound_ = true;
     }
     ~Device() { ss_destroy(ctx_); }
 
 private:
-    explicit Device(int device) { check(ss_create(device, &ctx_)); }
+    explicit Device(int device) : device_(device) { check(ss_create(device, &ctx_)); }
+    int device_ = 0;
     ss_ctx* ctx_ = nullptr;
     std::mutex mu_;
+    bool bound_ = false, color_bound_ = false;
+    uint64_t key_ = 0;
 };
+
+// Binds a scene to a device ahead of per-view calls (optional: every call
+// binds, but a bound scene with an unchanged content key is not re-uploaded).
+inline void bind_scene(const GaussianScene& scene, int device = 0) {
+    Device& d = Device::get(device);
+    std::lock_guard<std::mutex> lock(d.mutex());
+    d.bind(scene);
+}
+
+inline int device_count() {
+    int n = 0;
+    check(ss_device_count(&n));
+    return n;
+}
+
+// Devices 0..n-1 joined in one NCCL communicator (ss_comm_init_all), created
+// once per device count and kept for the process.
+inline void ensure_group(int n) {
+    static std::mutex mu;
+    static int joined = 0;
+    std::lock_guard<std::mutex> lock(mu);
+    if (joined == n) return;
+    std::vector<ss_ctx*> ctxs;
+    for (int d = 0; d < n; ++d) ctxs.push_back(Device::get(d).ctx());
+    check(ss_comm_init_all(ctxs.data(), n));
+    joined = n;
+}
 
 inline ss_camera to_c(const CameraPose& cam) {
     ss_camera c{};
@@ -188,9 +249,58 @@ inline std::vector<Projected2D> project_all(const GaussianScene& scene, const Ca
     return out;
 }
 
-// pipeline.hpp:280-470.  `workers` keeps the reference's view-to-worker
-// assignment; all workers of this process share the device context, whose
-// single fp32 accumulator stands in for the per-worker partials.
+namespace detail {
+// One view's masks in their on-disk encoding (RLE runs, no bitmap decode on
+// the host) and CLIP vectors, read as load_maskset / load_mask_embeddings do.
+struct ViewData {
+    std::vector<uint32_t> runs;
+    std::vector<uint64_t> offs;
+    std::vector<float> clip;
+};
+
+inline ViewData read_view(const DatasetManifest& manifest, const ImageEntry& entry) {
+    const std::string path = manifest.resolve(entry.mask_path);
+    std::ifstream is(path, std::ios::binary);
+    if (!is) throw IoError("cannot open mask file: " + path);
+    if (semsplat::detail::read_le<uint32_t>(is) != kMaskFileMagic) throw FormatError("bad mask file magic: " + path);
+    const uint32_t mw = semsplat::detail::read_le<uint32_t>(is), mh = semsplat::detail::read_le<uint32_t>(is);
+    const uint32_t count = semsplat::detail::read_le<uint32_t>(is);
+    if (mw != manifest.mask_width || mh != manifest.mask_height)
+        throw DataError("mask of image " + std::to_string(entry.image_id) +
+                        " does not match the manifest mask resolution");
+    std::vector<std::pair<uint32_t, std::vector<uint32_t>>> masks(count);
+    for (auto& m : masks) {
+        m.first = semsplat::detail::read_le<uint32_t>(is);
+        const uint64_t nr = semsplat::detail::read_le<uint64_t>(is);
+        m.second.resize(nr);
+        for (auto& r : m.second) r = semsplat::detail::read_le<uint32_t>(is);
+    }
+    std::sort(masks.begin(), masks.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    ViewData vd;
+    vd.offs.push_back(0);
+    for (auto& m : masks) {
+        vd.runs.insert(vd.runs.end(), m.second.begin(), m.second.end());
+        vd.offs.push_back(vd.runs.size());
+    }
+    const std::vector<MaskEmbedding> emb = load_mask_embeddings(manifest, entry.image_id, count);
+    vd.clip.resize(static_cast<size_t>(count) * manifest.embedding_dim);
+    for (uint32_t j = 0; j < count; ++j)
+        std::memcpy(vd.clip.data() + static_cast<size_t>(j) * manifest.embedding_dim, emb[j].vector.data(),
+                    manifest.embedding_dim * sizeof(float));
+    return vd;
+}
+} // namespace detail
+
+// pipeline.hpp:280-470.  Workers map to GPUs: with G = min(workers, visible
+// devices) devices, worker w (the reference's view-to-worker assignment,
+// round-robin or contiguous) runs on device w mod G, each device on its own
+// host thread with its own fp32 partial; for G > 1 the partials are combined
+// by one NCCL reduce-scatter per chunk of chunk_rows rows per device
+// (SS_OPT_COMBINE_ROWS; the reference's phase-2 chunks, pipeline.hpp:396-402)
+// and each device normalises the rows it receives (ss_encode_combine).  Per-
+// image failures stop their worker (pipeline.hpp:350-351); with several
+// workers they surface as PipelineError with one status line per worker,
+// naming its GPU.  `device` is the device of a single-GPU run.
 inline EmbeddingTable encode_scene(const GaussianScene& scene, const DatasetManifest& manifest, uint32_t workers,
                                    uint64_t chunk_rows, const EncodeOptions& options = {},
                                    EncodeStats* stats_out = nullptr, int device = 0) {
@@ -205,11 +315,18 @@ inline EmbeddingTable encode_scene(const GaussianScene& scene, const DatasetMani
             throw DataError("image " + std::to_string(e.image_id) + ": no camera with id " +
                             std::to_string(e.camera_id));
 
-    Device& d = Device::get(device);
-    std::lock_guard<std::mutex> lock(d.mutex());
-    d.bind(scene);
+    const int G = workers > 1 ? std::max(1, std::min<int>((int)workers, device_count())) : 1;
+    std::vector<Device*> devs;
+    for (int g = 0; g < G; ++g) devs.push_back(&Device::get(G == 1 ? device : g));
+    std::vector<std::unique_lock<std::mutex>> locks;
+    for (Device* d : devs) locks.emplace_back(d->mutex());
+    if (G > 1) ensure_group(G);
+    for (Device* d : devs) {
+        d->bind(scene);
+        check(ss_set_option(d->ctx(), SS_OPT_COMBINE_ROWS, G > 1 ? (int64_t)chunk_rows : 0));
+        check(ss_encode_begin(d->ctx(), manifest.embedding_dim, nullptr, nullptr));
+    }
     const auto t0 = std::chrono::steady_clock::now();
-    check(ss_encode_begin(d.ctx(), manifest.embedding_dim, nullptr, nullptr));
     const size_t n_img = manifest.images.size();
     const size_t block = (n_img + workers - 1) / workers;
     std::vector<std::string> failures(workers);
@@ -217,19 +334,14 @@ inline EmbeddingTable encode_scene(const GaussianScene& scene, const DatasetMani
     std::vector<double> worker_seconds(workers, 0.0);
     std::vector<size_t> worker_entries(workers, 0);
     const ss_weight_mode wmode = options.mode == WeightMode::kFalloffOnly ? SS_FALLOFF_ONLY : SS_ALPHA_COMPOSITED;
-    for (uint32_t rank = 0; rank < workers; ++rank) {
+
+    auto run_worker = [&](uint32_t rank, ss_ctx* ctx) {
         const auto ts = std::chrono::steady_clock::now();
-        // a worker's views go to the device as one batch (views overlap in the
+        // a worker's views go to its device as one batch (views overlap in the
         // device's pipeline lanes); host-side decoding errors stop the worker
         // at that image, as the reference's worker_body does
-        struct ViewData {
-            std::vector<uint32_t> runs;
-            std::vector<uint64_t> offs;
-            std::vector<float> clip;
-        };
-        std::vector<ViewData> data;
+        std::vector<detail::ViewData> data;
         std::vector<ss_camera> cams;
-        std::vector<uint32_t> image_ids;
         for (size_t idx = 0; idx < n_img; ++idx) {
             const bool mine = options.contiguous_batching ? (idx / block == rank) : (idx % workers == rank);
             if (!mine) continue;
@@ -237,41 +349,10 @@ inline EmbeddingTable encode_scene(const GaussianScene& scene, const DatasetMani
             try {
                 const CameraPose raster_cam = camera_scaled_to(*camera_by_id.at(entry.camera_id),
                                                                manifest.raster_width, manifest.raster_height);
-                // masks stay RLE: read the run streams straight from the mask file
-                const std::string path = manifest.resolve(entry.mask_path);
-                std::ifstream is(path, std::ios::binary);
-                if (!is) throw IoError("cannot open mask file: " + path);
-                if (detail::read_le<uint32_t>(is) != kMaskFileMagic) throw FormatError("bad mask file magic: " + path);
-                const uint32_t mw = detail::read_le<uint32_t>(is), mh = detail::read_le<uint32_t>(is);
-                const uint32_t count = detail::read_le<uint32_t>(is);
-                if (mw != manifest.mask_width || mh != manifest.mask_height)
-                    throw DataError("mask of image " + std::to_string(entry.image_id) +
-                                    " does not match the manifest mask resolution");
-                std::vector<std::pair<uint32_t, std::vector<uint32_t>>> masks(count);
-                for (auto& m : masks) {
-                    m.first = detail::read_le<uint32_t>(is);
-                    const uint64_t nr = detail::read_le<uint64_t>(is);
-                    m.second.resize(nr);
-                    for (auto& r : m.second) r = detail::read_le<uint32_t>(is);
-                }
-                std::sort(masks.begin(), masks.end(),
-                          [](const auto& a, const auto& b) { return a.first < b.first; });
-                ViewData vd;
-                vd.offs.push_back(0);
-                for (auto& m : masks) {
-                    vd.runs.insert(vd.runs.end(), m.second.begin(), m.second.end());
-                    vd.offs.push_back(vd.runs.size());
-                }
-                const std::vector<MaskEmbedding> emb = load_mask_embeddings(manifest, entry.image_id, count);
-                vd.clip.resize(static_cast<size_t>(count) * manifest.embedding_dim);
-                for (uint32_t j = 0; j < count; ++j)
-                    std::memcpy(vd.clip.data() + static_cast<size_t>(j) * manifest.embedding_dim,
-                                emb[j].vector.data(), manifest.embedding_dim * sizeof(float));
+                data.push_back(detail::read_view(manifest, entry));
                 ss_camera c = to_c(raster_cam);
                 c.image_id = entry.image_id;
                 cams.push_back(c);
-                image_ids.push_back(entry.image_id);
-                data.push_back(std::move(vd));
             } catch (const std::exception& ex) {
                 std::string m = ex.what();
                 const std::string pre = "image " + std::to_string(entry.image_id) + ":";
@@ -293,36 +374,85 @@ inline EmbeddingTable encode_scene(const GaussianScene& scene, const DatasetMani
             vms[v].n_runs = data[v].runs.size();
         }
         uint64_t before[5] = {}, after[5] = {};
-        check(ss_counters_read(d.ctx(), before));
+        check(ss_counters_read(ctx, before));
         if (!cams.empty()) {
-            const int st = ss_encode_views(d.ctx(), static_cast<uint32_t>(cams.size()), cams.data(), vms.data(), wmode);
-            if (st != SS_OK) {
-                // per-image errors already name the image ("image N: ...")
-                if (failures[rank].empty()) failures[rank] = ss_last_error();
-            }
+            const int st = ss_encode_views(ctx, static_cast<uint32_t>(cams.size()), cams.data(), vms.data(), wmode);
+            if (st != SS_OK && failures[rank].empty()) failures[rank] = ss_last_error(); // names the image
         }
-        check(ss_counters_read(d.ctx(), after));
+        check(ss_counters_read(ctx, after));
         worker_images[rank] = cams.size();
         worker_entries[rank] = static_cast<size_t>(after[3] - before[3]); // masked-weight (gid, mask) entries
         worker_seconds[rank] = std::chrono::duration<double>(std::chrono::steady_clock::now() - ts).count();
+    };
+    // one host thread per device, its workers in rank order
+    std::vector<std::string> device_errors(G);
+    auto run_device = [&](int g) {
+        try {
+            for (uint32_t w = (uint32_t)g; w < workers; w += (uint32_t)G) run_worker(w, devs[g]->ctx());
+        } catch (const std::exception& ex) {
+            device_errors[g] = ex.what();
+        }
+    };
+    if (G == 1) {
+        run_device(0);
+    } else {
+        std::vector<std::thread> threads;
+        for (int g = 0; g < G; ++g) threads.emplace_back(run_device, g);
+        for (auto& t : threads) t.join();
     }
+    for (int g = 0; g < G; ++g)
+        if (!device_errors[g].empty()) throw std::runtime_error("libsemsplat_b200: gpu " + std::to_string(g) + ": " +
+                                                                device_errors[g]);
     bool failed = false;
     for (const auto& f : failures) failed |= !f.empty();
     if (failed) {
         if (workers == 1) throw DataError(failures[0]);
         std::vector<std::string> status;
         for (uint32_t r = 0; r < workers; ++r)
-            status.push_back("worker " + std::to_string(r) + ": " + (failures[r].empty() ? "ok" : failures[r]));
+            status.push_back("worker " + std::to_string(r) + " (gpu " + std::to_string(G == 1 ? device : (int)(r % G)) +
+                             "): " + (failures[r].empty() ? "ok" : failures[r]));
         throw PipelineError("scene encoding failed", std::move(status), true);
     }
-    check(ss_synchronize(d.ctx()));
+    for (Device* d : devs) check(ss_synchronize(d->ctx()));
     const auto t1 = std::chrono::steady_clock::now();
     const uint64_t n = scene.size();
     EmbeddingTable table(n, manifest.embedding_dim);
-    const uint64_t step = (chunk_rows == 0 || chunk_rows > n) ? std::max<uint64_t>(n, 1) : chunk_rows;
-    for (uint64_t lo = 0; lo < n; lo += step) {
-        const uint64_t hi = std::min<uint64_t>(n, lo + step);
-        check(ss_encode_finalize(d.ctx(), lo, hi, table.row(lo), table.coverage.data() + lo, 0));
+    if (G == 1) {
+        const uint64_t step = (chunk_rows == 0 || chunk_rows > n) ? std::max<uint64_t>(n, 1) : chunk_rows;
+        for (uint64_t lo = 0; lo < n; lo += step) {
+            const uint64_t hi = std::min<uint64_t>(n, lo + step);
+            check(ss_encode_finalize(devs[0]->ctx(), lo, hi, table.row(lo), table.coverage.data() + lo, 0));
+        }
+    } else {
+        // combine_partials + finalize_into: every device reduce-scatters its
+        // partial and normalises the rows it receives (block-cyclic rounds)
+        std::vector<std::string> errs(G);
+        std::vector<std::thread> threads;
+        for (int g = 0; g < G; ++g)
+            threads.emplace_back([&, g] {
+                ss_ctx* ctx = devs[g]->ctx();
+                uint64_t rows_alloc = 0, blk = 0, rounds = 0, rank_rows = 0;
+                if (ss_combine_layout(ctx, &rows_alloc, &blk, &rounds, &rank_rows) != SS_OK) {
+                    errs[g] = ss_last_error();
+                    return;
+                }
+                std::vector<float> rows(rank_rows * manifest.embedding_dim), cov(rank_rows);
+                if (ss_encode_combine(ctx, rows.data(), cov.data(), 0) != SS_OK) {
+                    errs[g] = ss_last_error();
+                    return;
+                }
+                for (uint64_t q = 0; q < rounds; ++q)
+                    for (uint64_t i = 0; i < blk; ++i) {
+                        const uint64_t row = q * (uint64_t)G * blk + (uint64_t)g * blk + i, at = q * blk + i;
+                        if (row >= n) break;
+                        std::memcpy(table.row(row), rows.data() + at * manifest.embedding_dim,
+                                    manifest.embedding_dim * sizeof(float));
+                        table.coverage[row] = cov[at];
+                    }
+            });
+        for (auto& t : threads) t.join();
+        for (int g = 0; g < G; ++g)
+            if (!errs[g].empty()) throw std::runtime_error("libsemsplat_b200: gpu " + std::to_string(g) + ": " + errs[g]);
     }
     if (stats_out) {
         stats_out->phase1_seconds = std::chrono::duration<double>(t1 - t0).count();

@@ -42,7 +42,7 @@ PROJECTED_DTYPE = np.dtype([
 ENTRY_DTYPE = np.dtype([("gaussian_id", "<u4"), ("pixel", "<u4"), ("weight", "<f4")])
 
 K_NAMES = ["masks", "project", "sort", "bin", "raster", "contract", "normalize", "query", "h2d", "query_gemm",
-           "query_select"]
+           "query_select", "combine"]
 
 _lib = None
 
@@ -95,6 +95,13 @@ def lib() -> C.CDLL:
         "ss_profile_read": (i32, [vp, pd, pu64, pd]),
         "ss_counters_read": (i32, [vp, pu64]),
         "ss_launch_count": (i32, [vp, pu64, pu64]),
+        "ss_device_count": (i32, [C.POINTER(i32)]),
+        "ss_comm_unique_id": (i32, [vp]),
+        "ss_comm_init": (i32, [vp, i32, i32, vp]),
+        "ss_comm_init_all": (i32, [vp, i32]),
+        "ss_combine_layout": (i32, [vp, pu64, pu64, pu64, pu64]),
+        "ss_encode_combine": (i32, [vp, vp, vp, i32]),
+        "ss_combine_layout_for": (i32, [u64, i32, u64, pu64, pu64, pu64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -133,6 +140,7 @@ class Context:
         self.h = h
         self.device = device
         self._n = 0
+        self._nranks, self._rank = 1, 0
         self._dim = 0
 
     def close(self):
@@ -203,6 +211,56 @@ class Context:
 
     def synchronize(self):
         check(self._L.ss_synchronize(self.h))
+
+    # ---- multi-GPU combine (include/semsplat_b200.h, multi-GPU section)
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        buf = (C.c_ubyte * 128)()
+        check(lib().ss_comm_unique_id(buf))
+        return bytes(buf)
+
+    def comm_init(self, nranks: int, rank: int, uid: bytes):
+        buf = (C.c_ubyte * 128).from_buffer_copy(uid)
+        check(self._L.ss_comm_init(self.h, int(nranks), int(rank), buf))
+        self._nranks, self._rank = int(nranks), int(rank)
+
+    @staticmethod
+    def comm_init_all(ctxs):
+        arr = (C.c_void_p * len(ctxs))(*[c.h.value for c in ctxs])
+        check(lib().ss_comm_init_all(arr, len(ctxs)))
+        for i, c in enumerate(ctxs):
+            c._nranks, c._rank = len(ctxs), i
+
+    def set_combine_rows(self, rows: int):
+        """SS_OPT_COMBINE_ROWS: block rows of the block-cyclic combine (0 = contiguous shards)."""
+        check(self._L.ss_set_option(self.h, 6, int(rows)))
+
+    def combine_layout(self):
+        v = [C.c_uint64() for _ in range(4)]
+        check(self._L.ss_combine_layout(self.h, *[C.byref(x) for x in v]))
+        return dict(zip(("rows_alloc", "block_rows", "rounds", "rank_rows"), (x.value for x in v)))
+
+    def combine_device(self, d_rows: int, d_coverage: int):
+        """ss_encode_combine into device buffers (rank_rows x dim, rank_rows)."""
+        check(self._L.ss_encode_combine(self.h, C.c_void_p(d_rows), C.c_void_p(d_coverage), 1))
+
+    def combine(self):
+        """ss_encode_combine to host: (rows [rank_rows, dim], coverage [rank_rows], global row ids)."""
+        lay = self.combine_layout()
+        rr = lay["rank_rows"]
+        rows = np.zeros((rr, self._dim), np.float32)
+        cov = np.zeros(rr, np.float32)
+        check(self._L.ss_encode_combine(self.h, rows.ctypes.data_as(C.c_void_p), cov.ctypes.data_as(C.c_void_p), 0))
+        return rows, cov, self.combine_rows_of(lay)
+
+    def combine_rows_of(self, lay=None):
+        """Global row index of every combined row this rank holds (block-cyclic, round order)."""
+        lay = lay or self.combine_layout()
+        B, R = lay["block_rows"], lay["rounds"]
+        W, r = self._nranks, self._rank
+        q = np.arange(R, dtype=np.int64)[:, None]
+        i = np.arange(B, dtype=np.int64)[None, :]
+        return (q * W * B + r * B + i).reshape(-1)
 
     # ---- parity entry points
     def project(self, cam) -> np.ndarray:

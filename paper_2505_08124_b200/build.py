@@ -59,7 +59,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
             subprocess.run(cmd, check=True)
             relink = True
     if relink or LIB.stat().st_mtime < max(o.stat().st_mtime for o in objs):
-        cmd = [nvcc, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart"]
+        cmd = [nvcc, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart", "-ldl"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

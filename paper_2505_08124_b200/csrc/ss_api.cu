@@ -9,6 +9,8 @@
 // on one CUDA stream.  Replaces encode_scene's phase 1/phase 2 loops
 // (pipeline.hpp:280-470) for the views handed to it.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h> // types only: the library is resolved at run time (nccl_api)
 
 #include <algorithm>
 #include <cstdio>
@@ -238,6 +240,16 @@ struct ss_ctx {
     int bin_path = 0;   // SS_OPT_BIN_PATH
     int raster_algo = 0; // SS_OPT_RASTER
     int num_sms = 0;
+
+    // multi-GPU combine (ss_comm_*, ss_encode_combine)
+    ncclComm_t comm = nullptr;
+    bool own_comm = false;
+    int nranks = 1, rank = 0;
+    uint64_t combine_rows = 0;            // SS_OPT_COMBINE_ROWS
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_acc = nullptr, ev_rs[2] = {nullptr, nullptr}, ev_norm[2] = {nullptr, nullptr};
+    ss::DevBuf rs_sum[2], rs_tot[2], rs_stage;
+    uint64_t acc_rows = 0;                // accumulator rows (N padded to whole combine rounds)
 
     // instrumentation
     ss::ProfState prof;
@@ -843,6 +855,7 @@ void profile_drain(ss_ctx* c) {
     SS_CUDA(cudaStreamSynchronize(c->stream));
     for (auto& L : c->lanes) SS_CUDA(cudaStreamSynchronize(L.stream));
     SS_CUDA(cudaStreamSynchronize(c->cstream));
+    if (c->comm_stream) SS_CUDA(cudaStreamSynchronize(c->comm_stream));
     for (auto& pe : c->prof.pending) {
         float ms = 0;
         SS_CUDA(cudaEventElapsedTime(&ms, pe.second.first, pe.second.second));
@@ -851,6 +864,92 @@ void profile_drain(ss_ctx* c) {
         c->prof.pool.push_back(pe.second.second);
     }
     c->prof.pending.clear();
+}
+
+// ---------------------------------------------------------------- NCCL
+// Resolved at run time so the library never pins a second NCCL into a process
+// that already has one (torch's): the copy already loaded wins, then
+// $SS_NCCL_LIB, then libnccl.so.2 on the loader path.
+struct NcclApi {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                                  cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    std::string error;
+};
+
+const NcclApi& nccl_api() {
+    static NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) {
+            const char* env = getenv("SS_NCCL_LIB");
+            if (env && *env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+        }
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            a.error = std::string("cannot load NCCL (libnccl.so.2): ") + dlerror();
+            return a;
+        }
+        auto sym = [&](const char* n) { return dlsym(h, n); };
+        a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(sym("ncclGetUniqueId"));
+        a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(sym("ncclCommInitRank"));
+        a.CommInitAll = reinterpret_cast<decltype(a.CommInitAll)>(sym("ncclCommInitAll"));
+        a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(sym("ncclCommDestroy"));
+        a.ReduceScatter = reinterpret_cast<decltype(a.ReduceScatter)>(sym("ncclReduceScatter"));
+        a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(sym("ncclGroupStart"));
+        a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(sym("ncclGroupEnd"));
+        a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(sym("ncclGetErrorString"));
+        if (!a.GetUniqueId || !a.CommInitRank || !a.CommInitAll || !a.CommDestroy || !a.ReduceScatter ||
+            !a.GroupStart || !a.GroupEnd || !a.GetErrorString)
+            a.error = "libnccl.so.2 lacks a required symbol";
+        return a;
+    }();
+    if (!api.error.empty()) throw Error(SS_ERR_CUDA, api.error);
+    return api;
+}
+
+#define SS_NCCL(expr)                                                                                      \
+    do {                                                                                                   \
+        const NcclApi& _a = nccl_api();                                                                    \
+        ncclResult_t _r = (_a.expr);                                                                       \
+        if (_r != ncclSuccess)                                                                             \
+            throw Error(SS_ERR_CUDA, std::string("nccl") + #expr + ": " + _a.GetErrorString(_r));          \
+    } while (0)
+
+// Block-cyclic combine layout (include/semsplat_b200.h, multi-GPU section).
+struct CombineLayout {
+    uint64_t block = 0, rounds = 0, rows_alloc = 0;
+};
+CombineLayout combine_layout(uint64_t n, int nranks, uint64_t combine_rows) {
+    CombineLayout L;
+    const uint64_t W = (uint64_t)std::max(nranks, 1);
+    const uint64_t shard = std::max<uint64_t>((n + W - 1) / W, 1);
+    L.block = combine_rows ? std::min<uint64_t>(combine_rows, shard) : shard;
+    L.rounds = (n + W * L.block - 1) / (W * L.block);
+    if (L.rounds == 0) L.rounds = 1;
+    L.rows_alloc = L.rounds * W * L.block;
+    return L;
+}
+
+void comm_setup(ss_ctx* c) {
+    if (!c->comm_stream) SS_CUDA(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+    cudaEvent_t* evs[] = {&c->ev_acc, &c->ev_rs[0], &c->ev_rs[1], &c->ev_norm[0], &c->ev_norm[1]};
+    for (auto* e : evs)
+        if (!*e) SS_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+}
+
+void comm_release(ss_ctx* c) {
+    if (c->comm && c->own_comm) nccl_api().CommDestroy(c->comm);
+    c->comm = nullptr;
+    c->own_comm = false;
+    c->nranks = 1;
+    c->rank = 0;
 }
 
 } // namespace
@@ -924,6 +1023,20 @@ void ss_destroy(ss_ctx* c) {
         cudaEventDestroy(pe.second.second);
     }
     for (auto& L : c->lanes) L.release_all();
+    if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
+    try {
+        comm_release(c);
+    } catch (...) {
+    }
+    for (int i = 0; i < 2; ++i) {
+        c->rs_sum[i].release();
+        c->rs_tot[i].release();
+        if (c->ev_rs[i]) cudaEventDestroy(c->ev_rs[i]);
+        if (c->ev_norm[i]) cudaEventDestroy(c->ev_norm[i]);
+    }
+    c->rs_stage.release();
+    if (c->ev_acc) cudaEventDestroy(c->ev_acc);
+    if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     if (c->ev_user) cudaEventDestroy(c->ev_user);
     if (c->group_done) cudaEventDestroy(c->group_done);
     if (c->cstream) {
@@ -957,6 +1070,9 @@ int ss_set_option(ss_ctx* c, int option, int64_t value) {
         } else if (option == SS_OPT_QUERY_PATH) {
             if (value < 0 || value > 2) throw Error(SS_ERR_CONTRACT, "SS_OPT_QUERY_PATH must be 0, 1 or 2");
             c->query_path = (int)value;
+        } else if (option == SS_OPT_COMBINE_ROWS) {
+            if (value < 0) throw Error(SS_ERR_CONTRACT, "SS_OPT_COMBINE_ROWS must be >= 0");
+            c->combine_rows = (uint64_t)value;
         } else if (option == SS_OPT_RASTER) {
             if (value < 0 || value > 1) throw Error(SS_ERR_CONTRACT, "SS_OPT_RASTER must be 0 or 1");
             c->raster_algo = (int)value;
@@ -1223,7 +1339,10 @@ int ss_encode_begin(ss_ctx* c, uint32_t dim, float* d_sums, float* d_totals) {
             throw Error(SS_ERR_CONTRACT, "pass both external accumulators or neither");
         set_device(c);
         c->dim = dim;
-        const uint64_t N = std::max<uint64_t>(c->n, 1);
+        // rows padded to whole combine rounds (= N on one device without blocks);
+        // external buffers must hold ss_combine_layout's rows_alloc rows
+        const uint64_t N = std::max<uint64_t>(combine_layout(c->n, c->nranks, c->combine_rows).rows_alloc, 1);
+        c->acc_rows = N;
         if (d_sums) {
             c->sums = d_sums;
             c->totals = d_totals;
@@ -1702,6 +1821,156 @@ int ss_query_threshold(ss_ctx* c, const float* query, float tau, uint32_t* out_i
             out_sims[i] = f;
         }
         *out_count = m;
+    });
+}
+
+// ------------------------------------------------------------ multi-GPU
+int ss_device_count(int* n) {
+    return guarded([&] {
+        if (!n) throw Error(SS_ERR_CONTRACT, "output is null");
+        *n = 0;
+        cudaError_t e = cudaGetDeviceCount(n);
+        if (e != cudaSuccess) {
+            *n = 0;
+            cudaGetLastError();
+        }
+    });
+}
+
+int ss_comm_unique_id(unsigned char id[SS_NCCL_UNIQUE_ID_BYTES]) {
+    return guarded([&] {
+        static_assert(sizeof(ncclUniqueId) == SS_NCCL_UNIQUE_ID_BYTES, "ncclUniqueId size");
+        if (!id) throw Error(SS_ERR_CONTRACT, "id is null");
+        ncclUniqueId u;
+        SS_NCCL(GetUniqueId(&u));
+        std::memcpy(id, &u, sizeof(u));
+    });
+}
+
+int ss_comm_init(ss_ctx* c, int nranks, int rank, const unsigned char id[SS_NCCL_UNIQUE_ID_BYTES]) {
+    return guarded([&] {
+        if (!c || !id) throw Error(SS_ERR_CONTRACT, "ctx or id is null");
+        if (nranks < 1 || rank < 0 || rank >= nranks) throw Error(SS_ERR_CONTRACT, "rank out of range");
+        set_device(c);
+        comm_release(c);
+        comm_setup(c);
+        ncclUniqueId u;
+        std::memcpy(&u, id, sizeof(u));
+        ncclComm_t comm = nullptr;
+        SS_NCCL(CommInitRank(&comm, nranks, u, rank));
+        c->comm = comm;
+        c->own_comm = true;
+        c->nranks = nranks;
+        c->rank = rank;
+    });
+}
+
+int ss_comm_init_all(ss_ctx* const* ctxs, int n) {
+    return guarded([&] {
+        if (!ctxs || n < 1) throw Error(SS_ERR_CONTRACT, "need at least one context");
+        std::vector<int> devs(n);
+        for (int i = 0; i < n; ++i) {
+            if (!ctxs[i]) throw Error(SS_ERR_CONTRACT, "ctx is null");
+            devs[i] = ctxs[i]->device;
+            for (int j = 0; j < i; ++j)
+                if (devs[j] == devs[i]) throw Error(SS_ERR_CONTRACT, "ss_comm_init_all: one context per device");
+        }
+        std::vector<ncclComm_t> comms(n, nullptr);
+        for (int i = 0; i < n; ++i) {
+            set_device(ctxs[i]);
+            comm_release(ctxs[i]);
+            comm_setup(ctxs[i]);
+        }
+        SS_NCCL(CommInitAll(comms.data(), n, devs.data()));
+        for (int i = 0; i < n; ++i) {
+            ctxs[i]->comm = comms[i];
+            ctxs[i]->own_comm = true;
+            ctxs[i]->nranks = n;
+            ctxs[i]->rank = i;
+        }
+    });
+}
+
+int ss_combine_layout(ss_ctx* c, uint64_t* rows_alloc, uint64_t* block_rows, uint64_t* rounds, uint64_t* rank_rows) {
+    return guarded([&] {
+        if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
+        const CombineLayout L = combine_layout(c->n, c->nranks, c->combine_rows);
+        if (rows_alloc) *rows_alloc = L.rows_alloc;
+        if (block_rows) *block_rows = L.block;
+        if (rounds) *rounds = L.rounds;
+        if (rank_rows) *rank_rows = L.rounds * L.block;
+    });
+}
+
+int ss_combine_layout_for(uint64_t n, int nranks, uint64_t combine_rows, uint64_t* rows_alloc, uint64_t* block_rows,
+                          uint64_t* rounds) {
+    return guarded([&] {
+        if (nranks < 1) throw Error(SS_ERR_CONTRACT, "nranks must be >= 1");
+        const CombineLayout L = combine_layout(n, nranks, combine_rows);
+        if (rows_alloc) *rows_alloc = L.rows_alloc;
+        if (block_rows) *block_rows = L.block;
+        if (rounds) *rounds = L.rounds;
+    });
+}
+
+// combine_partials (pipeline.hpp:90-100: the partials' elementwise sum) as a
+// reduce-scatter per round on the communicator's stream, then finalize_into
+// (pipeline.hpp:120-135) of the received rows on the context's stream; round
+// q + 1's collective overlaps round q's normalisation (double-buffered).
+int ss_encode_combine(ss_ctx* c, float* rows_out, float* coverage_out, int out_on_device) {
+    return guarded([&] {
+        if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
+        if (!c->sums) throw Error(SS_ERR_CONTRACT, "combine before ss_encode_begin");
+        set_device(c);
+        const CombineLayout L = combine_layout(c->n, c->nranks, c->combine_rows);
+        if (L.rows_alloc != c->acc_rows)
+            throw Error(SS_ERR_CONTRACT, "ss_encode_combine: communicator or SS_OPT_COMBINE_ROWS changed after ss_encode_begin");
+        const uint64_t D = c->dim, W = (uint64_t)c->nranks, B = L.block;
+        cudaStream_t s = c->stream;
+        const bool collective = c->comm && W > 1;
+        if (collective) SS_CUDA(cudaEventRecord(c->ev_acc, s));
+        if (!out_on_device) c->rs_stage.ensure(B * (D + 1) * 4);
+        for (uint64_t q = 0; q < L.rounds; ++q) {
+            const int buf = (int)(q & 1);
+            const float* src_s;
+            const float* src_t;
+            if (collective) {
+                float* rs = static_cast<float*>(c->rs_sum[buf].ensure(B * D * 4));
+                float* rt = static_cast<float*>(c->rs_tot[buf].ensure(B * 4));
+                if (q == 0) SS_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_acc, 0));
+                if (q >= 2) SS_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_norm[buf], 0));
+                Scope sc(c, c->comm_stream, SS_K_COMBINE);
+                SS_NCCL(GroupStart());
+                SS_NCCL(ReduceScatter(c->sums + q * W * B * D, rs, B * D, ncclFloat32, ncclSum, c->comm,
+                                      c->comm_stream));
+                SS_NCCL(ReduceScatter(c->totals + q * W * B, rt, B, ncclFloat32, ncclSum, c->comm, c->comm_stream));
+                SS_NCCL(GroupEnd());
+                c->prof.launches[SS_K_COMBINE] += 1;
+                c->prof.bytes[SS_K_COMBINE] += (double)(W - 1) * B * (D + 1) * 4; // sent per rank
+                SS_CUDA(cudaEventRecord(c->ev_rs[buf], c->comm_stream));
+                SS_CUDA(cudaStreamWaitEvent(s, c->ev_rs[buf], 0));
+                src_s = rs;
+                src_t = rt;
+            } else {
+                src_s = c->sums + q * B * D; // one rank: its own partial is the combined one
+                src_t = c->totals + q * B;
+            }
+            float* dr = out_on_device ? rows_out + q * B * D : c->rs_stage.as<float>();
+            float* dc = out_on_device ? coverage_out + q * B : c->rs_stage.as<float>() + B * D;
+            {
+                Scope sc(c, s, SS_K_NORMALIZE);
+                own_launch(c, launch_normalize(src_s, src_t, B, (uint32_t)D, dr, dc,
+                                               c->counters.as<unsigned long long>() + 3, s),
+                           SS_K_NORMALIZE);
+                c->prof.bytes[SS_K_NORMALIZE] += (double)B * (4.0 * D + 8.0);
+            }
+            if (!out_on_device) {
+                SS_CUDA(cudaMemcpyAsync(rows_out + q * B * D, dr, B * D * 4, cudaMemcpyDeviceToHost, s));
+                SS_CUDA(cudaMemcpyAsync(coverage_out + q * B, dc, B * 4, cudaMemcpyDeviceToHost, s));
+                SS_CUDA(cudaStreamSynchronize(s)); // the staging buffer is reused next round
+            }
+            if (collective) SS_CUDA(cudaEventRecord(c->ev_norm[buf], s));
+        }
     });
 }
 

@@ -1,9 +1,12 @@
 """Multi-GPU plumbing of the embedding pass: one process per GPU
 (torch.distributed over NCCL), views sharded like the reference's workers
 (pipeline.hpp:309-311: round-robin idx % workers == rank, or contiguous
-blocks), one reduce-scatter of the N x D fp32 partial sums + N totals
-(the paper's "sum tensors from all GPUs"), each rank then
-normalises its row shard.  No other data-path collective exists.
+blocks), one reduce-scatter of the N x D fp32 partial sums + N totals per
+combine round (the paper's "sum tensors from all GPUs"; issued
+by libsemsplat_b200's own NCCL communicator, ss_encode_combine), each rank
+then normalises the rows it received.  No other data-path collective exists.
+This module holds the host-side mirror of that layout for the tests and the
+bench (combine_layout == ss_combine_layout_for).
 
 Query over a row-sharded store: each rank answers every
 query over its own rows, one all_gather of the per-rank (id, sim) top-k lists
@@ -23,33 +26,51 @@ def shard_views(n_views: int, world: int, rank: int, contiguous: bool = False) -
     return [v for v in range(n_views) if v % world == rank]
 
 
-def padded_rows(n: int, world: int) -> int:
-    """Rows padded to a multiple of the world size (reduce-scatter needs equal shards)."""
-    return (n + world - 1) // world * world
+def combine_layout(n: int, world: int, combine_rows: int = 0) -> dict:
+    """The block-cyclic row ownership of ss_encode_combine (include/semsplat_b200.h):
+    block B = combine_rows (0 = one contiguous shard of ceil(n / world) rows),
+    round q reduce-scatters rows [q*world*B, (q+1)*world*B) and rank r receives
+    [q*world*B + r*B, +B).  Mirrors ss_combine_layout_for."""
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    shard = max((n + world - 1) // world, 1)
+    block = min(combine_rows, shard) if combine_rows else shard
+    rounds = max((n + world * block - 1) // (world * block), 1)
+    return {"block_rows": block, "rounds": rounds, "rows_alloc": rounds * world * block,
+            "rank_rows": rounds * block}
 
 
-def shard_rows(n: int, world: int, rank: int):
-    """[lo, hi) rows of the table this rank normalises after the reduce-scatter."""
-    per = padded_rows(n, world) // world
-    lo = min(n, rank * per)
-    return lo, min(n, lo + per)
+def rows_of(n: int, world: int, rank: int, combine_rows: int = 0):
+    """Global table rows held by `rank` after the combine, in round order
+    (rows >= n are padding)."""
+    import numpy as np
+    lay = combine_layout(n, world, combine_rows)
+    b, r = lay["block_rows"], lay["rounds"]
+    q = np.arange(r, dtype=np.int64)[:, None]
+    i = np.arange(b, dtype=np.int64)[None, :]
+    return (q * world * b + rank * b + i).reshape(-1)
 
 
-def reduce_scatter_rows(out_shard, full, group=None):
-    """Sum `full` ([world*shard, ...]) over ranks, leave this rank's shard in
-    `out_shard`.  NCCL: one reduce_scatter_tensor.  Backends without it (gloo
-    on CPU, used by the tests) fall back to all_reduce + slice -- same result."""
+def reduce_scatter_rounds(full, world: int, rank: int, combine_rows: int = 0, n: int | None = None,
+                          group=None):
+    """The combine's collective on host tensors, for backends without a
+    reduce-scatter (gloo, used by the tests): per round an all_reduce of the
+    round's rows, then this rank's block.  `full` holds rows_alloc rows of the
+    layout for `n` table rows (first dim); returns this rank's rank_rows rows
+    in round order.  The product issues the same rounds as ncclReduceScatter
+    inside libsemsplat_b200 (ss_encode_combine)."""
+    import torch
     import torch.distributed as dist
-    backend = dist.get_backend(group)
-    if backend == "nccl":
-        dist.reduce_scatter_tensor(out_shard, full, group=group)
-        return out_shard
-    rank = dist.get_rank(group)
-    per = out_shard.shape[0]
-    tmp = full.clone()
-    dist.all_reduce(tmp, group=group)
-    out_shard.copy_(tmp[rank * per:(rank + 1) * per])
-    return out_shard
+    lay = combine_layout(full.shape[0] if n is None else n, world, combine_rows)
+    b = lay["block_rows"]
+    if full.shape[0] != lay["rows_alloc"]:
+        raise ValueError(f"expected {lay['rows_alloc']} accumulator rows, got {full.shape[0]}")
+    out = []
+    for q in range(lay["rounds"]):
+        part = full[q * world * b:(q + 1) * world * b].clone()
+        dist.all_reduce(part, group=group)
+        out.append(part[rank * b:(rank + 1) * b])
+    return torch.cat(out)
 
 
 def merge_topk(ids, sims, counts, k: int):

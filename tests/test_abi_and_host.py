@@ -139,15 +139,31 @@ def test_format_errors():
 
 
 def test_shard_views_matches_reference_assignment():
-    from paper_2505_08124_b200.multigpu import shard_rows, shard_views
+    from paper_2505_08124_b200.multigpu import shard_views
     for n, w in ((10, 3), (1000, 8), (7, 8), (0, 2)):
         rr = [shard_views(n, w, r) for r in range(w)]
         assert sorted(sum(rr, [])) == list(range(n))
         assert all(v % w == r for r in range(w) for v in rr[r])
         cc = [shard_views(n, w, r, contiguous=True) for r in range(w)]
         assert sum(cc, []) == list(range(n))
-        rows = [shard_rows(n, w, r) for r in range(w)]
-        assert rows[0][0] == 0 and rows[-1][1] == n and all(a[1] == b[0] for a, b in zip(rows, rows[1:]))
+
+
+@pytest.mark.parametrize("n,w,blk", [(2_000_000, 8, 0), (2_000_000, 8, 65536), (1501, 2, 97), (7, 8, 0), (5, 3, 2),
+                                     (1, 1, 0), (100, 1, 30)])
+def test_combine_layout_matches_library(n, w, blk):
+    """The Python mirror (multigpu.combine_layout / rows_of) of the library's
+    block-cyclic combine layout (ss_combine_layout_for, no device needed):
+    every table row is held by exactly one rank, rounds cover rows_alloc."""
+    import ctypes as C
+    from paper_2505_08124_b200._lib import lib
+    from paper_2505_08124_b200.multigpu import combine_layout, rows_of
+    ra, br, rd = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    assert lib().ss_combine_layout_for(n, w, blk, C.byref(ra), C.byref(br), C.byref(rd)) == 0
+    lay = combine_layout(n, w, blk)
+    assert (lay["rows_alloc"], lay["block_rows"], lay["rounds"]) == (ra.value, br.value, rd.value)
+    held = np.concatenate([rows_of(n, w, r, blk) for r in range(w)])
+    assert held.size == lay["rows_alloc"] and np.array_equal(np.sort(held), np.arange(lay["rows_alloc"]))
+    assert lay["rows_alloc"] >= n
 
 
 def test_error_kinds_map_to_reference_exceptions():

@@ -19,7 +19,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, combine_rows):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import sys
     from pathlib import Path
@@ -28,7 +28,7 @@ def _worker(rank, world, port, q):
     import torch.distributed as dist
 
     from oracle.bindings import Oracle
-    from paper_2505_08124_b200.multigpu import padded_rows, reduce_scatter_rows, shard_rows, shard_views
+    from paper_2505_08124_b200.multigpu import combine_layout, reduce_scatter_rounds, rows_of, shard_views
     from harness.workload import make_bench_workload
 
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -39,40 +39,48 @@ def _worker(rank, world, port, q):
     masks = [wl.masks[v] for v in mine]
     s, t = O.encode_partial(wl.scene, cams, masks, 32, 0, len(mine))
     n = 1501
-    npad = padded_rows(n, world)
-    full_s = torch.zeros((npad, 32), dtype=torch.float64)
-    full_t = torch.zeros((npad,), dtype=torch.float64)
+    lay = combine_layout(n, world, combine_rows)
+    full_s = torch.zeros((lay["rows_alloc"], 32), dtype=torch.float64)
+    full_t = torch.zeros((lay["rows_alloc"],), dtype=torch.float64)
     full_s[:n] = torch.from_numpy(s)
     full_t[:n] = torch.from_numpy(t)
-    per = npad // world
-    sh_s = torch.empty((per, 32), dtype=torch.float64)
-    sh_t = torch.empty((per,), dtype=torch.float64)
-    reduce_scatter_rows(sh_s, full_s)
-    reduce_scatter_rows(sh_t, full_t)
-    lo, hi = shard_rows(n, world, rank)
-    rows = np.zeros((hi - lo, 32), np.float32)
-    cov = np.zeros(hi - lo, np.float32)
-    O.L.sso_finalize(sh_s.numpy().ctypes.data, sh_t.numpy().ctypes.data, hi - lo, 32, rows.ctypes.data,
-                     cov.ctypes.data)
-    q.put((rank, lo, hi, rows, cov))
+    sh_s = reduce_scatter_rounds(full_s, world, rank, combine_rows, n)
+    sh_t = reduce_scatter_rounds(full_t, world, rank, combine_rows, n)
+    held = rows_of(n, world, rank, combine_rows)
+    keep = held < n
+    sh_s, sh_t, held = sh_s.numpy()[keep].copy(), sh_t.numpy()[keep].copy(), held[keep]
+    rows = np.zeros((held.size, 32), np.float32)
+    cov = np.zeros(held.size, np.float32)
+    O.L.sso_finalize(sh_s.ctypes.data, sh_t.ctypes.data, held.size, 32, rows.ctypes.data, cov.ctypes.data)
+    q.put((rank, held, rows, cov))
     dist.destroy_process_group()
 
 
-def test_two_rank_combine_matches_single_worker():
+@pytest.mark.parametrize("combine_rows", [0, 97])
+def test_two_rank_combine_matches_single_worker(combine_rows):
+    """Round-robin view shards, per-rank partials, the block-cyclic combine
+    rounds of ss_encode_combine (contiguous shards, and 97-row blocks: eight
+    rounds with a ragged last one), per-rank finalize == one worker."""
     import multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, combine_rows)) for r in range(2)]
     for p in procs:
         p.start()
     parts = [q.get(timeout=300) for _ in procs]
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    parts.sort()
-    rows = np.concatenate([p[3] for p in parts])
-    cov = np.concatenate([p[4] for p in parts])
+    n = 1501
+    rows = np.zeros((n, 32), np.float32)
+    cov = np.zeros(n, np.float32)
+    seen = np.zeros(n, np.int64)
+    for _, held, r, c in parts:
+        rows[held] = r
+        cov[held] = c
+        seen[held] += 1
+    assert (seen == 1).all()  # every table row is finalised by exactly one rank
 
     import sys
     from pathlib import Path
@@ -97,7 +105,7 @@ def _query_worker(rank, world, port, q):
     import torch.distributed as dist
 
     from oracle.bindings import Oracle
-    from paper_2505_08124_b200.multigpu import shard_rows, sharded_query_topk
+    from paper_2505_08124_b200.multigpu import rows_of, sharded_query_topk
 
     dist.init_process_group("gloo", rank=rank, world_size=world)
     rng = np.random.default_rng(44)
@@ -108,10 +116,11 @@ def _query_worker(rank, world, port, q):
     unit = np.stack([O.normalized_copy(r) for r in raw])
     ids = rng.permutation(n).astype(np.uint32)
     queries = np.concatenate([raw[[7, 100]], rng.uniform(-0.5, 0.5, (4, d)).astype(np.float32)])
-    lo, hi = shard_rows(n, world, rank)
+    held = rows_of(n, world, rank)
+    held = held[held < n]
 
     def local(qs, k):  # this rank's rows (the GPU product uses Context.query_topk)
-        return O.query_topk(ids[lo:hi], unit[lo:hi], qs, k)
+        return O.query_topk(ids[held], unit[held], qs, k)
 
     for k in (1, 12, 5000):
         mi, ms, mc = sharded_query_topk(local, queries, k)
