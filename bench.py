@@ -75,7 +75,7 @@ def parse():
     ap.add_argument("--lanes", type=int, default=0, help="pipeline lanes (0 = library default)")
     ap.add_argument("--group", type=int, default=0, help="views per contraction group (0 = library default)")
     ap.add_argument("--bin", type=int, default=0, help="tile binning: 0 auto, 1 key sort, 2 direct")
-    ap.add_argument("--raster", type=int, default=0, help="compositor: 0 staged evaluation, 1 per-step")
+    ap.add_argument("--raster", type=int, default=-1, help="compositor: 1 per-step (library default), 0 staged")
     ap.add_argument("--combine-rows", type=int, default=0,
                     help="rows per block of the block-cyclic combine (0 = contiguous shards)")
     ap.add_argument("--cpu-sample-queries", type=int, default=32)
@@ -402,7 +402,7 @@ def main():
         ctx.set_contract_group(args.group)
     if args.bin:
         ctx.set_bin_path(args.bin)
-    if args.raster:
+    if args.raster >= 0:
         ctx.set_raster_algo(args.raster)
 
     # device-resident inputs for `value`

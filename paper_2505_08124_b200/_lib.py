@@ -201,7 +201,7 @@ class Context:
         check(self._L.ss_set_option(self.h, 2, int(path)))
 
     def set_raster_algo(self, algo: int):
-        """SS_OPT_RASTER: 0 = staged-evaluation compositor (default), 1 = per-step compositor (same bits)."""
+        """SS_OPT_RASTER: 1 = per-step compositor (default), 0 = staged-evaluation compositor (same bits)."""
         check(self._L.ss_set_option(self.h, 5, int(algo)))
 
     def set_bin_path(self, path: int):

@@ -238,7 +238,7 @@ struct ss_ctx {
     bool store_half_ok = false;
     int query_path = 0; // SS_OPT_QUERY_PATH
     int bin_path = 0;   // SS_OPT_BIN_PATH
-    int raster_algo = 0; // SS_OPT_RASTER
+    int raster_algo = 1; // SS_OPT_RASTER (1 = per-step compositor, the faster one on every config)
     int num_sms = 0;
 
     // multi-GPU combine (ss_comm_*, ss_encode_combine)

@@ -66,7 +66,7 @@ struct RasterParams {
     const uint32_t* tile_start; // tile t is tile_list[start[t], end[t])
     const uint32_t* tile_end;
     uint32_t width, height, tiles_x;
-    uint32_t algo;                 // compositor: 0 = staged evaluation (default), 1 = per-step (SS_OPT_RASTER)
+    uint32_t algo;                 // compositor: 1 = per-step (default), 0 = staged evaluation (SS_OPT_RASTER)
     // capture mode
     uint32_t* pix_count;           // pass 0 output [P]
     const uint32_t* pix_offset;    // pass 1 input  [P]

@@ -689,3 +689,22 @@ def test_encode_more_than_128_masks_vs_oracle(gpu_ctx, oracle, m, dim):
     rel, cos = row_errors(rows, cov, er, ec)
     assert rel <= EMB_REL_TOL and cos >= EMB_COS_TOL, (rel, cos)
     np.testing.assert_allclose(cov, ec, rtol=1e-5)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_staged_compositor_matches_oracle(gpu_ctx, oracle, mode):
+    """SS_OPT_RASTER = 0 (staged evaluation): contributor lists bitwise and the
+    encode within tolerance, like the default per-step compositor."""
+    s = random_scene(1200, 61)
+    cam = make_test_camera(120, 90, 8.0)
+    wl = _bench_style(3000, 3, 80, 64, 48, 512, seed=62)
+    try:
+        gpu_ctx.set_raster_algo(0)
+        got = _capture(gpu_ctx, s, cam, mode)
+        rows, cov = _encode(gpu_ctx, wl.scene, wl.cams, wl.masks, 512, mode)
+    finally:
+        gpu_ctx.set_raster_algo(1)
+    _assert_capture_equal(got, oracle.rasterize(s, cam, mode), mode)
+    er, ec = oracle.encode(wl.scene, wl.cams, wl.masks, 512, mode=mode)
+    rel, cos = row_errors(rows, cov, er, ec)
+    assert rel <= EMB_REL_TOL and cos >= EMB_COS_TOL, (rel, cos)
