@@ -236,6 +236,9 @@ struct ss_ctx {
     // tensor-core query path: fp16 copy of the store, coarse scores, candidates
     ss::DevBuf store_half, qhalf, tc_scores, tc_thr, cand, cand_count, cand_sim;
     bool store_half_ok = false;
+    // upper bound of the store's row norms (1 for build_store's unit rows):
+    // the tensor-core query's error margin scales with it
+    float store_norm = 1.0f;
     int query_path = 0; // SS_OPT_QUERY_PATH
     int bin_path = 0;   // SS_OPT_BIN_PATH
     int raster_algo = 1; // SS_OPT_RASTER (1 = per-step compositor, the faster one on every config)
@@ -1432,6 +1435,16 @@ int ss_store_set(ss_ctx* c, const uint32_t* ids, const float* unit_rows, uint64_
                            cudaMemcpyHostToDevice));
         SS_CUDA(cudaMemcpy(c->store_rows.ensure(std::max<uint64_t>(count, 1) * dim * 4), unit_rows,
                            count * dim * 4, cudaMemcpyHostToDevice));
+        // the reference's VectorStore does not enforce unit rows (vecstore.hpp:61):
+        // bound the norms so the tensor-core margin stays a proof
+        auto* nb = static_cast<unsigned int*>(c->zero_flag.ensure(16));
+        SS_CUDA(cudaMemsetAsync(nb, 0, 4, c->stream));
+        own_launch(c, launch_row_norm_max(c->store_rows.as<float>(), count, dim, nb, c->stream), SS_K_QUERY);
+        SS_CUDA(cudaMemcpyAsync(c->h_u32, nb, 4, cudaMemcpyDeviceToHost, c->stream));
+        SS_CUDA(cudaStreamSynchronize(c->stream));
+        float nm;
+        std::memcpy(&nm, c->h_u32, 4);
+        c->store_norm = nm;
     });
 }
 
@@ -1469,6 +1482,7 @@ int ss_store_build(ss_ctx* c, const float* rows, const float* coverage, uint64_t
         c->store_count = count;
         c->store_dim = dim;
         c->store_half_ok = false;
+        c->store_norm = 1.0f; // normalized_copy rows
         if (count_out) *count_out = count;
     });
 }
@@ -1575,7 +1589,8 @@ void topk_sorted(ss_ctx* c, const float* d_qn, uint32_t nq, uint32_t k, uint32_t
     SS_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys, ksorted, (int)count, 0, 64, s));
     void* tmp = c->cub_tmp.ensure(tb);
     tb = c->cub_tmp.bytes;
-    std::vector<unsigned long long> hk(take);
+    // queries back to back on the stream; each query's first k keys are decoded
+    // into its result row on the device
     for (uint32_t q = 0; q < nq; ++q) {
         own_launch(c, launch_score(c->store_rows.as<float>(), count, c->store_dim, d_qn, q + 1, q, sc_buf, s),
                    SS_K_QUERY);
@@ -1583,21 +1598,15 @@ void topk_sorted(ss_ctx* c, const float* d_qn, uint32_t nq, uint32_t k, uint32_t
                    SS_K_QUERY);
         SS_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, keys, ksorted, (int)count, 0, 64, s));
         c->launches_cub += 1;
-        SS_CUDA(cudaMemcpyAsync(hk.data(), ksorted, take * 8, cudaMemcpyDeviceToHost, s));
-        SS_CUDA(cudaStreamSynchronize(s));
-        std::vector<uint32_t> ids(take);
-        std::vector<float> sims(take);
-        for (uint64_t i = 0; i < take; ++i) {
-            ids[i] = (uint32_t)(hk[i] & 0xffffffffu);
-            uint32_t b = ~(uint32_t)(hk[i] >> 32);
-            b = (b & 0x80000000u) ? (b & 0x7fffffffu) : ~b;
-            std::memcpy(&sims[i], &b, 4);
-        }
-        SS_CUDA(cudaMemcpyAsync(oid + (uint64_t)q * k, ids.data(), take * 4, cudaMemcpyHostToDevice, s));
-        SS_CUDA(cudaMemcpyAsync(osim + (uint64_t)q * k, sims.data(), take * 4, cudaMemcpyHostToDevice, s));
-        SS_CUDA(cudaStreamSynchronize(s));
+        own_launch(c, launch_decode_keys(ksorted, take, oid + (uint64_t)q * k, osim + (uint64_t)q * k, s),
+                   SS_K_QUERY);
     }
 }
+
+// |coarse - exact| <= kCoarseEps for unit rows and unit queries; every term
+// of the bound (fp16 operand rounding, fp32 accumulation, fp16 pilot scores,
+// the exact scorer's rounding) scales with the row norm
+float coarse_eps(const ss_ctx* c) { return ss::kCoarseEps * std::max(1.0f, c->store_norm); }
 
 constexpr uint32_t kQueryChunk = 1024; // queries per coarse-score pass
 constexpr uint32_t kCandCap = 4096;    // candidates kept per query
@@ -1635,7 +1644,7 @@ bool topk_tensor(ss_ctx* c, const float* d_qn, uint32_t nq, uint32_t k, uint32_t
             own_launch(c, ss::launch_coarse_pilot(c->store_half.p, (uint32_t)count, qc, nt, dim, pscores, c->num_sms, s),
                        SS_K_QUERY);
             own_launch(c,
-                       ss::launch_pilot_threshold(pscores, (uint32_t)count, nt, k, 2.0f * ss::kCoarseEps, thr + q0, s),
+                       ss::launch_pilot_threshold(pscores, (uint32_t)count, nt, k, 2.0f * coarse_eps(c), thr + q0, s),
                        SS_K_QUERY);
             c->prof.bytes[SS_K_QUERY_SELECT] += 2.0 * nt * (double)pcols * dim;
         }
@@ -1653,7 +1662,7 @@ bool topk_tensor(ss_ctx* c, const float* d_qn, uint32_t nq, uint32_t k, uint32_t
         Scope sr(c, s, SS_K_QUERY_SELECT);
         own_launch(c,
                    ss::launch_rescore(c->store_rows.as<float>(), c->store_ids.as<uint32_t>(), dim, d_qn, nq, cand,
-                                      cval, kCandCap, ccount, k, 2.0f * ss::kCoarseEps, oid, osim, s),
+                                      cval, kCandCap, ccount, k, 2.0f * coarse_eps(c), oid, osim, s),
                    SS_K_QUERY);
     }
     std::vector<uint32_t> hc(nq);
@@ -1676,7 +1685,8 @@ bool topk_tensor(ss_ctx* c, const float* d_qn, uint32_t nq, uint32_t k, uint32_t
 
 namespace {
 bool tc_eligible(const ss_ctx* c) {
-    return c->store_dim % 64 == 0 && c->store_dim <= 512 && c->store_count < (1ull << 31) &&
+    // rows beyond norm 1e4 (or non-finite) could overflow the fp16 operands and scores
+    return c->store_norm <= 1.0e4f && c->store_dim % 64 == 0 && c->store_dim <= 512 && c->store_count < (1ull << 31) &&
            (c->query_path == 2 || (c->query_path == 0 && c->store_count >= 16384));
 }
 
@@ -1703,7 +1713,7 @@ bool threshold_tensor(ss_ctx* c, const float* d_qn, float tau, uint32_t* out_ids
     auto* oid = static_cast<uint32_t*>(c->topk_ids.ensure((uint64_t)kCandCap * 4));
     auto* osim = static_cast<float*>(c->topk_sims.ensure((uint64_t)kCandCap * 4));
     c->h_u32[0] = 0;
-    float h_thr = tau - ss::kCoarseEps;
+    float h_thr = tau - coarse_eps(c);
     SS_CUDA(cudaMemcpyAsync(thr, &h_thr, 4, cudaMemcpyHostToDevice, s));
     SS_CUDA(cudaMemsetAsync(ccount, 0, 8, s));
     {

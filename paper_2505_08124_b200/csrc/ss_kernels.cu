@@ -1425,6 +1425,45 @@ __global__ void threshold_keys_kernel(const float* scores, const uint32_t* ids, 
     keys[i] = ((unsigned long long)b << 32) | ids[i];
 }
 
+// Inverse of threshold_keys_kernel for the first `take` sorted keys: query q's
+// ranked (id, sim) written straight into its result row (no host round trip).
+__global__ void decode_keys_kernel(const unsigned long long* keys, uint64_t take, uint32_t* ids, float* sims) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= take) return;
+    const unsigned long long k = keys[i];
+    ids[i] = (uint32_t)(k & 0xffffffffu);
+    uint32_t b = ~(uint32_t)(k >> 32);
+    b = (b & 0x80000000u) ? (b & 0x7fffffffu) : ~b;
+    sims[i] = __uint_as_float(b);
+}
+
+// Upper bound of the store's row norms (warp per row, f64 sum of squares,
+// rounded up): the tensor-core query's error bound scales with it.  Any
+// non-finite element reports +inf, which keeps such a store on the exact path.
+__global__ void __launch_bounds__(256) row_norm_max_kernel(const float* rows, uint64_t n, uint32_t dim,
+                                                           unsigned int* max_bits) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    float best = 0.0f;
+    for (uint64_t k = warp0; k < n; k += nwarps) {
+        const float* v = rows + k * dim;
+        double ns = 0.0;
+        bool finite = true;
+        for (uint32_t d = lane; d < dim; d += 32) {
+            const float x = v[d];
+            finite &= isfinite(x);
+            ns += (double)x * (double)x;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ns += __shfl_xor_sync(0xffffffffu, ns, o);
+        finite = __all_sync(0xffffffffu, finite);
+        const float nrm = finite ? __double2float_ru(sqrt(ns) * (1.0 + 1e-12)) : INFINITY;
+        best = fmaxf(best, nrm);
+    }
+    if (lane == 0 && best > 0.0f) atomicMax(max_bits, __float_as_uint(best)); // non-negative floats order as ints
+}
+
 } // namespace
 
 // ---------------------------------------------------------------- launchers
@@ -1692,6 +1731,19 @@ cudaError_t launch_threshold_keys(const float* scores, const uint32_t* ids, uint
                                   unsigned long long* keys, uint8_t* flags, cudaStream_t s) {
     if (!count) return cudaSuccess;
     threshold_keys_kernel<<<blocks_for(count, 256), 256, 0, s>>>(scores, ids, count, tau, keys, flags);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_decode_keys(const unsigned long long* keys, uint64_t take, uint32_t* ids, float* sims,
+                               cudaStream_t s) {
+    if (!take) return cudaSuccess;
+    decode_keys_kernel<<<blocks_for(take, 256), 256, 0, s>>>(keys, take, ids, sims);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_row_norm_max(const float* rows, uint64_t n, uint32_t dim, unsigned int* max_bits, cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    row_norm_max_kernel<<<warp_grid(n), 256, 0, s>>>(rows, n, dim, max_bits);
     return cudaGetLastError();
 }
 

@@ -111,5 +111,10 @@ cudaError_t launch_topk(const float* scores, const uint32_t* ids, uint64_t count
                         uint32_t q0, uint32_t* out_ids, float* out_sims, cudaStream_t s);
 cudaError_t launch_threshold_keys(const float* scores, const uint32_t* ids, uint64_t count, float tau,
                                   unsigned long long* keys, uint8_t* flags, cudaStream_t s);
+// first `take` sorted threshold keys -> (id, sim) result row, on the device
+cudaError_t launch_decode_keys(const unsigned long long* keys, uint64_t take, uint32_t* ids, float* sims,
+                               cudaStream_t s);
+// *max_bits = max(*max_bits, bits of an upper bound of every row's L2 norm); +inf bits for non-finite rows
+cudaError_t launch_row_norm_max(const float* rows, uint64_t n, uint32_t dim, unsigned int* max_bits, cudaStream_t s);
 
 } // namespace ss

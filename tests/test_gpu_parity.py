@@ -708,3 +708,26 @@ def test_staged_compositor_matches_oracle(gpu_ctx, oracle, mode):
     er, ec = oracle.encode(wl.scene, wl.cams, wl.masks, 512, mode=mode)
     rel, cos = row_errors(rows, cov, er, ec)
     assert rel <= EMB_REL_TOL and cos >= EMB_COS_TOL, (rel, cos)
+
+
+def test_query_tensor_core_non_unit_store_vs_oracle(gpu_ctx, oracle):
+    """The reference's VectorStore does not enforce unit rows (vecstore.hpp:61);
+    ss_store_set bounds the row norms and widens the tensor-core margin with
+    them, so non-unit stores stay exact on the tensor-core path, and stores
+    whose norms could overflow fp16 are answered by the exact scan."""
+    rng = np.random.default_rng(31)
+    raw = rng.standard_normal((6000, 128)).astype(np.float32)
+    unit = _unit_rows(oracle, raw)
+    scale = rng.uniform(0.2, 40.0, (6000, 1)).astype(np.float32)
+    rows = (unit * scale).astype(np.float32)
+    ids = rng.permutation(6000).astype(np.uint32)
+    q = rng.standard_normal((50, 128)).astype(np.float32)
+    before = gpu_ctx.query_stats()
+    _tc_vs_oracle(gpu_ctx, oracle, ids, rows, q, 10)
+    after = gpu_ctx.query_stats()
+    # answered on the tensor cores, no fallback
+    assert after["tc_queries"] - before["tc_queries"] == 50
+    assert after["exact_fallbacks"] == before["exact_fallbacks"]
+    rows[17] *= 1.0e5  # beyond the fp16-safe bound: the exact scan answers
+    _tc_vs_oracle(gpu_ctx, oracle, ids, rows, q, 10)
+    assert gpu_ctx.query_stats()["tc_queries"] == after["tc_queries"]
