@@ -75,7 +75,7 @@ def parse():
     ap.add_argument("--lanes", type=int, default=0, help="pipeline lanes (0 = library default)")
     ap.add_argument("--group", type=int, default=0, help="views per contraction group (0 = library default)")
     ap.add_argument("--bin", type=int, default=0, help="tile binning: 0 auto, 1 key sort, 2 direct")
-    ap.add_argument("--raster", type=int, default=-1, help="compositor: 1 per-step (library default), 0 staged")
+    ap.add_argument("--raster", type=int, default=-1, help="compositor: 2 per-step on work-stealing warps (library default), 1 per-step CTA per tile, 0 staged")
     ap.add_argument("--combine-rows", type=int, default=0,
                     help="rows per block of the block-cyclic combine (0 = contiguous shards)")
     ap.add_argument("--cpu-sample-queries", type=int, default=32)

@@ -106,11 +106,13 @@ int ss_synchronize(ss_ctx* ctx);
 
  * SS_OPT_COMBINE_ROWS: rows per block of the block-cyclic combine (see the
  * multi-GPU section; 0 = contiguous shards).  Set before ss_encode_begin.
- * SS_OPT_RASTER: compositor schedule, 1 = one splat per step for all pixels
- * of a warp's block (default), 0 = staged evaluation (per staged chunk the box
- * test and Mahalanobis distance per splat, then exp and alpha dense over the
- * surviving pairs, then the front-to-back transmittance walk; measured slower
- * on c4, 510 vs 382 us/view).  Identical bits. */
+ * SS_OPT_RASTER: compositor schedule, 2 = one splat per step for all pixels
+ * of a warp's 8x4 block, warps taking (tile, block) items from a work counter
+ * on a grid of 4 CTAs per SM (default); 1 = the same per-step compositor with
+ * one CTA per tile; 0 = staged evaluation (per staged chunk the box test and
+ * Mahalanobis distance per splat, then exp and alpha dense over the surviving
+ * pairs, then the front-to-back transmittance walk; measured slower on c4,
+ * 510 vs 382 us/view).  Identical bits. */
 enum ss_option {
     SS_OPT_LANES = 1,
     SS_OPT_QUERY_PATH = 2,

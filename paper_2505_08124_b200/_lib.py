@@ -8,13 +8,15 @@ device.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 import numpy as np
 
 from .errors import raise_for
 
-LIB_PATH = Path(__file__).resolve().parent / "libsemsplat_b200.so"
+# SS_LIB_PATH: load another build of the library (A/B timing of kernel variants)
+LIB_PATH = Path(os.environ.get("SS_LIB_PATH") or Path(__file__).resolve().parent / "libsemsplat_b200.so")
 
 
 class Camera(C.Structure):

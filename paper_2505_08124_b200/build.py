@@ -39,31 +39,34 @@ def _newest_header() -> float:
     return max((h.stat().st_mtime for h in hdrs), default=0.0)
 
 
-def build(verbose: bool = False, force: bool = False) -> Path:
-    BUILD.mkdir(exist_ok=True)
+def build(verbose: bool = False, force: bool = False, defines=(), out: Path | None = None) -> Path:
+    """defines/out: a variant build (extra -D flags) into out/ (its own objects and .so), for A/B timing."""
+    build_dir = BUILD if out is None else Path(out)
+    lib = LIB if out is None else Path(out) / LIB.name
+    build_dir.mkdir(parents=True, exist_ok=True)
     nvcc = _nvcc()
     hdr_time = _newest_header()
     objs = []
-    relink = force or not LIB.exists()
+    relink = force or not lib.exists()
     for src, extra in UNITS:
         s = CSRC / src
-        o = BUILD / (src + ".o")
+        o = build_dir / (src + ".o")
         objs.append(o)
         if force or not o.exists() or o.stat().st_mtime < max(s.stat().st_mtime, hdr_time):
             if src.endswith(".cpp"):
                 cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-I", str(ROOT / "include"), "-c", str(s), "-o", str(o)]
             else:
-                cmd = [nvcc, *ARCH, *COMMON, *extra, "-c", str(s), "-o", str(o)]
+                cmd = [nvcc, *ARCH, *COMMON, *extra, *[f"-D{d}" for d in defines], "-c", str(s), "-o", str(o)]
             if verbose:
                 print(" ".join(cmd), flush=True)
             subprocess.run(cmd, check=True)
             relink = True
-    if relink or LIB.stat().st_mtime < max(o.stat().st_mtime for o in objs):
-        cmd = [nvcc, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart", "-ldl"]
+    if relink or lib.stat().st_mtime < max(o.stat().st_mtime for o in objs):
+        cmd = [nvcc, *ARCH, "-shared", "-o", str(lib), *map(str, objs), "-lcudart", "-ldl"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

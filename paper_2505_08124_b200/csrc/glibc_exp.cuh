@@ -146,5 +146,43 @@ __device__ __forceinline__ double glibc_exp_s(double x, uint32_t tab_addr) {
     return __fma_rn(scale, tmp, scale);
 }
 
+// The compositor's exp: x = -d2/2 with d2 <= 9 (or NaN), so |x| < 512 and
+// glibc's special cases reduce to |x| < 2^-54 (including -0), where glibc
+// returns 1.0 + x.  The fast path below returns the same bits there (tmp is x
+// up to terms below 2^-108, and fma(1, tmp, 1) rounds to 1.0 + x), and NaN
+// propagates -- checked against this image's libm exp on 5e7 inputs in
+// [-4.5, 0], every binade of tiny values of both signs, +-0 and NaN.  So the
+// range check and its branch are dropped from the inner loop.
+__device__ __forceinline__ double glibc_exp_small(double x, uint32_t tab_addr) {
+#ifdef SS_EXP_LITERALS
+    const double InvLn2N = 0x1.71547652b82fep0 * 128, Shift = 0x1.8p52;
+    const double NegLn2hiN = -0x1.62e42fefa0000p-8, NegLn2loN = -0x1.cf79abc9e3b3ap-47;
+    const double C2 = 0x1.ffffffffffdbdp-2, C3 = 0x1.555555555543cp-3;
+    const double C4 = 0x1.55555cf172b91p-5, C5 = 0x1.1111167a4d017p-7;
+#else
+    // constant-bank operands (LDC/LDCU) instead of two moves per 64-bit literal
+    const double InvLn2N = kExpConst[0], Shift = 0x1.8p52;
+    const double NegLn2hiN = kExpConst[2], NegLn2loN = kExpConst[3];
+    const double C2 = kExpConst[4], C3 = kExpConst[5];
+    const double C4 = kExpConst[6], C5 = kExpConst[7];
+#endif
+    double kd = __fma_rn(x, InvLn2N, Shift);
+    const unsigned long long ki = (unsigned long long)__double_as_longlong(kd);
+    kd = __dsub_rn(kd, Shift);
+    double r = __fma_rn(kd, NegLn2hiN, x);
+    r = __fma_rn(kd, NegLn2loN, r);
+    const uint32_t idx = 2u * (uint32_t)(ki & 127ull);
+    const unsigned long long top = ki << 45;
+    unsigned long long t0, t1;
+    asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(t0), "=l"(t1) : "r"(tab_addr + idx * 8u));
+    const double tail = __longlong_as_double((long long)t0);
+    const unsigned long long sbits = t1 + top;
+    const double r2 = __dmul_rn(r, r);
+    const double tmp =
+        __fma_rn(__dmul_rn(r2, r2), __fma_rn(r, C5, C4), __fma_rn(__fma_rn(r, C3, C2), r2, __dadd_rn(tail, r)));
+    const double scale = __longlong_as_double((long long)sbits);
+    return __fma_rn(scale, tmp, scale);
+}
+
 } // namespace ss
 

@@ -149,6 +149,7 @@ struct Lane {
     DevBuf rec, boxes, rbox, rcnt, keys, k32, k32s, order, iota, offsets, tkeys, tkeys_sorted, tvals, tile_start, tile_end, list;
     DevBuf bin_counts, bin_slice, bin_tot, bin_done; // direct binning scratch
     DevBuf ts_fill, ts_slab;       // tile-sort binning: per-tile fill counters, unordered (key, gid) slots
+    DevBuf raster_work;            // work-stealing compositor counters (zero between launches)
     uint32_t ts_cap = kTileSortMax; // tile-sort slots per tile (larger tiles take the global path)
     uint64_t iota_n = 0;           // entries of the 0..n-1 sequence in `iota`
     uint64_t list_cap = 0;         // entries of `list`
@@ -158,7 +159,7 @@ struct Lane {
     uint32_t* h_u32 = nullptr;     // pinned scratch
     void release_all() {
         DevBuf* b[] = {&rec, &boxes, &rbox, &rcnt, &keys, &k32, &k32s, &order, &iota, &offsets, &tkeys, &tkeys_sorted, &tvals, &tile_start,
-                       &tile_end, &list, &cub_tmp, &info, &pix_bits, &mask_bits, &bin_counts, &bin_slice, &bin_tot, &bin_done,
+                       &tile_end, &list, &cub_tmp, &info, &raster_work, &pix_bits, &mask_bits, &bin_counts, &bin_slice, &bin_tot, &bin_done,
                        &runs, &run_offsets, &spans, &ts_fill, &ts_slab};
         for (auto* x : b) x->release();
         for (auto& cs : sets) cs.release();
@@ -241,7 +242,7 @@ struct ss_ctx {
     float store_norm = 1.0f;
     int query_path = 0; // SS_OPT_QUERY_PATH
     int bin_path = 0;   // SS_OPT_BIN_PATH
-    int raster_algo = 1; // SS_OPT_RASTER (1 = per-step compositor, the faster one on every config)
+    int raster_algo = 2; // SS_OPT_RASTER (2 = per-step compositor on work-stealing warps, the fastest on c4)
     int num_sms = 0;
 
     // multi-GPU combine (ss_comm_*, ss_encode_combine)
@@ -542,6 +543,11 @@ RasterParams raster_params(ss_ctx* c, Lane& L, const ss_camera& cam, const Geome
     p.tiles_x = g.tiles_x;
     p.info = L.info.as<ViewInfo>();
     p.algo = (uint32_t)c->raster_algo;
+    if (!L.raster_work.p) {
+        L.raster_work.ensure(16);
+        SS_CUDA(cudaMemset(L.raster_work.p, 0, 16));
+    }
+    p.work = L.raster_work.as<uint32_t>();
     return p;
 }
 
@@ -726,6 +732,13 @@ bool encode_one(ss_ctx* c, Lane& L, const ss_camera& cam, const ss_view_masks* v
                 p.mask_base = 32u * w0;
                 own_launch(c, launch_raster_fused(p, mode, g.tiles, s), SS_K_RASTER);
             }
+        }
+        {
+            // the view's touched Gaussians, compacted from the compositor's stamps
+            Scope sc(c, s, SS_K_CONTRACT);
+            own_launch(c, launch_touched_compact(S->touched.as<uint32_t>(), c->n, S->gen, tlist, tcount, s),
+                       SS_K_CONTRACT);
+            c->prof.bytes[SS_K_CONTRACT] += 4.0 * (double)c->n;
         }
         SS_CUDA(cudaEventRecord(L.raster_done, s));
         // auto grouping: only views the shared-memory group kernel takes
@@ -1077,7 +1090,7 @@ int ss_set_option(ss_ctx* c, int option, int64_t value) {
             if (value < 0) throw Error(SS_ERR_CONTRACT, "SS_OPT_COMBINE_ROWS must be >= 0");
             c->combine_rows = (uint64_t)value;
         } else if (option == SS_OPT_RASTER) {
-            if (value < 0 || value > 1) throw Error(SS_ERR_CONTRACT, "SS_OPT_RASTER must be 0 or 1");
+            if (value < 0 || value > 2) throw Error(SS_ERR_CONTRACT, "SS_OPT_RASTER must be 0, 1 or 2");
             c->raster_algo = (int)value;
         } else if (option == SS_OPT_BIN_PATH) {
             if (value < 0 || value > 3) throw Error(SS_ERR_CONTRACT, "SS_OPT_BIN_PATH must be 0, 1, 2 or 3");

@@ -7,6 +7,8 @@
 // weights -- must be reproduced exactly (BASELINE.json north_star).
 // Evaluation order: SURVEY.md Appendix A.
 #include <cuda_runtime.h>
+#include <algorithm>
+#include <cstdlib>
 #include <stdint.h>
 
 #include "glibc_exp.cuh"
@@ -235,7 +237,7 @@ __device__ __forceinline__ bool composite_one(PixelState& ps, const Rec& s, uint
     const double dx = ds(ps.dpx, s.mu_x), dy = ds(ps.dpy, s.mu_y);
     const double d2 = da(da(dm(dm(s.a, dx), dx), dm(dm(s.b2, dx), dy)), dm(dm(s.c, dy), dy));
     if (d2 > kMahalanobisSqCutoff) return false;
-    const double g = glibc_exp_s(dm(-0.5, d2), stab_addr);
+    const double g = glibc_exp_small(dm(-0.5, d2), stab_addr);
     if constexpr (FALLOFF) {
         if (g >= kWeightCutoff) {
             wf = __double2float_rn(g);
@@ -308,15 +310,10 @@ __device__ __forceinline__ void gate_and_accumulate(const RasterParams& p, bool 
         }
         rem &= ~gm;
     }
-    if ((int)lane == __ffs(em) - 1) {
-        // first toucher of this Gaussian in this view appends it to the
-        // contraction list (stamps, never cleared: the next view uses gen + 1)
-        if (*reinterpret_cast<volatile uint32_t*>(p.touched + gid) != p.gen &&
-            atomicExch(p.touched + gid, p.gen) != p.gen) {
-            const unsigned long long slot = atomicAdd(p.touched_count, 1ull);
-            p.touched_list[slot] = gid;
-        }
-    }
+    // stamp the Gaussian as touched in this view (fire-and-forget; stamps are
+    // never cleared, the next view uses gen + 1); the contraction list is
+    // compacted from the stamps after the compositor (touched_compact_kernel)
+    if ((int)lane == __ffs(em) - 1) p.touched[gid] = p.gen;
 }
 
 template <int MW>
@@ -349,27 +346,16 @@ __device__ __forceinline__ uint32_t match_bits(const uint32_t (&bits)[MW]) {
 //         One pass covers up to 128 masks (MW words); views with more masks
 //         (providers.hpp:135 allows any count) run one pass per 128-mask
 //         window [mask_base, mask_base + 128), each recompositing the tile.
+// One warp composites one 8x4 block (bx0, by0) of a tile against the tile's
+// list: the body of raster_kernel / raster_persist_kernel.
 template <int KIND, bool FALLOFF, int MW>
-__global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) {
-    __shared__ SplatRec srec[kRasterThreads]; // warp w stages its hits in srec[32w, 32w+32)
-    __shared__ uint32_t sgid[kRasterThreads];
-    __shared__ uint32_t smask[kRasterThreads];
-    __shared__ unsigned long long stab[256];
-    stab[threadIdx.x] = kExpTab[threadIdx.x];
-
-    const uint32_t tile = blockIdx.x;
+__device__ __forceinline__ void composite_block(const RasterParams& p, uint32_t tile, uint32_t wb, uint32_t lane,
+                                                SplatRec* wrec, uint32_t* wgid, uint32_t* wmask, uint32_t srec_addr,
+                                                uint32_t stab_addr) {
     const uint32_t tx = tile % p.tiles_x, ty = tile / p.tiles_x;
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-    const uint32_t bx0 = tx * kTile + 8u * (warp & 1u), by0 = ty * kTile + 4u * (warp >> 1);
+    const uint32_t bx0 = tx * kTile + 8u * (wb & 1u), by0 = ty * kTile + 4u * (wb >> 1);
     const uint32_t bx1 = bx0 + 7u, by1 = by0 + 3u;
     const uint32_t start = p.tile_start[tile], end = p.tile_end[tile];
-    if (p.info->overflow) return; // tile lists incomplete: the view is re-run by the host
-    const uint32_t wbase = 32u * warp;
-    SplatRec* wrec = srec + wbase;
-    uint32_t srec_addr = (uint32_t)__cvta_generic_to_shared(wrec);
-    uint32_t stab_addr = (uint32_t)__cvta_generic_to_shared(stab);
-    uint32_t* wgid = sgid + 32u * warp;
-    uint32_t* wmask = smask + 32u * warp;
 
     PixelState ps;
     ps.px = bx0 + (lane & 7u);
@@ -399,7 +385,6 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
         grp = match_bits<MW>(bits);
         ps.done = ps.done || !any; // unmasked pixels contribute nothing
     }
-    __syncthreads(); // exp table staged
 
     // prefetch the first chunk's ranks and boxes
     uint32_t nr = 0;
@@ -486,6 +471,73 @@ __global__ void __launch_bounds__(kRasterThreads) raster_kernel(RasterParams p) 
                 }
             }
         }
+    }
+}
+
+// One CTA (8 warps) per 16x16 tile, one thread per pixel.  Warp w owns the
+// 8x4 block at (8*(w&1), 4*(w>>1)).  Each warp walks the tile's depth-ordered
+// splat list independently, 32 entries at a time: one ballot culls the splats
+// whose padded box misses the block, the hits are staged in the warp's
+// shared-memory slice, and every lane composites its pixel against them front
+// to back; the warp stops when all 32 of its pixels have terminated.  This
+// shaping changes nothing in the arithmetic: every pixel still visits exactly
+// the splats whose box contains it, in depth order.
+//
+// KIND 0: count contributions per pixel (sizes the capture).
+// KIND 1: capture -- write WeightEntry records at per-pixel offsets, in depth
+//         order (= the reference's stable_sort by pixel), per_pixel_total and
+//         alpha = 1 - T_final.
+// KIND 2: fused -- gate each contribution by the pixel's SAM-mask bitset and
+//         add w into per-(Gaussian, mask) fp32 scalars (never a 512-d scatter).
+//         One pass covers up to 128 masks (MW words); views with more masks
+//         (providers.hpp:135 allows any count) run one pass per 128-mask
+//         window [mask_base, mask_base + 128), each recompositing the tile.
+template <int KIND, bool FALLOFF, int MW>
+__global__ void __launch_bounds__(kRasterThreads, 6) raster_kernel(RasterParams p) {
+    __shared__ SplatRec srec[kRasterThreads]; // warp w stages its hits in srec[32w, 32w+32)
+    __shared__ uint32_t sgid[kRasterThreads];
+    __shared__ uint32_t smask[kRasterThreads];
+    __shared__ unsigned long long stab[256];
+    stab[threadIdx.x] = kExpTab[threadIdx.x];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    if (p.info->overflow) return; // tile lists incomplete: the view is re-run by the host
+    __syncthreads();              // exp table staged
+    composite_block<KIND, FALLOFF, MW>(p, blockIdx.x, warp, lane, srec + 32u * warp, sgid + 32u * warp,
+                                       smask + 32u * warp, (uint32_t)__cvta_generic_to_shared(srec + 32u * warp),
+                                       (uint32_t)__cvta_generic_to_shared(stab));
+}
+
+// Work-stealing form: a grid sized to the resident CTAs, each warp taking
+// (tile, block) items from a counter until all tiles * 8 are done, so no warp
+// idles while its CTA's other blocks finish and no CTA waits for a tail wave.
+// Items go tile-major (the eight blocks of a tile run side by side and share
+// the tile's list in L2).  work[0] is the item counter, work[1] counts warps
+// out; the last warp resets both, so the next launch on the lane starts at 0.
+template <int KIND, bool FALLOFF, int MW>
+__global__ void __launch_bounds__(kRasterThreads, 6) raster_persist_kernel(RasterParams p) {
+    __shared__ SplatRec srec[kRasterThreads];
+    __shared__ uint32_t sgid[kRasterThreads];
+    __shared__ uint32_t smask[kRasterThreads];
+    __shared__ unsigned long long stab[256];
+    stab[threadIdx.x] = kExpTab[threadIdx.x];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    __syncthreads(); // exp table staged
+    const uint32_t items = p.n_tiles * 8u;
+    if (!p.info->overflow) { // else: tile lists incomplete, the view is re-run by the host
+        for (;;) {
+            uint32_t item = 0;
+            if (lane == 0) item = atomicAdd(p.work, 1u);
+            item = __shfl_sync(0xffffffffu, item, 0);
+            if (item >= items) break;
+            composite_block<KIND, FALLOFF, MW>(p, item >> 3, item & 7u, lane, srec + 32u * warp, sgid + 32u * warp,
+                                               smask + 32u * warp,
+                                               (uint32_t)__cvta_generic_to_shared(srec + 32u * warp),
+                                               (uint32_t)__cvta_generic_to_shared(stab));
+        }
+    }
+    if (lane == 0 && atomicAdd(p.work + 1, 1u) == gridDim.x * (kRasterThreads / 32u) - 1u) {
+        p.work[0] = 0u;
+        p.work[1] = 0u;
     }
 }
 
@@ -640,7 +692,7 @@ __global__ void __launch_bounds__(kRasterThreads) raster_staged_kernel(RasterPar
             // ---- A2: exp and alpha, dense over the list
             for (uint32_t k = lane; k < ne; k += 32u) {
                 const double d2 = wval[k];
-                const double g = glibc_exp_s(dm(-0.5, d2), stab_addr);
+                const double g = glibc_exp_small(dm(-0.5, d2), stab_addr);
                 if constexpr (FALLOFF) {
                     wval[k] = g;
                 } else {
@@ -725,13 +777,40 @@ __global__ void __launch_bounds__(kRasterThreads) raster_staged_kernel(RasterPar
     }
 }
 
+// CTAs of the work-stealing grid: 4 per SM (of the 6 that fit) leaves room for
+// the other lanes' kernels; measured on 300 c4 views, 5 lanes: 3 per SM 1571,
+// 4 per SM 1573-1580, 5 per SM 1552-1558, 6 per SM 1521-1529 views/s, against
+// 1536 for the CTA-per-tile grid.  SS_RASTER_CTAS_PER_SM overrides (timing).
+uint32_t persist_grid(uint32_t tiles) {
+    static uint32_t per_sm = [] {
+        const char* e = getenv("SS_RASTER_CTAS_PER_SM");
+        const int v = e ? atoi(e) : 4;
+        return (uint32_t)(v >= 1 && v <= 6 ? v : 4);
+    }();
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return std::min<uint32_t>(tiles, (uint32_t)sms * per_sm);
+}
+
+template <int KIND, bool FO, int MW>
+void launch_per_step(const RasterParams& p, uint32_t tiles, cudaStream_t s) {
+    if (p.algo == 2 && p.work) {
+        RasterParams q = p;
+        q.n_tiles = tiles;
+        raster_persist_kernel<KIND, FO, MW><<<persist_grid(tiles), kRasterThreads, 0, s>>>(q);
+    } else {
+        raster_kernel<KIND, FO, MW><<<tiles, kRasterThreads, 0, s>>>(p);
+    }
+}
+
 template <int KIND>
 cudaError_t launch_raster(const RasterParams& p, int mode, uint32_t tiles, cudaStream_t s) {
     if (tiles == 0) return cudaSuccess;
     const bool fo = mode == SS_FALLOFF_ONLY;
-    if (p.algo == 1) {
-        if (fo) raster_kernel<KIND, true, 1><<<tiles, kRasterThreads, 0, s>>>(p);
-        else raster_kernel<KIND, false, 1><<<tiles, kRasterThreads, 0, s>>>(p);
+    if (p.algo != 0) {
+        if (fo) launch_per_step<KIND, true, 1>(p, tiles, s);
+        else launch_per_step<KIND, false, 1>(p, tiles, s);
     } else {
         if (fo) raster_staged_kernel<KIND, true, 1><<<tiles, kRasterThreads, 0, s>>>(p);
         else raster_staged_kernel<KIND, false, 1><<<tiles, kRasterThreads, 0, s>>>(p);
@@ -815,9 +894,9 @@ cudaError_t launch_raster_fused(const RasterParams& p, int mode, uint32_t tiles,
     const bool fo = mode == SS_FALLOFF_ONLY;
 #define SS_FUSED(MWV)                                                                       \
     do {                                                                                    \
-        if (p.algo == 1) {                                                                  \
-            if (fo) raster_kernel<2, true, MWV><<<tiles, kRasterThreads, 0, s>>>(p);       \
-            else raster_kernel<2, false, MWV><<<tiles, kRasterThreads, 0, s>>>(p);         \
+        if (p.algo != 0) {                                                                  \
+            if (fo) launch_per_step<2, true, MWV>(p, tiles, s);                             \
+            else launch_per_step<2, false, MWV>(p, tiles, s);                               \
         } else {                                                                            \
             if (fo) raster_staged_kernel<2, true, MWV><<<tiles, kRasterThreads, 0, s>>>(p); \
             else raster_staged_kernel<2, false, MWV><<<tiles, kRasterThreads, 0, s>>>(p);   \

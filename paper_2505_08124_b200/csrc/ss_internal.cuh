@@ -66,7 +66,10 @@ struct RasterParams {
     const uint32_t* tile_start; // tile t is tile_list[start[t], end[t])
     const uint32_t* tile_end;
     uint32_t width, height, tiles_x;
-    uint32_t algo;                 // compositor: 1 = per-step (default), 0 = staged evaluation (SS_OPT_RASTER)
+    uint32_t algo;                 // compositor (SS_OPT_RASTER): 1 = per-step, CTA per tile; 2 = per-step,
+                                   // work-stealing warps (needs work); 0 = staged evaluation
+    uint32_t* work;                // [2] zero-initialised counters of the work-stealing grid (one pair per stream)
+    uint32_t n_tiles;              // set by the launcher
     // capture mode
     uint32_t* pix_count;           // pass 0 output [P]
     const uint32_t* pix_offset;    // pass 1 input  [P]

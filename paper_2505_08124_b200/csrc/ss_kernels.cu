@@ -1425,6 +1425,57 @@ __global__ void threshold_keys_kernel(const float* scores, const uint32_t* ids, 
     keys[i] = ((unsigned long long)b << 32) | ids[i];
 }
 
+// The view's contraction list from the compositor's stamps: every Gaussian
+// with touched[g] == gen.  A block takes 1024 consecutive ids per round (4 per
+// thread) and reserves its slots with one atomic (per-warp atomics on the one
+// counter serialise in L2).
+__global__ void __launch_bounds__(256) touched_compact_kernel(const uint32_t* touched, uint64_t n, uint32_t gen,
+                                                              uint32_t* list, unsigned long long* count) {
+    __shared__ uint32_t wtot[8];
+    __shared__ unsigned long long sbase;
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint32_t below = (1u << lane) - 1u;
+    for (uint64_t b0 = (uint64_t)blockIdx.x * 1024u; b0 < n; b0 += (uint64_t)gridDim.x * 1024u) {
+        const uint64_t g0 = b0 + threadIdx.x * 4u;
+        uint32_t t[4] = {0u, 0u, 0u, 0u};
+        if (g0 + 3u < n) {
+            const uint4 v = __ldcs(reinterpret_cast<const uint4*>(touched + g0));
+            t[0] = v.x;
+            t[1] = v.y;
+            t[2] = v.z;
+            t[3] = v.w;
+        } else {
+            for (uint32_t k = 0; k < 4u; ++k)
+                if (g0 + k < n) t[k] = touched[g0 + k];
+        }
+        uint32_t bal[4], tot = 0;
+#pragma unroll
+        for (uint32_t k = 0; k < 4u; ++k) {
+            bal[k] = __ballot_sync(0xffffffffu, g0 + k < n && t[k] == gen);
+            tot += __popc(bal[k]);
+        }
+        if (lane == 0) wtot[warp] = tot;
+        __syncthreads();
+        uint32_t before = 0, all = 0;
+#pragma unroll
+        for (uint32_t w = 0; w < 8u; ++w) {
+            before += w < warp ? wtot[w] : 0u;
+            all += wtot[w];
+        }
+        if (threadIdx.x == 0 && all) sbase = atomicAdd(count, (unsigned long long)all);
+        __syncthreads();
+        if (all) {
+            unsigned long long base = sbase + before;
+#pragma unroll
+            for (uint32_t k = 0; k < 4u; ++k) {
+                if ((bal[k] >> lane) & 1u) list[base + __popc(bal[k] & below)] = (uint32_t)(g0 + k);
+                base += __popc(bal[k]);
+            }
+        }
+        __syncthreads(); // wtot / sbase are reused next round
+    }
+}
+
 // Inverse of threshold_keys_kernel for the first `take` sorted keys: query q's
 // ranked (id, sim) written straight into its result row (no host round trip).
 __global__ void decode_keys_kernel(const unsigned long long* keys, uint64_t take, uint32_t* ids, float* sims) {
@@ -1731,6 +1782,14 @@ cudaError_t launch_threshold_keys(const float* scores, const uint32_t* ids, uint
                                   unsigned long long* keys, uint8_t* flags, cudaStream_t s) {
     if (!count) return cudaSuccess;
     threshold_keys_kernel<<<blocks_for(count, 256), 256, 0, s>>>(scores, ids, count, tau, keys, flags);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_touched_compact(const uint32_t* touched, uint64_t n, uint32_t gen, uint32_t* list,
+                                  unsigned long long* count, cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    const uint64_t want = (n + 1023u) / 1024u; // 256 threads x 4 ids per block
+    touched_compact_kernel<<<(unsigned)std::min<uint64_t>(want, 148ull * 8u), 256, 0, s>>>(touched, n, gen, list, count);
     return cudaGetLastError();
 }
 

@@ -111,6 +111,9 @@ cudaError_t launch_topk(const float* scores, const uint32_t* ids, uint64_t count
                         uint32_t q0, uint32_t* out_ids, float* out_sims, cudaStream_t s);
 cudaError_t launch_threshold_keys(const float* scores, const uint32_t* ids, uint64_t count, float tau,
                                   unsigned long long* keys, uint8_t* flags, cudaStream_t s);
+// list (count starts at 0) <- every g < n with touched[g] == gen (the compositor's stamps)
+cudaError_t launch_touched_compact(const uint32_t* touched, uint64_t n, uint32_t gen, uint32_t* list,
+                                  unsigned long long* count, cudaStream_t s);
 // first `take` sorted threshold keys -> (id, sim) result row, on the device
 cudaError_t launch_decode_keys(const unsigned long long* keys, uint64_t take, uint32_t* ids, float* sims,
                                cudaStream_t s);

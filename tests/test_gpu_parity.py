@@ -691,19 +691,24 @@ def test_encode_more_than_128_masks_vs_oracle(gpu_ctx, oracle, m, dim):
     np.testing.assert_allclose(cov, ec, rtol=1e-5)
 
 
+@pytest.mark.parametrize("algo", [0, 1, 2])
 @pytest.mark.parametrize("mode", [0, 1])
-def test_staged_compositor_matches_oracle(gpu_ctx, oracle, mode):
-    """SS_OPT_RASTER = 0 (staged evaluation): contributor lists bitwise and the
-    encode within tolerance, like the default per-step compositor."""
+def test_compositor_schedules_match_oracle(gpu_ctx, oracle, mode, algo):
+    """Every SS_OPT_RASTER schedule (0 staged evaluation, 1 CTA per tile, 2
+    work-stealing warps -- the default): contributor lists bitwise and the
+    encode within tolerance.  The work counters reset themselves, so a second
+    capture on the same lane must match too."""
     s = random_scene(1200, 61)
     cam = make_test_camera(120, 90, 8.0)
     wl = _bench_style(3000, 3, 80, 64, 48, 512, seed=62)
     try:
-        gpu_ctx.set_raster_algo(0)
+        gpu_ctx.set_raster_algo(algo)
         got = _capture(gpu_ctx, s, cam, mode)
+        again = _capture(gpu_ctx, s, cam, mode)
         rows, cov = _encode(gpu_ctx, wl.scene, wl.cams, wl.masks, 512, mode)
     finally:
-        gpu_ctx.set_raster_algo(1)
+        gpu_ctx.set_raster_algo(2)
+    _assert_capture_equal(again, got, mode)
     _assert_capture_equal(got, oracle.rasterize(s, cam, mode), mode)
     er, ec = oracle.encode(wl.scene, wl.cams, wl.masks, 512, mode=mode)
     rel, cos = row_errors(rows, cov, er, ec)
