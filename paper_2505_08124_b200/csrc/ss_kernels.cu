@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 
 #include <cub/block/block_scan.cuh>
 #include <cub/device/device_scan.cuh>
@@ -740,40 +741,48 @@ __global__ void __launch_bounds__(kTsSortThreads) tile_sort_kernel(TileSortParam
         if (tid + k * kTsSortThreads < n) out[atomicAdd(cnt + ((v[k].x - mn) >> sh), 1u)] = v[k];
     }
     __syncthreads();
-    // cnt[b] is now the end of bucket b (= the start of bucket b + 1); order
-    // each shared bucket by (key, then depth bits and id on equal keys)
-    for (uint32_t b = tid; b < B; b += kTsSortThreads) {
+    // cnt[b] is now the end of bucket b (= the start of bucket b + 1).  Each
+    // instance's final position is its bucket's start plus its rank among the
+    // bucket's members by (key, then depth bits and id on equal keys) -- the
+    // reference's depth_sort comparator -- and its id goes straight to the
+    // tile's list (buckets average ~1-2 members: O(s) compares per instance,
+    // no serial insertion sort).
+    uint32_t* dst = p.list + base;
+#pragma unroll
+    for (uint32_t k = 0; k < kTsPer; ++k) {
+        if (k >= per) break;
+        if (tid + k * kTsSortThreads >= n) continue;
+        const uint2 x = v[k];
+        const uint32_t b = (x.x - mn) >> sh;
         const uint32_t s0 = b ? cnt[b - 1] : 0u, e0 = cnt[b];
-        if (e0 - s0 < 2u) continue;
-        if (e0 - s0 > kTsBucketMax) {
-            s_fail = 1u;
-            continue;
-        }
-        for (uint32_t a = s0 + 1; a < e0; ++a) {
-            const uint2 x = out[a];
-            uint32_t c = a;
-            while (c > s0) {
-                const uint2 y = out[c - 1];
-                bool before = x.x < y.x;
-                if (x.x == y.x) // equal narrowed keys: the full depth bits, then the id
-                    before = depth_before(__ldg(p.keys + x.y), x.y, __ldg(p.keys + y.y), y.y);
-                if (!before) break;
-                out[c] = y;
-                --c;
+        uint32_t pos = s0;
+        if (e0 - s0 > 1u) {
+            if (e0 - s0 > kTsBucketMax) {
+                s_fail = 1u;
+                continue;
             }
-            out[c] = x;
+            unsigned long long kx = 0ull;
+            bool have_kx = false;
+            for (uint32_t c = s0; c < e0; ++c) {
+                const uint2 y = out[c];
+                bool before = y.x < x.x;
+                if (y.x == x.x && y.y != x.y) { // equal narrowed keys: the full depth bits, then the id
+                    if (!have_kx) {
+                        kx = __ldg(p.keys + x.y);
+                        have_kx = true;
+                    }
+                    before = depth_before(__ldg(p.keys + y.y), y.y, kx, x.y);
+                }
+                pos += before ? 1u : 0u;
+            }
         }
+        dst[pos] = x.y;
     }
     __syncthreads();
-    if (s_fail) {
-        if (tid == 0) {
-            atomicMax(&p.info->bin_fallback, 2u);
-            p.info->overflow = 1u;
-        }
-        return;
+    if (s_fail && tid == 0) { // massive exact ties: the view takes the global depth sort
+        atomicMax(&p.info->bin_fallback, 2u);
+        p.info->overflow = 1u;
     }
-    uint32_t* dst = p.list + base;
-    for (uint32_t i = tid; i < n; i += kTsSortThreads) dst[i] = out[i].y;
 }
 
 // --------------------------------------------------------- contraction
@@ -1690,6 +1699,17 @@ cudaError_t launch_contract(const ContractParams& p, uint64_t max_touched, cudaS
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    {
+        // SS_CONTRACT_CTAS: grid of the group passes (timing experiments; default one CTA per SM)
+        static const int override_ctas = [] {
+            const char* e = getenv("SS_CONTRACT_CTAS");
+            return e ? atoi(e) : 0;
+        }();
+        // default: 3/5 of the SMs, so compositor CTAs of other views keep the
+        // rest (300 c4 views: 148 CTAs 1580, 110 1603-1606, 90 1615-1616,
+        // 74 1597-1607, 50 1579-1590 views/s)
+        sms = override_ctas > 0 ? std::min(sms, override_ctas) : std::max(1, (sms * 3 + 2) / 5);
+    }
     static std::atomic<int> configured_g[64] = {};
     if (dev >= 0 && dev < 64 && !configured_g[dev].load()) {
         const void* ks[] = {(const void*)contract_group_pass_kernel<0, 3, 2, false>,
