@@ -225,6 +225,20 @@ int ss_store_build(ss_ctx* ctx, const float* rows, const float* coverage, uint64
 int ss_store_set(ss_ctx* ctx, const uint32_t* ids, const float* unit_rows, uint64_t count, uint32_t dim);
 /* Fetch the device store (ids: count; unit_rows: count x dim). */
 int ss_store_fetch(ss_ctx* ctx, uint32_t* ids, float* unit_rows);
+/* partition_store (vecstore.hpp:169-213) of the device store: records grouped
+ * by the uniform grid cell floor((mean - bbox.min) / cell_size) of their
+ * payload means (means_xyz: 3 floats per record, store order, host memory;
+ * bbox.min over the means widened to f64, NaN skipped), cells in (x, y, z)
+ * order, records in store order within a cell, out-of-range cell indices
+ * INT_MIN (x86 conversion).  ContractError unless cell_size > 0.  The result
+ * stays on the device until ss_store_partition_fetch. */
+int ss_store_partition(ss_ctx* ctx, const float* means_xyz, double cell_size, uint64_t* n_cells);
+/* Results of the last ss_store_partition (any pointer may be NULL):
+ * cells 3 x n_cells int32 (x, y, z); offsets n_cells + 1 (first record
+ * position of each cell, then count); order count (store record index at
+ * each position); ids count and rows count x dim in cell order; bbox_min 3. */
+int ss_store_partition_fetch(ss_ctx* ctx, int32_t* cells, uint64_t* offsets, uint32_t* order, uint32_t* ids,
+                             float* rows, double* bbox_min);
 /* query_topk (vecstore.hpp:121-132) for nq queries (raw, un-normalized):
  * out_ids/out_sims nq x k; out_counts[q] = min(k, count). */
 int ss_query_topk(ss_ctx* ctx, const float* queries, uint32_t nq, uint32_t k, uint32_t* out_ids, float* out_sims,

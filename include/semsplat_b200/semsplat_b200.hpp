@@ -13,7 +13,8 @@
 //   semsplat::query_topk(...)              vecstore.hpp:121   -> b200::query_topk
 //   semsplat::query_threshold(...)         vecstore.hpp:135   -> b200::query_threshold
 //   semsplat::run_query(...)               query.hpp:102     -> b200::run_query
-//   (device store -> host VectorStore for partition_store / snapshots: b200::fetch_store)
+//   semsplat::partition_store(...)        vecstore.hpp:169   -> b200::partition_store (device grouping)
+//   (device store -> host VectorStore for snapshots / select_partitions: b200::fetch_store)
 //
 // All compute runs in the sm_100a kernels behind the C ABI
 // (include/semsplat_b200.h); this header only marshals the reference's types.
@@ -518,6 +519,47 @@ inline VectorStore fetch_store(const DeviceStore& store) {
         out.add_record(ids[i], std::vector<float>(rows.begin() + i * store.dim, rows.begin() + (i + 1) * store.dim),
                        store.payloads.size() == store.count ? store.payloads[i] : Gaussian3D{});
     return out;
+}
+
+// vecstore.hpp:169-213: cell keys, the (x, y, z)-ordered grouping and the
+// row gather run on the device; the snapshots are the reference's own types
+// (bounds from the reference's f64 expressions on the device bbox.min).
+inline std::vector<PartitionSnapshot> partition_store(const DeviceStore& store, double cell_size) {
+    if (!(cell_size > 0)) throw ContractError("partition_store: cell_size must be positive");
+    if (store.count == 0) return {};
+    if (store.payloads.size() != store.count) throw ContractError("partition_store: the store has no payloads");
+    std::vector<float> means(3 * store.count);
+    for (size_t i = 0; i < store.count; ++i)
+        for (int a = 0; a < 3; ++a) means[3 * i + a] = store.payloads[i].mean[a];
+    Device& d = Device::get(store.device);
+    std::lock_guard<std::mutex> lock(d.mutex());
+    uint64_t nc = 0;
+    check(ss_store_partition(d.ctx(), means.data(), cell_size, &nc));
+    std::vector<int32_t> cells(3 * nc);
+    std::vector<uint64_t> offs(nc + 1);
+    std::vector<uint32_t> order(store.count), ids(store.count);
+    std::vector<float> rows(store.count * store.dim);
+    double bmin[3];
+    check(ss_store_partition_fetch(d.ctx(), cells.data(), offs.data(), order.data(), ids.data(), rows.data(), bmin));
+    Aabb bbox;
+    bbox.min = Eigen::Vector3d(bmin[0], bmin[1], bmin[2]);
+    std::vector<PartitionSnapshot> snapshots;
+    snapshots.reserve(nc);
+    for (uint64_t c = 0; c < nc; ++c) {
+        PartitionSnapshot snap;
+        const int32_t kx = cells[3 * c], ky = cells[3 * c + 1], kz = cells[3 * c + 2];
+        snap.cell = {kx, ky, kz};
+        snap.bounds.min = bbox.min + cell_size * Eigen::Vector3d(kx, ky, kz);
+        snap.bounds.max = bbox.min + cell_size * Eigen::Vector3d(kx + 1, ky + 1, kz + 1);
+        snap.store = VectorStore(store.dim);
+        snap.store.reserve(offs[c + 1] - offs[c]);
+        for (uint64_t j = offs[c]; j < offs[c + 1]; ++j)
+            snap.store.add_record(ids[j],
+                                  std::vector<float>(rows.begin() + j * store.dim, rows.begin() + (j + 1) * store.dim),
+                                  store.payloads[order[j]]);
+        snapshots.push_back(std::move(snap));
+    }
+    return snapshots;
 }
 
 // vecstore.hpp:121-132

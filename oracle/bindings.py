@@ -322,6 +322,7 @@ class Ref:
         L.ssref_normalized_copy.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p]
         L.ssref_build_store.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p,
                                         C.c_void_p]
+        L.ssref_partition_store.argtypes = [C.c_void_p] * 3 + [C.c_uint64, C.c_uint32, C.c_double] + [C.c_void_p] * 6
         self.L = L
 
     def _chk(self, rc):
@@ -512,3 +513,22 @@ class Ref:
         self._chk(self.L.ssref_query_threshold(_p(ids), _p(rows), ids.shape[0], rows.shape[1], _p(q),
                                                C.c_float(tau), _p(oid), _p(osim), C.byref(cnt)))
         return oid[:cnt.value].copy(), osim[:cnt.value].copy()
+
+    def partition_store(self, ids, rows, means, cell_size):
+        """vecstore.hpp:169-213 on a store with payload means: (cells [c,3],
+        bounds [c,6], offsets [c+1], ids, rows) in the reference's order."""
+        ids = np.ascontiguousarray(ids, np.uint32)
+        rows = np.ascontiguousarray(rows, np.float32)
+        means = np.ascontiguousarray(means, np.float32)
+        n = ids.shape[0]
+        cap = max(n, 1)
+        nc = C.c_uint64()
+        cells = np.zeros((cap, 3), np.int32)
+        bounds = np.zeros((cap, 6), np.float64)
+        offs = np.zeros(cap + 1, np.uint64)
+        oid = np.zeros(cap, np.uint32)
+        orow = np.zeros((cap, rows.shape[1]), np.float32)
+        self._chk(self.L.ssref_partition_store(_p(ids), _p(rows), _p(means), n, rows.shape[1], C.c_double(cell_size),
+                                               C.byref(nc), _p(cells), _p(bounds), _p(offs), _p(oid), _p(orow)))
+        c = nc.value
+        return cells[:c], bounds[:c], offs[:c + 1], oid[:n], orow[:n]

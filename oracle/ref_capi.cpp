@@ -459,6 +459,44 @@ int ssref_query_threshold(const uint32_t* ids, const float* unit_rows, uint64_t 
     });
 }
 
+// vecstore.hpp:169-213 partition_store over records with payload means
+// (means: 3 floats per record).  Outputs sized for count cells/records:
+// cells 3 x n_cells, bounds 6 x n_cells (min xyz, max xyz), offsets
+// n_cells + 1, ids / rows in cell order.
+int ssref_partition_store(const uint32_t* ids, const float* rows, const float* means, uint64_t count, uint32_t dim,
+                          double cell_size, uint64_t* n_cells, int32_t* cells, double* bounds, uint64_t* offsets,
+                          uint32_t* out_ids, float* out_rows) {
+    return guarded([&] {
+        VectorStore store(dim);
+        store.reserve(count);
+        std::vector<float> v(dim);
+        for (uint64_t i = 0; i < count; ++i) {
+            std::memcpy(v.data(), rows + i * dim, dim * sizeof(float));
+            Gaussian3D g;
+            g.id = ids[i];
+            g.mean = {means[3 * i], means[3 * i + 1], means[3 * i + 2]};
+            store.add_record(ids[i], v, g);
+        }
+        const std::vector<PartitionSnapshot> snaps = partition_store(store, cell_size);
+        *n_cells = snaps.size();
+        uint64_t pos = 0;
+        for (size_t c = 0; c < snaps.size(); ++c) {
+            const PartitionSnapshot& sn = snaps[c];
+            for (int a = 0; a < 3; ++a) {
+                cells[3 * c + a] = sn.cell[a];
+                bounds[6 * c + a] = sn.bounds.min[a];
+                bounds[6 * c + 3 + a] = sn.bounds.max[a];
+            }
+            offsets[c] = pos;
+            for (size_t i = 0; i < sn.store.count(); ++i, ++pos) {
+                out_ids[pos] = sn.store.id_at(i);
+                std::memcpy(out_rows + pos * dim, sn.store.vector_at(i), dim * sizeof(float));
+            }
+        }
+        offsets[snaps.size()] = pos;
+    });
+}
+
 uint32_t ssref_hardware_threads() { return std::thread::hardware_concurrency(); }
 
 } // extern "C"

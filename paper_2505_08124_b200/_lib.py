@@ -90,6 +90,8 @@ def lib() -> C.CDLL:
         "ss_store_build": (i32, [vp, pf, pf, u64, u32, pu64]),
         "ss_store_set": (i32, [vp, pu32, pf, u64, u32]),
         "ss_store_fetch": (i32, [vp, pu32, pf]),
+        "ss_store_partition": (i32, [vp, pf, C.c_double, pu64]),
+        "ss_store_partition_fetch": (i32, [vp, vp, pu64, pu32, pu32, pf, pd]),
         "ss_query_topk": (i32, [vp, pf, u32, u32, pu32, pf, pu64]),
         "ss_query_threshold": (i32, [vp, pf, f32, pu32, pf, u64, pu64]),
         "ss_profile_enable": (i32, [vp, i32]),
@@ -379,6 +381,27 @@ class Context:
         rows = np.zeros((cnt, dim), np.float32)
         check(self._L.ss_store_fetch(self.h, _ptr(ids, C.c_uint32), _ptr(rows, C.c_float)))
         return ids, rows
+
+    def store_partition(self, means, cell_size: float):
+        """vecstore.hpp:169-213 on the device store: (cells [c, 3] int32, offsets
+        [c + 1], order [count] store record per position, ids, rows, bbox_min [3])."""
+        cnt, dim = self._store
+        means = np.ascontiguousarray(means, np.float32).reshape(cnt, 3)
+        nc = C.c_uint64()
+        check(self._L.ss_store_partition(self.h, _ptr(means, C.c_float), C.c_double(cell_size), C.byref(nc)))
+        c = nc.value
+        cells = np.zeros((max(c, 1), 3), np.int32)
+        offs = np.zeros(c + 1, np.uint64)
+        order = np.zeros(max(cnt, 1), np.uint32)
+        ids = np.zeros(max(cnt, 1), np.uint32)
+        rows = np.zeros((max(cnt, 1), dim), np.float32)
+        bmin = np.zeros(3, np.float64)
+        check(self._L.ss_store_partition_fetch(self.h, cells.ctypes.data_as(C.c_void_p), _ptr(offs, C.c_uint64),
+                                               _ptr(order, C.c_uint32), _ptr(ids, C.c_uint32), _ptr(rows, C.c_float),
+                                               _ptr(bmin, C.c_double)))
+        if c == 0:
+            offs = np.zeros(0, np.uint64)
+        return cells[:c], offs, order[:cnt], ids[:cnt], rows[:cnt], bmin
 
     def query_topk(self, queries, k: int):
         q = np.ascontiguousarray(queries, np.float32)

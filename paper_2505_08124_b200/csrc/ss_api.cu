@@ -236,6 +236,10 @@ struct ss_ctx {
     uint32_t store_dim = 0;
     // tensor-core query path: fp16 copy of the store, coarse scores, candidates
     ss::DevBuf store_half, qhalf, tc_scores, tc_thr, cand, cand_count, cand_sim;
+    ss::DevBuf part_buf, part_means; // partition_store scratch + the records' means
+    ss::PartitionScratch part{};
+    uint64_t part_cells = 0;         // cells of the last ss_store_partition
+    double part_min[3] = {0, 0, 0};  // its bbox.min
     bool store_half_ok = false;
     // upper bound of the store's row norms (1 for build_store's unit rows):
     // the tensor-core query's error margin scales with it
@@ -1028,7 +1032,7 @@ void ss_destroy(ss_ctx* c) {
     if (c->cstream) cudaStreamSynchronize(c->cstream);
     ss::DevBuf* bufs[] = {&c->mean_op, &c->scale, &c->quat, &c->cov3, &c->cub_tmp, &c->num_sel, &c->info, &c->vstat, &c->union_list, &c->union_count, &c->pix_count,
                           &c->pix_offset, &c->entries, &c->per_pixel_total, &c->alpha, &c->color, &c->image, &c->counters, &c->sums_buf,
-                          &c->totals_buf, &c->store_rows, &c->store_ids, &c->qbuf, &c->qnorm, &c->scores,
+                          &c->totals_buf, &c->store_rows, &c->store_ids, &c->part_buf, &c->part_means, &c->qbuf, &c->qnorm, &c->scores,
                           &c->topk_ids, &c->topk_sims, &c->sel_flags, &c->thr_keys, &c->thr_keys_sorted, &c->thr_ids,
                           &c->thr_ids_sorted, &c->zero_flag, &c->store_half, &c->qhalf, &c->tc_scores, &c->tc_thr,
                           &c->cand, &c->cand_count, &c->cand_sim};
@@ -1542,6 +1546,91 @@ int ss_store_fetch(ss_ctx* c, uint32_t* ids, float* unit_rows) {
             SS_CUDA(cudaMemcpy(ids, c->store_ids.p, c->store_count * 4, cudaMemcpyDeviceToHost));
         if (unit_rows && c->store_count)
             SS_CUDA(cudaMemcpy(unit_rows, c->store_rows.p, c->store_count * c->store_dim * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
+// vecstore.hpp:169-213 partition_store of the device store
+int ss_store_partition(ss_ctx* c, const float* means_xyz, double cell_size, uint64_t* n_cells) {
+    return guarded([&] {
+        if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
+        if (!(cell_size > 0)) throw Error(SS_ERR_CONTRACT, "partition_store: cell_size must be positive");
+        set_device(c);
+        const uint64_t n = c->store_count;
+        c->part_cells = 0;
+        if (n_cells) *n_cells = 0;
+        if (n == 0) return;
+        if (n >= (1ull << 31)) throw Error(SS_ERR_CONTRACT, "partition_store: more than 2^31 records");
+        cudaStream_t s = c->stream;
+        const uint32_t dim = c->store_dim;
+        auto* means = static_cast<float*>(c->part_means.ensure(n * 12));
+        SS_CUDA(cudaMemcpyAsync(means, means_xyz, n * 12, cudaMemcpyHostToDevice, s));
+        // carve the scratch out of one allocation (256-byte aligned pieces)
+        const size_t tmp = ss::partition_tmp_bytes(n);
+        const size_t sizes[] = {24, n * 8, n * 8, n * 4, n * 4, n * 4, n * 4, n * 4, n * 4, n, n * 4, 16, n * 12,
+                                (n + 1) * 8, n * dim * 4ull, n * 4, tmp};
+        size_t total = 0;
+        for (size_t z : sizes) total += (z + 255) / 256 * 256;
+        char* b = static_cast<char*>(c->part_buf.ensure(total));
+        void* piece[17];
+        for (int i = 0; i < 17; ++i) {
+            piece[i] = b;
+            b += (sizes[i] + 255) / 256 * 256;
+        }
+        ss::PartitionScratch& w = c->part;
+        w.mn3 = static_cast<unsigned long long*>(piece[0]);
+        w.yz = static_cast<unsigned long long*>(piece[1]);
+        w.yz_s = static_cast<unsigned long long*>(piece[2]);
+        w.kx = static_cast<uint32_t*>(piece[3]);
+        w.kx_p = static_cast<uint32_t*>(piece[4]);
+        w.kx_s = static_cast<uint32_t*>(piece[5]);
+        w.idx = static_cast<uint32_t*>(piece[6]);
+        w.perm1 = static_cast<uint32_t*>(piece[7]);
+        w.perm2 = static_cast<uint32_t*>(piece[8]);
+        w.head = static_cast<uint8_t*>(piece[9]);
+        w.heads = static_cast<uint32_t*>(piece[10]);
+        w.n_heads = static_cast<int*>(piece[11]);
+        w.cells = static_cast<int32_t*>(piece[12]);
+        w.offsets = static_cast<uint64_t*>(piece[13]);
+        w.out_rows = static_cast<float*>(piece[14]);
+        w.out_ids = static_cast<uint32_t*>(piece[15]);
+        w.tmp = piece[16];
+        w.tmp_bytes = tmp;
+        own_launch(c,
+                   ss::launch_store_partition(means, c->store_rows.as<float>(), c->store_ids.as<uint32_t>(), n, dim,
+                                              cell_size, w, s),
+                   SS_K_QUERY, 9);
+        c->launches_cub += 3;
+        unsigned long long mn[3];
+        int nh = 0;
+        SS_CUDA(cudaMemcpyAsync(mn, w.mn3, 24, cudaMemcpyDeviceToHost, s));
+        SS_CUDA(cudaMemcpyAsync(&nh, w.n_heads, 4, cudaMemcpyDeviceToHost, s));
+        SS_CUDA(cudaStreamSynchronize(s));
+        for (int a = 0; a < 3; ++a) {
+            // inverse of the ordered-key map; all-NaN axes keep Aabb's initial DBL_MAX
+            const unsigned long long k = mn[a];
+            const unsigned long long bits = k == ~0ull ? 0x7fefffffffffffffull
+                                                       : ((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k);
+            std::memcpy(&c->part_min[a], &bits, 8);
+        }
+        c->part_cells = (uint64_t)nh;
+        if (n_cells) *n_cells = (uint64_t)nh;
+    });
+}
+
+int ss_store_partition_fetch(ss_ctx* c, int32_t* cells, uint64_t* offsets, uint32_t* order, uint32_t* ids,
+                             float* rows, double* bbox_min) {
+    return guarded([&] {
+        if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
+        set_device(c);
+        const uint64_t n = c->store_count, nc = c->part_cells;
+        if (bbox_min) std::memcpy(bbox_min, c->part_min, 24);
+        if (!nc) return;
+        const ss::PartitionScratch& w = c->part;
+        if (cells) SS_CUDA(cudaMemcpy(cells, w.cells, nc * 12, cudaMemcpyDeviceToHost));
+        if (offsets) SS_CUDA(cudaMemcpy(offsets, w.offsets, (nc + 1) * 8, cudaMemcpyDeviceToHost));
+        if (order) SS_CUDA(cudaMemcpy(order, w.perm2, n * 4, cudaMemcpyDeviceToHost));
+        if (ids) SS_CUDA(cudaMemcpy(ids, w.out_ids, n * 4, cudaMemcpyDeviceToHost));
+        if (rows) SS_CUDA(cudaMemcpy(rows, w.out_rows, n * c->store_dim * 4ull, cudaMemcpyDeviceToHost));
     });
 }
 

@@ -10,7 +10,10 @@
 
 #include <cub/block/block_scan.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
+#include <thrust/iterator/counting_iterator.h>
 #include <cub/iterator/transform_input_iterator.cuh>
 
 #include "ss_kernels.cuh"
@@ -1485,6 +1488,102 @@ __global__ void __launch_bounds__(256) touched_compact_kernel(const uint32_t* to
     }
 }
 
+// ---------------------------------------------------- partition_store
+// vecstore.hpp:169-213.  Doubles map to u64 keys whose unsigned order is the
+// numeric order (NaN means are skipped, as cwiseMin/cwiseMax skip them:
+// std::min(m, NaN) keeps m, scene.hpp:43-46).
+__device__ __forceinline__ unsigned long long dkey(double v) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double dkey_inv(unsigned long long k) {
+    return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k));
+}
+
+// bbox.min over the records' f32 means widened to f64 (Aabb::expand)
+__global__ void __launch_bounds__(256) bbox_min_kernel(const float* means, uint64_t n, unsigned long long* mn3) {
+    unsigned long long m[3] = {~0ull, ~0ull, ~0ull};
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        for (int a = 0; a < 3; ++a) {
+            const double v = (double)means[3 * i + a];
+            if (v == v) m[a] = min(m[a], dkey(v));
+        }
+    for (int a = 0; a < 3; ++a) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m[a] = min(m[a], __shfl_xor_sync(0xffffffffu, m[a], o));
+        if ((threadIdx.x & 31u) == 0 && m[a] != ~0ull) atomicMin(mn3 + a, m[a]);
+    }
+}
+
+// x86 cvttsd2si: NaN / out of range -> INT_MIN (static_cast<int32_t>(std::floor(...)) on the reference's target)
+__device__ __forceinline__ int32_t to_i32_x86(double v) {
+    if (!(v >= -2147483648.0 && v < 2147483648.0)) return INT32_MIN;
+    return (int32_t)v;
+}
+
+// cell key per record: floor((m - bbox.min) / cell_size) per axis, biased to
+// unsigned order (std::map<CellKey> compares the signed x, then y, then z);
+// yz = (y << 32) | z and x by record, idx = record index
+__global__ void __launch_bounds__(256) cell_keys_kernel(const float* means, uint64_t n,
+                                                        const unsigned long long* mn3, double cell,
+                                                        unsigned long long* yz, uint32_t* kx, uint32_t* idx) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint32_t k[3];
+    for (int a = 0; a < 3; ++a) {
+        const double lo = dkey_inv(mn3[a]);
+        const double q = __ddiv_rn(__dsub_rn((double)means[3 * i + a], lo), cell);
+        k[a] = (uint32_t)to_i32_x86(floor(q)) ^ 0x80000000u;
+    }
+    kx[i] = k[0];
+    yz[i] = ((unsigned long long)k[1] << 32) | k[2];
+    idx[i] = (uint32_t)i;
+}
+
+template <typename T>
+__global__ void gather_kernel(const T* src, const uint32_t* perm, uint64_t n, T* dst) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = src[perm[i]];
+}
+
+// heads of the cells in the sorted order
+__global__ void cell_heads_kernel(const uint32_t* kx, const unsigned long long* yz, uint64_t n, uint8_t* head) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    head[i] = i == 0 || kx[i] != kx[i - 1] || yz[i] != yz[i - 1];
+}
+
+// per cell: (x, y, z) signed and its first position
+__global__ void cell_list_kernel(const uint32_t* kx, const unsigned long long* yz, const uint32_t* heads,
+                                 const int* n_heads, int32_t* cells, uint64_t* offsets, uint64_t n) {
+    const int c = (int)(blockIdx.x * blockDim.x + threadIdx.x);
+    const int nc = *n_heads;
+    if (c > nc) return;
+    if (c == nc) {
+        offsets[c] = n;
+        return;
+    }
+    const uint32_t h = heads[c];
+    cells[3 * c + 0] = (int32_t)(kx[h] ^ 0x80000000u);
+    cells[3 * c + 1] = (int32_t)((uint32_t)(yz[h] >> 32) ^ 0x80000000u);
+    cells[3 * c + 2] = (int32_t)((uint32_t)yz[h] ^ 0x80000000u);
+    offsets[c] = h;
+}
+
+// rows and ids gathered into cell order (warp per record)
+__global__ void __launch_bounds__(256) gather_records_kernel(const float* rows, const uint32_t* ids,
+                                                             const uint32_t* order, uint64_t n, uint32_t dim,
+                                                             float* out_rows, uint32_t* out_ids) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t w0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t j = w0; j < n; j += nw) {
+        const uint32_t src = order[j];
+        if (lane == 0) out_ids[j] = ids[src];
+        for (uint32_t d = lane; d < dim; d += 32) out_rows[j * dim + d] = rows[(uint64_t)src * dim + d];
+    }
+}
+
 // Inverse of threshold_keys_kernel for the first `take` sorted keys: query q's
 // ranked (id, sim) written straight into its result row (no host round trip).
 __global__ void decode_keys_kernel(const unsigned long long* keys, uint64_t take, uint32_t* ids, float* sims) {
@@ -1810,6 +1909,44 @@ cudaError_t launch_touched_compact(const uint32_t* touched, uint64_t n, uint32_t
     if (!n) return cudaSuccess;
     const uint64_t want = (n + 1023u) / 1024u; // 256 threads x 4 ids per block
     touched_compact_kernel<<<(unsigned)std::min<uint64_t>(want, 148ull * 8u), 256, 0, s>>>(touched, n, gen, list, count);
+    return cudaGetLastError();
+}
+
+size_t partition_tmp_bytes(uint64_t n) {
+    size_t a = 0, b = 0, c = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, a, (const unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                                    (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n, 0, 64);
+    cub::DeviceRadixSort::SortPairs(nullptr, b, (const uint32_t*)nullptr, (uint32_t*)nullptr, (const uint32_t*)nullptr,
+                                    (uint32_t*)nullptr, (int)n, 0, 32);
+    thrust::counting_iterator<uint32_t> it(0);
+    cub::DeviceSelect::Flagged(nullptr, c, it, (const uint8_t*)nullptr, (uint32_t*)nullptr, (int*)nullptr, (int)n);
+    return std::max(a, std::max(b, c));
+}
+
+cudaError_t launch_store_partition(const float* means, const float* rows, const uint32_t* ids, uint64_t n,
+                                   uint32_t dim, double cell, const PartitionScratch& w, cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    cudaError_t e = cudaMemsetAsync(w.mn3, 0xff, 3 * sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return e;
+    bbox_min_kernel<<<(unsigned)std::min<uint64_t>(blocks_for(n, 256), 148ull * 8u), 256, 0, s>>>(means, n, w.mn3);
+    cell_keys_kernel<<<blocks_for(n, 256), 256, 0, s>>>(means, n, w.mn3, cell, w.yz, w.kx, w.idx);
+    // stable LSD: (y, z) first, then x -> cells in (x, y, z) order, records in store order within a cell
+    size_t tb = w.tmp_bytes;
+    e = cub::DeviceRadixSort::SortPairs(w.tmp, tb, w.yz, w.yz_s, w.idx, w.perm1, (int)n, 0, 64, s);
+    if (e != cudaSuccess) return e;
+    gather_kernel<uint32_t><<<blocks_for(n, 256), 256, 0, s>>>(w.kx, w.perm1, n, w.kx_p);
+    tb = w.tmp_bytes;
+    e = cub::DeviceRadixSort::SortPairs(w.tmp, tb, w.kx_p, w.kx_s, w.perm1, w.perm2, (int)n, 0, 32, s);
+    if (e != cudaSuccess) return e;
+    gather_kernel<unsigned long long><<<blocks_for(n, 256), 256, 0, s>>>(w.yz, w.perm2, n, w.yz_s);
+    cell_heads_kernel<<<blocks_for(n, 256), 256, 0, s>>>(w.kx_s, w.yz_s, n, w.head);
+    tb = w.tmp_bytes;
+    thrust::counting_iterator<uint32_t> it(0);
+    e = cub::DeviceSelect::Flagged(w.tmp, tb, it, w.head, w.heads, w.n_heads, (int)n, s);
+    if (e != cudaSuccess) return e;
+    cell_list_kernel<<<blocks_for(n + 1, 256), 256, 0, s>>>(w.kx_s, w.yz_s, w.heads, w.n_heads, w.cells, w.offsets,
+                                                            n);
+    gather_records_kernel<<<warp_grid(n), 256, 0, s>>>(rows, ids, w.perm2, n, dim, w.out_rows, w.out_ids);
     return cudaGetLastError();
 }
 

@@ -114,6 +114,25 @@ cudaError_t launch_threshold_keys(const float* scores, const uint32_t* ids, uint
 // list (count starts at 0) <- every g < n with touched[g] == gen (the compositor's stamps)
 cudaError_t launch_touched_compact(const uint32_t* touched, uint64_t n, uint32_t gen, uint32_t* list,
                                   unsigned long long* count, cudaStream_t s);
+// partition_store (vecstore.hpp:169-213) scratch, n records
+struct PartitionScratch {
+    unsigned long long* mn3;        // [3] bbox.min as ordered keys
+    unsigned long long *yz, *yz_s;  // [n] (y << 32 | z) by record; sorted scratch, then in cell order
+    uint32_t *kx, *kx_p, *kx_s;     // [n] x by record, permuted, sorted
+    uint32_t *idx, *perm1, *perm2;  // [n] iota, after the (y, z) pass, final record order
+    uint8_t* head;                  // [n]
+    uint32_t* heads;                // [n] first position of every cell
+    int* n_heads;                   // cells
+    int32_t* cells;                 // [3 n] (x, y, z) per cell
+    uint64_t* offsets;              // [n + 1] first position per cell, then n
+    float* out_rows;                // [n x dim] rows in cell order
+    uint32_t* out_ids;              // [n]
+    void* tmp;
+    size_t tmp_bytes;
+};
+size_t partition_tmp_bytes(uint64_t n);
+cudaError_t launch_store_partition(const float* means, const float* rows, const uint32_t* ids, uint64_t n,
+                                   uint32_t dim, double cell, const PartitionScratch& w, cudaStream_t s);
 // first `take` sorted threshold keys -> (id, sim) result row, on the device
 cudaError_t launch_decode_keys(const unsigned long long* keys, uint64_t take, uint32_t* ids, float* sims,
                                cudaStream_t s);

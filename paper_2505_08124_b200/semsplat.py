@@ -324,3 +324,34 @@ def query_threshold(store: VectorStore, q, tau: float):
     if q.shape[0] != store.dim():
         raise ContractError("query dimension differs from store dimension")
     return store.ctx.query_threshold(q, float(tau))
+
+
+class PartitionSnapshot:
+    """One grid cell of the partitioned store (vecstore.hpp:160-164): cell index,
+    bounds (min, max as f64 3-vectors) and the cell's ids / unit rows."""
+
+    def __init__(self, cell, bounds_min, bounds_max, ids, rows):
+        self.cell = cell
+        self.bounds_min = bounds_min
+        self.bounds_max = bounds_max
+        self.ids = ids
+        self.rows = rows
+
+
+def partition_store(store: VectorStore, means, cell_size: float) -> list:
+    """vecstore.hpp:169-213 on the device: records grouped by the uniform grid
+    cell of their payload means (means: [count, 3] in store order), cells in
+    (x, y, z) order, records in store order within a cell; bounds = bbox.min
+    + cell_size * cell (and + 1), the reference's f64 expressions."""
+    if not (cell_size > 0):
+        raise ContractError("partition_store: cell_size must be positive")
+    if store.count() == 0:
+        return []
+    cells, offs, _order, ids, rows, bmin = store.ctx.store_partition(means, float(cell_size))
+    out = []
+    for c in range(cells.shape[0]):
+        lo, hi = int(offs[c]), int(offs[c + 1])
+        k = cells[c].astype(np.float64)
+        out.append(PartitionSnapshot(tuple(int(v) for v in cells[c]), bmin + cell_size * k, bmin + cell_size * (k + 1.0),
+                                     ids[lo:hi], rows[lo:hi]))
+    return out

@@ -254,6 +254,46 @@ int main() {
         CHECK(rq);
     }
 
+    // --- partition_store (vecstore.hpp:169-213): device grouping vs the reference, incl. boundary means
+    {
+        const uint32_t dim = 16;
+        std::mt19937_64 rng(91);
+        VectorStore store(dim);
+        for (uint32_t i = 0; i < 3000; ++i) {
+            std::vector<float> v(dim);
+            for (auto& x : v) x = float(urand(rng, -1, 1));
+            Gaussian3D g;
+            g.id = 5000 - i;
+            // means on a 0.25 lattice land exactly on cell boundaries for cell sizes 0.5 / 1.0
+            g.mean = {float(std::floor(urand(rng, -12, 12)) * 0.25), float(urand(rng, -3, 3)),
+                      float(i % 7 == 0 ? 1.0 : urand(rng, 0, 2))};
+            store.add_record(g.id, normalized_copy(v.data(), dim), g);
+        }
+        const b200::DeviceStore ds = b200::upload_store(store);
+        bool pok = true;
+        for (double cell : {0.5, 1.0, 0.37, 1e-9}) {
+            const auto a = partition_store(store, cell);
+            const auto b = b200::partition_store(ds, cell);
+            pok = pok && a.size() == b.size();
+            for (size_t c = 0; pok && c < a.size(); ++c) {
+                pok = a[c].cell == b[c].cell && a[c].bounds.min == b[c].bounds.min &&
+                      a[c].bounds.max == b[c].bounds.max && a[c].store.count() == b[c].store.count();
+                for (size_t i = 0; pok && i < a[c].store.count(); ++i)
+                    pok = a[c].store.id_at(i) == b[c].store.id_at(i) &&
+                          std::memcmp(a[c].store.vector_at(i), b[c].store.vector_at(i), dim * sizeof(float)) == 0 &&
+                          a[c].store.payload_at(i).mean == b[c].store.payload_at(i).mean;
+            }
+        }
+        CHECK(pok);
+        bool contract = false;
+        try {
+            b200::partition_store(ds, 0.0);
+        } catch (const ContractError&) {
+            contract = true;
+        }
+        CHECK(contract);
+    }
+
     fs::remove_all(tmp);
     std::printf("dropin: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail == 0 ? 0 : 1;

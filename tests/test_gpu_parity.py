@@ -736,3 +736,31 @@ def test_query_tensor_core_non_unit_store_vs_oracle(gpu_ctx, oracle):
     rows[17] *= 1.0e5  # beyond the fp16-safe bound: the exact scan answers
     _tc_vs_oracle(gpu_ctx, oracle, ids, rows, q, 10)
     assert gpu_ctx.query_stats()["tc_queries"] == after["tc_queries"]
+
+
+@pytest.mark.parametrize("cell", [0.5, 1.0, 0.37, 1e-9])
+def test_partition_store_vs_reference(gpu_ctx, ref, cell):
+    """vecstore.hpp:169-213 partition_store on the device: cells, bounds, per-cell
+    ids / rows / order identical to the reference build -- means on exact cell
+    boundaries (half-open intervals), a NaN mean (skipped by the bbox, cell
+    INT_MIN), and a cell size whose indices overflow int32 (x86 INT_MIN)."""
+    from paper_2505_08124_b200 import semsplat
+    rng = np.random.default_rng(int(cell * 1000) + 3)
+    n, dim = 4000, 24
+    ids = rng.permutation(1 << 20)[:n].astype(np.uint32)
+    rows = rng.standard_normal((n, dim)).astype(np.float32)
+    means = np.stack([np.floor(rng.uniform(-12, 12, n)) * 0.25, rng.uniform(-3, 3, n),
+                      np.where(np.arange(n) % 7 == 0, 1.0, rng.uniform(0, 2, n))], 1).astype(np.float32)
+    means[11, 1] = np.nan
+    store = semsplat.VectorStore.from_unit_rows(ids, rows)
+    snaps = semsplat.partition_store(store, means, cell)
+    rc, rb, ro, rids, rrows = ref.partition_store(ids, rows, means, cell)
+    assert len(snaps) == rc.shape[0]
+    for c, sn in enumerate(snaps):
+        assert sn.cell == tuple(int(v) for v in rc[c])
+        assert sn.bounds_min.tobytes() == rb[c, :3].tobytes() and sn.bounds_max.tobytes() == rb[c, 3:].tobytes()
+        lo, hi = int(ro[c]), int(ro[c + 1])
+        assert np.array_equal(sn.ids, rids[lo:hi])
+        assert sn.rows.tobytes() == rrows[lo:hi].tobytes()
+    with pytest.raises(Exception):
+        semsplat.partition_store(store, means, 0.0)
