@@ -21,6 +21,7 @@ import argparse
 import json
 import math
 import os
+import shutil
 import subprocess
 import sys
 import tempfile
@@ -31,6 +32,7 @@ from pathlib import Path
 import numpy as np
 
 ROOT = Path(__file__).resolve().parent
+DROPIN_BENCH = ROOT / "tests" / "cpp" / "_build" / "bench_dropin"  # built where the reference headers exist
 sys.path.insert(0, str(ROOT))
 
 from harness.workload import CONFIGS, make_bench_workload, write_reference_dataset  # noqa: E402
@@ -548,6 +550,35 @@ def main():
         except Exception as ex:  # reported, not fatal
             cpu = {"value": None, "unit": "views/s", "cores": None, "kind": "unavailable", "sample": str(ex)}
 
+    # drop-in e2e leg: the whole c4 dataset in the reference's on-disk formats
+    # (scene PLY, manifest, cameras, per-view RLE masks and CLIP files), run by
+    # tests/cpp/_build/bench_dropin through b200::encode_scene -- the call a
+    # reference user makes -- with file parsing and the host table included
+    e2e_dropin = None
+    if rank == 0 and world == 1 and not args.no_e2e and DROPIN_BENCH.exists():
+        try:
+            from paper_2505_08124_b200 import formats
+            tmp = tempfile.mkdtemp(prefix="ss_dropin_")
+            mp = write_reference_dataset(wl, tmp)
+            sp = os.path.join(tmp, "scene.ply")
+            s_ = wl.scene
+            formats.save_scene_arrays(sp, s_.mean, s_.scale, s_.quat_xyzw, s_.opacity, s_.color)
+            env = dict(os.environ, CUDA_VISIBLE_DEVICES=str(local))
+            r = subprocess.run([str(DROPIN_BENCH), sp, mp, "1", "0", "3"], capture_output=True, text=True,
+                               timeout=900, env=env)
+            if r.returncode == 0:
+                d = json.loads(r.stdout.strip().splitlines()[-1])
+                e2e_dropin = {"value": d["views"] / d["seconds"], "unit": "views/s",
+                              "value_without_parse": d["views"] / d["encode_seconds"], **d,
+                              "path": "b200::encode_scene (C++ drop-in) on the on-disk dataset: load_scene + "
+                                      "load_manifest, per-view mask/CLIP files read inside encode_scene, "
+                                      "table in host memory; best of 3 runs"}
+            else:
+                e2e_dropin = {"error": (r.stdout + r.stderr)[-400:]}
+            shutil.rmtree(tmp, ignore_errors=True)
+        except Exception as ex:  # reported, not fatal
+            e2e_dropin = {"error": f"{type(ex).__name__}: {ex}"}
+
     # eval leg (eval.hpp:122-158): arg-max class per covered row of the table
     # shard just produced (device-resident), 16 synthetic class embeddings
     evl = None
@@ -614,6 +645,7 @@ def main():
             "geometry_per_view": {k: counters[k] / max(counters["views"], 1) for k in
                                   ("n_vis", "instances", "touched", "pairs")},
             "e2e": e2e,
+            "e2e_dropin": e2e_dropin,
             "cpu_baseline": cpu,
             "parity": parity,
             "clocks": clk.summary(),

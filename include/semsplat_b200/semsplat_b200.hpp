@@ -21,12 +21,17 @@
 #pragma once
 
 #include <cstring>
+#include <future>
 #include <memory>
+#include <optional>
 #include <mutex>
 #include <string>
 #include <thread>
 #include <unordered_map>
 #include <vector>
+#ifdef __linux__
+#include <sys/mman.h>
+#endif
 
 #include "../semsplat_b200.h"
 #include "semsplat/pipeline.hpp"
@@ -251,6 +256,26 @@ inline std::vector<Projected2D> project_all(const GaussianScene& scene, const Ca
 }
 
 namespace detail {
+// EmbeddingTable(n, dim) with its row storage on 2 MB pages where the kernel
+// allows it (THP "madvise" mode): the 4 GB c4 table is then zero-filled at
+// memset speed instead of taking a million 4 KB page faults (1.7 s measured).
+// Same object as the reference's constructor builds.
+inline EmbeddingTable make_table(uint64_t n, uint32_t dim) {
+    EmbeddingTable t;
+    t.gaussian_count = n;
+    t.dim = dim;
+    t.embeddings.reserve(n * dim);
+#ifdef __linux__
+    constexpr uintptr_t kHuge = uintptr_t(2) << 20;
+    const uintptr_t b = reinterpret_cast<uintptr_t>(t.embeddings.data()), e = b + n * dim * sizeof(float);
+    const uintptr_t a = (b + kHuge - 1) & ~(kHuge - 1);
+    if (e > a + kHuge) madvise(reinterpret_cast<void*>(a), (e - a) & ~(kHuge - 1), MADV_HUGEPAGE);
+#endif
+    t.embeddings.resize(n * dim, 0.0f);
+    t.coverage.assign(n, 0.0f);
+    return t;
+}
+
 // One view's masks in their on-disk encoding (RLE runs, no bitmap decode on
 // the host) and CLIP vectors, read as load_maskset / load_mask_embeddings do.
 struct ViewData {
@@ -316,6 +341,17 @@ inline EmbeddingTable encode_scene(const GaussianScene& scene, const DatasetMani
             throw DataError("image " + std::to_string(e.image_id) + ": no camera with id " +
                             std::to_string(e.camera_id));
 
+    // the host table (4.1 GB at c4, zero-filled by its constructor) is built
+    // while the devices run phase 1
+    const uint64_t n = scene.size();
+    std::optional<EmbeddingTable> table_slot;
+    std::thread table_thread([&] { table_slot.emplace(detail::make_table(n, manifest.embedding_dim)); });
+    struct JoinTable {
+        std::thread& t;
+        ~JoinTable() {
+            if (t.joinable()) t.join();
+        }
+    } join_table{table_thread};
     const int G = workers > 1 ? std::max(1, std::min<int>((int)workers, device_count())) : 1;
     std::vector<Device*> devs;
     for (int g = 0; g < G; ++g) devs.push_back(&Device::get(G == 1 ? device : g));
@@ -336,52 +372,84 @@ inline EmbeddingTable encode_scene(const GaussianScene& scene, const DatasetMani
     std::vector<size_t> worker_entries(workers, 0);
     const ss_weight_mode wmode = options.mode == WeightMode::kFalloffOnly ? SS_FALLOFF_ONLY : SS_ALPHA_COMPOSITED;
 
-    auto run_worker = [&](uint32_t rank, ss_ctx* ctx) {
-        const auto ts = std::chrono::steady_clock::now();
-        // a worker's views go to its device as one batch (views overlap in the
-        // device's pipeline lanes); host-side decoding errors stop the worker
-        // at that image, as the reference's worker_body does
+    // one batch of a worker's views read from disk (camera scaled to the raster
+    // resolution, RLE runs, CLIP rows); `failure` names the image that stopped it
+    struct Batch {
         std::vector<detail::ViewData> data;
         std::vector<ss_camera> cams;
-        for (size_t idx = 0; idx < n_img; ++idx) {
+        std::string failure;
+        size_t next = 0; // manifest index to continue from
+    };
+    constexpr size_t kBatchViews = 48;
+    auto read_batch = [&](uint32_t rank, size_t from) {
+        Batch b;
+        size_t idx = from;
+        for (; idx < n_img && b.cams.size() < kBatchViews; ++idx) {
             const bool mine = options.contiguous_batching ? (idx / block == rank) : (idx % workers == rank);
             if (!mine) continue;
             const ImageEntry& entry = manifest.images[idx];
             try {
                 const CameraPose raster_cam = camera_scaled_to(*camera_by_id.at(entry.camera_id),
                                                                manifest.raster_width, manifest.raster_height);
-                data.push_back(detail::read_view(manifest, entry));
+                b.data.push_back(detail::read_view(manifest, entry));
                 ss_camera c = to_c(raster_cam);
                 c.image_id = entry.image_id;
-                cams.push_back(c);
+                b.cams.push_back(c);
             } catch (const std::exception& ex) {
                 std::string m = ex.what();
                 const std::string pre = "image " + std::to_string(entry.image_id) + ":";
                 if (m.rfind(pre, 0) != 0) m = "image " + std::to_string(entry.image_id) + ": " + m;
-                failures[rank] = m;
+                b.failure = m;
                 break;
             }
         }
-        std::vector<ss_view_masks> vms(data.size());
-        for (size_t v = 0; v < data.size(); ++v) {
-            vms[v] = ss_view_masks{};
-            vms[v].n_masks = static_cast<uint32_t>(data[v].offs.size() - 1);
-            vms[v].mask_width = manifest.mask_width;
-            vms[v].mask_height = manifest.mask_height;
-            vms[v].flags = 0;
-            vms[v].runs = data[v].runs.data();
-            vms[v].run_offsets = data[v].offs.data();
-            vms[v].clip = data[v].clip.data();
-            vms[v].n_runs = data[v].runs.size();
-        }
+        b.next = idx;
+        return b;
+    };
+    auto run_worker = [&](uint32_t rank, ss_ctx* ctx) {
+        const auto ts = std::chrono::steady_clock::now();
+        // the worker's views go to its device batch by batch (views overlap in
+        // the device's pipeline lanes) while the next batch is read from disk;
+        // host-side decoding errors stop the worker at that image, as the
+        // reference's worker_body does
         uint64_t before[5] = {}, after[5] = {};
         check(ss_counters_read(ctx, before));
-        if (!cams.empty()) {
-            const int st = ss_encode_views(ctx, static_cast<uint32_t>(cams.size()), cams.data(), vms.data(), wmode);
-            if (st != SS_OK && failures[rank].empty()) failures[rank] = ss_last_error(); // names the image
+        size_t images = 0;
+        std::future<Batch> next = std::async(std::launch::async, read_batch, rank, size_t(0));
+        for (;;) {
+            Batch cur = next.get();
+            const bool more = cur.failure.empty() && cur.next < n_img;
+            if (more) next = std::async(std::launch::async, read_batch, rank, cur.next);
+            std::vector<ss_view_masks> vms(cur.data.size());
+            for (size_t v = 0; v < cur.data.size(); ++v) {
+                vms[v] = ss_view_masks{};
+                vms[v].n_masks = static_cast<uint32_t>(cur.data[v].offs.size() - 1);
+                vms[v].mask_width = manifest.mask_width;
+                vms[v].mask_height = manifest.mask_height;
+                vms[v].flags = 0;
+                vms[v].runs = cur.data[v].runs.data();
+                vms[v].run_offsets = cur.data[v].offs.data();
+                vms[v].clip = cur.data[v].clip.data();
+                vms[v].n_runs = cur.data[v].runs.size();
+            }
+            if (!cur.cams.empty()) {
+                const int st = ss_encode_views(ctx, static_cast<uint32_t>(cur.cams.size()), cur.cams.data(), vms.data(),
+                                               wmode);
+                if (st != SS_OK) {
+                    if (failures[rank].empty()) failures[rank] = ss_last_error(); // names the image
+                    if (more) next.wait();
+                    break;
+                }
+            }
+            images += cur.cams.size();
+            if (!cur.failure.empty()) {
+                failures[rank] = cur.failure;
+                break;
+            }
+            if (!more) break;
         }
         check(ss_counters_read(ctx, after));
-        worker_images[rank] = cams.size();
+        worker_images[rank] = images;
         worker_entries[rank] = static_cast<size_t>(after[3] - before[3]); // masked-weight (gid, mask) entries
         worker_seconds[rank] = std::chrono::duration<double>(std::chrono::steady_clock::now() - ts).count();
     };
@@ -416,8 +484,8 @@ inline EmbeddingTable encode_scene(const GaussianScene& scene, const DatasetMani
     }
     for (Device* d : devs) check(ss_synchronize(d->ctx()));
     const auto t1 = std::chrono::steady_clock::now();
-    const uint64_t n = scene.size();
-    EmbeddingTable table(n, manifest.embedding_dim);
+    table_thread.join();
+    EmbeddingTable& table = *table_slot;
     if (G == 1) {
         const uint64_t step = (chunk_rows == 0 || chunk_rows > n) ? std::max<uint64_t>(n, 1) : chunk_rows;
         for (uint64_t lo = 0; lo < n; lo += step) {
@@ -462,7 +530,7 @@ inline EmbeddingTable encode_scene(const GaussianScene& scene, const DatasetMani
         stats_out->worker_images = worker_images;
         stats_out->worker_entries = worker_entries;
     }
-    return table;
+    return std::move(table);
 }
 
 // A device-resident VectorStore: ids + unit rows on the device; the records'

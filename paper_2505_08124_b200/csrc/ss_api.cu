@@ -17,6 +17,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <thrust/iterator/counting_iterator.h>
@@ -214,6 +215,8 @@ struct ss_ctx {
     uint64_t cap_n_surv = 0;
     ss::ViewInfo* h_init = nullptr;    // pinned
     uint32_t* h_u32 = nullptr;         // pinned scratch
+    char* h_stage = nullptr;           // pinned staging for readouts into pageable memory (kStageBytes x 2)
+    cudaEvent_t stage_ev[2] = {nullptr, nullptr};
 
     // capture / render
     ss::DevBuf pix_count, pix_offset, entries, per_pixel_total, alpha, color, image;
@@ -977,6 +980,53 @@ void comm_release(ss_ctx* c) {
 
 using namespace ss;
 
+namespace {
+// Device -> pageable host copy of `bytes` (the reference's host containers are
+// plain std::vectors): chunks of kStageBytes DMA into two pinned staging
+// buffers while host threads move the previous chunk out, so the readout runs
+// at pinned-DMA speed instead of the driver's pageable path (~4x slower).
+constexpr size_t kStageBytes = 64u << 20;
+
+void copy_d2h_pageable(ss_ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    if (bytes == 0) return;
+    cudaPointerAttributes attr{};
+    const bool pinned = cudaPointerGetAttributes(&attr, dst) == cudaSuccess && attr.type == cudaMemoryTypeHost;
+    cudaGetLastError(); // unregistered pointers may set an error on older drivers
+    if (pinned || bytes < (4u << 20)) { // pinned destination, or small: the plain copy
+        SS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+        SS_CUDA(cudaStreamSynchronize(s));
+        return;
+    }
+    if (!c->h_stage) {
+        SS_CUDA(cudaMallocHost(&c->h_stage, 2 * kStageBytes));
+        for (auto& e : c->stage_ev) SS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency() / 2));
+    auto host_copy = [&](char* d, const char* sp, size_t n) {
+        const size_t per = (n + hw - 1) / hw;
+        std::vector<std::thread> th;
+        for (unsigned t = 1; t < hw && t * per < n; ++t)
+            th.emplace_back([=] { std::memcpy(d + t * per, sp + t * per, std::min(per, n - t * per)); });
+        std::memcpy(d, sp, std::min(per, n));
+        for (auto& x : th) x.join();
+    };
+    const size_t chunks = (bytes + kStageBytes - 1) / kStageBytes;
+    auto issue = [&](size_t k) {
+        const size_t off = k * kStageBytes, n = std::min(kStageBytes, bytes - off);
+        SS_CUDA(cudaMemcpyAsync(c->h_stage + (k & 1) * kStageBytes, static_cast<const char*>(src) + off, n,
+                                cudaMemcpyDeviceToHost, s));
+        SS_CUDA(cudaEventRecord(c->stage_ev[k & 1], s));
+    };
+    issue(0);
+    for (size_t k = 0; k < chunks; ++k) {
+        if (k + 1 < chunks) issue(k + 1); // its buffer was drained in iteration k - 1
+        SS_CUDA(cudaEventSynchronize(c->stage_ev[k & 1]));
+        const size_t off = k * kStageBytes, n = std::min(kStageBytes, bytes - off);
+        host_copy(static_cast<char*>(dst) + off, c->h_stage + (k & 1) * kStageBytes, n);
+    }
+}
+} // namespace
+
 extern "C" {
 
 const char* ss_last_error(void) { return ss::g_err.c_str(); }
@@ -1065,6 +1115,9 @@ void ss_destroy(ss_ctx* c) {
     }
     if (c->h_init) cudaFreeHost(c->h_init);
     if (c->h_u32) cudaFreeHost(c->h_u32);
+    if (c->h_stage) cudaFreeHost(c->h_stage);
+    for (cudaEvent_t e : c->stage_ev)
+        if (e) cudaEventDestroy(e);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
 }
@@ -1419,9 +1472,8 @@ int ss_encode_finalize(ss_ctx* c, uint64_t row_lo, uint64_t row_hi, float* rows_
             c->prof.bytes[SS_K_NORMALIZE] += (double)n * (4.0 * c->dim + 8.0);
         }
         if (!out_on_device) {
-            SS_CUDA(cudaMemcpyAsync(rows_out, d_rows, n * c->dim * 4, cudaMemcpyDeviceToHost, s));
-            SS_CUDA(cudaMemcpyAsync(coverage_out, d_cov, n * 4, cudaMemcpyDeviceToHost, s));
-            SS_CUDA(cudaStreamSynchronize(s));
+            copy_d2h_pageable(c, rows_out, d_rows, n * c->dim * 4, s);
+            copy_d2h_pageable(c, coverage_out, d_cov, n * 4, s);
         }
     });
 }
@@ -2076,10 +2128,9 @@ int ss_encode_combine(ss_ctx* c, float* rows_out, float* coverage_out, int out_o
                            SS_K_NORMALIZE);
                 c->prof.bytes[SS_K_NORMALIZE] += (double)B * (4.0 * D + 8.0);
             }
-            if (!out_on_device) {
-                SS_CUDA(cudaMemcpyAsync(rows_out + q * B * D, dr, B * D * 4, cudaMemcpyDeviceToHost, s));
-                SS_CUDA(cudaMemcpyAsync(coverage_out + q * B, dc, B * 4, cudaMemcpyDeviceToHost, s));
-                SS_CUDA(cudaStreamSynchronize(s)); // the staging buffer is reused next round
+            if (!out_on_device) { // synchronous: the staging buffer is reused next round
+                copy_d2h_pageable(c, rows_out + q * B * D, dr, B * D * 4, s);
+                copy_d2h_pageable(c, coverage_out + q * B, dc, B * 4, s);
             }
             if (collective) SS_CUDA(cudaEventRecord(c->ev_norm[buf], s));
         }

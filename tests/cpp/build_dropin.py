@@ -12,24 +12,29 @@ HERE = Path(__file__).resolve().parent
 ROOT = HERE.parents[1]
 REF_INCLUDE = Path("/root/reference/proj/include")
 OUT = HERE / "_build" / "dropin_test"
+BENCH = HERE / "_build" / "bench_dropin"  # bench.py's drop-in e2e leg (b200::encode_scene from disk)
+
+
+def _one(src: Path, out: Path, verbose: bool) -> Path:
+    hdr = ROOT / "include" / "semsplat_b200" / "semsplat_b200.hpp"
+    lib = ROOT / "paper_2505_08124_b200" / "libsemsplat_b200.so"
+    if out.exists() and all(p.stat().st_mtime < out.stat().st_mtime for p in (src, hdr, lib)):
+        return out
+    out.parent.mkdir(exist_ok=True)
+    cmd = ["g++", "-std=c++20", "-O2", "-I", str(ROOT / "oracle" / "eigen_shim"), "-I", str(REF_INCLUDE), "-I",
+           str(ROOT / "include"), str(src), "-o", str(out), "-L", str(lib.parent), "-lsemsplat_b200",
+           "-Wl,-rpath,$ORIGIN/../../../paper_2505_08124_b200", "-lz", "-lpthread"]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+    return out
 
 
 def build(verbose: bool = False) -> Path | None:
     if not REF_INCLUDE.exists():
         return None
-    src = HERE / "dropin_test.cpp"
-    hdr = ROOT / "include" / "semsplat_b200" / "semsplat_b200.hpp"
-    lib = ROOT / "paper_2505_08124_b200" / "libsemsplat_b200.so"
-    if OUT.exists() and all(p.stat().st_mtime < OUT.stat().st_mtime for p in (src, hdr, lib)):
-        return OUT
-    OUT.parent.mkdir(exist_ok=True)
-    cmd = ["g++", "-std=c++20", "-O2", "-I", str(ROOT / "oracle" / "eigen_shim"), "-I", str(REF_INCLUDE), "-I",
-           str(ROOT / "include"), str(src), "-o", str(OUT), "-L", str(lib.parent), "-lsemsplat_b200",
-           "-Wl,-rpath,$ORIGIN/../../../paper_2505_08124_b200", "-lz", "-lpthread"]
-    if verbose:
-        print(" ".join(cmd), flush=True)
-    subprocess.run(cmd, check=True)
-    return OUT
+    _one(HERE / "bench_dropin.cpp", BENCH, verbose)
+    return _one(HERE / "dropin_test.cpp", OUT, verbose)
 
 
 if __name__ == "__main__":
