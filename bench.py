@@ -528,6 +528,22 @@ def main():
                          "frac": ops / t_launch / peak64, "ops_per_launch": ops,
                          "ops_source": "profiles/ncu_traffic.json (smsp__sass_thread_inst_executed_op_d{add,mul,fma})",
                          "peak_source": "ss_probe_fp64_rate: eight DFMA chains per thread on every SM, this run"}
+    # the compositor's binding resource is instruction issue (ncu: IPC ~2.5-2.9
+    # of 4, fp64 pipe ~34 % busy): warp instructions per launch from the
+    # committed capture over the launch time, against 4 issue slots per SM per
+    # clock at the sampled SM clock
+    roofline_issue = None
+    winst = ncu_traffic(dom, "warp_inst_per_launch") if args.config == "c4" else None
+    if winst:
+        t_launch = dk["ms_per_step"] / max(dk["launches_per_step"], 1) / 1e3
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        mhz = (clk.summary() or {}).get("sm_mhz") or 1965.0
+        peak_issue = 4.0 * sms * mhz * 1e6
+        roofline_issue = {"bound": "issue", "kernel": dom, "achieved": winst / t_launch / 1e12,
+                          "peak": peak_issue / 1e12, "unit": "T warp-instructions/s", "frac": winst / t_launch / peak_issue,
+                          "inst_per_launch": winst,
+                          "inst_source": "profiles/ncu_traffic.json (smsp__inst_executed.sum of the committed capture)",
+                          "peak_source": f"4 issue slots x {sms} SMs x {mhz:.0f} MHz (sampled SM clock)"}
     steps = 1
     pass_bytes = sum(v["bytes"] for k, v in prof.items() if k not in ("h2d", "query"))
 
@@ -639,6 +655,7 @@ def main():
                        "dataset_gen_seconds": gen_s},
             "roofline": roofline,
             "roofline_fp64": roofline_fp64,
+            "roofline_issue": roofline_issue,
             "pass_algorithmic_gb": pass_bytes / 1e9,
             "pass_hbm_frac": pass_bytes / (ms_step / 1e3) / 1e9 / hbm,
             "kernels": kernels,
