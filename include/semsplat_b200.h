@@ -112,14 +112,20 @@ int ss_synchronize(ss_ctx* ctx);
  * one CTA per tile; 0 = staged evaluation (per staged chunk the box test and
  * Mahalanobis distance per splat, then exp and alpha dense over the surviving
  * pairs, then the front-to-back transmittance walk; measured slower on c4,
- * 510 vs 382 us/view).  Identical bits. */
+ * 510 vs 382 us/view).  Identical bits.
+ * SS_OPT_CONTRACT_TC: 1 = contract groups of 2-3 views (D = 512, <= 64 masks
+ * each) on the tensor cores (tcgen05 kind::f16, fp16 hi/lo split, fp32 TMEM
+ * accumulation; within the path's tolerance, not bit-identical to the CUDA-
+ * core order); 0 = the shared-memory CUDA-core passes (default: faster on
+ * c4 so far, 65 vs 82 us/view of SM time). */
 enum ss_option {
     SS_OPT_LANES = 1,
     SS_OPT_QUERY_PATH = 2,
     SS_OPT_CONTRACT_GROUP = 3,
     SS_OPT_BIN_PATH = 4,
     SS_OPT_RASTER = 5,
-    SS_OPT_COMBINE_ROWS = 6
+    SS_OPT_COMBINE_ROWS = 6,
+    SS_OPT_CONTRACT_TC = 7
 };
 int ss_set_option(ss_ctx* ctx, int option, int64_t value);
 

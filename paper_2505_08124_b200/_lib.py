@@ -178,6 +178,10 @@ class Context:
     def set_contract_group(self, n: int):
         check(self._L.ss_set_option(self.h, 3, int(n)))
 
+    def set_contract_tc(self, on: bool):
+        """SS_OPT_CONTRACT_TC: groups of 2-3 views on the tensor cores."""
+        check(self._L.ss_set_option(self.h, 7, int(bool(on))))
+
     def assign_classes(self, rows, coverage, label_ids, label_vecs):
         """eval.hpp:122-158 on the device: class id per row (-1 = unlabeled)."""
         rows = np.ascontiguousarray(rows, np.float32)

@@ -24,6 +24,7 @@ UNITS = [
     ("ss_kernels.cu", []),
     ("ss_api.cu", []),
     ("ss_query_tc.cu", []),
+    ("ss_contract_tc.cu", []),
 ]
 
 

@@ -212,6 +212,7 @@ struct ss_ctx {
     ss::DevBuf cub_tmp, num_sel, info; // store / query scratch
     ss::DevBuf vstat; // per-view status of the last batch
     ss::DevBuf union_list, union_count; // group contraction scratch
+    ss::DevBuf tc_scratch;              // tensor-core contraction: prepared CLIP operands
     uint64_t cap_n_surv = 0;
     ss::ViewInfo* h_init = nullptr;    // pinned
     uint32_t* h_u32 = nullptr;         // pinned scratch
@@ -249,6 +250,7 @@ struct ss_ctx {
     float store_norm = 1.0f;
     int query_path = 0; // SS_OPT_QUERY_PATH
     int bin_path = 0;   // SS_OPT_BIN_PATH
+    int contract_tc = 0; // SS_OPT_CONTRACT_TC
     int raster_algo = 2; // SS_OPT_RASTER (2 = per-step compositor on work-stealing warps, the fastest on c4)
     int num_sms = 0;
 
@@ -658,6 +660,8 @@ void flush_group(ss_ctx* c) {
     if (q.n_members > 1) {
         q.union_list = static_cast<uint2*>(c->union_list.ensure(std::max<uint64_t>(c->n * q.n_members, 1) * 8));
         q.union_count = static_cast<unsigned int*>(c->union_count.ensure(16));
+        if (c->contract_tc) q.tc_scratch = c->tc_scratch.ensure(contract_tc_scratch_bytes());
+        q.use_tc = c->contract_tc;
     }
     {
         Scope sc(c, st, SS_K_CONTRACT);
@@ -1080,7 +1084,7 @@ void ss_destroy(ss_ctx* c) {
     cudaStreamSynchronize(c->stream);
     for (auto& L : c->lanes) cudaStreamSynchronize(L.stream);
     if (c->cstream) cudaStreamSynchronize(c->cstream);
-    ss::DevBuf* bufs[] = {&c->mean_op, &c->scale, &c->quat, &c->cov3, &c->cub_tmp, &c->num_sel, &c->info, &c->vstat, &c->union_list, &c->union_count, &c->pix_count,
+    ss::DevBuf* bufs[] = {&c->mean_op, &c->scale, &c->quat, &c->cov3, &c->cub_tmp, &c->num_sel, &c->info, &c->vstat, &c->union_list, &c->union_count, &c->tc_scratch, &c->pix_count,
                           &c->pix_offset, &c->entries, &c->per_pixel_total, &c->alpha, &c->color, &c->image, &c->counters, &c->sums_buf,
                           &c->totals_buf, &c->store_rows, &c->store_ids, &c->part_buf, &c->part_means, &c->qbuf, &c->qnorm, &c->scores,
                           &c->topk_ids, &c->topk_sims, &c->sel_flags, &c->thr_keys, &c->thr_keys_sorted, &c->thr_ids,
@@ -1149,6 +1153,9 @@ int ss_set_option(ss_ctx* c, int option, int64_t value) {
         } else if (option == SS_OPT_RASTER) {
             if (value < 0 || value > 2) throw Error(SS_ERR_CONTRACT, "SS_OPT_RASTER must be 0, 1 or 2");
             c->raster_algo = (int)value;
+        } else if (option == SS_OPT_CONTRACT_TC) {
+            if (value < 0 || value > 1) throw Error(SS_ERR_CONTRACT, "SS_OPT_CONTRACT_TC must be 0 or 1");
+            c->contract_tc = (int)value;
         } else if (option == SS_OPT_BIN_PATH) {
             if (value < 0 || value > 3) throw Error(SS_ERR_CONTRACT, "SS_OPT_BIN_PATH must be 0, 1, 2 or 3");
             c->bin_path = (int)value;

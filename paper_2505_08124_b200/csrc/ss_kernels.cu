@@ -1799,7 +1799,7 @@ cudaError_t launch_contract(const ContractParams& p, uint64_t max_touched, cudaS
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     {
-        // SS_CONTRACT_CTAS: grid of the group passes (timing experiments; default one CTA per SM)
+        // SS_CONTRACT_CTAS: grid of the group passes (timing experiments)
         static const int override_ctas = [] {
             const char* e = getenv("SS_CONTRACT_CTAS");
             return e ? atoi(e) : 0;
@@ -1825,6 +1825,11 @@ cudaError_t launch_contract(const ContractParams& p, uint64_t max_touched, cudaS
         cudaError_t e = cudaMemsetAsync(p.union_count, 0, sizeof(unsigned int), s);
         if (e != cudaSuccess) return e;
         group_union_kernel<<<(unsigned)sms * 4u, 256, 0, s>>>(p, p.union_list, p.union_count);
+        if (p.use_tc && p.tc_scratch && contract_tc_eligible(p)) {
+            int full = 148; // one persistent CTA per SM (512 TMEM columns, ~196 KB shared each)
+            cudaDeviceGetAttribute(&full, cudaDevAttrMultiProcessorCount, dev);
+            return launch_contract_tc(p, p.tc_scratch, full, s);
+        }
         const size_t smem = (size_t)group_masks * 1024u;
         contract_group_pass_kernel<0, 3, 2, false><<<sms, 1024, smem, s>>>(p, p.union_list, p.union_count);
         contract_group_pass_kernel<1, 3, 2, false><<<sms, 1024, smem, s>>>(p, p.union_list, p.union_count);

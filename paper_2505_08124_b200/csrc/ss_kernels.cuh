@@ -28,7 +28,15 @@ struct ContractParams {
     unsigned long long* cum; // running totals: [0] G_v, [1] K_v (summed over views), [2] rows read+written
     uint2* union_list;       // group scratch: (gid, member mask), sum of the members' lists
     unsigned int* union_count;
+    void* tc_scratch;        // contract_tc_scratch_bytes(): prepared CLIP operands of the tensor-core path
+    int use_tc;              // SS_OPT_CONTRACT_TC: groups on the tensor cores (ss_contract_tc.cu)
 };
+
+// Tensor-core group contraction (ss_contract_tc.cu): 2-3 members, D = 512,
+// <= 64 masks each, union list required.
+size_t contract_tc_scratch_bytes();
+bool contract_tc_eligible(const ContractParams& p);
+cudaError_t launch_contract_tc(const ContractParams& p, void* scratch, int ctas, cudaStream_t s);
 
 cudaError_t launch_rle_to_bits(const uint32_t* runs, const uint64_t* run_offsets, uint32_t n_masks, uint32_t words,
                                uint32_t* bits, uint4* spans, unsigned int* n_spans, cudaStream_t s);

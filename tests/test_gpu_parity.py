@@ -253,15 +253,18 @@ def test_group_contraction_d512(gpu_ctx, oracle, m):
     masks = wl.masks[:5] + big.masks + wl.masks[5:]
     out = {}
     try:
-        for lanes, group in [(4, 1), (4, 0), (4, 2), (4, 3), (1, 3), (2, 0)]:
+        for lanes, group, tc in [(4, 1, 0), (4, 0, 0), (4, 2, 0), (4, 3, 0), (1, 3, 0), (2, 0, 0), (4, 0, 1),
+                                 (1, 2, 1)]:
             gpu_ctx.set_lanes(lanes)
             gpu_ctx.set_contract_group(group)
-            out[(lanes, group)] = _encode(gpu_ctx, wl.scene, cams, masks, 512)
+            gpu_ctx.set_contract_tc(tc)  # SS_OPT_CONTRACT_TC: groups on the tensor cores
+            out[(lanes, group, tc)] = _encode(gpu_ctx, wl.scene, cams, masks, 512)
     finally:
         gpu_ctx.set_lanes(4)
         gpu_ctx.set_contract_group(0)
+        gpu_ctx.set_contract_tc(0)
     er, ec = oracle.encode(wl.scene, cams, masks, 512)
-    ref_rows, ref_cov = out[(4, 1)]
+    ref_rows, ref_cov = out[(4, 1, 0)]
     for key, (rows, cov) in out.items():
         rel, cos = row_errors(rows, cov, ref_rows, ref_cov)
         assert rel <= 1e-5, (key, rel)
