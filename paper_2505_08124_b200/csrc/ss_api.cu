@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -151,7 +152,8 @@ struct Lane {
     DevBuf bin_counts, bin_slice, bin_tot, bin_done; // direct binning scratch
     DevBuf ts_fill, ts_slab;       // tile-sort binning: per-tile fill counters, unordered (key, gid) slots
     DevBuf raster_work;            // work-stealing compositor counters (zero between launches)
-    uint32_t ts_cap = kTileSortMax; // tile-sort slots per tile (larger tiles take the global path)
+    uint32_t ts_cap = kTileSortMax / 2; // tile-sort slots per tile: grows to kTileSortMax when a tile
+                                        // outgrows it (larger tiles take the global path)
     uint64_t iota_n = 0;           // entries of the 0..n-1 sequence in `iota`
     uint64_t list_cap = 0;         // entries of `list`
     DevBuf cub_tmp, info;

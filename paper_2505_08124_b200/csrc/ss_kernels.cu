@@ -640,12 +640,16 @@ __global__ void __launch_bounds__(kTsThreads) ts_scatter_kernel(TileSortParams p
 }
 
 constexpr uint32_t kTsSortThreads = 512;
-constexpr uint32_t kTsPer = kTileSortMax / kTsSortThreads; // slots per thread
 
-__global__ void __launch_bounds__(kTsSortThreads) tile_sort_kernel(TileSortParams p) {
-    extern __shared__ uint32_t sm[]; // cnt[kTileSortMax], then out[kTileSortMax] as (key, gid)
+// MAXN: the slot capacity of the launch (4096 by default: 48 KB of shared
+// memory and <= 40 registers, three CTAs per SM, which leaves room for the
+// other lanes' kernels; 8192 once a view had a larger tile).
+template <uint32_t MAXN, int MIN_CTAS>
+__global__ void __launch_bounds__(kTsSortThreads, MIN_CTAS) tile_sort_kernel(TileSortParams p) {
+    constexpr uint32_t kTsPer = MAXN / kTsSortThreads; // slots per thread
+    extern __shared__ uint32_t sm[]; // cnt[MAXN], then out[MAXN] as (key, gid)
     uint32_t* cnt = sm;
-    uint2* out = reinterpret_cast<uint2*>(sm + kTileSortMax);
+    uint2* out = reinterpret_cast<uint2*>(sm + MAXN);
     __shared__ uint32_t red_min[kTsSortThreads / 32], red_max[kTsSortThreads / 32];
     __shared__ uint32_t s_fail;
     const uint32_t t = blockIdx.x;
@@ -659,7 +663,7 @@ __global__ void __launch_bounds__(kTsSortThreads) tile_sort_kernel(TileSortParam
         s_fail = 0u;
     }
     if (n == 0) return;
-    if (n > kTileSortMax) {
+    if (n > MAXN) { // cannot happen: the scatter flags tiles beyond the slot capacity
         if (tid == 0) {
             atomicMax(&p.info->bin_fallback, 2u);
             p.info->overflow = 1u;
@@ -690,7 +694,7 @@ __global__ void __launch_bounds__(kTsSortThreads) tile_sort_kernel(TileSortParam
         red_min[warp] = mn;
         red_max[warp] = mx;
     }
-    // B = 2^lb >= n buckets (32 .. kTileSortMax) over [mn, mx]
+    // B = 2^lb >= n buckets (32 .. MAXN) over [mn, mx]
     uint32_t lb = 5;
     while ((1u << lb) < n) ++lb;
     const uint32_t B = 1u << lb;
@@ -1701,8 +1705,11 @@ cudaError_t launch_tile_sort_bin(const TileSortParams& p, cudaStream_t s) {
         cudaError_t e = cudaFuncSetAttribute(ts_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)(kTsMaxTiles * 4));
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(tile_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            e = cudaFuncSetAttribute(tile_sort_kernel<kTileSortMax, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)(3 * kTileSortMax * 4));
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(tile_sort_kernel<kTileSortMax / 2, 3>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * kTileSortMax / 2 * 4));
         if (e != cudaSuccess) return e;
         configured[dev].store(1);
     }
@@ -1712,7 +1719,10 @@ cudaError_t launch_tile_sort_bin(const TileSortParams& p, cudaStream_t s) {
         const unsigned chunks = (unsigned)((p.n + kTsChunk - 1) / kTsChunk);
         ts_scatter_kernel<<<chunks, kTsThreads, (size_t)p.tiles * 4, s>>>(p);
     }
-    tile_sort_kernel<<<p.tiles, kTsSortThreads, 3 * kTileSortMax * 4, s>>>(p);
+    if (p.cap <= kTileSortMax / 2)
+        tile_sort_kernel<kTileSortMax / 2, 3><<<p.tiles, kTsSortThreads, 3 * kTileSortMax / 2 * 4, s>>>(p);
+    else
+        tile_sort_kernel<kTileSortMax, 2><<<p.tiles, kTsSortThreads, 3 * kTileSortMax * 4, s>>>(p);
     return cudaGetLastError();
 }
 
