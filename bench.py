@@ -508,6 +508,11 @@ def main():
             kernels[k] = {"ms_per_step": v["ms"], "launches_per_step": v["launches"], "gb_per_step": v["bytes"] / 1e9,
                           "achieved_gbs": v["bytes"] / (v["ms"] / 1e3) / 1e9 if k != "h2d" else None,
                           "share_of_serial_step": v["ms"] / ms_prof}
+            # measured DRAM traffic of the class per view (committed ncu capture, c4) beside the algorithmic bytes
+            dv = ncu_traffic(k, "bytes_per_view") if args.config == "c4" else None
+            if dv:
+                kernels[k]["dram_gb_per_view_ncu"] = dv / 1e9
+                kernels[k]["algorithmic_gb_per_view"] = v["bytes"] / 1e9 / n_views
     dom = max((k for k in kernels if k not in ("h2d",)), key=lambda k: kernels[k]["ms_per_step"])
     dk = kernels[dom]
     roofline = {"bound": "hbm", "kernel": dom, "achieved": dk["achieved_gbs"], "peak": hbm, "unit": "GB/s",
