@@ -113,6 +113,12 @@ int ss_synchronize(ss_ctx* ctx);
  * Mahalanobis distance per splat, then exp and alpha dense over the surviving
  * pairs, then the front-to-back transmittance walk; measured slower on c4,
  * 510 vs 382 us/view).  Identical bits.
+ * SS_OPT_COMBINE_SPARSE: how ss_encode_combine moves the partials: 1 =
+ * only the rows some rank touched (default with a communicator of more than
+ * one rank: an all-reduce of covered flags, then a reduce-scatter of the
+ * covered rows packed per owner -- c4 touches ~6 % of the rows, so ~16x fewer
+ * bytes than the dense reduce-scatter), 0 = every row, 2 = the covered-row
+ * path even for a one-rank communicator (tests).  Same output rows.
  * SS_OPT_CONTRACT_TC: 1 = contract groups of 2-3 views (D = 512, <= 64 masks
  * each) on the tensor cores (tcgen05 kind::f16, fp16 hi/lo split, fp32 TMEM
  * accumulation; within the path's tolerance, not bit-identical to the CUDA-
@@ -125,7 +131,8 @@ enum ss_option {
     SS_OPT_BIN_PATH = 4,
     SS_OPT_RASTER = 5,
     SS_OPT_COMBINE_ROWS = 6,
-    SS_OPT_CONTRACT_TC = 7
+    SS_OPT_CONTRACT_TC = 7,
+    SS_OPT_COMBINE_SPARSE = 8
 };
 int ss_set_option(ss_ctx* ctx, int option, int64_t value);
 

@@ -243,6 +243,10 @@ class Context:
         """SS_OPT_COMBINE_ROWS: block rows of the block-cyclic combine (0 = contiguous shards)."""
         check(self._L.ss_set_option(self.h, 6, int(rows)))
 
+    def set_combine_sparse(self, mode: int):
+        """SS_OPT_COMBINE_SPARSE: 0 dense, 1 covered rows with a multi-rank communicator, 2 forced."""
+        check(self._L.ss_set_option(self.h, 8, int(mode)))
+
     def combine_layout(self):
         v = [C.c_uint64() for _ in range(4)]
         check(self._L.ss_combine_layout(self.h, *[C.byref(x) for x in v]))

@@ -264,6 +264,8 @@ struct ss_ctx {
     cudaStream_t comm_stream = nullptr;
     cudaEvent_t ev_acc = nullptr, ev_rs[2] = {nullptr, nullptr}, ev_norm[2] = {nullptr, nullptr};
     ss::DevBuf rs_sum[2], rs_tot[2], rs_stage;
+    int combine_sparse = 1;             // SS_OPT_COMBINE_SPARSE: 0 dense, 1 covered rows (with a communicator), 2 forced
+    ss::DevBuf sp_flags, sp_pos, sp_tmp, sp_send, sp_bounds;
     uint64_t acc_rows = 0;                // accumulator rows (N padded to whole combine rounds)
 
     // instrumentation
@@ -906,6 +908,8 @@ struct NcclApi {
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                                   cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -931,10 +935,11 @@ const NcclApi& nccl_api() {
         a.CommInitAll = reinterpret_cast<decltype(a.CommInitAll)>(sym("ncclCommInitAll"));
         a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(sym("ncclCommDestroy"));
         a.ReduceScatter = reinterpret_cast<decltype(a.ReduceScatter)>(sym("ncclReduceScatter"));
+        a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(sym("ncclAllReduce"));
         a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(sym("ncclGroupStart"));
         a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(sym("ncclGroupEnd"));
         a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(sym("ncclGetErrorString"));
-        if (!a.GetUniqueId || !a.CommInitRank || !a.CommInitAll || !a.CommDestroy || !a.ReduceScatter ||
+        if (!a.GetUniqueId || !a.CommInitRank || !a.CommInitAll || !a.CommDestroy || !a.ReduceScatter || !a.AllReduce ||
             !a.GroupStart || !a.GroupEnd || !a.GetErrorString)
             a.error = "libnccl.so.2 lacks a required symbol";
         return a;
@@ -1111,6 +1116,7 @@ void ss_destroy(ss_ctx* c) {
         if (c->ev_norm[i]) cudaEventDestroy(c->ev_norm[i]);
     }
     c->rs_stage.release();
+    for (ss::DevBuf* b : {&c->sp_flags, &c->sp_pos, &c->sp_tmp, &c->sp_send, &c->sp_bounds}) b->release();
     if (c->ev_acc) cudaEventDestroy(c->ev_acc);
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     if (c->ev_user) cudaEventDestroy(c->ev_user);
@@ -1155,6 +1161,9 @@ int ss_set_option(ss_ctx* c, int option, int64_t value) {
         } else if (option == SS_OPT_RASTER) {
             if (value < 0 || value > 2) throw Error(SS_ERR_CONTRACT, "SS_OPT_RASTER must be 0, 1 or 2");
             c->raster_algo = (int)value;
+        } else if (option == SS_OPT_COMBINE_SPARSE) {
+            if (value < 0 || value > 2) throw Error(SS_ERR_CONTRACT, "SS_OPT_COMBINE_SPARSE must be 0, 1 or 2");
+            c->combine_sparse = (int)value;
         } else if (option == SS_OPT_CONTRACT_TC) {
             if (value < 0 || value > 1) throw Error(SS_ERR_CONTRACT, "SS_OPT_CONTRACT_TC must be 0 or 1");
             c->contract_tc = (int)value;
@@ -2090,6 +2099,89 @@ int ss_combine_layout_for(uint64_t n, int nranks, uint64_t combine_rows, uint64_
 // reduce-scatter per round on the communicator's stream, then finalize_into
 // (pipeline.hpp:120-135) of the received rows on the context's stream; round
 // q + 1's collective overlaps round q's normalisation (double-buffered).
+namespace {
+// ss_encode_combine over the covered rows only (SS_OPT_COMBINE_SPARSE): per
+// round, an all-reduce (max) of every rank's covered flags, positions by a
+// scan, the covered rows of each owner block packed into equal P-row segments
+// (P = the largest owner's count), one grouped reduce-scatter of [sums |
+// totals] segments, and the owner unpacks and normalises its block.  The
+// rank's output block is the dense path's, row for row (uncovered rows zero).
+void combine_sparse_rounds(ss_ctx* c, const CombineLayout& L, float* rows_out, float* coverage_out,
+                           bool out_on_device) {
+    const uint64_t D = c->dim, W = (uint64_t)c->nranks, B = L.block, RB = W * B;
+    const uint64_t r = (uint64_t)c->rank;
+    cudaStream_t s = c->stream;
+    auto* flags = static_cast<uint8_t*>(c->sp_flags.ensure(RB + 1));
+    auto* pos = static_cast<uint32_t*>(c->sp_pos.ensure((RB + 1) * 4));
+    auto* bounds = static_cast<uint32_t*>(c->sp_bounds.ensure((W + 1) * 4));
+    size_t tb = 0;
+    SS_CUDA(launch_flag_positions(flags, RB, pos, nullptr, &tb, s));
+    void* tmp = c->sp_tmp.ensure(std::max<size_t>(tb, 1));
+    std::vector<uint32_t> hb(W + 1);
+    for (uint64_t q = 0; q < L.rounds; ++q) {
+        const uint64_t row0 = q * RB;
+        {
+            Scope sc(c, s, SS_K_COMBINE);
+            own_launch(c, launch_covered_flags(c->totals + row0, RB, flags, s), SS_K_COMBINE);
+            if (W > 1) SS_NCCL(AllReduce(flags, flags, RB, ncclUint8, ncclMax, c->comm, s));
+            size_t tb2 = tb;
+            SS_CUDA(launch_flag_positions(flags, RB, pos, tmp, &tb2, s));
+            c->launches_cub += 1;
+            for (uint64_t k = 0; k <= W; ++k)
+                SS_CUDA(cudaMemcpyAsync(hb.data() + k, pos + k * B, 4, cudaMemcpyDeviceToHost, s));
+            SS_CUDA(cudaStreamSynchronize(s));
+        }
+        uint64_t P = 0;
+        for (uint64_t k = 0; k < W; ++k) P = std::max<uint64_t>(P, hb[k + 1] - hb[k]);
+        const float* recv_s = nullptr;
+        const float* recv_t = nullptr;
+        if (P) {
+            Scope sc(c, s, SS_K_COMBINE);
+            auto* send = static_cast<float*>(c->sp_send.ensure((W * P * (D + 1) + P * (D + 1)) * 4));
+            float* send_s = send;
+            float* send_t = send + W * P * D;
+            float* rs = send_t + W * P;
+            float* rt = rs + P * D;
+            SS_CUDA(cudaMemsetAsync(send, 0, W * P * (D + 1) * 4, s)); // padding rows stay zero
+            own_launch(c,
+                       launch_sparse_pack(c->sums + row0 * D, c->totals + row0, RB, (uint32_t)D, B, flags, pos, P,
+                                          send_s, send_t, s),
+                       SS_K_COMBINE);
+            if (W > 1) {
+                SS_NCCL(GroupStart());
+                SS_NCCL(ReduceScatter(send_s, rs, P * D, ncclFloat32, ncclSum, c->comm, s));
+                SS_NCCL(ReduceScatter(send_t, rt, P, ncclFloat32, ncclSum, c->comm, s));
+                SS_NCCL(GroupEnd());
+                recv_s = rs;
+                recv_t = rt;
+            } else {
+                recv_s = send_s; // one rank: its packed rows are the combined ones
+                recv_t = send_t;
+            }
+            c->prof.launches[SS_K_COMBINE] += 1;
+            c->prof.bytes[SS_K_COMBINE] += (double)(W - 1) * P * (D + 1) * 4; // sent per rank
+        }
+        float* dr = out_on_device ? rows_out + q * B * D : c->rs_stage.as<float>();
+        float* dc = out_on_device ? coverage_out + q * B : c->rs_stage.as<float>() + B * D;
+        {
+            Scope sc(c, s, SS_K_NORMALIZE);
+            // P == 0: no covered row anywhere in the round; the unpack writes zeros
+            own_launch(c,
+                       launch_sparse_unpack(recv_s ? recv_s : c->sums, recv_t ? recv_t : c->totals, B, r * B, flags,
+                                            pos, (uint32_t)D, dr, dc, c->counters.as<unsigned long long>() + 3, s),
+                       SS_K_NORMALIZE);
+            c->prof.bytes[SS_K_NORMALIZE] += (double)B * (4.0 * D + 8.0);
+        }
+        if (!out_on_device) {
+            copy_d2h_pageable(c, rows_out + q * B * D, dr, B * D * 4, s);
+            copy_d2h_pageable(c, coverage_out + q * B, dc, B * 4, s);
+        } else if (q + 1 < L.rounds) {
+            SS_CUDA(cudaStreamSynchronize(s)); // flags / pos / send are reused next round
+        }
+    }
+}
+} // namespace
+
 int ss_encode_combine(ss_ctx* c, float* rows_out, float* coverage_out, int out_on_device) {
     return guarded([&] {
         if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
@@ -2101,8 +2193,13 @@ int ss_encode_combine(ss_ctx* c, float* rows_out, float* coverage_out, int out_o
         const uint64_t D = c->dim, W = (uint64_t)c->nranks, B = L.block;
         cudaStream_t s = c->stream;
         const bool collective = c->comm && W > 1;
-        if (collective) SS_CUDA(cudaEventRecord(c->ev_acc, s));
         if (!out_on_device) c->rs_stage.ensure(B * (D + 1) * 4);
+        const bool sparse = c->comm && (c->combine_sparse == 2 || (c->combine_sparse == 1 && W > 1));
+        if (sparse) {
+            combine_sparse_rounds(c, L, rows_out, coverage_out, out_on_device != 0);
+            return;
+        }
+        if (collective) SS_CUDA(cudaEventRecord(c->ev_acc, s));
         for (uint64_t q = 0; q < L.rounds; ++q) {
             const int buf = (int)(q & 1);
             const float* src_s;

@@ -14,11 +14,18 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
 #include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 #include <cub/iterator/transform_input_iterator.cuh>
 
 #include "ss_kernels.cuh"
 
 namespace ss {
+// flags[i] as a u32 for the exclusive scan of the sparse combine (i == n reads 0)
+struct FlagAt {
+    const uint8_t* f;
+    uint64_t n;
+    __host__ __device__ uint32_t operator()(uint64_t i) const { return i < n ? (uint32_t)f[i] : 0u; }
+};
 namespace {
 
 // ------------------------------------------------------------ mask decode
@@ -1962,6 +1969,89 @@ cudaError_t launch_store_partition(const float* means, const float* rows, const 
     cell_list_kernel<<<blocks_for(n + 1, 256), 256, 0, s>>>(w.kx_s, w.yz_s, w.heads, w.n_heads, w.cells, w.offsets,
                                                             n);
     gather_records_kernel<<<warp_grid(n), 256, 0, s>>>(rows, ids, w.perm2, n, dim, w.out_rows, w.out_ids);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------- covered-row (sparse) combine
+// Only rows some rank touched carry data (c4: ~6 % of the scene), so the
+// combine reduce-scatters those rows alone: global covered flags (an all-reduce
+// max of every rank's "total != 0"), positions by a scan, each rank packs its
+// partial's covered rows owner by owner (owner k = the rank that receives row
+// block k of the round) into equal P-row segments, and after the
+// reduce-scatter the owner unpacks its segment onto its block, normalising as
+// normalize_kernel does (uncovered rows are exact zeros).
+__global__ void covered_flags_kernel(const float* totals, uint64_t n, uint8_t* flags) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) flags[i] = totals[i] != 0.0f; // NaN totals count as touched
+}
+
+__global__ void __launch_bounds__(256) sparse_pack_kernel(const float* sums, const float* totals, uint64_t n,
+                                                          uint32_t dim, uint64_t block, const uint8_t* flags,
+                                                          const uint32_t* pos, uint64_t P, float* send_sums,
+                                                          float* send_tot) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t w0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t i = w0; i < n; i += nw) {
+        if (!flags[i]) continue;
+        const uint64_t k = i / block;
+        const uint64_t slot = k * P + (pos[i] - pos[k * block]);
+        const float* src = sums + i * dim;
+        float* dst = send_sums + slot * dim;
+        for (uint32_t d = lane; d < dim; d += 32) dst[d] = src[d];
+        if (lane == 0) send_tot[slot] = totals[i];
+    }
+}
+
+__global__ void __launch_bounds__(256) sparse_unpack_kernel(const float* recv_sums, const float* recv_tot,
+                                                            uint64_t block, uint64_t own0, const uint8_t* flags,
+                                                            const uint32_t* pos, uint32_t dim, float* rows,
+                                                            float* coverage, unsigned long long* covered) {
+    unsigned long long ncov = 0;
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t w0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t k = w0; k < block; k += nw) {
+        const uint64_t i = own0 + k; // row of the round
+        const bool f = flags[i] != 0;
+        const uint64_t j = f ? pos[i] - pos[own0] : 0;
+        const float t = f ? recv_tot[j] : 0.0f;
+        const bool cov = (double)t > 1e-8; // pipeline.hpp:120-135, as normalize_kernel
+        ncov += cov;
+        const double inv = cov ? 1.0 / (double)t : 0.0;
+        const float* sp = recv_sums + j * dim;
+        float* o = rows + k * dim;
+        for (uint32_t d = lane; d < dim; d += 32) o[d] = cov ? __double2float_rn((double)sp[d] * inv) : 0.0f;
+        if (lane == 0) coverage[k] = cov ? t : 0.0f;
+    }
+    if (covered && lane == 0 && ncov) atomicAdd(covered, ncov);
+}
+
+cudaError_t launch_covered_flags(const float* totals, uint64_t n, uint8_t* flags, cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    covered_flags_kernel<<<blocks_for(n, 256), 256, 0, s>>>(totals, n, flags);
+    return cudaGetLastError();
+}
+cudaError_t launch_flag_positions(const uint8_t* flags, uint64_t n, uint32_t* pos, void* tmp, size_t* tmp_bytes,
+                                  cudaStream_t s) {
+    // pos[i] = covered rows before i, pos[n] = all (exclusive scan over n + 1 items; flags[n] reads as 0)
+    auto in = thrust::make_transform_iterator(thrust::counting_iterator<uint64_t>(0),
+                                              FlagAt{flags, n});
+    return cub::DeviceScan::ExclusiveSum(tmp, *tmp_bytes, in, pos, (int)(n + 1), s);
+}
+cudaError_t launch_sparse_pack(const float* sums, const float* totals, uint64_t n, uint32_t dim, uint64_t block,
+                               const uint8_t* flags, const uint32_t* pos, uint64_t P, float* send_sums,
+                               float* send_tot, cudaStream_t s) {
+    if (!n || !P) return cudaSuccess;
+    sparse_pack_kernel<<<warp_grid(n), 256, 0, s>>>(sums, totals, n, dim, block, flags, pos, P, send_sums, send_tot);
+    return cudaGetLastError();
+}
+cudaError_t launch_sparse_unpack(const float* recv_sums, const float* recv_tot, uint64_t block, uint64_t own0,
+                                 const uint8_t* flags, const uint32_t* pos, uint32_t dim, float* rows, float* coverage,
+                                 unsigned long long* covered, cudaStream_t s) {
+    if (!block) return cudaSuccess;
+    sparse_unpack_kernel<<<warp_grid(block), 256, 0, s>>>(recv_sums, recv_tot, block, own0, flags, pos, dim, rows,
+                                                          coverage, covered);
     return cudaGetLastError();
 }
 

@@ -141,6 +141,17 @@ struct PartitionScratch {
 size_t partition_tmp_bytes(uint64_t n);
 cudaError_t launch_store_partition(const float* means, const float* rows, const uint32_t* ids, uint64_t n,
                                    uint32_t dim, double cell, const PartitionScratch& w, cudaStream_t s);
+// covered-row combine (ss_encode_combine with SS_OPT_COMBINE_SPARSE)
+cudaError_t launch_covered_flags(const float* totals, uint64_t n, uint8_t* flags, cudaStream_t s);
+// pos[0..n] exclusive prefix of flags (tmp == nullptr: *tmp_bytes <- scratch size)
+cudaError_t launch_flag_positions(const uint8_t* flags, uint64_t n, uint32_t* pos, void* tmp, size_t* tmp_bytes,
+                                  cudaStream_t s);
+cudaError_t launch_sparse_pack(const float* sums, const float* totals, uint64_t n, uint32_t dim, uint64_t block,
+                               const uint8_t* flags, const uint32_t* pos, uint64_t P, float* send_sums,
+                               float* send_tot, cudaStream_t s);
+cudaError_t launch_sparse_unpack(const float* recv_sums, const float* recv_tot, uint64_t block, uint64_t own0,
+                                 const uint8_t* flags, const uint32_t* pos, uint32_t dim, float* rows, float* coverage,
+                                 unsigned long long* covered, cudaStream_t s);
 // first `take` sorted threshold keys -> (id, sim) result row, on the device
 cudaError_t launch_decode_keys(const unsigned long long* keys, uint64_t take, uint32_t* ids, float* sims,
                                cudaStream_t s);

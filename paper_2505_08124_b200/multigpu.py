@@ -117,3 +117,47 @@ def sharded_query_topk(local_topk, queries, k: int, group=None):
     dist.all_gather(gc, tc, group=group)
     mi, ms, mc = merge_topk(torch.stack(gi), torch.stack(gs), torch.stack(gc), k)
     return mi.cpu().numpy().astype(np.uint32), ms.cpu().numpy(), mc.cpu().numpy().astype(np.uint64)
+
+
+def sparse_combine_mirror(partials_sums, partials_totals, block: int):
+    """Host mirror of ss_encode_combine's covered-row path (SS_OPT_COMBINE_SPARSE)
+    for one round of world x block rows: covered flags (all-reduce max of
+    total != 0), positions, each rank packs its covered rows per owner block
+    into P-row segments (P = the largest owner's count), the reduce-scatter
+    sums the packed buffers and hands segment k to rank k, which unpacks onto
+    its block.  Returns, per rank, (summed rows [block, D], summed totals
+    [block]) -- what the rank normalises; uncovered rows are zero."""
+    import numpy as np
+
+    world = len(partials_sums)
+    d = partials_sums[0].shape[1]
+    flags = np.zeros(world * block, bool)
+    for t in partials_totals:
+        flags |= t != 0
+    pos = np.concatenate([[0], np.cumsum(flags)]).astype(np.int64)
+    counts = [int(pos[(k + 1) * block] - pos[k * block]) for k in range(world)]
+    P = max(counts) if counts else 0
+    packed = []
+    for s, t in zip(partials_sums, partials_totals):
+        ps = np.zeros((world * P, d), s.dtype)
+        pt = np.zeros(world * P, t.dtype)
+        for i in np.nonzero(flags)[0]:
+            k = i // block
+            slot = k * P + (pos[i] - pos[k * block])
+            ps[slot] = s[i]
+            pt[slot] = t[i]
+        packed.append((ps, pt))
+    out = []
+    for r in range(world):
+        seg_s = sum(p[0][r * P:(r + 1) * P] for p in packed)
+        seg_t = sum(p[1][r * P:(r + 1) * P] for p in packed)
+        rows = np.zeros((block, d), partials_sums[0].dtype)
+        tots = np.zeros(block, partials_totals[0].dtype)
+        for k in range(block):
+            i = r * block + k
+            if flags[i]:
+                j = pos[i] - pos[r * block]
+                rows[k] = seg_s[j]
+                tots[k] = seg_t[j]
+        out.append((rows, tots))
+    return out

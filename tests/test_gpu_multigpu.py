@@ -45,10 +45,14 @@ def test_combine_without_communicator_equals_finalize(combine_rows):
     ctx.close()
 
 
-@pytest.mark.parametrize("how,combine_rows", [("rank", 0), ("rank", 777), ("all", 0)])
-def test_combine_through_nccl_one_rank(how, combine_rows):
+@pytest.mark.parametrize("how,combine_rows,sparse", [("rank", 0, 0), ("rank", 777, 0), ("all", 0, 0), ("rank", 0, 2),
+                                                     ("rank", 777, 2), ("all", 333, 2)])
+def test_combine_through_nccl_one_rank(how, combine_rows, sparse):
     """The NCCL path of ss_encode_combine (grouped reduce-scatter rounds on the
-    communicator's stream, normalisation overlapped on the context stream)."""
+    communicator's stream, normalisation overlapped on the context stream), and
+    the covered-row path (SS_OPT_COMBINE_SPARSE = 2 forces it for one rank:
+    covered flags, positions, per-owner packing and unpacking) -- both give the
+    rows of ss_encode_finalize bit for bit."""
     from paper_2505_08124_b200._lib import Context
     wl = _bench_style(3001, 3, 72, 56, 20, 32, seed=202)
     ctx = Context(0)
@@ -57,6 +61,7 @@ def test_combine_through_nccl_one_rank(how, combine_rows):
     else:
         Context.comm_init_all([ctx])
     ctx.set_combine_rows(combine_rows)
+    ctx.set_combine_sparse(sparse)
     _encode_into(ctx, wl, 32)
     whole_rows, whole_cov = ctx.encode_finalize()
     rows, cov, held = ctx.combine()

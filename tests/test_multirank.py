@@ -160,3 +160,27 @@ def test_two_rank_sharded_query_matches_single_store():
         assert np.array_equal(mc, ec), (rank, k)
         assert np.array_equal(mi[:, :kk], ei[:, :kk]), (rank, k)
         assert ms[:, :kk].tobytes() == es[:, :kk].tobytes(), (rank, k)
+
+
+@pytest.mark.parametrize("world,block", [(2, 50), (3, 17), (8, 9)])
+def test_sparse_combine_mirror_equals_dense(world, block):
+    """The covered-row combine (SS_OPT_COMBINE_SPARSE) moves only rows some
+    rank touched, packed per owner into equal segments; every rank must end up
+    with exactly the dense reduce-scatter's rows of its block (float64 sums
+    here, so the check is exact)."""
+    from paper_2505_08124_b200.multigpu import sparse_combine_mirror
+    rng = np.random.default_rng(world * 100 + block)
+    n, d = world * block, 6
+    sums, tots = [], []
+    for _ in range(world):
+        touched = rng.random(n) < 0.15
+        s = np.where(touched[:, None], rng.standard_normal((n, d)), 0.0)
+        t = np.where(touched, rng.uniform(0.1, 2.0, n), 0.0)
+        sums.append(s)
+        tots.append(t)
+    dense_s = sum(sums)
+    dense_t = sum(tots)
+    out = sparse_combine_mirror(sums, tots, block)
+    for r, (rs, rt) in enumerate(out):
+        assert np.array_equal(rs, dense_s[r * block:(r + 1) * block])
+        assert np.array_equal(rt, dense_t[r * block:(r + 1) * block])
