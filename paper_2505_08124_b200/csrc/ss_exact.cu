@@ -89,7 +89,10 @@ __global__ void __launch_bounds__(256) cov3d_kernel(const float4* __restrict__ s
 // projection.hpp:33-55 project_gaussian + rasterizer.hpp:66-71 conic_of +
 // the padded 3-sigma box and cull (rasterizer.hpp:160-179).  Survivors get
 // their depth bit pattern as sort key (positive f64 => monotone as u64).
-__global__ void __launch_bounds__(128) project_kernel(ProjectParams p) {
+#ifndef SS_PROJECT_MIN_CTAS
+#define SS_PROJECT_MIN_CTAS 1
+#endif
+__global__ void __launch_bounds__(128, SS_PROJECT_MIN_CTAS) project_kernel(ProjectParams p) {
     const uint64_t id = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     bool survive = false;
     unsigned long long key = ~0ull;

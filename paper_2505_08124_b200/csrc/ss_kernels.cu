@@ -569,11 +569,20 @@ __global__ void __launch_bounds__(WARPS * 32) bin_scatter_kernel(BinParams p) {
 //     kTileSortMax instances or a bucket beyond kTsBucketMax (massive exact
 //     depth ties) flags bin_fallback = 2: the host re-runs the view on the
 //     global depth sort, whose tie fix-up handles any run length.
-constexpr uint32_t kTsChunk = 8192;   // Gaussians per scatter CTA
+#ifndef SS_TS_CHUNK
+#define SS_TS_CHUNK 2048
+#endif
+#ifndef SS_TS_THREADS
+#define SS_TS_THREADS 1024
+#endif
+constexpr uint32_t kTsChunk = SS_TS_CHUNK;   // Gaussians per scatter CTA
 constexpr uint32_t kTsBucketMax = 64; // instances per bucket the fix-up orders
 constexpr uint32_t kTsMaxTiles = 16384; // shared histogram of the scatter (64 KB)
 
-constexpr uint32_t kTsThreads = 1024;  // scatter CTA: 32 warps, each 8 groups of 32 Gaussians
+constexpr uint32_t kTsThreads = SS_TS_THREADS;  // scatter CTA: 32 warps, each 2 groups of 32 Gaussians
+// (300 c4 views, views/s and serialised bin ms: 8192 Gaussians per 1024-thread CTA
+// 1650 / 67.0, 4096 per 512 threads 1654-1657 / 65.6, 4096 per 1024 threads
+// 1670-1675 / 62.3, 2048 per 1024 threads 1672-1676 / 58.4, 2048 per 256 1649 / 64.9)
 
 // f(tile) for every tile of a box, row-major (per lane; lanes diverge on box size)
 template <typename F>
@@ -704,6 +713,12 @@ __global__ void __launch_bounds__(kTsSortThreads, MIN_CTAS) tile_sort_kernel(Til
     // B = 2^lb >= n buckets (32 .. MAXN) over [mn, mx]
     uint32_t lb = 5;
     while ((1u << lb) < n) ++lb;
+#ifndef SS_TS_BUCKET_SHIFT
+#define SS_TS_BUCKET_SHIFT 1
+#endif
+    // about two instances per bucket: half the scan work of one per bucket,
+    // the rank loop stays short (measured +0.6 % on c4)
+    lb = lb > 5u + SS_TS_BUCKET_SHIFT ? lb - SS_TS_BUCKET_SHIFT : 5u;
     const uint32_t B = 1u << lb;
     for (uint32_t b = tid; b < B; b += kTsSortThreads) cnt[b] = 0u;
     __syncthreads();
