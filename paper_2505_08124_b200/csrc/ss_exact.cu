@@ -89,10 +89,10 @@ __global__ void __launch_bounds__(256) cov3d_kernel(const float4* __restrict__ s
 // projection.hpp:33-55 project_gaussian + rasterizer.hpp:66-71 conic_of +
 // the padded 3-sigma box and cull (rasterizer.hpp:160-179).  Survivors get
 // their depth bit pattern as sort key (positive f64 => monotone as u64).
-#ifndef SS_PROJECT_MIN_CTAS
-#define SS_PROJECT_MIN_CTAS 1
+#ifndef SS_PROJECT_THREADS
+#define SS_PROJECT_THREADS 128
 #endif
-__global__ void __launch_bounds__(128, SS_PROJECT_MIN_CTAS) project_kernel(ProjectParams p) {
+__global__ void __launch_bounds__(SS_PROJECT_THREADS) project_kernel(ProjectParams p) {
     const uint64_t id = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     bool survive = false;
     unsigned long long key = ~0ull;
@@ -877,8 +877,8 @@ cudaError_t launch_cov3d(const float4* scale, const float4* quat, uint64_t n, do
 
 cudaError_t launch_project(const ProjectParams& p, cudaStream_t s) {
     if (p.n == 0) return cudaSuccess;
-    const unsigned blocks = (unsigned)((p.n + 127) / 128);
-    project_kernel<<<blocks, 128, 0, s>>>(p);
+    const unsigned blocks = (unsigned)((p.n + SS_PROJECT_THREADS - 1) / SS_PROJECT_THREADS);
+    project_kernel<<<blocks, SS_PROJECT_THREADS, 0, s>>>(p);
     return cudaGetLastError();
 }
 

@@ -655,7 +655,10 @@ __global__ void __launch_bounds__(kTsThreads) ts_scatter_kernel(TileSortParams p
     }
 }
 
-constexpr uint32_t kTsSortThreads = 512;
+#ifndef SS_TS_SORT_THREADS
+#define SS_TS_SORT_THREADS 512
+#endif
+constexpr uint32_t kTsSortThreads = SS_TS_SORT_THREADS;
 
 // MAXN: the slot capacity of the launch (4096 by default: 48 KB of shared
 // memory and <= 40 registers, three CTAs per SM, which leaves room for the
