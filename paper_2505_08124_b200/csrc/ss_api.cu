@@ -146,7 +146,10 @@ struct ContractSet {
 struct Lane {
     cudaStream_t stream = nullptr;
     cudaEvent_t contract_done = nullptr, done = nullptr, raster_done = nullptr;
-    ContractSet sets[2];
+#ifndef SS_LANE_SETS
+#define SS_LANE_SETS 2
+#endif
+    ContractSet sets[SS_LANE_SETS]; // per-(Gaussian, mask) scalars in flight per lane (views awaiting contraction)
     uint32_t set_next = 0;
     DevBuf rec, boxes, rbox, rcnt, keys, k32, k32s, order, iota, offsets, tkeys, tkeys_sorted, tvals, tile_start, tile_end, list;
     DevBuf bin_counts, bin_slice, bin_tot, bin_done; // direct binning scratch
@@ -690,7 +693,7 @@ bool encode_one(ss_ctx* c, Lane& L, const ss_camera& cam, const ss_view_masks* v
     ContractSet* S = nullptr;
     if (M) {
         S = &L.sets[L.set_next];
-        L.set_next ^= 1u;
+        L.set_next = (L.set_next + 1u) % SS_LANE_SETS;
         if (S->in_group) flush_group(c); // the set is needed again before its group closed
         if (S->pending) {                // its last contraction must be done before we overwrite it
             SS_CUDA(cudaStreamWaitEvent(s, S->free_ev, 0));
