@@ -767,3 +767,38 @@ def test_partition_store_vs_reference(gpu_ctx, ref, cell):
         assert sn.rows.tobytes() == rrows[lo:hi].tobytes()
     with pytest.raises(Exception):
         semsplat.partition_store(store, means, 0.0)
+
+
+@pytest.mark.parametrize("lanes", [5, 2])
+def test_encode_mixed_global_fallback_views_multilane(gpu_ctx, oracle, lanes):
+    """A batch mixing views whose tile sort must fall back to the global depth
+    sort (a tile holding thousands of exact depth ties, more than one bucket of
+    the per-tile sort takes: bin_fallback 2, the view is re-run on the global
+    path) with ordinary views, across several pipeline lanes: the fallback
+    views are re-run while the others' results stand, and the table matches
+    the oracle."""
+    from harness.workload import rect_masks, synth_embedding
+    rng = np.random.default_rng(91)
+    n = 6000
+    mean = np.zeros((n, 3), np.float32)
+    mean[:2000, :2] = rng.uniform(-0.05, 0.05, (2000, 2))
+    mean[:2000, 2] = 5.0  # exact depth ties under an axis-aligned camera
+    mean[2000:, :2] = rng.uniform(-2.0, 2.0, (4000, 2))
+    mean[2000:, 2] = rng.uniform(4.0, 6.0, 4000)
+    s = scene_ns(mean, np.full((n, 3), 0.03), np.tile([0, 0, 0, 1.0], (n, 1)), rng.uniform(0.05, 0.4, n))
+    cams, masks = [], []
+    # principal points: the tie cluster on screen (fallback) or pushed off it (ordinary view)
+    for i, (cx, cy) in enumerate([(24, 24), (-200, 24), (30, 20), (24, -300), (18, 28), (-150, -150), (26, 26)]):
+        cams.append(plain_camera(60.0, 60.0, float(cx), float(cy), 48, 48, image_id=i))
+        runs, offs = rect_masks(500 + i, 48, 48, 6)
+        clip = np.stack([synth_embedding(f"fallback_{i}_{j}", 16) for j in range(6)])
+        masks.append((6, 48, 48, runs, offs, clip))
+    try:
+        gpu_ctx.set_lanes(lanes)
+        rows, cov = _encode(gpu_ctx, s, cams, masks, 16)
+    finally:
+        gpu_ctx.set_lanes(4)
+    er, ec = oracle.encode(s, cams, masks, 16)
+    rel, cos = row_errors(rows, cov, er, ec)
+    assert rel <= EMB_REL_TOL and cos >= EMB_COS_TOL, (rel, cos)
+    assert np.array_equal(cov > 0, ec > 0)
