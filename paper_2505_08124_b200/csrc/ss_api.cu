@@ -842,8 +842,7 @@ void encode_batch(ss_ctx* c, uint32_t nviews, const ss_camera* cams, const ss_vi
                 again.push_back(v);
                 if (st.bin_fallback == 1 && st.max_fill <= kTileSortMax) {
                     // a tile outgrew its slots: every lane's capacity grows to the largest tile seen
-                    uint32_t cap = 1024;
-                    while (cap < st.max_fill) cap <<= 1;
+                    const uint32_t cap = tile_sort_capacity(st.max_fill);
                     for (auto& L : c->lanes) L.ts_cap = std::max(L.ts_cap, cap);
                 } else if (st.bin_fallback) {
                     force_global[v] = 1; // beyond the in-CTA tile sort: the global depth sort path
@@ -1268,9 +1267,7 @@ void capture_view(ss_ctx* c, const ss_camera* cam, int mode, bool color, uint64_
         if (!L.h_info->overflow) break;
         if (attempt > 3) throw Error(SS_ERR_CUDA, "tile-list buffer kept overflowing");
         if (L.h_info->bin_fallback == 1 && L.h_info->max_fill <= kTileSortMax) {
-            uint32_t cap = 1024;
-            while (cap < L.h_info->max_fill) cap <<= 1;
-            L.ts_cap = std::max(L.ts_cap, cap);
+            L.ts_cap = std::max(L.ts_cap, tile_sort_capacity(L.h_info->max_fill));
         } else if (L.h_info->bin_fallback) {
             force_global = true;
         } else {

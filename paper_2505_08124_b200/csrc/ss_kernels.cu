@@ -663,12 +663,25 @@ constexpr uint32_t kTsSortThreads = SS_TS_SORT_THREADS;
 // MAXN: the slot capacity of the launch (4096 by default: 48 KB of shared
 // memory and <= 40 registers, three CTAs per SM, which leaves room for the
 // other lanes' kernels; 8192 once a view had a larger tile).
+#ifndef SS_TS_BUCKET_SHIFT
+#define SS_TS_BUCKET_SHIFT 1
+#endif
+// buckets the sort of a tile of up to n instances uses (lb below) at most
+__host__ __device__ constexpr uint32_t tile_sort_buckets(uint32_t n) {
+    uint32_t lb = 5;
+    while ((1u << lb) < n) ++lb;
+    return 1u << (lb > 5u + SS_TS_BUCKET_SHIFT ? lb - SS_TS_BUCKET_SHIFT : 5u);
+}
+__host__ __device__ constexpr size_t tile_sort_smem(uint32_t maxn) {
+    return (size_t)tile_sort_buckets(maxn) * 4 + (size_t)maxn * 8;
+}
+
 template <uint32_t MAXN, int MIN_CTAS>
 __global__ void __launch_bounds__(kTsSortThreads, MIN_CTAS) tile_sort_kernel(TileSortParams p) {
     constexpr uint32_t kTsPer = MAXN / kTsSortThreads; // slots per thread
-    extern __shared__ uint32_t sm[]; // cnt[MAXN], then out[MAXN] as (key, gid)
+    extern __shared__ uint32_t sm[]; // cnt[tile_sort_buckets(MAXN)], then out[MAXN] as (key, gid)
     uint32_t* cnt = sm;
-    uint2* out = reinterpret_cast<uint2*>(sm + MAXN);
+    uint2* out = reinterpret_cast<uint2*>(sm + tile_sort_buckets(MAXN));
     __shared__ uint32_t red_min[kTsSortThreads / 32], red_max[kTsSortThreads / 32];
     __shared__ uint32_t s_fail;
     const uint32_t t = blockIdx.x;
@@ -716,9 +729,6 @@ __global__ void __launch_bounds__(kTsSortThreads, MIN_CTAS) tile_sort_kernel(Til
     // B = 2^lb >= n buckets (32 .. MAXN) over [mn, mx]
     uint32_t lb = 5;
     while ((1u << lb) < n) ++lb;
-#ifndef SS_TS_BUCKET_SHIFT
-#define SS_TS_BUCKET_SHIFT 1
-#endif
     // about two instances per bucket: half the scan work of one per bucket,
     // the rank loop stays short (measured +0.6 % on c4)
     lb = lb > 5u + SS_TS_BUCKET_SHIFT ? lb - SS_TS_BUCKET_SHIFT : 5u;
@@ -1731,10 +1741,14 @@ cudaError_t launch_tile_sort_bin(const TileSortParams& p, cudaStream_t s) {
                                              (int)(kTsMaxTiles * 4));
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(tile_sort_kernel<kTileSortMax, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(3 * kTileSortMax * 4));
+                                     (int)tile_sort_smem(kTileSortMax));
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(tile_sort_kernel<kTileSortMax * 3 / 4, 3>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)tile_sort_smem(kTileSortMax * 3 / 4));
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(tile_sort_kernel<kTileSortMax / 2, 3>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * kTileSortMax / 2 * 4));
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_sort_smem(kTileSortMax / 2));
         if (e != cudaSuccess) return e;
         configured[dev].store(1);
     }
@@ -1744,10 +1758,15 @@ cudaError_t launch_tile_sort_bin(const TileSortParams& p, cudaStream_t s) {
         const unsigned chunks = (unsigned)((p.n + kTsChunk - 1) / kTsChunk);
         ts_scatter_kernel<<<chunks, kTsThreads, (size_t)p.tiles * 4, s>>>(p);
     }
+    // slot capacity 4096 / 6144 (c4's dense tiles reach ~5300 instances): 64 KB
+    // or less of shared memory, three CTAs per SM; 8192: two
     if (p.cap <= kTileSortMax / 2)
-        tile_sort_kernel<kTileSortMax / 2, 3><<<p.tiles, kTsSortThreads, 3 * kTileSortMax / 2 * 4, s>>>(p);
+        tile_sort_kernel<kTileSortMax / 2, 3><<<p.tiles, kTsSortThreads, tile_sort_smem(kTileSortMax / 2), s>>>(p);
+    else if (p.cap <= kTileSortMax * 3 / 4)
+        tile_sort_kernel<kTileSortMax * 3 / 4, 3>
+            <<<p.tiles, kTsSortThreads, tile_sort_smem(kTileSortMax * 3 / 4), s>>>(p);
     else
-        tile_sort_kernel<kTileSortMax, 2><<<p.tiles, kTsSortThreads, 3 * kTileSortMax * 4, s>>>(p);
+        tile_sort_kernel<kTileSortMax, 2><<<p.tiles, kTsSortThreads, tile_sort_smem(kTileSortMax), s>>>(p);
     return cudaGetLastError();
 }
 

@@ -94,6 +94,10 @@ struct TileSortParams {
     ViewInfo* info;
 };
 constexpr uint32_t kTileSortMax = 8192; // instances one CTA orders in shared memory
+// slot capacity for a view whose largest tile holds max_fill instances: 4096, 6144 or 8192
+inline uint32_t tile_sort_capacity(uint32_t max_fill) {
+    return max_fill <= kTileSortMax / 2 ? kTileSortMax / 2 : (max_fill <= kTileSortMax * 3 / 4 ? kTileSortMax * 3 / 4 : kTileSortMax);
+}
 uint32_t tile_sort_max_tiles();         // views with more tiles use the other paths
 cudaError_t launch_tile_sort_bin(const TileSortParams& p, cudaStream_t s);
 
