@@ -222,6 +222,10 @@ __global__ void __launch_bounds__(SS_PROJECT_THREADS) project_kernel(ProjectPara
 }
 
 // ------------------------------------------------------------- compositor
+#ifndef SS_PIX_SMEM
+#define SS_PIX_SMEM 1
+#endif
+
 // Per-pixel compositing state (rasterizer.hpp:112-133).
 struct PixelState {
     double T;
@@ -236,8 +240,9 @@ struct PixelState {
 // cutoff, alpha clamp, skip rule, weight cutoff and transmittance floor, in
 // its exact fp64 operation order.  Returns whether an entry is emitted.
 template <bool FALLOFF, typename Rec>
-__device__ __forceinline__ bool composite_one(PixelState& ps, const Rec& s, uint32_t stab_addr, float& wf) {
-    const double dx = ds(ps.dpx, s.mu_x), dy = ds(ps.dpy, s.mu_y);
+__device__ __forceinline__ bool composite_one(PixelState& ps, double dpx, double dpy, const Rec& s, uint32_t stab_addr,
+                                              float& wf) {
+    const double dx = ds(dpx, s.mu_x), dy = ds(dpy, s.mu_y);
     const double d2 = da(da(dm(dm(s.a, dx), dx), dm(dm(s.b2, dx), dy)), dm(dm(s.c, dy), dy));
     if (d2 > kMahalanobisSqCutoff) return false;
     const double g = glibc_exp_small(dm(-0.5, d2), stab_addr);
@@ -354,7 +359,7 @@ __device__ __forceinline__ uint32_t match_bits(const uint32_t (&bits)[MW]) {
 template <int KIND, bool FALLOFF, int MW>
 __device__ __forceinline__ void composite_block(const RasterParams& p, uint32_t tile, uint32_t wb, uint32_t lane,
                                                 SplatRec* wrec, uint32_t* wgid, uint32_t* wmask, uint32_t srec_addr,
-                                                uint32_t stab_addr) {
+                                                uint32_t stab_addr, uint32_t spix_addr) {
     const uint32_t tx = tile % p.tiles_x, ty = tile / p.tiles_x;
     const uint32_t bx0 = tx * kTile + 8u * (wb & 1u), by0 = ty * kTile + 4u * (wb >> 1);
     const uint32_t bx1 = bx0 + 7u, by1 = by0 + 3u;
@@ -367,6 +372,13 @@ __device__ __forceinline__ void composite_block(const RasterParams& p, uint32_t 
     ps.pixel = ps.py * p.width + ps.px;
     ps.dpx = (double)(int32_t)ps.px;
     ps.dpy = (double)(int32_t)ps.py;
+#if SS_PIX_SMEM
+    // the pixel's fp64 coordinates wait in the lane's shared-memory slot: one
+    // LDS per evaluated step instead of re-deriving and converting them (the
+    // 40-register budget cannot keep two doubles live across the loop)
+    const uint32_t pix_addr = spix_addr + lane * 16u;
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(pix_addr), "d"(ps.dpx), "d"(ps.dpy) : "memory");
+#endif
     ps.T = 1.0;
     ps.total = 0.0;
     ps.count = 0;
@@ -432,12 +444,23 @@ __device__ __forceinline__ void composite_block(const RasterParams& p, uint32_t 
             // keep the staging and exp-table addresses live instead of re-deriving
             // the shared window base for every splat
             asm volatile("" : "+r"(srec_addr), "+r"(stab_addr));
+#if SS_PIX_SMEM
+            asm volatile("" : "+r"(pix_addr));
+#endif
             const StagedSplat s = lds_splat(srec_addr + j * (uint32_t)sizeof(SplatRec));
             const uint32_t mj = __shfl_sync(0xffffffffu, smk, j);
             const uint32_t gj = __shfl_sync(0xffffffffu, sgd, j);
             float wf = 0.0f;
             bool c = false;
-            if ((mj & lane_bit) && !ps.done) c = composite_one<FALLOFF>(ps, s, stab_addr, wf);
+            if ((mj & lane_bit) && !ps.done) {
+#if SS_PIX_SMEM
+                double dpx, dpy;
+                asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(dpx), "=d"(dpy) : "r"(pix_addr));
+                c = composite_one<FALLOFF>(ps, dpx, dpy, s, stab_addr, wf);
+#else
+                c = composite_one<FALLOFF>(ps, ps.dpx, ps.dpy, s, stab_addr, wf);
+#endif
+            }
             if constexpr (KIND == 0) {
                 ps.count += c ? 1u : 0u;
             } else if constexpr (KIND == 1 || KIND == 3) {
@@ -501,13 +524,15 @@ __global__ void __launch_bounds__(kRasterThreads, 6) raster_kernel(RasterParams 
     __shared__ uint32_t sgid[kRasterThreads];
     __shared__ uint32_t smask[kRasterThreads];
     __shared__ unsigned long long stab[256];
+    __shared__ double2 spix[SS_PIX_SMEM ? kRasterThreads : 1];
     stab[threadIdx.x] = kExpTab[threadIdx.x];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     if (p.info->overflow) return; // tile lists incomplete: the view is re-run by the host
     __syncthreads();              // exp table staged
     composite_block<KIND, FALLOFF, MW>(p, blockIdx.x, warp, lane, srec + 32u * warp, sgid + 32u * warp,
                                        smask + 32u * warp, (uint32_t)__cvta_generic_to_shared(srec + 32u * warp),
-                                       (uint32_t)__cvta_generic_to_shared(stab));
+                                       (uint32_t)__cvta_generic_to_shared(stab),
+                                       (uint32_t)__cvta_generic_to_shared(spix + (SS_PIX_SMEM ? 32u * warp : 0u)));
 }
 
 // Work-stealing form: a grid sized to the resident CTAs, each warp taking
@@ -522,6 +547,7 @@ __global__ void __launch_bounds__(kRasterThreads, 6) raster_persist_kernel(Raste
     __shared__ uint32_t sgid[kRasterThreads];
     __shared__ uint32_t smask[kRasterThreads];
     __shared__ unsigned long long stab[256];
+    __shared__ double2 spix[SS_PIX_SMEM ? kRasterThreads : 1];
     stab[threadIdx.x] = kExpTab[threadIdx.x];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     __syncthreads(); // exp table staged
@@ -535,7 +561,8 @@ __global__ void __launch_bounds__(kRasterThreads, 6) raster_persist_kernel(Raste
             composite_block<KIND, FALLOFF, MW>(p, item >> 3, item & 7u, lane, srec + 32u * warp, sgid + 32u * warp,
                                                smask + 32u * warp,
                                                (uint32_t)__cvta_generic_to_shared(srec + 32u * warp),
-                                               (uint32_t)__cvta_generic_to_shared(stab));
+                                               (uint32_t)__cvta_generic_to_shared(stab),
+                                               (uint32_t)__cvta_generic_to_shared(spix + (SS_PIX_SMEM ? 32u * warp : 0u)));
         }
     }
     if (lane == 0 && atomicAdd(p.work + 1, 1u) == gridDim.x * (kRasterThreads / 32u) - 1u) {
