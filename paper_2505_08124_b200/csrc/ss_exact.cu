@@ -358,7 +358,7 @@ __device__ __forceinline__ uint32_t match_bits(const uint32_t (&bits)[MW]) {
 // list: the body of raster_kernel / raster_persist_kernel.
 template <int KIND, bool FALLOFF, int MW>
 __device__ __forceinline__ void composite_block(const RasterParams& p, uint32_t tile, uint32_t wb, uint32_t lane,
-                                                SplatRec* wrec, uint32_t* wgid, uint32_t* wmask, uint32_t srec_addr,
+                                                SplatRec* wrec, uint2* wmg, uint32_t srec_addr,
                                                 uint32_t stab_addr, uint32_t spix_addr) {
     const uint32_t tx = tile % p.tiles_x, ty = tile / p.tiles_x;
     const uint32_t bx0 = tx * kTile + 8u * (wb & 1u), by0 = ty * kTile + 4u * (wb >> 1);
@@ -376,7 +376,7 @@ __device__ __forceinline__ void composite_block(const RasterParams& p, uint32_t 
     // the pixel's fp64 coordinates wait in the lane's shared-memory slot: one
     // LDS per evaluated step instead of re-deriving and converting them (the
     // 40-register budget cannot keep two doubles live across the loop)
-    const uint32_t pix_addr = spix_addr + lane * 16u;
+    uint32_t pix_addr = spix_addr + lane * 16u;
     asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(pix_addr), "d"(ps.dpx), "d"(ps.dpy) : "memory");
 #endif
     ps.T = 1.0;
@@ -409,6 +409,7 @@ __device__ __forceinline__ void composite_block(const RasterParams& p, uint32_t 
         nbox = __ldg(p.boxes + nr);
     }
     const uint32_t lane_bit = 1u << lane;
+    uint32_t mg_addr = (uint32_t)__cvta_generic_to_shared(wmg);
     for (uint32_t base = start; base < end; base += 32u) {
         const uint32_t live = ~__ballot_sync(0xffffffffu, ps.done);
         if (live == 0u) break;
@@ -432,24 +433,23 @@ __device__ __forceinline__ void composite_block(const RasterParams& p, uint32_t 
             dst[0] = __ldg(src);
             dst[1] = __ldg(src + 1);
             dst[2] = __ldg(src + 2);
-            wgid[slot] = r;
-            wmask[slot] = m;
+            wmg[slot] = make_uint2(m, r);
         }
         __syncwarp();
         const uint32_t nh = __popc(cand);
-        // staged splat j's pixel mask and id live in lane j's registers
-        const uint32_t smk = lane < nh ? wmask[lane] : 0u;
-        const uint32_t sgd = lane < nh ? wgid[lane] : 0u;
-        for (uint32_t j = 0; j < nh; ++j) {
+        // running shared addresses of staged splat j's record and (mask, id)
+        uint32_t ra = srec_addr, ma = mg_addr;
+        for (uint32_t j = 0; j < nh; ++j, ra += (uint32_t)sizeof(SplatRec), ma += 8u) {
             // keep the staging and exp-table addresses live instead of re-deriving
             // the shared window base for every splat
-            asm volatile("" : "+r"(srec_addr), "+r"(stab_addr));
+            asm volatile("" : "+r"(ra), "+r"(stab_addr), "+r"(ma));
 #if SS_PIX_SMEM
             asm volatile("" : "+r"(pix_addr));
 #endif
-            const StagedSplat s = lds_splat(srec_addr + j * (uint32_t)sizeof(SplatRec));
-            const uint32_t mj = __shfl_sync(0xffffffffu, smk, j);
-            const uint32_t gj = __shfl_sync(0xffffffffu, sgd, j);
+            const StagedSplat s = lds_splat(ra);
+            // staged splat j's pixel mask and id: one broadcast shared load
+            uint32_t mj, gj;
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(mj), "=r"(gj) : "r"(ma));
             float wf = 0.0f;
             bool c = false;
             if ((mj & lane_bit) && !ps.done) {
@@ -521,16 +521,15 @@ __device__ __forceinline__ void composite_block(const RasterParams& p, uint32_t 
 template <int KIND, bool FALLOFF, int MW>
 __global__ void __launch_bounds__(kRasterThreads, 6) raster_kernel(RasterParams p) {
     __shared__ SplatRec srec[kRasterThreads]; // warp w stages its hits in srec[32w, 32w+32)
-    __shared__ uint32_t sgid[kRasterThreads];
-    __shared__ uint32_t smask[kRasterThreads];
+    __shared__ uint2 smg[kRasterThreads];
     __shared__ unsigned long long stab[256];
     __shared__ double2 spix[SS_PIX_SMEM ? kRasterThreads : 1];
     stab[threadIdx.x] = kExpTab[threadIdx.x];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     if (p.info->overflow) return; // tile lists incomplete: the view is re-run by the host
     __syncthreads();              // exp table staged
-    composite_block<KIND, FALLOFF, MW>(p, blockIdx.x, warp, lane, srec + 32u * warp, sgid + 32u * warp,
-                                       smask + 32u * warp, (uint32_t)__cvta_generic_to_shared(srec + 32u * warp),
+    composite_block<KIND, FALLOFF, MW>(p, blockIdx.x, warp, lane, srec + 32u * warp, smg + 32u * warp,
+                                       (uint32_t)__cvta_generic_to_shared(srec + 32u * warp),
                                        (uint32_t)__cvta_generic_to_shared(stab),
                                        (uint32_t)__cvta_generic_to_shared(spix + (SS_PIX_SMEM ? 32u * warp : 0u)));
 }
@@ -544,8 +543,7 @@ __global__ void __launch_bounds__(kRasterThreads, 6) raster_kernel(RasterParams 
 template <int KIND, bool FALLOFF, int MW>
 __global__ void __launch_bounds__(kRasterThreads, 6) raster_persist_kernel(RasterParams p) {
     __shared__ SplatRec srec[kRasterThreads];
-    __shared__ uint32_t sgid[kRasterThreads];
-    __shared__ uint32_t smask[kRasterThreads];
+    __shared__ uint2 smg[kRasterThreads];
     __shared__ unsigned long long stab[256];
     __shared__ double2 spix[SS_PIX_SMEM ? kRasterThreads : 1];
     stab[threadIdx.x] = kExpTab[threadIdx.x];
@@ -558,8 +556,7 @@ __global__ void __launch_bounds__(kRasterThreads, 6) raster_persist_kernel(Raste
             if (lane == 0) item = atomicAdd(p.work, 1u);
             item = __shfl_sync(0xffffffffu, item, 0);
             if (item >= items) break;
-            composite_block<KIND, FALLOFF, MW>(p, item >> 3, item & 7u, lane, srec + 32u * warp, sgid + 32u * warp,
-                                               smask + 32u * warp,
+            composite_block<KIND, FALLOFF, MW>(p, item >> 3, item & 7u, lane, srec + 32u * warp, smg + 32u * warp,
                                                (uint32_t)__cvta_generic_to_shared(srec + 32u * warp),
                                                (uint32_t)__cvta_generic_to_shared(stab),
                                                (uint32_t)__cvta_generic_to_shared(spix + (SS_PIX_SMEM ? 32u * warp : 0u)));
