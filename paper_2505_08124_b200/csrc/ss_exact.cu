@@ -234,6 +234,7 @@ struct PixelState {
     uint32_t px, py;
     double dpx, dpy;
     bool inside, done;
+    uint32_t lbit; // per-step compositor: the lane's bit while compositing, 0 once done
 };
 
 // Evaluate one splat at one pixel: the reference's box test, Mahalanobis
@@ -264,7 +265,10 @@ __device__ __forceinline__ bool composite_one(PixelState& ps, double dpx, double
         const bool emit = w >= kCompositeConst[2];
         if (emit) wf = __double2float_rn(w);
         ps.T = dm(ps.T, ds(1.0, alpha));
-        if (ps.T < kCompositeConst[3]) ps.done = true;
+        if (ps.T < kCompositeConst[3]) {
+            ps.done = true;
+            ps.lbit = 0u;
+        }
         return emit;
     }
 }
@@ -400,6 +404,9 @@ __device__ __forceinline__ void composite_block(const RasterParams& p, uint32_t 
         grp = match_bits<MW>(bits);
         ps.done = ps.done || !any; // unmasked pixels contribute nothing
     }
+    // the loop tests "still compositing" as the lane's bit (one LOP3 against
+    // the staged splat's pixel mask); ps.done is not read below
+    ps.lbit = ps.done ? 0u : 1u << lane;
 
     // prefetch the first chunk's ranks and boxes
     uint32_t nr = 0;
@@ -411,7 +418,7 @@ __device__ __forceinline__ void composite_block(const RasterParams& p, uint32_t 
     const uint32_t lane_bit = 1u << lane;
     uint32_t mg_addr = (uint32_t)__cvta_generic_to_shared(wmg);
     for (uint32_t base = start; base < end; base += 32u) {
-        const uint32_t live = ~__ballot_sync(0xffffffffu, ps.done);
+        const uint32_t live = __ballot_sync(0xffffffffu, ps.lbit != 0u);
         if (live == 0u) break;
         const uint32_t i = base + lane;
         const uint32_t r = nr;
@@ -450,9 +457,9 @@ __device__ __forceinline__ void composite_block(const RasterParams& p, uint32_t 
             // staged splat j's pixel mask and id: one broadcast shared load
             uint32_t mj, gj;
             asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(mj), "=r"(gj) : "r"(ma));
-            float wf = 0.0f;
+            float wf; // read only when c
             bool c = false;
-            if ((mj & lane_bit) && !ps.done) {
+            if (mj & ps.lbit) {
 #if SS_PIX_SMEM
                 double dpx, dpy;
                 asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(dpx), "=d"(dpy) : "r"(pix_addr));
@@ -478,7 +485,7 @@ __device__ __forceinline__ void composite_block(const RasterParams& p, uint32_t 
             } else {
                 gate_and_accumulate<MW>(p, c, wf, grp, bits, gj, lane);
             }
-            if ((j & 7u) == 7u && __all_sync(0xffffffffu, ps.done)) break;
+            if ((j & 7u) == 7u && __all_sync(0xffffffffu, ps.lbit == 0u)) break;
         }
         __syncwarp();
     }
