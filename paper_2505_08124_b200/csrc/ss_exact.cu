@@ -444,48 +444,54 @@ __device__ __forceinline__ void composite_block(const RasterParams& p, uint32_t 
         }
         __syncwarp();
         const uint32_t nh = __popc(cand);
-        // running shared addresses of staged splat j's record and (mask, id)
+        // running shared addresses of staged splat j's record and (mask, id);
+        // the steps go in unrolled groups of 8 (constant offsets, one bound
+        // test per step, the all-terminated vote once per group)
         uint32_t ra = srec_addr, ma = mg_addr;
-        for (uint32_t j = 0; j < nh; ++j, ra += (uint32_t)sizeof(SplatRec), ma += 8u) {
+        for (uint32_t j0 = 0; j0 < nh; j0 += 8u, ra += 8u * (uint32_t)sizeof(SplatRec), ma += 64u) {
             // keep the staging and exp-table addresses live instead of re-deriving
             // the shared window base for every splat
             asm volatile("" : "+r"(ra), "+r"(stab_addr), "+r"(ma));
 #if SS_PIX_SMEM
             asm volatile("" : "+r"(pix_addr));
 #endif
-            const StagedSplat s = lds_splat(ra);
-            // staged splat j's pixel mask and id: one broadcast shared load
-            uint32_t mj, gj;
-            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(mj), "=r"(gj) : "r"(ma));
-            float wf; // read only when c
-            bool c = false;
-            if (mj & ps.lbit) {
+#pragma unroll
+            for (uint32_t k = 0; k < 8u; ++k) {
+                if (j0 + k >= nh) break;
+                const StagedSplat s = lds_splat(ra + k * (uint32_t)sizeof(SplatRec));
+                // staged splat j's pixel mask and id: one broadcast shared load
+                uint32_t mj, gj;
+                asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(mj), "=r"(gj) : "r"(ma + 8u * k));
+                float wf; // read only when c
+                bool c = false;
+                if (mj & ps.lbit) {
 #if SS_PIX_SMEM
-                double dpx, dpy;
-                asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(dpx), "=d"(dpy) : "r"(pix_addr));
-                c = composite_one<FALLOFF>(ps, dpx, dpy, s, stab_addr, wf);
+                    double dpx, dpy;
+                    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(dpx), "=d"(dpy) : "r"(pix_addr));
+                    c = composite_one<FALLOFF>(ps, dpx, dpy, s, stab_addr, wf);
 #else
-                c = composite_one<FALLOFF>(ps, ps.dpx, ps.dpy, s, stab_addr, wf);
+                    c = composite_one<FALLOFF>(ps, ps.dpx, ps.dpy, s, stab_addr, wf);
 #endif
-            }
-            if constexpr (KIND == 0) {
-                ps.count += c ? 1u : 0u;
-            } else if constexpr (KIND == 1 || KIND == 3) {
-                if (c) {
-                    p.entries[ps.out++] = ss_weight_entry{gj, ps.pixel, wf};
-                    ps.total = da(ps.total, (double)wf);
-                    if constexpr (KIND == 3) {
-                        // color_sum += double(wf) * color (rasterizer.hpp:231), per component
-                        const float4 col = __ldg(p.color + gj);
-                        csum[0] = da(csum[0], dm((double)wf, (double)col.x));
-                        csum[1] = da(csum[1], dm((double)wf, (double)col.y));
-                        csum[2] = da(csum[2], dm((double)wf, (double)col.z));
-                    }
                 }
-            } else {
-                gate_and_accumulate<MW>(p, c, wf, grp, bits, gj, lane);
+                if constexpr (KIND == 0) {
+                    ps.count += c ? 1u : 0u;
+                } else if constexpr (KIND == 1 || KIND == 3) {
+                    if (c) {
+                        p.entries[ps.out++] = ss_weight_entry{gj, ps.pixel, wf};
+                        ps.total = da(ps.total, (double)wf);
+                        if constexpr (KIND == 3) {
+                            // color_sum += double(wf) * color (rasterizer.hpp:231), per component
+                            const float4 col = __ldg(p.color + gj);
+                            csum[0] = da(csum[0], dm((double)wf, (double)col.x));
+                            csum[1] = da(csum[1], dm((double)wf, (double)col.y));
+                            csum[2] = da(csum[2], dm((double)wf, (double)col.z));
+                        }
+                    }
+                } else {
+                    gate_and_accumulate<MW>(p, c, wf, grp, bits, gj, lane);
+                }
             }
-            if ((j & 7u) == 7u && __all_sync(0xffffffffu, ps.lbit == 0u)) break;
+            if (__all_sync(0xffffffffu, ps.lbit == 0u)) break;
         }
         __syncwarp();
     }
