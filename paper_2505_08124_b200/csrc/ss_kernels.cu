@@ -789,12 +789,12 @@ __global__ void __launch_bounds__(kTsSortThreads, MIN_CTAS) tile_sort_kernel(Til
     // reference's depth_sort comparator -- and its id goes straight to the
     // tile's list (buckets average ~1-2 members: O(s) compares per instance,
     // no serial insertion sort).
+    // Threads take the instances in bucket order (out[i]), so a warp's lanes
+    // share buckets of similar size (one large bucket no longer stalls 31
+    // lanes of small ones) and the list writes land near i, coalesced.
     uint32_t* dst = p.list + base;
-#pragma unroll
-    for (uint32_t k = 0; k < kTsPer; ++k) {
-        if (k >= per) break;
-        if (tid + k * kTsSortThreads >= n) continue;
-        const uint2 x = v[k];
+    for (uint32_t i = tid; i < n; i += kTsSortThreads) {
+        const uint2 x = out[i];
         const uint32_t b = (x.x - mn) >> sh;
         const uint32_t s0 = b ? cnt[b - 1] : 0u, e0 = cnt[b];
         uint32_t pos = s0;
