@@ -596,9 +596,11 @@ __device__ __forceinline__ void for_box_tiles(uint2 box, uint32_t tiles_x, F&& f
 
 __global__ void __launch_bounds__(kTsThreads) ts_scatter_kernel(TileSortParams p) {
     extern __shared__ uint32_t hist[]; // [tiles]: counts, then cursors
+    __shared__ uint32_t s_over;        // a tile of this chunk outgrew its capacity
     const uint64_t base = (uint64_t)blockIdx.x * kTsChunk;
     if (base >= p.n) return;
     for (uint32_t t = threadIdx.x; t < p.tiles; t += blockDim.x) hist[t] = 0u;
+    if (threadIdx.x == 0) s_over = 0u;
     const uint32_t lane = threadIdx.x & 31u;
     constexpr uint32_t groups = kTsChunk / kTsThreads;
     // thread i takes Gaussians base + i + g * kTsThreads (coalesced)
@@ -629,7 +631,7 @@ __global__ void __launch_bounds__(kTsThreads) ts_scatter_kernel(TileSortParams p
         mine += c;
         const uint32_t b = atomicAdd(p.fill + t, c);
         mfill = max(mfill, b + c);
-        hist[t] = b + c <= p.cap ? t * p.cap + b : 0xffffffffu;
+        hist[t] = t * p.cap + b;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -642,16 +644,19 @@ __global__ void __launch_bounds__(kTsThreads) ts_scatter_kernel(TileSortParams p
             atomicMax(&p.info->max_fill, mfill);
             atomicMax(&p.info->bin_fallback, 1u);
             p.info->overflow = 1u;
+            s_over = 1u;
         }
     }
     __syncthreads();
+    // a chunk with an overflowing tile writes nothing (its slots could run past
+    // the slab; the view is re-run with a larger capacity), so no per-instance
+    // bounds test below
+    if (s_over) return;
 #pragma unroll
     for (uint32_t g = 0; g < groups; ++g) {
         const uint32_t id = (uint32_t)(base + threadIdx.x + (uint64_t)g * kTsThreads);
         const uint2 v = make_uint2(k32[g], id);
-        for_box_tiles(box[g], p.tiles_x, [&](uint32_t t) {
-            if (hist[t] != 0xffffffffu) p.slab[atomicAdd(hist + t, 1u)] = v;
-        });
+        for_box_tiles(box[g], p.tiles_x, [&](uint32_t t) { p.slab[atomicAdd(hist + t, 1u)] = v; });
     }
 }
 
