@@ -78,6 +78,8 @@ def parse():
     ap.add_argument("--group", type=int, default=0, help="views per contraction group (0 = library default)")
     ap.add_argument("--bin", type=int, default=0, help="tile binning: 0 auto, 1 key sort, 2 direct")
     ap.add_argument("--raster", type=int, default=-1, help="compositor: 2 per-step on work-stealing warps (library default), 1 per-step CTA per tile, 0 staged")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="SS_OPT_DETERMINISTIC: fixed-point per-(Gaussian, mask) scalars (bitwise run-to-run)")
     ap.add_argument("--combine-rows", type=int, default=0,
                     help="rows per block of the block-cyclic combine (0 = contiguous shards)")
     ap.add_argument("--cpu-sample-queries", type=int, default=32)
@@ -406,6 +408,8 @@ def main():
         ctx.set_bin_path(args.bin)
     if args.raster >= 0:
         ctx.set_raster_algo(args.raster)
+    if args.deterministic:
+        ctx.set_deterministic(True)
 
     # device-resident inputs for `value`
     dev = torch.device("cuda", local)
@@ -657,7 +661,9 @@ def main():
                        "nccl": {"nranks": world, "communicator": "libsemsplat_b200 (ss_comm_init)"} if world > 1
                        else None,
                        "l2": "inputs larger than L2 (N x 512 fp32 sums = %.1f GB RMW per pass)" % (N * D * 4 / 1e9),
-                       "dataset_gen_seconds": gen_s},
+                       "dataset_gen_seconds": gen_s,
+                       "scalars": "u64 fixed point (SS_OPT_DETERMINISTIC: bitwise run-to-run)" if args.deterministic
+                       else "f32 atomics (library default)"},
             "roofline": roofline,
             "roofline_fp64": roofline_fp64,
             "roofline_issue": roofline_issue,

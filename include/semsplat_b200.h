@@ -123,7 +123,14 @@ int ss_synchronize(ss_ctx* ctx);
  * each) on the tensor cores (tcgen05 kind::f16, fp16 hi/lo split, fp32 TMEM
  * accumulation; within the path's tolerance, not bit-identical to the CUDA-
  * core order); 0 = the shared-memory CUDA-core passes (default: faster on
- * c4 so far, 65 vs 82 us/view of SM time). */
+ * c4 so far, 65 vs 82 us/view of SM time).
+ * SS_OPT_DETERMINISTIC: 1 = the per-(Gaussian, mask) scalars are u64 fixed
+ * point (2^-32 units) added with integer atomics: every added group sum is an
+ * f32 >= 1/255, a multiple of 2^-31, so the additions are exact in any
+ * order and the table is bitwise identical run to run and for every lane
+ * count and contraction grouping (pipeline.hpp:272-279); 0 = f32 atomics
+ * (default: 3.6 % faster on c4; results differ run to run in the last bits,
+ * well inside the path's tolerance).  Set before ss_encode_begin. */
 enum ss_option {
     SS_OPT_LANES = 1,
     SS_OPT_QUERY_PATH = 2,
@@ -132,7 +139,8 @@ enum ss_option {
     SS_OPT_RASTER = 5,
     SS_OPT_COMBINE_ROWS = 6,
     SS_OPT_CONTRACT_TC = 7,
-    SS_OPT_COMBINE_SPARSE = 8
+    SS_OPT_COMBINE_SPARSE = 8,
+    SS_OPT_DETERMINISTIC = 9
 };
 int ss_set_option(ss_ctx* ctx, int option, int64_t value);
 

@@ -20,6 +20,7 @@
 // (include/semsplat_b200.h); this header only marshals the reference's types.
 #pragma once
 
+#include <atomic>
 #include <cstring>
 #include <future>
 #include <memory>
@@ -317,6 +318,17 @@ inline ViewData read_view(const DatasetManifest& manifest, const ImageEntry& ent
 }
 } // namespace detail
 
+// SS_OPT_DETERMINISTIC for encode_scene: fixed-point per-(Gaussian, mask)
+// scalars, so the table is bitwise identical run to run (the reference's
+// contract for a fixed worker count, pipeline.hpp:272-279) at ~3.6 % of c4
+// throughput.  Off by default (f32 atomics: last-bit differences between
+// runs, inside the path's tolerance).
+inline std::atomic<bool>& deterministic_flag() {
+    static std::atomic<bool> f{false};
+    return f;
+}
+inline void set_deterministic(bool on) { deterministic_flag() = on; }
+
 // pipeline.hpp:280-470.  Workers map to GPUs: with G = min(workers, visible
 // devices) devices, worker w (the reference's view-to-worker assignment,
 // round-robin or contiguous) runs on device w mod G, each device on its own
@@ -361,6 +373,7 @@ inline EmbeddingTable encode_scene(const GaussianScene& scene, const DatasetMani
     for (Device* d : devs) {
         d->bind(scene);
         check(ss_set_option(d->ctx(), SS_OPT_COMBINE_ROWS, G > 1 ? (int64_t)chunk_rows : 0));
+        check(ss_set_option(d->ctx(), SS_OPT_DETERMINISTIC, deterministic_flag() ? 1 : 0));
         check(ss_encode_begin(d->ctx(), manifest.embedding_dim, nullptr, nullptr));
     }
     const auto t0 = std::chrono::steady_clock::now();

@@ -182,6 +182,10 @@ class Context:
         """SS_OPT_CONTRACT_TC: groups of 2-3 views on the tensor cores."""
         check(self._L.ss_set_option(self.h, 7, int(bool(on))))
 
+    def set_deterministic(self, on: bool):
+        """SS_OPT_DETERMINISTIC: fixed-point per-(Gaussian, mask) scalars, bitwise run-to-run results."""
+        check(self._L.ss_set_option(self.h, 9, int(bool(on))))
+
     def assign_classes(self, rows, coverage, label_ids, label_vecs):
         """eval.hpp:122-158 on the device: class id per row (-1 = unlabeled)."""
         rows = np.ascontiguousarray(rows, np.float32)

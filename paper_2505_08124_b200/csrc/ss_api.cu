@@ -125,6 +125,7 @@ struct ProfState {
 struct ContractSet {
     DevBuf acc, touched, touched_list, clip, tcount;
     uint64_t acc_elems = 0;        // zero-initialised elements of acc
+    bool acc_fix = false;          // acc holds acc_t (fixed point) rather than float
     uint32_t gen = 0;              // last stamp handed out
     cudaEvent_t free_ev = nullptr; // recorded after the contraction that consumed this set
     bool pending = false;          // a contraction reading this set has been issued
@@ -256,6 +257,7 @@ struct ss_ctx {
     int query_path = 0; // SS_OPT_QUERY_PATH
     int bin_path = 0;   // SS_OPT_BIN_PATH
     int contract_tc = 0; // SS_OPT_CONTRACT_TC
+    bool deterministic = false; // SS_OPT_DETERMINISTIC: fixed-point per-(Gaussian, mask) scalars
     int raster_algo = 2; // SS_OPT_RASTER (2 = per-step compositor on work-stealing warps, the fastest on c4)
     int num_sms = 0;
 
@@ -654,7 +656,8 @@ void flush_group(ss_ctx* c) {
         q.m[i].touched_count = g.set->tcount.as<unsigned long long>();
         q.m[i].touched = g.set->touched.as<uint32_t>();
         q.m[i].gen = g.set->gen;
-        q.m[i].acc = g.set->acc.as<float>();
+        q.m[i].acc = g.set->acc.p;
+        q.m[i].fix = g.set->acc_fix ? 1u : 0u;
         q.m[i].n_masks = g.n_masks;
         q.m[i].clip = g.clip;
         c->prof.bytes[SS_K_CONTRACT] += (double)g.n_masks * c->dim * 4;
@@ -716,13 +719,17 @@ bool encode_one(ss_ctx* c, Lane& L, const ss_camera& cam, const ss_view_masks* v
     const Geometry g = run_geometry(c, L, s, cam, force_global);
     if (M) {
         // per-(Gaussian, mask) scalars: grow-only and kept zero by consume-and-clear
+        // (zero is all-zero bytes in both representations, so a set switches
+        // representation by size alone)
         const uint64_t need = c->n * (uint64_t)M;
-        if (need > S->acc_elems) {
+        const uint64_t esz = c->deterministic ? sizeof(acc_t) : sizeof(float);
+        if (need * esz > S->acc.bytes) {
             S->acc.release();
-            S->acc.ensure(need * 4);
+            S->acc.ensure(need * esz);
             SS_CUDA(cudaMemsetAsync(S->acc.p, 0, S->acc.bytes, s));
-            S->acc_elems = S->acc.bytes / 4;
         }
+        S->acc_fix = c->deterministic;
+        S->acc_elems = S->acc.bytes / esz;
         if (S->touched.bytes < c->n * 4 || S->gen == 0xffffffffu) {
             S->touched.release();
             S->touched.ensure(c->n * 4);
@@ -739,7 +746,8 @@ bool encode_one(ss_ctx* c, Lane& L, const ss_camera& cam, const ss_view_masks* v
             p.pix_bits = L.pix_bits.as<uint32_t>();
             p.n_masks = M;
             p.bits_stride = words;
-            p.acc = S->acc.as<float>();
+            p.acc = S->acc.p;
+            p.acc_fix = S->acc_fix ? 1u : 0u;
             p.touched = S->touched.as<uint32_t>();
             p.touched_list = tlist;
             p.touched_count = tcount;
@@ -1166,6 +1174,9 @@ int ss_set_option(ss_ctx* c, int option, int64_t value) {
         } else if (option == SS_OPT_COMBINE_SPARSE) {
             if (value < 0 || value > 2) throw Error(SS_ERR_CONTRACT, "SS_OPT_COMBINE_SPARSE must be 0, 1 or 2");
             c->combine_sparse = (int)value;
+        } else if (option == SS_OPT_DETERMINISTIC) {
+            if (value < 0 || value > 1) throw Error(SS_ERR_CONTRACT, "SS_OPT_DETERMINISTIC must be 0 or 1");
+            c->deterministic = value != 0;
         } else if (option == SS_OPT_CONTRACT_TC) {
             if (value < 0 || value > 1) throw Error(SS_ERR_CONTRACT, "SS_OPT_CONTRACT_TC must be 0 or 1");
             c->contract_tc = (int)value;
@@ -2273,8 +2284,8 @@ int ss_profile_read(ss_ctx* c, double* ms, uint64_t* launches, double* bytes) {
         set_device(c);
         profile_drain(c);
         // fold the device-side counters into raster / contract / normalize bytes:
-        // K_v pairs (8 B read-modify-write each, written by the compositor and
-        // read + cleared by the contraction), rows read and written by the
+        // K_v pairs (one 4 B scalar each, written by the compositor, read and
+        // cleared by the contraction; fixed-point scalars are 8 B), rows read and written by the
         // contraction (once per group: the union of the members' touched
         // sets), covered rows whose sums normalize reads
         unsigned long long h[4];
@@ -2287,8 +2298,9 @@ int ss_profile_read(ss_ctx* c, double* ms, uint64_t* launches, double* bytes) {
         }
         if (bytes) {
             const double D = c->dim ? c->dim : 512;
-            bytes[SS_K_RASTER] += 8.0 * kv;
-            bytes[SS_K_CONTRACT] += 8.0 * kv + rows * (8.0 * D + 8.0);
+            const double sb = c->deterministic ? 8.0 : 4.0;
+            bytes[SS_K_RASTER] += 2.0 * sb * kv;
+            bytes[SS_K_CONTRACT] += 2.0 * sb * kv + rows * (8.0 * D + 8.0);
             bytes[SS_K_NORMALIZE] += covered * 4.0 * D;
         }
     });

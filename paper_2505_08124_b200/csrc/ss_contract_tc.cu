@@ -289,9 +289,9 @@ __global__ void __launch_bounds__(THREADS, 1) contract_tc_kernel(ContractParams 
                     const uint2 nx = ulist[e_next];
                     for (uint32_t j = 0; j < nm; ++j)
                         if ((nx.y >> j) & 1u) {
-                            const float* a = p.m[j].acc + (size_t)nx.x * p.m[j].n_masks;
+                            const char* a = static_cast<const char*>(acc_row(p.m[j], nx.x).p);
                             asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
-                            asm volatile("prefetch.global.L2 [%0];" ::"l"(a + 32));
+                            asm volatile("prefetch.global.L2 [%0];" ::"l"(a + 128));
                         }
                 }
             }
@@ -311,9 +311,9 @@ __global__ void __launch_bounds__(THREADS, 1) contract_tc_kernel(ContractParams 
                         v[q][j][0] = v[q][j][1] = 0.0f;
                         if (j < nm && ((mask[q] >> j) & 1u)) {
                             const uint32_t M = p.m[j].n_masks;
-                            const float* accrow = p.m[j].acc + (size_t)gid[q] * M;
-                            if (2u * lane < M) v[q][j][0] = accrow[2u * lane];
-                            if (2u * lane + 1u < M) v[q][j][1] = accrow[2u * lane + 1u];
+                            const AccRow accrow = acc_row(p.m[j], gid[q]);
+                            if (2u * lane < M) v[q][j][0] = accrow.get(2u * lane);
+                            if (2u * lane + 1u < M) v[q][j][1] = accrow.get(2u * lane + 1u);
                         }
                     }
                 }
@@ -325,10 +325,9 @@ __global__ void __launch_bounds__(THREADS, 1) contract_tc_kernel(ContractParams 
                     for (uint32_t j = 0; j < MAXM; ++j) {
                         if (j < nm && ((mask[q] >> j) & 1u)) {
                             // consume and clear the member's scalars; totals in member order
-                            const uint32_t M = p.m[j].n_masks;
-                            float* accrow = p.m[j].acc + (size_t)gid[q] * M;
-                            if (v[q][j][0] != 0.0f) accrow[2u * lane] = 0.0f;
-                            if (v[q][j][1] != 0.0f) accrow[2u * lane + 1u] = 0.0f;
+                            const AccRow accrow = acc_row(p.m[j], gid[q]);
+                            if (v[q][j][0] != 0.0f) accrow.clear(2u * lane);
+                            if (v[q][j][1] != 0.0f) accrow.clear(2u * lane + 1u);
                             pairs += __popc(__ballot_sync(0xffffffffu, v[q][j][0] != 0.0f)) +
                                      __popc(__ballot_sync(0xffffffffu, v[q][j][1] != 0.0f));
                             float vs = v[q][j][0] + v[q][j][1];

@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 #include <stdint.h>
 
 #include "glibc_exp.cuh"
@@ -302,13 +303,16 @@ __device__ __forceinline__ uint32_t block_box_mask(uint32_t sx0, uint32_t sx1, u
 // Fused-mode gating of one pixel slot's contribution: lanes with identical
 // mask bitsets are summed with an xor butterfly (bit-identical in every lane),
 // then lane m adds the group sum to mask 32w+m when the group has that bit.
-template <int MW>
+// FIX: the scalars are u64 fixed point (KIND 4, SS_OPT_DETERMINISTIC): the
+// group sum is added exactly by an integer atomic.
+template <int MW, bool FIX>
 __device__ __forceinline__ void gate_and_accumulate(const RasterParams& p, bool contrib, float wf, uint32_t grp,
                                                     const uint32_t (&bits)[MW], uint32_t gid, uint32_t lane) {
     const uint32_t em = __ballot_sync(0xffffffffu, contrib);
     if (!em) return;
     uint32_t rem = em;
-    float* row = p.acc + (size_t)gid * p.n_masks + p.mask_base + lane;
+    using Acc = typename std::conditional<FIX, acc_t, float>::type;
+    Acc* row = static_cast<Acc*>(p.acc) + ((size_t)gid * p.n_masks + p.mask_base + lane);
     while (rem) {
         const int leader = __ffs(rem) - 1;
         const uint32_t gm = __shfl_sync(0xffffffffu, grp, leader);
@@ -318,7 +322,10 @@ __device__ __forceinline__ void gate_and_accumulate(const RasterParams& p, bool 
 #pragma unroll
         for (int w = 0; w < MW; ++w) {
             const uint32_t gb = __shfl_sync(0xffffffffu, bits[w], leader);
-            if ((gb >> lane) & 1u) atomicAdd(row + w * 32, v);
+            if ((gb >> lane) & 1u) {
+                if constexpr (FIX) atomicAdd(row + w * 32, acc_fix(v));
+                else atomicAdd(row + w * 32, v);
+            }
         }
         rem &= ~gm;
     }
@@ -358,6 +365,7 @@ __device__ __forceinline__ uint32_t match_bits(const uint32_t (&bits)[MW]) {
 //         One pass covers up to 128 masks (MW words); views with more masks
 //         (providers.hpp:135 allows any count) run one pass per 128-mask
 //         window [mask_base, mask_base + 128), each recompositing the tile.
+// KIND 4: KIND 2 with u64 fixed-point scalars (SS_OPT_DETERMINISTIC).
 // One warp composites one 8x4 block (bx0, by0) of a tile against the tile's
 // list: the body of raster_kernel / raster_persist_kernel.
 template <int KIND, bool FALLOFF, int MW>
@@ -394,7 +402,7 @@ __device__ __forceinline__ void composite_block(const RasterParams& p, uint32_t 
     }
     uint32_t bits[MW];
     uint32_t grp = 0;
-    if constexpr (KIND == 2) {
+    if constexpr (KIND == 2 || KIND == 4) {
         bool any = false;
 #pragma unroll
         for (int w = 0; w < MW; ++w) {
@@ -488,7 +496,7 @@ __device__ __forceinline__ void composite_block(const RasterParams& p, uint32_t 
                         }
                     }
                 } else {
-                    gate_and_accumulate<MW>(p, c, wf, grp, bits, gj, lane);
+                    gate_and_accumulate<MW, KIND == 4>(p, c, wf, grp, bits, gj, lane);
                 }
             }
             if (__all_sync(0xffffffffu, ps.lbit == 0u)) break;
@@ -787,7 +795,7 @@ __global__ void __launch_bounds__(kRasterThreads) raster_staged_kernel(RasterPar
                         }
                     }
                 } else {
-                    gate_and_accumulate<MW>(p, c, wf, grp, bits, gj, lane);
+                    gate_and_accumulate<MW, false>(p, c, wf, grp, bits, gj, lane);
                 }
                 if ((++steps & 7u) == 0u && __all_sync(0xffffffffu, ps.done)) {
                     finished = true;
@@ -934,7 +942,10 @@ cudaError_t launch_raster_fused(const RasterParams& p, int mode, uint32_t tiles,
     const bool fo = mode == SS_FALLOFF_ONLY;
 #define SS_FUSED(MWV)                                                                       \
     do {                                                                                    \
-        if (p.algo != 0) {                                                                  \
+        if (p.acc_fix) { /* fixed-point scalars: the per-step compositor, KIND 4 */         \
+            if (fo) launch_per_step<4, true, MWV>(p, tiles, s);                             \
+            else launch_per_step<4, false, MWV>(p, tiles, s);                               \
+        } else if (p.algo != 0) {                                                           \
             if (fo) launch_per_step<2, true, MWV>(p, tiles, s);                             \
             else launch_per_step<2, false, MWV>(p, tiles, s);                               \
         } else {                                                                            \

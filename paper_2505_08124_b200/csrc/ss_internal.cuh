@@ -25,6 +25,19 @@ struct __align__(16) SplatRec {
 };
 static_assert(sizeof(SplatRec) == 48, "SplatRec must stay 48 B");
 
+// Per-(Gaussian, mask) weight scalars (mask_weights, pipeline.hpp:25-49):
+// f32 by default; with SS_OPT_DETERMINISTIC u64 fixed point in units of
+// 2^-32.  Every value the compositor adds is an f32 sum of emitted weights,
+// each >= 1/255 > 2^-8, hence a multiple of 2^-31: the integer atomics add it
+// exactly and in any order, so the scalars -- and everything contracted from
+// them -- are bitwise identical run to run and for any lane count (the
+// reference's determinism contract, pipeline.hpp:272-279), where f32 atomics
+// round in arrival order.  (Measured on c4: 3.6 % slower, the 64-bit
+// atomics and the doubled scalar reads.)
+typedef unsigned long long acc_t;
+__device__ __forceinline__ acc_t acc_fix(float v) { return __float2ull_rn(v * 4294967296.0f); }
+__device__ __forceinline__ float acc_val(acc_t a) { return __ull2float_rn(a) * 2.3283064365386963e-10f; }
+
 // Per-view scalars kept on the device; the host reads them only at batch
 // boundaries (copied into a per-view status array), never per view.
 struct ViewInfo {
@@ -83,7 +96,8 @@ struct RasterParams {
     uint32_t mask_words, n_masks;  // words of this pass's window (1, 2 or 4); masks of the view
     uint32_t bits_stride;          // words per pixel in pix_bits (= mask_words unless windowed)
     uint32_t mask_base;            // first mask of the window (multiple of 128; word offset mask_base / 32)
-    float* acc;                    // [N * n_masks] per-(Gaussian, mask) scalars
+    void* acc;                     // [N * n_masks] per-(Gaussian, mask) scalars: float, or acc_t (KIND 4)
+    uint32_t acc_fix;              // scalars are acc_t (SS_OPT_DETERMINISTIC): the compositor runs KIND 4
     uint32_t* touched;             // [N] generation stamp of the last view that touched the Gaussian
     uint32_t* touched_list;        // [N] Gaussian ids touched in this view
     unsigned long long* touched_count; // entries of touched_list

@@ -845,14 +845,14 @@ template <bool DIM512, bool CLIP_SMEM = false>
 __device__ __forceinline__ void contract_member(const ContractMember& m, uint32_t gid, uint32_t lane, uint32_t dim,
                                                 float* row, float4 (&racc)[4], float& wsum,
                                                 unsigned long long& pairs) {
-    float* accrow = m.acc + (size_t)gid * m.n_masks;
+    const AccRow accrow = acc_row(m, gid);
     float vsum = 0.0f;
     for (uint32_t c = 0; c < m.n_masks; c += 32) {
         const uint32_t mi = c + lane;
         float v = 0.0f;
         if (mi < m.n_masks) {
-            v = accrow[mi];
-            if (v != 0.0f) accrow[mi] = 0.0f;
+            v = accrow.get(mi);
+            if (v != 0.0f) accrow.clear(mi);
         }
         vsum += v;
         uint32_t bal = __ballot_sync(0xffffffffu, v != 0.0f);
@@ -964,9 +964,9 @@ __global__ void __launch_bounds__(kContractThreads, 1) contract_smem_kernel(Cont
 #pragma unroll
         for (int q = 0; q < 4; ++q) r[q] = row[lane + 32 * q];
         w = p.totals[gid];
-        const float* accrow = m.acc + (size_t)gid * M;
-        v0 = lane < M ? accrow[lane] : 0.0f;
-        v1 = lane + 32u < M ? accrow[lane + 32u] : 0.0f;
+        const AccRow accrow = acc_row(m, gid);
+        v0 = lane < M ? accrow.get(lane) : 0.0f;
+        v1 = lane + 32u < M ? accrow.get(lane + 32u) : 0.0f;
     };
     uint64_t t = warp0;
     if (t < total) {
@@ -986,13 +986,13 @@ __global__ void __launch_bounds__(kContractThreads, 1) contract_smem_kernel(Cont
             float nw = 0.0f, nv0 = 0.0f, nv1 = 0.0f;
             if (tn < total) fetch(ngid, nacc, nw, nv0, nv1);
             // contract_member<true, true> on the prefetched mask weights
-            float* accrow = m.acc + (size_t)gid * M;
+            const AccRow accrow = acc_row(m, gid);
             float vsum = 0.0f;
 #pragma unroll
             for (uint32_t c = 0; c < 64u; c += 32u) {
                 if (c >= M) break;
                 const float v = c == 0 ? v0 : v1;
-                if (v != 0.0f) accrow[c + lane] = 0.0f;
+                if (v != 0.0f) accrow.clear(c + lane);
                 vsum += v;
                 uint32_t bal = __ballot_sync(0xffffffffu, v != 0.0f);
                 pairs += __popc(bal);
@@ -1089,8 +1089,9 @@ __global__ void __launch_bounds__(256) group_union_kernel(ContractParams p, uint
 }
 
 // MEMBERS: views in the group (<= 3); CH: 32-mask chunks per view (2: M <= 64,
-// 4: M <= 128); DIRECT: a single view, walked through its own touched list.
-template <uint32_t H, uint32_t MEMBERS, uint32_t CH, bool DIRECT>
+// 4: M <= 128); DIRECT: a single view, walked through its own touched list;
+// FIX: the members' scalars are fixed point (SS_OPT_DETERMINISTIC).
+template <uint32_t H, uint32_t MEMBERS, uint32_t CH, bool DIRECT, bool FIX>
 __global__ void __launch_bounds__(1024, 1) contract_group_pass_kernel(ContractParams p, const uint2* ulist,
                                                                      const unsigned int* ucount) {
     extern __shared__ float4 sclip4[]; // per member: n_masks x 64 float4 (D-half H)
@@ -1135,10 +1136,10 @@ __global__ void __launch_bounds__(1024, 1) contract_group_pass_kernel(ContractPa
 #pragma unroll
             for (uint32_t c = 0; c < CH; ++c) x.v[j][c] = 0.0f;
             if (j < nm && ((u.y >> j) & 1u)) {
-                const float* accrow = p.m[j].acc + (size_t)u.x * p.m[j].n_masks;
+                const auto accrow = acc_row_t<FIX>(p.m[j], u.x);
 #pragma unroll
                 for (uint32_t c = 0; c < CH; ++c)
-                    if (32u * c + lane < p.m[j].n_masks) x.v[j][c] = accrow[32u * c + lane];
+                    if (32u * c + lane < p.m[j].n_masks) x.v[j][c] = accrow.get(32u * c + lane);
             }
         }
     };
@@ -1160,14 +1161,14 @@ __global__ void __launch_bounds__(1024, 1) contract_group_pass_kernel(ContractPa
             for (uint32_t j = 0; j < MEMBERS; ++j) {
                 if (j >= nm || !((u.y >> j) & 1u)) continue;
                 const uint32_t M = p.m[j].n_masks;
-                float* accrow = p.m[j].acc + (size_t)u.x * M;
+                const auto accrow = acc_row_t<FIX>(p.m[j], u.x);
                 const float4* clip = sclip4 + soff[j];
                 float vsum = 0.0f;
 #pragma unroll
                 for (uint32_t c = 0; c < CH; ++c) {
                     if (32u * c >= M) break;
                     const float v = cur.v[j][c];
-                    if (H && v != 0.0f) accrow[32u * c + lane] = 0.0f;
+                    if (H && v != 0.0f) accrow.clear(32u * c + lane);
                     vsum += v;
                     uint32_t bal = __ballot_sync(0xffffffffu, v != 0.0f);
                     if (H) pairs += __popc(bal);
@@ -1870,17 +1871,31 @@ cudaError_t launch_contract(const ContractParams& p, uint64_t max_touched, cudaS
     }
     static std::atomic<int> configured_g[64] = {};
     if (dev >= 0 && dev < 64 && !configured_g[dev].load()) {
-        const void* ks[] = {(const void*)contract_group_pass_kernel<0, 3, 2, false>,
-                            (const void*)contract_group_pass_kernel<1, 3, 2, false>,
-                            (const void*)contract_group_pass_kernel<0, 1, 4, true>,
-                            (const void*)contract_group_pass_kernel<1, 1, 4, true>};
+        const void* ks[] = {(const void*)contract_group_pass_kernel<0, 3, 2, false, false>,
+                            (const void*)contract_group_pass_kernel<1, 3, 2, false, false>,
+                            (const void*)contract_group_pass_kernel<0, 1, 4, true, false>,
+                            (const void*)contract_group_pass_kernel<1, 1, 4, true, false>,
+                            (const void*)contract_group_pass_kernel<0, 3, 2, false, true>,
+                            (const void*)contract_group_pass_kernel<1, 3, 2, false, true>,
+                            (const void*)contract_group_pass_kernel<0, 1, 4, true, true>,
+                            (const void*)contract_group_pass_kernel<1, 1, 4, true, true>};
         for (const void* k : ks) {
             cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 192 * 1024);
             if (e != cudaSuccess) return e;
         }
         configured_g[dev].store(1);
     }
-    if (p.n_members >= 2 && p.n_members < kMaxGroup && p.dim == 512 && small && group_masks <= 192 && p.union_list) {
+    // the group kernels take the scalars' representation as a template
+    // parameter; a group mixing both (the option changed mid-group) takes the
+    // general kernel
+    bool any_fix = false, all_fix = true;
+    for (uint32_t i = 0; i < p.n_members; ++i) {
+        any_fix = any_fix || p.m[i].fix;
+        all_fix = all_fix && p.m[i].fix;
+    }
+    const bool mixed = any_fix && !all_fix;
+    if (!mixed && p.n_members >= 2 && p.n_members < kMaxGroup && p.dim == 512 && small && group_masks <= 192 &&
+        p.union_list) {
         cudaError_t e = cudaMemsetAsync(p.union_count, 0, sizeof(unsigned int), s);
         if (e != cudaSuccess) return e;
         group_union_kernel<<<(unsigned)sms * 4u, 256, 0, s>>>(p, p.union_list, p.union_count);
@@ -1890,15 +1905,25 @@ cudaError_t launch_contract(const ContractParams& p, uint64_t max_touched, cudaS
             return launch_contract_tc(p, p.tc_scratch, full, s);
         }
         const size_t smem = (size_t)group_masks * 1024u;
-        contract_group_pass_kernel<0, 3, 2, false><<<sms, 1024, smem, s>>>(p, p.union_list, p.union_count);
-        contract_group_pass_kernel<1, 3, 2, false><<<sms, 1024, smem, s>>>(p, p.union_list, p.union_count);
+        if (all_fix) {
+            contract_group_pass_kernel<0, 3, 2, false, true><<<sms, 1024, smem, s>>>(p, p.union_list, p.union_count);
+            contract_group_pass_kernel<1, 3, 2, false, true><<<sms, 1024, smem, s>>>(p, p.union_list, p.union_count);
+        } else {
+            contract_group_pass_kernel<0, 3, 2, false, false><<<sms, 1024, smem, s>>>(p, p.union_list, p.union_count);
+            contract_group_pass_kernel<1, 3, 2, false, false><<<sms, 1024, smem, s>>>(p, p.union_list, p.union_count);
+        }
         return cudaGetLastError();
     }
     if (p.n_members == 1 && p.dim == 512 && p.m[0].n_masks <= 128) {
         // one view with 65..128 masks: its CLIP half-rows (<= 128 KB) per pass
         const size_t smem = (size_t)p.m[0].n_masks * 1024u;
-        contract_group_pass_kernel<0, 1, 4, true><<<sms, 1024, smem, s>>>(p, nullptr, nullptr);
-        contract_group_pass_kernel<1, 1, 4, true><<<sms, 1024, smem, s>>>(p, nullptr, nullptr);
+        if (all_fix) {
+            contract_group_pass_kernel<0, 1, 4, true, true><<<sms, 1024, smem, s>>>(p, nullptr, nullptr);
+            contract_group_pass_kernel<1, 1, 4, true, true><<<sms, 1024, smem, s>>>(p, nullptr, nullptr);
+        } else {
+            contract_group_pass_kernel<0, 1, 4, true, false><<<sms, 1024, smem, s>>>(p, nullptr, nullptr);
+            contract_group_pass_kernel<1, 1, 4, true, false><<<sms, 1024, smem, s>>>(p, nullptr, nullptr);
+        }
         return cudaGetLastError();
     }
     if (p.dim == 512)

@@ -1,5 +1,7 @@
 // Launchers of the non-exact kernels (ss_kernels.cu).
 #pragma once
+#include <type_traits>
+
 #include "ss_internal.cuh"
 
 namespace ss {
@@ -10,10 +12,45 @@ struct ContractMember {
     const unsigned long long* touched_count;
     const uint32_t* touched;             // generation stamps
     uint32_t gen;                        // the view's stamp
-    float* acc;                          // [N x n_masks], consumed and cleared
+    void* acc;                           // [N x n_masks] float (or acc_t if fix), consumed and cleared
+    uint32_t fix;                        // scalars in fixed point (SS_OPT_DETERMINISTIC)
     uint32_t n_masks;
     const float* clip;                   // [n_masks x dim]
 };
+
+// One Gaussian's row of a member's scalars, in either representation.
+struct AccRow {
+    void* p;
+    bool fix;
+    __device__ __forceinline__ float get(uint32_t i) const {
+        return fix ? acc_val(static_cast<const acc_t*>(p)[i]) : static_cast<const float*>(p)[i];
+    }
+    __device__ __forceinline__ void clear(uint32_t i) const {
+        if (fix) static_cast<acc_t*>(p)[i] = 0ull;
+        else static_cast<float*>(p)[i] = 0.0f;
+    }
+};
+__device__ __forceinline__ AccRow acc_row(const ContractMember& m, uint64_t gid) {
+    const size_t off = (size_t)gid * m.n_masks;
+    return AccRow{m.fix ? (void*)(static_cast<acc_t*>(m.acc) + off) : (void*)(static_cast<float*>(m.acc) + off),
+                  m.fix != 0};
+}
+
+// The same with the representation fixed at compile time (the hot group kernels).
+template <bool FIX>
+struct AccRowT {
+    using T = typename std::conditional<FIX, acc_t, float>::type;
+    T* p;
+    __device__ __forceinline__ float get(uint32_t i) const {
+        if constexpr (FIX) return acc_val(p[i]);
+        else return p[i];
+    }
+    __device__ __forceinline__ void clear(uint32_t i) const { p[i] = T(0); }
+};
+template <bool FIX>
+__device__ __forceinline__ AccRowT<FIX> acc_row_t(const ContractMember& m, uint64_t gid) {
+    return AccRowT<FIX>{static_cast<typename AccRowT<FIX>::T*>(m.acc) + (size_t)gid * m.n_masks};
+}
 
 constexpr uint32_t kMaxGroup = 4;
 

@@ -6,6 +6,7 @@
 // run by tests/test_gpu_dropin.py on the GPU box.
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <filesystem>
 #include <random>
 #include <string>
@@ -122,6 +123,16 @@ int main() {
             CHECK(stats.worker_images == ref_stats.worker_images);
             CHECK(stats.worker_entries == ref_stats.worker_entries); // (gid, mask) entries per worker
         }
+        // pipeline.hpp:272-279: with SS_OPT_DETERMINISTIC the table is bitwise
+        // identical run to run
+        b200::set_deterministic(true);
+        const EmbeddingTable d1 = b200::encode_scene(scene, manifest, 1, 0);
+        const EmbeddingTable d2 = b200::encode_scene(scene, manifest, 1, 0);
+        b200::set_deterministic(false);
+        CHECK(max_row_rel_diff(ref, d1) <= 1e-4);
+        CHECK(d1.embeddings.size() == d2.embeddings.size() && d1.coverage.size() == d2.coverage.size() &&
+              std::memcmp(d1.embeddings.data(), d2.embeddings.data(), d1.embeddings.size() * sizeof(float)) == 0 &&
+              std::memcmp(d1.coverage.data(), d2.coverage.data(), d1.coverage.size() * sizeof(float)) == 0);
     }
 
     // --- failure paths (test_pipeline.cpp:356-393)

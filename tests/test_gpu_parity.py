@@ -243,29 +243,36 @@ def test_group_contraction_d512(gpu_ctx, oracle, m):
     """D = 512 views with <= 64 masks are contracted in groups (auto: three at a
     time; the two-pass shared-memory group kernels), including a partial last
     group and a view with more masks that is contracted alone.  The per-row
-    contraction order is the single-view one; the compositor's fp32 atomics
-    into the per-(Gaussian, mask) scalars make runs differ in the last bits,
-    so configurations agree to 1e-5 relative per row with identical covered
-    sets, and each matches the oracle to the north-star tolerance."""
+    contraction order is the single-view one; with SS_OPT_DETERMINISTIC the
+    per-(Gaussian, mask) scalars are exact fixed-point sums, so every CUDA-core
+    configuration is bitwise identical; with the default f32 atomics (last-bit
+    run-to-run differences) and on the tensor cores (split-fp16 operands)
+    configurations agree to 1e-5 relative per row; each matches the oracle to
+    the north-star tolerance."""
     wl = _bench_style(4000, 8, 80, 64, m, 512, seed=77)
     big = _bench_style(4000, 1, 80, 64, 100, 512, seed=78)
     cams = wl.cams[:5] + big.cams + wl.cams[5:]
     masks = wl.masks[:5] + big.masks + wl.masks[5:]
     out = {}
     try:
-        for lanes, group, tc in [(4, 1, 0), (4, 0, 0), (4, 2, 0), (4, 3, 0), (1, 3, 0), (2, 0, 0), (4, 0, 1),
-                                 (1, 2, 1)]:
-            gpu_ctx.set_lanes(lanes)
-            gpu_ctx.set_contract_group(group)
-            gpu_ctx.set_contract_tc(tc)  # SS_OPT_CONTRACT_TC: groups on the tensor cores
-            out[(lanes, group, tc)] = _encode(gpu_ctx, wl.scene, cams, masks, 512)
+        for det in (1, 0):
+            gpu_ctx.set_deterministic(det)
+            for lanes, group, tc in [(4, 1, 0), (4, 0, 0), (4, 2, 0), (4, 3, 0), (1, 3, 0), (2, 0, 0), (4, 0, 1),
+                                     (1, 2, 1)]:
+                gpu_ctx.set_lanes(lanes)
+                gpu_ctx.set_contract_group(group)
+                gpu_ctx.set_contract_tc(tc)  # SS_OPT_CONTRACT_TC: groups on the tensor cores
+                out[(lanes, group, tc, det)] = _encode(gpu_ctx, wl.scene, cams, masks, 512)
     finally:
         gpu_ctx.set_lanes(4)
         gpu_ctx.set_contract_group(0)
         gpu_ctx.set_contract_tc(0)
+        gpu_ctx.set_deterministic(0)
     er, ec = oracle.encode(wl.scene, cams, masks, 512)
-    ref_rows, ref_cov = out[(4, 1, 0)]
+    ref_rows, ref_cov = out[(4, 1, 0, 1)]
     for key, (rows, cov) in out.items():
+        if key[2] == 0 and key[3] == 1:
+            assert np.array_equal(rows, ref_rows) and np.array_equal(cov, ref_cov), key
         rel, cos = row_errors(rows, cov, ref_rows, ref_cov)
         assert rel <= 1e-5, (key, rel)
         rel, cos = row_errors(rows, cov, er, ec)
@@ -289,6 +296,34 @@ def test_encode_lane_count_does_not_change_results(gpu_ctx, oracle, lanes, group
     rel, cos = row_errors(rows, cov, er, ec)
     assert rel <= EMB_REL_TOL and cos >= EMB_COS_TOL, (lanes, rel, cos)
     np.testing.assert_allclose(cov, ec, rtol=1e-5)
+
+
+def test_encode_is_bitwise_deterministic(gpu_ctx, oracle):
+    """pipeline.hpp:272-279: for a fixed worker count the table is bitwise
+    identical run to run.  With SS_OPT_DETERMINISTIC the compositor adds exact
+    f32 group sums into u64 fixed-point scalars (integer atomics: any arrival
+    order gives the same bits) and the contraction runs in view order, so
+    repeated runs -- and every lane count and contraction grouping -- give the
+    same bits, which also match the oracle."""
+    wl = _bench_style(4000, 7, 80, 64, 40, 512, seed=93)
+    runs = []
+    try:
+        gpu_ctx.set_deterministic(1)
+        for lanes, group in [(5, 0), (5, 0), (1, 1), (3, 3), (2, 2), (6, 0)]:
+            gpu_ctx.set_lanes(lanes)
+            gpu_ctx.set_contract_group(group)
+            runs.append(((lanes, group), _encode(gpu_ctx, wl.scene, wl.cams, wl.masks, 512)))
+    finally:
+        gpu_ctx.set_lanes(4)
+        gpu_ctx.set_contract_group(0)
+        gpu_ctx.set_deterministic(0)
+    (_, (rows0, cov0)) = runs[0]
+    assert np.count_nonzero(cov0) > 100
+    for key, (rows, cov) in runs[1:]:
+        assert np.array_equal(rows, rows0) and np.array_equal(cov, cov0), key
+    er, ec = oracle.encode(wl.scene, wl.cams, wl.masks, 512)
+    rel, cos = row_errors(rows0, cov0, er, ec)
+    assert rel <= EMB_REL_TOL and cos >= EMB_COS_TOL, (rel, cos)
 
 
 def test_encode_falloff_mode_vs_oracle(gpu_ctx, oracle):
