@@ -129,7 +129,7 @@ int ss_synchronize(ss_ctx* ctx);
  * f32 >= 1/255, a multiple of 2^-31, so the additions are exact in any
  * order and the table is bitwise identical run to run and for every lane
  * count and contraction grouping (pipeline.hpp:272-279); 0 = f32 atomics
- * (default: 3.6 % faster on c4; results differ run to run in the last bits,
+ * (default: 4-5 % faster on c4; results differ run to run in the last bits,
  * well inside the path's tolerance).  Set before ss_encode_begin. */
 enum ss_option {
     SS_OPT_LANES = 1,

@@ -320,7 +320,7 @@ inline ViewData read_view(const DatasetManifest& manifest, const ImageEntry& ent
 
 // SS_OPT_DETERMINISTIC for encode_scene: fixed-point per-(Gaussian, mask)
 // scalars, so the table is bitwise identical run to run (the reference's
-// contract for a fixed worker count, pipeline.hpp:272-279) at ~3.6 % of c4
+// contract for a fixed worker count, pipeline.hpp:272-279) at ~4-5 % of c4
 // throughput.  Off by default (f32 atomics: last-bit differences between
 // runs, inside the path's tolerance).
 inline std::atomic<bool>& deterministic_flag() {

@@ -32,7 +32,7 @@ static_assert(sizeof(SplatRec) == 48, "SplatRec must stay 48 B");
 // exactly and in any order, so the scalars -- and everything contracted from
 // them -- are bitwise identical run to run and for any lane count (the
 // reference's determinism contract, pipeline.hpp:272-279), where f32 atomics
-// round in arrival order.  (Measured on c4: 3.6 % slower, the 64-bit
+// round in arrival order.  (Measured on c4: 4-5 % slower, the 64-bit
 // atomics and the doubled scalar reads.)
 typedef unsigned long long acc_t;
 __device__ __forceinline__ acc_t acc_fix(float v) { return __float2ull_rn(v * 4294967296.0f); }

@@ -594,7 +594,7 @@ __device__ __forceinline__ void for_box_tiles(uint2 box, uint32_t tiles_x, F&& f
         for (uint32_t tx = tx0; tx <= tx1; ++tx) f(ty * tiles_x + tx);
 }
 
-__global__ void __launch_bounds__(kTsThreads) ts_scatter_kernel(TileSortParams p) {
+__global__ void __launch_bounds__(kTsThreads, 2048 / kTsThreads) ts_scatter_kernel(TileSortParams p) {
     extern __shared__ uint32_t hist[]; // [tiles]: counts, then cursors
     __shared__ uint32_t s_over;        // a tile of this chunk outgrew its capacity
     const uint64_t base = (uint64_t)blockIdx.x * kTsChunk;
@@ -623,15 +623,26 @@ __global__ void __launch_bounds__(kTsThreads) ts_scatter_kernel(TileSortParams p
         k32[g] = box[g].x != kCulledBox ? (uint32_t)((__ldg(p.keys + id) - mn) >> sh) : 0u; // monotone in depth
     }
     __syncthreads();
-    // reserve each touched tile's slots: one global atomic per (chunk, tile)
+    // reserve each touched tile's slots: one global atomic per (chunk, tile),
+    // a thread's (up to 4) reservations in flight together
     uint32_t mine = 0, mfill = 0;
-    for (uint32_t t = threadIdx.x; t < p.tiles; t += blockDim.x) {
-        const uint32_t c = hist[t];
-        if (!c) continue;
-        mine += c;
-        const uint32_t b = atomicAdd(p.fill + t, c);
-        mfill = max(mfill, b + c);
-        hist[t] = t * p.cap + b;
+    for (uint32_t t0 = threadIdx.x; t0 < p.tiles; t0 += 4u * blockDim.x) {
+        uint32_t c[4], b[4];
+#pragma unroll
+        for (uint32_t k = 0; k < 4; ++k) {
+            const uint32_t t = t0 + k * blockDim.x;
+            c[k] = t < p.tiles ? hist[t] : 0u;
+        }
+#pragma unroll
+        for (uint32_t k = 0; k < 4; ++k) b[k] = c[k] ? atomicAdd(p.fill + t0 + k * blockDim.x, c[k]) : 0u;
+#pragma unroll
+        for (uint32_t k = 0; k < 4; ++k) {
+            if (!c[k]) continue;
+            const uint32_t t = t0 + k * blockDim.x;
+            mine += c[k];
+            mfill = max(mfill, b[k] + c[k]);
+            hist[t] = t * p.cap + b[k];
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
