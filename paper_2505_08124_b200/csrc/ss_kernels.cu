@@ -819,19 +819,26 @@ __global__ void __launch_bounds__(kTsSortThreads, MIN_CTAS) tile_sort_kernel(Til
                 s_fail = 1u;
                 continue;
             }
-            unsigned long long kx = 0ull;
-            bool have_kx = false;
+            // branch-free count of the members with a smaller narrowed key;
+            // equal narrowed keys (rare: 2^32 levels over the view's depth
+            // range) take the exact pass below
+            uint32_t lt = 0, tie = 0;
             for (uint32_t c = s0; c < e0; ++c) {
                 const uint2 y = out[c];
-                bool before = y.x < x.x;
-                if (y.x == x.x && y.y != x.y) { // equal narrowed keys: the full depth bits, then the id
-                    if (!have_kx) {
-                        kx = __ldg(p.keys + x.y);
-                        have_kx = true;
-                    }
-                    before = depth_before(__ldg(p.keys + y.y), y.y, kx, x.y);
+                lt += y.x < x.x ? 1u : 0u;
+                tie |= (y.x == x.x) & (y.y != x.y);
+            }
+            if (!tie) {
+                pos += lt;
+            } else {
+                const unsigned long long kx = __ldg(p.keys + x.y);
+                for (uint32_t c = s0; c < e0; ++c) {
+                    const uint2 y = out[c];
+                    bool before = y.x < x.x;
+                    if (y.x == x.x && y.y != x.y) // equal narrowed keys: the full depth bits, then the id
+                        before = depth_before(__ldg(p.keys + y.y), y.y, kx, x.y);
+                    pos += before ? 1u : 0u;
                 }
-                pos += before ? 1u : 0u;
             }
         }
         dst[pos] = x.y;
