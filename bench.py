@@ -78,6 +78,8 @@ def parse():
     ap.add_argument("--group", type=int, default=0, help="views per contraction group (0 = library default)")
     ap.add_argument("--bin", type=int, default=0, help="tile binning: 0 auto, 1 key sort, 2 direct")
     ap.add_argument("--raster", type=int, default=-1, help="compositor: 2 per-step on work-stealing warps (library default), 1 per-step CTA per tile, 0 staged")
+    ap.add_argument("--sort-prefix", type=int, default=-1,
+                    help="SS_OPT_SORT_PREFIX (-1 = library default, 0 = full tile sorts)")
     ap.add_argument("--deterministic", action="store_true",
                     help="SS_OPT_DETERMINISTIC: fixed-point per-(Gaussian, mask) scalars (bitwise run-to-run)")
     ap.add_argument("--combine-rows", type=int, default=0,
@@ -410,6 +412,8 @@ def main():
         ctx.set_raster_algo(args.raster)
     if args.deterministic:
         ctx.set_deterministic(True)
+    if args.sort_prefix >= 0:
+        ctx.set_sort_prefix(args.sort_prefix)
 
     # device-resident inputs for `value`
     dev = torch.device("cuda", local)

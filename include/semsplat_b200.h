@@ -130,7 +130,14 @@ int ss_synchronize(ss_ctx* ctx);
  * order and the table is bitwise identical run to run and for every lane
  * count and contraction grouping (pipeline.hpp:272-279); 0 = f32 atomics
  * (default: 4-5 % faster on c4; results differ run to run in the last bits,
- * well inside the path's tolerance).  Set before ss_encode_begin. */
+ * well inside the path's tolerance).  Set before ss_encode_begin.
+ * SS_OPT_SORT_PREFIX: in the fused pass (alpha-composited, <= 128 masks) a
+ * tile of n > P instances is put in (depth, id) order only over its first
+ * max(P, n / 4) instances (whole key buckets, exactly the head of the full
+ * order); a compositor block that reaches the end of that prefix with pixels
+ * still compositing saves its transmittances, the tile is then sorted in full
+ * and the block resumes where it stopped -- the same per-pixel sequence, the
+ * same bits.  0 = full sorts; default 1024. */
 enum ss_option {
     SS_OPT_LANES = 1,
     SS_OPT_QUERY_PATH = 2,
@@ -140,7 +147,8 @@ enum ss_option {
     SS_OPT_COMBINE_ROWS = 6,
     SS_OPT_CONTRACT_TC = 7,
     SS_OPT_COMBINE_SPARSE = 8,
-    SS_OPT_DETERMINISTIC = 9
+    SS_OPT_DETERMINISTIC = 9,
+    SS_OPT_SORT_PREFIX = 10
 };
 int ss_set_option(ss_ctx* ctx, int option, int64_t value);
 

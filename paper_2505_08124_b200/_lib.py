@@ -182,6 +182,10 @@ class Context:
         """SS_OPT_CONTRACT_TC: groups of 2-3 views on the tensor cores."""
         check(self._L.ss_set_option(self.h, 7, int(bool(on))))
 
+    def set_sort_prefix(self, n: int):
+        """SS_OPT_SORT_PREFIX: tile lists of the fused pass ranked over a prefix (0 = full sorts)."""
+        check(self._L.ss_set_option(self.h, 10, int(n)))
+
     def set_deterministic(self, on: bool):
         """SS_OPT_DETERMINISTIC: fixed-point per-(Gaussian, mask) scalars, bitwise run-to-run results."""
         check(self._L.ss_set_option(self.h, 9, int(bool(on))))

@@ -28,6 +28,12 @@
 #include <cub/iterator/counting_input_iterator.cuh>
 
 #include "ss_kernels.cuh"
+
+// SS_OPT_SORT_PREFIX default: tiles of more than this many instances are
+// ranked over their first max(this, n / 4) instances in the fused pass
+#ifndef SS_SORT_PREFIX_DEFAULT
+#define SS_SORT_PREFIX_DEFAULT 1024
+#endif
 #include "ss_query_tc.cuh"
 
 namespace ss {
@@ -156,6 +162,11 @@ struct Lane {
     DevBuf bin_counts, bin_slice, bin_tot, bin_done; // direct binning scratch
     DevBuf ts_fill, ts_slab;       // tile-sort binning: per-tile fill counters, unordered (key, gid) slots
     DevBuf raster_work;            // work-stealing compositor counters (zero between launches)
+    // prefix-sorted tile lists (SS_OPT_SORT_PREFIX): saved block state of the
+    // fused pass, queued blocks / tiles, the fixup sort's parameters
+    DevBuf rs_T, rs_state, rs_items, rs_tiles, rs_need, rs_count;
+    uint32_t rs_tiles_cap = 0;     // tiles the rs_* buffers hold
+    TileSortParams ts_params{};    // the view's tile-sort binning (for the fixup sort)
     uint32_t ts_cap = kTileSortMax / 2; // tile-sort slots per tile: grows to kTileSortMax when a tile
                                         // outgrows it (larger tiles take the global path)
     uint64_t iota_n = 0;           // entries of the 0..n-1 sequence in `iota`
@@ -167,7 +178,8 @@ struct Lane {
     void release_all() {
         DevBuf* b[] = {&rec, &boxes, &rbox, &rcnt, &keys, &k32, &k32s, &order, &iota, &offsets, &tkeys, &tkeys_sorted, &tvals, &tile_start,
                        &tile_end, &list, &cub_tmp, &info, &raster_work, &pix_bits, &mask_bits, &bin_counts, &bin_slice, &bin_tot, &bin_done,
-                       &runs, &run_offsets, &spans, &ts_fill, &ts_slab};
+                       &runs, &run_offsets, &spans, &ts_fill, &ts_slab, &rs_T, &rs_state, &rs_items, &rs_tiles,
+                       &rs_need, &rs_count};
         for (auto* x : b) x->release();
         for (auto& cs : sets) cs.release();
         if (raster_done) cudaEventDestroy(raster_done);
@@ -257,6 +269,7 @@ struct ss_ctx {
     int query_path = 0; // SS_OPT_QUERY_PATH
     int bin_path = 0;   // SS_OPT_BIN_PATH
     int contract_tc = 0; // SS_OPT_CONTRACT_TC
+    uint32_t sort_prefix = SS_SORT_PREFIX_DEFAULT; // SS_OPT_SORT_PREFIX (0: full tile sorts)
     bool deterministic = false; // SS_OPT_DETERMINISTIC: fixed-point per-(Gaussian, mask) scalars
     int raster_algo = 2; // SS_OPT_RASTER (2 = per-step compositor on work-stealing warps, the fastest on c4)
     int num_sms = 0;
@@ -352,6 +365,7 @@ struct Geometry {
     uint32_t tiles_x = 0, tiles_y = 0, tiles = 0;
     bool k16 = true; // 16-bit tile keys
     bool tile_sort = false; // lists from the tile-sort binning (no global depth order)
+    bool prefix = false;    // tile lists sorted only over a prefix (fused pass resumes the rest)
 };
 
 // The fused pass bins by tile sort (SS_OPT_BIN_PATH 0 or 3) unless the view
@@ -367,7 +381,7 @@ bool use_tile_sort(const ss_ctx* c, uint32_t tiles, bool force_global) {
 // offsets and key ranges stay on the device; a view whose tile lists would
 // overflow the list buffer raises info->overflow and its compositor skips.
 Geometry run_geometry(ss_ctx* c, Lane& L, cudaStream_t s, const ss_camera& cam, bool force_global = false,
-                      bool need_order = false) {
+                      bool need_order = false, uint32_t prefix_min = 0) {
     Geometry g;
     const uint64_t N = c->n;
     g.tiles_x = (cam.width + kTile - 1) / kTile;
@@ -440,6 +454,34 @@ Geometry run_geometry(ss_ctx* c, Lane& L, cudaStream_t s, const ss_camera& cam, 
         tp.start = tstart;
         tp.end = tend;
         tp.info = info;
+        tp.prefix_min = 0;
+        tp.fix_tiles = nullptr;
+        tp.fix_count = nullptr;
+        tp.need = nullptr;
+        if (prefix_min && !need_order) {
+            // prefix mode: per-block resume state, zero / NaN between views
+            // (the resume and fixup kernels reset what they consume)
+            if (L.rs_tiles_cap < g.tiles) {
+                const uint64_t items = (uint64_t)g.tiles * 8u;
+                L.rs_T.release();
+                L.rs_state.release();
+                L.rs_need.release();
+                SS_CUDA(cudaMemsetAsync(L.rs_T.ensure(items * 32u * 8u), 0xff, items * 32u * 8u, s));
+                SS_CUDA(cudaMemsetAsync(L.rs_state.ensure(items * 8u), 0, items * 8u, s));
+                L.rs_items.ensure(items * 4u);
+                L.rs_tiles.ensure((uint64_t)g.tiles * 4u);
+                SS_CUDA(cudaMemsetAsync(L.rs_need.ensure((uint64_t)g.tiles * 4u), 0, (uint64_t)g.tiles * 4u, s));
+                L.rs_count.ensure(16);
+                L.rs_tiles_cap = g.tiles;
+            }
+            SS_CUDA(cudaMemsetAsync(L.rs_count.p, 0, 8, s));
+            tp.prefix_min = prefix_min;
+            tp.fix_tiles = L.rs_tiles.as<uint32_t>();
+            tp.fix_count = L.rs_count.as<uint32_t>();
+            tp.need = L.rs_need.as<uint32_t>();
+            g.prefix = true;
+        }
+        L.ts_params = tp;
         own_launch(c, launch_tile_sort_bin(tp, s), SS_K_BIN, 2);
         if (!need_order) return g;
     }
@@ -716,7 +758,15 @@ bool encode_one(ss_ctx* c, Lane& L, const ss_camera& cam, const ss_view_masks* v
         SS_CUDA(cudaMemcpyAsync(dc, vm->clip, (size_t)M * c->dim * 4, cudaMemcpyHostToDevice, s));
         c->prof.bytes[SS_K_H2D] += (double)M * c->dim * 4;
     }
-    const Geometry g = run_geometry(c, L, s, cam, force_global);
+    // prefix-sorted tile lists for the fused pass: one per-step compositor pass
+    // (<= 128 masks) in alpha-composited mode (falloff pixels never terminate;
+    // the staged-evaluation compositor has no resume path)
+    const bool staged = c->raster_algo == 0 && !c->deterministic;
+    const uint32_t prefix = M && c->sort_prefix && words <= (uint32_t)kMaxMaskWords && mode == SS_ALPHA_COMPOSITED &&
+                                    !staged
+                                ? c->sort_prefix
+                                : 0u;
+    const Geometry g = run_geometry(c, L, s, cam, force_global, false, prefix);
     if (M) {
         // per-(Gaussian, mask) scalars: grow-only and kept zero by consume-and-clear
         // (zero is all-zero bytes in both representations, so a set switches
@@ -752,11 +802,26 @@ bool encode_one(ss_ctx* c, Lane& L, const ss_camera& cam, const ss_view_masks* v
             p.touched_list = tlist;
             p.touched_count = tcount;
             p.gen = S->gen;
+            if (g.prefix) {
+                p.tile_full = L.ts_params.fill;
+                p.rs_T = L.rs_T.as<double>();
+                p.rs_state = L.rs_state.as<uint2>();
+                p.rs_items = L.rs_items.as<uint32_t>();
+                p.rs_count = L.rs_count.as<uint32_t>();
+                p.rs_tiles = L.rs_tiles.as<uint32_t>();
+                p.rs_need = L.rs_need.as<uint32_t>();
+            }
             // one pass per 128-mask window (a single pass for M <= 128)
             for (uint32_t w0 = 0; w0 < words; w0 += kMaxMaskWords) {
                 p.mask_words = std::min<uint32_t>(words - w0, kMaxMaskWords);
                 p.mask_base = 32u * w0;
                 own_launch(c, launch_raster_fused(p, mode, g.tiles, s), SS_K_RASTER);
+            }
+            if (g.prefix) {
+                // the tiles whose prefix some block exhausted: sorted in full,
+                // then those blocks continue where they stopped
+                own_launch(c, launch_tile_sort_fixup(L.ts_params, s), SS_K_RASTER);
+                own_launch(c, launch_raster_resume(p, mode, s), SS_K_RASTER);
             }
         }
         {
@@ -1174,6 +1239,9 @@ int ss_set_option(ss_ctx* c, int option, int64_t value) {
         } else if (option == SS_OPT_COMBINE_SPARSE) {
             if (value < 0 || value > 2) throw Error(SS_ERR_CONTRACT, "SS_OPT_COMBINE_SPARSE must be 0, 1 or 2");
             c->combine_sparse = (int)value;
+        } else if (option == SS_OPT_SORT_PREFIX) {
+            if (value < 0 || value > 65536) throw Error(SS_ERR_CONTRACT, "SS_OPT_SORT_PREFIX must be 0..65536");
+            c->sort_prefix = (uint32_t)value;
         } else if (option == SS_OPT_DETERMINISTIC) {
             if (value < 0 || value > 1) throw Error(SS_ERR_CONTRACT, "SS_OPT_DETERMINISTIC must be 0 or 1");
             c->deterministic = value != 0;

@@ -368,7 +368,9 @@ __device__ __forceinline__ uint32_t match_bits(const uint32_t (&bits)[MW]) {
 // KIND 4: KIND 2 with u64 fixed-point scalars (SS_OPT_DETERMINISTIC).
 // One warp composites one 8x4 block (bx0, by0) of a tile against the tile's
 // list: the body of raster_kernel / raster_persist_kernel.
-template <int KIND, bool FALLOFF, int MW>
+// RESUME: continue a block the prefix-sorted pass left unfinished, from its
+// saved list position and per-pixel transmittance (raster_resume_kernel).
+template <int KIND, bool FALLOFF, int MW, bool RESUME = false>
 __device__ __forceinline__ void composite_block(const RasterParams& p, uint32_t tile, uint32_t wb, uint32_t lane,
                                                 SplatRec* wrec, uint2* wmg, uint32_t srec_addr,
                                                 uint32_t stab_addr, uint32_t spix_addr) {
@@ -415,17 +417,31 @@ __device__ __forceinline__ void composite_block(const RasterParams& p, uint32_t 
     // the loop tests "still compositing" as the lane's bit (one LOP3 against
     // the staged splat's pixel mask); ps.done is not read below
     ps.lbit = ps.done ? 0u : 1u << lane;
+    uint32_t first = start;
+    if constexpr (RESUME) {
+        // the saved list position and transmittance; pixels that were not
+        // compositing at the end of the prefix saved nothing (NaN).  The slots
+        // are reset for the next view (T back to NaN, the block's flag to 0).
+        const uint32_t item = tile * 8u + wb;
+        first = p.rs_state[item].y;
+        double* tslot = p.rs_T + (size_t)item * 32u + lane;
+        ps.T = *tslot;
+        *tslot = __longlong_as_double(-1ll); // NaN
+        if (!(ps.T >= 0.0)) ps.lbit = 0u;
+        __syncwarp();
+        if (lane == 0) p.rs_state[item].x = 0u;
+    }
 
     // prefetch the first chunk's ranks and boxes
     uint32_t nr = 0;
     uint2 nbox = make_uint2(0u, 0u);
-    if (start + lane < end) {
-        nr = __ldg(p.tile_list + start + lane);
+    if (first + lane < end) {
+        nr = __ldg(p.tile_list + first + lane);
         nbox = __ldg(p.boxes + nr);
     }
     const uint32_t lane_bit = 1u << lane;
     uint32_t mg_addr = (uint32_t)__cvta_generic_to_shared(wmg);
-    for (uint32_t base = start; base < end; base += 32u) {
+    for (uint32_t base = first; base < end; base += 32u) {
         const uint32_t live = __ballot_sync(0xffffffffu, ps.lbit != 0u);
         if (live == 0u) break;
         const uint32_t i = base + lane;
@@ -500,6 +516,28 @@ __device__ __forceinline__ void composite_block(const RasterParams& p, uint32_t 
                 }
             }
             if (__all_sync(0xffffffffu, ps.lbit == 0u)) break;
+        }
+        if constexpr ((KIND == 2 || KIND == 4) && !RESUME) {
+            if (base + 32u >= end && p.tile_full && ps.lbit) {
+                // this pixel is still compositing at the end of the list.  The
+                // block is re-derived from the pixel; if the tile's list is only
+                // a prefix, save the pixel's transmittance and queue the block
+                // (first such lane) and its tile: it resumes after the fixup
+                // sort completes the tile (raster_resume_kernel)
+                double dpx, dpy;
+                asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(dpx), "=d"(dpy) : "r"(pix_addr));
+                const uint32_t px = (uint32_t)dpx, py = (uint32_t)dpy;
+                const uint32_t rt = (py / kTile) * p.tiles_x + px / kTile;
+                const uint32_t item = rt * 8u + ((py % kTile) >> 2) * 2u + ((px % kTile) >> 3);
+                if (end - p.tile_start[rt] < p.tile_full[rt]) {
+                    p.rs_T[(size_t)item * 32u + (px & 7u) + 8u * (py & 3u)] = ps.T;
+                    if (atomicExch(&p.rs_state[item].x, 1u) == 0u) {
+                        p.rs_state[item].y = end;
+                        p.rs_items[atomicAdd(p.rs_count, 1u)] = item;
+                        if (atomicExch(p.rs_need + rt, 1u) == 0u) p.rs_tiles[atomicAdd(p.rs_count + 1, 1u)] = rt;
+                    }
+                }
+            }
         }
         __syncwarp();
     }
@@ -586,6 +624,30 @@ __global__ void __launch_bounds__(kRasterThreads, 6) raster_persist_kernel(Raste
     if (lane == 0 && atomicAdd(p.work + 1, 1u) == gridDim.x * (kRasterThreads / 32u) - 1u) {
         p.work[0] = 0u;
         p.work[1] = 0u;
+    }
+}
+
+// The blocks a prefix-sorted fused pass saved (rs_items), after the fixup
+// sort completed their tiles' lists: each warp takes items in turn and
+// continues from the saved list position with the saved transmittance --
+// the same front-to-back sequence per pixel as one uninterrupted walk.
+template <int KIND, bool FALLOFF, int MW>
+__global__ void __launch_bounds__(kRasterThreads, 6) raster_resume_kernel(RasterParams p) {
+    __shared__ SplatRec srec[kRasterThreads];
+    __shared__ uint2 smg[kRasterThreads];
+    __shared__ unsigned long long stab[256];
+    __shared__ double2 spix[SS_PIX_SMEM ? kRasterThreads : 1];
+    stab[threadIdx.x] = kExpTab[threadIdx.x];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    __syncthreads(); // exp table staged
+    if (p.info->overflow) return;
+    const uint32_t n_items = p.rs_count[0];
+    for (uint32_t k = blockIdx.x * (kRasterThreads / 32u) + warp; k < n_items; k += gridDim.x * (kRasterThreads / 32u)) {
+        const uint32_t item = p.rs_items[k];
+        composite_block<KIND, FALLOFF, MW, true>(p, item >> 3, item & 7u, lane, srec + 32u * warp, smg + 32u * warp,
+                                                 (uint32_t)__cvta_generic_to_shared(srec + 32u * warp),
+                                                 (uint32_t)__cvta_generic_to_shared(stab),
+                                                 (uint32_t)__cvta_generic_to_shared(spix + (SS_PIX_SMEM ? 32u * warp : 0u)));
     }
 }
 
@@ -935,6 +997,33 @@ cudaError_t launch_raster_capture(const RasterParams& p, int mode, uint32_t tile
 }
 cudaError_t launch_raster_render(const RasterParams& p, int mode, uint32_t tiles, cudaStream_t s) {
     return launch_raster<3>(p, mode, tiles, s);
+}
+
+cudaError_t launch_raster_resume(const RasterParams& p, int mode, cudaStream_t s) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const bool fo = mode == SS_FALLOFF_ONLY;
+#define SS_RESUME(K, MWV)                                                         \
+    do {                                                                          \
+        if (fo) raster_resume_kernel<K, true, MWV><<<sms, kRasterThreads, 0, s>>>(p); \
+        else raster_resume_kernel<K, false, MWV><<<sms, kRasterThreads, 0, s>>>(p);   \
+    } while (0)
+#define SS_RESUME_MW(MWV)                   \
+    do {                                    \
+        if (p.acc_fix) SS_RESUME(4, MWV);   \
+        else SS_RESUME(2, MWV);             \
+    } while (0)
+    switch (p.mask_words) {
+    case 1: SS_RESUME_MW(1); break;
+    case 2: SS_RESUME_MW(2); break;
+    case 3:
+    case 4: SS_RESUME_MW(4); break;
+    default: return cudaErrorInvalidValue;
+    }
+#undef SS_RESUME_MW
+#undef SS_RESUME
+    return cudaGetLastError();
 }
 
 cudaError_t launch_raster_fused(const RasterParams& p, int mode, uint32_t tiles, cudaStream_t s) {

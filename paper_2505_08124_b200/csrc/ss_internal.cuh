@@ -103,6 +103,17 @@ struct RasterParams {
     unsigned long long* touched_count; // entries of touched_list
     uint32_t gen;                  // this view's stamp (never 0)
     ViewInfo* info;
+    // prefix-sorted tile lists (fused pass, SS_OPT_SORT_PREFIX): tile t's list
+    // holds the first end - start of tile_full[t] instances; a block that
+    // exhausts it with live pixels saves its state and is resumed after the
+    // fixup sort (raster_resume_kernel)
+    const uint32_t* tile_full;     // [tiles] instances per tile, or null (full lists)
+    double* rs_T;                  // [tiles * 8 * 32] saved transmittance per pixel
+    uint2* rs_state;               // [tiles * 8] (live lanes, list position reached)
+    uint32_t* rs_items;            // [tiles * 8] (tile << 3 | block) to resume
+    uint32_t* rs_count;            // [2]: items, tiles queued for the fixup sort
+    uint32_t* rs_tiles;            // [tiles] tiles queued for the fixup sort
+    uint32_t* rs_need;             // [tiles] tile queued (the fixup clears it)
 };
 
 // Kernel launchers (return cudaError_t of the launch).
@@ -113,5 +124,7 @@ cudaError_t launch_raster_count(const RasterParams& p, int mode, uint32_t tiles,
 cudaError_t launch_raster_capture(const RasterParams& p, int mode, uint32_t tiles, cudaStream_t s);
 cudaError_t launch_raster_render(const RasterParams& p, int mode, uint32_t tiles, cudaStream_t s);
 cudaError_t launch_raster_fused(const RasterParams& p, int mode, uint32_t tiles, cudaStream_t s);
+// the blocks a prefix-sorted fused pass left unfinished, after the fixup sort
+cudaError_t launch_raster_resume(const RasterParams& p, int mode, cudaStream_t s);
 
 } // namespace ss

@@ -692,15 +692,13 @@ __host__ __device__ constexpr size_t tile_sort_smem(uint32_t maxn) {
     return (size_t)tile_sort_buckets(maxn) * 4 + (size_t)maxn * 8;
 }
 
-template <uint32_t MAXN, int MIN_CTAS>
-__global__ void __launch_bounds__(kTsSortThreads, MIN_CTAS) tile_sort_kernel(TileSortParams p) {
+// FIXUP: CTA k sorts tile fix_tiles[k] in full (k < fix_count[1]) and clears
+// its need flag; otherwise CTA t sorts tile t (a prefix of it in prefix mode).
+template <uint32_t MAXN, bool FIXUP>
+__device__ __forceinline__ void tile_sort_one(const TileSortParams& p, uint32_t t, uint32_t* cnt, uint2* out,
+                                              uint32_t* red_min, uint32_t* red_max, uint32_t& s_fail,
+                                              uint32_t& s_prefix) {
     constexpr uint32_t kTsPer = MAXN / kTsSortThreads; // slots per thread
-    extern __shared__ uint32_t sm[]; // cnt[tile_sort_buckets(MAXN)], then out[MAXN] as (key, gid)
-    uint32_t* cnt = sm;
-    uint2* out = reinterpret_cast<uint2*>(sm + tile_sort_buckets(MAXN));
-    __shared__ uint32_t red_min[kTsSortThreads / 32], red_max[kTsSortThreads / 32];
-    __shared__ uint32_t s_fail;
-    const uint32_t t = blockIdx.x;
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     if (p.info->overflow) return; // the view is re-run
     const uint32_t n = p.fill[t];
@@ -798,7 +796,30 @@ __global__ void __launch_bounds__(kTsSortThreads, MIN_CTAS) tile_sort_kernel(Til
         if (k >= per) break;
         if (tid + k * kTsSortThreads < n) out[atomicAdd(cnt + ((v[k].x - mn) >> sh), 1u)] = v[k];
     }
+    // prefix mode: rank only the whole buckets holding the first
+    // max(prefix_min, n / 4) instances (buckets are key-ordered, so they are
+    // exactly the first entries of the full order); every bucket is still
+    // checked against kTsBucketMax now, so the fixup sort of the rest cannot
+    // fail after the compositor has used the prefix
+    if (tid == 0) s_prefix = n;
+    if (!FIXUP && p.prefix_min && n > p.prefix_min) {
+        __syncthreads();
+        if (tid == 0) {
+            const uint32_t target = max(p.prefix_min, n >> 2);
+            uint32_t lo = 0, hi = B - 1; // first bucket whose end reaches target
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (cnt[mid] >= target) hi = mid;
+                else lo = mid + 1;
+            }
+            s_prefix = cnt[lo];
+        }
+        for (uint32_t b = tid; b < B; b += kTsSortThreads)
+            if (cnt[b] - (b ? cnt[b - 1] : 0u) > kTsBucketMax) s_fail = 1u;
+    }
     __syncthreads();
+    const uint32_t P = s_prefix;
+    if (P < n && tid == 0) p.end[t] = (uint32_t)base + P;
     // cnt[b] is now the end of bucket b (= the start of bucket b + 1).  Each
     // instance's final position is its bucket's start plus its rank among the
     // bucket's members by (key, then depth bits and id on equal keys) -- the
@@ -809,7 +830,7 @@ __global__ void __launch_bounds__(kTsSortThreads, MIN_CTAS) tile_sort_kernel(Til
     // share buckets of similar size (one large bucket no longer stalls 31
     // lanes of small ones) and the list writes land near i, coalesced.
     uint32_t* dst = p.list + base;
-    for (uint32_t i = tid; i < n; i += kTsSortThreads) {
+    for (uint32_t i = tid; i < P; i += kTsSortThreads) {
         const uint2 x = out[i];
         const uint32_t b = (x.x - mn) >> sh;
         const uint32_t s0 = b ? cnt[b - 1] : 0u, e0 = cnt[b];
@@ -847,6 +868,27 @@ __global__ void __launch_bounds__(kTsSortThreads, MIN_CTAS) tile_sort_kernel(Til
     if (s_fail && tid == 0) { // massive exact ties: the view takes the global depth sort
         atomicMax(&p.info->bin_fallback, 2u);
         p.info->overflow = 1u;
+    }
+}
+
+template <uint32_t MAXN, int MIN_CTAS, bool FIXUP>
+__global__ void __launch_bounds__(kTsSortThreads, MIN_CTAS) tile_sort_kernel(TileSortParams p) {
+    extern __shared__ uint32_t sm[]; // cnt[tile_sort_buckets(MAXN)], then out[MAXN] as (key, gid)
+    uint32_t* cnt = sm;
+    uint2* out = reinterpret_cast<uint2*>(sm + tile_sort_buckets(MAXN));
+    __shared__ uint32_t red_min[kTsSortThreads / 32], red_max[kTsSortThreads / 32];
+    __shared__ uint32_t s_fail, s_prefix;
+    if constexpr (FIXUP) {
+        // a small grid walks the queued tiles (most views queue a few dozen)
+        const uint32_t count = p.fix_count[1];
+        for (uint32_t k = blockIdx.x; k < count; k += gridDim.x) {
+            const uint32_t t = p.fix_tiles[k];
+            if (threadIdx.x == 0) p.need[t] = 0u;
+            tile_sort_one<MAXN, true>(p, t, cnt, out, red_min, red_max, s_fail, s_prefix);
+            __syncthreads(); // shared memory reused by the next tile
+        }
+    } else {
+        tile_sort_one<MAXN, false>(p, blockIdx.x, cnt, out, red_min, red_max, s_fail, s_prefix);
     }
 }
 
@@ -1755,6 +1797,41 @@ cudaError_t launch_emit_instances(const uint2* rbox, const uint32_t* order, uint
 
 uint32_t tile_sort_max_tiles() { return kTsMaxTiles; }
 
+template <bool FIXUP>
+cudaError_t configure_tile_sort() {
+    cudaError_t e = cudaFuncSetAttribute(tile_sort_kernel<kTileSortMax, 2, FIXUP>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_sort_smem(kTileSortMax));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(tile_sort_kernel<kTileSortMax * 3 / 4, 3, FIXUP>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_sort_smem(kTileSortMax * 3 / 4));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(tile_sort_kernel<kTileSortMax / 2, 3, FIXUP>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_sort_smem(kTileSortMax / 2));
+    return e;
+}
+
+template <bool FIXUP>
+void launch_tile_sort_kernel(const TileSortParams& p, unsigned grid, cudaStream_t s) {
+    // slot capacity 4096 / 6144 (c4's dense tiles reach ~5300 instances): 64 KB
+    // or less of shared memory, three CTAs per SM; 8192: two
+    if (p.cap <= kTileSortMax / 2)
+        tile_sort_kernel<kTileSortMax / 2, 3, FIXUP><<<grid, kTsSortThreads, tile_sort_smem(kTileSortMax / 2), s>>>(p);
+    else if (p.cap <= kTileSortMax * 3 / 4)
+        tile_sort_kernel<kTileSortMax * 3 / 4, 3, FIXUP>
+            <<<grid, kTsSortThreads, tile_sort_smem(kTileSortMax * 3 / 4), s>>>(p);
+    else
+        tile_sort_kernel<kTileSortMax, 2, FIXUP><<<grid, kTsSortThreads, tile_sort_smem(kTileSortMax), s>>>(p);
+}
+
+cudaError_t launch_tile_sort_fixup(const TileSortParams& p, cudaStream_t s) {
+    // one CTA per SM walks the queued tiles
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    launch_tile_sort_kernel<true>(p, std::min<unsigned>((unsigned)sms, p.tiles), s);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_tile_sort_bin(const TileSortParams& p, cudaStream_t s) {
     if (p.tiles > kTsMaxTiles) return cudaErrorInvalidValue;
     int dev = 0;
@@ -1763,16 +1840,8 @@ cudaError_t launch_tile_sort_bin(const TileSortParams& p, cudaStream_t s) {
     if (dev >= 0 && dev < 64 && !configured[dev].load()) {
         cudaError_t e = cudaFuncSetAttribute(ts_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)(kTsMaxTiles * 4));
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(tile_sort_kernel<kTileSortMax, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)tile_sort_smem(kTileSortMax));
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(tile_sort_kernel<kTileSortMax * 3 / 4, 3>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)tile_sort_smem(kTileSortMax * 3 / 4));
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(tile_sort_kernel<kTileSortMax / 2, 3>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_sort_smem(kTileSortMax / 2));
+        if (e == cudaSuccess) e = configure_tile_sort<false>();
+        if (e == cudaSuccess) e = configure_tile_sort<true>();
         if (e != cudaSuccess) return e;
         configured[dev].store(1);
     }
@@ -1782,15 +1851,7 @@ cudaError_t launch_tile_sort_bin(const TileSortParams& p, cudaStream_t s) {
         const unsigned chunks = (unsigned)((p.n + kTsChunk - 1) / kTsChunk);
         ts_scatter_kernel<<<chunks, kTsThreads, (size_t)p.tiles * 4, s>>>(p);
     }
-    // slot capacity 4096 / 6144 (c4's dense tiles reach ~5300 instances): 64 KB
-    // or less of shared memory, three CTAs per SM; 8192: two
-    if (p.cap <= kTileSortMax / 2)
-        tile_sort_kernel<kTileSortMax / 2, 3><<<p.tiles, kTsSortThreads, tile_sort_smem(kTileSortMax / 2), s>>>(p);
-    else if (p.cap <= kTileSortMax * 3 / 4)
-        tile_sort_kernel<kTileSortMax * 3 / 4, 3>
-            <<<p.tiles, kTsSortThreads, tile_sort_smem(kTileSortMax * 3 / 4), s>>>(p);
-    else
-        tile_sort_kernel<kTileSortMax, 2><<<p.tiles, kTsSortThreads, tile_sort_smem(kTileSortMax), s>>>(p);
+    launch_tile_sort_kernel<false>(p, p.tiles, s);
     return cudaGetLastError();
 }
 

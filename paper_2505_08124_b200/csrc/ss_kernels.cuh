@@ -129,6 +129,14 @@ struct TileSortParams {
     uint32_t* start;                 // [tiles] list ranges
     uint32_t* end;
     ViewInfo* info;
+    // prefix mode (fused pass): a tile of n > prefix_min instances is ranked
+    // only over its first max(prefix_min, n / 4) instances (whole buckets),
+    // end = start + that prefix; blocks that exhaust it with live pixels are
+    // resumed after the fixup sort (fix_tiles, fix_count[1]) completes the tile
+    uint32_t prefix_min;             // 0: full sort
+    const uint32_t* fix_tiles;       // fixup launch: tiles to sort in full
+    const uint32_t* fix_count;       // [1] = number of fix_tiles
+    uint32_t* need;                  // [tiles] tile queued for the fixup (cleared by it)
 };
 constexpr uint32_t kTileSortMax = 8192; // instances one CTA orders in shared memory
 // slot capacity for a view whose largest tile holds max_fill instances: 4096, 6144 or 8192
@@ -137,6 +145,8 @@ inline uint32_t tile_sort_capacity(uint32_t max_fill) {
 }
 uint32_t tile_sort_max_tiles();         // views with more tiles use the other paths
 cudaError_t launch_tile_sort_bin(const TileSortParams& p, cudaStream_t s);
+// the full sort of the tiles the resumed compositor needs (prefix mode)
+cudaError_t launch_tile_sort_fixup(const TileSortParams& p, cudaStream_t s);
 
 // warps per scatter CTA for a tile count (0: too many tiles, use the sort path)
 uint32_t bin_scatter_warps(uint32_t tiles);

@@ -326,6 +326,30 @@ def test_encode_is_bitwise_deterministic(gpu_ctx, oracle):
     assert rel <= EMB_REL_TOL and cos >= EMB_COS_TOL, (rel, cos)
 
 
+@pytest.mark.parametrize("prefix", [8, 48, 300])
+def test_sort_prefix_resume_is_bitwise(gpu_ctx, oracle, prefix):
+    """SS_OPT_SORT_PREFIX: tile lists ranked only over a prefix, the blocks
+    that exhaust it resumed after the fixup sort.  Tiny prefixes force most
+    blocks through the save / fixup / resume path; with fixed-point scalars
+    the table is bitwise the one from full sorts, and matches the oracle."""
+    wl = _bench_style(6000, 4, 96, 80, 40, 512, seed=121)
+    out = {}
+    try:
+        gpu_ctx.set_deterministic(1)
+        for pf in (0, prefix):
+            gpu_ctx.set_sort_prefix(pf)
+            out[pf] = _encode(gpu_ctx, wl.scene, wl.cams, wl.masks, 512)
+    finally:
+        gpu_ctx.set_sort_prefix(1024)
+        gpu_ctx.set_deterministic(0)
+    (r0, c0), (r1, c1) = out[0], out[prefix]
+    assert np.count_nonzero(c0) > 100
+    assert np.array_equal(r0, r1) and np.array_equal(c0, c1)
+    er, ec = oracle.encode(wl.scene, wl.cams, wl.masks, 512)
+    rel, cos = row_errors(r1, c1, er, ec)
+    assert rel <= EMB_REL_TOL and cos >= EMB_COS_TOL, (rel, cos)
+
+
 def test_encode_falloff_mode_vs_oracle(gpu_ctx, oracle):
     wl = _bench_style(1500, 2, 64, 64, 20, 16, seed=77)
     rows, cov = _encode(gpu_ctx, wl.scene, wl.cams, wl.masks, 16, mode=1)

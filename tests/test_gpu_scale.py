@@ -62,3 +62,22 @@ def test_config_view_bitwise_vs_oracle(gpu_ctx, oracle, name):
 def cfg_view(name):
     # a view away from index 0 so the orbit camera is off-axis
     return {"c2": 37, "c3": 101, "c4": 613}[name]
+
+
+def test_c4_sort_prefix_is_bitwise(gpu_ctx):
+    """c4 geometry (2M Gaussians, 1152x864, 64 masks): the default prefix-
+    sorted tile lists (SS_OPT_SORT_PREFIX 1024, blocks resumed after the fixup
+    sort) give bitwise the table of full tile sorts (fixed-point scalars)."""
+    wl, cfg = _config_workload("c4", [0, 1, 2])
+    out = {}
+    try:
+        gpu_ctx.set_deterministic(1)
+        for pf in (0, 1024):
+            gpu_ctx.set_sort_prefix(pf)
+            out[pf] = _encode(gpu_ctx, wl.scene, wl.cams, wl.masks, cfg["dim"])
+    finally:
+        gpu_ctx.set_sort_prefix(1024)
+        gpu_ctx.set_deterministic(0)
+    (r0, c0), (r1, c1) = out[0], out[1024]
+    assert np.count_nonzero(c0) > 1000
+    assert np.array_equal(r0, r1) and np.array_equal(c0, c1)
