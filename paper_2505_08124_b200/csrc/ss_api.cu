@@ -817,12 +817,34 @@ bool encode_one(ss_ctx* c, Lane& L, const ss_camera& cam, const ss_view_masks* v
                 p.mask_base = 32u * w0;
                 own_launch(c, launch_raster_fused(p, mode, g.tiles, s), SS_K_RASTER);
             }
-            if (g.prefix) {
-                // the tiles whose prefix some block exhausted: sorted in full,
-                // then those blocks continue where they stopped
-                own_launch(c, launch_tile_sort_fixup(L.ts_params, s), SS_K_RASTER);
-                own_launch(c, launch_raster_resume(p, mode, s), SS_K_RASTER);
+        }
+        if (g.prefix) {
+            // the tiles whose prefix some block exhausted: sorted in full (bin
+            // time), then those blocks continue where they stopped (raster
+            // time; the raster class counts the main pass as its launch, so
+            // per-launch figures stay those of the compositor pass)
+            {
+                Scope sc(c, s, SS_K_BIN);
+                own_launch(c, launch_tile_sort_fixup(L.ts_params, s), SS_K_BIN, 0);
+                c->launches_own += 1;
             }
+            Scope sc(c, s, SS_K_RASTER);
+            RasterParams p = raster_params(c, L, cam, g);
+            p.pix_bits = L.pix_bits.as<uint32_t>();
+            p.n_masks = M;
+            p.bits_stride = words;
+            p.mask_words = words;
+            p.mask_base = 0;
+            p.acc = S->acc.p;
+            p.acc_fix = S->acc_fix ? 1u : 0u;
+            p.touched = S->touched.as<uint32_t>();
+            p.gen = S->gen;
+            p.rs_T = L.rs_T.as<double>();
+            p.rs_state = L.rs_state.as<uint2>();
+            p.rs_items = L.rs_items.as<uint32_t>();
+            p.rs_count = L.rs_count.as<uint32_t>();
+            own_launch(c, launch_raster_resume(p, mode, s), SS_K_RASTER, 0);
+            c->launches_own += 1;
         }
         {
             // the view's touched Gaussians, compacted from the compositor's stamps
