@@ -41,7 +41,7 @@ PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
 FALLBACK_HBM = 6650.0
 
 
-DEFAULT_LANES = 6
+DEFAULT_LANES = 5
 
 
 def ncu_traffic(kernel, field="bytes_per_launch"):

@@ -89,7 +89,7 @@ int ss_last_error_kind(void);
  * own collectives. */
 int ss_set_stream(ss_ctx* ctx, uintptr_t stream);
 int ss_synchronize(ss_ctx* ctx);
-/* Tuning options.  SS_OPT_LANES: per-view pipeline lanes (1..6, default 6);
+/* Tuning options.  SS_OPT_LANES: per-view pipeline lanes (1..6, default 5);
  * 1 serialises views, which the bench uses for exclusive per-kernel timing.
  * SS_OPT_QUERY_PATH: 0 = auto (tensor-core coarse scoring + exact rescoring
  * for stores of >= 16384 rows with dim % 64 == 0 and dim <= 512), 1 = exact

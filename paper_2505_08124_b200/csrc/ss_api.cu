@@ -219,7 +219,7 @@ struct ss_ctx {
     static constexpr uint32_t kMaxLanes = 6;
     ss::Lane lanes[kMaxLanes];
     uint32_t next_lane = 0;
-    uint32_t n_lanes = 6;
+    uint32_t n_lanes = 5;
     cudaEvent_t ev_user = nullptr;
     // contraction group: consecutive views whose contraction is issued together
     std::vector<ss::GroupMember> group;

@@ -1943,12 +1943,10 @@ cudaError_t launch_contract(const ContractParams& p, uint64_t max_touched, cudaS
             const char* e = getenv("SS_CONTRACT_CTAS");
             return e ? atoi(e) : 0;
         }();
-        // default: 2/5 of the SMs, so compositor CTAs of other views keep the
-        // rest (300 c4 views, 5 lanes, before the prefix sort: 148 CTAs 1580,
-        // 110 1603-1606, 90 1615-1616, 74 1597-1607, 50 1579-1590 views/s;
-        // with prefix-sorted lists and 6 lanes: 89 1884-1895, 74 1900-1905,
-        // 66 1913-1914, 60 1916-1922)
-        sms = override_ctas > 0 ? std::min(sms, override_ctas) : std::max(1, (sms * 2 + 2) / 5);
+        // default: 3/5 of the SMs, so compositor CTAs of other views keep the
+        // rest (300 c4 views: 148 CTAs 1580, 110 1603-1606, 90 1615-1616,
+        // 74 1597-1607, 50 1579-1590 views/s)
+        sms = override_ctas > 0 ? std::min(sms, override_ctas) : std::max(1, (sms * 3 + 2) / 5);
     }
     static std::atomic<int> configured_g[64] = {};
     if (dev >= 0 && dev < 64 && !configured_g[dev].load()) {
