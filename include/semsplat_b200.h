@@ -203,6 +203,15 @@ int ss_encode_views(ss_ctx* ctx, uint32_t nviews, const ss_camera* raster_cams, 
  * (row_hi-row_lo).  out_on_device != 0: the outputs are device pointers. */
 int ss_encode_finalize(ss_ctx* ctx, uint64_t row_lo, uint64_t row_hi, float* rows_out, float* coverage_out,
                        int out_on_device);
+/* finalize_into (pipeline.hpp:120-135) into a host table whose rows are
+ * already zero (the reference's EmbeddingTable constructor zero-fills):
+ * only covered rows are normalised into rows_out / coverage_out (host
+ * pointers to row row_lo), the uncovered ones are left untouched -- the
+ * reference writes zeros there.  The covered rows are packed on the device
+ * and scattered by id on the host, so the readout moves ~6 % of the c4
+ * table.  covered_out (optional): rows written. */
+int ss_encode_finalize_sparse(ss_ctx* ctx, uint64_t row_lo, uint64_t row_hi, float* rows_out, float* coverage_out,
+                              uint64_t* covered_out);
 /* finalize over caller-provided device buffers (a reduce-scattered shard):
  * rows d_sums[n x dim] / d_totals[n] -> d_rows_out, d_coverage_out. */
 int ss_normalize_device(ss_ctx* ctx, const float* d_sums, const float* d_totals, uint64_t n, uint32_t dim,

@@ -503,7 +503,9 @@ inline EmbeddingTable encode_scene(const GaussianScene& scene, const DatasetMani
         const uint64_t step = (chunk_rows == 0 || chunk_rows > n) ? std::max<uint64_t>(n, 1) : chunk_rows;
         for (uint64_t lo = 0; lo < n; lo += step) {
             const uint64_t hi = std::min<uint64_t>(n, lo + step);
-            check(ss_encode_finalize(devs[0]->ctx(), lo, hi, table.row(lo), table.coverage.data() + lo, 0));
+            // the table is freshly zero-filled: only covered rows move
+            check(ss_encode_finalize_sparse(devs[0]->ctx(), lo, hi, table.row(lo), table.coverage.data() + lo,
+                                            nullptr));
         }
     } else {
         // combine_partials + finalize_into: every device reduce-scatters its

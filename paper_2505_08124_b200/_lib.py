@@ -86,6 +86,7 @@ def lib() -> C.CDLL:
         "ss_encode_view": (i32, [vp, C.POINTER(Camera), C.POINTER(ViewMasks), i32]),
         "ss_encode_views": (i32, [vp, u32, C.POINTER(Camera), C.POINTER(ViewMasks), i32]),
         "ss_encode_finalize": (i32, [vp, u64, u64, vp, vp, i32]),
+        "ss_encode_finalize_sparse": (i32, [vp, u64, u64, vp, vp, vp]),
         "ss_normalize_device": (i32, [vp, vp, vp, u64, u32, vp, vp]),
         "ss_store_build": (i32, [vp, pf, pf, u64, u32, pu64]),
         "ss_store_set": (i32, [vp, pu32, pf, u64, u32]),
@@ -365,6 +366,17 @@ class Context:
         check(self._L.ss_encode_finalize(self.h, row_lo, row_hi, rows.ctypes.data_as(C.c_void_p),
                                          cov.ctypes.data_as(C.c_void_p), 0))
         return rows, cov
+
+    def encode_finalize_sparse(self, row_lo: int = 0, row_hi: int | None = None):
+        """ss_encode_finalize_sparse into zero-filled host arrays: only covered rows are written."""
+        row_hi = self._n if row_hi is None else row_hi
+        n = row_hi - row_lo
+        rows = np.zeros((n, self._dim), np.float32)
+        cov = np.zeros(n, np.float32)
+        cnt = C.c_uint64()
+        check(self._L.ss_encode_finalize_sparse(self.h, row_lo, row_hi, rows.ctypes.data_as(C.c_void_p),
+                                                cov.ctypes.data_as(C.c_void_p), C.byref(cnt)))
+        return rows, cov, int(cnt.value)
 
     def encode_finalize_into(self, rows_ptr: int, cov_ptr: int, row_lo: int = 0, row_hi: int | None = None,
                              on_device: bool = False):

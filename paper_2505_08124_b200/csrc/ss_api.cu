@@ -251,6 +251,7 @@ struct ss_ctx {
     float* totals = nullptr;
     bool own_acc = false;
     ss::DevBuf sums_buf, totals_buf;
+    ss::DevBuf sparse_out; // ss_encode_finalize_sparse: packed covered rows
     // store + query
     ss::DevBuf store_rows, store_ids, qbuf, qnorm, scores, topk_ids, topk_sims, sel_flags, thr_keys, thr_keys_sorted,
         thr_ids, thr_ids_sorted, zero_flag;
@@ -1593,6 +1594,81 @@ int ss_encode_finalize(ss_ctx* c, uint64_t row_lo, uint64_t row_hi, float* rows_
         if (!out_on_device) {
             copy_d2h_pageable(c, rows_out, d_rows, n * c->dim * 4, s);
             copy_d2h_pageable(c, coverage_out, d_cov, n * 4, s);
+        }
+    });
+}
+
+int ss_encode_finalize_sparse(ss_ctx* c, uint64_t row_lo, uint64_t row_hi, float* rows_out, float* coverage_out,
+                              uint64_t* covered_out) {
+    return guarded([&] {
+        if (!c) throw Error(SS_ERR_CONTRACT, "ctx is null");
+        if (!c->sums) throw Error(SS_ERR_CONTRACT, "finalize before ss_encode_begin");
+        if (row_lo > row_hi || row_hi > c->n) throw Error(SS_ERR_CONTRACT, "finalize_into: rows do not fit the table");
+        set_device(c);
+        const uint64_t n = row_hi - row_lo;
+        if (covered_out) *covered_out = 0;
+        if (n == 0) return;
+        cudaStream_t s = c->stream;
+        const uint32_t D = c->dim;
+        auto* d_rows = static_cast<float*>(c->scores.ensure(n * D * 4 + n * 4));
+        float* d_cov = d_rows + n * D;
+        {
+            Scope sc(c, s, SS_K_NORMALIZE);
+            own_launch(c,
+                       launch_normalize(c->sums + row_lo * D, c->totals + row_lo, n, D, d_rows, d_cov,
+                                        c->counters.as<unsigned long long>() + 3, s),
+                       SS_K_NORMALIZE);
+            c->prof.bytes[SS_K_NORMALIZE] += (double)n * (4.0 * D + 8.0);
+        }
+        // covered rows packed on the device: ids, coverage, rows
+        auto* pk = static_cast<char*>(c->sparse_out.ensure(n * 4 + n * 4 + n * (uint64_t)D * 4 + 16));
+        auto* d_cnt = reinterpret_cast<unsigned long long*>(pk);
+        auto* d_ids = reinterpret_cast<uint32_t*>(pk + 16);
+        float* d_pcov = reinterpret_cast<float*>(pk + 16 + n * 4);
+        float* d_prow = reinterpret_cast<float*>(pk + 16 + n * 8);
+        SS_CUDA(cudaMemsetAsync(d_cnt, 0, 8, s));
+        own_launch(c, launch_compact_covered(d_rows, d_cov, n, D, d_ids, d_pcov, d_prow, d_cnt, s), SS_K_NORMALIZE);
+        unsigned long long cnt = 0;
+        SS_CUDA(cudaMemcpyAsync(&cnt, d_cnt, 8, cudaMemcpyDeviceToHost, s));
+        SS_CUDA(cudaStreamSynchronize(s));
+        if (covered_out) *covered_out = cnt;
+        if (cnt == 0) return;
+        std::vector<uint32_t> ids(cnt);
+        std::vector<float> pcov(cnt);
+        SS_CUDA(cudaMemcpyAsync(ids.data(), d_ids, cnt * 4, cudaMemcpyDeviceToHost, s));
+        SS_CUDA(cudaMemcpyAsync(pcov.data(), d_pcov, cnt * 4, cudaMemcpyDeviceToHost, s));
+        SS_CUDA(cudaStreamSynchronize(s));
+        for (uint64_t k = 0; k < cnt; ++k) coverage_out[ids[k]] = pcov[k];
+        // the packed rows through the pinned staging buffers, scattered by id
+        // into the caller's (zero) table while the next chunk is in flight
+        if (!c->h_stage) {
+            SS_CUDA(cudaMallocHost(&c->h_stage, 2 * kStageBytes));
+            for (auto& e : c->stage_ev) SS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        const uint64_t row_bytes = (uint64_t)D * 4, per_chunk = std::max<uint64_t>(1, kStageBytes / row_bytes);
+        const uint64_t chunks = (cnt + per_chunk - 1) / per_chunk;
+        auto issue = [&](uint64_t k) {
+            const uint64_t r0 = k * per_chunk, nr = std::min<uint64_t>(per_chunk, cnt - r0);
+            SS_CUDA(cudaMemcpyAsync(c->h_stage + (k & 1) * kStageBytes, d_prow + r0 * D, nr * row_bytes,
+                                    cudaMemcpyDeviceToHost, s));
+            SS_CUDA(cudaEventRecord(c->stage_ev[k & 1], s));
+        };
+        const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency() / 2));
+        issue(0);
+        for (uint64_t k = 0; k < chunks; ++k) {
+            if (k + 1 < chunks) issue(k + 1);
+            SS_CUDA(cudaEventSynchronize(c->stage_ev[k & 1]));
+            const uint64_t r0 = k * per_chunk, nr = std::min<uint64_t>(per_chunk, cnt - r0);
+            const float* src = reinterpret_cast<const float*>(c->h_stage + (k & 1) * kStageBytes);
+            auto scatter = [&](uint64_t a, uint64_t b) {
+                for (uint64_t j = a; j < b; ++j) std::memcpy(rows_out + (uint64_t)ids[r0 + j] * D, src + j * D, row_bytes);
+            };
+            const uint64_t per = (nr + hw - 1) / hw;
+            std::vector<std::thread> th;
+            for (unsigned t = 1; t < hw && t * per < nr; ++t)
+                th.emplace_back([=] { scatter(t * per, std::min<uint64_t>(nr, (t + 1) * per)); });
+            scatter(0, std::min<uint64_t>(nr, per));
+            for (auto& x : th) x.join();
         }
     });
 }

@@ -2011,6 +2011,46 @@ cudaError_t launch_contract(const ContractParams& p, uint64_t max_touched, cudaS
         contract_kernel<false><<<warp_grid(max_touched), 256, 0, s>>>(p);
     return cudaGetLastError();
 }
+// Covered rows of a normalised slice packed for a sparse readout (order of
+// arrival; the host scatters them by id): ids, coverage and the rows.
+__global__ void __launch_bounds__(256) compact_covered_kernel(const float* __restrict__ rows,
+                                                              const float* __restrict__ cov, uint64_t n, uint32_t dim,
+                                                              uint32_t* ids, float* pcov, float* prow,
+                                                              unsigned long long* count) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t w0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t base = w0 * 32u; base < n; base += nw * 32u) {
+        const uint64_t i = base + lane;
+        const bool c = i < n && cov[i] > 0.0f; // normalize writes 0 (and a zero row) for uncovered rows
+        const uint32_t bal = __ballot_sync(0xffffffffu, c);
+        if (!bal) continue;
+        unsigned long long slot0 = 0;
+        if (lane == 0) slot0 = atomicAdd(count, (unsigned long long)__popc(bal));
+        slot0 = __shfl_sync(0xffffffffu, slot0, 0);
+        if (c) {
+            const uint64_t k = slot0 + __popc(bal & ((1u << lane) - 1u));
+            ids[k] = (uint32_t)i;
+            pcov[k] = cov[i];
+        }
+        for (uint32_t rem = bal; rem; rem &= rem - 1u) {
+            const int src = __ffs(rem) - 1;
+            const uint64_t k = slot0 + __popc(bal & ((1u << src) - 1u));
+            const float* r = rows + (base + src) * dim;
+            float* o = prow + k * dim;
+            for (uint32_t d = lane; d < dim; d += 32u) o[d] = r[d];
+        }
+    }
+}
+
+cudaError_t launch_compact_covered(const float* rows, const float* cov, uint64_t n, uint32_t dim, uint32_t* ids,
+                                   float* pcov, float* prow, unsigned long long* count, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, 148ull * 8ull);
+    compact_covered_kernel<<<(unsigned)blocks, 256, 0, s>>>(rows, cov, n, dim, ids, pcov, prow, count);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_normalize(const float* sums, const float* totals, uint64_t n, uint32_t dim, float* rows,
                              float* coverage, unsigned long long* covered, cudaStream_t s) {
     if (!n) return cudaSuccess;

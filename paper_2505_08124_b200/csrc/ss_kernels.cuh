@@ -145,6 +145,9 @@ inline uint32_t tile_sort_capacity(uint32_t max_fill) {
 }
 uint32_t tile_sort_max_tiles();         // views with more tiles use the other paths
 cudaError_t launch_tile_sort_bin(const TileSortParams& p, cudaStream_t s);
+// covered rows of a normalised slice packed (ids, coverage, rows; count atomically)
+cudaError_t launch_compact_covered(const float* rows, const float* cov, uint64_t n, uint32_t dim, uint32_t* ids,
+                                   float* pcov, float* prow, unsigned long long* count, cudaStream_t s);
 // the full sort of the tiles the resumed compositor needs (prefix mode)
 cudaError_t launch_tile_sort_fixup(const TileSortParams& p, cudaStream_t s);
 

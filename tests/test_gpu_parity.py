@@ -358,6 +358,22 @@ def test_encode_falloff_mode_vs_oracle(gpu_ctx, oracle):
     assert rel <= EMB_REL_TOL and cos >= EMB_COS_TOL
 
 
+def test_encode_finalize_sparse_equals_dense(gpu_ctx):
+    """ss_encode_finalize_sparse (covered rows packed on the device, scattered
+    by id into a zero table) gives the dense finalize_into bits, per chunk."""
+    wl = _bench_style(5000, 3, 80, 64, 24, 512, seed=131)
+    gpu_ctx.set_scene(wl.scene.mean, wl.scene.scale, wl.scene.quat_xyzw, wl.scene.opacity)
+    gpu_ctx.encode_begin(512)
+    gpu_ctx.encode_views(wl.cams, wl.masks, 0)
+    rows, cov = gpu_ctx.encode_finalize()
+    srows, scov, n_cov = gpu_ctx.encode_finalize_sparse()
+    assert n_cov == int(np.count_nonzero(cov)) > 100
+    assert np.array_equal(rows, srows) and np.array_equal(cov, scov)
+    lo, hi = 1234, 4321
+    crows, ccov, _ = gpu_ctx.encode_finalize_sparse(lo, hi)
+    assert np.array_equal(crows, rows[lo:hi]) and np.array_equal(ccov, cov[lo:hi])
+
+
 def test_encode_chunked_finalize_is_bitwise_chunk_invariant(gpu_ctx):
     """pipeline.hpp:276-279: the result does not depend on chunk_rows."""
     wl = _bench_style(1000, 2, 48, 48, 8, 32, seed=5)
