@@ -697,13 +697,16 @@ __host__ __device__ constexpr size_t tile_sort_smem(uint32_t maxn) {
 template <uint32_t MAXN, bool FIXUP>
 __device__ __forceinline__ void tile_sort_one(const TileSortParams& p, uint32_t t, uint32_t* cnt, uint2* out,
                                               uint32_t* red_min, uint32_t* red_max, uint32_t& s_fail,
-                                              uint32_t& s_prefix) {
+                                              uint32_t& s_prefix, uint32_t& s_lo) {
     constexpr uint32_t kTsPer = MAXN / kTsSortThreads; // slots per thread
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     if (p.info->overflow) return; // the view is re-run
     const uint32_t n = p.fill[t];
     const size_t base = (size_t)t * p.cap;
     if (tid == 0) {
+        // fixup: the prefix the main sort already ranked (its list end) is
+        // left as written; only the rest is ranked here
+        s_lo = FIXUP ? p.end[t] - (uint32_t)base : 0u;
         p.start[t] = (uint32_t)base;
         p.end[t] = (uint32_t)base + n;
         s_fail = 0u;
@@ -830,7 +833,7 @@ __device__ __forceinline__ void tile_sort_one(const TileSortParams& p, uint32_t 
     // share buckets of similar size (one large bucket no longer stalls 31
     // lanes of small ones) and the list writes land near i, coalesced.
     uint32_t* dst = p.list + base;
-    for (uint32_t i = tid; i < P; i += kTsSortThreads) {
+    for (uint32_t i = s_lo + tid; i < P; i += kTsSortThreads) {
         const uint2 x = out[i];
         const uint32_t b = (x.x - mn) >> sh;
         const uint32_t s0 = b ? cnt[b - 1] : 0u, e0 = cnt[b];
@@ -877,18 +880,18 @@ __global__ void __launch_bounds__(kTsSortThreads, MIN_CTAS) tile_sort_kernel(Til
     uint32_t* cnt = sm;
     uint2* out = reinterpret_cast<uint2*>(sm + tile_sort_buckets(MAXN));
     __shared__ uint32_t red_min[kTsSortThreads / 32], red_max[kTsSortThreads / 32];
-    __shared__ uint32_t s_fail, s_prefix;
+    __shared__ uint32_t s_fail, s_prefix, s_lo;
     if constexpr (FIXUP) {
         // a small grid walks the queued tiles (most views queue a few dozen)
         const uint32_t count = p.fix_count[1];
         for (uint32_t k = blockIdx.x; k < count; k += gridDim.x) {
             const uint32_t t = p.fix_tiles[k];
             if (threadIdx.x == 0) p.need[t] = 0u;
-            tile_sort_one<MAXN, true>(p, t, cnt, out, red_min, red_max, s_fail, s_prefix);
+            tile_sort_one<MAXN, true>(p, t, cnt, out, red_min, red_max, s_fail, s_prefix, s_lo);
             __syncthreads(); // shared memory reused by the next tile
         }
     } else {
-        tile_sort_one<MAXN, false>(p, blockIdx.x, cnt, out, red_min, red_max, s_fail, s_prefix);
+        tile_sort_one<MAXN, false>(p, blockIdx.x, cnt, out, red_min, red_max, s_fail, s_prefix, s_lo);
     }
 }
 
